@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""bench.py -- decode tokens/s of the Mixtral-8x7B-shaped MoE expert-layer
+stack vs the number of 4-bit experts (BASELINE.json metric), on B200.
+
+Workload (BASELINE.json configs[2], the metric's "decode tokens/s vs #4-bit
+experts" on one GPU): 32 layers x 8 experts (d=4096, ffn=14336), top-2,
+batch-1 decode, synthetic weights from the seeded generator, plan =
+plan_quality(n4, seed 0) with every expert device-resident.  The headline
+`value` is at n4 = 128 of 256 (half the experts int4-g128); `sweep` carries
+the full n4 = 0..256 curve.  A "step" = one decode token through all 32
+layers (route -> gate/up GEMV -> down GEMV -> combine, one CUDA graph).
+
+  value     device-timed (CUDA events on the engine stream), inputs resident
+  e2e       through the public API with host buffers (moe_engine_decode_host:
+            H2D of the token's embedding, decode, D2H of the output, synced)
+  roofline  the dominant kernel pair (expert FFN gate/up + down) timed with
+            CUDA events per layer on its launch stream; algorithmic bytes =
+            distinct selected experts' weights+scales + activations
+  cpu_baseline  the CPU port (oracle/, OpenMP over all host threads) on a
+            bounded sample: one layer's experts prepared, T-token layer
+            forwards timed, extrapolated x32 layers
+
+No L2 flush is needed: one step streams 64 distinct experts (5.8-22.5 GB)
+through a 126 MB L2.  `--impl reference` times the CPU port alone (the
+reference, /root/reference, has no tensor math: SPEC.md:13).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+D_MODEL, D_FFN, LAYERS, EXPERTS, TOPK = 4096, 14336, 32, 8, 2
+METRIC = "decode tokens/s vs #4-bit experts (Mixtral-8x7B shape); expert-FFN HBM GB/s"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.out = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.out, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.out.close()
+
+    def summary(self):
+        if self.proc is None or not self.path:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_port_tokens_per_s(n4_layer_prec, T, seconds=12.0, layer=0, seed=0):
+    """The CPU port (oracle) on one layer with prepared weights; returns
+    (tok/s extrapolated to 32 layers, threads, sample description)."""
+    from oracle.oracle import OracleLib
+    orc = OracleLib()
+    m = orc.model(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, seed)
+    prep = orc.prepare_layer(m, layer, n4_layer_prec)
+    x = orc.step_input(m, 0, T)
+    orc.moe_layer_w(m, prep, x, T)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        x_in = orc.step_input(m, reps + 1, T)
+        orc.moe_layer_w(m, prep, x_in, T)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or reps >= 400:
+            break
+    per_layer = el / reps
+    tps = T / (per_layer * LAYERS)
+    n4l = sum(1 for p in n4_layer_prec if p == 0)
+    sample = (f"layer {layer} of {LAYERS} ({n4l}/8 experts int4 per the plan), {reps} x {T}-token layer forwards "
+              f"in {el:.1f} s, extrapolated x{LAYERS} layers")
+    return tps, orc.num_threads(), sample
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import paper_2407_14417_b200 as moe
+    prof = moe.profile_for_shape(D_MODEL, D_FFN, LAYERS, EXPERTS, TOPK)
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, args.n4, 0), moe.HardwareProfile(10**15), prof)
+    prec = plan.precision[:EXPERTS]
+    from oracle.oracle import OracleLib
+    orc = OracleLib()
+    m = orc.model(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, 0)
+    prep = orc.prepare_layer(m, 0, prec)
+    T = args.tokens
+    for w in range(args.warmup):
+        orc.moe_layer_w(m, prep, orc.step_input(m, w, T), T)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        orc.moe_layer_w(m, prep, orc.step_input(m, 1000 + s, T), T)
+    el = time.perf_counter() - t0
+    per_layer = el / args.steps
+    tps = T / (per_layer * LAYERS)
+    sample = (f"layer 0 of {LAYERS} ({sum(1 for p in prec if p == 0)}/8 int4), {args.steps} x {T}-token layer "
+              f"forwards, extrapolated x{LAYERS} layers")
+    line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_layer * LAYERS * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16/int4-g128 (fp32 acc)",
+            "data": "synthetic (seeded generator)",
+            "config": {"workload": "mixtral8x7b-shape 32-layer MoE stack decode", "n4": args.n4, "batch": T,
+                       "d_model": D_MODEL, "d_ffn": D_FFN, "layers": LAYERS, "experts": EXPERTS, "top_k": TOPK},
+            "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": orc.num_threads(), "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference repo has no tensor math (SPEC.md:13); CPU port of its path = oracle/ (OpenMP)"}
+    print(json.dumps(line), flush=True)
+
+
+def time_engine(moe, torch, eng, T, steps, warmup):
+    stream = torch.cuda.ExternalStream(eng.stream_ptr)
+    for w in range(warmup):
+        eng.synth_input(w, T)
+        eng.decode(T)
+    eng.sync()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(steps):
+        eng.decode(T)
+    end.record(stream)
+    end.synchronize()
+    return start.elapsed_time(end) / steps
+
+
+def run_ours(args, rank, world, device):
+    import torch
+    import paper_2407_14417_b200 as moe
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    prof = moe.profile_for_shape(D_MODEL, D_FFN, LAYERS, EXPERTS, TOPK)
+    T = args.tokens
+    hbm_peak, peak_kind = peaks()
+    s16, s4 = moe.expert_size(prof, 1), moe.expert_size(prof, 0)
+
+    def build(n4):
+        plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 0), moe.HardwareProfile(10**15), prof)
+        eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan, max_tokens=T, seed=args.seed + rank,
+                            device=device)
+        return plan, eng
+
+    # ---- headline point ---------------------------------------------------
+    plan, eng = build(args.n4)
+    eng.synth_input(0, T)
+    eng.decode(T)  # capture the graph
+    eng.sync()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(device) as clk:
+        ms = time_engine(moe, torch, eng, T, args.steps, args.warmup)
+    clocks = clk.summary()
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * T * 1000.0 / ms
+
+    # ---- roofline: per-layer expert FFN (gate/up + down), CUDA events -----
+    ffn_ms, ffn_bytes = [], []
+    for _ in range(3):
+        eng.synth_input(7, T)
+        m_, b_, kps = eng.profile_step(T)
+        ffn_ms += m_
+        ffn_bytes += b_
+    avg_ms = sum(ffn_ms) / len(ffn_ms)
+    avg_bytes = sum(ffn_bytes) / len(ffn_bytes)
+    achieved = avg_bytes / (avg_ms * 1e-3) / 1e9
+    ffn_share = (avg_ms * LAYERS) / ms
+    step_bytes = sum(ffn_bytes[:LAYERS])
+
+    # ---- e2e through the public API with host buffers -----------------------
+    import numpy as np
+    xh = torch.empty(T * D_MODEL, dtype=torch.int16).pin_memory()
+    oh = torch.empty(T * D_MODEL, dtype=torch.int16).pin_memory()
+    eng.synth_input(3, T)
+    eng.sync()
+    xh.copy_(torch.as_tensor(_DevBytes(eng.input_ptr, T * D_MODEL * 2), device=f"cuda:{device}").view(torch.int16).cpu())
+    for _ in range(max(1, args.warmup)):
+        eng.decode_host(xh.data_ptr(), T, oh.data_ptr())
+    e_steps = max(10, min(args.steps, 200))
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        eng.decode_host(xh.data_ptr(), T, oh.data_ptr())
+    e2e_s = (time.perf_counter() - t0) / e_steps
+    if dist:
+        t = torch.tensor([e2e_s], device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = world * T / e2e_s
+    eng.close()
+    del eng
+
+    # ---- n4 sweep (the metric's x axis) -------------------------------------
+    sweep = []
+    if args.sweep:
+        for n4 in args.sweep_points:
+            p, e = build(n4)
+            e.synth_input(0, T)
+            e.decode(T)
+            e.sync()
+            m = time_engine(moe, torch, e, T, max(20, min(args.steps, 100)), 3)
+            fm, fb, _ = e.profile_step(T)
+            sweep.append({"n4": n4, "tokens_per_s": round(T * 1000.0 / m, 2), "ms_per_step": round(m, 4),
+                          "expert_gb_per_token": round(sum(fb) / 1e9 / T, 3),
+                          "ffn_gbs": round(sum(fb) / (sum(fm) * 1e-3) / 1e9, 1)})
+            e.close()
+            del e
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tps, cores, sample = cpu_port_tokens_per_s(plan.precision[:EXPERTS], T, seconds=args.cpu_seconds)
+        cpu = {"value": round(tps, 4), "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16 / int4-g128 weights, bf16 activations, fp32 accumulate",
+            "data": "synthetic (seeded counter-based generator, int4 = RTN-g128 of the bf16 masters)",
+            "config": {"workload": "mixtral8x7b-shape 32-layer MoE stack, batch-%d decode" % T, "n4": args.n4,
+                       "of": LAYERS * EXPERTS, "plan": "plan_quality seed 0, all device-resident",
+                       "d_model": D_MODEL, "d_ffn": D_FFN, "layers": LAYERS, "experts": EXPERTS, "top_k": TOPK,
+                       "batch": T, "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "no flush: each step streams %.1f GB of distinct expert weights >> 126 MB L2"
+                             % (step_bytes / 1e9)},
+            "e2e": {"value": round(e2e, 3), "unit": "tokens/s", "h2d_bytes_per_step": T * D_MODEL * 2,
+                    "d2h_bytes_per_step": T * D_MODEL * 2},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "expert FFN (ffn_gateup_kernel + ffn_down_kernel) per layer",
+                         "bytes_per_launch": round(avg_bytes), "ms_per_launch": round(avg_ms, 5),
+                         "ffn_share_of_step": round(ffn_share, 4)},
+            "gpu_launches": kps * (args.steps),
+            "kernels_per_step": kps,
+            "clocks": clocks,
+            "sweep": sweep,
+            "cpu_baseline": cpu,
+            "bytes_per_expert": {"bf16": s16, "int4_g128": s4},
+        }
+        print(json.dumps(line), flush=True)
+
+
+class _DevBytes:
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n4", type=int, default=128)
+    ap.add_argument("--tokens", type=int, default=1, help="decode batch T")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false")
+    ap.add_argument("--sweep-points", type=lambda s: [int(v) for v in s.split(",")],
+                    default=[0, 32, 64, 96, 128, 160, 192, 224, 256])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

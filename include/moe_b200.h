@@ -1,0 +1,242 @@
+/*
+ * moe_b200.h -- C ABI of the B200 MoE expert-layer hot path.
+ *
+ * This is the drop-in boundary under the reference's operator API
+ * (/root/reference/proj/include/moeserve):
+ *   router call           generate_trace   gating.hpp:33      -> moe_gate_topk (+ moe_generate_trace)
+ *   placement config      make_plan        planner.hpp:71     -> moe_make_plan
+ *   MoE-layer forward     simulate         simulator.hpp:58   -> moe_engine_* / moe_ffn / moe_combine
+ *                                                                (+ moe_simulate for the cost model)
+ * The reference has no FFI of its own (C++ headers only);
+ * INTEGRATION.md shows the ctypes / C++ binding a maintainer would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; device pointers are caller-owned and the
+ *     kernels are stream-ordered (cudaStream_t passed as void*); nothing in
+ *     the kernel entry points allocates.
+ *   - every entry point returns a status mirroring the reference CLI exit
+ *     codes (cli.hpp:7-8): 0 ok, 1 internal (CUDA) error, 2 usage (bad
+ *     shape / argument), 3 parse or validation error, 4 infeasible budget.
+ *     moe_last_error() returns the thread's last message.
+ *   - bf16 tensors are passed as void* (uint16 storage), int4-g128 weights
+ *     as packed uint32 + bf16 scales (format in DESIGN.md, "int4 format").
+ *   - no CPU fallback: without a CUDA device the kernel entry points return 1.
+ */
+#ifndef MOE_B200_H
+#define MOE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_MAX_EXPERTS 64
+#define MOE_MAX_TOPK 8
+
+enum { MOE_OK = 0, MOE_ERR_INTERNAL = 1, MOE_ERR_USAGE = 2, MOE_ERR_VALIDATION = 3,
+       MOE_ERR_INFEASIBLE = 4 };
+enum { MOE_P4 = 0, MOE_P16 = 1 };          /* Precision (profiles.hpp:17)   */
+enum { MOE_GPU = 0, MOE_CPU = 1 };         /* Location  (planner.hpp:13)    */
+enum { MOE_THROUGHPUT = 0, MOE_QUALITY = 1 };
+
+const char* moe_last_error(void);
+int moe_version(void);
+
+/* ------------------------------------------------------------------------
+ * Profiles and placement config (reference profiles.hpp / planner.hpp).
+ * ---------------------------------------------------------------------- */
+typedef struct {                 /* ModelProfile, profiles.hpp:29-43 */
+    int32_t num_layers, experts_per_layer, top_k, pad_;
+    int64_t size_nonexpert_bytes, size_expert16_bytes;
+    double quant_ratio, compute_latency16_s, compute_penalty4, nonexpert_latency_s;
+} moe_model_profile;
+
+typedef struct {                 /* HardwareProfile, profiles.hpp:45-52 */
+    int64_t gpu_mem_bytes;
+    double transfer_bw_bytes_per_s;
+} moe_hardware_profile;
+
+typedef struct {                 /* TaskRequest, profiles.hpp:55-59 (n4_target -1 = none) */
+    int32_t preference, n4_target;
+    uint64_t seed;
+} moe_task_request;
+
+typedef struct {                 /* ExpertState, planner.hpp:22-26 */
+    int32_t precision, location;
+} moe_expert_state;
+
+/* which: 0 mixtral-sec41, 1 mixtral-table1 (profiles.cpp:66-75) */
+int moe_profile_builtin(int which, moe_model_profile* out);
+/* Profile whose expert sizes equal the engine's allocations for d x f experts. */
+int moe_profile_for_shape(int d_model, int d_ffn, int num_layers, int experts_per_layer, int top_k,
+                          int64_t size_nonexpert_bytes, moe_model_profile* out);
+int moe_load_profiles(const char* document, moe_model_profile* model, moe_hardware_profile* hw);
+int64_t moe_parse_size(const char* text);                              /* -1 on error */
+int64_t moe_expert_size(const moe_model_profile* p, int precision);
+int moe_model_size(const moe_model_profile* p, int n4, int nonexpert_precision /*0 P4,1 P8,2 P16*/,
+                   int64_t* out);
+uint64_t moe_profile_fingerprint(const moe_model_profile* p);
+int moe_num_experts_16(int64_t mem_gpu, const moe_model_profile* p);    /* Eq. 1 */
+/* make_plan (planner.hpp:71): entries[num_experts] indexed layer*E + slot. */
+int moe_make_plan(const moe_task_request* task, const moe_hardware_profile* hw,
+                  const moe_model_profile* p, moe_expert_state* entries, int64_t* swap_slot_bytes);
+int moe_assign_locations(const int32_t* precisions, const moe_hardware_profile* hw,
+                         const moe_model_profile* p, uint64_t seed, moe_expert_state* entries,
+                         int64_t* swap_slot_bytes);
+int64_t moe_gpu_footprint(const moe_expert_state* entries, int64_t swap_slot_bytes,
+                          const moe_model_profile* p);
+/* Number of validate_plan() violations (0 = valid); messages joined by '\n'
+ * into msg (capacity cap) when msg != NULL. */
+int moe_validate_plan(const moe_expert_state* entries, int n_entries, int64_t swap_slot_bytes,
+                      const moe_hardware_profile* hw, const moe_model_profile* p, char* msg,
+                      int cap);
+
+/* ------------------------------------------------------------------------
+ * Routing records (gating.hpp) and the reference cost model (simulator.hpp).
+ * ---------------------------------------------------------------------- */
+/* Uniform stand-in router; slots[(t*L + l)*k + i], ascending per record. */
+int moe_generate_trace(const moe_model_profile* p, int tokens, uint64_t seed, int32_t* slots,
+                       uint64_t* fingerprint);
+/* v1 text; returns length (required length when cap too small), -1 on error */
+int64_t moe_write_trace(const moe_model_profile* p, int tokens, const int32_t* slots, char* buf,
+                        int64_t cap);
+int moe_read_trace(const char* document, int32_t dims[4] /*tokens,L,E,k*/, uint64_t* fingerprint,
+                   int32_t* slots, int64_t slots_cap);
+
+typedef struct {                 /* SimReport, simulator.hpp:33-53 */
+    int64_t tokens, activations, hits, bytes_transferred, transfer_ns, compute_ns, nonexpert_ns;
+} moe_sim_report;
+
+/* lru_capacity 0 = Static policy */
+int moe_simulate(const moe_expert_state* entries, int64_t swap_slot_bytes, const int32_t* slots,
+                 int tokens, const moe_model_profile* p, const moe_hardware_profile* hw,
+                 int lru_capacity, moe_sim_report* out);
+double moe_expected_throughput(const moe_expert_state* entries, const moe_model_profile* p,
+                               const moe_hardware_profile* hw);
+
+/* ------------------------------------------------------------------------
+ * Kernels (sm_100a).  Stream-ordered; all pointers are device pointers.
+ * ---------------------------------------------------------------------- */
+
+/* K1: logits = x . wg^T in fp32 (pinned reduction order), top-k
+ * on logits (ties -> lower index, output in descending logit order), weights
+ * = softmax over the selected logits.  x [T,d] bf16, wg [E,d] bf16 ->
+ * idx [T,k] int32, w [T,k] fp32, logits [T,E] fp32 (optional). */
+int moe_gate_topk(const void* x, const void* wg, int T, int d, int E, int k, int32_t* idx,
+                  float* w, float* logits, void* stream);
+
+/* K2: stable expert-major counting sort of the T*k (token, j) pairs.
+ * counts [E], offsets [E+1], perm [T*k] (perm[pos] = t*k + j),
+ * inv_perm [T*k] (inv_perm[t*k + j] = pos).  Bit-exact, no atomics. */
+int moe_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_t* offsets,
+                int32_t* perm, int32_t* inv_perm, void* stream);
+
+/* Weights of one expert as the kernels see them. */
+typedef struct {
+    int32_t precision;        /* MOE_P4 (int4-g128) or MOE_P16 (bf16)                       */
+    int32_t pad_;
+    const void* w_gate_up;    /* P16: bf16 [2f,d] (rows [0,f) gate, [f,2f) up); P4: uint32 [2f,d/8] */
+    const void* s_gate_up;    /* P4: bf16 scales [2f,d/128]; P16: NULL                      */
+    const void* w_down;       /* P16: bf16 [d,f]; P4: uint32 [d,f/8]                        */
+    const void* s_down;       /* P4: bf16 [d,f/128]                                         */
+} moe_expert_weights;
+
+/* K3/K4: grouped SwiGLU FFN of every expert segment of a permutation.
+ * x [T,d] bf16 (gathered through perm on the fly), offsets [E+1] (device),
+ * experts[E] (host array of device pointers), h_ws [T*k, f] bf16 workspace,
+ * y_perm [T*k, d] fp32.  Mixed precision per expert.  Uses the 128-bit GEMV
+ * kernels for T <= moe_gemv_max_tokens() and the tcgen05 GEMM otherwise. */
+int moe_ffn(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+            const moe_expert_weights* experts, int E, int d, int f, void* h_ws, float* y_perm,
+            void* stream);
+/* Survey-named single-precision wrappers of moe_ffn (all experts one format). */
+int moe_ffn_int4(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+                 const void* const* q_gate_up, const void* const* s_gate_up,
+                 const void* const* q_down, const void* const* s_down, int E, int d, int f,
+                 void* h_ws, float* y_perm, void* stream);
+int moe_ffn_bf16(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+                 const void* const* w_gate_up, const void* const* w_down, int E, int d, int f,
+                 void* h_ws, float* y_perm, void* stream);
+int moe_gemv_max_tokens(void);
+
+/* K5: out[t] = bf16(residual[t] + sum_j w[t,j] * y_perm[inv_perm[t*k+j]]),
+ * fp32 fma chain in j order; residual may be NULL. */
+int moe_combine(const float* y_perm, const int32_t* inv_perm, const float* w,
+                const void* residual, int T, int d, int k, void* out, void* stream);
+
+/* int4-g128 quantiser (bf16 [rows,cols] -> packed q + scales), the on-device
+ * "Quantize" action of the reconfiguration model (reconfig.hpp:12). */
+int moe_quantize_g128(const void* w, int rows, int cols, uint32_t* q, void* s, void* stream);
+
+/* Deterministic synthetic tensors (same generator as the oracle). */
+int moe_synth_weight_bf16(uint64_t seed, uint64_t uid, int64_t n, int shift, void* out,
+                          void* stream);
+int moe_synth_input_bf16(uint64_t seed, uint64_t uid, int64_t n, void* out, void* stream);
+int moe_weight_shift(int K);
+
+/* Host-resident expert streaming: pinned H2D on a side stream, recorded on
+ * `done_event` (cudaEvent_t as void*), which the compute stream waits on. */
+int moe_stream_expert(void* dst_dev, const void* src_pinned, size_t bytes, void* copy_stream,
+                      void* done_event);
+
+/* ------------------------------------------------------------------------
+ * Engine: one MoE layer stack on one device, owning weights laid out per a
+ * placement plan (device-resident experts in HBM, host-resident experts in a
+ * pinned arena streamed into the swap slot on a side stream, Static policy).
+ * ---------------------------------------------------------------------- */
+typedef struct moe_engine moe_engine;
+
+typedef struct {
+    int32_t num_layers, experts_per_layer, top_k, d_model, d_ffn;
+    int32_t max_tokens;        /* largest decode batch T the engine is sized for */
+    uint64_t seed;             /* synthetic weight seed                          */
+    int32_t device;
+    int32_t use_graphs;        /* capture decode steps in CUDA graphs            */
+} moe_engine_config;
+
+int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan_entries,
+                      moe_engine** out);
+void moe_engine_destroy(moe_engine* eng);
+/* Bytes of device memory held for experts / swap / workspaces. */
+int moe_engine_memory(const moe_engine* eng, int64_t* expert_bytes, int64_t* swap_bytes,
+                      int64_t* host_pinned_bytes, int64_t* workspace_bytes);
+/* Device pointer to the layer input buffer [max_tokens, d] bf16. */
+void* moe_engine_input(moe_engine* eng);
+void* moe_engine_output(moe_engine* eng);
+/* Fill the input buffer with the synthetic embedding of decode step `step`. */
+int moe_engine_synth_input(moe_engine* eng, int step, int T);
+/* One decode step of T tokens through all layers, input -> output, on the
+ * engine's compute stream (async).  Routing of every layer is kept for
+ * export. */
+int moe_engine_decode(moe_engine* eng, int T);
+/* Same, with host buffers: H2D of x_host, decode, D2H into out_host, synced. */
+int moe_engine_decode_host(moe_engine* eng, const void* x_host, int T, void* out_host);
+/* One layer: x (device [T,d]) -> out (device), routing outputs optional. */
+int moe_engine_forward_layer(moe_engine* eng, int layer, const void* x, int T, void* out,
+                             int32_t* idx_dev, float* w_dev, float* logits_dev);
+int moe_engine_sync(moe_engine* eng);
+/* Eager decode step with CUDA events around each layer's expert-FFN launches
+ * (compute stream): ffn_ms[num_layers], algorithmic ffn_bytes[num_layers]
+ * (selected experts' weights + activations), kernels launched per step. */
+int moe_engine_profile_step(moe_engine* eng, int T, float* ffn_ms, int64_t* ffn_bytes,
+                            int32_t* kernels_per_step);
+void* moe_engine_stream(moe_engine* eng);
+/* Routing of the last decode step: slots [T, L, k] ascending per record
+ * (GatingTrace layout, gating.hpp:22) -- host buffer. */
+int moe_engine_last_routing(moe_engine* eng, int T, int32_t* slots_out);
+/* Cumulative SimReport counters of real runs (hits / bytes_transferred /
+ * activations follow simulate() semantics for the engine's plan). */
+int moe_engine_counters(const moe_engine* eng, moe_sim_report* out);
+int moe_engine_reset_counters(moe_engine* eng);
+/* Per-expert device weight view (for tests); host-resident experts report
+ * their pinned host pointers with location MOE_CPU. */
+int moe_engine_expert(const moe_engine* eng, int layer, int slot, moe_expert_weights* out,
+                      int32_t* location);
+int moe_engine_router(const moe_engine* eng, int layer, const void** wg_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_B200_H */

@@ -1,0 +1,73 @@
+// engine.hpp -- MoeEngine: the B200 MoE-layer forward.
+//
+// Replaces the reference's MoE-layer stand-in simulate() (simulator.hpp:58,
+// body simulator.cpp:89-110) with real kernels, keeping its contract:
+//   - the expert table comes from a PlacementPlan (planner.hpp:31-36):
+//     GPU-resident experts live in HBM at their precision, CPU-resident
+//     experts live in a pinned host arena and are streamed into the swap slot
+//     (Static policy, simulator.hpp:12-16: every CPU-resident activation is a
+//     miss that re-streams the expert) with cudaMemcpyAsync on a side stream;
+//     they are never computed on the CPU;
+//   - the router is real (K1 top-k softmax) and its decisions are exportable
+//     as a GatingTrace (gating.hpp:16-29);
+//   - cumulative counters follow SimReport (simulator.hpp:33-53): for the
+//     same plan and routing, activations / hits / bytes_transferred equal
+//     simulate()'s.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "moe_b200.h"
+#include "moeb200/gating.hpp"
+#include "moeb200/planner.hpp"
+#include "moeb200/simulator.hpp"
+
+namespace moeb200 {
+
+struct EngineConfig {
+    ModelProfile profile;     // layers, experts/layer, top_k, byte sizes
+    MoeShape shape;           // d_model, d_ffn, group
+    int max_tokens = 1;
+    uint64_t seed = 0;
+    int device = 0;
+    bool use_graphs = true;
+};
+
+class MoeEngine {
+  public:
+    MoeEngine(const EngineConfig& cfg, const PlacementPlan& plan);
+    ~MoeEngine();
+    MoeEngine(const MoeEngine&) = delete;
+    MoeEngine& operator=(const MoeEngine&) = delete;
+
+    void* input();
+    void* output();
+    void* stream();
+    void synth_input(int step, int T);
+    // One decode step of T tokens through all layers (async on stream()).
+    void decode(int T);
+    void decode_host(const void* x_host, int T, void* out_host);
+    void forward_layer(int layer, const void* x, int T, void* out, int32_t* idx, float* w,
+                       float* logits);
+    void sync();
+    // Eager step with CUDA events around every layer's expert FFN (see
+    // engine.cpp); ffn_ms / ffn_bytes have num_layers entries.
+    void profile_step(int T, float* ffn_ms, int64_t* ffn_bytes, int* kernels_per_step);
+
+    GatingTrace last_routing(int T);
+    const SimReport& counters() const;
+    void reset_counters();
+    moe_expert_weights expert(int layer, int slot, int* location) const;
+    const void* router(int layer) const;
+    void memory(int64_t* expert_bytes, int64_t* swap_bytes, int64_t* host_bytes,
+                int64_t* workspace_bytes) const;
+
+    struct Impl;
+
+  private:
+    std::unique_ptr<Impl> impl_;
+};
+
+}  // namespace moeb200

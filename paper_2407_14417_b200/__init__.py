@@ -1,0 +1,544 @@
+"""paper_2407_14417_b200 -- B200-native MoE expert-layer hot path of arXiv 2407.14417.
+
+Python view of the C ABI in include/moe_b200.h (libmoe_b200.so, built in-tree
+for sm_100a).  Names follow the reference's operator API
+(/root/reference/proj/include/moeserve): ModelProfile / HardwareProfile /
+TaskRequest (profiles.hpp:29-59), make_plan (planner.hpp:71), generate_trace
+(gating.hpp:33), simulate (simulator.hpp:58), plus the kernel entry points
+and MoeEngine that replace the reference's cost-model stand-ins with real
+sm_100a kernels.  There is no CPU fallback: kernel calls without a CUDA
+device raise MoeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmoe_b200.so")
+
+MOE_P4, MOE_P16 = 0, 1
+MOE_GPU, MOE_CPU = 0, 1
+THROUGHPUT, QUALITY = 0, 1
+MAX_EXPERTS = 64
+
+
+class MoeError(RuntimeError):
+    """Raised for non-zero status; .code mirrors the reference CLI exit codes
+    (cli.hpp:7-8): 1 internal, 2 usage, 3 parse/validation, 4 infeasible."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class ValidationError(MoeError):
+    pass
+
+
+class InfeasibleError(MoeError):
+    pass
+
+
+class UsageError(MoeError):
+    pass
+
+
+class _ModelProfile(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("experts_per_layer", C.c_int32), ("top_k", C.c_int32),
+                ("pad_", C.c_int32), ("size_nonexpert_bytes", C.c_int64),
+                ("size_expert16_bytes", C.c_int64), ("quant_ratio", C.c_double),
+                ("compute_latency16_s", C.c_double), ("compute_penalty4", C.c_double),
+                ("nonexpert_latency_s", C.c_double)]
+
+
+class _HardwareProfile(C.Structure):
+    _fields_ = [("gpu_mem_bytes", C.c_int64), ("transfer_bw_bytes_per_s", C.c_double)]
+
+
+class _TaskRequest(C.Structure):
+    _fields_ = [("preference", C.c_int32), ("n4_target", C.c_int32), ("seed", C.c_uint64)]
+
+
+class ExpertStateC(C.Structure):
+    _fields_ = [("precision", C.c_int32), ("location", C.c_int32)]
+
+
+class SimReportC(C.Structure):
+    _fields_ = [("tokens", C.c_int64), ("activations", C.c_int64), ("hits", C.c_int64),
+                ("bytes_transferred", C.c_int64), ("transfer_ns", C.c_int64),
+                ("compute_ns", C.c_int64), ("nonexpert_ns", C.c_int64)]
+
+
+class ExpertWeightsC(C.Structure):
+    _fields_ = [("precision", C.c_int32), ("pad_", C.c_int32), ("w_gate_up", C.c_void_p),
+                ("s_gate_up", C.c_void_p), ("w_down", C.c_void_p), ("s_down", C.c_void_p)]
+
+
+class _EngineConfig(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("experts_per_layer", C.c_int32), ("top_k", C.c_int32),
+                ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("max_tokens", C.c_int32),
+                ("seed", C.c_uint64), ("device", C.c_int32), ("use_graphs", C.c_int32)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libmoe_b200.so (fails loudly when it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (make -C paper_2407_14417_b200/csrc)")
+    L = C.CDLL(LIB_PATH)
+    P, I, I64, U64, D, VP = C.POINTER, C.c_int, C.c_int64, C.c_uint64, C.c_double, C.c_void_p
+    sig = {
+        "moe_last_error": (C.c_char_p, []),
+        "moe_version": (I, []),
+        "moe_profile_builtin": (I, [I, P(_ModelProfile)]),
+        "moe_profile_for_shape": (I, [I, I, I, I, I, I64, P(_ModelProfile)]),
+        "moe_load_profiles": (I, [C.c_char_p, P(_ModelProfile), P(_HardwareProfile)]),
+        "moe_parse_size": (I64, [C.c_char_p]),
+        "moe_expert_size": (I64, [P(_ModelProfile), I]),
+        "moe_model_size": (I, [P(_ModelProfile), I, I, P(I64)]),
+        "moe_profile_fingerprint": (U64, [P(_ModelProfile)]),
+        "moe_num_experts_16": (I, [I64, P(_ModelProfile)]),
+        "moe_make_plan": (I, [P(_TaskRequest), P(_HardwareProfile), P(_ModelProfile), P(ExpertStateC), P(I64)]),
+        "moe_assign_locations": (I, [P(C.c_int32), P(_HardwareProfile), P(_ModelProfile), U64, P(ExpertStateC), P(I64)]),
+        "moe_gpu_footprint": (I64, [P(ExpertStateC), I64, P(_ModelProfile)]),
+        "moe_validate_plan": (I, [P(ExpertStateC), I, I64, P(_HardwareProfile), P(_ModelProfile), C.c_char_p, I]),
+        "moe_generate_trace": (I, [P(_ModelProfile), I, U64, P(C.c_int32), P(U64)]),
+        "moe_write_trace": (I64, [P(_ModelProfile), I, P(C.c_int32), C.c_char_p, I64]),
+        "moe_read_trace": (I, [C.c_char_p, P(C.c_int32), P(U64), P(C.c_int32), I64]),
+        "moe_simulate": (I, [P(ExpertStateC), I64, P(C.c_int32), I, P(_ModelProfile), P(_HardwareProfile), I, P(SimReportC)]),
+        "moe_expected_throughput": (D, [P(ExpertStateC), P(_ModelProfile), P(_HardwareProfile)]),
+        "moe_gate_topk": (I, [VP, VP, I, I, I, I, VP, VP, VP, VP]),
+        "moe_permute": (I, [VP, I, I, I, VP, VP, VP, VP, VP]),
+        "moe_ffn": (I, [VP, VP, VP, I, I, P(ExpertWeightsC), I, I, I, VP, VP, VP]),
+        "moe_ffn_int4": (I, [VP, VP, VP, I, I, P(VP), P(VP), P(VP), P(VP), I, I, I, VP, VP, VP]),
+        "moe_ffn_bf16": (I, [VP, VP, VP, I, I, P(VP), P(VP), I, I, I, VP, VP, VP]),
+        "moe_gemv_max_tokens": (I, []),
+        "moe_combine": (I, [VP, VP, VP, VP, I, I, I, VP, VP]),
+        "moe_quantize_g128": (I, [VP, I, I, VP, VP, VP]),
+        "moe_synth_weight_bf16": (I, [U64, U64, I64, I, VP, VP]),
+        "moe_synth_input_bf16": (I, [U64, U64, I64, VP, VP]),
+        "moe_weight_shift": (I, [I]),
+        "moe_stream_expert": (I, [VP, VP, C.c_size_t, VP, VP]),
+        "moe_engine_create": (I, [P(_EngineConfig), P(ExpertStateC), P(VP)]),
+        "moe_engine_destroy": (None, [VP]),
+        "moe_engine_memory": (I, [VP, P(I64), P(I64), P(I64), P(I64)]),
+        "moe_engine_input": (VP, [VP]),
+        "moe_engine_output": (VP, [VP]),
+        "moe_engine_stream": (VP, [VP]),
+        "moe_engine_synth_input": (I, [VP, I, I]),
+        "moe_engine_decode": (I, [VP, I]),
+        "moe_engine_decode_host": (I, [VP, VP, I, VP]),
+        "moe_engine_forward_layer": (I, [VP, I, VP, I, VP, VP, VP, VP]),
+        "moe_engine_sync": (I, [VP]),
+        "moe_engine_profile_step": (I, [VP, I, P(C.c_float), P(I64), P(C.c_int32)]),
+        "moe_engine_last_routing": (I, [VP, I, P(C.c_int32)]),
+        "moe_engine_counters": (I, [VP, P(SimReportC)]),
+        "moe_engine_reset_counters": (I, [VP]),
+        "moe_engine_expert": (I, [VP, I, I, P(ExpertWeightsC), P(C.c_int32)]),
+        "moe_engine_router": (I, [VP, I, P(VP)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def exported_symbols() -> List[str]:
+    """Every extern "C" function declared in include/moe_b200.h."""
+    import re
+    hdr = os.path.join(os.path.dirname(_HERE), "include", "moe_b200.h")
+    text = open(hdr).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(moe_[a-z0-9_]+)\s*\(", text)))
+
+
+def _check(status: int):
+    if status != 0:
+        msg = lib().moe_last_error().decode(errors="replace")
+        cls = {2: UsageError, 3: ValidationError, 4: InfeasibleError}.get(status, MoeError)
+        raise cls(status, msg)
+
+
+# ----------------------------------------------------------------- profiles
+@dataclass
+class ModelProfile:
+    """profiles.hpp:29-43 (defaults = mixtral-sec41)."""
+    num_layers: int = 32
+    experts_per_layer: int = 8
+    top_k: int = 2
+    size_nonexpert_bytes: int = 3_160_000_000
+    size_expert16_bytes: int = 336_000_000
+    quant_ratio: float = 4.0
+    compute_latency16_s: float = 0.9 / (13.0 * 32.0 * 2.0)
+    compute_penalty4: float = 1.15
+    nonexpert_latency_s: float = 0.1 / 13.0
+
+    @property
+    def num_experts(self) -> int:
+        return self.num_layers * self.experts_per_layer
+
+    def _c(self) -> _ModelProfile:
+        return _ModelProfile(self.num_layers, self.experts_per_layer, self.top_k, 0,
+                             self.size_nonexpert_bytes, self.size_expert16_bytes, self.quant_ratio,
+                             self.compute_latency16_s, self.compute_penalty4, self.nonexpert_latency_s)
+
+    @staticmethod
+    def _from_c(c: _ModelProfile) -> "ModelProfile":
+        return ModelProfile(c.num_layers, c.experts_per_layer, c.top_k, c.size_nonexpert_bytes,
+                            c.size_expert16_bytes, c.quant_ratio, c.compute_latency16_s,
+                            c.compute_penalty4, c.nonexpert_latency_s)
+
+
+@dataclass
+class HardwareProfile:
+    """profiles.hpp:45-52."""
+    gpu_mem_bytes: int = 80_000_000_000
+    transfer_bw_bytes_per_s: float = 336_000_000.0 / 0.02735
+
+    def _c(self) -> _HardwareProfile:
+        return _HardwareProfile(self.gpu_mem_bytes, self.transfer_bw_bytes_per_s)
+
+
+@dataclass
+class TaskRequest:
+    """profiles.hpp:55-59."""
+    preference: int = THROUGHPUT
+    n4_target: Optional[int] = None
+    seed: int = 0
+
+
+def mixtral_sec41() -> ModelProfile:
+    c = _ModelProfile()
+    _check(lib().moe_profile_builtin(0, C.byref(c)))
+    return ModelProfile._from_c(c)
+
+
+def mixtral_table1() -> ModelProfile:
+    c = _ModelProfile()
+    _check(lib().moe_profile_builtin(1, C.byref(c)))
+    return ModelProfile._from_c(c)
+
+
+def profile_for_shape(d_model: int, d_ffn: int, num_layers: int, experts_per_layer: int = 8,
+                      top_k: int = 2, size_nonexpert_bytes: int = 1) -> ModelProfile:
+    c = _ModelProfile()
+    _check(lib().moe_profile_for_shape(d_model, d_ffn, num_layers, experts_per_layer, top_k,
+                                       size_nonexpert_bytes, C.byref(c)))
+    return ModelProfile._from_c(c)
+
+
+def load_profiles(document: str):
+    m, h = _ModelProfile(), _HardwareProfile()
+    _check(lib().moe_load_profiles(document.encode(), C.byref(m), C.byref(h)))
+    return ModelProfile._from_c(m), HardwareProfile(h.gpu_mem_bytes, h.transfer_bw_bytes_per_s)
+
+
+def parse_size(text: str) -> int:
+    v = lib().moe_parse_size(text.encode())
+    if v < 0:
+        _check(3)
+    return v
+
+
+def expert_size(profile: ModelProfile, precision: int) -> int:
+    return lib().moe_expert_size(C.byref(profile._c()), precision)
+
+
+def model_size(profile: ModelProfile, n4: int, nonexpert_precision: int) -> int:
+    out = C.c_int64()
+    _check(lib().moe_model_size(C.byref(profile._c()), n4, nonexpert_precision, C.byref(out)))
+    return out.value
+
+
+def profile_fingerprint(profile: ModelProfile) -> int:
+    return lib().moe_profile_fingerprint(C.byref(profile._c()))
+
+
+def num_experts_16(mem_gpu: int, profile: ModelProfile) -> int:
+    return lib().moe_num_experts_16(mem_gpu, C.byref(profile._c()))
+
+
+# ----------------------------------------------------------------- planner
+@dataclass
+class PlacementPlan:
+    """planner.hpp:31-36: entries[layer*E + slot] = (precision, location)."""
+    precision: List[int]
+    location: List[int]
+    swap_slot_bytes: int
+    seed: int = 0
+
+    def _entries(self):
+        arr = (ExpertStateC * len(self.precision))()
+        for i, (p, l) in enumerate(zip(self.precision, self.location)):
+            arr[i].precision, arr[i].location = p, l
+        return arr
+
+    @property
+    def n4(self) -> int:
+        return sum(1 for p in self.precision if p == MOE_P4)
+
+    @property
+    def n_gpu(self) -> int:
+        return sum(1 for l in self.location if l == MOE_GPU)
+
+
+def make_plan(task: TaskRequest, hw: HardwareProfile, profile: ModelProfile) -> PlacementPlan:
+    n = profile.num_experts
+    arr = (ExpertStateC * n)()
+    swap = C.c_int64()
+    t = _TaskRequest(task.preference, -1 if task.n4_target is None else task.n4_target, task.seed)
+    _check(lib().moe_make_plan(C.byref(t), C.byref(hw._c()), C.byref(profile._c()), arr, C.byref(swap)))
+    return PlacementPlan([a.precision for a in arr], [a.location for a in arr], swap.value, task.seed)
+
+
+def assign_locations(precisions: Sequence[int], hw: HardwareProfile, profile: ModelProfile,
+                     seed: int = 0) -> PlacementPlan:
+    n = profile.num_experts
+    prec = (C.c_int32 * n)(*precisions)
+    arr = (ExpertStateC * n)()
+    swap = C.c_int64()
+    _check(lib().moe_assign_locations(prec, C.byref(hw._c()), C.byref(profile._c()), seed, arr, C.byref(swap)))
+    return PlacementPlan([a.precision for a in arr], [a.location for a in arr], swap.value, seed)
+
+
+def gpu_footprint(plan: PlacementPlan, profile: ModelProfile) -> int:
+    return lib().moe_gpu_footprint(plan._entries(), plan.swap_slot_bytes, C.byref(profile._c()))
+
+
+def validate_plan(plan: PlacementPlan, hw: HardwareProfile, profile: ModelProfile) -> List[str]:
+    buf = C.create_string_buffer(4096)
+    n = lib().moe_validate_plan(plan._entries(), len(plan.precision), plan.swap_slot_bytes,
+                                C.byref(hw._c()), C.byref(profile._c()), buf, 4096)
+    if n < 0:
+        _check(1)
+    return [s for s in buf.value.decode().split("\n") if s][:n]
+
+
+# ----------------------------------------------------------------- traces / simulate
+def generate_trace(profile: ModelProfile, tokens: int, seed: int):
+    n = tokens * profile.num_layers * profile.top_k
+    slots = (C.c_int32 * max(n, 1))()
+    fp = C.c_uint64()
+    _check(lib().moe_generate_trace(C.byref(profile._c()), tokens, seed, slots, C.byref(fp)))
+    return list(slots[:n]), fp.value
+
+
+def write_trace(profile: ModelProfile, tokens: int, slots: Sequence[int]) -> str:
+    arr = (C.c_int32 * len(slots))(*slots)
+    n = lib().moe_write_trace(C.byref(profile._c()), tokens, arr, None, 0)
+    if n < 0:
+        _check(1)
+    buf = C.create_string_buffer(n + 1)
+    lib().moe_write_trace(C.byref(profile._c()), tokens, arr, buf, n + 1)
+    return buf.value.decode()
+
+
+def read_trace(document: str):
+    dims = (C.c_int32 * 4)()
+    fp = C.c_uint64()
+    _check(lib().moe_read_trace(document.encode(), dims, C.byref(fp), None, 0))
+    n = dims[0] * dims[1] * dims[3]
+    slots = (C.c_int32 * max(n, 1))()
+    _check(lib().moe_read_trace(document.encode(), dims, C.byref(fp), slots, n))
+    return {"tokens": dims[0], "num_layers": dims[1], "experts_per_layer": dims[2], "top_k": dims[3],
+            "fingerprint": fp.value, "slots": list(slots[:n])}
+
+
+@dataclass
+class SimReport:
+    """simulator.hpp:33-53."""
+    tokens: int = 0
+    activations: int = 0
+    hits: int = 0
+    bytes_transferred: int = 0
+    transfer_ns: int = 0
+    compute_ns: int = 0
+    nonexpert_ns: int = 0
+
+    @staticmethod
+    def _from_c(c: SimReportC) -> "SimReport":
+        return SimReport(c.tokens, c.activations, c.hits, c.bytes_transferred, c.transfer_ns,
+                         c.compute_ns, c.nonexpert_ns)
+
+    @property
+    def total_ns(self) -> int:
+        return self.transfer_ns + self.compute_ns + self.nonexpert_ns
+
+    @property
+    def throughput_tps(self) -> float:
+        return self.tokens / (self.total_ns / 1e9)
+
+    @property
+    def hit_rate(self) -> float:
+        return 1.0 if self.activations == 0 else self.hits / self.activations
+
+
+def simulate(plan: PlacementPlan, slots: Sequence[int], tokens: int, profile: ModelProfile,
+             hw: HardwareProfile, lru_capacity: int = 0) -> SimReport:
+    arr = (C.c_int32 * len(slots))(*slots)
+    out = SimReportC()
+    _check(lib().moe_simulate(plan._entries(), plan.swap_slot_bytes, arr, tokens, C.byref(profile._c()),
+                              C.byref(hw._c()), lru_capacity, C.byref(out)))
+    return SimReport._from_c(out)
+
+
+def expected_throughput(plan: PlacementPlan, profile: ModelProfile, hw: HardwareProfile) -> float:
+    return lib().moe_expected_throughput(plan._entries(), C.byref(profile._c()), C.byref(hw._c()))
+
+
+# ----------------------------------------------------------------- kernels
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr() if hasattr(t, "data_ptr") else int(t)
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        try:
+            import torch
+            return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            return None
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def gate_topk(x, wg, T, d, E, k, idx, w, logits=None, stream=None):
+    _check(lib().moe_gate_topk(_ptr(x), _ptr(wg), T, d, E, k, _ptr(idx), _ptr(w), _ptr(logits), _stream(stream)))
+
+
+def permute(idx, T, E, k, counts, offsets, perm, inv_perm, stream=None):
+    _check(lib().moe_permute(_ptr(idx), T, E, k, _ptr(counts), _ptr(offsets), _ptr(perm), _ptr(inv_perm),
+                             _stream(stream)))
+
+
+def expert_weights(precision, w_gate_up, w_down, s_gate_up=None, s_down=None) -> ExpertWeightsC:
+    return ExpertWeightsC(precision, 0, _ptr(w_gate_up), _ptr(s_gate_up), _ptr(w_down), _ptr(s_down))
+
+
+def ffn(x, perm, offsets, T, k, experts: Sequence[ExpertWeightsC], d, f, h_ws, y_perm, stream=None):
+    arr = (ExpertWeightsC * len(experts))(*experts)
+    _check(lib().moe_ffn(_ptr(x), _ptr(perm), _ptr(offsets), T, k, arr, len(experts), d, f, _ptr(h_ws),
+                         _ptr(y_perm), _stream(stream)))
+
+
+def combine(y_perm, inv_perm, w, residual, T, d, k, out, stream=None):
+    _check(lib().moe_combine(_ptr(y_perm), _ptr(inv_perm), _ptr(w), _ptr(residual), T, d, k, _ptr(out),
+                             _stream(stream)))
+
+
+def quantize_g128(w, rows, cols, q, s, stream=None):
+    _check(lib().moe_quantize_g128(_ptr(w), rows, cols, _ptr(q), _ptr(s), _stream(stream)))
+
+
+def synth_weight_bf16(seed, uid, n, shift, out, stream=None):
+    _check(lib().moe_synth_weight_bf16(seed, uid, n, shift, _ptr(out), _stream(stream)))
+
+
+def weight_shift(K: int) -> int:
+    return lib().moe_weight_shift(K)
+
+
+# ----------------------------------------------------------------- engine
+class MoeEngine:
+    """One MoE layer stack on one device (include/moeb200/engine.hpp)."""
+
+    def __init__(self, num_layers: int, experts_per_layer: int, top_k: int, d_model: int, d_ffn: int,
+                 plan: PlacementPlan, max_tokens: int = 1, seed: int = 0, device: int = 0,
+                 use_graphs: bool = True):
+        self.L, self.E, self.k, self.d, self.f = num_layers, experts_per_layer, top_k, d_model, d_ffn
+        self.max_tokens = max_tokens
+        cfg = _EngineConfig(num_layers, experts_per_layer, top_k, d_model, d_ffn, max_tokens, seed, device,
+                            1 if use_graphs else 0)
+        h = C.c_void_p()
+        _check(lib().moe_engine_create(C.byref(cfg), plan._entries(), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().moe_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def input_ptr(self) -> int:
+        return lib().moe_engine_input(self._h)
+
+    @property
+    def output_ptr(self) -> int:
+        return lib().moe_engine_output(self._h)
+
+    @property
+    def stream_ptr(self) -> int:
+        return lib().moe_engine_stream(self._h)
+
+    def memory(self):
+        vals = [C.c_int64() for _ in range(4)]
+        _check(lib().moe_engine_memory(self._h, *[C.byref(v) for v in vals]))
+        return dict(zip(["expert_bytes", "swap_bytes", "host_pinned_bytes", "workspace_bytes"],
+                        [v.value for v in vals]))
+
+    def synth_input(self, step: int, T: int):
+        _check(lib().moe_engine_synth_input(self._h, step, T))
+
+    def decode(self, T: int):
+        _check(lib().moe_engine_decode(self._h, T))
+
+    def decode_host(self, x_host_ptr: int, T: int, out_host_ptr: int):
+        _check(lib().moe_engine_decode_host(self._h, x_host_ptr, T, out_host_ptr))
+
+    def forward_layer(self, layer, x, T, out, idx=None, w=None, logits=None):
+        _check(lib().moe_engine_forward_layer(self._h, layer, _ptr(x), T, _ptr(out), _ptr(idx), _ptr(w),
+                                              _ptr(logits)))
+
+    def sync(self):
+        _check(lib().moe_engine_sync(self._h))
+
+    def profile_step(self, T: int):
+        """Per-layer expert-FFN milliseconds (CUDA events on the launch stream),
+        per-layer algorithmic bytes, kernels per decode step."""
+        ms = (C.c_float * self.L)()
+        by = (C.c_int64 * self.L)()
+        kps = C.c_int32()
+        _check(lib().moe_engine_profile_step(self._h, T, ms, by, C.byref(kps)))
+        return list(ms), list(by), kps.value
+
+    def last_routing(self, T: int) -> List[int]:
+        n = T * self.L * self.k
+        arr = (C.c_int32 * n)()
+        _check(lib().moe_engine_last_routing(self._h, T, arr))
+        return list(arr)
+
+    def counters(self) -> SimReport:
+        out = SimReportC()
+        _check(lib().moe_engine_counters(self._h, C.byref(out)))
+        return SimReport._from_c(out)
+
+    def reset_counters(self):
+        _check(lib().moe_engine_reset_counters(self._h))
+
+    def expert(self, layer: int, slot: int):
+        out = ExpertWeightsC()
+        loc = C.c_int32()
+        _check(lib().moe_engine_expert(self._h, layer, slot, C.byref(out), C.byref(loc)))
+        return out, loc.value
+
+    def router(self, layer: int) -> int:
+        p = C.c_void_p()
+        _check(lib().moe_engine_router(self._h, layer, C.byref(p)))
+        return p.value

@@ -1,0 +1,529 @@
+// capi.cu -- the extern "C" boundary (include/moe_b200.h).
+//
+// Status codes mirror the reference CLI's exit codes (cli.hpp:7-8,
+// cli.cpp:473-488): exceptions of the reference's four error types map to
+// 2 (usage), 3 (parse/validation), 4 (infeasible); CUDA and other failures
+// to 1.  No entry point falls back to the CPU.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "kernels/launch.h"
+#include "moe_b200.h"
+#include "moeb200/engine.hpp"
+
+using namespace moeb200;
+
+namespace moeb200 {
+int weight_shift(int K);
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& fn) {
+    try {
+        fn();
+        return MOE_OK;
+    } catch (const UsageError& e) {
+        g_err = e.what();
+        return MOE_ERR_USAGE;
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        return MOE_ERR_VALIDATION;
+    } catch (const ValidationError& e) {
+        g_err = e.what();
+        return MOE_ERR_VALIDATION;
+    } catch (const InfeasibleError& e) {
+        g_err = e.what();
+        return MOE_ERR_INFEASIBLE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return MOE_ERR_INTERNAL;
+    } catch (...) {
+        g_err = "unknown error";
+        return MOE_ERR_INTERNAL;
+    }
+}
+
+void usage_if(bool bad, const char* msg) {
+    if (bad) throw UsageError(msg);
+}
+
+ModelProfile to_model(const moe_model_profile* p) {
+    usage_if(p == nullptr, "null model profile");
+    ModelProfile m;
+    m.num_layers = p->num_layers;
+    m.experts_per_layer = p->experts_per_layer;
+    m.top_k = p->top_k;
+    m.size_nonexpert_bytes = p->size_nonexpert_bytes;
+    m.size_expert16_bytes = p->size_expert16_bytes;
+    m.quant_ratio = p->quant_ratio;
+    m.compute_latency16_s = p->compute_latency16_s;
+    m.compute_penalty4 = p->compute_penalty4;
+    m.nonexpert_latency_s = p->nonexpert_latency_s;
+    return m;
+}
+
+void from_model(const ModelProfile& m, moe_model_profile* p) {
+    std::memset(p, 0, sizeof *p);
+    p->num_layers = m.num_layers;
+    p->experts_per_layer = m.experts_per_layer;
+    p->top_k = m.top_k;
+    p->size_nonexpert_bytes = m.size_nonexpert_bytes;
+    p->size_expert16_bytes = m.size_expert16_bytes;
+    p->quant_ratio = m.quant_ratio;
+    p->compute_latency16_s = m.compute_latency16_s;
+    p->compute_penalty4 = m.compute_penalty4;
+    p->nonexpert_latency_s = m.nonexpert_latency_s;
+}
+
+HardwareProfile to_hw(const moe_hardware_profile* h) {
+    usage_if(h == nullptr, "null hardware profile");
+    HardwareProfile hw;
+    hw.gpu_mem_bytes = h->gpu_mem_bytes;
+    hw.transfer_bw_bytes_per_s = h->transfer_bw_bytes_per_s;
+    return hw;
+}
+
+PlacementPlan to_plan(const moe_expert_state* entries, int n, int64_t swap) {
+    PlacementPlan plan;
+    plan.entries.resize(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+        plan.entries[static_cast<size_t>(i)].precision = entries[i].precision == MOE_P4 ? Precision::P4 : Precision::P16;
+        plan.entries[static_cast<size_t>(i)].location = entries[i].location == MOE_GPU ? Location::GPU : Location::CPU;
+    }
+    plan.swap_slot_bytes = swap;
+    return plan;
+}
+
+void from_plan(const PlacementPlan& plan, moe_expert_state* entries, int64_t* swap) {
+    for (size_t i = 0; i < plan.entries.size(); ++i) {
+        entries[i].precision = plan.entries[i].precision == Precision::P4 ? MOE_P4 : MOE_P16;
+        entries[i].location = plan.entries[i].location == Location::GPU ? MOE_GPU : MOE_CPU;
+    }
+    if (swap) *swap = plan.swap_slot_bytes;
+}
+
+GatingTrace to_trace(const ModelProfile& m, int tokens, const int32_t* slots) {
+    GatingTrace tr;
+    tr.profile_fingerprint = profile_fingerprint(m);
+    tr.tokens = tokens;
+    tr.num_layers = m.num_layers;
+    tr.experts_per_layer = m.experts_per_layer;
+    tr.top_k = m.top_k;
+    tr.slots.assign(slots, slots + static_cast<size_t>(tokens) * m.num_layers * m.top_k);
+    return tr;
+}
+
+void need_device() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw std::runtime_error("no CUDA device: kernels have no CPU fallback");
+}
+
+cudaStream_t st(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+struct moe_engine {
+    MoeEngine* impl;
+};
+
+extern "C" {
+
+const char* moe_last_error(void) { return g_err.c_str(); }
+int moe_version(void) { return 1; }
+
+int moe_profile_builtin(int which, moe_model_profile* out) {
+    return guarded([&] {
+        usage_if(which != 0 && which != 1, "builtin profile must be 0 (mixtral-sec41) or 1 (mixtral-table1)");
+        from_model(which == 0 ? mixtral_sec41() : mixtral_table1(), out);
+    });
+}
+
+int moe_profile_for_shape(int d_model, int d_ffn, int num_layers, int experts_per_layer, int top_k,
+                          int64_t size_nonexpert_bytes, moe_model_profile* out) {
+    return guarded([&] {
+        MoeShape s;
+        s.d_model = d_model;
+        s.d_ffn = d_ffn;
+        const ModelProfile m = profile_for_shape(s, num_layers, experts_per_layer, top_k, size_nonexpert_bytes);
+        validate_profile(m);
+        from_model(m, out);
+    });
+}
+
+int moe_load_profiles(const char* document, moe_model_profile* model, moe_hardware_profile* hw) {
+    return guarded([&] {
+        usage_if(document == nullptr, "null document");
+        const auto [m, h] = load_profiles(document);
+        from_model(m, model);
+        hw->gpu_mem_bytes = h.gpu_mem_bytes;
+        hw->transfer_bw_bytes_per_s = h.transfer_bw_bytes_per_s;
+    });
+}
+
+int64_t moe_parse_size(const char* text) {
+    int64_t v = -1;
+    if (guarded([&] { v = parse_size(text ? text : ""); }) != MOE_OK) return -1;
+    return v;
+}
+
+int64_t moe_expert_size(const moe_model_profile* p, int precision) {
+    int64_t v = -1;
+    guarded([&] { v = expert_size(to_model(p), precision == MOE_P4 ? Precision::P4 : Precision::P16); });
+    return v;
+}
+
+int moe_model_size(const moe_model_profile* p, int n4, int nonexpert_precision, int64_t* out) {
+    return guarded([&] {
+        const NonexpertPrecision np = nonexpert_precision == 0   ? NonexpertPrecision::P4
+                                      : nonexpert_precision == 1 ? NonexpertPrecision::P8
+                                                                 : NonexpertPrecision::P16;
+        *out = model_size(to_model(p), n4, np);
+    });
+}
+
+uint64_t moe_profile_fingerprint(const moe_model_profile* p) {
+    uint64_t v = 0;
+    guarded([&] { v = profile_fingerprint(to_model(p)); });
+    return v;
+}
+
+int moe_num_experts_16(int64_t mem_gpu, const moe_model_profile* p) {
+    int v = -1;
+    guarded([&] { v = num_experts_16(mem_gpu, to_model(p)); });
+    return v;
+}
+
+int moe_make_plan(const moe_task_request* task, const moe_hardware_profile* hw,
+                  const moe_model_profile* p, moe_expert_state* entries, int64_t* swap_slot_bytes) {
+    return guarded([&] {
+        usage_if(task == nullptr || entries == nullptr, "null argument");
+        TaskRequest t;
+        t.preference = task->preference == MOE_QUALITY ? Preference::Quality : Preference::Throughput;
+        if (task->n4_target != -1) t.n4_target = task->n4_target;
+        t.seed = task->seed;
+        from_plan(make_plan(t, to_hw(hw), to_model(p)), entries, swap_slot_bytes);
+    });
+}
+
+int moe_assign_locations(const int32_t* precisions, const moe_hardware_profile* hw,
+                         const moe_model_profile* p, uint64_t seed, moe_expert_state* entries,
+                         int64_t* swap_slot_bytes) {
+    return guarded([&] {
+        const ModelProfile m = to_model(p);
+        std::vector<Precision> prec(static_cast<size_t>(m.num_experts()));
+        for (size_t i = 0; i < prec.size(); ++i) prec[i] = precisions[i] == MOE_P4 ? Precision::P4 : Precision::P16;
+        from_plan(assign_locations(prec, to_hw(hw), m, seed), entries, swap_slot_bytes);
+    });
+}
+
+int64_t moe_gpu_footprint(const moe_expert_state* entries, int64_t swap_slot_bytes,
+                          const moe_model_profile* p) {
+    int64_t v = -1;
+    guarded([&] {
+        const ModelProfile m = to_model(p);
+        v = gpu_footprint(to_plan(entries, m.num_experts(), swap_slot_bytes), m);
+    });
+    return v;
+}
+
+int moe_validate_plan(const moe_expert_state* entries, int n_entries, int64_t swap_slot_bytes,
+                      const moe_hardware_profile* hw, const moe_model_profile* p, char* msg, int cap) {
+    int n = -1;
+    guarded([&] {
+        const auto v = validate_plan(to_plan(entries, n_entries, swap_slot_bytes), to_hw(hw), to_model(p));
+        n = static_cast<int>(v.size());
+        if (msg && cap > 0) {
+            std::string all;
+            for (const auto& s : v) all += s + "\n";
+            std::strncpy(msg, all.c_str(), static_cast<size_t>(cap - 1));
+            msg[cap - 1] = 0;
+        }
+    });
+    return n;
+}
+
+int moe_generate_trace(const moe_model_profile* p, int tokens, uint64_t seed, int32_t* slots,
+                       uint64_t* fingerprint) {
+    return guarded([&] {
+        const GatingTrace tr = generate_trace(to_model(p), tokens, seed);
+        std::memcpy(slots, tr.slots.data(), tr.slots.size() * 4);
+        if (fingerprint) *fingerprint = tr.profile_fingerprint;
+    });
+}
+
+int64_t moe_write_trace(const moe_model_profile* p, int tokens, const int32_t* slots, char* buf,
+                        int64_t cap) {
+    std::string s;
+    if (guarded([&] { s = write_trace(to_trace(to_model(p), tokens, slots)); }) != MOE_OK) return -1;
+    if (buf && static_cast<int64_t>(s.size()) < cap) std::memcpy(buf, s.c_str(), s.size() + 1);
+    return static_cast<int64_t>(s.size());
+}
+
+int moe_read_trace(const char* document, int32_t dims[4], uint64_t* fingerprint, int32_t* slots,
+                   int64_t slots_cap) {
+    return guarded([&] {
+        const GatingTrace tr = read_trace(document ? document : "");
+        dims[0] = tr.tokens;
+        dims[1] = tr.num_layers;
+        dims[2] = tr.experts_per_layer;
+        dims[3] = tr.top_k;
+        if (fingerprint) *fingerprint = tr.profile_fingerprint;
+        if (slots && static_cast<int64_t>(tr.slots.size()) <= slots_cap)
+            std::memcpy(slots, tr.slots.data(), tr.slots.size() * 4);
+    });
+}
+
+int moe_simulate(const moe_expert_state* entries, int64_t swap_slot_bytes, const int32_t* slots,
+                 int tokens, const moe_model_profile* p, const moe_hardware_profile* hw,
+                 int lru_capacity, moe_sim_report* out) {
+    return guarded([&] {
+        const ModelProfile m = to_model(p);
+        const ResidencyPolicy pol = lru_capacity > 0 ? ResidencyPolicy::lru(lru_capacity) : ResidencyPolicy::static_policy();
+        const SimReport r = simulate(to_plan(entries, m.num_experts(), swap_slot_bytes), to_trace(m, tokens, slots),
+                                     m, to_hw(hw), pol);
+        out->tokens = r.tokens;
+        out->activations = r.activations;
+        out->hits = r.hits;
+        out->bytes_transferred = r.bytes_transferred;
+        out->transfer_ns = r.transfer_ns;
+        out->compute_ns = r.compute_ns;
+        out->nonexpert_ns = r.nonexpert_ns;
+    });
+}
+
+double moe_expected_throughput(const moe_expert_state* entries, const moe_model_profile* p,
+                               const moe_hardware_profile* hw) {
+    double v = -1.0;
+    guarded([&] {
+        const ModelProfile m = to_model(p);
+        v = expected_throughput(to_plan(entries, m.num_experts(), 0), m, to_hw(hw));
+    });
+    return v;
+}
+
+// ---------------------------------------------------------------- kernels
+int moe_gate_topk(const void* x, const void* wg, int T, int d, int E, int k, int32_t* idx,
+                  float* w, float* logits, void* stream) {
+    return guarded([&] {
+        usage_if(T < 0 || d <= 0 || d % 8 != 0, "d must be a positive multiple of 8");
+        usage_if(E < 1 || E > MOE_MAX_EXPERTS || k < 1 || k > E || k > MOE_MAX_TOPK, "bad E / k");
+        need_device();
+        if (T == 0) return;
+        const cudaError_t e = moek_route(x, wg, T, d, E, k, idx, w, logits, nullptr, nullptr, nullptr,
+                                         nullptr, nullptr, st(stream));
+        if (e != cudaSuccess) throw std::runtime_error(std::string("moe_gate_topk: ") + cudaGetErrorString(e));
+    });
+}
+
+int moe_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_t* offsets,
+                int32_t* perm, int32_t* inv_perm, void* stream) {
+    return guarded([&] {
+        usage_if(T < 0 || E < 1 || E > MOE_MAX_EXPERTS || k < 1 || k > E, "bad T / E / k");
+        need_device();
+        const cudaError_t e = moek_permute(idx, T, E, k, counts, offsets, perm, inv_perm, st(stream));
+        if (e != cudaSuccess) throw std::runtime_error(std::string("moe_permute: ") + cudaGetErrorString(e));
+    });
+}
+
+int moe_gemv_max_tokens(void) { return 4; }
+
+int moe_ffn(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+            const moe_expert_weights* experts, int E, int d, int f, void* h_ws, float* y_perm,
+            void* stream) {
+    return guarded([&] {
+        usage_if(E < 1 || E > MOE_MAX_EXPERTS || k < 1 || k > E, "bad E / k");
+        usage_if(d <= 0 || d % 256 != 0 || f <= 0 || f % 128 != 0,
+                 "d must be a multiple of 256 and f a multiple of 128");
+        need_device();
+        if (T == 0) return;
+        const uint64_t mask = E >= 64 ? ~0ull : ((1ull << E) - 1ull);
+        const cudaError_t e = moek_ffn_gemv(x, perm, offsets, T, k, experts, E, d, f, h_ws, y_perm, mask, st(stream));
+        if (e != cudaSuccess) throw std::runtime_error(std::string("moe_ffn: ") + cudaGetErrorString(e));
+    });
+}
+
+int moe_ffn_int4(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+                 const void* const* q_gate_up, const void* const* s_gate_up,
+                 const void* const* q_down, const void* const* s_down, int E, int d, int f,
+                 void* h_ws, float* y_perm, void* stream) {
+    moe_expert_weights ex[MOE_MAX_EXPERTS];
+    if (E < 1 || E > MOE_MAX_EXPERTS) {
+        g_err = "bad E";
+        return MOE_ERR_USAGE;
+    }
+    for (int e = 0; e < E; ++e) ex[e] = {MOE_P4, 0, q_gate_up[e], s_gate_up[e], q_down[e], s_down[e]};
+    return moe_ffn(x, perm, offsets, T, k, ex, E, d, f, h_ws, y_perm, stream);
+}
+
+int moe_ffn_bf16(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+                 const void* const* w_gate_up, const void* const* w_down, int E, int d, int f,
+                 void* h_ws, float* y_perm, void* stream) {
+    moe_expert_weights ex[MOE_MAX_EXPERTS];
+    if (E < 1 || E > MOE_MAX_EXPERTS) {
+        g_err = "bad E";
+        return MOE_ERR_USAGE;
+    }
+    for (int e = 0; e < E; ++e) ex[e] = {MOE_P16, 0, w_gate_up[e], nullptr, w_down[e], nullptr};
+    return moe_ffn(x, perm, offsets, T, k, ex, E, d, f, h_ws, y_perm, stream);
+}
+
+int moe_combine(const float* y_perm, const int32_t* inv_perm, const float* w, const void* residual,
+                int T, int d, int k, void* out, void* stream) {
+    return guarded([&] {
+        usage_if(T < 0 || d <= 0 || d % 4 != 0 || k < 1, "bad T / d / k");
+        need_device();
+        const cudaError_t e = moek_combine(y_perm, inv_perm, w, residual, T, d, k, out, st(stream));
+        if (e != cudaSuccess) throw std::runtime_error(std::string("moe_combine: ") + cudaGetErrorString(e));
+    });
+}
+
+int moe_quantize_g128(const void* w, int rows, int cols, uint32_t* q, void* s, void* stream) {
+    return guarded([&] {
+        usage_if(rows < 0 || cols <= 0 || cols % 128 != 0, "cols must be a positive multiple of 128");
+        need_device();
+        const cudaError_t e = moek_quantize(w, rows, cols, q, s, st(stream));
+        if (e != cudaSuccess) throw std::runtime_error(std::string("moe_quantize_g128: ") + cudaGetErrorString(e));
+    });
+}
+
+int moe_synth_weight_bf16(uint64_t seed, uint64_t uid, int64_t n, int shift, void* out, void* stream) {
+    return guarded([&] {
+        need_device();
+        const cudaError_t e = moek_synth_weight(seed, uid, n, shift, out, st(stream));
+        if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    });
+}
+
+int moe_synth_input_bf16(uint64_t seed, uint64_t uid, int64_t n, void* out, void* stream) {
+    return guarded([&] {
+        need_device();
+        const cudaError_t e = moek_synth_input(seed, uid, n, out, st(stream));
+        if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    });
+}
+
+int moe_weight_shift(int K) { return weight_shift(K); }
+
+int moe_stream_expert(void* dst_dev, const void* src_pinned, size_t bytes, void* copy_stream,
+                      void* done_event) {
+    return guarded([&] {
+        need_device();
+        cudaError_t e = cudaMemcpyAsync(dst_dev, src_pinned, bytes, cudaMemcpyHostToDevice, st(copy_stream));
+        if (e == cudaSuccess && done_event) e = cudaEventRecord(static_cast<cudaEvent_t>(done_event), st(copy_stream));
+        if (e != cudaSuccess) throw std::runtime_error(std::string("moe_stream_expert: ") + cudaGetErrorString(e));
+    });
+}
+
+// ---------------------------------------------------------------- engine
+int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan_entries,
+                      moe_engine** out) {
+    return guarded([&] {
+        usage_if(cfg == nullptr || plan_entries == nullptr || out == nullptr, "null argument");
+        MoeShape shape;
+        shape.d_model = cfg->d_model;
+        shape.d_ffn = cfg->d_ffn;
+        EngineConfig ec;
+        ec.shape = shape;
+        ec.profile = profile_for_shape(shape, cfg->num_layers, cfg->experts_per_layer, cfg->top_k, 1);
+        ec.max_tokens = cfg->max_tokens;
+        ec.seed = cfg->seed;
+        ec.device = cfg->device;
+        ec.use_graphs = cfg->use_graphs != 0;
+        const int n = cfg->num_layers * cfg->experts_per_layer;
+        PlacementPlan plan = to_plan(plan_entries, n, 0);
+        plan.swap_slot_bytes = required_swap_bytes(plan, ec.profile);
+        *out = new moe_engine{new MoeEngine(ec, plan)};
+    });
+}
+
+void moe_engine_destroy(moe_engine* eng) {
+    if (!eng) return;
+    delete eng->impl;
+    delete eng;
+}
+
+int moe_engine_memory(const moe_engine* eng, int64_t* expert_bytes, int64_t* swap_bytes,
+                      int64_t* host_pinned_bytes, int64_t* workspace_bytes) {
+    return guarded([&] { eng->impl->memory(expert_bytes, swap_bytes, host_pinned_bytes, workspace_bytes); });
+}
+
+void* moe_engine_input(moe_engine* eng) { return eng ? eng->impl->input() : nullptr; }
+void* moe_engine_output(moe_engine* eng) { return eng ? eng->impl->output() : nullptr; }
+void* moe_engine_stream(moe_engine* eng) { return eng ? eng->impl->stream() : nullptr; }
+
+int moe_engine_synth_input(moe_engine* eng, int step, int T) {
+    return guarded([&] { eng->impl->synth_input(step, T); });
+}
+
+int moe_engine_decode(moe_engine* eng, int T) {
+    return guarded([&] { eng->impl->decode(T); });
+}
+
+int moe_engine_decode_host(moe_engine* eng, const void* x_host, int T, void* out_host) {
+    return guarded([&] { eng->impl->decode_host(x_host, T, out_host); });
+}
+
+int moe_engine_forward_layer(moe_engine* eng, int layer, const void* x, int T, void* out,
+                             int32_t* idx_dev, float* w_dev, float* logits_dev) {
+    return guarded([&] { eng->impl->forward_layer(layer, x, T, out, idx_dev, w_dev, logits_dev); });
+}
+
+int moe_engine_sync(moe_engine* eng) {
+    return guarded([&] { eng->impl->sync(); });
+}
+
+int moe_engine_profile_step(moe_engine* eng, int T, float* ffn_ms, int64_t* ffn_bytes,
+                            int32_t* kernels_per_step) {
+    return guarded([&] {
+        int k = 0;
+        eng->impl->profile_step(T, ffn_ms, ffn_bytes, &k);
+        if (kernels_per_step) *kernels_per_step = k;
+    });
+}
+
+int moe_engine_last_routing(moe_engine* eng, int T, int32_t* slots_out) {
+    return guarded([&] {
+        const GatingTrace tr = eng->impl->last_routing(T);
+        std::memcpy(slots_out, tr.slots.data(), tr.slots.size() * 4);
+    });
+}
+
+int moe_engine_counters(const moe_engine* eng, moe_sim_report* out) {
+    return guarded([&] {
+        const SimReport& r = eng->impl->counters();
+        out->tokens = r.tokens;
+        out->activations = r.activations;
+        out->hits = r.hits;
+        out->bytes_transferred = r.bytes_transferred;
+        out->transfer_ns = r.transfer_ns;
+        out->compute_ns = r.compute_ns;
+        out->nonexpert_ns = r.nonexpert_ns;
+    });
+}
+
+int moe_engine_reset_counters(moe_engine* eng) {
+    return guarded([&] { eng->impl->reset_counters(); });
+}
+
+int moe_engine_expert(const moe_engine* eng, int layer, int slot, moe_expert_weights* out,
+                      int32_t* location) {
+    return guarded([&] {
+        int loc = 0;
+        *out = eng->impl->expert(layer, slot, &loc);
+        if (location) *location = loc;
+    });
+}
+
+int moe_engine_router(const moe_engine* eng, int layer, const void** wg_dev) {
+    return guarded([&] { *wg_dev = eng->impl->router(layer); });
+}
+
+}  // extern "C"

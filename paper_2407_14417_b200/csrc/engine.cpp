@@ -1,0 +1,492 @@
+// engine.cu -- MoeEngine (see include/moeb200/engine.hpp).
+//
+// HBM layout: one device arena holds every GPU-resident expert back to back
+// (256-byte aligned), one pinned host arena holds the CPU-resident experts,
+// one swap slot of plan.swap_slot_bytes receives streamed experts.  Per
+// expert (d = d_model, f = d_ffn):
+//   bf16 : [w_gate_up 2f*d bf16][w_down d*f bf16]                  = 6df B
+//   int4 : [q_gate_up 2f*d/8 u32][s_gate_up 2f*d/128 bf16]
+//          [q_down d*f/8 u32][s_down d*f/128 bf16]                 = 99df/64 B
+// which are exactly expert_size(P16) / expert_size(P4) of the profile made by
+// profile_for_shape(), so bytes_transferred is the bytes really copied.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <stdexcept>
+#include <string>
+
+#include "kernels/launch.h"
+#include "moeb200/engine.hpp"
+
+namespace moeb200 {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+uint64_t uid_expert(int e, int tensor) { return (static_cast<uint64_t>(e) << 4) | static_cast<uint64_t>(tensor); }
+uint64_t uid_router(int layer) { return (1ULL << 48) | static_cast<uint64_t>(layer); }
+uint64_t uid_input(int step) { return (2ULL << 48) | static_cast<uint64_t>(step); }
+
+}  // namespace
+
+int weight_shift(int K) {
+    return static_cast<int>(std::lround(std::log2(73.9 * std::sqrt(static_cast<double>(K)))));
+}
+
+struct MoeEngine::Impl {
+    EngineConfig cfg;
+    PlacementPlan plan;
+    int L = 0, E = 0, K = 0, d = 0, f = 0, Tmax = 0;
+    size_t size16 = 0, size4 = 0;
+
+    cudaStream_t compute = nullptr, copy = nullptr;
+    cudaEvent_t copy_done = nullptr, slot_free = nullptr;
+
+    char* dev_arena = nullptr;
+    size_t dev_bytes = 0;
+    char* host_arena = nullptr;
+    size_t host_bytes = 0;
+    char* swap = nullptr;
+    size_t swap_bytes = 0;
+    uint16_t* wg = nullptr;  // [L][E][d]
+
+    std::vector<moe_expert_weights> weights;  // [L*E]
+    std::vector<int> location;                // [L*E]
+    std::vector<char> layer_has_cpu;
+
+    uint16_t* xin = nullptr;
+    uint16_t* xout = nullptr;
+    uint16_t* xbuf[2] = {nullptr, nullptr};
+    int32_t* idx = nullptr;   // [L][Tmax*K]
+    float* wts = nullptr;     // [L][Tmax*K]
+    int32_t* counts = nullptr;
+    int32_t* offsets = nullptr;
+    int32_t* perm = nullptr;
+    int32_t* inv = nullptr;
+    unsigned int* ticket = nullptr;
+    uint16_t* h = nullptr;
+    float* y = nullptr;
+    int32_t* idx_host = nullptr;  // pinned [Tmax*K]
+    size_t ws_bytes = 0;
+
+    SimReport counters;
+    std::map<int, cudaGraphExec_t> graphs;
+
+    moe_expert_weights view(char* base, Precision p) const {
+        moe_expert_weights w{};
+        const size_t fd = static_cast<size_t>(f) * d;
+        if (p == Precision::P16) {
+            w.precision = MOE_P16;
+            w.w_gate_up = base;
+            w.w_down = base + 4 * fd;
+        } else {
+            w.precision = MOE_P4;
+            w.w_gate_up = base;
+            w.s_gate_up = base + fd;
+            w.w_down = base + fd + fd / 32;
+            w.s_down = base + fd + fd / 32 + fd / 2;
+        }
+        return w;
+    }
+
+    void dev_alloc(void** p, size_t bytes) {
+        ck(cudaMalloc(p, bytes), "cudaMalloc");
+        ws_bytes += bytes;
+    }
+
+    void init(const EngineConfig& c, const PlacementPlan& pl) {
+        cfg = c;
+        plan = pl;
+        L = c.profile.num_layers;
+        E = c.profile.experts_per_layer;
+        K = c.profile.top_k;
+        d = c.shape.d_model;
+        f = c.shape.d_ffn;
+        Tmax = c.max_tokens;
+        validate_profile(c.profile);
+        validate_shape(c.shape);
+        if (E > MOE_MAX_EXPERTS) throw ValidationError("experts_per_layer exceeds MOE_MAX_EXPERTS");
+        if (K > MOE_MAX_TOPK) throw ValidationError("top_k exceeds MOE_MAX_TOPK");
+        if (Tmax < 1) throw ValidationError("max_tokens must be >= 1");
+        if (static_cast<int>(plan.entries.size()) != L * E)
+            throw ValidationError("plan covers " + std::to_string(plan.entries.size()) +
+                                  " experts, engine has " + std::to_string(L * E));
+        size16 = static_cast<size_t>(expert_bytes_bf16(c.shape));
+        size4 = static_cast<size_t>(expert_bytes_int4(c.shape));
+        if (static_cast<size_t>(expert_size(c.profile, Precision::P16)) != size16 ||
+            static_cast<size_t>(expert_size(c.profile, Precision::P4)) != size4)
+            throw ValidationError("profile expert sizes do not match the tensor shape "
+                                  "(build the profile with profile_for_shape)");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw std::runtime_error("no CUDA device: the MoE engine has no CPU fallback");
+        ck(cudaSetDevice(c.device), "cudaSetDevice");
+        ck(cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking), "stream");
+        ck(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreateWithFlags(&copy_done, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&slot_free, cudaEventDisableTiming), "event");
+
+        // arenas
+        std::vector<size_t> off(static_cast<size_t>(L * E));
+        layer_has_cpu.assign(static_cast<size_t>(L), 0);
+        location.assign(static_cast<size_t>(L * E), MOE_GPU);
+        size_t swap_need = 0;
+        for (int i = 0; i < L * E; ++i) {
+            const ExpertState st = plan.entries[static_cast<size_t>(i)];
+            const size_t sz = st.precision == Precision::P16 ? size16 : size4;
+            if (st.location == Location::GPU) {
+                off[static_cast<size_t>(i)] = dev_bytes;
+                dev_bytes += align_up(sz, 256);
+            } else {
+                off[static_cast<size_t>(i)] = host_bytes;
+                host_bytes += align_up(sz, 256);
+                layer_has_cpu[static_cast<size_t>(i / E)] = 1;
+                location[static_cast<size_t>(i)] = MOE_CPU;
+                swap_need = std::max(swap_need, sz);
+            }
+        }
+        if (static_cast<size_t>(plan.swap_slot_bytes) < swap_need)
+            throw ValidationError("plan swap_slot_bytes smaller than the largest CPU-resident expert");
+        if (dev_bytes) ck(cudaMalloc(&dev_arena, dev_bytes), "cudaMalloc(expert arena)");
+        if (host_bytes) ck(cudaHostAlloc(&host_arena, host_bytes, cudaHostAllocDefault), "cudaHostAlloc(host arena)");
+        swap_bytes = static_cast<size_t>(plan.swap_slot_bytes);
+        if (swap_bytes) ck(cudaMalloc(&swap, swap_bytes), "cudaMalloc(swap slot)");
+        weights.resize(static_cast<size_t>(L * E));
+        for (int i = 0; i < L * E; ++i) {
+            const ExpertState st = plan.entries[static_cast<size_t>(i)];
+            char* base = (st.location == Location::GPU ? dev_arena : host_arena) + off[static_cast<size_t>(i)];
+            weights[static_cast<size_t>(i)] = view(base, st.precision);
+        }
+
+        // workspaces
+        const size_t TK = static_cast<size_t>(Tmax) * K;
+        dev_alloc(reinterpret_cast<void**>(&wg), static_cast<size_t>(L) * E * d * 2);
+        dev_alloc(reinterpret_cast<void**>(&xin), static_cast<size_t>(Tmax) * d * 2);
+        dev_alloc(reinterpret_cast<void**>(&xout), static_cast<size_t>(Tmax) * d * 2);
+        dev_alloc(reinterpret_cast<void**>(&xbuf[0]), static_cast<size_t>(Tmax) * d * 2);
+        dev_alloc(reinterpret_cast<void**>(&xbuf[1]), static_cast<size_t>(Tmax) * d * 2);
+        dev_alloc(reinterpret_cast<void**>(&idx), static_cast<size_t>(L) * TK * 4);
+        dev_alloc(reinterpret_cast<void**>(&wts), static_cast<size_t>(L) * TK * 4);
+        dev_alloc(reinterpret_cast<void**>(&counts), static_cast<size_t>(E) * 4);
+        dev_alloc(reinterpret_cast<void**>(&offsets), static_cast<size_t>(E + 1) * 4);
+        dev_alloc(reinterpret_cast<void**>(&perm), TK * 4);
+        dev_alloc(reinterpret_cast<void**>(&inv), TK * 4);
+        dev_alloc(reinterpret_cast<void**>(&ticket), 4);
+        dev_alloc(reinterpret_cast<void**>(&h), TK * f * 2);
+        dev_alloc(reinterpret_cast<void**>(&y), TK * d * 4);
+        ck(cudaMemsetAsync(ticket, 0, 4, compute), "memset");
+        ck(cudaMemsetAsync(xin, 0, static_cast<size_t>(Tmax) * d * 2, compute), "memset");
+        ck(cudaHostAlloc(reinterpret_cast<void**>(&idx_host), TK * 4, cudaHostAllocDefault), "cudaHostAlloc");
+
+        materialize();
+    }
+
+    // Synthetic weights: bf16 masters from the counter-based generator,
+    // quantised to int4-g128 on device for P4 experts (the same definitions
+    // as oracle/moe_oracle.cpp), CPU-resident experts copied to the arena.
+    void materialize() {
+        const size_t fd = static_cast<size_t>(f) * d;
+        const int sh_gu = weight_shift(d), sh_d = weight_shift(f);
+        for (int l = 0; l < L; ++l)
+            ck(moek_synth_weight(cfg.seed, uid_router(l), static_cast<long long>(E) * d, sh_gu,
+                                 wg + static_cast<size_t>(l) * E * d, compute), "synth router");
+        char* tmp16 = nullptr;
+        char* tmp4 = nullptr;
+        bool need16 = false, need4 = false;
+        for (const ExpertState& st : plan.entries) {
+            if (st.precision == Precision::P4 || st.location == Location::CPU) need16 = true;
+            if (st.precision == Precision::P4 && st.location == Location::CPU) need4 = true;
+        }
+        if (need16) ck(cudaMalloc(&tmp16, size16), "cudaMalloc(tmp)");
+        if (need4) ck(cudaMalloc(&tmp4, size4), "cudaMalloc(tmp)");
+        for (int e = 0; e < L * E; ++e) {
+            const ExpertState st = plan.entries[static_cast<size_t>(e)];
+            const bool direct = st.precision == Precision::P16 && st.location == Location::GPU;
+            char* master = direct ? static_cast<char*>(const_cast<void*>(weights[static_cast<size_t>(e)].w_gate_up)) : tmp16;
+            ck(moek_synth_weight(cfg.seed, uid_expert(e, 1), static_cast<long long>(2 * fd), sh_gu, master, compute), "synth");
+            ck(moek_synth_weight(cfg.seed, uid_expert(e, 2), static_cast<long long>(fd), sh_d, master + 4 * fd, compute), "synth");
+            if (direct) continue;
+            char* dst = st.location == Location::GPU ? static_cast<char*>(const_cast<void*>(weights[static_cast<size_t>(e)].w_gate_up))
+                                                     : (st.precision == Precision::P4 ? tmp4 : tmp16);
+            if (st.precision == Precision::P4) {
+                moe_expert_weights v = view(dst, Precision::P4);
+                ck(moek_quantize(master, 2 * f, d, static_cast<uint32_t*>(const_cast<void*>(v.w_gate_up)),
+                                 const_cast<void*>(v.s_gate_up), compute), "quantize");
+                ck(moek_quantize(master + 4 * fd, d, f, static_cast<uint32_t*>(const_cast<void*>(v.w_down)),
+                                 const_cast<void*>(v.s_down), compute), "quantize");
+            }
+            if (st.location == Location::CPU) {
+                const size_t sz = st.precision == Precision::P16 ? size16 : size4;
+                ck(cudaMemcpyAsync(const_cast<void*>(weights[static_cast<size_t>(e)].w_gate_up), dst, sz,
+                                   cudaMemcpyDeviceToHost, compute), "D2H");
+                ck(cudaStreamSynchronize(compute), "sync");  // tmp reused next iteration
+            }
+        }
+        ck(cudaStreamSynchronize(compute), "sync");
+        if (tmp16) cudaFree(tmp16);
+        if (tmp4) cudaFree(tmp4);
+    }
+
+    void destroy() {
+        for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+        graphs.clear();
+        if (compute) cudaStreamSynchronize(compute);
+        if (copy) cudaStreamSynchronize(copy);
+        void* devp[] = {dev_arena, swap, wg, xin, xout, xbuf[0], xbuf[1], idx, wts, counts, offsets, perm, inv, ticket, h, y};
+        for (void* p : devp)
+            if (p) cudaFree(p);
+        if (host_arena) cudaFreeHost(host_arena);
+        if (idx_host) cudaFreeHost(idx_host);
+        if (copy_done) cudaEventDestroy(copy_done);
+        if (slot_free) cudaEventDestroy(slot_free);
+        if (compute) cudaStreamDestroy(compute);
+        if (copy) cudaStreamDestroy(copy);
+    }
+
+    uint64_t mask_all() const { return E >= 64 ? ~0ull : ((1ull << E) - 1ull); }
+
+    // One MoE layer: route -> FFN (streaming CPU-resident experts through the
+    // swap slot, Static policy) -> combine with residual.
+    void layer(int l, const uint16_t* x, int T, uint16_t* out, int32_t* idx_l, float* w_l, float* logits) {
+        const moe_expert_weights* lw = weights.data() + static_cast<size_t>(l) * E;
+        ck(moek_route(x, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx_l, w_l, logits, counts,
+                      offsets, perm, inv, ticket, compute), "route");
+        counters.activations += static_cast<int64_t>(T) * K;
+        if (!layer_has_cpu[static_cast<size_t>(l)]) {
+            counters.hits += static_cast<int64_t>(T) * K;
+            ck(moek_ffn_gemv(x, perm, offsets, T, K, lw, E, d, f, h, y, mask_all(), compute), "ffn");
+        } else {
+            ck(cudaMemcpyAsync(idx_host, idx_l, static_cast<size_t>(T) * K * 4, cudaMemcpyDeviceToHost, compute), "D2H idx");
+            ck(cudaStreamSynchronize(compute), "sync");
+            uint64_t sel = 0;
+            for (int i = 0; i < T * K; ++i) {
+                const int s = idx_host[i];
+                sel |= 1ull << s;
+                const ExpertState st = plan.entries[static_cast<size_t>(l * E + s)];
+                if (st.location == Location::GPU) {
+                    ++counters.hits;
+                } else {
+                    counters.bytes_transferred += static_cast<int64_t>(st.precision == Precision::P16 ? size16 : size4);
+                }
+            }
+            uint64_t resident = 0;
+            for (int s = 0; s < E; ++s)
+                if (((sel >> s) & 1ull) && location[static_cast<size_t>(l * E + s)] == MOE_GPU) resident |= 1ull << s;
+            if (resident)
+                ck(moek_ffn_gemv(x, perm, offsets, T, K, lw, E, d, f, h, y, resident, compute), "ffn");
+            std::vector<moe_expert_weights> tmp(lw, lw + E);
+            for (int s = 0; s < E; ++s) {
+                if (!((sel >> s) & 1ull) || location[static_cast<size_t>(l * E + s)] == MOE_GPU) continue;
+                const moe_expert_weights& hw = lw[s];
+                const size_t sz = hw.precision == MOE_P16 ? size16 : size4;
+                // Static swap semantics: the slot is reused by the next miss
+                // only after the previous expert's FFN has consumed it.
+                ck(cudaStreamWaitEvent(copy, slot_free, 0), "wait");
+                ck(cudaMemcpyAsync(swap, hw.w_gate_up, sz, cudaMemcpyHostToDevice, copy), "H2D expert");
+                ck(cudaEventRecord(copy_done, copy), "record");
+                ck(cudaStreamWaitEvent(compute, copy_done, 0), "wait");
+                tmp[static_cast<size_t>(s)] = view(swap, hw.precision == MOE_P16 ? Precision::P16 : Precision::P4);
+                ck(moek_ffn_gemv(x, perm, offsets, T, K, tmp.data(), E, d, f, h, y, 1ull << s, compute), "ffn");
+                ck(cudaEventRecord(slot_free, compute), "record");
+            }
+        }
+        ck(moek_combine(y, inv, w_l, x, T, d, K, out, compute), "combine");
+    }
+
+    void run_layers(int T) {
+        const uint16_t* src = xin;
+        const size_t TK = static_cast<size_t>(Tmax) * K;
+        for (int l = 0; l < L; ++l) {
+            uint16_t* dst = l == L - 1 ? xout : xbuf[l & 1];
+            layer(l, src, T, dst, idx + l * TK, wts + l * TK, nullptr);
+            src = dst;
+        }
+    }
+
+    // Eager decode step with CUDA events (on the compute stream, where the
+    // kernels are launched) bracketing each layer's expert-FFN launches.
+    // Returns per-layer FFN milliseconds and the algorithmic bytes that FFN
+    // must move: weights + scales of the distinct selected experts, the x
+    // rows read, h written and read back, y written.
+    void profile_step(int T, float* ffn_ms, int64_t* ffn_bytes, int* kernels_per_step) {
+        if (T < 1 || T > Tmax) throw ValidationError("T must be in [1, max_tokens]");
+        for (char c : layer_has_cpu)
+            if (c) throw UsageError("profile_step needs an all-device-resident plan");
+        std::vector<cudaEvent_t> ev(static_cast<size_t>(2 * L));
+        for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+        const SimReport saved = counters;
+        const uint16_t* src = xin;
+        const size_t TK = static_cast<size_t>(Tmax) * K;
+        for (int l = 0; l < L; ++l) {
+            uint16_t* dst = l == L - 1 ? xout : xbuf[l & 1];
+            const moe_expert_weights* lw = weights.data() + static_cast<size_t>(l) * E;
+            ck(moek_route(src, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx + l * TK, wts + l * TK,
+                          nullptr, counts, offsets, perm, inv, ticket, compute), "route");
+            ck(cudaEventRecord(ev[static_cast<size_t>(2 * l)], compute), "record");
+            ck(moek_ffn_gemv(src, perm, offsets, T, K, lw, E, d, f, h, y, mask_all(), compute), "ffn");
+            ck(cudaEventRecord(ev[static_cast<size_t>(2 * l + 1)], compute), "record");
+            ck(moek_combine(y, inv, wts + l * TK, src, T, d, K, dst, compute), "combine");
+            src = dst;
+        }
+        ck(cudaStreamSynchronize(compute), "sync");
+        counters = saved;
+        std::vector<int32_t> all(static_cast<size_t>(L) * TK);
+        ck(cudaMemcpy(all.data(), idx, all.size() * 4, cudaMemcpyDeviceToHost), "D2H routing");
+        for (int l = 0; l < L; ++l) {
+            float ms = 0.0f;
+            ck(cudaEventElapsedTime(&ms, ev[static_cast<size_t>(2 * l)], ev[static_cast<size_t>(2 * l + 1)]), "elapsed");
+            ffn_ms[l] = ms;
+            uint64_t sel = 0;
+            for (int i = 0; i < T * K; ++i) sel |= 1ull << all[static_cast<size_t>(l) * TK + static_cast<size_t>(i)];
+            int64_t bytes = 0;
+            for (int s = 0; s < E; ++s)
+                if ((sel >> s) & 1ull)
+                    bytes += static_cast<int64_t>(plan.entries[static_cast<size_t>(l * E + s)].precision == Precision::P16 ? size16 : size4);
+            bytes += static_cast<int64_t>(T) * K * d * 2      // x rows gathered
+                     + static_cast<int64_t>(T) * K * f * 2 * 2  // h written + read
+                     + static_cast<int64_t>(T) * K * d * 4;     // y written
+            ffn_bytes[l] = bytes;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        if (kernels_per_step) *kernels_per_step = 4 * L;  // route, gate/up, down, combine
+    }
+
+    bool graphable() const {
+        if (!cfg.use_graphs) return false;
+        for (char c : layer_has_cpu)
+            if (c) return false;
+        return true;
+    }
+
+    void decode(int T) {
+        if (T < 1 || T > Tmax) throw ValidationError("T must be in [1, max_tokens]");
+        if (!graphable()) {
+            run_layers(T);
+            return;
+        }
+        auto it = graphs.find(T);
+        if (it == graphs.end()) {
+            // warm the launch-geometry caches outside capture
+            const SimReport saved = counters;
+            run_layers(T);
+            ck(cudaStreamSynchronize(compute), "sync");
+            counters = saved;
+            cudaGraph_t g = nullptr;
+            ck(cudaStreamBeginCapture(compute, cudaStreamCaptureModeThreadLocal), "capture");
+            run_layers(T);
+            ck(cudaStreamEndCapture(compute, &g), "capture end");
+            counters = saved;
+            cudaGraphExec_t ge = nullptr;
+            ck(cudaGraphInstantiate(&ge, g, 0), "instantiate");
+            cudaGraphDestroy(g);
+            it = graphs.emplace(T, ge).first;
+        }
+        ck(cudaGraphLaunch(it->second, compute), "graph launch");
+        counters.activations += static_cast<int64_t>(T) * K * L;
+        counters.hits += static_cast<int64_t>(T) * K * L;
+    }
+};
+
+MoeEngine::MoeEngine(const EngineConfig& cfg, const PlacementPlan& plan) : impl_(new Impl) {
+    try {
+        impl_->init(cfg, plan);
+    } catch (...) {
+        impl_->destroy();
+        throw;
+    }
+}
+
+MoeEngine::~MoeEngine() { impl_->destroy(); }
+
+void* MoeEngine::input() { return impl_->xin; }
+void* MoeEngine::output() { return impl_->xout; }
+void* MoeEngine::stream() { return impl_->compute; }
+
+void MoeEngine::synth_input(int step, int T) {
+    if (T < 1 || T > impl_->Tmax) throw ValidationError("T must be in [1, max_tokens]");
+    ck(moek_synth_input(impl_->cfg.seed, uid_input(step), static_cast<long long>(T) * impl_->d, impl_->xin,
+                        impl_->compute), "synth input");
+}
+
+void MoeEngine::decode(int T) {
+    impl_->decode(T);
+    impl_->counters.tokens += T;
+}
+
+void MoeEngine::decode_host(const void* x_host, int T, void* out_host) {
+    if (T < 1 || T > impl_->Tmax) throw ValidationError("T must be in [1, max_tokens]");
+    const size_t bytes = static_cast<size_t>(T) * impl_->d * 2;
+    ck(cudaMemcpyAsync(impl_->xin, x_host, bytes, cudaMemcpyHostToDevice, impl_->compute), "H2D x");
+    decode(T);
+    ck(cudaMemcpyAsync(out_host, impl_->xout, bytes, cudaMemcpyDeviceToHost, impl_->compute), "D2H out");
+    ck(cudaStreamSynchronize(impl_->compute), "sync");
+}
+
+void MoeEngine::forward_layer(int layer, const void* x, int T, void* out, int32_t* idx, float* w,
+                              float* logits) {
+    if (layer < 0 || layer >= impl_->L) throw ValidationError("layer out of range");
+    if (T < 1 || T > impl_->Tmax) throw ValidationError("T must be in [1, max_tokens]");
+    impl_->layer(layer, static_cast<const uint16_t*>(x), T, static_cast<uint16_t*>(out), idx, w, logits);
+}
+
+void MoeEngine::sync() { ck(cudaStreamSynchronize(impl_->compute), "sync"); }
+
+void MoeEngine::profile_step(int T, float* ffn_ms, int64_t* ffn_bytes, int* kernels_per_step) {
+    impl_->profile_step(T, ffn_ms, ffn_bytes, kernels_per_step);
+}
+
+GatingTrace MoeEngine::last_routing(int T) {
+    Impl& m = *impl_;
+    sync();
+    const size_t TK = static_cast<size_t>(m.Tmax) * m.K;
+    std::vector<int32_t> all(static_cast<size_t>(m.L) * TK);
+    ck(cudaMemcpy(all.data(), m.idx, all.size() * 4, cudaMemcpyDeviceToHost), "D2H routing");
+    GatingTrace tr;
+    tr.profile_fingerprint = profile_fingerprint(m.cfg.profile);
+    tr.tokens = T;
+    tr.num_layers = m.L;
+    tr.experts_per_layer = m.E;
+    tr.top_k = m.K;
+    tr.slots.resize(static_cast<size_t>(T) * m.L * m.K);
+    for (int t = 0; t < T; ++t)
+        for (int l = 0; l < m.L; ++l) {
+            int32_t* rec = tr.slots.data() + (static_cast<size_t>(t) * m.L + l) * m.K;
+            for (int j = 0; j < m.K; ++j) rec[j] = all[static_cast<size_t>(l) * TK + static_cast<size_t>(t) * m.K + j];
+            std::sort(rec, rec + m.K);
+        }
+    return tr;
+}
+
+const SimReport& MoeEngine::counters() const { return impl_->counters; }
+void MoeEngine::reset_counters() { impl_->counters = SimReport{}; }
+
+moe_expert_weights MoeEngine::expert(int layer, int slot, int* location) const {
+    const Impl& m = *impl_;
+    if (layer < 0 || layer >= m.L || slot < 0 || slot >= m.E) throw ValidationError("expert id out of range");
+    const size_t i = static_cast<size_t>(layer) * m.E + slot;
+    if (location) *location = m.location[i];
+    return m.weights[i];
+}
+
+const void* MoeEngine::router(int layer) const {
+    if (layer < 0 || layer >= impl_->L) throw ValidationError("layer out of range");
+    return impl_->wg + static_cast<size_t>(layer) * impl_->E * impl_->d;
+}
+
+void MoeEngine::memory(int64_t* expert_bytes, int64_t* swap_bytes, int64_t* host_bytes,
+                       int64_t* workspace_bytes) const {
+    if (expert_bytes) *expert_bytes = static_cast<int64_t>(impl_->dev_bytes);
+    if (swap_bytes) *swap_bytes = static_cast<int64_t>(impl_->swap_bytes);
+    if (host_bytes) *host_bytes = static_cast<int64_t>(impl_->host_bytes);
+    if (workspace_bytes) *workspace_bytes = static_cast<int64_t>(impl_->ws_bytes);
+}
+
+}  // namespace moeb200

@@ -1,0 +1,112 @@
+// common.cuh -- shared device helpers for the sm_100a MoE kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "moe_b200.h"
+
+#define MOE_DEVI __device__ __forceinline__
+
+namespace moek {
+
+constexpr int kWarp = 32;
+constexpr int kMaxExperts = MOE_MAX_EXPERTS;
+
+MOE_DEVI float bf2f(uint16_t b) { return __uint_as_float(static_cast<uint32_t>(b) << 16); }
+MOE_DEVI float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+MOE_DEVI float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+
+// round-to-nearest-even fp32 -> bf16 (same definition as the oracle's f2bf)
+MOE_DEVI uint16_t f2bf(float f) {
+    uint32_t u = __float_as_uint(f);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+
+// 128-bit streaming load for weights: read exactly once per step, so bypass
+// L1 allocation (the read-only, evict-first path).
+MOE_DEVI uint4 ld_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+MOE_DEVI uint16_t ld_nc_u16(const void* p) {
+    uint16_t r;
+    asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(r) : "l"(p));
+    return r;
+}
+
+// acc += bf16 * bf16 with fp32 accumulate: one FHFMA.BF16 on sm_100a (PTX
+// fma.rn.f32.bf16).  The product of two bf16 values is exact in fp32, so this
+// is an fp32 FMA with bf16 operands -- no unpacking instructions.
+MOE_DEVI float fma_lo(uint32_t w, uint32_t x, float acc) {
+    uint16_t a, ah, b, bh;
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(a), "=h"(ah) : "r"(w));
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(b), "=h"(bh) : "r"(x));
+    asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(acc) : "h"(a), "h"(b));
+    return acc;
+}
+MOE_DEVI float fma_hi(uint32_t w, uint32_t x, float acc) {
+    uint16_t a, al, b, bl;
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(al), "=h"(a) : "r"(w));
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(bl), "=h"(b) : "r"(x));
+    asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(acc) : "h"(a), "h"(b));
+    return acc;
+}
+
+// bf16x2 FMA, one rounding per half.
+MOE_DEVI uint32_t hfma2_bf16(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// (a & mask) | orv in one LOP3
+MOE_DEVI uint32_t and_or(uint32_t a, uint32_t mask, uint32_t orv) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(mask), "r"(orv));
+    return d;
+}
+
+// ---- int4-g128 word decode -------------------------------------------------
+// A packed word holds elements j = 0..7 of 8 consecutive K positions, element
+// j at bit 4*(j/2) + 16*(j%2), biased u = q + 8.  OR-ing a nibble into the
+// mantissa of bf16 128.0 (0x4300) gives 128 + u (low mantissa bits) or
+// 128 + 16u (bits 4-7); one bf16x2 FMA then yields q exactly:
+//   (128 + u) * 1      - 136 = q        (elements 0,1 / 4,5)
+//   (128 + 16u) * 1/16 - 16  = q        (elements 2,3 / 6,7)
+// Result: four bf16x2 pairs (q0,q1) (q2,q3) (q4,q5) (q6,q7), all exact.
+constexpr uint32_t kBf16One2 = 0x3F803F80u;   // (1.0, 1.0)
+constexpr uint32_t kBf16M136x2 = 0xC308C308u; // (-136, -136)
+constexpr uint32_t kBf16Sixteenth2 = 0x3D803D80u;  // (1/16, 1/16)
+constexpr uint32_t kBf16M16x2 = 0xC180C180u;  // (-16, -16)
+
+MOE_DEVI void decode_q8(uint32_t w, uint32_t& p01, uint32_t& p23, uint32_t& p45, uint32_t& p67) {
+    const uint32_t w8 = w >> 8;
+    p01 = hfma2_bf16(and_or(w, 0x000F000Fu, 0x43004300u), kBf16One2, kBf16M136x2);
+    p23 = hfma2_bf16(and_or(w, 0x00F000F0u, 0x43004300u), kBf16Sixteenth2, kBf16M16x2);
+    p45 = hfma2_bf16(and_or(w8, 0x000F000Fu, 0x43004300u), kBf16One2, kBf16M136x2);
+    p67 = hfma2_bf16(and_or(w8, 0x00F000F0u, 0x43004300u), kBf16Sixteenth2, kBf16M16x2);
+}
+
+MOE_DEVI float warp_sum(float v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+MOE_DEVI float silu_f(float g) { return g / (1.0f + expf(-g)); }
+
+#define MOE_CUDA_OK(expr)                                   \
+    do {                                                    \
+        cudaError_t err__ = (expr);                         \
+        if (err__ != cudaSuccess) return err__;             \
+    } while (0)
+
+}  // namespace moek

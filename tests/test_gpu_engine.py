@@ -1,0 +1,188 @@
+"""MoeEngine parity: the B200 MoE-layer forward vs the CPU oracle, and its
+SimReport counters vs the reference simulate() on the exported routing.
+
+Config C1 of BASELINE.json (tiny: 2 layers, 8 experts top-2, d=512,
+ffn=1792, 4 of 8 experts per layer int4 via assign_quantization(8, seed=1),
+32-token decode) and C2 (one Mixtral-shaped layer, all-bf16 vs all-int4).
+"""
+import numpy as np
+import pytest
+
+from helpers import MIXTRAL, RTOL_BF16, TINY, assert_close, bf16_to_f32, read_device, to_dev, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_mod(cuda):
+    import torch
+    return torch
+
+
+def quality_plan(moe, cfg, n4, seed, budget=10**15):
+    prof = moe.profile_for_shape(cfg["d_model"], cfg["d_ffn"], cfg["num_layers"], cfg["experts_per_layer"],
+                                 cfg["top_k"])
+    return prof, moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, seed), moe.HardwareProfile(budget), prof)
+
+
+def make_engine(moe, cfg, plan, seed, T=1, graphs=True):
+    return moe.MoeEngine(cfg["num_layers"], cfg["experts_per_layer"], cfg["top_k"], cfg["d_model"], cfg["d_ffn"],
+                         plan, max_tokens=T, seed=seed, use_graphs=graphs)
+
+
+def layer_precisions(plan, layer, E):
+    return plan.precision[layer * E:(layer + 1) * E]
+
+
+def test_tiny_plan_is_4_of_8_per_layer(moe):
+    _, plan = quality_plan(moe, TINY, 8, 1)
+    assert [sum(1 for p in plan.precision[l * 8:(l + 1) * 8] if p == 0) for l in range(2)] == [4, 4]
+    assert plan.n_gpu == 16
+
+
+@pytest.mark.parametrize("T", [1, 3, 4, 8])
+def test_tiny_layer_parity(moe, orc, torch_mod, cuda, T):
+    torch = torch_mod
+    seed = 42
+    _, plan = quality_plan(moe, TINY, 8, 1)
+    eng = make_engine(moe, TINY, plan, seed, T)
+    m = orc.model(2, 8, 2, 512, 1792, seed)
+    x = orc.step_input(m, 0, T)
+    for layer in range(2):
+        prec = layer_precisions(plan, layer, 8)
+        out_ref, idx_ref, w_ref, lg_ref = orc.moe_layer(m, layer, prec, x, T)
+        xd = to_dev(x, torch, cuda)
+        out = torch.empty(T * 512, dtype=torch.int16, device=cuda)
+        idx = torch.empty(T * 2, dtype=torch.int32, device=cuda)
+        w = torch.empty(T * 2, dtype=torch.float32, device=cuda)
+        lg = torch.empty(T * 8, dtype=torch.float32, device=cuda)
+        eng.forward_layer(layer, xd, T, out, idx, w, lg)
+        eng.sync()
+        assert np.array_equal(to_np(lg, np.float32).view(np.uint32).reshape(T, 8), lg_ref.view(np.uint32))
+        assert np.array_equal(to_np(idx, np.int32).reshape(T, 2), idx_ref)
+        got = to_np(out, np.uint16).reshape(T, 512)
+        assert_close(bf16_to_f32(got), bf16_to_f32(out_ref), RTOL_BF16, f"layer {layer}")
+        x = got  # feed the GPU's output to the next layer (per-layer parity on identical inputs)
+    eng.close()
+
+
+def test_tiny_decode_32_steps(moe, orc, torch_mod, cuda):
+    """C1: 32-token decode through the stack (CUDA graph), vs the oracle
+    stack run free on the same step inputs."""
+    torch = torch_mod
+    seed = 42
+    prof, plan = quality_plan(moe, TINY, 8, 1)
+    eng = make_engine(moe, TINY, plan, seed, 1, graphs=True)
+    m = orc.model(2, 8, 2, 512, 1792, seed)
+    flips = 0
+    for step in range(32):
+        eng.synth_input(step, 1)
+        eng.decode(1)
+        got = read_device(torch, eng.output_ptr, 512 * 2).view(np.uint16)
+        x = orc.step_input(m, step, 1)
+        routing = []
+        for layer in range(2):
+            x, idx_ref, _, _ = orc.moe_layer(m, layer, layer_precisions(plan, layer, 8), x, 1)
+            routing.extend(sorted(idx_ref[0].tolist()))
+        assert_close(bf16_to_f32(got), bf16_to_f32(x), RTOL_BF16, f"step {step}")
+        flips += routing != eng.last_routing(1)
+    assert flips == 0
+    c = eng.counters()
+    assert c.tokens == 32 and c.activations == 32 * 2 * 2 and c.hits == c.activations
+    eng.close()
+
+
+def test_graph_equals_eager(moe, orc, torch_mod, cuda):
+    torch = torch_mod
+    _, plan = quality_plan(moe, TINY, 8, 1)
+    outs = []
+    for graphs in (True, False):
+        eng = make_engine(moe, TINY, plan, 7, 4, graphs=graphs)
+        eng.synth_input(3, 4)
+        eng.decode(4)
+        eng.sync()
+        outs.append(read_device(torch, eng.output_ptr, 4 * 512 * 2))
+        eng.close()
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_decode_host_equals_device(moe, torch_mod, cuda):
+    torch = torch_mod
+    _, plan = quality_plan(moe, TINY, 8, 1)
+    eng = make_engine(moe, TINY, plan, 9, 2)
+    eng.synth_input(5, 2)
+    eng.decode(2)
+    eng.sync()
+    dev_out = read_device(torch, eng.output_ptr, 2 * 512 * 2)
+    x = read_device(torch, eng.input_ptr, 2 * 512 * 2)
+    out = np.empty_like(x)
+    eng.decode_host(x.ctypes.data, 2, out.ctypes.data)
+    assert np.array_equal(out, dev_out)
+    eng.close()
+
+
+@pytest.mark.parametrize("budget_frac", [0.5, 0.25, 0.0])
+def test_host_streaming_counters_match_simulate(moe, ref, torch_mod, cuda, budget_frac):
+    """C4 semantics on the tiny shape: host-resident experts streamed into the
+    swap slot (Static).  Counters == reference simulate() on the exported
+    routing; outputs identical to the all-resident engine."""
+    torch = torch_mod
+    prof = moe.profile_for_shape(512, 1792, 2)
+    n4 = 8
+    full = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 1), moe.HardwareProfile(10**15), prof)
+    foot = moe.gpu_footprint(full, prof)
+    s16 = moe.expert_size(prof, 1)
+    budget = int(prof.size_nonexpert_bytes + s16 + budget_frac * (foot - prof.size_nonexpert_bytes))
+    hw = moe.HardwareProfile(budget)
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 1), hw, prof)
+    assert plan.n_gpu < 16
+    st, rprec, rloc, rswap = ref.make_plan(prof, budget, hw.transfer_bw_bytes_per_s, 1, n4, 1)
+    assert st == 0 and list(rprec) == plan.precision and list(rloc) == plan.location and rswap == plan.swap_slot_bytes
+
+    eng = make_engine(moe, TINY, plan, 11, 1)
+    base = make_engine(moe, TINY, full, 11, 1)
+    trace = []
+    for step in range(12):
+        for e in (eng, base):
+            e.synth_input(step, 1)
+            e.decode(1)
+            e.sync()
+        a = read_device(torch, eng.output_ptr, 1024)
+        b = read_device(torch, base.output_ptr, 1024)
+        assert np.array_equal(a, b), "streamed experts must compute bit-identically"
+        trace.extend(eng.last_routing(1))
+    c = eng.counters()
+    st, sim = ref.simulate(prof, hw.transfer_bw_bytes_per_s, plan.precision, plan.location, plan.swap_slot_bytes,
+                           12, np.array(trace, np.int32))
+    assert st == 0
+    assert (c.activations, c.hits, c.bytes_transferred) == (sim[0], sim[1], sim[2])
+    mine = moe.simulate(plan, trace, 12, prof, hw)
+    assert (mine.activations, mine.hits, mine.bytes_transferred) == (sim[0], sim[1], sim[2])
+    eng.close()
+    base.close()
+
+
+@pytest.mark.parametrize("precision", [1, 0])
+@pytest.mark.parametrize("T", [1, 4])
+def test_mixtral_layer_parity(moe, orc, torch_mod, cuda, precision, T):
+    """C2: one Mixtral-shaped layer (d=4096, f=14336, 8 experts top-2), all-bf16
+    vs all-int4, on identical inputs."""
+    torch = torch_mod
+    cfg = dict(MIXTRAL, num_layers=1)
+    prof = moe.profile_for_shape(4096, 14336, 1)
+    plan = moe.assign_locations([precision] * 8, moe.HardwareProfile(10**15), prof)
+    eng = make_engine(moe, cfg, plan, 2024, T)
+    m = orc.model(1, 8, 2, 4096, 14336, 2024)
+    x = orc.step_input(m, 0, T)
+    out_ref, idx_ref, _, lg_ref = orc.moe_layer(m, 0, [precision] * 8, x, T)
+    out = torch.empty(T * 4096, dtype=torch.int16, device=cuda)
+    idx = torch.empty(T * 2, dtype=torch.int32, device=cuda)
+    w = torch.empty(T * 2, dtype=torch.float32, device=cuda)
+    lg = torch.empty(T * 8, dtype=torch.float32, device=cuda)
+    eng.forward_layer(0, to_dev(x, torch, cuda), T, out, idx, w, lg)
+    eng.sync()
+    assert np.array_equal(to_np(lg, np.float32).view(np.uint32).reshape(T, 8), lg_ref.view(np.uint32))
+    assert np.array_equal(to_np(idx, np.int32).reshape(T, 2), idx_ref)
+    assert_close(bf16_to_f32(to_np(out, np.uint16).reshape(T, 4096)), bf16_to_f32(out_ref), RTOL_BF16,
+                 f"mixtral layer {'bf16' if precision else 'int4'}")
+    eng.close()
