@@ -77,23 +77,21 @@ MOE_DEVI uint32_t and_or(uint32_t a, uint32_t mask, uint32_t orv) {
 // ---- int4-g128 word decode -------------------------------------------------
 // A packed word holds elements j = 0..7 of 8 consecutive K positions, element
 // j at bit 4*(j/2) + 16*(j%2), biased u = q + 8.  OR-ing a nibble into the
-// mantissa of bf16 128.0 (0x4300) gives 128 + u (low mantissa bits) or
-// 128 + 16u (bits 4-7); one bf16x2 FMA then yields q exactly:
-//   (128 + u) * 1      - 136 = q        (elements 0,1 / 4,5)
-//   (128 + 16u) * 1/16 - 16  = q        (elements 2,3 / 6,7)
-// Result: four bf16x2 pairs (q0,q1) (q2,q3) (q4,q5) (q6,q7), all exact.
-constexpr uint32_t kBf16One2 = 0x3F803F80u;   // (1.0, 1.0)
-constexpr uint32_t kBf16M136x2 = 0xC308C308u; // (-136, -136)
-constexpr uint32_t kBf16Sixteenth2 = 0x3D803D80u;  // (1/16, 1/16)
-constexpr uint32_t kBf16M16x2 = 0xC180C180u;  // (-16, -16)
-
-MOE_DEVI void decode_q8(uint32_t w, uint32_t& p01, uint32_t& p23, uint32_t& p45, uint32_t& p67) {
-    const uint32_t w8 = w >> 8;
-    p01 = hfma2_bf16(and_or(w, 0x000F000Fu, 0x43004300u), kBf16One2, kBf16M136x2);
-    p23 = hfma2_bf16(and_or(w, 0x00F000F0u, 0x43004300u), kBf16Sixteenth2, kBf16M16x2);
-    p45 = hfma2_bf16(and_or(w8, 0x000F000Fu, 0x43004300u), kBf16One2, kBf16M136x2);
-    p67 = hfma2_bf16(and_or(w8, 0x00F000F0u, 0x43004300u), kBf16Sixteenth2, kBf16M16x2);
+// low mantissa bits of bf16 128.0 (0x4300) gives the exact bf16 value 128 + u
+// (bf16 has 7 mantissa bits, so every pair is first shifted down to bits
+// 0-3 / 16-19).  Result: four bf16x2 pairs (128+u0, 128+u1) ... (128+u6,
+// 128+u7) for 3 SHF + 4 LOP3.  The kernels accumulate sum((128+u) x) with
+// FHFMA and remove the bias once per 32-element chunk:
+//   sum(q x) = sum((128+u) x) - 136 * sum(x)
+// with sum(x) precomputed per token and chunk, then apply the group scale:
+// y += s * sum(q x), i.e. the exact dequant value q*s.
+MOE_DEVI void decode_u8(uint32_t w, uint32_t& p01, uint32_t& p23, uint32_t& p45, uint32_t& p67) {
+    p01 = and_or(w, 0x000F000Fu, 0x43004300u);
+    p23 = and_or(w >> 4, 0x000F000Fu, 0x43004300u);
+    p45 = and_or(w >> 8, 0x000F000Fu, 0x43004300u);
+    p67 = and_or(w >> 12, 0x000F000Fu, 0x43004300u);
 }
+constexpr float kInt4Bias = 136.0f;  // 128 (magic) + 8 (storage bias)
 
 MOE_DEVI float warp_sum(float v) {
 #pragma unroll

@@ -66,7 +66,7 @@ MOE_DEVI int expert_of_segment(const int* seg, int E, int s) {
 // ---- one gate/up row pair --------------------------------------------------
 template <int MT>
 MOE_DEVI void rowpair_int4(const moe_expert_weights& W, int n, int d, int f, const uint16_t* xs,
-                           int lane, float (&ag)[MT], float (&au)[MT]) {
+                           const float* xsum, int lane, float (&ag)[MT], float (&au)[MT]) {
     const int wpr = d / 8;                     // uint32 words per row
     const uint4* qg = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(W.w_gate_up) + static_cast<size_t>(n) * wpr);
     const uint4* qu = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(W.w_gate_up) + static_cast<size_t>(n + f) * wpr);
@@ -100,8 +100,8 @@ MOE_DEVI void rowpair_int4(const moe_expert_weights& W, int n, int d, int f, con
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 uint32_t g0, g1, g2, g3, u0, u1, u2, u3;
-                decode_q8(gw[q], g0, g1, g2, g3);
-                decode_q8(uw[q], u0, u1, u2, u3);
+                decode_u8(gw[q], g0, g1, g2, g3);
+                decode_u8(uw[q], u0, u1, u2, u3);
 #pragma unroll
                 for (int m = 0; m < MT; ++m) {
                     const uint4 xv = *reinterpret_cast<const uint4*>(xs + static_cast<size_t>(m) * d + c * 32 + q * 8);
@@ -118,8 +118,9 @@ MOE_DEVI void rowpair_int4(const moe_expert_weights& W, int n, int d, int f, con
             const float sgf = bf2f(sgv[i]), suf = bf2f(suv[i]);
 #pragma unroll
             for (int m = 0; m < MT; ++m) {
-                ag[m] = __fmaf_rn(sgf, cg[m], ag[m]);
-                au[m] = __fmaf_rn(suf, cu[m], au[m]);
+                const float xc = xsum[m * nch + c];
+                ag[m] = __fmaf_rn(sgf, __fmaf_rn(-kInt4Bias, xc, cg[m]), ag[m]);
+                au[m] = __fmaf_rn(suf, __fmaf_rn(-kInt4Bias, xc, cu[m]), au[m]);
             }
         }
     }
@@ -168,8 +169,8 @@ MOE_DEVI void rowpair_bf16(const moe_expert_weights& W, int n, int d, int f, con
 
 // ---- one down-projection row ------------------------------------------------
 template <int MT>
-MOE_DEVI void row_down_int4(const moe_expert_weights& W, int j, int f, const uint16_t* hs, int lane,
-                            float (&acc)[MT]) {
+MOE_DEVI void row_down_int4(const moe_expert_weights& W, int j, int f, const uint16_t* hs,
+                            const float* hsum, int lane, float (&acc)[MT]) {
     const uint4* q = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(W.w_down) + static_cast<size_t>(j) * (f / 8));
     const uint16_t* s = static_cast<const uint16_t*>(W.s_down) + static_cast<size_t>(j) * (f / 128);
     const int nch = f / 32;
@@ -197,7 +198,7 @@ MOE_DEVI void row_down_int4(const moe_expert_weights& W, int j, int f, const uin
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
                 uint32_t p0, p1, p2, p3;
-                decode_q8(ww[qq], p0, p1, p2, p3);
+                decode_u8(ww[qq], p0, p1, p2, p3);
 #pragma unroll
                 for (int m = 0; m < MT; ++m) {
                     const uint4 hv = *reinterpret_cast<const uint4*>(hs + static_cast<size_t>(m) * f + c * 32 + qq * 8);
@@ -209,7 +210,8 @@ MOE_DEVI void row_down_int4(const moe_expert_weights& W, int j, int f, const uin
             }
             const float sf = bf2f(sv[i]);
 #pragma unroll
-            for (int m = 0; m < MT; ++m) acc[m] = __fmaf_rn(sf, cc[m], acc[m]);
+            for (int m = 0; m < MT; ++m)
+                acc[m] = __fmaf_rn(sf, __fmaf_rn(-kInt4Bias, hsum[m * nch + c], cc[m]), acc[m]);
         }
     }
 }
@@ -246,11 +248,31 @@ MOE_DEVI void row_down_bf16(const moe_expert_weights& W, int j, int f, const uin
     }
 }
 
+// Per-token, per-32-element chunk sums of a staged activation tile (the
+// int4 bias correction, see decode_u8).  Fixed summation order.
+MOE_DEVI void chunk_sums(const uint16_t* tile, float* sums, int rows, int K) {
+    const int nch = K / 32;
+    for (int i = threadIdx.x; i < rows * nch; i += blockDim.x) {
+        const uint4* p = reinterpret_cast<const uint4*>(tile + static_cast<size_t>(i) * 32);
+        float acc = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 v = p[q];
+            acc += bf16_lo(v.x) + bf16_hi(v.x);
+            acc += bf16_lo(v.y) + bf16_hi(v.y);
+            acc += bf16_lo(v.z) + bf16_hi(v.z);
+            acc += bf16_lo(v.w) + bf16_hi(v.w);
+        }
+        sums[i] = acc;
+    }
+}
+
 // ---- kernels ----------------------------------------------------------------
 template <int MT>
 __global__ void __launch_bounds__(kFfnThreads) ffn_gateup_kernel(const __grid_constant__ FfnArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
-    uint16_t* xs = reinterpret_cast<uint16_t*>(smem);  // [MT][d]
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem);                              // [MT][d]
+    float* xsum = reinterpret_cast<float*>(smem + static_cast<size_t>(MT) * a.d * 2);  // [MT][d/32]
     __shared__ int seg[MOE_MAX_EXPERTS + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nseg = build_segments<MT>(a, seg);
@@ -276,13 +298,17 @@ __global__ void __launch_bounds__(kFfnThreads) ffn_gateup_kernel(const __grid_co
         }
         __syncthreads();
         const moe_expert_weights& W = a.ex[e];
+        if (W.precision == MOE_P4) {
+            chunk_sums(xs, xsum, MT, a.d);
+            __syncthreads();
+        }
         const int n_base = static_cast<int>(r - static_cast<long long>(s) * a.f);
         const int cnt = static_cast<int>(piece_end - r);
         for (int i = warp; i < cnt; i += kFfnWarps) {
             const int n = n_base + i;
             float ag[MT], au[MT];
             if (W.precision == MOE_P4)
-                rowpair_int4<MT>(W, n, a.d, a.f, xs, lane, ag, au);
+                rowpair_int4<MT>(W, n, a.d, a.f, xs, xsum, lane, ag, au);
             else
                 rowpair_bf16<MT>(W, n, a.d, a.f, xs, lane, ag, au);
 #pragma unroll
@@ -300,7 +326,8 @@ __global__ void __launch_bounds__(kFfnThreads) ffn_gateup_kernel(const __grid_co
 template <int MT>
 __global__ void __launch_bounds__(kFfnThreads) ffn_down_kernel(const __grid_constant__ FfnArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
-    uint16_t* hs = reinterpret_cast<uint16_t*>(smem);  // [MT][f]
+    uint16_t* hs = reinterpret_cast<uint16_t*>(smem);                              // [MT][f]
+    float* hsum = reinterpret_cast<float*>(smem + static_cast<size_t>(MT) * a.f * 2);  // [MT][f/32]
     __shared__ int seg[MOE_MAX_EXPERTS + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nseg = build_segments<MT>(a, seg);
@@ -323,13 +350,17 @@ __global__ void __launch_bounds__(kFfnThreads) ffn_down_kernel(const __grid_cons
         }
         __syncthreads();
         const moe_expert_weights& W = a.ex[e];
+        if (W.precision == MOE_P4) {
+            chunk_sums(hs, hsum, MT, a.f);
+            __syncthreads();
+        }
         const int j_base = static_cast<int>(r - static_cast<long long>(s) * a.d);
         const int cnt = static_cast<int>(piece_end - r);
         for (int i = warp; i < cnt; i += kFfnWarps) {
             const int j = j_base + i;
             float acc[MT];
             if (W.precision == MOE_P4)
-                row_down_int4<MT>(W, j, a.f, hs, lane, acc);
+                row_down_int4<MT>(W, j, a.f, hs, hsum, lane, acc);
             else
                 row_down_bf16<MT>(W, j, a.f, hs, lane, acc);
 #pragma unroll
@@ -347,8 +378,8 @@ cudaError_t launch_ffn(const FfnArgs& a, cudaStream_t stream) {
     // Launch geometry is a pure function of (d, f): cache it so the hot path
     // issues no attribute/occupancy queries (and stays graph-capturable).
     static int cached_d = -1, cached_f = -1, grid_gu = 0, grid_dn = 0;
-    const size_t smem_gu = static_cast<size_t>(MT) * a.d * 2;
-    const size_t smem_dn = static_cast<size_t>(MT) * a.f * 2;
+    const size_t smem_gu = static_cast<size_t>(MT) * a.d * 2 + static_cast<size_t>(MT) * (a.d / 32) * 4;
+    const size_t smem_dn = static_cast<size_t>(MT) * a.f * 2 + static_cast<size_t>(MT) * (a.f / 32) * 4;
     if (cached_d != a.d || cached_f != a.f) {
         MOE_CUDA_OK(cudaFuncSetAttribute(ffn_gateup_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_gu)));
         MOE_CUDA_OK(cudaFuncSetAttribute(ffn_down_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_dn)));
