@@ -133,32 +133,36 @@ int moe_gate_topk(const void* x, const void* wg, int T, int d, int E, int k, int
 int moe_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_t* offsets,
                 int32_t* perm, int32_t* inv_perm, void* stream);
 
-/* Weights of one expert as the kernels see them. */
+/* Weights of one expert as the kernels see them: every matrix [R rows, K]
+ * in the fragment-block layout (16 rows x 128 K per block, DESIGN.md "HBM
+ * layout"; produced by moe_pack_bf16_blocks / moe_quantize_g128). */
 typedef struct {
     int32_t precision;        /* MOE_P4 (int4-g128) or MOE_P16 (bf16)                       */
     int32_t pad_;
-    const void* w_gate_up;    /* P16: bf16 [2f,d] (rows [0,f) gate, [f,2f) up); P4: uint32 [2f,d/8] */
-    const void* s_gate_up;    /* P4: bf16 scales [2f,d/128]; P16: NULL                      */
-    const void* w_down;       /* P16: bf16 [d,f]; P4: uint32 [d,f/8]                        */
-    const void* s_down;       /* P4: bf16 [d,f/128]                                         */
+    const void* w_gate_up;    /* [2f, d]: rows [0,f) gate, [f,2f) up; P16 bf16 blocks, P4 int4 blocks */
+    const void* s_gate_up;    /* P4: bf16 scale blocks; P16: NULL                           */
+    const void* w_down;       /* [d, f] blocks                                              */
+    const void* s_down;       /* P4: bf16 scale blocks                                      */
 } moe_expert_weights;
 
-/* K3/K4: grouped SwiGLU FFN of every expert segment of a permutation.
- * x [T,d] bf16 (gathered through perm on the fly), offsets [E+1] (device),
- * experts[E] (host array of device pointers), h_ws [T*k, f] bf16 workspace,
- * y_perm [T*k, d] fp32.  Mixed precision per expert.  Uses the 128-bit GEMV
- * kernels for T <= moe_gemv_max_tokens() and the tcgen05 GEMM otherwise. */
+/* K3/K4: grouped SwiGLU FFN of every expert segment of a permutation, on the
+ * tensor-core GEMV (<= 8 tokens per expert share each weight byte; larger
+ * segments are tiled).  x [T,d] bf16 (natural order), offsets [E+1] (device),
+ * experts[E] (host array of device pointers), y_perm [T*k, d] fp32.
+ * Mixed precision per expert.  `workspace` (moe_ffn_workspace_bytes) must be
+ * zero-filled before its first use; calls leave it reusable. */
+size_t moe_ffn_workspace_bytes(int T, int k, int E, int d, int f);
 int moe_ffn(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
-            const moe_expert_weights* experts, int E, int d, int f, void* h_ws, float* y_perm,
-            void* stream);
+            const moe_expert_weights* experts, int E, int d, int f, void* workspace,
+            size_t ws_bytes, float* y_perm, void* stream);
 /* Survey-named single-precision wrappers of moe_ffn (all experts one format). */
 int moe_ffn_int4(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
                  const void* const* q_gate_up, const void* const* s_gate_up,
                  const void* const* q_down, const void* const* s_down, int E, int d, int f,
-                 void* h_ws, float* y_perm, void* stream);
+                 void* workspace, size_t ws_bytes, float* y_perm, void* stream);
 int moe_ffn_bf16(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
                  const void* const* w_gate_up, const void* const* w_down, int E, int d, int f,
-                 void* h_ws, float* y_perm, void* stream);
+                 void* workspace, size_t ws_bytes, float* y_perm, void* stream);
 int moe_gemv_max_tokens(void);
 
 /* K5: out[t] = bf16(residual[t] + sum_j w[t,j] * y_perm[inv_perm[t*k+j]]),
@@ -166,9 +170,12 @@ int moe_gemv_max_tokens(void);
 int moe_combine(const float* y_perm, const int32_t* inv_perm, const float* w,
                 const void* residual, int T, int d, int k, void* out, void* stream);
 
-/* int4-g128 quantiser (bf16 [rows,cols] -> packed q + scales), the on-device
- * "Quantize" action of the reconfiguration model (reconfig.hpp:12). */
+/* int4-g128 quantiser: logical row-major bf16 [rows,cols] -> int4 fragment
+ * blocks q (rows*cols/8 uint32) + scale blocks s (rows*cols/128 bf16); the
+ * on-device "Quantize" action of the reconfiguration model (reconfig.hpp:12). */
 int moe_quantize_g128(const void* w, int rows, int cols, uint32_t* q, void* s, void* stream);
+/* logical row-major bf16 [rows,cols] -> bf16 fragment blocks */
+int moe_pack_bf16_blocks(const void* w, int rows, int cols, void* out, void* stream);
 
 /* Deterministic synthetic tensors (same generator as the oracle). */
 int moe_synth_weight_bf16(uint64_t seed, uint64_t uid, int64_t n, int shift, void* out,

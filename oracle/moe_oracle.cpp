@@ -374,6 +374,90 @@ void orc_moe_layer(const orc_model* m, int layer, const int* precision, const ui
     orc_moe_layer_w(m, wg.data(), ex.data(), x, T, out, idx_out, w_out, logits);
 }
 
+// ---- fragment-block storage layout (see moe_oracle.h) ----------------------
+int orc_perm_k(int k) {
+    const int g = k / 128, kin = k % 128;
+    const int kk = kin / 16, t = (kin % 8) / 2, hi = (kin % 16) / 8, e = kin % 2;
+    return g * 128 + t * 32 + kk * 4 + hi * 2 + e;
+}
+
+namespace {
+
+struct BlockPos {
+    size_t block;  // block index rt*G + g
+    int lane, half, r, gr;
+};
+
+inline BlockPos block_pos(int row, int k, int cols) {
+    const int G = cols / 128;
+    const int rt = row / 16, rr = row % 16;
+    const int p = orc_perm_k(k % 128);
+    BlockPos b;
+    b.block = static_cast<size_t>(rt) * G + k / 128;
+    b.gr = rr % 8;
+    b.half = rr / 8;
+    b.r = p % 32;
+    b.lane = b.gr * 4 + p / 32;
+    return b;
+}
+
+inline size_t bf16_block_index(const BlockPos& b) {  // in uint16 units
+    return b.block * 2048 + static_cast<size_t>(((b.half * 4 + b.r / 8) * 32 + b.lane) * 8 + (b.r % 8));
+}
+
+inline size_t int4_block_word(const BlockPos& b) {  // in uint32 units
+    return b.block * 256 + static_cast<size_t>((b.half * 32 + b.lane) * 4 + b.r / 8);
+}
+
+}  // namespace
+
+void orc_pack_bf16_blocks(const uint16_t* w, int rows, int cols, uint16_t* out) {
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) out[bf16_block_index(block_pos(r, c, cols))] = w[static_cast<size_t>(r) * cols + c];
+}
+
+void orc_unpack_bf16_blocks(const uint16_t* blk, int rows, int cols, uint16_t* out) {
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) out[static_cast<size_t>(r) * cols + c] = blk[bf16_block_index(block_pos(r, c, cols))];
+}
+
+void orc_pack_int4_blocks(const uint32_t* q, const uint16_t* s, int rows, int cols, uint32_t* qb,
+                          uint16_t* sb) {
+    const int G = cols / 128;
+    std::memset(qb, 0, static_cast<size_t>(rows) * cols / 2);
+#pragma omp parallel for schedule(static)
+    for (int rt = 0; rt < rows / 16; ++rt)
+        for (int rr = 0; rr < 16; ++rr) {
+            const int r = rt * 16 + rr;
+            for (int c = 0; c < cols; ++c) {
+                const uint32_t u = (q[static_cast<size_t>(r) * (cols / 8) + c / 8] >> nibble_shift(c & 7)) & 15u;
+                const BlockPos b = block_pos(r, c, cols);
+                qb[int4_block_word(b)] |= u << nibble_shift(b.r % 8);
+            }
+            for (int g = 0; g < G; ++g)
+                sb[(static_cast<size_t>(rt) * G + g) * 16 + (rr % 8) * 2 + rr / 8] = s[static_cast<size_t>(r) * G + g];
+        }
+}
+
+void orc_unpack_int4_blocks(const uint32_t* qb, const uint16_t* sb, int rows, int cols, uint32_t* q,
+                            uint16_t* s) {
+    const int G = cols / 128;
+    std::memset(q, 0, static_cast<size_t>(rows) * cols / 2);
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < rows; ++r) {
+        const int rt = r / 16, rr = r % 16;
+        for (int c = 0; c < cols; ++c) {
+            const BlockPos b = block_pos(r, c, cols);
+            const uint32_t u = (qb[int4_block_word(b)] >> nibble_shift(b.r % 8)) & 15u;
+            q[static_cast<size_t>(r) * (cols / 8) + c / 8] |= u << nibble_shift(c & 7);
+        }
+        for (int g = 0; g < G; ++g)
+            s[static_cast<size_t>(r) * G + g] = sb[(static_cast<size_t>(rt) * G + g) * 16 + (rr % 8) * 2 + rr / 8];
+    }
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

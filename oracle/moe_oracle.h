@@ -47,6 +47,28 @@ int orc_weight_shift(int K);
 void orc_quantize_g128(const uint16_t* w, int rows, int cols, uint32_t* q, uint16_t* s);
 void orc_dequant_g128(const uint32_t* q, const uint16_t* s, int rows, int cols, float* w_out);
 
+/* ---- device storage layout ("fragment blocks") ----
+ * The engine stores every expert matrix [R rows, K cols] (R % 16 == 0,
+ * K % 128 == 0) as blocks of 16 rows x 128 K, block (rt, g) at index
+ * rt*(K/128) + g.  Inside a group, K position k is permuted to
+ *   pi(k) = t*32 + kk*4 + hi*2 + e   (kk = k/16, t = (k%8)/2, hi = (k%16)/8, e = k%2)
+ * so that lane (gr, t) of an mma.m16n8k16 finds its fragments contiguous.
+ * Element (row, k) with rr = row%16, gr = rr%8, half = rr/8,
+ * p = pi(k%128), r = p%32, lane = gr*4 + p/32:
+ *   bf16 block (4096 B): byte ((half*4 + r/8)*32 + lane)*16 + (r%8)*2
+ *   int4 block (1024 B): word ((half*32 + lane)*4 + r/8), nibble (r%8) placed
+ *                        at bit 4*(j/2)+16*(j%2) with j = r%8, biased u=q+8
+ *   int4 scales (32 B per block): bf16 at byte gr*4 + half*2
+ * Activations fed to the GEMV (x / h) use the same pi within each group. */
+int orc_perm_k(int k);                                    /* pi(k % 128) + 128*(k/128) */
+void orc_pack_bf16_blocks(const uint16_t* w, int rows, int cols, uint16_t* out);
+void orc_unpack_bf16_blocks(const uint16_t* blk, int rows, int cols, uint16_t* out);
+/* q/s in the row-major format above -> block format (and back) */
+void orc_pack_int4_blocks(const uint32_t* q, const uint16_t* s, int rows, int cols,
+                          uint32_t* qb, uint16_t* sb);
+void orc_unpack_int4_blocks(const uint32_t* qb, const uint16_t* sb, int rows, int cols,
+                            uint32_t* q, uint16_t* s);
+
 /* ---- K1 router: fp32 logits in the pinned lane/butterfly order, top-k on
  *      logits (ties -> lower index), softmax over the selected logits ---- */
 void orc_gate_topk(const uint16_t* x, const uint16_t* wg, int T, int d, int E, int k,

@@ -62,6 +62,11 @@ class OracleLib:
             "orc_moe_layer": (None, [P(OrcModel), I, VP, VP, I, VP, VP, VP, VP]),
             "orc_moe_layer_w": (None, [P(OrcModel), VP, P(OrcExpert), VP, I, VP, VP, VP, VP]),
             "orc_num_threads": (I, []),
+            "orc_perm_k": (I, [I]),
+            "orc_pack_bf16_blocks": (None, [VP, I, I, VP]),
+            "orc_unpack_bf16_blocks": (None, [VP, I, I, VP]),
+            "orc_pack_int4_blocks": (None, [VP, VP, I, I, VP, VP]),
+            "orc_unpack_int4_blocks": (None, [VP, VP, I, I, VP, VP]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -110,6 +115,29 @@ class OracleLib:
         x = np.empty(T * m.d_model, np.uint16)
         self.L.orc_step_input(C.byref(m), step, T, _np_ptr(x))
         return x.reshape(T, m.d_model)
+
+    # device storage layout ------------------------------------------------
+    def pack_bf16_blocks(self, w, rows, cols):
+        out = np.empty(rows * cols, np.uint16)
+        self.L.orc_pack_bf16_blocks(_np_ptr(np.ascontiguousarray(w, np.uint16)), rows, cols, _np_ptr(out))
+        return out
+
+    def pack_int4_blocks(self, q, s, rows, cols):
+        qb = np.empty(rows * cols // 8, np.uint32)
+        sb = np.empty(rows * cols // 128, np.uint16)
+        self.L.orc_pack_int4_blocks(_np_ptr(np.ascontiguousarray(q, np.uint32)), _np_ptr(np.ascontiguousarray(s, np.uint16)),
+                                    rows, cols, _np_ptr(qb), _np_ptr(sb))
+        return qb, sb
+
+    def unpack_int4_blocks(self, qb, sb, rows, cols):
+        q = np.empty(rows * cols // 8, np.uint32)
+        s = np.empty(rows * cols // 128, np.uint16)
+        self.L.orc_unpack_int4_blocks(_np_ptr(np.ascontiguousarray(qb, np.uint32)), _np_ptr(np.ascontiguousarray(sb, np.uint16)),
+                                      rows, cols, _np_ptr(q), _np_ptr(s))
+        return q.reshape(rows, cols // 8), s.reshape(rows, cols // 128)
+
+    def perm_k(self, k):
+        return self.L.orc_perm_k(k)
 
     # math -------------------------------------------------------------------
     def quantize(self, w, rows, cols):

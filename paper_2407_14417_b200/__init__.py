@@ -117,9 +117,11 @@ def lib() -> C.CDLL:
         "moe_expected_throughput": (D, [P(ExpertStateC), P(_ModelProfile), P(_HardwareProfile)]),
         "moe_gate_topk": (I, [VP, VP, I, I, I, I, VP, VP, VP, VP]),
         "moe_permute": (I, [VP, I, I, I, VP, VP, VP, VP, VP]),
-        "moe_ffn": (I, [VP, VP, VP, I, I, P(ExpertWeightsC), I, I, I, VP, VP, VP]),
-        "moe_ffn_int4": (I, [VP, VP, VP, I, I, P(VP), P(VP), P(VP), P(VP), I, I, I, VP, VP, VP]),
-        "moe_ffn_bf16": (I, [VP, VP, VP, I, I, P(VP), P(VP), I, I, I, VP, VP, VP]),
+        "moe_ffn_workspace_bytes": (C.c_size_t, [I, I, I, I, I]),
+        "moe_ffn": (I, [VP, VP, VP, I, I, P(ExpertWeightsC), I, I, I, VP, C.c_size_t, VP, VP]),
+        "moe_ffn_int4": (I, [VP, VP, VP, I, I, P(VP), P(VP), P(VP), P(VP), I, I, I, VP, C.c_size_t, VP, VP]),
+        "moe_ffn_bf16": (I, [VP, VP, VP, I, I, P(VP), P(VP), I, I, I, VP, C.c_size_t, VP, VP]),
+        "moe_pack_bf16_blocks": (I, [VP, I, I, VP, VP]),
         "moe_gemv_max_tokens": (I, []),
         "moe_combine": (I, [VP, VP, VP, VP, I, I, I, VP, VP]),
         "moe_quantize_g128": (I, [VP, I, I, VP, VP, VP]),
@@ -426,10 +428,20 @@ def expert_weights(precision, w_gate_up, w_down, s_gate_up=None, s_down=None) ->
     return ExpertWeightsC(precision, 0, _ptr(w_gate_up), _ptr(s_gate_up), _ptr(w_down), _ptr(s_down))
 
 
-def ffn(x, perm, offsets, T, k, experts: Sequence[ExpertWeightsC], d, f, h_ws, y_perm, stream=None):
+def ffn_workspace_bytes(T, k, E, d, f) -> int:
+    return lib().moe_ffn_workspace_bytes(T, k, E, d, f)
+
+
+def ffn(x, perm, offsets, T, k, experts: Sequence[ExpertWeightsC], d, f, workspace, ws_bytes, y_perm,
+        stream=None):
+    """K3/K4 grouped SwiGLU FFN; `workspace` (ffn_workspace_bytes) zero-filled once."""
     arr = (ExpertWeightsC * len(experts))(*experts)
-    _check(lib().moe_ffn(_ptr(x), _ptr(perm), _ptr(offsets), T, k, arr, len(experts), d, f, _ptr(h_ws),
-                         _ptr(y_perm), _stream(stream)))
+    _check(lib().moe_ffn(_ptr(x), _ptr(perm), _ptr(offsets), T, k, arr, len(experts), d, f, _ptr(workspace),
+                         ws_bytes, _ptr(y_perm), _stream(stream)))
+
+
+def pack_bf16_blocks(w, rows, cols, out, stream=None):
+    _check(lib().moe_pack_bf16_blocks(_ptr(w), rows, cols, _ptr(out), _stream(stream)))
 
 
 def combine(y_perm, inv_perm, w, residual, T, d, k, out, stream=None):

@@ -333,19 +333,50 @@ int moe_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_
     });
 }
 
-int moe_gemv_max_tokens(void) { return 4; }
+int moe_gemv_max_tokens(void) { return 8; }
+
+namespace {
+
+size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+struct WsLayout {
+    size_t xperm, hperm, part, counters, total;
+};
+
+WsLayout ws_layout(int T, int k, int E, int d, int f) {
+    WsLayout w{};
+    w.xperm = 0;
+    w.hperm = w.xperm + align256(static_cast<size_t>(T) * d * 2);
+    w.part = w.hperm + align256(static_cast<size_t>(T) * k * f * 2);
+    w.counters = w.part + align256(moek_gemv_partial_floats(T, k, d, f) * 4);
+    w.total = w.counters + align256(moek_gemv_counter_count(T, E, d, f) * 4);
+    return w;
+}
+
+}  // namespace
+
+size_t moe_ffn_workspace_bytes(int T, int k, int E, int d, int f) {
+    if (T < 1 || k < 1 || E < 1 || d < 128 || f < 128) return 0;
+    return ws_layout(T, k, E, d, f).total;
+}
 
 int moe_ffn(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
-            const moe_expert_weights* experts, int E, int d, int f, void* h_ws, float* y_perm,
-            void* stream) {
+            const moe_expert_weights* experts, int E, int d, int f, void* workspace, size_t ws_bytes,
+            float* y_perm, void* stream) {
     return guarded([&] {
         usage_if(E < 1 || E > MOE_MAX_EXPERTS || k < 1 || k > E, "bad E / k");
         usage_if(d <= 0 || d % 256 != 0 || f <= 0 || f % 128 != 0,
                  "d must be a multiple of 256 and f a multiple of 128");
         need_device();
         if (T == 0) return;
+        const WsLayout L = ws_layout(T, k, E, d, f);
+        usage_if(workspace == nullptr || ws_bytes < L.total, "workspace too small (moe_ffn_workspace_bytes)");
+        char* base = static_cast<char*>(workspace);
+        GemvWorkspace ws{base + L.xperm, base + L.hperm, reinterpret_cast<float*>(base + L.part),
+                         reinterpret_cast<unsigned int*>(base + L.counters)};
         const uint64_t mask = E >= 64 ? ~0ull : ((1ull << E) - 1ull);
-        const cudaError_t e = moek_ffn_gemv(x, perm, offsets, T, k, experts, E, d, f, h_ws, y_perm, mask, st(stream));
+        const cudaError_t e = moek_ffn_mma(ws, x, perm, offsets, nullptr, nullptr, nullptr, T, k, experts, E, d, f,
+                                           mask, nullptr, y_perm, false, st(stream));
         if (e != cudaSuccess) throw std::runtime_error(std::string("moe_ffn: ") + cudaGetErrorString(e));
     });
 }
@@ -353,26 +384,26 @@ int moe_ffn(const void* x, const int32_t* perm, const int32_t* offsets, int T, i
 int moe_ffn_int4(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
                  const void* const* q_gate_up, const void* const* s_gate_up,
                  const void* const* q_down, const void* const* s_down, int E, int d, int f,
-                 void* h_ws, float* y_perm, void* stream) {
+                 void* workspace, size_t ws_bytes, float* y_perm, void* stream) {
     moe_expert_weights ex[MOE_MAX_EXPERTS];
     if (E < 1 || E > MOE_MAX_EXPERTS) {
         g_err = "bad E";
         return MOE_ERR_USAGE;
     }
     for (int e = 0; e < E; ++e) ex[e] = {MOE_P4, 0, q_gate_up[e], s_gate_up[e], q_down[e], s_down[e]};
-    return moe_ffn(x, perm, offsets, T, k, ex, E, d, f, h_ws, y_perm, stream);
+    return moe_ffn(x, perm, offsets, T, k, ex, E, d, f, workspace, ws_bytes, y_perm, stream);
 }
 
 int moe_ffn_bf16(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
                  const void* const* w_gate_up, const void* const* w_down, int E, int d, int f,
-                 void* h_ws, float* y_perm, void* stream) {
+                 void* workspace, size_t ws_bytes, float* y_perm, void* stream) {
     moe_expert_weights ex[MOE_MAX_EXPERTS];
     if (E < 1 || E > MOE_MAX_EXPERTS) {
         g_err = "bad E";
         return MOE_ERR_USAGE;
     }
     for (int e = 0; e < E; ++e) ex[e] = {MOE_P16, 0, w_gate_up[e], nullptr, w_down[e], nullptr};
-    return moe_ffn(x, perm, offsets, T, k, ex, E, d, f, h_ws, y_perm, stream);
+    return moe_ffn(x, perm, offsets, T, k, ex, E, d, f, workspace, ws_bytes, y_perm, stream);
 }
 
 int moe_combine(const float* y_perm, const int32_t* inv_perm, const float* w, const void* residual,
@@ -387,10 +418,21 @@ int moe_combine(const float* y_perm, const int32_t* inv_perm, const float* w, co
 
 int moe_quantize_g128(const void* w, int rows, int cols, uint32_t* q, void* s, void* stream) {
     return guarded([&] {
-        usage_if(rows < 0 || cols <= 0 || cols % 128 != 0, "cols must be a positive multiple of 128");
+        usage_if(rows < 0 || rows % 16 != 0 || cols <= 0 || cols % 128 != 0,
+                 "rows must be a multiple of 16 and cols a positive multiple of 128");
         need_device();
-        const cudaError_t e = moek_quantize(w, rows, cols, q, s, st(stream));
+        const cudaError_t e = moek_quantize_blocks(w, rows, cols, q, s, st(stream));
         if (e != cudaSuccess) throw std::runtime_error(std::string("moe_quantize_g128: ") + cudaGetErrorString(e));
+    });
+}
+
+int moe_pack_bf16_blocks(const void* w, int rows, int cols, void* out, void* stream) {
+    return guarded([&] {
+        usage_if(rows < 0 || rows % 16 != 0 || cols <= 0 || cols % 128 != 0,
+                 "rows must be a multiple of 16 and cols a positive multiple of 128");
+        need_device();
+        const cudaError_t e = moek_pack_bf16_blocks(w, rows, cols, out, st(stream));
+        if (e != cudaSuccess) throw std::runtime_error(std::string("moe_pack_bf16_blocks: ") + cudaGetErrorString(e));
     });
 }
 

@@ -72,8 +72,8 @@ struct MoeEngine::Impl {
     int32_t* perm = nullptr;
     int32_t* inv = nullptr;
     unsigned int* ticket = nullptr;
-    uint16_t* h = nullptr;
-    float* y = nullptr;
+    float* y = nullptr;          // per-slot expert outputs (streamed-expert path)
+    GemvWorkspace gws{};
     int32_t* idx_host = nullptr;  // pinned [Tmax*K]
     size_t ws_bytes = 0;
 
@@ -180,8 +180,15 @@ struct MoeEngine::Impl {
         dev_alloc(reinterpret_cast<void**>(&perm), TK * 4);
         dev_alloc(reinterpret_cast<void**>(&inv), TK * 4);
         dev_alloc(reinterpret_cast<void**>(&ticket), 4);
-        dev_alloc(reinterpret_cast<void**>(&h), TK * f * 2);
         dev_alloc(reinterpret_cast<void**>(&y), TK * d * 4);
+        dev_alloc(&gws.xperm, static_cast<size_t>(Tmax) * d * 2);
+        dev_alloc(&gws.hperm, TK * f * 2);
+        const size_t nparts = moek_gemv_partial_floats(Tmax, K, d, f);
+        const size_t nctr = moek_gemv_counter_count(Tmax, E, d, f);
+        dev_alloc(reinterpret_cast<void**>(&gws.part), nparts * 4);
+        dev_alloc(reinterpret_cast<void**>(&gws.counters), nctr * 4);
+        ck(cudaMemsetAsync(gws.counters, 0, nctr * 4, compute), "memset");
+        ck(cudaMemsetAsync(gws.hperm, 0, TK * f * 2, compute), "memset");
         ck(cudaMemsetAsync(ticket, 0, 4, compute), "memset");
         ck(cudaMemsetAsync(xin, 0, static_cast<size_t>(Tmax) * d * 2, compute), "memset");
         ck(cudaHostAlloc(reinterpret_cast<void**>(&idx_host), TK * 4, cudaHostAllocDefault), "cudaHostAlloc");
@@ -198,41 +205,36 @@ struct MoeEngine::Impl {
         for (int l = 0; l < L; ++l)
             ck(moek_synth_weight(cfg.seed, uid_router(l), static_cast<long long>(E) * d, sh_gu,
                                  wg + static_cast<size_t>(l) * E * d, compute), "synth router");
-        char* tmp16 = nullptr;
-        char* tmp4 = nullptr;
-        bool need16 = false, need4 = false;
-        for (const ExpertState& st : plan.entries) {
-            if (st.precision == Precision::P4 || st.location == Location::CPU) need16 = true;
-            if (st.precision == Precision::P4 && st.location == Location::CPU) need4 = true;
-        }
-        if (need16) ck(cudaMalloc(&tmp16, size16), "cudaMalloc(tmp)");
-        if (need4) ck(cudaMalloc(&tmp4, size4), "cudaMalloc(tmp)");
+        // logical (row-major) bf16 master -> fragment blocks (bf16 or int4)
+        char* master = nullptr;
+        char* stage = nullptr;
+        ck(cudaMalloc(&master, size16), "cudaMalloc(master)");
+        if (host_bytes) ck(cudaMalloc(&stage, size16), "cudaMalloc(stage)");
         for (int e = 0; e < L * E; ++e) {
             const ExpertState st = plan.entries[static_cast<size_t>(e)];
-            const bool direct = st.precision == Precision::P16 && st.location == Location::GPU;
-            char* master = direct ? static_cast<char*>(const_cast<void*>(weights[static_cast<size_t>(e)].w_gate_up)) : tmp16;
             ck(moek_synth_weight(cfg.seed, uid_expert(e, 1), static_cast<long long>(2 * fd), sh_gu, master, compute), "synth");
             ck(moek_synth_weight(cfg.seed, uid_expert(e, 2), static_cast<long long>(fd), sh_d, master + 4 * fd, compute), "synth");
-            if (direct) continue;
             char* dst = st.location == Location::GPU ? static_cast<char*>(const_cast<void*>(weights[static_cast<size_t>(e)].w_gate_up))
-                                                     : (st.precision == Precision::P4 ? tmp4 : tmp16);
-            if (st.precision == Precision::P4) {
-                moe_expert_weights v = view(dst, Precision::P4);
-                ck(moek_quantize(master, 2 * f, d, static_cast<uint32_t*>(const_cast<void*>(v.w_gate_up)),
-                                 const_cast<void*>(v.s_gate_up), compute), "quantize");
-                ck(moek_quantize(master + 4 * fd, d, f, static_cast<uint32_t*>(const_cast<void*>(v.w_down)),
-                                 const_cast<void*>(v.s_down), compute), "quantize");
+                                                     : stage;
+            moe_expert_weights v = view(dst, st.precision);
+            if (st.precision == Precision::P16) {
+                ck(moek_pack_bf16_blocks(master, 2 * f, d, const_cast<void*>(v.w_gate_up), compute), "pack");
+                ck(moek_pack_bf16_blocks(master + 4 * fd, d, f, const_cast<void*>(v.w_down), compute), "pack");
+            } else {
+                ck(moek_quantize_blocks(master, 2 * f, d, static_cast<uint32_t*>(const_cast<void*>(v.w_gate_up)),
+                                        const_cast<void*>(v.s_gate_up), compute), "quantize");
+                ck(moek_quantize_blocks(master + 4 * fd, d, f, static_cast<uint32_t*>(const_cast<void*>(v.w_down)),
+                                        const_cast<void*>(v.s_down), compute), "quantize");
             }
             if (st.location == Location::CPU) {
                 const size_t sz = st.precision == Precision::P16 ? size16 : size4;
-                ck(cudaMemcpyAsync(const_cast<void*>(weights[static_cast<size_t>(e)].w_gate_up), dst, sz,
+                ck(cudaMemcpyAsync(const_cast<void*>(weights[static_cast<size_t>(e)].w_gate_up), stage, sz,
                                    cudaMemcpyDeviceToHost, compute), "D2H");
-                ck(cudaStreamSynchronize(compute), "sync");  // tmp reused next iteration
             }
+            ck(cudaStreamSynchronize(compute), "sync");  // master / stage reused next iteration
         }
-        ck(cudaStreamSynchronize(compute), "sync");
-        if (tmp16) cudaFree(tmp16);
-        if (tmp4) cudaFree(tmp4);
+        cudaFree(master);
+        if (stage) cudaFree(stage);
     }
 
     void destroy() {
@@ -240,7 +242,8 @@ struct MoeEngine::Impl {
         graphs.clear();
         if (compute) cudaStreamSynchronize(compute);
         if (copy) cudaStreamSynchronize(copy);
-        void* devp[] = {dev_arena, swap, wg, xin, xout, xbuf[0], xbuf[1], idx, wts, counts, offsets, perm, inv, ticket, h, y};
+        void* devp[] = {dev_arena, swap, wg, xin, xout, xbuf[0], xbuf[1], idx, wts, counts, offsets, perm, inv, ticket, y,
+                         gws.xperm, gws.hperm, gws.part, gws.counters};
         for (void* p : devp)
             if (p) cudaFree(p);
         if (host_arena) cudaFreeHost(host_arena);
@@ -262,7 +265,9 @@ struct MoeEngine::Impl {
         counters.activations += static_cast<int64_t>(T) * K;
         if (!layer_has_cpu[static_cast<size_t>(l)]) {
             counters.hits += static_cast<int64_t>(T) * K;
-            ck(moek_ffn_gemv(x, perm, offsets, T, K, lw, E, d, f, h, y, mask_all(), compute), "ffn");
+            ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, lw, E, d, f, mask_all(), out, nullptr,
+                            false, compute), "ffn");
+            return;
         } else {
             ck(cudaMemcpyAsync(idx_host, idx_l, static_cast<size_t>(T) * K * 4, cudaMemcpyDeviceToHost, compute), "D2H idx");
             ck(cudaStreamSynchronize(compute), "sync");
@@ -280,8 +285,12 @@ struct MoeEngine::Impl {
             uint64_t resident = 0;
             for (int s = 0; s < E; ++s)
                 if (((sel >> s) & 1ull) && location[static_cast<size_t>(l * E + s)] == MOE_GPU) resident |= 1ull << s;
-            if (resident)
-                ck(moek_ffn_gemv(x, perm, offsets, T, K, lw, E, d, f, h, y, resident, compute), "ffn");
+            bool permuted = false;  // x -> xperm done once per layer
+            if (resident) {
+                ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, lw, E, d, f, resident, nullptr, y,
+                                permuted, compute), "ffn");
+                permuted = true;
+            }
             std::vector<moe_expert_weights> tmp(lw, lw + E);
             for (int s = 0; s < E; ++s) {
                 if (!((sel >> s) & 1ull) || location[static_cast<size_t>(l * E + s)] == MOE_GPU) continue;
@@ -294,7 +303,9 @@ struct MoeEngine::Impl {
                 ck(cudaEventRecord(copy_done, copy), "record");
                 ck(cudaStreamWaitEvent(compute, copy_done, 0), "wait");
                 tmp[static_cast<size_t>(s)] = view(swap, hw.precision == MOE_P16 ? Precision::P16 : Precision::P4);
-                ck(moek_ffn_gemv(x, perm, offsets, T, K, tmp.data(), E, d, f, h, y, 1ull << s, compute), "ffn");
+                ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, tmp.data(), E, d, f, 1ull << s, nullptr, y,
+                                permuted, compute), "ffn");
+                permuted = true;
                 ck(cudaEventRecord(slot_free, compute), "record");
             }
         }
@@ -331,9 +342,9 @@ struct MoeEngine::Impl {
             ck(moek_route(src, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx + l * TK, wts + l * TK,
                           nullptr, counts, offsets, perm, inv, ticket, compute), "route");
             ck(cudaEventRecord(ev[static_cast<size_t>(2 * l)], compute), "record");
-            ck(moek_ffn_gemv(src, perm, offsets, T, K, lw, E, d, f, h, y, mask_all(), compute), "ffn");
+            ck(moek_ffn_mma(gws, src, perm, offsets, inv, wts + l * TK, src, T, K, lw, E, d, f, mask_all(), dst,
+                            nullptr, false, compute), "ffn");
             ck(cudaEventRecord(ev[static_cast<size_t>(2 * l + 1)], compute), "record");
-            ck(moek_combine(y, inv, wts + l * TK, src, T, d, K, dst, compute), "combine");
             src = dst;
         }
         ck(cudaStreamSynchronize(compute), "sync");
@@ -356,7 +367,7 @@ struct MoeEngine::Impl {
             ffn_bytes[l] = bytes;
         }
         for (auto& e : ev) cudaEventDestroy(e);
-        if (kernels_per_step) *kernels_per_step = 4 * L;  // route, gate/up, down, combine
+        if (kernels_per_step) *kernels_per_step = 4 * L;  // route, permute-x, gate/up, down(+combine)
     }
 
     bool graphable() const {

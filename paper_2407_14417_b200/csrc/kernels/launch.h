@@ -11,10 +11,29 @@ cudaError_t moek_route(const void* x, const void* wg, int T, int d, int E, int k
                        int32_t* inv_perm, unsigned int* ticket, cudaStream_t stream);
 cudaError_t moek_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_t* offsets,
                          int32_t* perm, int32_t* inv_perm, cudaStream_t stream);
-// active_mask: bit e set -> expert e's segments are computed by this launch.
-cudaError_t moek_ffn_gemv(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
-                          const moe_expert_weights* experts, int E, int d, int f, void* h_ws,
-                          float* y_perm, uint64_t active_mask, cudaStream_t stream);
+// Workspace of the tensor-core GEMV FFN (must be zeroed once; the kernels
+// leave the arrival counters at zero).
+struct GemvWorkspace {
+    void* xperm;              // [T][d] bf16, K-permuted
+    void* hperm;              // [T*k][f] bf16, K-permuted
+    float* part;              // partial run sums
+    unsigned int* counters;   // arrival counters
+};
+size_t moek_gemv_partial_floats(int T, int k, int d, int f);
+size_t moek_gemv_counter_count(int T, int E, int d, int f);
+cudaError_t moek_permute_rows(const void* x, int rows, int K, void* xperm, cudaStream_t stream);
+// Expert FFN of every active expert segment (bit e of active_mask): gate/up
+// GEMV + fused SwiGLU, down GEMV + fused combine (out != null: out[t] =
+// bf16(resid[t] + sum_j w[t,j] y[inv[t*k+j]])) or per-slot y (out == null).
+cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* perm,
+                         const int32_t* offsets, const int32_t* inv, const float* wts,
+                         const void* resid, int T, int k, const moe_expert_weights* experts, int E,
+                         int d, int f, uint64_t active_mask, void* out, float* y, bool xperm_ready,
+                         cudaStream_t stream);
+// Storage-layout converters (logical row-major -> fragment blocks).
+cudaError_t moek_pack_bf16_blocks(const void* w, int rows, int cols, void* out, cudaStream_t stream);
+cudaError_t moek_quantize_blocks(const void* w, int rows, int cols, uint32_t* qb, void* sb,
+                                 cudaStream_t stream);
 cudaError_t moek_combine(const float* y, const int32_t* inv, const float* w, const void* res, int T,
                          int d, int k, void* out, cudaStream_t stream);
 cudaError_t moek_quantize(const void* w, int rows, int cols, uint32_t* q, void* s, cudaStream_t stream);

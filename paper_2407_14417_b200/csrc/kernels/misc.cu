@@ -67,6 +67,63 @@ __global__ void quantize_kernel(const uint16_t* __restrict__ w, int rows, int co
     if (lane == 0) s[static_cast<size_t>(r) * groups + g] = sb;
 }
 
+// ---- fragment-block storage layout (oracle orc_pack_*_blocks) -------------
+MOE_DEVI int perm_pos(int kin) {  // pi(k) within a 128-group
+    return ((kin & 7) >> 1) * 32 + (kin >> 4) * 4 + ((kin >> 3) & 1) * 2 + (kin & 1);
+}
+MOE_DEVI int inv_perm_pos(int p) {  // pi^-1
+    const int t = p >> 5, r = p & 31;
+    return (r >> 2) * 16 + ((r >> 1) & 1) * 8 + t * 2 + (r & 1);
+}
+
+__global__ void pack_bf16_blocks_kernel(const uint16_t* __restrict__ w, int rows, int cols,
+                                        uint16_t* __restrict__ out) {
+    const long long n = static_cast<long long>(rows) * cols;
+    const int G = cols / 128;
+    for (long long o = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; o < n;
+         o += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int row = static_cast<int>(o / cols), c = static_cast<int>(o - static_cast<long long>(row) * cols);
+        const int rt = row >> 4, rr = row & 15, gr = rr & 7, half = rr >> 3;
+        const int p = perm_pos(c & 127), r = p & 31, lane = gr * 4 + (p >> 5);
+        const size_t blk = static_cast<size_t>(rt) * G + (c >> 7);
+        out[blk * 2048 + static_cast<size_t>(((half * 4 + (r >> 3)) * 32 + lane) * 8 + (r & 7))] = w[o];
+    }
+}
+
+// int4-g128 RTN quantiser writing the block layout: one warp per (row,
+// 128-group).  Same arithmetic as orc_quantize_g128.
+__global__ void quantize_blocks_kernel(const uint16_t* __restrict__ w, int rows, int cols,
+                                       uint32_t* __restrict__ qb, uint16_t* __restrict__ sb) {
+    const int G = cols / 128;
+    const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= static_cast<long long>(rows) * G) return;
+    const int row = static_cast<int>(wid / G), g = static_cast<int>(wid - static_cast<long long>(row) * G);
+    const uint16_t* src = w + static_cast<size_t>(row) * cols + g * 128;
+    const uint2 raw = *reinterpret_cast<const uint2*>(src + lane * 4);
+    float amax = fmaxf(fmaxf(fabsf(bf16_lo(raw.x)), fabsf(bf16_hi(raw.x))),
+                       fmaxf(fabsf(bf16_lo(raw.y)), fabsf(bf16_hi(raw.y))));
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+    const uint16_t s16 = amax == 0.0f ? f2bf(1.0f) : f2bf(__fdiv_rn(amax, 7.0f));
+    const float sf = bf2f(s16);
+    const int rt = row >> 4, rr = row & 15, gr = rr & 7, half = rr >> 3;
+    const size_t blk = static_cast<size_t>(rt) * G + g;
+    if (lane < 16) {
+        const int tb = lane >> 2, q = lane & 3;  // lane-block t, word q
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int k = inv_perm_pos(tb * 32 + q * 8 + j);
+            float qv = rintf(__fdiv_rn(bf2f(src[k]), sf));
+            qv = fminf(7.0f, fmaxf(-8.0f, qv));
+            word |= static_cast<uint32_t>(static_cast<int>(qv) + 8) << (4 * (j >> 1) + 16 * (j & 1));
+        }
+        qb[blk * 256 + static_cast<size_t>((half * 32 + gr * 4 + tb) * 4 + q)] = word;
+    }
+    if (lane == 0) sb[blk * 16 + gr * 2 + half] = s16;
+}
+
 MOE_DEVI uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
@@ -129,6 +186,25 @@ cudaError_t moek_quantize(const void* w, int rows, int cols, uint32_t* q, void* 
     const int threads = 256;
     moek::quantize_kernel<<<static_cast<unsigned>((warps * 32 + threads - 1) / threads), threads, 0, stream>>>(
         static_cast<const uint16_t*>(w), rows, cols, q, static_cast<uint16_t*>(s));
+    return cudaGetLastError();
+}
+
+cudaError_t moek_pack_bf16_blocks(const void* w, int rows, int cols, void* out, cudaStream_t stream) {
+    const long long n = static_cast<long long>(rows) * cols;
+    if (n == 0) return cudaSuccess;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    moek::pack_bf16_blocks_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        static_cast<const uint16_t*>(w), rows, cols, static_cast<uint16_t*>(out));
+    return cudaGetLastError();
+}
+
+cudaError_t moek_quantize_blocks(const void* w, int rows, int cols, uint32_t* qb, void* sb, cudaStream_t stream) {
+    const long long warps = static_cast<long long>(rows) * (cols / 128);
+    if (warps == 0) return cudaSuccess;
+    const int threads = 256;
+    moek::quantize_blocks_kernel<<<static_cast<unsigned>((warps * 32 + threads - 1) / threads), threads, 0, stream>>>(
+        static_cast<const uint16_t*>(w), rows, cols, qb, static_cast<uint16_t*>(sb));
     return cudaGetLastError();
 }
 

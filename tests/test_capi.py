@@ -60,7 +60,7 @@ def test_kernels_fail_loudly_without_a_device(moe):
 def test_status_codes_mirror_cli(moe):
     # usage (2): bad shape before any device work
     with pytest.raises(moe.UsageError):
-        moe.ffn(None, None, None, 1, 2, [], 512, 1792, None, None, stream=0)
+        moe.ffn(None, None, None, 1, 2, [], 512, 1792, None, 0, None, stream=0)
     # validation (3) / infeasible (4) from the planner
     with pytest.raises(moe.ValidationError):
         moe.make_plan(moe.TaskRequest(moe.QUALITY, None, 0), moe.HardwareProfile(10**11), moe.mixtral_sec41())

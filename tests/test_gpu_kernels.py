@@ -29,20 +29,31 @@ def test_synth_weight_bitexact(moe, orc, torch_mod, cuda):
         assert moe.weight_shift(K) == orc.weight_shift(K)
 
 
-@pytest.mark.parametrize("rows,cols", [(1, 128), (7, 512), (64, 1792), (3, 4096)])
+@pytest.mark.parametrize("rows,cols", [(16, 128), (32, 512), (64, 1792), (48, 4096)])
 def test_quantize_bitexact(moe, orc, torch_mod, cuda, rows, cols):
+    """GPU quantiser (fragment-block output) == oracle RTN quantiser, packed."""
     torch = torch_mod
     w = orc.synth_weight(3, 99 + rows, rows * cols, orc.weight_shift(cols)).reshape(rows, cols)
-    if rows > 1:
-        w[1, :128] = 0  # all-zero group -> scale 1.0
+    w[1, :128] = 0  # all-zero group -> scale 1.0
     q_ref, s_ref = orc.quantize(w, rows, cols)
+    qb_ref, sb_ref = orc.pack_int4_blocks(q_ref, s_ref, rows, cols)
     wd = to_dev(w, torch, cuda)
     q = torch.empty(rows * cols // 8, dtype=torch.int32, device=cuda)
     s = torch.empty(rows * cols // 128, dtype=torch.int16, device=cuda)
     moe.quantize_g128(wd, rows, cols, q, s)
     torch.cuda.synchronize()
-    assert np.array_equal(to_np(q, np.uint32).reshape(rows, -1), q_ref)
-    assert np.array_equal(to_np(s, np.uint16).reshape(rows, -1), s_ref)
+    assert np.array_equal(to_np(q, np.uint32), qb_ref)
+    assert np.array_equal(to_np(s, np.uint16), sb_ref)
+
+
+@pytest.mark.parametrize("rows,cols", [(16, 128), (48, 1792), (32, 4096)])
+def test_pack_bf16_blocks_bitexact(moe, orc, torch_mod, cuda, rows, cols):
+    torch = torch_mod
+    w = orc.synth_weight(5, rows, rows * cols, 9)
+    out = torch.empty(rows * cols, dtype=torch.int16, device=cuda)
+    moe.pack_bf16_blocks(to_dev(w, torch, cuda), rows, cols, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(out, np.uint16), orc.pack_bf16_blocks(w, rows, cols))
 
 
 @pytest.mark.parametrize("T,d,E,k", [(1, 512, 8, 2), (32, 512, 8, 2), (5, 4096, 8, 2), (257, 4096, 8, 2),
@@ -106,20 +117,25 @@ def test_permute_bitexact(moe, orc, torch_mod, cuda, T, E, k, mode):
 
 
 def _expert_tensors(orc, torch, cuda, m, e, precision):
+    """Host (logical) tensors for the oracle, device tensors in block layout."""
+    d, f = m.d_model, m.d_ffn
     if precision == 1:
         gu, dn = orc.expert_bf16(m, e)
-        dev = (to_dev(gu, torch, cuda), to_dev(dn, torch, cuda))
+        dev = (to_dev(orc.pack_bf16_blocks(gu, 2 * f, d), torch, cuda), to_dev(orc.pack_bf16_blocks(dn, d, f), torch, cuda))
         return dev, (gu, dn)
     qgu, sgu, qd, sd = orc.expert_int4(m, e)
-    dev = tuple(to_dev(a, torch, cuda) for a in (qgu, sgu, qd, sd))
+    qgub, sgub = orc.pack_int4_blocks(qgu, sgu, 2 * f, d)
+    qdb, sdb = orc.pack_int4_blocks(qd, sd, d, f)
+    dev = tuple(to_dev(a, torch, cuda) for a in (qgub, sgub, qdb, sdb))
     return dev, (qgu, sgu, qd, sd)
 
 
-@pytest.mark.parametrize("T", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("T", [1, 2, 3, 4, 6, 8, 13])
 @pytest.mark.parametrize("mix", ["bf16", "int4", "mixed"])
-def test_ffn_grouped_vs_oracle(moe, orc, torch_mod, cuda, T, mix):
+@pytest.mark.parametrize("shape", [(512, 1792), (1024, 2048)])
+def test_ffn_grouped_vs_oracle(moe, orc, torch_mod, cuda, T, mix, shape):
     torch = torch_mod
-    d, f, E, k = 512, 1792, 8, 2
+    (d, f), E, k = shape, 8, 2
     m = orc.model(1, E, k, d, f, 1234)
     prec = {"bf16": [1] * E, "int4": [0] * E, "mixed": [0, 1] * (E // 2)}[mix]
     x = orc.step_input(m, T, T)
@@ -136,10 +152,12 @@ def test_ffn_grouped_vs_oracle(moe, orc, torch_mod, cuda, T, mix):
             experts.append(moe.expert_weights(moe.MOE_P16, dev[0], dev[1]))
         else:
             experts.append(moe.expert_weights(moe.MOE_P4, dev[0], dev[2], dev[1], dev[3]))
-    h_ws = torch.empty(T * k * f, dtype=torch.int16, device=cuda)
+    nws = moe.ffn_workspace_bytes(T, k, E, d, f)
+    ws = torch.zeros(nws, dtype=torch.uint8, device=cuda)
     y = torch.full((T * k * d,), float("nan"), dtype=torch.float32, device=cuda)
-    moe.ffn(to_dev(x, torch, cuda), to_dev(perm, torch, cuda), to_dev(offsets, torch, cuda), T, k, experts, d, f,
-            h_ws, y)
+    for _ in range(2):  # the workspace is reusable: counters return to zero
+        moe.ffn(to_dev(x, torch, cuda), to_dev(perm, torch, cuda), to_dev(offsets, torch, cuda), T, k, experts, d,
+                f, ws, nws, y)
     torch.cuda.synchronize()
     y = to_np(y, np.float32).reshape(T * k, d)
     for e in range(E):
@@ -178,4 +196,4 @@ def test_no_fallback_errors_are_loud(moe, torch_mod, cuda):
     with pytest.raises(moe.UsageError):
         moe.gate_topk(None, None, 1, 100, 8, 2, None, None)  # d % 8 != 0
     with pytest.raises(moe.UsageError):
-        moe.ffn(None, None, None, 1, 2, [], 512, 1792, None, None)  # E = 0
+        moe.ffn(None, None, None, 1, 2, [], 512, 1792, None, 0, None)  # E = 0
