@@ -243,6 +243,11 @@ int moe_engine_expert(const moe_engine* eng, int layer, int slot, moe_expert_wei
                       int32_t* location);
 int moe_engine_router(const moe_engine* eng, int layer, const void** wg_dev);
 
+/* Debug: device buffer receiving per-warp phase timestamps of the GEMV
+ * kernels ([2 passes][148*12 warps][8] uint64: entry, after PDL wait, first
+ * item ready, end, items, runs, epilogues, CTA); NULL disables. */
+int moe_debug_gemv_trace(void* buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -146,6 +146,7 @@ def lib() -> C.CDLL:
         "moe_engine_reset_counters": (I, [VP]),
         "moe_engine_expert": (I, [VP, I, I, P(ExpertWeightsC), P(C.c_int32)]),
         "moe_engine_router": (I, [VP, I, P(VP)]),
+        "moe_debug_gemv_trace": (I, [VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

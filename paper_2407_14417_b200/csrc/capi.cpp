@@ -335,29 +335,9 @@ int moe_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_
 
 int moe_gemv_max_tokens(void) { return 8; }
 
-namespace {
-
-size_t align256(size_t v) { return (v + 255) / 256 * 256; }
-
-struct WsLayout {
-    size_t xperm, hperm, part, counters, total;
-};
-
-WsLayout ws_layout(int T, int k, int E, int d, int f) {
-    WsLayout w{};
-    w.xperm = 0;
-    w.hperm = w.xperm + align256(static_cast<size_t>(T) * d * 2);
-    w.part = w.hperm + align256(static_cast<size_t>(T) * k * f * 2);
-    w.counters = w.part + align256(moek_gemv_partial_floats(T, k, d, f) * 4);
-    w.total = w.counters + align256(moek_gemv_counter_count(T, E, d, f) * 4);
-    return w;
-}
-
-}  // namespace
-
 size_t moe_ffn_workspace_bytes(int T, int k, int E, int d, int f) {
     if (T < 1 || k < 1 || E < 1 || d < 128 || f < 128) return 0;
-    return ws_layout(T, k, E, d, f).total;
+    return moek_gemv_workspace_bytes(T, k, d, f);
 }
 
 int moe_ffn(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
@@ -369,11 +349,9 @@ int moe_ffn(const void* x, const int32_t* perm, const int32_t* offsets, int T, i
                  "d must be a multiple of 256 and f a multiple of 128");
         need_device();
         if (T == 0) return;
-        const WsLayout L = ws_layout(T, k, E, d, f);
-        usage_if(workspace == nullptr || ws_bytes < L.total, "workspace too small (moe_ffn_workspace_bytes)");
-        char* base = static_cast<char*>(workspace);
-        GemvWorkspace ws{base + L.xperm, base + L.hperm, reinterpret_cast<float*>(base + L.part),
-                         reinterpret_cast<unsigned int*>(base + L.counters)};
+        usage_if(workspace == nullptr || ws_bytes < moek_gemv_workspace_bytes(T, k, d, f),
+                 "workspace too small (moe_ffn_workspace_bytes)");
+        const GemvWorkspace ws = moek_gemv_workspace_view(workspace, T, k, d, f);
         const uint64_t mask = E >= 64 ? ~0ull : ((1ull << E) - 1ull);
         const cudaError_t e = moek_ffn_mma(ws, x, perm, offsets, nullptr, nullptr, nullptr, T, k, experts, E, d, f,
                                            mask, nullptr, y_perm, false, st(stream));
@@ -561,6 +539,14 @@ int moe_engine_expert(const moe_engine* eng, int layer, int slot, moe_expert_wei
         int loc = 0;
         *out = eng->impl->expert(layer, slot, &loc);
         if (location) *location = loc;
+    });
+}
+
+int moe_debug_gemv_trace(void* buf) {
+    return guarded([&] {
+        need_device();
+        const cudaError_t e = moek_debug_gemv_trace(buf);
+        if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
     });
 }
 

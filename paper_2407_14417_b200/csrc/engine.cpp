@@ -74,6 +74,7 @@ struct MoeEngine::Impl {
     unsigned int* ticket = nullptr;
     float* y = nullptr;          // per-slot expert outputs (streamed-expert path)
     GemvWorkspace gws{};
+    void* gws_base = nullptr;
     int32_t* idx_host = nullptr;  // pinned [Tmax*K]
     size_t ws_bytes = 0;
 
@@ -181,14 +182,10 @@ struct MoeEngine::Impl {
         dev_alloc(reinterpret_cast<void**>(&inv), TK * 4);
         dev_alloc(reinterpret_cast<void**>(&ticket), 4);
         dev_alloc(reinterpret_cast<void**>(&y), TK * d * 4);
-        dev_alloc(&gws.xperm, static_cast<size_t>(Tmax) * d * 2);
-        dev_alloc(&gws.hperm, TK * f * 2);
-        const size_t nparts = moek_gemv_partial_floats(Tmax, K, d, f);
-        const size_t nctr = moek_gemv_counter_count(Tmax, E, d, f);
-        dev_alloc(reinterpret_cast<void**>(&gws.part), nparts * 4);
-        dev_alloc(reinterpret_cast<void**>(&gws.counters), nctr * 4);
-        ck(cudaMemsetAsync(gws.counters, 0, nctr * 4, compute), "memset");
-        ck(cudaMemsetAsync(gws.hperm, 0, TK * f * 2, compute), "memset");
+        const size_t ws_bytes = moek_gemv_workspace_bytes(Tmax, K, d, f);
+        dev_alloc(&gws_base, ws_bytes);
+        ck(cudaMemsetAsync(gws_base, 0, ws_bytes, compute), "memset");
+        gws = moek_gemv_workspace_view(gws_base, Tmax, K, d, f);
         ck(cudaMemsetAsync(ticket, 0, 4, compute), "memset");
         ck(cudaMemsetAsync(xin, 0, static_cast<size_t>(Tmax) * d * 2, compute), "memset");
         ck(cudaHostAlloc(reinterpret_cast<void**>(&idx_host), TK * 4, cudaHostAllocDefault), "cudaHostAlloc");
@@ -243,7 +240,7 @@ struct MoeEngine::Impl {
         if (compute) cudaStreamSynchronize(compute);
         if (copy) cudaStreamSynchronize(copy);
         void* devp[] = {dev_arena, swap, wg, xin, xout, xbuf[0], xbuf[1], idx, wts, counts, offsets, perm, inv, ticket, y,
-                         gws.xperm, gws.hperm, gws.part, gws.counters};
+                         gws_base};
         for (void* p : devp)
             if (p) cudaFree(p);
         if (host_arena) cudaFreeHost(host_arena);

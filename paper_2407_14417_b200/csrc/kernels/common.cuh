@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "moe_b200.h"
 
 #define MOE_DEVI __device__ __forceinline__
@@ -93,6 +95,14 @@ MOE_DEVI void decode_u8(uint32_t w, uint32_t& p01, uint32_t& p23, uint32_t& p45,
 }
 constexpr float kInt4Bias = 136.0f;  // 128 (magic) + 8 (storage bias)
 
+// Programmatic dependent launch (PDL): every kernel of a layer is launched
+// with programmatic stream serialization.  A kernel may read outputs of
+// kernels two or more launches back before pdl_wait() (each kernel triggers
+// its dependents only after its own pdl_wait(), so those are complete), and
+// must call pdl_wait() before reading its immediate predecessor's output.
+MOE_DEVI void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+MOE_DEVI void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 MOE_DEVI float warp_sum(float v) {
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -106,5 +116,23 @@ MOE_DEVI float silu_f(float g) { return g / (1.0f + expf(-g)); }
         cudaError_t err__ = (expr);                         \
         if (err__ != cudaSuccess) return err__;             \
     } while (0)
+
+// Host: launch with programmatic stream serialization (PDL edge to the
+// previous kernel in the stream; captured as a programmatic graph edge).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace moek

@@ -1,114 +1,116 @@
 // gemv.cu -- K3/K4 expert-FFN GEMV for decode batches (<= 8 tokens per
-// expert): int4-g128 and bf16 experts, mixed in one launch.
+// expert segment): int4-g128 and bf16 experts, mixed in one launch.
 //
 // Replaces the constant compute latency of the reference's MoE-layer
 // stand-in (simulator.cpp:31-32, :107) with the expert math of HF
 // MixtralExperts (modeling_mixtral.py:90-95).
 //
-// Weights live in HBM as 16-row x 128-K "fragment blocks" (oracle
-// orc_pack_*_blocks): one 128-bit load per lane per 512-byte block part gives
-// each lane exactly its mma.m16n8k16 A fragments, so every warp load is one
-// fully used 512-byte transaction.  int4 fragments are decoded in registers
-// (LOP3 magic-number -> bf16 128+u, one bf16x2 FMA -> q exactly); the tensor
-// core does the multiply-accumulate (fp32), the per-group scale is applied
-// after each 128-K group: y += s * sum(q*x), i.e. exact dequant values q*s.
-// Activations are read in the same K permutation (xperm / hperm) so the B
-// fragments are 128-bit loads too; up to 8 tokens of an expert share every
-// weight byte (the n=8 MMA columns).
+// Data path (B200):
+//   HBM --cp.async.bulk (TMA bulk copy, mbarrier complete_tx)--> per-warp
+//   shared-memory ring (3 stages x 8.25 KB) --LDS.128--> mma.m16n8k16 A
+//   fragments.  Each warp owns a contiguous range of equal-byte work items
+//   and keeps its next items in flight while computing the current one, so
+//   the bytes in flight per SM (up to 8 warps x 3 x 8 KB) do not depend on
+//   register pressure.
+// Weights are stored as 16-row x 128-K "fragment blocks" (oracle
+// orc_pack_*_blocks): a work item (16-row tile, K-part) is one contiguous
+// span of blocks (one bulk copy), and a lane's 16-byte smem read is exactly
+// its A fragment.  int4 fragments are decoded in registers (LOP3 magic
+// number -> bf16 128+u, one bf16x2 FMA -> q exactly); the tensor core does
+// the multiply-accumulate in fp32 and the group scale is applied after each
+// 128-K group, y += s * sum(q*x) -- the exact dequant values q*s.  B
+// fragments (x or h) come from a K-permuted copy (xperm / hperm) with the
+// same 128-bit pattern.  Up to 8 tokens of an expert share each weight byte.
 //
-// Work decomposition: items = (segment, 16-row tile, K-part) with K-parts of
-// equal bytes (int4: 8 groups, bf16: 2 groups).  The item space is cut into
-// equal contiguous ranges, one per warp of a persistent grid; a warp
-// accumulates consecutive K-parts of a row tile in registers ("runs") and
-// writes one fp32 partial per run.  Per-tile arrival counters elect the last
-// warp, which reduces the runs in fixed K order (deterministic) and runs the
-// fused epilogue: SwiGLU + bf16 rounding of h (gate/up pass) or the
-// routing-weighted combine + residual (down pass).
+// Split-K bookkeeping: a warp accumulates consecutive K-parts of a row tile
+// in registers ("run") and adds one fp32 partial into a zero-initialised
+// slot per run; per-tile counters count finished items, and the warp that
+// completes a tile reduces its K-part slots in fixed order (deterministic),
+// re-zeroes them, and runs the fused epilogue: SwiGLU + bf16 h (gate/up
+// pass) or routing-weighted combine + residual (down pass).
 #include "common.cuh"
 #include "launch.h"
 
 namespace moek {
 
-constexpr int kGemvThreads = 256;
-constexpr int kGemvWarps = kGemvThreads / 32;
-constexpr int kTile = 8;      // tokens per segment tile (MMA n)
-constexpr int kMaxSegs = 256;
+constexpr int kWarps = 12;
+constexpr int kThreads = kWarps * 32;
+constexpr int kStages = 2;
+constexpr int kStageBytes = 8192 + 256;  // 8 KB of weights + int4 scales
+constexpr int kTile = 8;                 // tokens per segment tile (MMA n)
+constexpr int kMaxSegs = 128;
 
 struct GemvArgs {
     const int32_t* offsets;   // [E+1]
     const int32_t* perm;      // [T*k]: slot -> t*k + j
     int T, k, E;
-    int rows, K;              // matrix rows / columns
+    int kshift;               // log2(k)
+    int rows, K;              // matrix rows / columns of this pass
     int down;                 // 0 gate/up pass, 1 down pass
-    int gk4, gk16;            // groups per K-part (int4, bf16)
+    int gk4, gk16;            // 128-K groups per item (int4, bf16)
     const uint16_t* bperm;    // B operand, K-permuted: [T][K] (gate/up) or [T*k][K] (down)
-    float* part;              // partial sums [kp_stride][T*k][rows]
-    int kp_stride;
-    unsigned int* counters;   // arrival counters (zeroed; reset by the last arriver)
-    // gate/up epilogue
-    uint16_t* hperm;          // [T*k][f] K-permuted h
+    const float* bsum;        // per-(B row, 128-group) sums of B: [rows of B][K/128]
+    float* part;              // zeroed partial slots [KPmax][T*k][rows]
+    unsigned int* counters;   // zeroed arrival counters
+    unsigned int* gcounters;  // zeroed per-(segment, h group) counters (gate/up)
+    uint16_t* hperm;          // gate/up epilogue output [T*k][f] (K-permuted)
+    float* hsum16;            // gate/up epilogue: sums of 16 h rows [T*k][f/16]
+    float* hsum;              // gate/up epilogue: sums of 128 h rows [T*k][f/128]
     int f;
-    // down epilogue
-    const float* wts;         // [T*k] routing weights
+    const float* wts;         // down epilogue: routing weights [T*k]
     const int32_t* inv;       // [T*k]
     const uint16_t* resid;    // [T][d] or null
-    uint16_t* out;            // [T][d]; null -> write y
-    float* y;                 // [T*k][d] (when out == null)
+    uint16_t* out;            // [T][d]; null -> write y per slot
+    float* y;                 // [T*k][d]
     uint64_t active_mask;
     moe_expert_weights ex[MOE_MAX_EXPERTS];
 };
 
 struct SegTable {
     int n;
+    int items_per_rt;         // sum over segments of KP (down-pass tile total)
     int e[kMaxSegs];
     int tile[kMaxSegs];
     int kp[kMaxSegs];
+    int gk[kMaxSegs];
     long long pre[kMaxSegs + 1];
 };
 
-MOE_DEVI int ktile_groups(const GemvArgs& a, int prec) { return prec == MOE_P4 ? a.gk4 : a.gk16; }
-
-// Segments = (expert, tile of <= 8 tokens) of the active experts, in expert
-// order; items per segment = (rows/16) * KP.
-MOE_DEVI void build_segs(const GemvArgs& a, SegTable& st) {
-    if (threadIdx.x == 0) {
-        const int RT = a.rows / 16, G = a.K / 128;
-        int n = 0;
-        long long acc = 0;
-        for (int e = 0; e < a.E; ++e) {
-            if (!((a.active_mask >> e) & 1ull)) continue;
-            const int m = a.offsets[e + 1] - a.offsets[e];
-            const int kp = G / ktile_groups(a, a.ex[e].precision);
-            for (int t = 0; t * kTile < m && n < kMaxSegs; ++t) {
-                st.e[n] = e;
-                st.tile[n] = t;
-                st.kp[n] = kp;
-                st.pre[n] = acc;
-                acc += static_cast<long long>(RT) * kp;
-                ++n;
-            }
-        }
-        st.pre[n] = acc;
-        st.n = n;
-    }
-    __syncthreads();
+// ---- PTX wrappers: mbarrier + bulk async copy ------------------------------
+MOE_DEVI uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+MOE_DEVI void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-
-MOE_DEVI long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
-
-// Number of runs covering item range [lo, hi) when N items are cut into W
-// equal ranges start(w) = floor(w*N/W).
-MOE_DEVI int runs_in(long long lo, long long hi, long long N, long long W) {
-    return 1 + static_cast<int>(ceil_div(hi * W, N) - ceil_div((lo + 1) * W, N));
+MOE_DEVI void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
 }
-
-MOE_DEVI bool is_run_start(long long i, long long lo, long long N, long long W) {
-    if (i == lo) return true;
-    const long long w = ceil_div(i * W, N);
-    return w < W && (w * N) / W == i;
+MOE_DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
-
-MOE_DEVI uint4 ld_b(const uint16_t* p) { return *reinterpret_cast<const uint4*>(p); }
+MOE_DEVI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+MOE_DEVI void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// Release-only arrival: orders this warp's partial stores (after __syncwarp)
+// before the counter update without the L1 invalidation a full gpu-scope
+// fence costs; only the completing warp pays the acquire fence.
+MOE_DEVI unsigned int atom_add_release(unsigned int* p, unsigned int v) {
+    unsigned int old;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+MOE_DEVI void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 MOE_DEVI void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                        uint32_t b1) {
@@ -119,79 +121,116 @@ MOE_DEVI void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uin
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// exact q (bf16x2) from a packed word: four pairs for MMAs kk=2q (p01, p23)
-// and kk=2q+1 (p45, p67)
-MOE_DEVI void decode_q(uint32_t w, uint32_t& p01, uint32_t& p23, uint32_t& p45, uint32_t& p67) {
-    constexpr uint32_t one2 = 0x3F803F80u, m136 = 0xC308C308u;
-    p01 = hfma2_bf16(and_or(w, 0x000F000Fu, 0x43004300u), one2, m136);
-    p23 = hfma2_bf16(and_or(w >> 4, 0x000F000Fu, 0x43004300u), one2, m136);
-    p45 = hfma2_bf16(and_or(w >> 8, 0x000F000Fu, 0x43004300u), one2, m136);
-    p67 = hfma2_bf16(and_or(w >> 12, 0x000F000Fu, 0x43004300u), one2, m136);
+// Optional per-warp phase trace (moe_debug_gemv_trace): globaltimer stamps
+// [entry, after pdl_wait, first item ready, loop end] + item / run / epilogue
+// counts, 8 x u64 per warp.  Null (the default) costs one branch per warp.
+__device__ unsigned long long* g_gemv_trace = nullptr;
+MOE_DEVI unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
-// One int4 item: GK groups of a 16-row tile, C += sum_g s_g * (A_g . B_g).
-template <int GKMAX>
-MOE_DEVI void item_int4(const uint8_t* wblk, const uint16_t* sblk, int gk, const uint16_t* bp, bool bvalid,
-                        int lane, float (&acc)[4]) {
-    uint4 wq[GKMAX][2];
-    uint32_t sc[GKMAX];
+MOE_DEVI uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
+MOE_DEVI uint4 ldb(const uint16_t* p) { return *reinterpret_cast<const uint4*>(p); }
+
+// B fragments of one 128-K group: 4 x 16 B of this lane's token row
+MOE_DEVI void load_b(uint4 (&b)[4], const uint16_t* bp, bool valid) {
 #pragma unroll
-    for (int g = 0; g < GKMAX; ++g) {
-        if (g < gk) {
-            wq[g][0] = ld_stream(wblk + static_cast<size_t>(g) * 1024 + lane * 16);
-            wq[g][1] = ld_stream(wblk + static_cast<size_t>(g) * 1024 + 512 + lane * 16);
-            sc[g] = __ldg(reinterpret_cast<const uint32_t*>(sblk + static_cast<size_t>(g) * 16) + (lane >> 2));
-        }
-    }
+    for (int c = 0; c < 4; ++c) b[c] = valid ? ldb(bp + c * 8) : make_uint4(0, 0, 0, 0);
+}
+
+// biased bf16 pairs (128+u) from a packed word (3 SHF + 4 LOP3, no FMA):
+// pairs for MMA kk=2q (p01 reg0, p23 reg2) and kk=2q+1 (p45, p67)
+MOE_DEVI void decode_u(uint32_t w, uint32_t& p01, uint32_t& p23, uint32_t& p45, uint32_t& p67) {
+    p01 = and_or(w, 0x000F000Fu, 0x43004300u);
+    p23 = and_or(w >> 4, 0x000F000Fu, 0x43004300u);
+    p45 = and_or(w >> 8, 0x000F000Fu, 0x43004300u);
+    p67 = and_or(w >> 12, 0x000F000Fu, 0x43004300u);
+}
+
+// One int4 item (gk 128-K groups).  The MMA sees the biased values 128+u
+// (exact in bf16); per group sum(q x) = sum((128+u) x) - 136 sum(x), with
+// sum(x) of the column's activation group (scol0: column 2t, scol1: 2t+1),
+// then y += s * sum(q x) (two independent HMMA chains per group).
+MOE_DEVI void item_int4(const uint8_t* stage, int gk, const uint16_t* bp, bool bvalid, const float* scol0,
+                        const float* scol1, int g0, int lane, float (&acc)[4]) {
     const int t = lane & 3;
+    const uint8_t* sc = stage + gk * 1024;
+    float sv0[8], sv1[8];
 #pragma unroll
-    for (int g = 0; g < GKMAX; ++g) {
+    for (int g = 0; g < 8; ++g) {
+        sv0[g] = (scol0 && g < gk) ? __ldg(scol0 + g0 + g) : 0.0f;
+        sv1[g] = (scol1 && g < gk) ? __ldg(scol1 + g0 + g) : 0.0f;
+    }
+    uint4 ba[4], bb[4];
+    load_b(ba, bp + t * 32, bvalid);
+#pragma unroll
+    for (int g = 0; g < 8; g += 2) {
         if (g >= gk) break;
-        uint4 b[4];
+        // ping-pong B buffers (no register copies): ba = group g, bb = g+1
+        if (g + 1 < gk) load_b(bb, bp + (g + 1) * 128 + t * 32, bvalid);
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-            b[c] = bvalid ? ld_b(bp + static_cast<size_t>(g) * 128 + t * 32 + c * 8) : make_uint4(0, 0, 0, 0);
-        float cg[4] = {0.f, 0.f, 0.f, 0.f};
-        const uint32_t lo[4] = {wq[g][0].x, wq[g][0].y, wq[g][0].z, wq[g][0].w};
-        const uint32_t hi[4] = {wq[g][1].x, wq[g][1].y, wq[g][1].z, wq[g][1].w};
+        for (int h = 0; h < 2; ++h) {
+            const int gg = g + h;
+            if (gg >= gk) break;
+            const uint4(&b)[4] = h == 0 ? ba : bb;
+            const uint32_t s2 = *reinterpret_cast<const uint32_t*>(sc + gg * 32 + (lane >> 2) * 4);
+            const float S0 = sv0[gg], S1 = sv1[gg];
+            const uint4 wl = lds128(stage + gg * 1024 + lane * 16);
+            const uint4 wh = lds128(stage + gg * 1024 + 512 + lane * 16);
+            const uint32_t lo[4] = {wl.x, wl.y, wl.z, wl.w};
+            const uint32_t hi[4] = {wh.x, wh.y, wh.z, wh.w};
+            float cg[4] = {0.f, 0.f, 0.f, 0.f}, ch[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint32_t r0, r2, r0b, r2b, s0, s2, s0b, s2b;
-            decode_q(lo[q], r0, r2, r0b, r2b);   // row gr
-            decode_q(hi[q], s0, s2, s0b, s2b);   // row gr+8
-            mma_bf16(cg, r0, s0, r2, s2, b[q].x, b[q].y);
-            mma_bf16(cg, r0b, s0b, r2b, s2b, b[q].z, b[q].w);
+            for (int q = 0; q < 4; ++q) {
+                uint32_t r0, r2, r0b, r2b, s0, sq2, s0b, s2b;
+                decode_u(lo[q], r0, r2, r0b, r2b);   // row gr
+                decode_u(hi[q], s0, sq2, s0b, s2b);  // row gr+8
+                mma_bf16(cg, r0, s0, r2, sq2, b[q].x, b[q].y);
+                mma_bf16(ch, r0b, s0b, r2b, s2b, b[q].z, b[q].w);
+            }
+            const float s_lo = bf16_lo(s2), s_hi = bf16_hi(s2);
+            acc[0] = __fmaf_rn(s_lo, __fmaf_rn(-kInt4Bias, S0, cg[0] + ch[0]), acc[0]);
+            acc[1] = __fmaf_rn(s_lo, __fmaf_rn(-kInt4Bias, S1, cg[1] + ch[1]), acc[1]);
+            acc[2] = __fmaf_rn(s_hi, __fmaf_rn(-kInt4Bias, S0, cg[2] + ch[2]), acc[2]);
+            acc[3] = __fmaf_rn(s_hi, __fmaf_rn(-kInt4Bias, S1, cg[3] + ch[3]), acc[3]);
+            if (h == 0 && g + 2 < gk) load_b(ba, bp + (g + 2) * 128 + t * 32, bvalid);
         }
-        const float s_lo = bf16_lo(sc[g]), s_hi = bf16_hi(sc[g]);
-        acc[0] = __fmaf_rn(s_lo, cg[0], acc[0]);
-        acc[1] = __fmaf_rn(s_lo, cg[1], acc[1]);
-        acc[2] = __fmaf_rn(s_hi, cg[2], acc[2]);
-        acc[3] = __fmaf_rn(s_hi, cg[3], acc[3]);
     }
 }
 
-// One bf16 item: GK groups, A fragments straight from memory.
-template <int GKMAX>
-MOE_DEVI void item_bf16(const uint8_t* wblk, int gk, const uint16_t* bp, bool bvalid, int lane,
-                        float (&acc)[4]) {
-    uint4 wv[GKMAX][8];
-#pragma unroll
-    for (int g = 0; g < GKMAX; ++g)
-        if (g < gk)
-#pragma unroll
-            for (int p = 0; p < 8; ++p) wv[g][p] = ld_stream(wblk + static_cast<size_t>(g) * 4096 + p * 512 + lane * 16);
+MOE_DEVI void item_bf16(const uint8_t* stage, int gk, const uint16_t* bp, bool bvalid, int lane, float (&acc)[4]) {
     const int t = lane & 3;
+    float c1[4] = {0.f, 0.f, 0.f, 0.f};  // second chain (odd kk)
+    uint4 ba[4], bb[4];
+    load_b(ba, bp + t * 32, bvalid);
+    for (int g = 0; g < gk; g += 2) {
+        if (g + 1 < gk) load_b(bb, bp + (g + 1) * 128 + t * 32, bvalid);
 #pragma unroll
-    for (int g = 0; g < GKMAX; ++g) {
-        if (g >= gk) break;
+        for (int h = 0; h < 2; ++h) {
+            const int gg = g + h;
+            if (gg >= gk) break;
+            const uint4(&b)[4] = h == 0 ? ba : bb;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const uint4 b = bvalid ? ld_b(bp + static_cast<size_t>(g) * 128 + t * 32 + c * 8) : make_uint4(0, 0, 0, 0);
-            // part c = row gr words for kk=2c,2c+1; part 4+c = row gr+8
-            mma_bf16(acc, wv[g][c].x, wv[g][4 + c].x, wv[g][c].y, wv[g][4 + c].y, b.x, b.y);
-            mma_bf16(acc, wv[g][c].z, wv[g][4 + c].z, wv[g][c].w, wv[g][4 + c].w, b.z, b.w);
+            for (int c = 0; c < 4; ++c) {
+                // part c = row gr words for kk = 2c, 2c+1; part 4+c = row gr+8
+                const uint4 lo = lds128(stage + gg * 4096 + c * 512 + lane * 16);
+                const uint4 hi = lds128(stage + gg * 4096 + (4 + c) * 512 + lane * 16);
+                mma_bf16(acc, lo.x, hi.x, lo.y, hi.y, b[c].x, b[c].y);
+                mma_bf16(c1, lo.z, hi.z, lo.w, hi.w, b[c].z, b[c].w);
+            }
+            if (h == 0 && g + 2 < gk) load_b(ba, bp + (g + 2) * 128 + t * 32, bvalid);
         }
     }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) acc[r] += c1[r];
+}
+
+// token of a permutation slot (perm[slot] = t*k + j); k is a power of two in
+// every config we run, so this is a shift (division otherwise)
+MOE_DEVI int tok_of_slot(const GemvArgs& a, int slot) {
+    return a.kshift >= 0 ? a.perm[slot] >> a.kshift : a.perm[slot] / a.k;
 }
 
 // K-permuted position of natural index n (orc_perm_k)
@@ -200,16 +239,59 @@ MOE_DEVI int perm_k(int n) {
     return (n & ~127) + ((kin & 7) >> 1) * 32 + (kin >> 4) * 4 + ((kin >> 3) & 1) * 2 + (kin & 1);
 }
 
-// reduce the fp32 partial runs of (segment s, row) for one slot
-MOE_DEVI float reduce_runs(const GemvArgs& a, const SegTable& st, int s, int rt, int row, int slot,
-                           long long N, long long W) {
-    const int KP = st.kp[s];
-    const long long lo = st.pre[s] + static_cast<long long>(rt) * KP;
+MOE_DEVI void build_segs(const GemvArgs& a, SegTable& st, int* cnt) {
+    // expert token counts read in parallel (one L2 round trip), then a short
+    // serial pass over <= 64 experts in shared memory
+    if (threadIdx.x < a.E)
+        cnt[threadIdx.x] = ((a.active_mask >> threadIdx.x) & 1ull)
+                               ? a.offsets[threadIdx.x + 1] - a.offsets[threadIdx.x]
+                               : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int RT = a.rows / 16, G = a.K / 128;
+        int n = 0, items_rt = 0;
+        long long acc = 0;
+        for (int e = 0; e < a.E; ++e) {
+            const int m = cnt[e];
+            if (m == 0) continue;
+            const int gk = a.ex[e].precision == MOE_P4 ? a.gk4 : a.gk16;
+            const int kp = G / gk;
+            for (int t = 0; t * kTile < m && n < kMaxSegs; ++t) {
+                st.e[n] = e;
+                st.tile[n] = t;
+                st.kp[n] = kp;
+                st.gk[n] = gk;
+                st.pre[n] = acc;
+                acc += static_cast<long long>(RT) * kp;
+                items_rt += kp;
+                ++n;
+            }
+        }
+        st.pre[n] = acc;
+        st.n = n;
+        st.items_per_rt = items_rt;
+    }
+    __syncthreads();
+}
+
+// reduce + re-zero the K-part slots of (row, slot)
+MOE_DEVI float take_partial(const GemvArgs& a, int kp_count, int row, int slot) {
     const int nslots = a.T * a.k;
+    const size_t stride = static_cast<size_t>(nslots) * a.rows;
+    float* base = a.part + static_cast<size_t>(slot) * a.rows + row;
     float v = 0.0f;
-    for (int kp = 0; kp < KP; ++kp)
-        if (is_run_start(lo + kp, lo, N, W))
-            v += __ldcg(a.part + (static_cast<size_t>(kp) * nslots + slot) * a.rows + row);
+    for (int kp = 0; kp < kp_count; kp += 8) {
+        float x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = kp + u < kp_count ? __ldcg(base + (kp + u) * stride) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (x[u] != 0.0f) {
+                v += x[u];
+                __stcg(base + (kp + u) * stride, 0.0f);
+            }
+        }
+    }
     return v;
 }
 
@@ -222,32 +304,60 @@ MOE_DEVI int seg_of_slot(const GemvArgs& a, const SegTable& st, int slot) {
     return -1;
 }
 
-// gate/up epilogue for pair tile prt of segment s: h = bf16(silu(g) * u)
-MOE_DEVI void epilogue_gateup(const GemvArgs& a, const SegTable& st, int s, int prt, long long N, long long W,
-                              int lane) {
+// SwiGLU for the 16 rows of pair tile prt and every token of segment s, plus
+// the activation-group sums the int4 down pass needs: sum of the 16 rounded
+// h values (fixed xor-butterfly order), and -- by the last of the 8 pair
+// tiles of a 128-row group -- their fixed-order total.
+MOE_DEVI void epilogue_gateup(const GemvArgs& a, const SegTable& st, int s, int prt, int lane) {
     const int e = st.e[s];
     const int slot0 = a.offsets[e] + st.tile[s] * kTile;
     const int m_cnt = min(kTile, a.offsets[e + 1] - slot0);
-    const int ftiles = a.f / 16;
-    for (int i = lane; i < m_cnt * 16; i += 32) {
-        const int m = i >> 4, rr = i & 15;
-        const int n = prt * 16 + rr, slot = slot0 + m;
-        const float g = reduce_runs(a, st, s, prt, n, slot, N, W);
-        const float u = reduce_runs(a, st, s, prt + ftiles, a.f + n, slot, N, W);
-        a.hperm[static_cast<size_t>(slot) * a.f + perm_k(n)] = f2bf(silu_f(g) * u);
+    const int f16 = a.f / 16, f128 = a.f / 128;
+    for (int i0 = 0; i0 < m_cnt * 16; i0 += 32) {
+        const int i = i0 + lane;
+        const int m = i >> 4, n = prt * 16 + (i & 15), slot = slot0 + m;
+        float hv = 0.0f;
+        if (i < m_cnt * 16) {
+            const float g = take_partial(a, st.kp[s], n, slot);
+            const float u = take_partial(a, st.kp[s], a.f + n, slot);
+            const uint16_t hb = f2bf(silu_f(g) * u);
+            a.hperm[static_cast<size_t>(slot) * a.f + perm_k(n)] = hb;
+            hv = bf2f(hb);
+        }
+        // sum over the 16 rows held by each half-warp
+#pragma unroll
+        for (int off = 8; off >= 1; off >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, off);
+        if ((lane & 15) == 0 && i < m_cnt * 16) __stcg(a.hsum16 + static_cast<size_t>(slot) * f16 + prt, hv);
+    }
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+        unsigned int* ctr = a.gcounters + static_cast<size_t>(s) * f128 + prt / 8;
+        if (atom_add_release(ctr, 1u) + 1 == 8u) {
+            *ctr = 0;
+            last = 1;
+        }
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+        const int g = prt / 8;
+        for (int m = lane; m < m_cnt; m += 32) {
+            const float* p = a.hsum16 + static_cast<size_t>(slot0 + m) * f16 + g * 8;
+            float v = 0.0f;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) v += __ldcg(p + r);
+            a.hsum[static_cast<size_t>(slot0 + m) * f128 + g] = v;
+        }
     }
 }
 
-// down epilogue for row tile rt: y per slot (reduced runs), then combine
-MOE_DEVI void epilogue_down(const GemvArgs& a, const SegTable& st, int rt, long long N, long long W, int lane) {
+MOE_DEVI void epilogue_down(const GemvArgs& a, const SegTable& st, int rt, int lane) {
     const int d = a.rows;
     if (a.out == nullptr) {
-        const int nslots = a.T * a.k;
-        for (int i = lane; i < nslots * 16; i += 32) {
+        for (int i = lane; i < a.T * a.k * 16; i += 32) {
             const int slot = i >> 4, j = rt * 16 + (i & 15);
             const int s = seg_of_slot(a, st, slot);
-            if (s < 0) continue;
-            a.y[static_cast<size_t>(slot) * d + j] = reduce_runs(a, st, s, rt, j, slot, N, W);
+            if (s >= 0) a.y[static_cast<size_t>(slot) * d + j] = take_partial(a, st.kp[s], j, slot);
         }
         return;
     }
@@ -257,209 +367,358 @@ MOE_DEVI void epilogue_down(const GemvArgs& a, const SegTable& st, int rt, long 
         for (int jj = 0; jj < a.k; ++jj) {
             const int slot = a.inv[t * a.k + jj];
             const int s = seg_of_slot(a, st, slot);
-            const float yv = s < 0 ? 0.0f : reduce_runs(a, st, s, rt, j, slot, N, W);
+            const float yv = s < 0 ? 0.0f : take_partial(a, st.kp[s], j, slot);
             accv = __fmaf_rn(a.wts[t * a.k + jj], yv, accv);
         }
         a.out[static_cast<size_t>(t) * d + j] = f2bf(accv);
     }
 }
 
-template <int GK4, int GK16>
-__global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const __grid_constant__ GemvArgs a) {
+struct ItemIt {
+    int s, rt, kp;
+};
+
+MOE_DEVI void advance(ItemIt& it, const SegTable& st, int RT) {
+    if (++it.kp == st.kp[it.s]) {
+        it.kp = 0;
+        if (++it.rt == RT) {
+            it.rt = 0;
+            ++it.s;
+        }
+    }
+}
+
+MOE_DEVI ItemIt locate(long long i, const SegTable& st) {
+    ItemIt it{0, 0, 0};
+    while (st.pre[it.s + 1] <= i) ++it.s;
+    const long long local = i - st.pre[it.s];
+    it.rt = static_cast<int>(local / st.kp[it.s]);
+    it.kp = static_cast<int>(local - static_cast<long long>(it.rt) * st.kp[it.s]);
+    return it;
+}
+
+// issue the bulk copies of one item into a ring stage (lane 0 only)
+MOE_DEVI void issue_item(const GemvArgs& a, const SegTable& st, const ItemIt& it, uint8_t* stage, uint64_t* bar) {
+    const moe_expert_weights& W = a.ex[st.e[it.s]];
+    const int G = a.K / 128, gk = st.gk[it.s];
+    const size_t blk = static_cast<size_t>(it.rt) * G + static_cast<size_t>(it.kp) * gk;
+    const uint8_t* w = static_cast<const uint8_t*>(a.down ? W.w_down : W.w_gate_up);
+    if (W.precision == MOE_P4) {
+        const uint8_t* sc = static_cast<const uint8_t*>(a.down ? W.s_down : W.s_gate_up);
+        mbar_expect_tx(bar, gk * 1024 + gk * 32);
+        bulk_g2s(stage, w + blk * 1024, gk * 1024, bar);
+        bulk_g2s(stage + gk * 1024, sc + blk * 32, gk * 32, bar);
+    } else {
+        mbar_expect_tx(bar, gk * 4096);
+        bulk_g2s(stage, w + blk * 4096, gk * 4096, bar);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) gemv_kernel(const __grid_constant__ GemvArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
     __shared__ SegTable st;
-    build_segs(a, st);
-    const int lane = threadIdx.x & 31;
-    const long long W = static_cast<long long>(gridDim.x) * kGemvWarps;
-    const long long wid = static_cast<long long>(blockIdx.x) * kGemvWarps + (threadIdx.x >> 5);
-    const long long N = st.pre[st.n];
-    if (N == 0) return;
-    long long i = wid * N / W;
-    const long long i_end = (wid + 1) * N / W;
-    if (i >= i_end) return;
+    __shared__ __align__(8) uint64_t bars[kWarps][kStages];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* ring = smem + static_cast<size_t>(warp) * kStages * kStageBytes;
+    if (lane == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[warp][s], 1);
+        fence_mbar_init();
+    }
+    __shared__ int cnt[MOE_MAX_EXPERTS];
+    // Routing (offsets) comes from the route kernel two launches back, so the
+    // segment table and the first weight bulk copies are issued before the
+    // PDL wait -- weight streaming overlaps the predecessor's tail.
+    const unsigned long long t_entry = gtimer();
+    build_segs(a, st, cnt);  // contains __syncthreads
+    const int N = static_cast<int>(st.pre[st.n]);
+    const int W = static_cast<int>(gridDim.x) * kWarps;
+    const int wid = static_cast<int>(blockIdx.x) * kWarps + warp;
+    // equal contiguous ranges: q items each, the first r warps one more
+    const int q = N / W, r = N - q * W;
+    const long long i0 = static_cast<long long>(wid) * q + min(wid, r);
+    const long long i1 = i0 + q + (wid < r ? 1 : 0);
+    const int RT = a.rows / 16;
     const int nslots = a.T * a.k;
     const int gr = lane >> 2, t = lane & 3;
-    const int G = a.K / 128;
-    const int RT = a.rows / 16;
-    int s = 0;
-    while (st.pre[s + 1] <= i) ++s;
 
-    while (i < i_end) {
+    // prologue: fill the ring (weights only: independent of the predecessor)
+    ItemIt issue_it{0, 0, 0};
+    long long issued = i0;
+    if (i0 < i1) {
+        issue_it = locate(i0, st);
+        for (int s = 0; s < kStages && issued < i1; ++s, ++issued) {
+            if (lane == 0) issue_item(a, st, issue_it, ring + s * kStageBytes, &bars[warp][s]);
+            advance(issue_it, st, RT);
+        }
+    }
+    pdl_wait();     // B operand / counters / partials of the predecessor
+    pdl_trigger();
+    if (i0 >= i1) return;
+    const unsigned long long t_wait = gtimer();
+    unsigned long long t_first = 0;
+    int n_runs = 0, n_epi = 0;
+
+    ItemIt it = locate(i0, st);
+    long long i = i0;
+    uint32_t phase_bits = 0;  // per-stage parity
+    int stage = 0;
+    while (i < i1) {
+        const int s = it.s, rt = it.rt;
         const int e = st.e[s];
-        const moe_expert_weights& Wt = a.ex[e];
-        const int prec = Wt.precision;
-        const int KP = st.kp[s];
-        const int gk = G / KP;
-        const long long local = i - st.pre[s];
-        const int rt = static_cast<int>(local / KP);
-        int kp = static_cast<int>(local - static_cast<long long>(rt) * KP);
-        const int kp0 = kp;
+        const int prec = a.ex[e].precision;
+        const int gk = st.gk[s];
+        const int kp0 = it.kp;
         const int slot0 = a.offsets[e] + st.tile[s] * kTile;
         const int m_cnt = min(kTile, a.offsets[e + 1] - slot0);
-        // B row for this lane's MMA column gr
         const bool bvalid = gr < m_cnt;
         int brow = 0;
-        if (bvalid) brow = a.down ? slot0 + gr : a.perm[slot0 + gr] / a.k;
+        if (bvalid) brow = a.down ? slot0 + gr : tok_of_slot(a, slot0 + gr);
         const uint16_t* brow_p = a.bperm + static_cast<size_t>(brow) * a.K;
-        const uint8_t* wbase = static_cast<const uint8_t*>(a.down ? Wt.w_down : Wt.w_gate_up);
-        const uint16_t* sbase = static_cast<const uint16_t*>(a.down ? Wt.s_down : Wt.s_gate_up);
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (; kp < KP && i < i_end; ++kp, ++i) {
-            const size_t blk = static_cast<size_t>(rt) * G + static_cast<size_t>(kp) * gk;
-            const uint16_t* bp = brow_p + static_cast<size_t>(kp) * gk * 128;
-            if (prec == MOE_P4)
-                item_int4<GK4>(wbase + blk * 1024, sbase + blk * 16, gk, bp, bvalid, lane, acc);
-            else
-                item_bf16<GK16>(wbase + blk * 4096, gk, bp, bvalid, lane, acc);
+        // activation-group sums of this lane's two C columns (int4 bias)
+        const int G = a.K / 128;
+        const float* scol[2] = {nullptr, nullptr};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int n = 2 * t + c;
+            if (n < m_cnt) {
+                const int rb = a.down ? slot0 + n : tok_of_slot(a, slot0 + n);
+                scol[c] = a.bsum + static_cast<size_t>(rb) * G;
+            }
         }
-        // flush the run: C columns 2t, 2t+1 = tokens of the tile; rows gr, gr+8
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        int run_len = 0;
+        // one run: consecutive K-parts of (s, rt) within this warp's range
+        while (i < i1 && it.s == s && it.rt == rt) {
+            mbar_wait(&bars[warp][stage], (phase_bits >> stage) & 1u);
+            if (t_first == 0) t_first = gtimer();
+            phase_bits ^= 1u << stage;
+            const uint8_t* sp = ring + stage * kStageBytes;
+            const uint16_t* bp = brow_p + static_cast<size_t>(it.kp) * gk * 128;
+            if (prec == MOE_P4)
+                item_int4(sp, gk, bp, bvalid, scol[0], scol[1], it.kp * gk, lane, acc);
+            else
+                item_bf16(sp, gk, bp, bvalid, lane, acc);
+            // release the stage and refill it with the item kStages ahead
+            fence_proxy_async();
+            __syncwarp();
+            if (issued < i1) {
+                if (lane == 0) issue_item(a, st, issue_it, ring + stage * kStageBytes, &bars[warp][stage]);
+                advance(issue_it, st, RT);
+                ++issued;
+            }
+            stage = stage + 1 == kStages ? 0 : stage + 1;
+            advance(it, st, RT);
+            ++i;
+            ++run_len;
+        }
+        // flush the run into its (zeroed) K-part slot: columns 2t, 2t+1
         const int row = rt * 16 + gr;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const int m = 2 * t + c;
             if (m < m_cnt) {
                 float* p = a.part + (static_cast<size_t>(kp0) * nslots + slot0 + m) * a.rows;
-                p[row] = acc[c];
-                p[row + 8] = acc[2 + c];
+                __stcg(p + row, acc[c]);
+                __stcg(p + row + 8, acc[2 + c]);
             }
         }
-        __threadfence();
         __syncwarp();
-        // arrival
         int last = 0;
         if (lane == 0) {
+            unsigned int* ctr;
+            unsigned int total;
             if (!a.down) {
                 const int ftiles = a.f / 16;
-                const int prt = rt % ftiles;
-                const long long lo_g = st.pre[s] + static_cast<long long>(prt) * KP;
-                const long long lo_u = st.pre[s] + static_cast<long long>(prt + ftiles) * KP;
-                const int need = runs_in(lo_g, lo_g + KP, N, W) + runs_in(lo_u, lo_u + KP, N, W);
-                unsigned int* ctr = a.counters + static_cast<size_t>(s) * ftiles + prt;
-                if (atomicAdd(ctr, 1u) + 1 == static_cast<unsigned>(need)) {
-                    *ctr = 0;
-                    last = 1;
-                }
+                ctr = a.counters + static_cast<size_t>(s) * ftiles + (rt >= ftiles ? rt - ftiles : rt);
+                total = 2u * static_cast<unsigned>(st.kp[s]);
             } else {
-                int need = 0;
-                for (int ss = 0; ss < st.n; ++ss) {
-                    const long long lo = st.pre[ss] + static_cast<long long>(rt) * st.kp[ss];
-                    need += runs_in(lo, lo + st.kp[ss], N, W);
-                }
-                unsigned int* ctr = a.counters + rt;
-                if (atomicAdd(ctr, 1u) + 1 == static_cast<unsigned>(need)) {
-                    *ctr = 0;
-                    last = 1;
-                }
+                ctr = a.counters + rt;
+                total = static_cast<unsigned>(st.items_per_rt);
+            }
+            // The completing warp reads the partials with L2-coherent ld.cg
+            // after observing the final count (no L1-invalidating acquire
+            // fence: every value it reads was written by other SMs to L2).
+            if (atom_add_release(ctr, static_cast<unsigned>(run_len)) + run_len == total) {
+                *ctr = 0;
+                last = 1;
             }
         }
         last = __shfl_sync(0xffffffffu, last, 0);
+        ++n_runs;
         if (last) {
-            __threadfence();
+            ++n_epi;
             if (!a.down)
-                epilogue_gateup(a, st, s, rt % (a.f / 16), N, W, lane);
+                epilogue_gateup(a, st, s, rt >= a.f / 16 ? rt - a.f / 16 : rt, lane);
             else
-                epilogue_down(a, st, rt, N, W, lane);
+                epilogue_down(a, st, rt, lane);
         }
-        if (i < i_end && i >= st.pre[s + 1]) ++s;
-        (void)RT;
+    }
+    unsigned long long* tr = g_gemv_trace;
+    if (tr != nullptr && lane == 0) {
+        tr += (static_cast<size_t>(a.down) * gridDim.x * kWarps + static_cast<size_t>(wid)) * 8;
+        tr[0] = t_entry;
+        tr[1] = t_wait;
+        tr[2] = t_first;
+        tr[3] = gtimer();
+        tr[4] = static_cast<unsigned long long>(i1 - i0);
+        tr[5] = static_cast<unsigned long long>(n_runs);
+        tr[6] = static_cast<unsigned long long>(n_epi);
+        tr[7] = static_cast<unsigned long long>(blockIdx.x);
     }
 }
 
-// x (natural, [T][K]) -> xperm (K-permuted per 128-group), one thread per
-// 8 elements of output
-__global__ void permute_rows_kernel(const uint16_t* __restrict__ x, int rows, int K, uint16_t* __restrict__ xp) {
-    const long long n = static_cast<long long>(rows) * K;
-    for (long long o = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; o < n;
-         o += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long r = o / K;
-        const int c = static_cast<int>(o - r * K);
-        xp[r * K + perm_k(c)] = x[o];
+// x (natural, [rows][K]) -> K-permuted copy + per-128-group sums (fixed
+// xor-butterfly order).  One warp per (row, group); lane owns 4 elements.
+__global__ void permute_rows_kernel(const uint16_t* __restrict__ x, int rows, int K, uint16_t* __restrict__ xp,
+                                    float* __restrict__ xsum) {
+    const int G = K / 128;
+    const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    pdl_wait();     // x is the previous layer's output
+    pdl_trigger();
+    if (wid >= static_cast<long long>(rows) * G) return;
+    const long long r = wid / G;
+    const int g = static_cast<int>(wid - r * G);
+    const uint16_t* src = x + r * K + g * 128 + lane * 4;
+    uint16_t* dst = xp + r * K + g * 128;
+    float s = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint16_t v = src[j];
+        dst[perm_k(lane * 4 + j)] = v;
+        s += bf2f(v);
     }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) xsum[r * G + g] = s;
 }
 
-template <int GK4, int GK16>
-cudaError_t launch_gemv(const GemvArgs& a, cudaStream_t stream) {
-    static int grid = 0;
-    if (grid == 0) {
-        int dev = 0, sms = 0, occ = 0;
-        MOE_CUDA_OK(cudaGetDevice(&dev));
-        MOE_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        MOE_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_kernel<GK4, GK16>, kGemvThreads, 0));
-        grid = sms * (occ > 0 ? occ : 1);
-    }
-    gemv_kernel<GK4, GK16><<<grid, kGemvThreads, 0, stream>>>(a);
-    return cudaGetLastError();
-}
-
-int pick_gk(int G, int maxgk) {
+int host_pick_gk(int G, int maxgk) {
     for (int g = maxgk; g > 1; g >>= 1)
         if (G % g == 0) return g;
     return 1;
 }
 
 cudaError_t launch_pass(GemvArgs& a, cudaStream_t stream) {
+    static int grid = 0;
+    const size_t smem = static_cast<size_t>(kWarps) * kStages * kStageBytes;
+    if (grid == 0) {
+        MOE_CUDA_OK(cudaFuncSetAttribute(gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int dev = 0, sms = 0;
+        MOE_CUDA_OK(cudaGetDevice(&dev));
+        MOE_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        grid = sms;
+    }
     const int G = a.K / 128;
-    a.gk4 = pick_gk(G, 4);
-    a.gk16 = pick_gk(G, 2);
-    if (a.gk4 == 4) return launch_gemv<4, 2>(a, stream);
-    return launch_gemv<2, 2>(a, stream);
+    a.gk4 = host_pick_gk(G, 8);
+    a.gk16 = host_pick_gk(G, 2);
+    return launch_pdl(gemv_kernel, dim3(grid), dim3(kThreads), smem, stream, a);
 }
 
 }  // namespace moek
 
-size_t moek_gemv_partial_floats(int T, int k, int d, int f) {
-    // K-parts per matrix are at most G/1 for bf16 with gk16 = 1; size for the
-    // worst case (gk16 >= 1 -> KP <= G).
+namespace {
+
+size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+struct WsSizes {
+    size_t xperm, xsum, hperm, hsum16, hsum, part, counters, gcounters;
+};
+
+WsSizes ws_sizes(int T, int k, int d, int f) {
     const size_t slots = static_cast<size_t>(T) * k;
+    WsSizes w;
+    w.xperm = static_cast<size_t>(T) * d * 2;
+    w.xsum = static_cast<size_t>(T) * (d / 128) * 4;
+    w.hperm = slots * f * 2;
+    w.hsum16 = slots * (f / 16) * 4;
+    w.hsum = slots * (f / 128) * 4;
+    // K-parts per pass <= number of 128-K groups
     const size_t gu = static_cast<size_t>(d / 128) * slots * 2 * f;
     const size_t dn = static_cast<size_t>(f / 128) * slots * d;
-    return gu > dn ? gu : dn;
+    w.part = (gu > dn ? gu : dn) * 4;
+    const size_t cgu = static_cast<size_t>(moek::kMaxSegs) * (f / 16);
+    const size_t cdn = static_cast<size_t>(d) / 16;
+    w.counters = (cgu > cdn ? cgu : cdn) * 4;
+    w.gcounters = static_cast<size_t>(moek::kMaxSegs) * (f / 128) * 4;
+    return w;
 }
 
-size_t moek_gemv_counter_count(int T, int E, int d, int f) {
-    const size_t segs = static_cast<size_t>(E) * ((T + moek::kTile - 1) / moek::kTile);
-    const size_t gu = segs * (f / 16);
-    const size_t dn = static_cast<size_t>(d) / 16;
-    return gu > dn ? gu : dn;
+}  // namespace
+
+cudaError_t moek_debug_gemv_trace(void* buf) {
+    return cudaMemcpyToSymbol(moek::g_gemv_trace, &buf, sizeof(buf));
 }
 
-cudaError_t moek_permute_rows(const void* x, int rows, int K, void* xperm, cudaStream_t stream) {
-    const long long n = static_cast<long long>(rows) * K;
-    if (n == 0) return cudaSuccess;
-    long long blocks = (n + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    moek::permute_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
-        static_cast<const uint16_t*>(x), rows, K, static_cast<uint16_t*>(xperm));
-    return cudaGetLastError();
+size_t moek_gemv_workspace_bytes(int T, int k, int d, int f) {
+    const WsSizes w = ws_sizes(T, k, d, f);
+    return align256(w.xperm) + align256(w.xsum) + align256(w.hperm) + align256(w.hsum16) + align256(w.hsum) +
+           align256(w.part) + align256(w.counters) + align256(w.gcounters);
+}
+
+GemvWorkspace moek_gemv_workspace_view(void* base, int T, int k, int d, int f) {
+    const WsSizes w = ws_sizes(T, k, d, f);
+    char* p = static_cast<char*>(base);
+    GemvWorkspace ws{};
+    ws.xperm = p;
+    p += align256(w.xperm);
+    ws.xsum = reinterpret_cast<float*>(p);
+    p += align256(w.xsum);
+    ws.hperm = p;
+    p += align256(w.hperm);
+    ws.hsum16 = reinterpret_cast<float*>(p);
+    p += align256(w.hsum16);
+    ws.hsum = reinterpret_cast<float*>(p);
+    p += align256(w.hsum);
+    ws.part = reinterpret_cast<float*>(p);
+    p += align256(w.part);
+    ws.counters = reinterpret_cast<unsigned int*>(p);
+    p += align256(w.counters);
+    ws.gcounters = reinterpret_cast<unsigned int*>(p);
+    return ws;
+}
+
+cudaError_t moek_permute_rows(const void* x, int rows, int K, void* xperm, float* xsum, cudaStream_t stream) {
+    const long long warps = static_cast<long long>(rows) * (K / 128);
+    if (warps == 0) return cudaSuccess;
+    return moek::launch_pdl(moek::permute_rows_kernel, dim3(static_cast<unsigned>((warps * 32 + 255) / 256)), dim3(256),
+                            0, stream, static_cast<const uint16_t*>(x), rows, K, static_cast<uint16_t*>(xperm), xsum);
 }
 
 cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* perm, const int32_t* offsets,
                          const int32_t* inv, const float* wts, const void* resid, int T, int k,
                          const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask, void* out,
                          float* y, bool xperm_ready, cudaStream_t stream) {
-    if (!xperm_ready) MOE_CUDA_OK(moek_permute_rows(x, T, d, ws.xperm, stream));
+    if (!xperm_ready) MOE_CUDA_OK(moek_permute_rows(x, T, d, ws.xperm, ws.xsum, stream));
     moek::GemvArgs a{};
     a.offsets = offsets;
     a.perm = perm;
     a.T = T;
     a.k = k;
+    a.kshift = (k & (k - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(k)) : -1;
     a.E = E;
     a.active_mask = active_mask;
     for (int e = 0; e < E; ++e) a.ex[e] = experts[e];
     a.part = ws.part;
     a.counters = ws.counters;
+    a.gcounters = ws.gcounters;
     a.f = f;
-    // gate/up pass: [2f, d] x xperm -> hperm
+    // gate/up pass: [2f, d] x xperm -> hperm (fused SwiGLU + h group sums)
     a.rows = 2 * f;
     a.K = d;
     a.down = 0;
     a.bperm = static_cast<const uint16_t*>(ws.xperm);
+    a.bsum = ws.xsum;
     a.hperm = static_cast<uint16_t*>(ws.hperm);
+    a.hsum16 = ws.hsum16;
+    a.hsum = ws.hsum;
     MOE_CUDA_OK(moek::launch_pass(a, stream));
-    // down pass: [d, f] x hperm -> combine (or y)
+    // down pass: [d, f] x hperm -> combine (or per-slot y)
     a.rows = d;
     a.K = f;
     a.down = 1;
     a.bperm = static_cast<const uint16_t*>(ws.hperm);
+    a.bsum = ws.hsum;
     a.wts = wts;
     a.inv = inv;
     a.resid = static_cast<const uint16_t*>(resid);

@@ -15,13 +15,19 @@ cudaError_t moek_permute(const int32_t* idx, int T, int E, int k, int32_t* count
 // leave the arrival counters at zero).
 struct GemvWorkspace {
     void* xperm;              // [T][d] bf16, K-permuted
+    float* xsum;              // [T][d/128] activation group sums
     void* hperm;              // [T*k][f] bf16, K-permuted
-    float* part;              // partial run sums
-    unsigned int* counters;   // arrival counters
+    float* hsum16;            // [T*k][f/16]
+    float* hsum;              // [T*k][f/128]
+    float* part;              // zeroed partial run sums
+    unsigned int* counters;   // zeroed arrival counters
+    unsigned int* gcounters;  // zeroed per-(segment, h group) counters
 };
-size_t moek_gemv_partial_floats(int T, int k, int d, int f);
-size_t moek_gemv_counter_count(int T, int E, int d, int f);
-cudaError_t moek_permute_rows(const void* x, int rows, int K, void* xperm, cudaStream_t stream);
+// One zero-filled allocation of moek_gemv_workspace_bytes, carved by _view.
+size_t moek_gemv_workspace_bytes(int T, int k, int d, int f);
+GemvWorkspace moek_gemv_workspace_view(void* base, int T, int k, int d, int f);
+cudaError_t moek_permute_rows(const void* x, int rows, int K, void* xperm, float* xsum,
+                              cudaStream_t stream);
 // Expert FFN of every active expert segment (bit e of active_mask): gate/up
 // GEMV + fused SwiGLU, down GEMV + fused combine (out != null: out[t] =
 // bf16(resid[t] + sum_j w[t,j] y[inv[t*k+j]])) or per-slot y (out == null).
@@ -41,3 +47,6 @@ cudaError_t moek_synth_weight(uint64_t seed, uint64_t uid, long long n, int shif
                               cudaStream_t stream);
 cudaError_t moek_synth_input(uint64_t seed, uint64_t uid, long long n, void* out, cudaStream_t stream);
 int moek_weight_shift(int K);
+// Debug: per-warp phase trace buffer for the GEMV kernels (null disables);
+// [2 passes][148*warps][8] u64.
+cudaError_t moek_debug_gemv_trace(void* buf);

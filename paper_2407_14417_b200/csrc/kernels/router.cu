@@ -113,6 +113,8 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
 
     const int t = blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    pdl_wait();     // x is the previous layer's output
+    pdl_trigger();
     const uint16_t* xt = a.x + static_cast<size_t>(t) * a.d;
     for (int i = threadIdx.x * 8; i < a.d; i += blockDim.x * 8) {
         if (i + 8 <= a.d)
@@ -181,8 +183,7 @@ cudaError_t moek_route(const void* x, const void* wg, int T, int d, int E, int k
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
-    moek::route_kernel<<<T, moek::kRouteThreads, smem, stream>>>(a);
-    return cudaGetLastError();
+    return moek::launch_pdl(moek::route_kernel, dim3(T), dim3(moek::kRouteThreads), smem, stream, a);
 }
 
 cudaError_t moek_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_t* offsets,
