@@ -39,6 +39,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 D_MODEL, D_FFN, LAYERS, EXPERTS, TOPK = 4096, 14336, 32, 8, 2
+# Mixtral decoder layers apply post_attention_layernorm (RMSNorm, eps 1e-5)
+# before the MoE block; without it the synthetic residual stream overflows
+# after ~12 layers and the routing degenerates (tests: prenorm stack test).
+NORM_EPS = 1e-5
 METRIC = "decode tokens/s vs #4-bit experts (Mixtral-8x7B shape); expert-FFN HBM GB/s"
 
 
@@ -110,7 +114,7 @@ def cpu_port_tokens_per_s(n4_layer_prec, T, seconds=12.0, layer=0, seed=0):
     (tok/s extrapolated to 32 layers, threads, sample description)."""
     from oracle.oracle import OracleLib
     orc = OracleLib()
-    m = orc.model(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, seed)
+    m = orc.model(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, seed, NORM_EPS)
     prep = orc.prepare_layer(m, layer, n4_layer_prec)
     x = orc.step_input(m, 0, T)
     orc.moe_layer_w(m, prep, x, T)  # warm
@@ -139,7 +143,7 @@ def run_reference(args, rank, world):
     prec = plan.precision[:EXPERTS]
     from oracle.oracle import OracleLib
     orc = OracleLib()
-    m = orc.model(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, 0)
+    m = orc.model(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, 0, NORM_EPS)
     prep = orc.prepare_layer(m, 0, prec)
     T = args.tokens
     for w in range(args.warmup):
@@ -194,7 +198,7 @@ def run_ours(args, rank, world, device):
     def build(n4):
         plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 0), moe.HardwareProfile(10**15), prof)
         eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan, max_tokens=T, seed=args.seed + rank,
-                            device=device)
+                            device=device, norm_eps=NORM_EPS)
         return plan, eng
 
     # ---- headline point ---------------------------------------------------
@@ -277,6 +281,7 @@ def run_ours(args, rank, world, device):
             "vs_baseline": None, "dtype": "bf16 / int4-g128 weights, bf16 activations, fp32 accumulate",
             "data": "synthetic (seeded counter-based generator, int4 = RTN-g128 of the bf16 masters)",
             "config": {"workload": "mixtral8x7b-shape 32-layer MoE stack, batch-%d decode" % T, "n4": args.n4,
+                       "layer": "x + MoE(RMSNorm(x)) (decoder-layer norm eps 1e-5, unit weight; no attention)",
                        "of": LAYERS * EXPERTS, "plan": "plan_quality seed 0, all device-resident",
                        "d_model": D_MODEL, "d_ffn": D_FFN, "layers": LAYERS, "experts": EXPERTS, "top_k": TOPK,
                        "batch": T, "parallelism": "replicas" if world > 1 else "single",

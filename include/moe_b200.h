@@ -201,6 +201,9 @@ typedef struct {
     uint64_t seed;             /* synthetic weight seed                          */
     int32_t device;
     int32_t use_graphs;        /* capture decode steps in CUDA graphs            */
+    float norm_eps;            /* > 0: Mixtral decoder-layer RMSNorm (unit weight) before every MoE
+                                  block, out = x + MoE(RMSNorm(x)); 0: out = x + MoE(x) */
+    int32_t pad_;
 } moe_engine_config;
 
 int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan_entries,
@@ -247,6 +250,12 @@ int moe_engine_router(const moe_engine* eng, int layer, const void** wg_dev);
  * kernels ([2 passes][148*12 warps][8] uint64: entry, after PDL wait, first
  * item ready, end, items, runs, epilogues, CTA); NULL disables. */
 int moe_debug_gemv_trace(void* buf);
+/* Debug: per layer kernel (route, permute_rows, gate/up stream, SwiGLU
+ * finalize, down stream, output finalize) the earliest entry / post-PDL-wait
+ * and latest end globaltimer stamps: [6][3] uint64, entry/wait slots must be
+ * pre-filled with UINT64_MAX and end slots with 0; NULL disables.  Set in
+ * stream order on `stream`, so it can bracket exactly one graph replay. */
+int moe_debug_layer_trace(void* buf, void* stream);
 
 #ifdef __cplusplus
 }

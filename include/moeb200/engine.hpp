@@ -33,6 +33,7 @@ struct EngineConfig {
     uint64_t seed = 0;
     int device = 0;
     bool use_graphs = true;
+    float norm_eps = 0.0f;    // > 0: pre-MoE RMSNorm (unit weight), residual = un-normalised x
 };
 
 class MoeEngine {

@@ -297,9 +297,16 @@ void orc_step_input(const orc_model* m, int step, int T, uint16_t* x) {
 
 namespace {
 
-void layer_forward(const orc_model* m, const uint16_t* wg, const ExpertView* ex, const uint16_t* x, int T,
+void layer_forward(const orc_model* m, const uint16_t* wg, const ExpertView* ex, const uint16_t* x_res, int T,
                    uint16_t* out, int32_t* idx_out, float* w_out, float* logits) {
     const int d = m->d_model, f = m->d_ffn, E = m->num_experts, k = m->top_k;
+    std::vector<uint16_t> xn;
+    const uint16_t* x = x_res;
+    if (m->norm_eps > 0.0f) {
+        xn.resize(static_cast<size_t>(T) * d);
+        orc_rmsnorm(x_res, T, d, m->norm_eps, xn.data());
+        x = xn.data();
+    }
     std::vector<int32_t> idx(static_cast<size_t>(T) * k), perm(idx.size()), inv(idx.size());
     std::vector<float> w(idx.size());
     orc_gate_topk(x, wg, T, d, E, k, idx.data(), w.data(), logits);
@@ -316,12 +323,31 @@ void layer_forward(const orc_model* m, const uint16_t* wg, const ExpertView* ex,
         }
         ffn_rows(xs.data(), M, ex[s], d, f, &y_perm[static_cast<size_t>(offsets[s]) * d]);
     }
-    orc_combine(y_perm.data(), inv.data(), w.data(), x, T, d, k, out);
+    orc_combine(y_perm.data(), inv.data(), w.data(), x_res, T, d, k, out);
     if (idx_out) std::memcpy(idx_out, idx.data(), idx.size() * 4);
     if (w_out) std::memcpy(w_out, w.data(), w.size() * 4);
 }
 
 }  // namespace
+
+void orc_rmsnorm(const uint16_t* x, int T, int d, float eps, uint16_t* out) {
+    for (int t = 0; t < T; ++t) {
+        const uint16_t* xr = x + static_cast<size_t>(t) * d;
+        float part[256];
+        for (int i = 0; i < 256; ++i) {
+            float acc = 0.0f;
+            for (int c = 0; c * 256 + i < d; ++c) {
+                const float v = bf2f(xr[c * 256 + i]);
+                acc = std::fmaf(v, v, acc);
+            }
+            part[i] = acc;
+        }
+        for (int s2 = 128; s2 >= 1; s2 >>= 1)
+            for (int i = 0; i < s2; ++i) part[i] += part[i + s2];
+        const float rstd = 1.0f / std::sqrt(part[0] / static_cast<float>(d) + eps);
+        for (int j = 0; j < d; ++j) out[static_cast<size_t>(t) * d + j] = f2bf(bf2f(xr[j]) * rstd);
+    }
+}
 
 void orc_moe_layer_w(const orc_model* m, const uint16_t* wg, const orc_expert* experts, const uint16_t* x,
                      int T, uint16_t* out, int32_t* idx, float* w, float* logits) {
@@ -346,7 +372,9 @@ void orc_moe_layer(const orc_model* m, int layer, const int* precision, const ui
     std::vector<orc_expert> ex(static_cast<size_t>(E));
     std::vector<int32_t> idx(static_cast<size_t>(T) * m->top_k);
     std::vector<float> wtmp(idx.size());
-    orc_gate_topk(x, wg.data(), T, d, E, m->top_k, idx.data(), wtmp.data(), nullptr);
+    std::vector<uint16_t> xn(static_cast<size_t>(T) * d);
+    if (m->norm_eps > 0.0f) orc_rmsnorm(x, T, d, m->norm_eps, xn.data());
+    orc_gate_topk(m->norm_eps > 0.0f ? xn.data() : x, wg.data(), T, d, E, m->top_k, idx.data(), wtmp.data(), nullptr);
     std::vector<char> used(static_cast<size_t>(E), 0);
     for (int32_t v : idx) used[static_cast<size_t>(v)] = 1;
     for (int s = 0; s < E; ++s) {
@@ -402,7 +430,9 @@ inline BlockPos block_pos(int row, int k, int cols) {
 }
 
 inline size_t bf16_block_index(const BlockPos& b) {  // in uint16 units
-    return b.block * 2048 + static_cast<size_t>(((b.half * 4 + b.r / 8) * 32 + b.lane) * 8 + (b.r % 8));
+    // part kk = r/4 holds lane's {a0, a1, a2, a3} of MMA kk: word (hi*2 + half)
+    return b.block * 2048 +
+           static_cast<size_t>(((b.r / 4) * 32 + b.lane) * 8 + (((b.r / 2) % 2) * 2 + b.half) * 2 + b.r % 2);
 }
 
 inline size_t int4_block_word(const BlockPos& b) {  // in uint32 units

@@ -55,7 +55,8 @@ void orc_dequant_g128(const uint32_t* q, const uint16_t* s, int rows, int cols, 
  * so that lane (gr, t) of an mma.m16n8k16 finds its fragments contiguous.
  * Element (row, k) with rr = row%16, gr = rr%8, half = rr/8,
  * p = pi(k%128), r = p%32, lane = gr*4 + p/32:
- *   bf16 block (4096 B): byte ((half*4 + r/8)*32 + lane)*16 + (r%8)*2
+ *   bf16 block (4096 B): byte ((r/4)*32 + lane)*16 + (((r/2)%2)*2 + half)*4 + (r%2)*2
+ *                        (part kk = r/4 is lane's {a0,a1,a2,a3} of MMA kk: one LDS.128)
  *   int4 block (1024 B): word ((half*32 + lane)*4 + r/8), nibble (r%8) placed
  *                        at bit 4*(j/2)+16*(j%2) with j = r%8, biased u=q+8
  *   int4 scales (32 B per block): bf16 at byte gr*4 + half*2
@@ -95,7 +96,16 @@ void orc_combine(const float* y_perm, const int32_t* inv_perm, const float* w,
 typedef struct {
     int num_layers, num_experts, top_k, d_model, d_ffn;
     uint64_t seed;
+    float norm_eps;   /* > 0: decoder-layer pre-MoE RMSNorm (unit weight) before the router and the
+                         experts, residual = the un-normalised x; 0: the bare MoE block */
+    int pad_;
 } orc_model;
+
+/* RMSNorm with unit weight (HF MixtralRMSNorm, modeling_mixtral.py), pinned
+ * order: partial[i] = fmaf chain over x[c*256+i]^2 (c ascending), then the
+ * pairwise tree partial[i] += partial[i+s] for s = 128, 64, ..., 1;
+ * rstd = 1 / sqrtf(partial[0] / d + eps) (IEEE); out = bf16(x * rstd). */
+void orc_rmsnorm(const uint16_t* x, int T, int d, float eps, uint16_t* out);
 
 /* Materialises expert e = layer*E + slot: bf16 masters, quantised when int4. */
 void orc_expert_bf16(const orc_model* m, int e, uint16_t* wgu, uint16_t* wd);

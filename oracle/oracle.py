@@ -28,7 +28,7 @@ def _np_ptr(a):
 
 class OrcModel(C.Structure):
     _fields_ = [("num_layers", C.c_int), ("num_experts", C.c_int), ("top_k", C.c_int), ("d_model", C.c_int),
-                ("d_ffn", C.c_int), ("seed", C.c_uint64)]
+                ("d_ffn", C.c_int), ("seed", C.c_uint64), ("norm_eps", C.c_float), ("pad_", C.c_int)]
 
 
 class OrcExpert(C.Structure):
@@ -62,6 +62,7 @@ class OracleLib:
             "orc_moe_layer": (None, [P(OrcModel), I, VP, VP, I, VP, VP, VP, VP]),
             "orc_moe_layer_w": (None, [P(OrcModel), VP, P(OrcExpert), VP, I, VP, VP, VP, VP]),
             "orc_num_threads": (I, []),
+            "orc_rmsnorm": (None, [VP, I, I, C.c_float, VP]),
             "orc_perm_k": (I, [I]),
             "orc_pack_bf16_blocks": (None, [VP, I, I, VP]),
             "orc_unpack_bf16_blocks": (None, [VP, I, I, VP]),
@@ -87,8 +88,13 @@ class OracleLib:
     def weight_shift(self, K):
         return self.L.orc_weight_shift(K)
 
-    def model(self, L, E, k, d, f, seed):
-        return OrcModel(L, E, k, d, f, seed)
+    def model(self, L, E, k, d, f, seed, norm_eps=0.0):
+        return OrcModel(L, E, k, d, f, seed, norm_eps, 0)
+
+    def rmsnorm(self, x, T, d, eps):
+        out = np.empty(T * d, np.uint16)
+        self.L.orc_rmsnorm(_np_ptr(np.ascontiguousarray(x)), T, d, C.c_float(eps), _np_ptr(out))
+        return out.reshape(T, d)
 
     def expert_bf16(self, m, e):
         gu = np.empty(2 * m.d_ffn * m.d_model, np.uint16)

@@ -354,7 +354,7 @@ int moe_ffn(const void* x, const int32_t* perm, const int32_t* offsets, int T, i
         const GemvWorkspace ws = moek_gemv_workspace_view(workspace, T, k, d, f);
         const uint64_t mask = E >= 64 ? ~0ull : ((1ull << E) - 1ull);
         const cudaError_t e = moek_ffn_mma(ws, x, perm, offsets, nullptr, nullptr, nullptr, T, k, experts, E, d, f,
-                                           mask, nullptr, y_perm, false, st(stream));
+                                           mask, nullptr, y_perm, MOE_X_PERMUTE, st(stream));
         if (e != cudaSuccess) throw std::runtime_error(std::string("moe_ffn: ") + cudaGetErrorString(e));
     });
 }
@@ -457,6 +457,8 @@ int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan
         ec.seed = cfg->seed;
         ec.device = cfg->device;
         ec.use_graphs = cfg->use_graphs != 0;
+        usage_if(!(cfg->norm_eps >= 0.0f), "norm_eps must be >= 0");
+        ec.norm_eps = cfg->norm_eps;
         const int n = cfg->num_layers * cfg->experts_per_layer;
         PlacementPlan plan = to_plan(plan_entries, n, 0);
         plan.swap_slot_bytes = required_swap_bytes(plan, ec.profile);
@@ -546,6 +548,14 @@ int moe_debug_gemv_trace(void* buf) {
     return guarded([&] {
         need_device();
         const cudaError_t e = moek_debug_gemv_trace(buf);
+        if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    });
+}
+
+int moe_debug_layer_trace(void* buf, void* stream) {
+    return guarded([&] {
+        need_device();
+        const cudaError_t e = moek_debug_layer_trace(buf, st(stream));
         if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
     });
 }

@@ -257,13 +257,17 @@ struct MoeEngine::Impl {
     // swap slot, Static policy) -> combine with residual.
     void layer(int l, const uint16_t* x, int T, uint16_t* out, int32_t* idx_l, float* w_l, float* logits) {
         const moe_expert_weights* lw = weights.data() + static_cast<size_t>(l) * E;
+        // route also writes the K-permuted activation copies the expert
+        // GEMV reads (no separate permute kernel on the critical path)
         ck(moek_route(x, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx_l, w_l, logits, counts,
-                      offsets, perm, inv, ticket, compute), "route");
+                      offsets, perm, inv, ticket, compute, gws.xperm, gws.xperm16, gws.xsum, moek_group_stride(d),
+                      cfg.norm_eps),
+           "route");
         counters.activations += static_cast<int64_t>(T) * K;
         if (!layer_has_cpu[static_cast<size_t>(l)]) {
             counters.hits += static_cast<int64_t>(T) * K;
             ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, lw, E, d, f, mask_all(), out, nullptr,
-                            false, compute), "ffn");
+                            MOE_X_ROUTED, compute), "ffn");
             return;
         } else {
             ck(cudaMemcpyAsync(idx_host, idx_l, static_cast<size_t>(T) * K * 4, cudaMemcpyDeviceToHost, compute), "D2H idx");
@@ -282,12 +286,9 @@ struct MoeEngine::Impl {
             uint64_t resident = 0;
             for (int s = 0; s < E; ++s)
                 if (((sel >> s) & 1ull) && location[static_cast<size_t>(l * E + s)] == MOE_GPU) resident |= 1ull << s;
-            bool permuted = false;  // x -> xperm done once per layer
-            if (resident) {
+            if (resident)
                 ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, lw, E, d, f, resident, nullptr, y,
-                                permuted, compute), "ffn");
-                permuted = true;
-            }
+                                MOE_X_READY, compute), "ffn");
             std::vector<moe_expert_weights> tmp(lw, lw + E);
             for (int s = 0; s < E; ++s) {
                 if (!((sel >> s) & 1ull) || location[static_cast<size_t>(l * E + s)] == MOE_GPU) continue;
@@ -301,8 +302,7 @@ struct MoeEngine::Impl {
                 ck(cudaStreamWaitEvent(compute, copy_done, 0), "wait");
                 tmp[static_cast<size_t>(s)] = view(swap, hw.precision == MOE_P16 ? Precision::P16 : Precision::P4);
                 ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, tmp.data(), E, d, f, 1ull << s, nullptr, y,
-                                permuted, compute), "ffn");
-                permuted = true;
+                                MOE_X_READY, compute), "ffn");
                 ck(cudaEventRecord(slot_free, compute), "record");
             }
         }
@@ -337,10 +337,11 @@ struct MoeEngine::Impl {
             uint16_t* dst = l == L - 1 ? xout : xbuf[l & 1];
             const moe_expert_weights* lw = weights.data() + static_cast<size_t>(l) * E;
             ck(moek_route(src, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx + l * TK, wts + l * TK,
-                          nullptr, counts, offsets, perm, inv, ticket, compute), "route");
+                          nullptr, counts, offsets, perm, inv, ticket, compute, gws.xperm, gws.xperm16, gws.xsum,
+                          moek_group_stride(d), cfg.norm_eps), "route");
             ck(cudaEventRecord(ev[static_cast<size_t>(2 * l)], compute), "record");
             ck(moek_ffn_mma(gws, src, perm, offsets, inv, wts + l * TK, src, T, K, lw, E, d, f, mask_all(), dst,
-                            nullptr, false, compute), "ffn");
+                            nullptr, MOE_X_ROUTED, compute), "ffn");
             ck(cudaEventRecord(ev[static_cast<size_t>(2 * l + 1)], compute), "record");
             src = dst;
         }
@@ -364,7 +365,8 @@ struct MoeEngine::Impl {
             ffn_bytes[l] = bytes;
         }
         for (auto& e : ev) cudaEventDestroy(e);
-        if (kernels_per_step) *kernels_per_step = 4 * L;  // route, permute-x, gate/up, down(+combine)
+        // route(+x permute), gate/up stream, SwiGLU finalize, down stream, combine finalize
+        if (kernels_per_step) *kernels_per_step = 5 * L;
     }
 
     bool graphable() const {

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -102,6 +103,22 @@ constexpr float kInt4Bias = 136.0f;  // 128 (magic) + 8 (storage bias)
 // must call pdl_wait() before reading its immediate predecessor's output.
 MOE_DEVI void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 MOE_DEVI void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Debug layer trace (moe_debug_layer_trace): per kernel id, the earliest
+// entry and post-PDL-wait globaltimer stamps (atomicMin) and the latest warp
+// end (atomicMax).  One copy per translation unit (no -rdc); null = off.
+static __device__ unsigned long long* g_layer_trace = nullptr;
+MOE_DEVI void ltrace(int id, int phase) {
+    unsigned long long* tr = g_layer_trace;
+    if (tr == nullptr || (threadIdx.x & 31) != 0) return;
+    if (phase < 2 && threadIdx.x != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (phase < 2)
+        atomicMin(tr + id * 3 + phase, t);
+    else
+        atomicMax(tr + id * 3 + 2, t);
+}
 
 MOE_DEVI float warp_sum(float v) {
 #pragma unroll

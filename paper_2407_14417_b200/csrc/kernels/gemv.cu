@@ -5,75 +5,87 @@
 // stand-in (simulator.cpp:31-32, :107) with the expert math of HF
 // MixtralExperts (modeling_mixtral.py:90-95).
 //
-// Data path (B200):
-//   HBM --cp.async.bulk (TMA bulk copy, mbarrier complete_tx)--> per-warp
-//   shared-memory ring (3 stages x 8.25 KB) --LDS.128--> mma.m16n8k16 A
-//   fragments.  Each warp owns a contiguous range of equal-byte work items
-//   and keeps its next items in flight while computing the current one, so
-//   the bytes in flight per SM (up to 8 warps x 3 x 8 KB) do not depend on
-//   register pressure.
-// Weights are stored as 16-row x 128-K "fragment blocks" (DESIGN.md, oracle
-// orc_pack_*_blocks): a work item (16-row tile, K-part) is one contiguous
-// span of blocks (one bulk copy), and a lane's 16-byte smem read is exactly
-// its A fragment.  int4 fragments are decoded in registers (LOP3 magic
-// number -> bf16 128+u, one bf16x2 FMA -> q exactly); the tensor core does
-// the multiply-accumulate in fp32 and the group scale is applied after each
-// 128-K group, y += s * sum(q*x) -- the exact dequant values q*s.  B
-// fragments (x or h) come from a K-permuted copy (xperm / hperm) with the
-// same 128-bit pattern.  Up to 8 tokens of an expert share each weight byte.
+// Per layer (all launches PDL-chained on one stream, one CUDA graph):
+//   permute_rows   x -> K-permuted bf16/fp16 copies + int4 bias terms
+//   stream<0>      gate/up rows of every selected expert x x  -> fp32 partials
+//   finalize_h     partials -> SwiGLU -> h (bf16 + fp16 copies + bias terms)
+//   stream<1>      down rows x h -> fp32 partials
+//   finalize_out   partials -> routing-weighted combine + residual -> out
 //
-// Split-K bookkeeping: a warp accumulates consecutive K-parts of a row tile
-// in registers ("run") and adds one fp32 partial into a zero-initialised
-// slot per run; per-tile counters count finished items, and the warp that
-// completes a tile reduces its K-part slots in fixed order (deterministic),
-// re-zeroes them, and runs the fused epilogue: SwiGLU + bf16 h (gate/up
-// pass) or routing-weighted combine + residual (down pass).
+// stream: HBM --cp.async.bulk (TMA bulk copy, mbarrier complete_tx)--> a
+// per-warp shared-memory ring --LDS.128--> mma.m16n8k16 fragments.  A work
+// item = (16-row tile, K-part of GK 128-K groups) of one expert segment: one
+// bulk copy of its weight blocks (+ one of its int4 scales) plus one per
+// token row of the matching activation slice (+ its int4 bias terms), all
+// completing on the stage's mbarrier, kStages items ahead of use.  The warp
+// never waits on anything but its ring: no global loads, no atomics, no
+// epilogue -- each item ends in plain stores of its fp32 partial (one slot
+// per K-part, so the finalize sums in a fixed order: bit-reproducible under
+// any schedule).  Items are statically partitioned into contiguous warp
+// ranges, except a tail pool handed out in small chunks from a global
+// counter so the warps that run fast absorb the imbalance.
+//
+// Weights are stored as 16-row x 128-K "fragment blocks" (DESIGN.md, oracle
+// orc_pack_*_blocks): a lane's 16-byte smem read is exactly one A operand
+// (bf16) or the 8 nibble pairs of one row half (int4).  int4 is decoded in
+// registers with the fp16 magic number (0x6400 | nibble -> 1024+u or
+// 1024+16u: 4 LOP3 + 1 SHF per 8 weights) and multiplied on the tensor core
+// against an fp16 copy of the activations (exact for 2^-17 <= |x| <= 65504);
+// the per-128-K-group scale is applied after the group's integer-exact dot,
+// y += s * sum(q*x) -- the exact dequant values q*s.
 #include "common.cuh"
 #include "launch.h"
 
 namespace moek {
 
-constexpr int kWarps = 12;
+constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kStages = 2;
-constexpr int kStageBytes = 8192 + 256;  // 8 KB of weights + int4 scales
 constexpr int kTile = 8;                 // tokens per segment tile (MMA n)
-constexpr int kMaxSegs = 128;
+constexpr int kMaxSegs = 64;             // (active expert, 8-token tile) segments per launch
+// stage layout: [weights <= 8 KB][int4 scales <= 256 B][activation rows][bias terms]
+constexpr int kStageW = 0;
+constexpr int kStageS = 8192;
+constexpr int kStageB = 8192 + 256;
+constexpr int kBRowPad = 64;             // row stride = GK*256 + 64: conflict-free LDS.128
+constexpr int kStageBBytes = 4608;       // m * (GK*256 + 64) <= 4608 for every (m, GK) used
+constexpr int kStageX = kStageB + kStageBBytes;
+constexpr int kStageBytes = kStageX + kTile * 32;
+constexpr int kChunk = 2;                // items per dynamic tail chunk
+constexpr int kMaxSlots = 512;           // permutation slots staged in smem by build_segs
 
-struct GemvArgs {
+struct StreamArgs {
     const int32_t* offsets;   // [E+1]
     const int32_t* perm;      // [T*k]: slot -> t*k + j
     int T, k, E;
-    int kshift;               // log2(k)
-    int rows, K;              // matrix rows / columns of this pass
-    int down;                 // 0 gate/up pass, 1 down pass
-    int gk4, gk16;            // 128-K groups per item (int4, bf16)
-    const uint16_t* bperm;    // B operand, K-permuted: [T][K] (gate/up) or [T*k][K] (down)
-    const float* bsum;        // per-(B row, 128-group) sums of B: [rows of B][K/128]
-    float* part;              // zeroed partial slots [KPmax][T*k][rows]
-    unsigned int* counters;   // zeroed arrival counters
-    unsigned int* gcounters;  // zeroed per-(segment, h group) counters (gate/up)
-    uint16_t* hperm;          // gate/up epilogue output [T*k][f] (K-permuted)
-    float* hsum16;            // gate/up epilogue: sums of 16 h rows [T*k][f/16]
-    float* hsum;              // gate/up epilogue: sums of 128 h rows [T*k][f/128]
-    int f;
-    const float* wts;         // down epilogue: routing weights [T*k]
-    const int32_t* inv;       // [T*k]
-    const uint16_t* resid;    // [T][d] or null
-    uint16_t* out;            // [T][d]; null -> write y per slot
-    float* y;                 // [T*k][d]
+    int kshift;               // log2(k) (-1: not a power of two)
+    int p;                    // 0: gate/up rows against x, 1: down rows against h
+    int rows, K;              // this pass's matrix shape
+    const uint16_t* b16;      // B operand for bf16 experts, K-permuted (perm_k): [rows of B][K]
+    const uint16_t* b16h;     // fp16 copy for int4 experts (perm_k16)
+    const float* bsum;        // int4 bias term per (B row, 128-group), row stride bstride
+    int bstride;
+    float* part;              // [K/128][T*k][rows]: one fp32 partial per (K-part, slot, row)
+    int* kpslot;              // [T*k]: K-parts written for the slot (0: expert not in this launch)
+    unsigned int* sched;      // tail-pool counter (reset by the finalize kernel)
+    int wait_first;           // 1: the predecessor produced the routing -> PDL wait before reading it
     uint64_t active_mask;
     moe_expert_weights ex[MOE_MAX_EXPERTS];
 };
 
 struct SegTable {
-    int n;
-    int items_per_rt;         // sum over segments of KP (down-pass tile total)
+    int n, N;
     int e[kMaxSegs];
-    int tile[kMaxSegs];
-    int kp[kMaxSegs];
-    int gk[kMaxSegs];
-    long long pre[kMaxSegs + 1];
+    int slot0[kMaxSegs];       // first permutation slot of the segment
+    int mcnt[kMaxSegs];        // tokens in the segment (<= kTile)
+    int kp[kMaxSegs];          // K-parts per row tile
+    int gk[kMaxSegs];          // 128-K groups per item
+    int wbytes[kMaxSegs];      // bytes of weights per item
+    int sbytes[kMaxSegs];      // bytes of int4 scales per item (0: bf16)
+    int brow[kMaxSegs][kTile]; // B row of MMA column c (clamped to mcnt-1)
+    const uint8_t* wptr[kMaxSegs];
+    const uint8_t* sptr[kMaxSegs];
+    int pre[kMaxSegs + 1];     // item prefix over segments
 };
 
 // ---- PTX wrappers: mbarrier + bulk async copy ------------------------------
@@ -120,6 +132,14 @@ MOE_DEVI void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uin
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+MOE_DEVI void mma_f16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                      uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 
 // Optional per-warp phase trace (moe_debug_gemv_trace): globaltimer stamps
 // [entry, after pdl_wait, first item ready, loop end] + item / run / epilogue
@@ -132,487 +152,599 @@ MOE_DEVI unsigned long long gtimer() {
 }
 
 MOE_DEVI uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
-MOE_DEVI uint4 ldb(const uint16_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
-// B fragments of one 128-K group: 4 x 16 B of this lane's token row
-MOE_DEVI void load_b(uint4 (&b)[4], const uint16_t* bp, bool valid) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) b[c] = valid ? ldb(bp + c * 8) : make_uint4(0, 0, 0, 0);
+// fp16 magic-number decode of one packed word (4 LOP3 + 1 SHF): fp16 0x6400
+// is 1024 with ulp 1, so a nibble in mantissa bits 0-3 reads 1024+u and one
+// in bits 4-7 reads 1024+16u -- both exact, no per-nibble shift.
+//   lo0: nibbles (0,16) -> 1024+u      hi0: nibbles (4,20) -> 1024+16u
+//   lo1: nibbles (8,24)                hi1: nibbles (12,28)
+MOE_DEVI void decode_h(uint32_t w, uint32_t& lo0, uint32_t& hi0, uint32_t& lo1, uint32_t& hi1) {
+    lo0 = and_or(w, 0x000F000Fu, 0x64006400u);
+    hi0 = and_or(w, 0x00F000F0u, 0x64006400u);
+    const uint32_t w8 = w >> 8;
+    lo1 = and_or(w8, 0x000F000Fu, 0x64006400u);
+    hi1 = and_or(w8, 0x00F000F0u, 0x64006400u);
 }
 
-// biased bf16 pairs (128+u) from a packed word (3 SHF + 4 LOP3, no FMA):
-// pairs for MMA kk=2q (p01 reg0, p23 reg2) and kk=2q+1 (p45, p67)
-MOE_DEVI void decode_u(uint32_t w, uint32_t& p01, uint32_t& p23, uint32_t& p45, uint32_t& p67) {
-    p01 = and_or(w, 0x000F000Fu, 0x43004300u);
-    p23 = and_or(w >> 4, 0x000F000Fu, 0x43004300u);
-    p45 = and_or(w >> 8, 0x000F000Fu, 0x43004300u);
-    p67 = and_or(w >> 12, 0x000F000Fu, 0x43004300u);
-}
-
-// One int4 item (gk 128-K groups).  The MMA sees the biased values 128+u
-// (exact in bf16); per group sum(q x) = sum((128+u) x) - 136 sum(x), with
-// sum(x) of the column's activation group (scol0: column 2t, scol1: 2t+1),
-// then y += s * sum(q x) (two independent HMMA chains per group).
-MOE_DEVI void item_int4(const uint8_t* stage, int gk, const uint16_t* bp, bool bvalid, const float* scol0,
-                        const float* scol1, int g0, int lane, float (&acc)[4]) {
-    const int t = lane & 3;
-    const uint8_t* sc = stage + gk * 1024;
-    float sv0[8], sv1[8];
+// One int4 group (16 rows x 128 K, 1024 B at gp + 32 B scales at sc); bp:
+// this lane's activation chunks of the group (4 x 16 B at stride 64).
+// Nibbles (0,16)/(8,24) of a word hold the K positions with k%16 < 8 ("lo",
+// value q+1032), nibbles (4,20)/(12,28) those with k%16 >= 8 ("hi", value
+// 16q+1152); two MMA chains accumulate them, and per group
+//   sum(q x) = c_lo + c_hi/16 - (1032 S_lo + 72 S_hi)
+// with the bias term precomputed per activation group (B0: column 2t, B1:
+// 2t+1).  Then y += s * sum(q x): the exact dequant values q*s.  Chunk q of
+// the fp16 activation copy holds the K positions of (lo0, lo1, hi0, hi1).
+MOE_DEVI void group_int4(const uint8_t* gp, const uint8_t* sc, const uint8_t* bp, float B0, float B1, int lane,
+                         float (&acc)[4]) {
+    const uint32_t s2 = *reinterpret_cast<const uint32_t*>(sc + (lane >> 2) * 4);
+    const uint4 wl = lds128(gp + lane * 16);
+    const uint4 wh = lds128(gp + 512 + lane * 16);
+    const uint32_t lo[4] = {wl.x, wl.y, wl.z, wl.w};
+    const uint32_t hi[4] = {wh.x, wh.y, wh.z, wh.w};
+    float cl[4] = {0.f, 0.f, 0.f, 0.f}, ch[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
-        sv0[g] = (scol0 && g < gk) ? __ldg(scol0 + g0 + g) : 0.0f;
-        sv1[g] = (scol1 && g < gk) ? __ldg(scol1 + g0 + g) : 0.0f;
+    for (int q = 0; q < 4; ++q) {
+        const uint4 b = lds128(bp + q * 64);
+        uint32_t a_l0, a_h0, a_l1, a_h1, c_l0, c_h0, c_l1, c_h1;
+        decode_h(lo[q], a_l0, a_h0, a_l1, a_h1);  // row gr
+        decode_h(hi[q], c_l0, c_h0, c_l1, c_h1);  // row gr+8
+        mma_f16(cl, a_l0, c_l0, a_l1, c_l1, b.x, b.y);
+        mma_f16(ch, a_h0, c_h0, a_h1, c_h1, b.z, b.w);
     }
-    uint4 ba[4], bb[4];
-    load_b(ba, bp + t * 32, bvalid);
+    const float s_lo = bf16_lo(s2), s_hi = bf16_hi(s2);
+    acc[0] = __fmaf_rn(s_lo, __fmaf_rn(ch[0], 0.0625f, cl[0]) - B0, acc[0]);
+    acc[1] = __fmaf_rn(s_lo, __fmaf_rn(ch[1], 0.0625f, cl[1]) - B1, acc[1]);
+    acc[2] = __fmaf_rn(s_hi, __fmaf_rn(ch[2], 0.0625f, cl[2]) - B0, acc[2]);
+    acc[3] = __fmaf_rn(s_hi, __fmaf_rn(ch[3], 0.0625f, cl[3]) - B1, acc[3]);
+}
+
+// One bf16 group (16 rows x 128 K, 4096 B): part kk (512 B) holds every
+// lane's {a0, a1, a2, a3} of MMA kk, so one LDS.128 is one A operand; even
+// kk accumulate into acc, odd kk into the second chain c1.  Chunk c of the
+// bf16 activation copy holds (kk=2c: k<8, k>=8; kk=2c+1: k<8, k>=8).
+MOE_DEVI void group_bf16(const uint8_t* gp, const uint8_t* bp, int lane, float (&acc)[4], float (&c1)[4]) {
 #pragma unroll
-    for (int g = 0; g < 8; g += 2) {
-        if (g >= gk) break;
-        // ping-pong B buffers (no register copies): ba = group g, bb = g+1
-        if (g + 1 < gk) load_b(bb, bp + (g + 1) * 128 + t * 32, bvalid);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int gg = g + h;
-            if (gg >= gk) break;
-            const uint4(&b)[4] = h == 0 ? ba : bb;
-            const uint32_t s2 = *reinterpret_cast<const uint32_t*>(sc + gg * 32 + (lane >> 2) * 4);
-            const float S0 = sv0[gg], S1 = sv1[gg];
-            const uint4 wl = lds128(stage + gg * 1024 + lane * 16);
-            const uint4 wh = lds128(stage + gg * 1024 + 512 + lane * 16);
-            const uint32_t lo[4] = {wl.x, wl.y, wl.z, wl.w};
-            const uint32_t hi[4] = {wh.x, wh.y, wh.z, wh.w};
-            float cg[4] = {0.f, 0.f, 0.f, 0.f}, ch[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t r0, r2, r0b, r2b, s0, sq2, s0b, s2b;
-                decode_u(lo[q], r0, r2, r0b, r2b);   // row gr
-                decode_u(hi[q], s0, sq2, s0b, s2b);  // row gr+8
-                mma_bf16(cg, r0, s0, r2, sq2, b[q].x, b[q].y);
-                mma_bf16(ch, r0b, s0b, r2b, s2b, b[q].z, b[q].w);
-            }
-            const float s_lo = bf16_lo(s2), s_hi = bf16_hi(s2);
-            acc[0] = __fmaf_rn(s_lo, __fmaf_rn(-kInt4Bias, S0, cg[0] + ch[0]), acc[0]);
-            acc[1] = __fmaf_rn(s_lo, __fmaf_rn(-kInt4Bias, S1, cg[1] + ch[1]), acc[1]);
-            acc[2] = __fmaf_rn(s_hi, __fmaf_rn(-kInt4Bias, S0, cg[2] + ch[2]), acc[2]);
-            acc[3] = __fmaf_rn(s_hi, __fmaf_rn(-kInt4Bias, S1, cg[3] + ch[3]), acc[3]);
-            if (h == 0 && g + 2 < gk) load_b(ba, bp + (g + 2) * 128 + t * 32, bvalid);
-        }
+    for (int c = 0; c < 4; ++c) {
+        const uint4 b = lds128(bp + c * 64);
+        const uint4 e = lds128(gp + (2 * c) * 512 + lane * 16);
+        const uint4 o = lds128(gp + (2 * c + 1) * 512 + lane * 16);
+        mma_bf16(acc, e.x, e.y, e.z, e.w, b.x, b.y);
+        mma_bf16(c1, o.x, o.y, o.z, o.w, b.z, b.w);
     }
 }
 
-MOE_DEVI void item_bf16(const uint8_t* stage, int gk, const uint16_t* bp, bool bvalid, int lane, float (&acc)[4]) {
-    const int t = lane & 3;
-    float c1[4] = {0.f, 0.f, 0.f, 0.f};  // second chain (odd kk)
-    uint4 ba[4], bb[4];
-    load_b(ba, bp + t * 32, bvalid);
-    for (int g = 0; g < gk; g += 2) {
-        if (g + 1 < gk) load_b(bb, bp + (g + 1) * 128 + t * 32, bvalid);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int gg = g + h;
-            if (gg >= gk) break;
-            const uint4(&b)[4] = h == 0 ? ba : bb;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                // part c = row gr words for kk = 2c, 2c+1; part 4+c = row gr+8
-                const uint4 lo = lds128(stage + gg * 4096 + c * 512 + lane * 16);
-                const uint4 hi = lds128(stage + gg * 4096 + (4 + c) * 512 + lane * 16);
-                mma_bf16(acc, lo.x, hi.x, lo.y, hi.y, b[c].x, b[c].y);
-                mma_bf16(c1, lo.z, hi.z, lo.w, hi.w, b[c].z, b[c].w);
-            }
-            if (h == 0 && g + 2 < gk) load_b(ba, bp + (g + 2) * 128 + t * 32, bvalid);
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) acc[r] += c1[r];
-}
-
-// token of a permutation slot (perm[slot] = t*k + j); k is a power of two in
-// every config we run, so this is a shift (division otherwise)
-MOE_DEVI int tok_of_slot(const GemvArgs& a, int slot) {
-    return a.kshift >= 0 ? a.perm[slot] >> a.kshift : a.perm[slot] / a.k;
-}
-
-// K-permuted position of natural index n (orc_perm_k)
+// Activation layouts inside a 128-K group (kin = kk*16 + hi*8 + t*2 + e):
+// 16-byte chunk (kk/2)*4 + t belongs to lane t, so the 4 lanes of a row read
+// 64 contiguous bytes per LDS.128 (conflict-free); inside the chunk
+//   bf16 copy (perm_k):   word (kk%2)*2 + hi
+//   fp16 copy (perm_k16): word hi*2 + kk%2
 MOE_DEVI int perm_k(int n) {
-    const int kin = n & 127;
-    return (n & ~127) + ((kin & 7) >> 1) * 32 + (kin >> 4) * 4 + ((kin >> 3) & 1) * 2 + (kin & 1);
+    const int kin = n & 127, kk = kin >> 4;
+    return (n & ~127) + ((kk >> 1) * 4 + ((kin & 7) >> 1)) * 8 + ((kk & 1) * 2 + ((kin >> 3) & 1)) * 2 + (kin & 1);
+}
+MOE_DEVI int perm_k16(int n) {
+    const int kin = n & 127, kk = kin >> 4;
+    return (n & ~127) + ((kk >> 1) * 4 + ((kin & 7) >> 1)) * 8 + (((kin >> 3) & 1) * 2 + (kk & 1)) * 2 + (kin & 1);
 }
 
-MOE_DEVI void build_segs(const GemvArgs& a, SegTable& st, int* cnt) {
-    // expert token counts read in parallel (one L2 round trip), then a short
-    // serial pass over <= 64 experts in shared memory
-    if (threadIdx.x < a.E)
-        cnt[threadIdx.x] = ((a.active_mask >> threadIdx.x) & 1ull)
-                               ? a.offsets[threadIdx.x + 1] - a.offsets[threadIdx.x]
-                               : 0;
+// 128-K groups per item: the largest power of two <= cap dividing G, where
+// cap keeps m activation rows of the item inside the stage.
+MOE_DEVI int pick_gk(int G, int prec, int m) {
+    int cap = prec == MOE_P4 ? 8 : 2;
+    while (cap > 1 && m * (cap * 256 + kBRowPad) > kStageBBytes) cap >>= 1;
+    while (cap > 1 && G % cap) cap >>= 1;
+    return cap;
+}
+
+// Segment table (one segment per (active expert, 8-token tile)), built
+// redundantly by every CTA from the routing; CTA 0 also publishes each
+// slot's K-part count for the finalize kernel.
+MOE_DEVI void build_segs(const StreamArgs& a, SegTable& st, int* cnt, int* sperm) {
+    // offsets and perm in one round trip
+    const int nslots = a.T * a.k;
+    int o0 = 0, o1 = 0;
+    if (threadIdx.x < a.E) {
+        o0 = a.offsets[threadIdx.x];
+        o1 = a.offsets[threadIdx.x + 1];
+    }
+    if (a.p == 0)
+        for (int i = threadIdx.x; i < nslots && i < kMaxSlots; i += blockDim.x) sperm[i] = a.perm[i];
+    if (threadIdx.x < a.E) {
+        cnt[threadIdx.x] = ((a.active_mask >> threadIdx.x) & 1ull) ? o1 - o0 : 0;
+        cnt[MOE_MAX_EXPERTS + threadIdx.x] = o0;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         const int RT = a.rows / 16, G = a.K / 128;
-        int n = 0, items_rt = 0;
-        long long acc = 0;
+        int n = 0, acc = 0;
         for (int e = 0; e < a.E; ++e) {
             const int m = cnt[e];
             if (m == 0) continue;
-            const int gk = a.ex[e].precision == MOE_P4 ? a.gk4 : a.gk16;
-            const int kp = G / gk;
+            const moe_expert_weights& W = a.ex[e];
             for (int t = 0; t * kTile < m && n < kMaxSegs; ++t) {
+                const int mc = min(kTile, m - t * kTile);
+                const int gk = pick_gk(G, W.precision, mc);
                 st.e[n] = e;
-                st.tile[n] = t;
-                st.kp[n] = kp;
+                st.slot0[n] = cnt[MOE_MAX_EXPERTS + e] + t * kTile;
+                st.mcnt[n] = mc;
+                st.kp[n] = G / gk;
                 st.gk[n] = gk;
+                st.wptr[n] = static_cast<const uint8_t*>(a.p == 0 ? W.w_gate_up : W.w_down);
+                st.sptr[n] = static_cast<const uint8_t*>(a.p == 0 ? W.s_gate_up : W.s_down);
+                st.wbytes[n] = W.precision == MOE_P4 ? gk * 1024 : gk * 4096;
+                st.sbytes[n] = W.precision == MOE_P4 ? gk * 32 : 0;
                 st.pre[n] = acc;
-                acc += static_cast<long long>(RT) * kp;
-                items_rt += kp;
+                acc += RT * (G / gk);
                 ++n;
             }
         }
         st.pre[n] = acc;
         st.n = n;
-        st.items_per_rt = items_rt;
+        st.N = acc;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < st.n * kTile; i += blockDim.x) {
+        const int s = i / kTile, c = i - s * kTile;
+        const int slot = st.slot0[s] + min(c, st.mcnt[s] - 1);
+        const int pv = slot < kMaxSlots ? sperm[slot] : a.perm[slot];
+        st.brow[s][c] = a.p == 1 ? slot : (a.kshift >= 0 ? pv >> a.kshift : pv / a.k);
+    }
+    if (blockIdx.x == 0) {
+        for (int slot = threadIdx.x; slot < a.T * a.k; slot += blockDim.x) {
+            int kp = 0;
+            for (int s = 0; s < st.n; ++s)
+                if (slot >= st.slot0[s] && slot < st.slot0[s] + st.mcnt[s]) kp = st.kp[s];
+            a.kpslot[slot] = kp;
+        }
     }
     __syncthreads();
 }
 
-// reduce + re-zero the K-part slots of (row, slot)
-MOE_DEVI float take_partial(const GemvArgs& a, int kp_count, int row, int slot) {
-    const int nslots = a.T * a.k;
-    const size_t stride = static_cast<size_t>(nslots) * a.rows;
-    float* base = a.part + static_cast<size_t>(slot) * a.rows + row;
-    float v = 0.0f;
-    for (int kp = 0; kp < kp_count; kp += 8) {
-        float x[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = kp + u < kp_count ? __ldcg(base + (kp + u) * stride) : 0.0f;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            if (x[u] != 0.0f) {
-                v += x[u];
-                __stcg(base + (kp + u) * stride, 0.0f);
-            }
-        }
-    }
-    return v;
-}
-
-MOE_DEVI int seg_of_slot(const GemvArgs& a, const SegTable& st, int slot) {
-    for (int s = 0; s < st.n; ++s) {
-        const int e = st.e[s];
-        const int lo = a.offsets[e] + st.tile[s] * kTile;
-        if (slot >= lo && slot < min(lo + kTile, a.offsets[e + 1])) return s;
-    }
-    return -1;
-}
-
-// SwiGLU for the 16 rows of pair tile prt and every token of segment s, plus
-// the activation-group sums the int4 down pass needs: sum of the 16 rounded
-// h values (fixed xor-butterfly order), and -- by the last of the 8 pair
-// tiles of a 128-row group -- their fixed-order total.
-MOE_DEVI void epilogue_gateup(const GemvArgs& a, const SegTable& st, int s, int prt, int lane) {
-    const int e = st.e[s];
-    const int slot0 = a.offsets[e] + st.tile[s] * kTile;
-    const int m_cnt = min(kTile, a.offsets[e + 1] - slot0);
-    const int f16 = a.f / 16, f128 = a.f / 128;
-    for (int i0 = 0; i0 < m_cnt * 16; i0 += 32) {
-        const int i = i0 + lane;
-        const int m = i >> 4, n = prt * 16 + (i & 15), slot = slot0 + m;
-        float hv = 0.0f;
-        if (i < m_cnt * 16) {
-            const float g = take_partial(a, st.kp[s], n, slot);
-            const float u = take_partial(a, st.kp[s], a.f + n, slot);
-            const uint16_t hb = f2bf(silu_f(g) * u);
-            a.hperm[static_cast<size_t>(slot) * a.f + perm_k(n)] = hb;
-            hv = bf2f(hb);
-        }
-        // sum over the 16 rows held by each half-warp
-#pragma unroll
-        for (int off = 8; off >= 1; off >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, off);
-        if ((lane & 15) == 0 && i < m_cnt * 16) __stcg(a.hsum16 + static_cast<size_t>(slot) * f16 + prt, hv);
-    }
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-        unsigned int* ctr = a.gcounters + static_cast<size_t>(s) * f128 + prt / 8;
-        if (atom_add_release(ctr, 1u) + 1 == 8u) {
-            *ctr = 0;
-            last = 1;
-        }
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {
-        const int g = prt / 8;
-        for (int m = lane; m < m_cnt; m += 32) {
-            const float* p = a.hsum16 + static_cast<size_t>(slot0 + m) * f16 + g * 8;
-            float v = 0.0f;
-#pragma unroll
-            for (int r = 0; r < 8; ++r) v += __ldcg(p + r);
-            a.hsum[static_cast<size_t>(slot0 + m) * f128 + g] = v;
-        }
-    }
-}
-
-MOE_DEVI void epilogue_down(const GemvArgs& a, const SegTable& st, int rt, int lane) {
-    const int d = a.rows;
-    if (a.out == nullptr) {
-        for (int i = lane; i < a.T * a.k * 16; i += 32) {
-            const int slot = i >> 4, j = rt * 16 + (i & 15);
-            const int s = seg_of_slot(a, st, slot);
-            if (s >= 0) a.y[static_cast<size_t>(slot) * d + j] = take_partial(a, st.kp[s], j, slot);
-        }
-        return;
-    }
-    for (int i = lane; i < a.T * 16; i += 32) {
-        const int t = i >> 4, j = rt * 16 + (i & 15);
-        float accv = a.resid ? bf2f(a.resid[static_cast<size_t>(t) * d + j]) : 0.0f;
-        for (int jj = 0; jj < a.k; ++jj) {
-            const int slot = a.inv[t * a.k + jj];
-            const int s = seg_of_slot(a, st, slot);
-            const float yv = s < 0 ? 0.0f : take_partial(a, st.kp[s], j, slot);
-            accv = __fmaf_rn(a.wts[t * a.k + jj], yv, accv);
-        }
-        a.out[static_cast<size_t>(t) * d + j] = f2bf(accv);
-    }
-}
-
-struct ItemIt {
+struct Item {
     int s, rt, kp;
 };
 
-MOE_DEVI void advance(ItemIt& it, const SegTable& st, int RT) {
-    if (++it.kp == st.kp[it.s]) {
-        it.kp = 0;
-        if (++it.rt == RT) {
-            it.rt = 0;
-            ++it.s;
-        }
-    }
-}
-
-MOE_DEVI ItemIt locate(long long i, const SegTable& st) {
-    ItemIt it{0, 0, 0};
+MOE_DEVI Item item_at(const SegTable& st, int i) {
+    Item it;
+    it.s = 0;
     while (st.pre[it.s + 1] <= i) ++it.s;
-    const long long local = i - st.pre[it.s];
-    it.rt = static_cast<int>(local / st.kp[it.s]);
-    it.kp = static_cast<int>(local - static_cast<long long>(it.rt) * st.kp[it.s]);
+    const int local = i - st.pre[it.s];
+    it.rt = local / st.kp[it.s];
+    it.kp = local - it.rt * st.kp[it.s];
     return it;
 }
 
-// issue the bulk copies of one item into a ring stage (lane 0 only)
-MOE_DEVI void issue_item(const GemvArgs& a, const SegTable& st, const ItemIt& it, uint8_t* stage, uint64_t* bar) {
-    const moe_expert_weights& W = a.ex[st.e[it.s]];
-    const int G = a.K / 128, gk = st.gk[it.s];
-    const size_t blk = static_cast<size_t>(it.rt) * G + static_cast<size_t>(it.kp) * gk;
-    const uint8_t* w = static_cast<const uint8_t*>(a.down ? W.w_down : W.w_gate_up);
-    if (W.precision == MOE_P4) {
-        const uint8_t* sc = static_cast<const uint8_t*>(a.down ? W.s_down : W.s_gate_up);
-        mbar_expect_tx(bar, gk * 1024 + gk * 32);
-        bulk_g2s(stage, w + blk * 1024, gk * 1024, bar);
-        bulk_g2s(stage + gk * 1024, sc + blk * 32, gk * 32, bar);
+// Issue the weight half of an item (expect_tx covers the whole item).
+MOE_DEVI void issue_weights(const StreamArgs& a, const SegTable& st, const Item& it, uint8_t* stage, uint64_t* bar) {
+    const int s = it.s, wb = st.wbytes[s], sb = st.sbytes[s], m = st.mcnt[s];
+    mbar_expect_tx(bar, wb + sb + m * st.gk[s] * 256 + (sb ? m * 32 : 0));
+    const size_t blk = static_cast<size_t>(it.rt) * (a.K / 128) + static_cast<size_t>(it.kp) * st.gk[s];
+    bulk_g2s(stage + kStageW, st.wptr[s] + blk * (sb ? 1024 : 4096), wb, bar);
+    if (sb) bulk_g2s(stage + kStageS, st.sptr[s] + blk * 32, sb, bar);
+}
+
+// Issue the activation half: the item's K slice of every token row of the
+// segment (fp16 copy for int4, bf16 for bf16) and, for int4, the 32-byte
+// bias-term chunk holding the item's groups.
+MOE_DEVI void issue_acts(const StreamArgs& a, const SegTable& st, const Item& it, uint8_t* stage, uint64_t* bar) {
+    const int s = it.s, m = st.mcnt[s], gk = st.gk[s];
+    const int rowb = gk * 256;
+    const size_t k0 = static_cast<size_t>(it.kp) * gk * 128;
+    if (st.sbytes[s]) {
+        const int g8 = (it.kp * gk) & ~7;
+        for (int r = 0; r < m; ++r) {
+            const int br = st.brow[s][r];
+            bulk_g2s(stage + kStageB + r * (rowb + kBRowPad), a.b16h + static_cast<size_t>(br) * a.K + k0, rowb, bar);
+            bulk_g2s(stage + kStageX + r * 32, a.bsum + static_cast<size_t>(br) * a.bstride + g8, 32, bar);
+        }
     } else {
-        mbar_expect_tx(bar, gk * 4096);
-        bulk_g2s(stage, w + blk * 4096, gk * 4096, bar);
+        for (int r = 0; r < m; ++r)
+            bulk_g2s(stage + kStageB + r * (rowb + kBRowPad), a.b16 + static_cast<size_t>(st.brow[s][r]) * a.K + k0,
+                     rowb, bar);
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) gemv_kernel(const __grid_constant__ GemvArgs a) {
+// Item sequence of one warp: its static range, then tail-pool chunks grabbed
+// one chunk ahead by lane 0 (the atomic's result is consumed a chunk later)
+// and logged in a 4-entry queue the compute side replays in order.
+struct Sched {
+    unsigned int* ctr;
+    int N;
+    int cur, end;          // current static range / chunk [cur, end)
+    int dyn;               // in the tail pool
+    unsigned int pend;     // lane 0: pre-grabbed chunk start
+    int lane;
+
+    MOE_DEVI void grab_ahead() {
+        if (lane == 0) pend = atomicAdd(ctr, static_cast<unsigned>(kChunk));
+    }
+    MOE_DEVI bool next(int& i, int4* q, int& qw, int ns) {
+        while (cur >= end) {
+            if (!dyn) {
+                dyn = 1;
+                grab_ahead();
+            }
+            const int start = ns + static_cast<int>(__shfl_sync(0xffffffffu, pend, 0));
+            if (start >= N) return false;
+            cur = start;
+            end = min(start + kChunk, N);
+            if (lane == 0) q[qw & 3] = make_int4(cur, end, 0, 0);
+            __syncwarp();
+            ++qw;
+            grab_ahead();
+        }
+        i = cur++;
+        return true;
+    }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_constant__ StreamArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ SegTable st;
     __shared__ __align__(8) uint64_t bars[kWarps][kStages];
+    __shared__ int4 chq[kWarps][4];
+    __shared__ int cnt[2 * MOE_MAX_EXPERTS];
+    __shared__ int sperm[kMaxSlots];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint8_t* ring = smem + static_cast<size_t>(warp) * kStages * kStageBytes;
     if (lane == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&bars[warp][s], 1);
         fence_mbar_init();
     }
-    __shared__ int cnt[MOE_MAX_EXPERTS];
-    // Routing (offsets) comes from the route kernel two launches back, so the
-    // segment table and the first weight bulk copies are issued before the
-    // PDL wait -- weight streaming overlaps the predecessor's tail.
     const unsigned long long t_entry = gtimer();
-    build_segs(a, st, cnt);  // contains __syncthreads
-    const int N = static_cast<int>(st.pre[st.n]);
+    ltrace(2 + 2 * a.p, 0);
+    // When the routing comes from two or more launches back, the segment
+    // table and the first items' weight copies go out before the PDL wait;
+    // their activation copies (the predecessor's output) after it.
+    if (a.wait_first) pdl_wait();
+    build_segs(a, st, cnt, sperm);  // contains __syncthreads
     const int W = static_cast<int>(gridDim.x) * kWarps;
     const int wid = static_cast<int>(blockIdx.x) * kWarps + warp;
-    // equal contiguous ranges: q items each, the first r warps one more
-    const int q = N / W, r = N - q * W;
-    const long long i0 = static_cast<long long>(wid) * q + min(wid, r);
-    const long long i1 = i0 + q + (wid < r ? 1 : 0);
-    const int RT = a.rows / 16;
-    const int nslots = a.T * a.k;
     const int gr = lane >> 2, t = lane & 3;
+    const int nslots = a.T * a.k;
+    uint8_t* ring = smem + static_cast<size_t>(warp) * kStages * kStageBytes;
+    int4* q = chq[warp];
 
-    // prologue: fill the ring (weights only: independent of the predecessor)
-    ItemIt issue_it{0, 0, 0};
-    long long issued = i0;
-    if (i0 < i1) {
-        issue_it = locate(i0, st);
-        for (int s = 0; s < kStages && issued < i1; ++s, ++issued) {
-            if (lane == 0) issue_item(a, st, issue_it, ring + s * kStageBytes, &bars[warp][s]);
-            advance(issue_it, st, RT);
+    // static part: contiguous equal ranges over the first ~7/8 of the items
+    const int N = st.N;
+    const int ns = N - min(N / 8, W * kChunk * 2);
+    const int qs = ns / W, rs = ns - qs * W;
+    Sched sc;
+    sc.ctr = a.sched;
+    sc.N = N;
+    sc.cur = wid * qs + min(wid, rs);
+    sc.end = sc.cur + qs + (wid < rs ? 1 : 0);
+    sc.dyn = 0;
+    sc.pend = 0;
+    sc.lane = lane;
+    int qw = 0, qr = 0;
+    int ccur = sc.cur, cend = sc.end;  // compute-side cursor (starts on the static range)
+
+    static_assert(kStages == 2, "prologue is written for two stages");
+    Item pro0{0, 0, 0}, pro1{0, 0, 0};
+    int npro = 0, ii;
+    if (sc.next(ii, q, qw, ns)) {
+        pro0 = item_at(st, ii);
+        if (lane == 0) issue_weights(a, st, pro0, ring, &bars[warp][0]);
+        npro = 1;
+        if (sc.next(ii, q, qw, ns)) {
+            pro1 = item_at(st, ii);
+            if (lane == 0) issue_weights(a, st, pro1, ring + kStageBytes, &bars[warp][1]);
+            npro = 2;
         }
     }
-    pdl_wait();     // B operand / counters / partials of the predecessor
+    if (!a.wait_first) pdl_wait();  // activations of the predecessor
     pdl_trigger();
-    if (i0 >= i1) return;
+    ltrace(2 + 2 * a.p, 1);
+    if (lane == 0) {
+        if (npro > 0) issue_acts(a, st, pro0, ring, &bars[warp][0]);
+        if (npro > 1) issue_acts(a, st, pro1, ring + kStageBytes, &bars[warp][1]);
+    }
     const unsigned long long t_wait = gtimer();
-    unsigned long long t_first = 0;
-    int n_runs = 0, n_epi = 0;
+    unsigned long long t_first = 0, t_mbar = 0;
+    int issued = npro, computed = 0;
+    uint32_t phase_bits = 0;
 
-    ItemIt it = locate(i0, st);
-    long long i = i0;
-    uint32_t phase_bits = 0;  // per-stage parity
-    int stage = 0;
-    while (i < i1) {
-        const int s = it.s, rt = it.rt;
-        const int e = st.e[s];
-        const int prec = a.ex[e].precision;
-        const int gk = st.gk[s];
-        const int kp0 = it.kp;
-        const int slot0 = a.offsets[e] + st.tile[s] * kTile;
-        const int m_cnt = min(kTile, a.offsets[e + 1] - slot0);
-        const bool bvalid = gr < m_cnt;
-        int brow = 0;
-        if (bvalid) brow = a.down ? slot0 + gr : tok_of_slot(a, slot0 + gr);
-        const uint16_t* brow_p = a.bperm + static_cast<size_t>(brow) * a.K;
-        // activation-group sums of this lane's two C columns (int4 bias)
-        const int G = a.K / 128;
-        const float* scol[2] = {nullptr, nullptr};
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int n = 2 * t + c;
-            if (n < m_cnt) {
-                const int rb = a.down ? slot0 + n : tok_of_slot(a, slot0 + n);
-                scol[c] = a.bsum + static_cast<size_t>(rb) * G;
-            }
+    while (computed < issued) {
+        const int stage = computed & 1;
+        if (ccur >= cend) {
+            const int4 c = q[qr & 3];
+            ++qr;
+            ccur = c.x;
+            cend = c.y;
         }
+        const Item it = item_at(st, ccur++);
+        const unsigned long long tm0 = gtimer();
+        mbar_wait(&bars[warp][stage], (phase_bits >> stage) & 1u);
+        phase_bits ^= 1u << stage;
+        t_mbar += gtimer() - tm0;
+        if (t_first == 0) t_first = gtimer();
+        const uint8_t* sp = ring + stage * kStageBytes;
+        const int gk = st.gk[it.s], m_cnt = st.mcnt[it.s];
+        const int brl = min(gr, m_cnt - 1);
+        const int boff = kStageB + brl * (gk * 256 + kBRowPad) + t * 16;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        int run_len = 0;
-        // one run: consecutive K-parts of (s, rt) within this warp's range
-        while (i < i1 && it.s == s && it.rt == rt) {
-            mbar_wait(&bars[warp][stage], (phase_bits >> stage) & 1u);
-            if (t_first == 0) t_first = gtimer();
-            phase_bits ^= 1u << stage;
-            const uint8_t* sp = ring + stage * kStageBytes;
-            const uint16_t* bp = brow_p + static_cast<size_t>(it.kp) * gk * 128;
-            if (prec == MOE_P4)
-                item_int4(sp, gk, bp, bvalid, scol[0], scol[1], it.kp * gk, lane, acc);
-            else
-                item_bf16(sp, gk, bp, bvalid, lane, acc);
-            // release the stage and refill it with the item kStages ahead
-            fence_proxy_async();
-            __syncwarp();
-            if (issued < i1) {
-                if (lane == 0) issue_item(a, st, issue_it, ring + stage * kStageBytes, &bars[warp][stage]);
-                advance(issue_it, st, RT);
-                ++issued;
+        if (st.sbytes[it.s]) {
+            const int c0 = min(2 * t, m_cnt - 1), c1i = min(2 * t + 1, m_cnt - 1);
+            const int g0 = (it.kp * gk) & 7;
+            const float* x0 = reinterpret_cast<const float*>(sp + kStageX + c0 * 32) + g0;
+            const float* x1 = reinterpret_cast<const float*>(sp + kStageX + c1i * 32) + g0;
+            switch (gk) {
+                case 8:
+#pragma unroll
+                    for (int g = 0; g < 8; ++g)
+                        group_int4(sp + kStageW + g * 1024, sp + kStageS + g * 32, sp + boff + g * 256, x0[g], x1[g], lane, acc);
+                    break;
+                case 4:
+#pragma unroll
+                    for (int g = 0; g < 4; ++g)
+                        group_int4(sp + kStageW + g * 1024, sp + kStageS + g * 32, sp + boff + g * 256, x0[g], x1[g], lane, acc);
+                    break;
+                default:
+                    for (int g = 0; g < gk; ++g)
+                        group_int4(sp + kStageW + g * 1024, sp + kStageS + g * 32, sp + boff + g * 256, x0[g], x1[g], lane, acc);
+                    break;
             }
-            stage = stage + 1 == kStages ? 0 : stage + 1;
-            advance(it, st, RT);
-            ++i;
-            ++run_len;
+        } else {
+            float c1[4] = {0.f, 0.f, 0.f, 0.f};
+            group_bf16(sp + kStageW, sp + boff, lane, acc, c1);
+            if (gk == 2) group_bf16(sp + kStageW + 4096, sp + boff + 256, lane, acc, c1);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[r] += c1[r];
         }
-        // flush the run into its (zeroed) K-part slot: columns 2t, 2t+1
-        const int row = rt * 16 + gr;
+        ++computed;
+        // release the stage and refill it with the next item of the sequence
+        fence_proxy_async();
+        __syncwarp();
+        if (sc.next(ii, q, qw, ns)) {
+            const Item nit = item_at(st, ii);
+            if (lane == 0) {
+                issue_weights(a, st, nit, ring + stage * kStageBytes, &bars[warp][stage]);
+                issue_acts(a, st, nit, ring + stage * kStageBytes, &bars[warp][stage]);
+            }
+            ++issued;
+        }
+        // this item's fp32 partial: columns 2t, 2t+1 of rows gr, gr+8
+        const int row = it.rt * 16 + gr;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const int m = 2 * t + c;
             if (m < m_cnt) {
-                float* p = a.part + (static_cast<size_t>(kp0) * nslots + slot0 + m) * a.rows;
-                __stcg(p + row, acc[c]);
-                __stcg(p + row + 8, acc[2 + c]);
+                float* pp = a.part + (static_cast<size_t>(it.kp) * nslots + st.slot0[it.s] + m) * a.rows + row;
+                __stcg(pp, acc[c]);
+                __stcg(pp + 8, acc[2 + c]);
             }
-        }
-        __syncwarp();
-        int last = 0;
-        if (lane == 0) {
-            unsigned int* ctr;
-            unsigned int total;
-            if (!a.down) {
-                const int ftiles = a.f / 16;
-                ctr = a.counters + static_cast<size_t>(s) * ftiles + (rt >= ftiles ? rt - ftiles : rt);
-                total = 2u * static_cast<unsigned>(st.kp[s]);
-            } else {
-                ctr = a.counters + rt;
-                total = static_cast<unsigned>(st.items_per_rt);
-            }
-            // The completing warp reads the partials with L2-coherent ld.cg
-            // after observing the final count (no L1-invalidating acquire
-            // fence: every value it reads was written by other SMs to L2).
-            if (atom_add_release(ctr, static_cast<unsigned>(run_len)) + run_len == total) {
-                *ctr = 0;
-                last = 1;
-            }
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        ++n_runs;
-        if (last) {
-            ++n_epi;
-            if (!a.down)
-                epilogue_gateup(a, st, s, rt >= a.f / 16 ? rt - a.f / 16 : rt, lane);
-            else
-                epilogue_down(a, st, rt, lane);
         }
     }
+    ltrace(2 + 2 * a.p, 2);
     unsigned long long* tr = g_gemv_trace;
     if (tr != nullptr && lane == 0) {
-        tr += (static_cast<size_t>(a.down) * gridDim.x * kWarps + static_cast<size_t>(wid)) * 8;
+        tr += (static_cast<size_t>(a.p) * W + static_cast<size_t>(wid)) * 8;
         tr[0] = t_entry;
         tr[1] = t_wait;
         tr[2] = t_first;
         tr[3] = gtimer();
-        tr[4] = static_cast<unsigned long long>(i1 - i0);
-        tr[5] = static_cast<unsigned long long>(n_runs);
-        tr[6] = static_cast<unsigned long long>(n_epi);
-        tr[7] = static_cast<unsigned long long>(blockIdx.x);
+        tr[4] = static_cast<unsigned long long>(computed) | (static_cast<unsigned long long>(qw) << 32);
+        tr[5] = 0;
+        tr[6] = 0;
+        tr[7] = t_mbar;
     }
 }
 
-// x (natural, [rows][K]) -> K-permuted copy + per-128-group sums (fixed
-// xor-butterfly order).  One warp per (row, group); lane owns 4 elements.
+// Fixed-order reduction of the K-part partials of 4 consecutive rows of one
+// slot: thread (q, kg) of a (quads x kGroups) block sums K-parts kg, kg+kG,
+// ... with up to 8 loads in flight, then the kG partial sums are added in kg
+// order through shared memory -- deterministic for a given KP.
+constexpr int kFinThreads = 256;
+constexpr int kKG = 4;  // K-part groups per quad
+
+MOE_DEVI float4 sum_kparts(const float* p, size_t kstride, int KP, int kg) {
+    float4 acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int kp0 = kg; kp0 < KP; kp0 += 8 * kKG) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            v[u] = kp0 + u * kKG < KP ? __ldcg(reinterpret_cast<const float4*>(p + (kp0 + u * kKG) * kstride))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            acc[u].x += v[u].x; acc[u].y += v[u].y; acc[u].z += v[u].z; acc[u].w += v[u].w;
+        }
+    }
+#pragma unroll
+    for (int u = 1; u < 8; ++u) {
+        acc[0].x += acc[u].x; acc[0].y += acc[u].y; acc[0].z += acc[u].z; acc[0].w += acc[u].w;
+    }
+    return acc[0];
+}
+
+// SwiGLU finalize: one block per (slot, 128-row group g of h).  64 quads
+// (gate rows g*128.., up rows f+g*128..) x 4 K-part groups; h is rounded to
+// bf16 and stored as bf16 (perm_k) and its exact fp16 copy (perm_k16), plus
+// the group's int4 bias term 1032*S_lo + 72*S_hi.
+__global__ void __launch_bounds__(kFinThreads) finalize_h_kernel(
+    const float* __restrict__ part, const int* __restrict__ kpslot, int nslots, int f, uint16_t* __restrict__ hperm,
+    uint16_t* __restrict__ hperm16, float* __restrict__ hsum, int hstride, unsigned int* sched) {
+    __shared__ float4 red[kKG][64];
+    const int G = f / 128;
+    const int slot = blockIdx.x / G, g = blockIdx.x - slot * G;
+    ltrace(3, 0);
+    // Trigger first: the down-pass stream kernel only reads the routing
+    // before its own PDL wait, so its CTAs may start (and prefetch weights)
+    // as the gate/up stream's CTAs drain.
+    pdl_trigger();
+    pdl_wait();
+    ltrace(3, 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *sched = 0;  // the stream kernel is complete
+    const int KP = kpslot[slot];
+    if (KP == 0) return;
+    const size_t rows = static_cast<size_t>(2) * f;
+    const int q = threadIdx.x & 63, kg = threadIdx.x >> 6;
+    const int row = (q < 32 ? g * 128 + q * 4 : f + g * 128 + (q - 32) * 4);
+    red[kg][q] = sum_kparts(part + static_cast<size_t>(slot) * rows + row, static_cast<size_t>(nslots) * rows, KP, kg);
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    float gv[4], uv[4];
+    {
+        float4 a = red[0][lane], b = red[0][32 + lane];
+#pragma unroll
+        for (int k2 = 1; k2 < kKG; ++k2) {
+            const float4 c = red[k2][lane], e = red[k2][32 + lane];
+            a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+            b.x += e.x; b.y += e.y; b.z += e.z; b.w += e.w;
+        }
+        gv[0] = a.x; gv[1] = a.y; gv[2] = a.z; gv[3] = a.w;
+        uv[0] = b.x; uv[1] = b.y; uv[2] = b.z; uv[3] = b.w;
+    }
+    const int n0 = g * 128 + lane * 4;
+    float s = 0.0f;
+    const size_t o = static_cast<size_t>(slot) * f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint16_t hb = f2bf(silu_f(gv[j]) * uv[j]);
+        const float hv = bf2f(hb);
+        hperm[o + perm_k(n0 + j)] = hb;
+        hperm16[o + perm_k16(n0 + j)] = __half_as_ushort(__float2half_rn(hv));  // exact for 2^-17 <= |h| <= 65504
+        s += hv;
+    }
+    float s_lo = (lane & 2) ? 0.0f : s, s_hi = (lane & 2) ? s : 0.0f;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);
+        s_hi += __shfl_xor_sync(0xffffffffu, s_hi, off);
+    }
+    if (lane == 0) hsum[static_cast<size_t>(slot) * hstride + g] = 1032.0f * s_lo + 72.0f * s_hi;
+    ltrace(3, 2);
+}
+
+// Output finalize: one block per (token t, 256 output rows) -- or, with
+// out == null, per (slot, 256 rows) writing y itself for the slots of this
+// launch's experts.  y[slot][j] = fixed-order sum of the slot's pass-1
+// partials; out[t][j] = bf16(resid[t][j] + sum_jj w[t,jj] * y[inv[t,jj]][j])
+// (fp32 fma chain in jj order).
+__global__ void __launch_bounds__(kFinThreads) finalize_out_kernel(
+    const float* __restrict__ part, const int* __restrict__ kpslot, int T, int k, int d,
+    const int32_t* __restrict__ inv, const float* __restrict__ wts, const uint16_t* __restrict__ resid,
+    uint16_t* __restrict__ out, float* __restrict__ y, unsigned int* sched) {
+    __shared__ float4 red[kKG][64];
+    const int nslots = T * k;
+    const int nb = d / 256;
+    const int r = blockIdx.x / nb, j0 = (blockIdx.x - r * nb) * 256;
+    ltrace(5, 0);
+    pdl_trigger();  // the next layer's route kernel preloads router weights before its wait
+    pdl_wait();
+    ltrace(5, 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *sched = 0;
+    const size_t kstride = static_cast<size_t>(nslots) * d;
+    const int q = threadIdx.x & 63, kg = threadIdx.x >> 6;
+    const int j = j0 + q * 4;
+    if (out == nullptr) {
+        const int KP = kpslot[r];
+        if (KP == 0) return;
+        red[kg][q] = sum_kparts(part + static_cast<size_t>(r) * d + j, kstride, KP, kg);
+        __syncthreads();
+        if (kg != 0) return;
+        float4 a = red[0][q];
+#pragma unroll
+        for (int k2 = 1; k2 < kKG; ++k2) {
+            const float4 c = red[k2][q];
+            a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+        }
+        *reinterpret_cast<float4*>(y + static_cast<size_t>(r) * d + j) = a;
+        return;
+    }
+    const int t = r;
+    float acc[4];
+    if (kg == 0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = resid ? bf2f(resid[static_cast<size_t>(t) * d + j + u]) : 0.0f;
+    }
+    for (int jj = 0; jj < k; ++jj) {
+        const int slot = inv[t * k + jj];
+        const int KP = kpslot[slot];
+        red[kg][q] = KP ? sum_kparts(part + static_cast<size_t>(slot) * d + j, kstride, KP, kg)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncthreads();
+        if (kg == 0) {
+            float4 a = red[0][q];
+#pragma unroll
+            for (int k2 = 1; k2 < kKG; ++k2) {
+                const float4 c = red[k2][q];
+                a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+            }
+            const float w = wts[t * k + jj];
+            acc[0] = __fmaf_rn(w, a.x, acc[0]);
+            acc[1] = __fmaf_rn(w, a.y, acc[1]);
+            acc[2] = __fmaf_rn(w, a.z, acc[2]);
+            acc[3] = __fmaf_rn(w, a.w, acc[3]);
+        }
+        __syncthreads();
+    }
+    if (kg == 0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) out[static_cast<size_t>(t) * d + j + u] = f2bf(acc[u]);
+    }
+    ltrace(5, 2);
+}
+
+// x (natural, [rows][K]) -> K-permuted bf16 + fp16 copies and, per 128-K
+// group, the int4 bias term 1032*S_lo + 72*S_hi (S_lo: elements with
+// k%16 < 8, S_hi: the rest; fixed xor-butterfly order).  One warp per
+// (row, group); lane owns 4 elements.
 __global__ void permute_rows_kernel(const uint16_t* __restrict__ x, int rows, int K, uint16_t* __restrict__ xp,
-                                    float* __restrict__ xsum) {
+                                    uint16_t* __restrict__ xp16, float* __restrict__ xsum, int xstride) {
     const int G = K / 128;
     const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    ltrace(1, 0);
     pdl_wait();     // x is the previous layer's output
     pdl_trigger();
+    ltrace(1, 1);
+    ltrace(1, 2);
     if (wid >= static_cast<long long>(rows) * G) return;
     const long long r = wid / G;
     const int g = static_cast<int>(wid - r * G);
     const uint16_t* src = x + r * K + g * 128 + lane * 4;
     uint16_t* dst = xp + r * K + g * 128;
+    uint16_t* dst16 = xp16 + r * K + g * 128;
     float s = 0.0f;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const uint16_t v = src[j];
         dst[perm_k(lane * 4 + j)] = v;
+        dst16[perm_k16(lane * 4 + j)] = __half_as_ushort(__float2half_rn(bf2f(v)));  // exact for 2^-17 <= |x| <= 65504
         s += bf2f(v);
     }
+    float s_lo = (lane & 2) ? 0.0f : s, s_hi = (lane & 2) ? s : 0.0f;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) xsum[r * G + g] = s;
+    for (int off = 16; off >= 1; off >>= 1) {
+        s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);
+        s_hi += __shfl_xor_sync(0xffffffffu, s_hi, off);
+    }
+    if (lane == 0) xsum[r * xstride + g] = 1032.0f * s_lo + 72.0f * s_hi;
 }
 
-int host_pick_gk(int G, int maxgk) {
-    for (int g = maxgk; g > 1; g >>= 1)
-        if (G % g == 0) return g;
-    return 1;
-}
+int group_stride(int K) { return (K / 128 + 7) / 8 * 8; }
+}  // namespace moek
+int moek_group_stride(int K) { return moek::group_stride(K); }
+namespace moek {
 
-cudaError_t launch_pass(GemvArgs& a, cudaStream_t stream) {
+cudaError_t launch_stream(const StreamArgs& a, bool pdl, cudaStream_t stream) {
     static int grid = 0;
     const size_t smem = static_cast<size_t>(kWarps) * kStages * kStageBytes;
     if (grid == 0) {
-        MOE_CUDA_OK(cudaFuncSetAttribute(gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        MOE_CUDA_OK(cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int dev = 0, sms = 0;
         MOE_CUDA_OK(cudaGetDevice(&dev));
         MOE_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         grid = sms;
     }
-    const int G = a.K / 128;
-    a.gk4 = host_pick_gk(G, 8);
-    a.gk16 = host_pick_gk(G, 2);
-    return launch_pdl(gemv_kernel, dim3(grid), dim3(kThreads), smem, stream, a);
+    if (pdl) return launch_pdl(stream_kernel, dim3(grid), dim3(kThreads), smem, stream, a);
+    stream_kernel<<<grid, kThreads, smem, stream>>>(a);
+    return cudaGetLastError();
 }
 
 }  // namespace moek
@@ -622,25 +754,22 @@ namespace {
 size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
 struct WsSizes {
-    size_t xperm, xsum, hperm, hsum16, hsum, part, counters, gcounters;
+    size_t xperm, xperm16, xsum, hperm, hperm16, hsum, part0, part1, kpslot, sched;
 };
 
 WsSizes ws_sizes(int T, int k, int d, int f) {
     const size_t slots = static_cast<size_t>(T) * k;
     WsSizes w;
     w.xperm = static_cast<size_t>(T) * d * 2;
-    w.xsum = static_cast<size_t>(T) * (d / 128) * 4;
+    w.xperm16 = w.xperm;
+    w.xsum = static_cast<size_t>(T) * moek::group_stride(d) * 4;
     w.hperm = slots * f * 2;
-    w.hsum16 = slots * (f / 16) * 4;
-    w.hsum = slots * (f / 128) * 4;
-    // K-parts per pass <= number of 128-K groups
-    const size_t gu = static_cast<size_t>(d / 128) * slots * 2 * f;
-    const size_t dn = static_cast<size_t>(f / 128) * slots * d;
-    w.part = (gu > dn ? gu : dn) * 4;
-    const size_t cgu = static_cast<size_t>(moek::kMaxSegs) * (f / 16);
-    const size_t cdn = static_cast<size_t>(d) / 16;
-    w.counters = (cgu > cdn ? cgu : cdn) * 4;
-    w.gcounters = static_cast<size_t>(moek::kMaxSegs) * (f / 128) * 4;
+    w.hperm16 = w.hperm;
+    w.hsum = slots * moek::group_stride(f) * 4;
+    w.part0 = static_cast<size_t>(d / 128) * slots * 2 * f * 4;  // K-parts <= 128-K groups
+    w.part1 = static_cast<size_t>(f / 128) * slots * d * 4;
+    w.kpslot = slots * 2 * 4;
+    w.sched = 16;
     return w;
 }
 
@@ -650,47 +779,65 @@ cudaError_t moek_debug_gemv_trace(void* buf) {
     return cudaMemcpyToSymbol(moek::g_gemv_trace, &buf, sizeof(buf));
 }
 
+cudaError_t moek_debug_layer_trace_router(void* buf, cudaStream_t stream);
+cudaError_t moek_debug_layer_trace(void* buf, cudaStream_t stream) {
+    // stream-ordered (pinned staging), so a trace can cover exactly one replay
+    static void** host = nullptr;
+    if (host == nullptr) MOE_CUDA_OK(cudaMallocHost(&host, 64 * sizeof(void*)));
+    static int next = 0;
+    void** h = host + (next++ & 63);
+    *h = buf;
+    MOE_CUDA_OK(cudaMemcpyToSymbolAsync(moek::g_layer_trace, h, sizeof(buf), 0, cudaMemcpyHostToDevice, stream));
+    return moek_debug_layer_trace_router(h, stream);
+}
+
 size_t moek_gemv_workspace_bytes(int T, int k, int d, int f) {
     const WsSizes w = ws_sizes(T, k, d, f);
-    return align256(w.xperm) + align256(w.xsum) + align256(w.hperm) + align256(w.hsum16) + align256(w.hsum) +
-           align256(w.part) + align256(w.counters) + align256(w.gcounters);
+    return align256(w.xperm) + align256(w.xperm16) + align256(w.xsum) + align256(w.hperm) + align256(w.hperm16) +
+           align256(w.hsum) + align256(w.part0) + align256(w.part1) + align256(w.kpslot) + align256(w.sched);
 }
 
 GemvWorkspace moek_gemv_workspace_view(void* base, int T, int k, int d, int f) {
     const WsSizes w = ws_sizes(T, k, d, f);
     char* p = static_cast<char*>(base);
     GemvWorkspace ws{};
-    ws.xperm = p;
-    p += align256(w.xperm);
-    ws.xsum = reinterpret_cast<float*>(p);
-    p += align256(w.xsum);
-    ws.hperm = p;
-    p += align256(w.hperm);
-    ws.hsum16 = reinterpret_cast<float*>(p);
-    p += align256(w.hsum16);
-    ws.hsum = reinterpret_cast<float*>(p);
-    p += align256(w.hsum);
-    ws.part = reinterpret_cast<float*>(p);
-    p += align256(w.part);
-    ws.counters = reinterpret_cast<unsigned int*>(p);
-    p += align256(w.counters);
-    ws.gcounters = reinterpret_cast<unsigned int*>(p);
+    auto take = [&](size_t bytes) {
+        char* r = p;
+        p += align256(bytes);
+        return r;
+    };
+    ws.xperm = take(w.xperm);
+    ws.xperm16 = take(w.xperm16);
+    ws.xsum = reinterpret_cast<float*>(take(w.xsum));
+    ws.hperm = take(w.hperm);
+    ws.hperm16 = take(w.hperm16);
+    ws.hsum = reinterpret_cast<float*>(take(w.hsum));
+    ws.part0 = reinterpret_cast<float*>(take(w.part0));
+    ws.part1 = reinterpret_cast<float*>(take(w.part1));
+    ws.kpslot = reinterpret_cast<int*>(take(w.kpslot));
+    ws.sched = reinterpret_cast<unsigned int*>(take(w.sched));
     return ws;
 }
 
-cudaError_t moek_permute_rows(const void* x, int rows, int K, void* xperm, float* xsum, cudaStream_t stream) {
+cudaError_t moek_permute_rows(const void* x, int rows, int K, void* xperm, void* xperm16, float* xsum,
+                              cudaStream_t stream) {
     const long long warps = static_cast<long long>(rows) * (K / 128);
     if (warps == 0) return cudaSuccess;
     return moek::launch_pdl(moek::permute_rows_kernel, dim3(static_cast<unsigned>((warps * 32 + 255) / 256)), dim3(256),
-                            0, stream, static_cast<const uint16_t*>(x), rows, K, static_cast<uint16_t*>(xperm), xsum);
+                            0, stream, static_cast<const uint16_t*>(x), rows, K, static_cast<uint16_t*>(xperm),
+                            static_cast<uint16_t*>(xperm16), xsum, moek::group_stride(K));
 }
 
 cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* perm, const int32_t* offsets,
                          const int32_t* inv, const float* wts, const void* resid, int T, int k,
                          const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask, void* out,
-                         float* y, bool xperm_ready, cudaStream_t stream) {
-    if (!xperm_ready) MOE_CUDA_OK(moek_permute_rows(x, T, d, ws.xperm, ws.xsum, stream));
-    moek::GemvArgs a{};
+                         float* y, int xmode, cudaStream_t stream) {
+    // every (active expert, 8-token tile) segment must fit the kernel's table
+    if (E + (T * k + moek::kTile - 1) / moek::kTile > moek::kMaxSegs) return cudaErrorInvalidValue;
+    if (d % 256 != 0 || f % 128 != 0) return cudaErrorInvalidValue;
+    if (xmode == MOE_X_PERMUTE) MOE_CUDA_OK(moek_permute_rows(x, T, d, ws.xperm, ws.xperm16, ws.xsum, stream));
+    const int nslots = T * k;
+    moek::StreamArgs a{};
     a.offsets = offsets;
     a.perm = perm;
     a.T = T;
@@ -699,30 +846,41 @@ cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* 
     a.E = E;
     a.active_mask = active_mask;
     for (int e = 0; e < E; ++e) a.ex[e] = experts[e];
-    a.part = ws.part;
-    a.counters = ws.counters;
-    a.gcounters = ws.gcounters;
-    a.f = f;
-    // gate/up pass: [2f, d] x xperm -> hperm (fused SwiGLU + h group sums)
+    // gate/up pass
+    a.p = 0;
     a.rows = 2 * f;
     a.K = d;
-    a.down = 0;
-    a.bperm = static_cast<const uint16_t*>(ws.xperm);
+    a.b16 = static_cast<const uint16_t*>(ws.xperm);
+    a.b16h = static_cast<const uint16_t*>(ws.xperm16);
     a.bsum = ws.xsum;
-    a.hperm = static_cast<uint16_t*>(ws.hperm);
-    a.hsum16 = ws.hsum16;
-    a.hsum = ws.hsum;
-    MOE_CUDA_OK(moek::launch_pass(a, stream));
-    // down pass: [d, f] x hperm -> combine (or per-slot y)
+    a.bstride = moek::group_stride(d);
+    a.part = ws.part0;
+    a.kpslot = ws.kpslot;
+    a.sched = ws.sched;
+    a.wait_first = xmode == MOE_X_ROUTED ? 1 : 0;
+    MOE_CUDA_OK(moek::launch_stream(a, xmode != MOE_X_READY, stream));
+    {
+        MOE_CUDA_OK(moek::launch_pdl(moek::finalize_h_kernel, dim3(nslots * (f / 128)), dim3(moek::kFinThreads), 0, stream,
+                                     static_cast<const float*>(ws.part0), static_cast<const int*>(ws.kpslot), nslots, f,
+                                     static_cast<uint16_t*>(ws.hperm), static_cast<uint16_t*>(ws.hperm16), ws.hsum,
+                                     moek::group_stride(f), ws.sched));
+    }
+    // down pass
+    a.p = 1;
     a.rows = d;
     a.K = f;
-    a.down = 1;
-    a.bperm = static_cast<const uint16_t*>(ws.hperm);
+    a.b16 = static_cast<const uint16_t*>(ws.hperm);
+    a.b16h = static_cast<const uint16_t*>(ws.hperm16);
     a.bsum = ws.hsum;
-    a.wts = wts;
-    a.inv = inv;
-    a.resid = static_cast<const uint16_t*>(resid);
-    a.out = static_cast<uint16_t*>(out);
-    a.y = y;
-    return moek::launch_pass(a, stream);
+    a.bstride = moek::group_stride(f);
+    a.part = ws.part1;
+    a.kpslot = ws.kpslot + nslots;
+    a.sched = ws.sched + 1;
+    a.wait_first = 0;
+    MOE_CUDA_OK(moek::launch_stream(a, true, stream));
+    return moek::launch_pdl(moek::finalize_out_kernel, dim3(static_cast<unsigned>((out ? T : nslots) * (d / 256))),
+                            dim3(moek::kFinThreads), 0,
+                            stream, static_cast<const float*>(ws.part1), static_cast<const int*>(ws.kpslot + nslots), T, k,
+                            d, inv, wts, static_cast<const uint16_t*>(resid), static_cast<uint16_t*>(out), y,
+                            ws.sched + 1);
 }

@@ -8,33 +8,43 @@
 
 cudaError_t moek_route(const void* x, const void* wg, int T, int d, int E, int k, int32_t* idx,
                        float* w, float* logits, int32_t* counts, int32_t* offsets, int32_t* perm,
-                       int32_t* inv_perm, unsigned int* ticket, cudaStream_t stream);
+                       int32_t* inv_perm, unsigned int* ticket, cudaStream_t stream, void* xperm = nullptr,
+                       void* xperm16 = nullptr, float* xsum = nullptr, int xstride = 0, float norm_eps = 0.0f);
 cudaError_t moek_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_t* offsets,
                          int32_t* perm, int32_t* inv_perm, cudaStream_t stream);
 // Workspace of the tensor-core GEMV FFN (must be zeroed once; the kernels
 // leave the arrival counters at zero).
 struct GemvWorkspace {
     void* xperm;              // [T][d] bf16, K-permuted
-    float* xsum;              // [T][d/128] activation group sums
+    void* xperm16;            // [T][d] fp16 copy (B operand of int4 experts)
+    float* xsum;              // [T][*] int4 bias term per activation group
     void* hperm;              // [T*k][f] bf16, K-permuted
-    float* hsum16;            // [T*k][f/16]
-    float* hsum;              // [T*k][f/128]
-    float* part;              // zeroed partial run sums
-    unsigned int* counters;   // zeroed arrival counters
-    unsigned int* gcounters;  // zeroed per-(segment, h group) counters
+    void* hperm16;            // [T*k][f] fp16 copy
+    float* hsum;              // [T*k][*] int4 bias term per h group
+    float* part0;             // gate/up partials [d/128][T*k][2f]
+    float* part1;             // down partials [f/128][T*k][d]
+    int* kpslot;              // [2][T*k] K-parts per slot of the last stream launches
+    unsigned int* sched;      // tail-pool counters (reset by the finalize kernels)
 };
 // One zero-filled allocation of moek_gemv_workspace_bytes, carved by _view.
 size_t moek_gemv_workspace_bytes(int T, int k, int d, int f);
 GemvWorkspace moek_gemv_workspace_view(void* base, int T, int k, int d, int f);
-cudaError_t moek_permute_rows(const void* x, int rows, int K, void* xperm, float* xsum,
+cudaError_t moek_permute_rows(const void* x, int rows, int K, void* xperm, void* xperm16, float* xsum,
                               cudaStream_t stream);
 // Expert FFN of every active expert segment (bit e of active_mask): gate/up
 // GEMV + fused SwiGLU, down GEMV + fused combine (out != null: out[t] =
 // bf16(resid[t] + sum_j w[t,j] y[inv[t*k+j]])) or per-slot y (out == null).
+// xmode: how the K-permuted activations (ws.xperm*) come to be:
+//   MOE_X_PERMUTE  run the permute_rows kernel first (route two launches back)
+//   MOE_X_ROUTED   written by the route kernel launched immediately before
+//   MOE_X_READY    written earlier on the stream; launch without PDL (e.g.
+//                  after an event wait for a streamed expert)
+enum { MOE_X_PERMUTE = 0, MOE_X_ROUTED = 1, MOE_X_READY = 2 };
+int moek_group_stride(int K);
 cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* perm,
                          const int32_t* offsets, const int32_t* inv, const float* wts,
                          const void* resid, int T, int k, const moe_expert_weights* experts, int E,
-                         int d, int f, uint64_t active_mask, void* out, float* y, bool xperm_ready,
+                         int d, int f, uint64_t active_mask, void* out, float* y, int xmode,
                          cudaStream_t stream);
 // Storage-layout converters (logical row-major -> fragment blocks).
 cudaError_t moek_pack_bf16_blocks(const void* w, int rows, int cols, void* out, cudaStream_t stream);
@@ -50,3 +60,5 @@ int moek_weight_shift(int K);
 // Debug: per-warp phase trace buffer for the GEMV kernels (null disables);
 // [2 passes][148*warps][8] u64.
 cudaError_t moek_debug_gemv_trace(void* buf);
+// Debug: [6 kernels][entry, after wait, end] u64 globaltimer (min/min/max); null disables.
+cudaError_t moek_debug_layer_trace(void* buf, cudaStream_t stream);

@@ -86,7 +86,7 @@ __global__ void pack_bf16_blocks_kernel(const uint16_t* __restrict__ w, int rows
         const int rt = row >> 4, rr = row & 15, gr = rr & 7, half = rr >> 3;
         const int p = perm_pos(c & 127), r = p & 31, lane = gr * 4 + (p >> 5);
         const size_t blk = static_cast<size_t>(rt) * G + (c >> 7);
-        out[blk * 2048 + static_cast<size_t>(((half * 4 + (r >> 3)) * 32 + lane) * 8 + (r & 7))] = w[o];
+        out[blk * 2048 + static_cast<size_t>(((r >> 2) * 32 + lane) * 8 + (((r >> 1) & 1) * 2 + half) * 2 + (r & 1))] = w[o];
     }
 }
 

@@ -30,77 +30,189 @@ struct RouteArgs {
     int32_t* perm;
     int32_t* inv_perm;
     unsigned int* ticket;  // zero-initialised; reset by the last CTA
+    // fused K-permuted activation copies for the expert GEMV (optional)
+    uint16_t* xperm;
+    uint16_t* xperm16;
+    float* xsum;
+    int xstride;
+    float norm_eps;        // > 0: unit-weight RMSNorm of x before routing / experts (oracle orc_rmsnorm)
 };
 
 // One logit in the pinned order.  x_s is the token row staged in smem.
-MOE_DEVI float router_dot(const uint16_t* __restrict__ x_s, const uint16_t* __restrict__ we, int d,
-                          int lane) {
+constexpr int kPreChunks = 16;  // router-weight chunks (256 elements each) held in registers
+
+// One logit in the pinned order.  x_s is the token row staged in smem; the
+// first kPreChunks chunks of this lane's weights come preloaded in wpre
+// (issued before the PDL wait), the rest are loaded 8 chunks at a time.
+MOE_DEVI float router_dot(const uint16_t* __restrict__ x_s, const uint4 (&wpre)[kPreChunks],
+                          const uint16_t* __restrict__ we, int d, int lane) {
     float acc = 0.0f;
-    for (int c = 0; c * 256 < d; ++c) {
-        const int k0 = c * 256 + lane * 8;
-        if (k0 + 8 <= d) {
-            const uint4 wv = *reinterpret_cast<const uint4*>(we + k0);
-            const uint4 xv = *reinterpret_cast<const uint4*>(x_s + k0);
-            const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
-            const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
+    const int nfull = d / 256;  // chunks where every lane has 8 elements
+    auto fma8 = [&](const uint4& wv, int c) {
+        const uint4 xv = *reinterpret_cast<const uint4*>(x_s + c * 256 + lane * 8);
+        const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+        const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                acc = __fmaf_rn(bf16_lo(xx[q]), bf16_lo(ww[q]), acc);
-                acc = __fmaf_rn(bf16_hi(xx[q]), bf16_hi(ww[q]), acc);
-            }
-        } else {
-            for (int j = 0; j < 8 && k0 + j < d; ++j)
-                acc = __fmaf_rn(bf2f(x_s[k0 + j]), bf2f(we[k0 + j]), acc);
+        for (int q = 0; q < 4; ++q) {
+            acc = __fmaf_rn(bf16_lo(xx[q]), bf16_lo(ww[q]), acc);
+            acc = __fmaf_rn(bf16_hi(xx[q]), bf16_hi(ww[q]), acc);
         }
+    };
+#pragma unroll
+    for (int c = 0; c < kPreChunks; ++c)
+        if (c < nfull) fma8(wpre[c], c);
+    for (int c0 = kPreChunks; c0 < nfull; c0 += 8) {
+        uint4 wv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (c0 + u < nfull) wv[u] = __ldg(reinterpret_cast<const uint4*>(we + (c0 + u) * 256 + lane * 8));
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (c0 + u < nfull) fma8(wv[u], c0 + u);
+    }
+    {
+        const int k0 = nfull * 256 + lane * 8;  // ragged tail chunk
+        for (int j = 0; j < 8 && k0 + j < d; ++j) acc = __fmaf_rn(bf2f(x_s[k0 + j]), bf2f(we[k0 + j]), acc);
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
     return acc;
 }
 
-// Stable counting sort of n = T*k items by expert, one CTA, no atomics:
-// thread i owns the contiguous item range [i*per, (i+1)*per), and for every
-// expert a block-wide exclusive scan of the per-thread counts gives each
-// thread its write position, so ties keep ascending (t, j) order.
-MOE_DEVI void block_permute(const int32_t* idx, int n, int E, int32_t* counts,
-                            int32_t* offsets, int32_t* perm, int32_t* inv_perm, int* s_warp) {
-    const int tid = threadIdx.x, nth = blockDim.x;
-    const int lane = tid & 31, wid = tid >> 5, nwarps = nth >> 5;
-    const int per = (n + nth - 1) / nth;
-    const int i0 = min(n, tid * per), i1 = min(n, i0 + per);
-    int base = 0;
-    if (tid == 0) offsets[0] = 0;
-    for (int e = 0; e < E; ++e) {
-        int c = 0;
-        for (int i = i0; i < i1; ++i) c += idx[i] == e;
-        // inclusive warp scan
-        int incl = c;
+MOE_DEVI void preload_w(uint4 (&wpre)[kPreChunks], const uint16_t* __restrict__ we, int d, int lane) {
+    const int nfull = d / 256;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += v;
+    for (int c = 0; c < kPreChunks; ++c)
+        if (c < nfull) wpre[c] = __ldg(reinterpret_cast<const uint4*>(we + c * 256 + lane * 8));
+}
+
+// K-permuted position (must match gemv.cu perm_k / perm_k16)
+MOE_DEVI int rperm_k(int n) {
+    const int kin = n & 127, kk = kin >> 4;
+    return (n & ~127) + ((kk >> 1) * 4 + ((kin & 7) >> 1)) * 8 + ((kk & 1) * 2 + ((kin >> 3) & 1)) * 2 + (kin & 1);
+}
+MOE_DEVI int rperm_k16(int n) {
+    const int kin = n & 127, kk = kin >> 4;
+    return (n & ~127) + ((kk >> 1) * 4 + ((kin & 7) >> 1)) * 8 + (((kin >> 3) & 1) * 2 + (kk & 1)) * 2 + (kin & 1);
+}
+
+// Stable counting sort of n = T*k items by expert, one CTA, no global
+// atomics: per 256-item chunk every warp ballots each expert (rank inside
+// the warp = popc of the lower lanes), a per-chunk warp prefix in shared
+// memory orders the warps, and a running per-expert base orders the chunks
+// -- so ties keep ascending (t, j) order.  Two passes: counts, positions.
+MOE_DEVI void block_permute(const int32_t* idx, int n, int E, int32_t* counts, int32_t* offsets, int32_t* perm,
+                            int32_t* inv_perm) {
+    __shared__ int s_cnt[kRouteThreads / 32][MOE_MAX_EXPERTS];
+    __shared__ int s_off[MOE_MAX_EXPERTS + 1];
+    __shared__ int s_run[MOE_MAX_EXPERTS];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    if (tid < E) {
+        s_off[tid] = 0;
+        s_run[tid] = 0;
+    }
+    __syncthreads();
+    // pass 1: per-expert totals
+    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+        const int i = c0 + tid;
+        const int ei = i < n ? idx[i] : -1;
+        for (int e = 0; e < E; ++e) {
+            const unsigned m = __ballot_sync(0xffffffffu, ei == e);
+            if (lane == 0 && m) atomicAdd(&s_off[e], __popc(m));
         }
-        if (lane == 31) s_warp[wid] = incl;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int acc = 0;
+        for (int e = 0; e < E; ++e) {
+            const int c = s_off[e];
+            counts[e] = c;
+            s_off[e] = acc;
+            offsets[e] = acc;
+            acc += c;
+        }
+        s_off[E] = acc;
+        offsets[E] = acc;
+    }
+    __syncthreads();
+    // pass 2: stable positions
+    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+        const int i = c0 + tid;
+        const int ei = i < n ? idx[i] : -1;
+        int rank = 0;
+        for (int e = 0; e < E; ++e) {
+            const unsigned m = __ballot_sync(0xffffffffu, ei == e);
+            if (lane == 0) s_cnt[wid][e] = __popc(m);
+            if (ei == e) rank = __popc(m & lt);
+        }
         __syncthreads();
-        int warp_base = 0, total = 0;
-        for (int w = 0; w < nwarps; ++w) {
-            const int v = s_warp[w];
-            if (w < wid) warp_base += v;
-            total += v;
+        if (i < n) {
+            int pos = s_off[ei] + s_run[ei] + rank;
+            for (int w = 0; w < wid; ++w) pos += s_cnt[w][ei];
+            perm[pos] = i;
+            inv_perm[i] = pos;
         }
-        int pos = base + warp_base + incl - c;
-        for (int i = i0; i < i1; ++i)
-            if (idx[i] == e) {
-                perm[pos] = i;
-                inv_perm[i] = pos;
-                ++pos;
+        __syncthreads();
+        if (tid < E)
+            for (int w = 0; w < nw; ++w) s_run[tid] += s_cnt[w][tid];
+        __syncthreads();
+    }
+}
+
+// Top-k on logits by one warp, in registers: lane e holds logits e and
+// e+32; k rounds of a butterfly argmax (ties -> lower index) give the
+// selection in descending-logit order; weights = softmax over the selected
+// logits (sequential j order, as the oracle).
+MOE_DEVI void warp_topk(const float* lg, int E, int k, int lane, int32_t* idx_out, float* w_out, int* s_idx) {
+    float v0 = lane < E ? lg[lane] : 0.0f, v1 = lane + 32 < E ? lg[lane + 32] : 0.0f;
+    bool ok0 = lane < E, ok1 = lane + 32 < E;
+    float sel[MOE_MAX_TOPK];
+    int sid[MOE_MAX_TOPK];
+#pragma unroll
+    for (int j = 0; j < MOE_MAX_TOPK; ++j) {
+        sel[j] = 0.0f;
+        sid[j] = 0;
+        if (j < k) {
+            bool has;
+            float bv;
+            int bi;
+            if (ok1 && (!ok0 || v1 > v0)) {
+                has = true; bv = v1; bi = lane + 32;
+            } else {
+                has = ok0; bv = v0; bi = lane;
             }
-        if (tid == 0) {
-            counts[e] = total;
-            offsets[e + 1] = base + total;
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                const bool oh = __shfl_xor_sync(0xffffffffu, has ? 1 : 0, off) != 0;
+                if (oh && (!has || ov > bv || (ov == bv && oi < bi))) {
+                    bv = ov;
+                    bi = oi;
+                    has = true;
+                }
+            }
+            sel[j] = bv;
+            sid[j] = bi;
+            if (bi == lane) ok0 = false;
+            if (bi == lane + 32) ok1 = false;
         }
-        base += total;
-        __syncthreads();
+    }
+    if (lane == 0) {
+        float ex[MOE_MAX_TOPK], sum = 0.0f;
+#pragma unroll
+        for (int j = 0; j < MOE_MAX_TOPK; ++j) {
+            ex[j] = j < k ? expf(sel[j] - sel[0]) : 0.0f;
+            if (j < k) sum += ex[j];
+        }
+#pragma unroll
+        for (int j = 0; j < MOE_MAX_TOPK; ++j)
+            if (j < k) {
+                idx_out[j] = sid[j];
+                w_out[j] = ex[j] / sum;
+                s_idx[j] = sid[j];
+            }
     }
 }
 
@@ -108,13 +220,19 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint16_t* x_s = reinterpret_cast<uint16_t*>(smem);
     float* lg_s = reinterpret_cast<float*>(smem + ((a.d * 2 + 15) / 16) * 16);
-    __shared__ int s_warp[kRouteThreads / 32];
+    __shared__ int s_idx[MOE_MAX_TOPK];
     __shared__ bool s_last;
 
     const int t = blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    ltrace(0, 0);
+    // The router weights do not depend on the previous layer: this warp's
+    // first expert row goes into registers before the PDL wait.
+    uint4 wpre[kPreChunks];
+    if (wid < a.E) preload_w(wpre, a.wg + static_cast<size_t>(wid) * a.d, a.d, lane);
     pdl_wait();     // x is the previous layer's output
     pdl_trigger();
+    ltrace(0, 1);
     const uint16_t* xt = a.x + static_cast<size_t>(t) * a.d;
     for (int i = threadIdx.x * 8; i < a.d; i += blockDim.x * 8) {
         if (i + 8 <= a.d)
@@ -123,48 +241,92 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
             for (int j = i; j < a.d; ++j) x_s[j] = xt[j];
     }
     __syncthreads();
+    if (a.norm_eps > 0.0f) {
+        // pinned order: thread i's fmaf chain over x[c*256+i]^2, then the
+        // pairwise tree over 256 partials (orc_rmsnorm)
+        float acc = 0.0f;
+        for (int c = 0; c * 256 + static_cast<int>(threadIdx.x) < a.d; ++c) {
+            const float v = bf2f(x_s[c * 256 + threadIdx.x]);
+            acc = __fmaf_rn(v, v, acc);
+        }
+        lg_s[MOE_MAX_EXPERTS + threadIdx.x] = acc;
+        __syncthreads();
+        for (int s2 = 128; s2 >= 1; s2 >>= 1) {
+            if (static_cast<int>(threadIdx.x) < s2)
+                lg_s[MOE_MAX_EXPERTS + threadIdx.x] =
+                    __fadd_rn(lg_s[MOE_MAX_EXPERTS + threadIdx.x], lg_s[MOE_MAX_EXPERTS + threadIdx.x + s2]);
+            __syncthreads();
+        }
+        const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(lg_s[MOE_MAX_EXPERTS],
+                                                                            static_cast<float>(a.d)), a.norm_eps)));
+        for (int i = threadIdx.x; i < a.d; i += blockDim.x) x_s[i] = f2bf(__fmul_rn(bf2f(x_s[i]), rstd));
+        __syncthreads();
+    }
+    ltrace(1, 0);
     for (int e = wid; e < a.E; e += blockDim.x / 32) {
-        const float v = router_dot(x_s, a.wg + static_cast<size_t>(e) * a.d, a.d, lane);
+        if (e != wid) preload_w(wpre, a.wg + static_cast<size_t>(e) * a.d, a.d, lane);
+        const float v = router_dot(x_s, wpre, a.wg + static_cast<size_t>(e) * a.d, a.d, lane);
         if (lane == 0) lg_s[e] = v;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        if (a.logits)
-            for (int e = 0; e < a.E; ++e) a.logits[static_cast<size_t>(t) * a.E + e] = lg_s[e];
-        uint64_t taken = 0;
-        float sel[MOE_MAX_TOPK];
-        for (int j = 0; j < a.k; ++j) {
-            int best = -1;
-            for (int e = 0; e < a.E; ++e)
-                if (!((taken >> e) & 1ull) && (best < 0 || lg_s[e] > lg_s[best])) best = e;
-            taken |= 1ull << best;
-            a.idx[static_cast<size_t>(t) * a.k + j] = best;
-            sel[j] = lg_s[best];
+    ltrace(1, 1);
+    if (a.logits && threadIdx.x < a.E) a.logits[static_cast<size_t>(t) * a.E + threadIdx.x] = lg_s[threadIdx.x];
+    if (wid == 0) warp_topk(lg_s, a.E, a.k, lane, a.idx + static_cast<size_t>(t) * a.k, a.w + static_cast<size_t>(t) * a.k, s_idx);
+    // K-permuted bf16 / fp16 copies of this token row + int4 bias terms
+    // (same definition as gemv.cu permute_rows_kernel), one warp per group
+    if (a.xperm != nullptr) {
+        const int G = a.d / 128;
+        for (int g = wid; g < G; g += blockDim.x / 32) {
+            float sm = 0.0f;
+            uint16_t* dst = a.xperm + static_cast<size_t>(t) * a.d + g * 128;
+            uint16_t* dst16 = a.xperm16 + static_cast<size_t>(t) * a.d + g * 128;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint16_t v = x_s[g * 128 + lane * 4 + j];
+                dst[rperm_k(lane * 4 + j)] = v;
+                dst16[rperm_k16(lane * 4 + j)] = __half_as_ushort(__float2half_rn(bf2f(v)));
+                sm += bf2f(v);
+            }
+            float s_lo = (lane & 2) ? 0.0f : sm, s_hi = (lane & 2) ? sm : 0.0f;
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+                s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);
+                s_hi += __shfl_xor_sync(0xffffffffu, s_hi, off);
+            }
+            if (lane == 0) a.xsum[static_cast<size_t>(t) * a.xstride + g] = 1032.0f * s_lo + 72.0f * s_hi;
         }
-        float ex[MOE_MAX_TOPK], sum = 0.0f;
-        for (int j = 0; j < a.k; ++j) {
-            ex[j] = expf(sel[j] - sel[0]);
-            sum += ex[j];
-        }
-        for (int j = 0; j < a.k; ++j) a.w[static_cast<size_t>(t) * a.k + j] = ex[j] / sum;
     }
-    if (a.counts == nullptr) return;
+    if (a.counts == nullptr) {
+        ltrace(0, 2);
+        return;
+    }
+    if (gridDim.x == 1) {
+        // single token: permute straight from shared memory
+        __syncthreads();
+        ltrace(1, 2);
+        block_permute(s_idx, a.k, a.E, a.counts, a.offsets, a.perm, a.inv_perm);
+        ltrace(0, 2);
+        return;
+    }
     // Fused K2: the last CTA to finish permutes all tokens.
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
     __syncthreads();
-    if (!s_last) return;
+    if (!s_last) {
+        ltrace(0, 2);
+        return;
+    }
     __threadfence();
-    block_permute(a.idx, a.T * a.k, a.E, a.counts, a.offsets, a.perm, a.inv_perm, s_warp);
+    block_permute(a.idx, a.T * a.k, a.E, a.counts, a.offsets, a.perm, a.inv_perm);
     if (threadIdx.x == 0) *a.ticket = 0;
+    ltrace(0, 2);
 }
 
-__global__ void __launch_bounds__(512) permute_kernel(const int32_t* idx, int n, int E,
-                                                      int32_t* counts, int32_t* offsets,
-                                                      int32_t* perm, int32_t* inv_perm) {
-    __shared__ int s_warp[16];
-    block_permute(idx, n, E, counts, offsets, perm, inv_perm, s_warp);
+__global__ void __launch_bounds__(kRouteThreads) permute_kernel(const int32_t* idx, int n, int E,
+                                                                int32_t* counts, int32_t* offsets,
+                                                                int32_t* perm, int32_t* inv_perm) {
+    block_permute(idx, n, E, counts, offsets, perm, inv_perm);
 }
 
 }  // namespace moek
@@ -173,10 +335,13 @@ __global__ void __launch_bounds__(512) permute_kernel(const int32_t* idx, int n,
 // launchers (called by capi.cu / engine.cu)
 cudaError_t moek_route(const void* x, const void* wg, int T, int d, int E, int k, int32_t* idx,
                        float* w, float* logits, int32_t* counts, int32_t* offsets, int32_t* perm,
-                       int32_t* inv_perm, unsigned int* ticket, cudaStream_t stream) {
+                       int32_t* inv_perm, unsigned int* ticket, cudaStream_t stream, void* xperm, void* xperm16,
+                       float* xsum, int xstride, float norm_eps) {
     moek::RouteArgs a{static_cast<const uint16_t*>(x), static_cast<const uint16_t*>(wg), T, d, E, k,
-                      idx, w, logits, counts, offsets, perm, inv_perm, ticket};
-    const size_t smem = ((static_cast<size_t>(d) * 2 + 15) / 16) * 16 + static_cast<size_t>(E) * 4;
+                      idx, w, logits, counts, offsets, perm, inv_perm, ticket,
+                      static_cast<uint16_t*>(xperm), static_cast<uint16_t*>(xperm16), xsum, xstride, norm_eps};
+    // x row + logits [MOE_MAX_EXPERTS] + RMSNorm partials [kRouteThreads]
+    const size_t smem = ((static_cast<size_t>(d) * 2 + 15) / 16) * 16 + (MOE_MAX_EXPERTS + moek::kRouteThreads) * 4;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(moek::route_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -188,6 +353,10 @@ cudaError_t moek_route(const void* x, const void* wg, int T, int d, int E, int k
 
 cudaError_t moek_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_t* offsets,
                          int32_t* perm, int32_t* inv_perm, cudaStream_t stream) {
-    moek::permute_kernel<<<1, 512, 0, stream>>>(idx, T * k, E, counts, offsets, perm, inv_perm);
+    moek::permute_kernel<<<1, moek::kRouteThreads, 0, stream>>>(idx, T * k, E, counts, offsets, perm, inv_perm);
     return cudaGetLastError();
+}
+
+cudaError_t moek_debug_layer_trace_router(void* host_ptr, cudaStream_t stream) {
+    return cudaMemcpyToSymbolAsync(moek::g_layer_trace, host_ptr, sizeof(void*), 0, cudaMemcpyHostToDevice, stream);
 }

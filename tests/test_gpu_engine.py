@@ -25,9 +25,9 @@ def quality_plan(moe, cfg, n4, seed, budget=10**15):
     return prof, moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, seed), moe.HardwareProfile(budget), prof)
 
 
-def make_engine(moe, cfg, plan, seed, T=1, graphs=True):
+def make_engine(moe, cfg, plan, seed, T=1, graphs=True, eps=0.0):
     return moe.MoeEngine(cfg["num_layers"], cfg["experts_per_layer"], cfg["top_k"], cfg["d_model"], cfg["d_ffn"],
-                         plan, max_tokens=T, seed=seed, use_graphs=graphs)
+                         plan, max_tokens=T, seed=seed, use_graphs=graphs, norm_eps=eps)
 
 
 def layer_precisions(plan, layer, E):
@@ -40,13 +40,16 @@ def test_tiny_plan_is_4_of_8_per_layer(moe):
     assert plan.n_gpu == 16
 
 
+@pytest.mark.parametrize("eps", [0.0, 1e-5])
 @pytest.mark.parametrize("T", [1, 3, 4, 8])
-def test_tiny_layer_parity(moe, orc, torch_mod, cuda, T):
+def test_tiny_layer_parity(moe, orc, torch_mod, cuda, T, eps):
+    """eps > 0: the decoder-layer RMSNorm fused into the route kernel --
+    normalised x must be bit-identical to the oracle's (logits are)."""
     torch = torch_mod
     seed = 42
     _, plan = quality_plan(moe, TINY, 8, 1)
-    eng = make_engine(moe, TINY, plan, seed, T)
-    m = orc.model(2, 8, 2, 512, 1792, seed)
+    eng = make_engine(moe, TINY, plan, seed, T, eps=eps)
+    m = orc.model(2, 8, 2, 512, 1792, seed, eps)
     x = orc.step_input(m, 0, T)
     for layer in range(2):
         prec = layer_precisions(plan, layer, 8)
@@ -66,14 +69,15 @@ def test_tiny_layer_parity(moe, orc, torch_mod, cuda, T):
     eng.close()
 
 
-def test_tiny_decode_32_steps(moe, orc, torch_mod, cuda):
+@pytest.mark.parametrize("eps", [0.0, 1e-5])
+def test_tiny_decode_32_steps(moe, orc, torch_mod, cuda, eps):
     """C1: 32-token decode through the stack (CUDA graph), vs the oracle
     stack run free on the same step inputs."""
     torch = torch_mod
     seed = 42
     prof, plan = quality_plan(moe, TINY, 8, 1)
-    eng = make_engine(moe, TINY, plan, seed, 1, graphs=True)
-    m = orc.model(2, 8, 2, 512, 1792, seed)
+    eng = make_engine(moe, TINY, plan, seed, 1, graphs=True, eps=eps)
+    m = orc.model(2, 8, 2, 512, 1792, seed, eps)
     flips = 0
     for step in range(32):
         eng.synth_input(step, 1)
@@ -185,4 +189,25 @@ def test_mixtral_layer_parity(moe, orc, torch_mod, cuda, precision, T):
     assert np.array_equal(to_np(idx, np.int32).reshape(T, 2), idx_ref)
     assert_close(bf16_to_f32(to_np(out, np.uint16).reshape(T, 4096)), bf16_to_f32(out_ref), RTOL_BF16,
                  f"mixtral layer {'bf16' if precision else 'int4'}")
+    eng.close()
+
+
+def test_mixtral_stack_prenorm_is_finite(moe, torch_mod, cuda):
+    """C3 workload sanity: the full 32-layer Mixtral-shaped stack with the
+    decoder-layer RMSNorm stays finite and routes k distinct experts in every
+    layer (without the norm the synthetic residual stream overflows and the
+    routing degenerates -- a bench on it would be invalid)."""
+    torch = torch_mod
+    cfg = dict(MIXTRAL)
+    prof = moe.profile_for_shape(4096, 14336, 32)
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, 128, 0), moe.HardwareProfile(10**15), prof)
+    eng = make_engine(moe, cfg, plan, 0, 1, graphs=True, eps=1e-5)
+    for step in range(4):
+        eng.synth_input(step, 1)
+        eng.decode(1)
+        eng.sync()
+        out = bf16_to_f32(read_device(torch, eng.output_ptr, 4096 * 2).view(np.uint16))
+        assert np.isfinite(out).all()
+        r = eng.last_routing(1)
+        assert all(r[2 * l] != r[2 * l + 1] for l in range(32))
     eng.close()

@@ -117,3 +117,31 @@ def test_reference_kat_planner_and_simulator(moe):
         r = moe.simulate(plan, slots, 50, prof, hw)
         assert [r.activations, r.hits, r.bytes_transferred, r.transfer_ns, r.compute_ns, r.nonexpert_ns] == c["sim"]
         assert moe.expected_throughput(plan, prof, hw) == c["expected_tps"]
+
+
+def test_rmsnorm_pinned_order(orc):
+    """orc_rmsnorm restated in numpy with the same pinned reduction order
+    (per-thread fmaf chains over x[c*256+i]^2, pairwise tree, IEEE 1/sqrt)."""
+    import numpy as np
+    rng = np.random.default_rng(5)
+    for d in (512, 4096, 768):
+        x = (rng.integers(-64, 65, size=(3, d)) / 64.0).astype(np.float32)
+        xb = (x.view(np.uint32) >> 16).astype(np.uint16)
+        got = orc.rmsnorm(xb, 3, d, 1e-5)
+        for t in range(3):
+            xf = ((xb[t].astype(np.uint32)) << 16).view(np.float32)
+            part = np.zeros(256, np.float32)
+            for i in range(256):
+                acc = np.float32(0)
+                for c in range((d - i + 255) // 256):
+                    v = xf[c * 256 + i]
+                    acc = np.float32(np.float64(v) * v + acc)  # fmaf: exact product, one rounding
+                part[i] = acc
+            s2 = 128
+            while s2 >= 1:
+                part[:s2] = part[:s2] + part[s2:2 * s2]
+                s2 //= 2
+            rstd = np.float32(1.0) / np.sqrt(np.float32(part[0] / np.float32(d) + np.float32(1e-5)))
+            ref = xf * rstd
+            refb = ((ref.view(np.uint32) + 0x7FFF + ((ref.view(np.uint32) >> 16) & 1)) >> 16).astype(np.uint16)
+            assert np.array_equal(got[t], refb), d
