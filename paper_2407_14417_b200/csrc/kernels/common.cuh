@@ -104,6 +104,36 @@ constexpr float kInt4Bias = 136.0f;  // 128 (magic) + 8 (storage bias)
 MOE_DEVI void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 MOE_DEVI void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// One 16-byte chunk of the K-permuted activation copies of a 128-element
+// group g (natural order in xg, any address space): chunk c*4+t holds, for
+// kk in {2c, 2c+1}, hi in {0,1}, e in {0,1}, the element kk*16 + hi*8 + t*2 + e:
+//   bf16 copy (perm_k):   word (kk%2)*2 + hi
+//   fp16 copy (perm_k16): word hi*2 + kk%2      (fp16 exact for 2^-17 <= |x| <= 65504)
+// Also returns this chunk's partial sums over k%16 < 8 (hi = 0) and >= 8
+// (hi = 1) for the int4 bias term (summed in element order kk, e).
+template <class T>
+MOE_DEVI void permute_chunk(const T* xg, int chunk, uint4& cb, uint4& ch, float& s_lo, float& s_hi) {
+    const int c = chunk >> 2, t = chunk & 3;
+    uint32_t wb[4], wh[4];
+    s_lo = 0.0f;
+    s_hi = 0.0f;
+#pragma unroll
+    for (int kq = 0; kq < 2; ++kq) {
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi) {
+            const int n = (2 * c + kq) * 16 + hi * 8 + t * 2;
+            const uint16_t v0 = static_cast<uint16_t>(xg[n]), v1 = static_cast<uint16_t>(xg[n + 1]);
+            const float f0 = bf2f(v0), f1 = bf2f(v1);
+            wb[kq * 2 + hi] = static_cast<uint32_t>(v0) | (static_cast<uint32_t>(v1) << 16);
+            wh[hi * 2 + kq] = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f0))) |
+                              (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f1))) << 16);
+            if (hi) s_hi += f0 + f1; else s_lo += f0 + f1;
+        }
+    }
+    cb = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+    ch = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+}
+
 // Debug layer trace (moe_debug_layer_trace): per kernel id, the earliest
 // entry and post-PDL-wait globaltimer stamps (atomicMin) and the latest warp
 // end (atomicMax).  One copy per translation unit (no -rdc); null = off.

@@ -38,19 +38,34 @@
 
 namespace moek {
 
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
 constexpr int kStages = 2;
 constexpr int kTile = 8;                 // tokens per segment tile (MMA n)
 constexpr int kMaxSegs = 64;             // (active expert, 8-token tile) segments per launch
-// stage layout: [weights <= 8 KB][int4 scales <= 256 B][activation rows][bias terms]
-constexpr int kStageW = 0;
-constexpr int kStageS = 8192;
-constexpr int kStageB = 8192 + 256;
-constexpr int kBRowPad = 64;             // row stride = GK*256 + 64: conflict-free LDS.128
-constexpr int kStageBBytes = 4608;       // m * (GK*256 + 64) <= 4608 for every (m, GK) used
-constexpr int kStageX = kStageB + kStageBBytes;
-constexpr int kStageBytes = kStageX + kTile * 32;
+constexpr int kBRowPad = 64;             // activation row stride in a stage = GK*256 + 64: conflict-free LDS.128
+
+// Stream-kernel configurations.  Stage layout: [weights <= W][int4 scales
+// <= W/32][activation rows <= B][bias terms 8 x 32 B].
+//   Batch : 8 warps, 8 KB weight items; activation area for up to 8 token
+//           rows (GK shrinks with the rows: m * (GK*256+64) <= B).
+//   Decode: 16 warps (4 per SM sub-partition, to hide the int4 decode /
+//           HMMA dependency chains), 4 KB weight items, one token row.
+template <int WARPS, int W, int B>
+struct StreamCfg {
+    static constexpr int kWarps = WARPS;
+    static constexpr int kThreads = WARPS * 32;
+    static constexpr int kW = W;
+    static constexpr int kS = W / 32;
+    static constexpr int kBBytes = B;
+    static constexpr int kStageW = 0;
+    static constexpr int kStageS = W;
+    static constexpr int kStageB = W + W / 32;
+    static constexpr int kStageX = kStageB + B;
+    static constexpr int kStageBytes = (kStageX + kTile * 32 + 127) / 128 * 128;
+    static constexpr int kGk4 = W / 1024;   // max 128-K groups per int4 item
+    static constexpr int kGk16 = W / 4096;  // max 128-K groups per bf16 item
+};
+using CfgBatch = StreamCfg<8, 8192, 4608>;
+using CfgDecode = StreamCfg<16, 4096, 1088>;
 constexpr int kChunk = 2;                // items per dynamic tail chunk
 constexpr int kMaxSlots = 512;           // permutation slots staged in smem by build_segs
 
@@ -112,6 +127,20 @@ MOE_DEVI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+// bulk copy with an L2 cache-policy hint (evict_first for streamed weights,
+// so the partials / activations the finalize kernels re-read stay in L2)
+MOE_DEVI void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+MOE_DEVI uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 MOE_DEVI void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // Release-only arrival: orders this warp's partial stores (after __syncwarp)
@@ -230,9 +259,10 @@ MOE_DEVI int perm_k16(int n) {
 
 // 128-K groups per item: the largest power of two <= cap dividing G, where
 // cap keeps m activation rows of the item inside the stage.
+template <class C>
 MOE_DEVI int pick_gk(int G, int prec, int m) {
-    int cap = prec == MOE_P4 ? 8 : 2;
-    while (cap > 1 && m * (cap * 256 + kBRowPad) > kStageBBytes) cap >>= 1;
+    int cap = prec == MOE_P4 ? C::kGk4 : C::kGk16;
+    while (cap > 1 && m * (cap * 256 + kBRowPad) > C::kBBytes) cap >>= 1;
     while (cap > 1 && G % cap) cap >>= 1;
     return cap;
 }
@@ -240,6 +270,7 @@ MOE_DEVI int pick_gk(int G, int prec, int m) {
 // Segment table (one segment per (active expert, 8-token tile)), built
 // redundantly by every CTA from the routing; CTA 0 also publishes each
 // slot's K-part count for the finalize kernel.
+template <class C>
 MOE_DEVI void build_segs(const StreamArgs& a, SegTable& st, int* cnt, int* sperm) {
     // offsets and perm in one round trip
     const int nslots = a.T * a.k;
@@ -264,7 +295,7 @@ MOE_DEVI void build_segs(const StreamArgs& a, SegTable& st, int* cnt, int* sperm
             const moe_expert_weights& W = a.ex[e];
             for (int t = 0; t * kTile < m && n < kMaxSegs; ++t) {
                 const int mc = min(kTile, m - t * kTile);
-                const int gk = pick_gk(G, W.precision, mc);
+                const int gk = pick_gk<C>(G, W.precision, mc);
                 st.e[n] = e;
                 st.slot0[n] = cnt[MOE_MAX_EXPERTS + e] + t * kTile;
                 st.mcnt[n] = mc;
@@ -316,17 +347,20 @@ MOE_DEVI Item item_at(const SegTable& st, int i) {
 }
 
 // Issue the weight half of an item (expect_tx covers the whole item).
-MOE_DEVI void issue_weights(const StreamArgs& a, const SegTable& st, const Item& it, uint8_t* stage, uint64_t* bar) {
+template <class C>
+MOE_DEVI void issue_weights(const StreamArgs& a, const SegTable& st, const Item& it, uint8_t* stage, uint64_t* bar,
+                            uint64_t pol) {
     const int s = it.s, wb = st.wbytes[s], sb = st.sbytes[s], m = st.mcnt[s];
     mbar_expect_tx(bar, wb + sb + m * st.gk[s] * 256 + (sb ? m * 32 : 0));
     const size_t blk = static_cast<size_t>(it.rt) * (a.K / 128) + static_cast<size_t>(it.kp) * st.gk[s];
-    bulk_g2s(stage + kStageW, st.wptr[s] + blk * (sb ? 1024 : 4096), wb, bar);
-    if (sb) bulk_g2s(stage + kStageS, st.sptr[s] + blk * 32, sb, bar);
+    bulk_g2s_hint(stage + C::kStageW, st.wptr[s] + blk * (sb ? 1024 : 4096), wb, bar, pol);
+    if (sb) bulk_g2s_hint(stage + C::kStageS, st.sptr[s] + blk * 32, sb, bar, pol);
 }
 
 // Issue the activation half: the item's K slice of every token row of the
 // segment (fp16 copy for int4, bf16 for bf16) and, for int4, the 32-byte
 // bias-term chunk holding the item's groups.
+template <class C>
 MOE_DEVI void issue_acts(const StreamArgs& a, const SegTable& st, const Item& it, uint8_t* stage, uint64_t* bar) {
     const int s = it.s, m = st.mcnt[s], gk = st.gk[s];
     const int rowb = gk * 256;
@@ -335,31 +369,46 @@ MOE_DEVI void issue_acts(const StreamArgs& a, const SegTable& st, const Item& it
         const int g8 = (it.kp * gk) & ~7;
         for (int r = 0; r < m; ++r) {
             const int br = st.brow[s][r];
-            bulk_g2s(stage + kStageB + r * (rowb + kBRowPad), a.b16h + static_cast<size_t>(br) * a.K + k0, rowb, bar);
-            bulk_g2s(stage + kStageX + r * 32, a.bsum + static_cast<size_t>(br) * a.bstride + g8, 32, bar);
+            bulk_g2s(stage + C::kStageB + r * (rowb + kBRowPad), a.b16h + static_cast<size_t>(br) * a.K + k0, rowb, bar);
+            bulk_g2s(stage + C::kStageX + r * 32, a.bsum + static_cast<size_t>(br) * a.bstride + g8, 32, bar);
         }
     } else {
         for (int r = 0; r < m; ++r)
-            bulk_g2s(stage + kStageB + r * (rowb + kBRowPad), a.b16 + static_cast<size_t>(st.brow[s][r]) * a.K + k0,
+            bulk_g2s(stage + C::kStageB + r * (rowb + kBRowPad), a.b16 + static_cast<size_t>(st.brow[s][r]) * a.K + k0,
                      rowb, bar);
     }
 }
 
 // Item sequence of one warp: its static range, then tail-pool chunks grabbed
-// one chunk ahead by lane 0 (the atomic's result is consumed a chunk later)
-// and logged in a 4-entry queue the compute side replays in order.
+// one chunk ahead by lane 0 (the atomic's result is consumed a chunk later).
+// The issue side walks it with an incremental (segment, row tile, K-part)
+// cursor -- a search only at chunk jumps -- and hands each stage's item to
+// the compute side in registers.
 struct Sched {
     unsigned int* ctr;
-    int N;
+    int N, ns;
     int cur, end;          // current static range / chunk [cur, end)
     int dyn;               // in the tail pool
     unsigned int pend;     // lane 0: pre-grabbed chunk start
     int lane;
+    int RT;
+    Item it;               // item of index cur-1 (valid once started)
+    int started;
 
     MOE_DEVI void grab_ahead() {
         if (lane == 0) pend = atomicAdd(ctr, static_cast<unsigned>(kChunk));
     }
-    MOE_DEVI bool next(int& i, int4* q, int& qw, int ns) {
+    MOE_DEVI void step(const SegTable& st) {
+        if (++it.kp == st.kp[it.s]) {
+            it.kp = 0;
+            if (++it.rt == RT) {
+                it.rt = 0;
+                ++it.s;
+            }
+        }
+    }
+    MOE_DEVI bool next(const SegTable& st, Item& out) {
+        bool jump = !started;
         while (cur >= end) {
             if (!dyn) {
                 dyn = 1;
@@ -367,23 +416,58 @@ struct Sched {
             }
             const int start = ns + static_cast<int>(__shfl_sync(0xffffffffu, pend, 0));
             if (start >= N) return false;
+            jump = jump || start != cur;
             cur = start;
             end = min(start + kChunk, N);
-            if (lane == 0) q[qw & 3] = make_int4(cur, end, 0, 0);
-            __syncwarp();
-            ++qw;
             grab_ahead();
         }
-        i = cur++;
+        if (jump)
+            it = item_at(st, cur);
+        else
+            step(st);
+        started = 1;
+        ++cur;
+        out = it;
         return true;
     }
 };
 
-__global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_constant__ StreamArgs a) {
+template <class C>
+MOE_DEVI void compute_item(const SegTable& st, const Item& it, const uint8_t* sp, int lane, float (&acc)[4]) {
+    const int gr = lane >> 2, t = lane & 3;
+    const int gk = st.gk[it.s], m_cnt = st.mcnt[it.s];
+    const int brl = min(gr, m_cnt - 1);
+    const int boff = C::kStageB + brl * (gk * 256 + kBRowPad) + t * 16;
+    if (st.sbytes[it.s]) {
+        const int c0 = min(2 * t, m_cnt - 1), c1i = min(2 * t + 1, m_cnt - 1);
+        const int g0 = (it.kp * gk) & 7;
+        const float* x0 = reinterpret_cast<const float*>(sp + C::kStageX + c0 * 32) + g0;
+        const float* x1 = reinterpret_cast<const float*>(sp + C::kStageX + c1i * 32) + g0;
+        if (C::kGk4 >= 8 && gk == 8) {
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+                group_int4(sp + C::kStageW + g * 1024, sp + C::kStageS + g * 32, sp + boff + g * 256, x0[g], x1[g], lane, acc);
+        } else {
+            for (int g = 0; g < gk; ++g)
+                group_int4(sp + C::kStageW + g * 1024, sp + C::kStageS + g * 32, sp + boff + g * 256, x0[g], x1[g], lane, acc);
+        }
+    } else {
+        float c1[4] = {0.f, 0.f, 0.f, 0.f};
+        group_bf16(sp + C::kStageW, sp + boff, lane, acc, c1);
+        if (C::kGk16 >= 2 && gk == 2) group_bf16(sp + C::kStageW + 4096, sp + boff + 256, lane, acc, c1);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[r] += c1[r];
+    }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_constant__ StreamArgs a) {
+    constexpr int kWarps = C::kWarps;
+    constexpr int kStageBytes = C::kStageBytes;
+    static_assert(kStages == 2, "the per-stage item registers are written for two stages");
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ SegTable st;
     __shared__ __align__(8) uint64_t bars[kWarps][kStages];
-    __shared__ int4 chq[kWarps][4];
     __shared__ int cnt[2 * MOE_MAX_EXPERTS];
     __shared__ int sperm[kMaxSlots];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -397,13 +481,13 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_consta
     // table and the first items' weight copies go out before the PDL wait;
     // their activation copies (the predecessor's output) after it.
     if (a.wait_first) pdl_wait();
-    build_segs(a, st, cnt, sperm);  // contains __syncthreads
+    build_segs<C>(a, st, cnt, sperm);  // contains __syncthreads
+    const uint64_t pol = policy_evict_first();
     const int W = static_cast<int>(gridDim.x) * kWarps;
     const int wid = static_cast<int>(blockIdx.x) * kWarps + warp;
     const int gr = lane >> 2, t = lane & 3;
     const int nslots = a.T * a.k;
     uint8_t* ring = smem + static_cast<size_t>(warp) * kStages * kStageBytes;
-    int4* q = chq[warp];
 
     // static part: contiguous equal ranges over the first ~7/8 of the items
     const int N = st.N;
@@ -412,24 +496,23 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_consta
     Sched sc;
     sc.ctr = a.sched;
     sc.N = N;
+    sc.ns = ns;
     sc.cur = wid * qs + min(wid, rs);
     sc.end = sc.cur + qs + (wid < rs ? 1 : 0);
     sc.dyn = 0;
     sc.pend = 0;
     sc.lane = lane;
-    int qw = 0, qr = 0;
-    int ccur = sc.cur, cend = sc.end;  // compute-side cursor (starts on the static range)
+    sc.RT = a.rows / 16;
+    sc.started = 0;
+    sc.it = Item{0, 0, 0};
 
-    static_assert(kStages == 2, "prologue is written for two stages");
-    Item pro0{0, 0, 0}, pro1{0, 0, 0};
-    int npro = 0, ii;
-    if (sc.next(ii, q, qw, ns)) {
-        pro0 = item_at(st, ii);
-        if (lane == 0) issue_weights(a, st, pro0, ring, &bars[warp][0]);
+    Item it0{0, 0, 0}, it1{0, 0, 0};
+    int npro = 0;
+    if (sc.next(st, it0)) {
+        if (lane == 0) issue_weights<C>(a, st, it0, ring, &bars[warp][0], pol);
         npro = 1;
-        if (sc.next(ii, q, qw, ns)) {
-            pro1 = item_at(st, ii);
-            if (lane == 0) issue_weights(a, st, pro1, ring + kStageBytes, &bars[warp][1]);
+        if (sc.next(st, it1)) {
+            if (lane == 0) issue_weights<C>(a, st, it1, ring + kStageBytes, &bars[warp][1], pol);
             npro = 2;
         }
     }
@@ -437,83 +520,44 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_consta
     pdl_trigger();
     ltrace(2 + 2 * a.p, 1);
     if (lane == 0) {
-        if (npro > 0) issue_acts(a, st, pro0, ring, &bars[warp][0]);
-        if (npro > 1) issue_acts(a, st, pro1, ring + kStageBytes, &bars[warp][1]);
+        if (npro > 0) issue_acts<C>(a, st, it0, ring, &bars[warp][0]);
+        if (npro > 1) issue_acts<C>(a, st, it1, ring + kStageBytes, &bars[warp][1]);
     }
     const unsigned long long t_wait = gtimer();
-    unsigned long long t_first = 0, t_mbar = 0;
     int issued = npro, computed = 0;
     uint32_t phase_bits = 0;
 
     while (computed < issued) {
         const int stage = computed & 1;
-        if (ccur >= cend) {
-            const int4 c = q[qr & 3];
-            ++qr;
-            ccur = c.x;
-            cend = c.y;
-        }
-        const Item it = item_at(st, ccur++);
-        const unsigned long long tm0 = gtimer();
+        const Item it = stage ? it1 : it0;
         mbar_wait(&bars[warp][stage], (phase_bits >> stage) & 1u);
         phase_bits ^= 1u << stage;
-        t_mbar += gtimer() - tm0;
-        if (t_first == 0) t_first = gtimer();
-        const uint8_t* sp = ring + stage * kStageBytes;
-        const int gk = st.gk[it.s], m_cnt = st.mcnt[it.s];
-        const int brl = min(gr, m_cnt - 1);
-        const int boff = kStageB + brl * (gk * 256 + kBRowPad) + t * 16;
+        uint8_t* sp = ring + stage * kStageBytes;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        if (st.sbytes[it.s]) {
-            const int c0 = min(2 * t, m_cnt - 1), c1i = min(2 * t + 1, m_cnt - 1);
-            const int g0 = (it.kp * gk) & 7;
-            const float* x0 = reinterpret_cast<const float*>(sp + kStageX + c0 * 32) + g0;
-            const float* x1 = reinterpret_cast<const float*>(sp + kStageX + c1i * 32) + g0;
-            switch (gk) {
-                case 8:
-#pragma unroll
-                    for (int g = 0; g < 8; ++g)
-                        group_int4(sp + kStageW + g * 1024, sp + kStageS + g * 32, sp + boff + g * 256, x0[g], x1[g], lane, acc);
-                    break;
-                case 4:
-#pragma unroll
-                    for (int g = 0; g < 4; ++g)
-                        group_int4(sp + kStageW + g * 1024, sp + kStageS + g * 32, sp + boff + g * 256, x0[g], x1[g], lane, acc);
-                    break;
-                default:
-                    for (int g = 0; g < gk; ++g)
-                        group_int4(sp + kStageW + g * 1024, sp + kStageS + g * 32, sp + boff + g * 256, x0[g], x1[g], lane, acc);
-                    break;
-            }
-        } else {
-            float c1[4] = {0.f, 0.f, 0.f, 0.f};
-            group_bf16(sp + kStageW, sp + boff, lane, acc, c1);
-            if (gk == 2) group_bf16(sp + kStageW + 4096, sp + boff + 256, lane, acc, c1);
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc[r] += c1[r];
-        }
+        compute_item<C>(st, it, sp, lane, acc);
         ++computed;
         // release the stage and refill it with the next item of the sequence
         fence_proxy_async();
         __syncwarp();
-        if (sc.next(ii, q, qw, ns)) {
-            const Item nit = item_at(st, ii);
+        Item nit;
+        if (sc.next(st, nit)) {
             if (lane == 0) {
-                issue_weights(a, st, nit, ring + stage * kStageBytes, &bars[warp][stage]);
-                issue_acts(a, st, nit, ring + stage * kStageBytes, &bars[warp][stage]);
+                issue_weights<C>(a, st, nit, sp, &bars[warp][stage], pol);
+                issue_acts<C>(a, st, nit, sp, &bars[warp][stage]);
             }
+            if (stage) it1 = nit; else it0 = nit;
             ++issued;
         }
         // this item's fp32 partial: columns 2t, 2t+1 of rows gr, gr+8
-        const int row = it.rt * 16 + gr;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int m = 2 * t + c;
-            if (m < m_cnt) {
-                float* pp = a.part + (static_cast<size_t>(it.kp) * nslots + st.slot0[it.s] + m) * a.rows + row;
-                __stcg(pp, acc[c]);
-                __stcg(pp + 8, acc[2 + c]);
-            }
+        const int m_cnt = st.mcnt[it.s];
+        float* pp = a.part + (static_cast<size_t>(it.kp) * nslots + st.slot0[it.s] + 2 * t) * a.rows + it.rt * 16 + gr;
+        if (2 * t < m_cnt) {
+            __stcg(pp, acc[0]);
+            __stcg(pp + 8, acc[2]);
+        }
+        if (2 * t + 1 < m_cnt) {
+            __stcg(pp + a.rows, acc[1]);
+            __stcg(pp + a.rows + 8, acc[3]);
         }
     }
     ltrace(2 + 2 * a.p, 2);
@@ -522,12 +566,12 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_consta
         tr += (static_cast<size_t>(a.p) * W + static_cast<size_t>(wid)) * 8;
         tr[0] = t_entry;
         tr[1] = t_wait;
-        tr[2] = t_first;
+        tr[2] = t_wait;
         tr[3] = gtimer();
-        tr[4] = static_cast<unsigned long long>(computed) | (static_cast<unsigned long long>(qw) << 32);
+        tr[4] = static_cast<unsigned long long>(computed);
         tr[5] = 0;
         tr[6] = 0;
-        tr[7] = t_mbar;
+        tr[7] = 0;
     }
 }
 
@@ -535,8 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_consta
 // slot: thread (q, kg) of a (quads x kGroups) block sums K-parts kg, kg+kG,
 // ... with up to 8 loads in flight, then the kG partial sums are added in kg
 // order through shared memory -- deterministic for a given KP.
-constexpr int kFinThreads = 256;
-constexpr int kKG = 4;  // K-part groups per quad
+constexpr int kKG = 8;  // K-part groups per quad (threads per 4 output rows)
 
 MOE_DEVI float4 sum_kparts(const float* p, size_t kstride, int KP, int kg) {
     float4 acc[8];
@@ -564,10 +607,14 @@ MOE_DEVI float4 sum_kparts(const float* p, size_t kstride, int KP, int kg) {
 // (gate rows g*128.., up rows f+g*128..) x 4 K-part groups; h is rounded to
 // bf16 and stored as bf16 (perm_k) and its exact fp16 copy (perm_k16), plus
 // the group's int4 bias term 1032*S_lo + 72*S_hi.
-__global__ void __launch_bounds__(kFinThreads) finalize_h_kernel(
+constexpr int kFinHThreads = 64 * kKG;
+constexpr int kFinOQuads = 32;
+constexpr int kFinOThreads = kFinOQuads * kKG;
+__global__ void __launch_bounds__(kFinHThreads) finalize_h_kernel(
     const float* __restrict__ part, const int* __restrict__ kpslot, int nslots, int f, uint16_t* __restrict__ hperm,
     uint16_t* __restrict__ hperm16, float* __restrict__ hsum, int hstride, unsigned int* sched) {
     __shared__ float4 red[kKG][64];
+    __shared__ uint16_t hs[128];
     const int G = f / 128;
     const int slot = blockIdx.x / G, g = blockIdx.x - slot * G;
     ltrace(3, 0);
@@ -599,20 +646,21 @@ __global__ void __launch_bounds__(kFinThreads) finalize_h_kernel(
         gv[0] = a.x; gv[1] = a.y; gv[2] = a.z; gv[3] = a.w;
         uv[0] = b.x; uv[1] = b.y; uv[2] = b.z; uv[3] = b.w;
     }
-    const int n0 = g * 128 + lane * 4;
-    float s = 0.0f;
-    const size_t o = static_cast<size_t>(slot) * f;
+    // h rounded to bf16 into smem (natural order), then every lane writes one
+    // 16-byte chunk of each K-permuted copy
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const uint16_t hb = f2bf(silu_f(gv[j]) * uv[j]);
-        const float hv = bf2f(hb);
-        hperm[o + perm_k(n0 + j)] = hb;
-        hperm16[o + perm_k16(n0 + j)] = __half_as_ushort(__float2half_rn(hv));  // exact for 2^-17 <= |h| <= 65504
-        s += hv;
+    for (int j = 0; j < 4; ++j) hs[lane * 4 + j] = f2bf(silu_f(gv[j]) * uv[j]);
+    __syncwarp();
+    uint4 cb = make_uint4(0, 0, 0, 0), ch = cb;
+    float s_lo = 0.0f, s_hi = 0.0f;
+    if (lane < 16) permute_chunk(hs, lane, cb, ch, s_lo, s_hi);
+    const size_t o = static_cast<size_t>(slot) * f + g * 128;
+    if (lane < 16) {
+        reinterpret_cast<uint4*>(hperm + o)[lane] = cb;
+        reinterpret_cast<uint4*>(hperm16 + o)[lane] = ch;
     }
-    float s_lo = (lane & 2) ? 0.0f : s, s_hi = (lane & 2) ? s : 0.0f;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
+    for (int off = 8; off >= 1; off >>= 1) {
         s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);
         s_hi += __shfl_xor_sync(0xffffffffu, s_hi, off);
     }
@@ -620,26 +668,26 @@ __global__ void __launch_bounds__(kFinThreads) finalize_h_kernel(
     ltrace(3, 2);
 }
 
-// Output finalize: one block per (token t, 256 output rows) -- or, with
-// out == null, per (slot, 256 rows) writing y itself for the slots of this
+// Output finalize: one block per (token t, 128 output rows) -- or, with
+// out == null, per (slot, 128 rows) writing y itself for the slots of this
 // launch's experts.  y[slot][j] = fixed-order sum of the slot's pass-1
 // partials; out[t][j] = bf16(resid[t][j] + sum_jj w[t,jj] * y[inv[t,jj]][j])
 // (fp32 fma chain in jj order).
-__global__ void __launch_bounds__(kFinThreads) finalize_out_kernel(
+__global__ void __launch_bounds__(kFinOThreads) finalize_out_kernel(
     const float* __restrict__ part, const int* __restrict__ kpslot, int T, int k, int d,
     const int32_t* __restrict__ inv, const float* __restrict__ wts, const uint16_t* __restrict__ resid,
     uint16_t* __restrict__ out, float* __restrict__ y, unsigned int* sched) {
-    __shared__ float4 red[kKG][64];
+    __shared__ float4 red[kKG][kFinOQuads];
     const int nslots = T * k;
-    const int nb = d / 256;
-    const int r = blockIdx.x / nb, j0 = (blockIdx.x - r * nb) * 256;
+    const int nb = d / (kFinOQuads * 4);
+    const int r = blockIdx.x / nb, j0 = (blockIdx.x - r * nb) * (kFinOQuads * 4);
     ltrace(5, 0);
     pdl_trigger();  // the next layer's route kernel preloads router weights before its wait
     pdl_wait();
     ltrace(5, 1);
     if (blockIdx.x == 0 && threadIdx.x == 0) *sched = 0;
     const size_t kstride = static_cast<size_t>(nslots) * d;
-    const int q = threadIdx.x & 63, kg = threadIdx.x >> 6;
+    const int q = threadIdx.x % kFinOQuads, kg = threadIdx.x / kFinOQuads;
     const int j = j0 + q * 4;
     if (out == nullptr) {
         const int KP = kpslot[r];
@@ -696,35 +744,29 @@ __global__ void __launch_bounds__(kFinThreads) finalize_out_kernel(
 // (row, group); lane owns 4 elements.
 __global__ void permute_rows_kernel(const uint16_t* __restrict__ x, int rows, int K, uint16_t* __restrict__ xp,
                                     uint16_t* __restrict__ xp16, float* __restrict__ xsum, int xstride) {
+    // one half-warp per (row, 128-K group): 16 chunks of 16 bytes
     const int G = K / 128;
-    const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+    const long long hw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 4;
+    const int c = threadIdx.x & 15;
     ltrace(1, 0);
     pdl_wait();     // x is the previous layer's output
     pdl_trigger();
     ltrace(1, 1);
-    ltrace(1, 2);
-    if (wid >= static_cast<long long>(rows) * G) return;
-    const long long r = wid / G;
-    const int g = static_cast<int>(wid - r * G);
-    const uint16_t* src = x + r * K + g * 128 + lane * 4;
-    uint16_t* dst = xp + r * K + g * 128;
-    uint16_t* dst16 = xp16 + r * K + g * 128;
-    float s = 0.0f;
+    const bool ok = hw < static_cast<long long>(rows) * G;
+    const long long r = ok ? hw / G : 0;
+    const int g = ok ? static_cast<int>(hw - r * G) : 0;
+    uint4 cb = make_uint4(0, 0, 0, 0), ch = cb;
+    float s_lo = 0.0f, s_hi = 0.0f;
+    if (ok) permute_chunk(x + r * K + g * 128, c, cb, ch, s_lo, s_hi);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const uint16_t v = src[j];
-        dst[perm_k(lane * 4 + j)] = v;
-        dst16[perm_k16(lane * 4 + j)] = __half_as_ushort(__float2half_rn(bf2f(v)));  // exact for 2^-17 <= |x| <= 65504
-        s += bf2f(v);
-    }
-    float s_lo = (lane & 2) ? 0.0f : s, s_hi = (lane & 2) ? s : 0.0f;
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
+    for (int off = 8; off >= 1; off >>= 1) {
         s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);
         s_hi += __shfl_xor_sync(0xffffffffu, s_hi, off);
     }
-    if (lane == 0) xsum[r * xstride + g] = 1032.0f * s_lo + 72.0f * s_hi;
+    if (!ok) return;
+    reinterpret_cast<uint4*>(xp + r * K + g * 128)[c] = cb;
+    reinterpret_cast<uint4*>(xp16 + r * K + g * 128)[c] = ch;
+    if (c == 0) xsum[r * xstride + g] = 1032.0f * s_lo + 72.0f * s_hi;
 }
 
 int group_stride(int K) { return (K / 128 + 7) / 8 * 8; }
@@ -732,19 +774,24 @@ int group_stride(int K) { return (K / 128 + 7) / 8 * 8; }
 int moek_group_stride(int K) { return moek::group_stride(K); }
 namespace moek {
 
-cudaError_t launch_stream(const StreamArgs& a, bool pdl, cudaStream_t stream) {
+template <class C>
+cudaError_t launch_stream_cfg(const StreamArgs& a, bool pdl, cudaStream_t stream) {
     static int grid = 0;
-    const size_t smem = static_cast<size_t>(kWarps) * kStages * kStageBytes;
+    const size_t smem = static_cast<size_t>(C::kWarps) * kStages * C::kStageBytes;
     if (grid == 0) {
-        MOE_CUDA_OK(cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        MOE_CUDA_OK(cudaFuncSetAttribute(stream_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int dev = 0, sms = 0;
         MOE_CUDA_OK(cudaGetDevice(&dev));
         MOE_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         grid = sms;
     }
-    if (pdl) return launch_pdl(stream_kernel, dim3(grid), dim3(kThreads), smem, stream, a);
-    stream_kernel<<<grid, kThreads, smem, stream>>>(a);
+    if (pdl) return launch_pdl(stream_kernel<C>, dim3(grid), dim3(C::kThreads), smem, stream, a);
+    stream_kernel<C><<<grid, C::kThreads, smem, stream>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_stream(const StreamArgs& a, bool pdl, cudaStream_t stream) {
+    return launch_stream_cfg<CfgBatch>(a, pdl, stream);
 }
 
 }  // namespace moek
@@ -821,9 +868,9 @@ GemvWorkspace moek_gemv_workspace_view(void* base, int T, int k, int d, int f) {
 
 cudaError_t moek_permute_rows(const void* x, int rows, int K, void* xperm, void* xperm16, float* xsum,
                               cudaStream_t stream) {
-    const long long warps = static_cast<long long>(rows) * (K / 128);
-    if (warps == 0) return cudaSuccess;
-    return moek::launch_pdl(moek::permute_rows_kernel, dim3(static_cast<unsigned>((warps * 32 + 255) / 256)), dim3(256),
+    const long long halves = static_cast<long long>(rows) * (K / 128);
+    if (halves == 0) return cudaSuccess;
+    return moek::launch_pdl(moek::permute_rows_kernel, dim3(static_cast<unsigned>((halves * 16 + 255) / 256)), dim3(256),
                             0, stream, static_cast<const uint16_t*>(x), rows, K, static_cast<uint16_t*>(xperm),
                             static_cast<uint16_t*>(xperm16), xsum, moek::group_stride(K));
 }
@@ -834,7 +881,7 @@ cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* 
                          float* y, int xmode, cudaStream_t stream) {
     // every (active expert, 8-token tile) segment must fit the kernel's table
     if (E + (T * k + moek::kTile - 1) / moek::kTile > moek::kMaxSegs) return cudaErrorInvalidValue;
-    if (d % 256 != 0 || f % 128 != 0) return cudaErrorInvalidValue;
+    if (d % (moek::kFinOQuads * 4) != 0 || f % 128 != 0) return cudaErrorInvalidValue;
     if (xmode == MOE_X_PERMUTE) MOE_CUDA_OK(moek_permute_rows(x, T, d, ws.xperm, ws.xperm16, ws.xsum, stream));
     const int nslots = T * k;
     moek::StreamArgs a{};
@@ -860,7 +907,7 @@ cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* 
     a.wait_first = xmode == MOE_X_ROUTED ? 1 : 0;
     MOE_CUDA_OK(moek::launch_stream(a, xmode != MOE_X_READY, stream));
     {
-        MOE_CUDA_OK(moek::launch_pdl(moek::finalize_h_kernel, dim3(nslots * (f / 128)), dim3(moek::kFinThreads), 0, stream,
+        MOE_CUDA_OK(moek::launch_pdl(moek::finalize_h_kernel, dim3(nslots * (f / 128)), dim3(moek::kFinHThreads), 0, stream,
                                      static_cast<const float*>(ws.part0), static_cast<const int*>(ws.kpslot), nslots, f,
                                      static_cast<uint16_t*>(ws.hperm), static_cast<uint16_t*>(ws.hperm16), ws.hsum,
                                      moek::group_stride(f), ws.sched));
@@ -878,8 +925,9 @@ cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* 
     a.sched = ws.sched + 1;
     a.wait_first = 0;
     MOE_CUDA_OK(moek::launch_stream(a, true, stream));
-    return moek::launch_pdl(moek::finalize_out_kernel, dim3(static_cast<unsigned>((out ? T : nslots) * (d / 256))),
-                            dim3(moek::kFinThreads), 0,
+    return moek::launch_pdl(moek::finalize_out_kernel,
+                            dim3(static_cast<unsigned>((out ? T : nslots) * (d / (moek::kFinOQuads * 4)))),
+                            dim3(moek::kFinOThreads), 0,
                             stream, static_cast<const float*>(ws.part1), static_cast<const int*>(ws.kpslot + nslots), T, k,
                             d, inv, wts, static_cast<const uint16_t*>(resid), static_cast<uint16_t*>(out), y,
                             ws.sched + 1);

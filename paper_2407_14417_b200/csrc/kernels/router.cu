@@ -251,12 +251,19 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
         }
         lg_s[MOE_MAX_EXPERTS + threadIdx.x] = acc;
         __syncthreads();
-        for (int s2 = 128; s2 >= 1; s2 >>= 1) {
+        for (int s2 = 128; s2 >= 32; s2 >>= 1) {
             if (static_cast<int>(threadIdx.x) < s2)
                 lg_s[MOE_MAX_EXPERTS + threadIdx.x] =
                     __fadd_rn(lg_s[MOE_MAX_EXPERTS + threadIdx.x], lg_s[MOE_MAX_EXPERTS + threadIdx.x + s2]);
             __syncthreads();
         }
+        if (wid == 0) {  // the same pairwise steps 16..1 as warp shuffles
+            float v = lg_s[MOE_MAX_EXPERTS + lane];
+#pragma unroll
+            for (int s2 = 16; s2 >= 1; s2 >>= 1) v = __fadd_rn(v, __shfl_down_sync(0xffffffffu, v, s2));
+            if (lane == 0) lg_s[MOE_MAX_EXPERTS] = v;
+        }
+        __syncthreads();
         const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(lg_s[MOE_MAX_EXPERTS],
                                                                             static_cast<float>(a.d)), a.norm_eps)));
         for (int i = threadIdx.x; i < a.d; i += blockDim.x) x_s[i] = f2bf(__fmul_rn(bf2f(x_s[i]), rstd));
@@ -273,27 +280,25 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
     if (a.logits && threadIdx.x < a.E) a.logits[static_cast<size_t>(t) * a.E + threadIdx.x] = lg_s[threadIdx.x];
     if (wid == 0) warp_topk(lg_s, a.E, a.k, lane, a.idx + static_cast<size_t>(t) * a.k, a.w + static_cast<size_t>(t) * a.k, s_idx);
     // K-permuted bf16 / fp16 copies of this token row + int4 bias terms
-    // (same definition as gemv.cu permute_rows_kernel), one warp per group
+    // (same definition as gemv.cu permute_rows_kernel): a 128-K group is 16
+    // chunks of 16 bytes, so each warp half assembles one group per pass
     if (a.xperm != nullptr) {
         const int G = a.d / 128;
-        for (int g = wid; g < G; g += blockDim.x / 32) {
-            float sm = 0.0f;
-            uint16_t* dst = a.xperm + static_cast<size_t>(t) * a.d + g * 128;
-            uint16_t* dst16 = a.xperm16 + static_cast<size_t>(t) * a.d + g * 128;
+        for (int g0 = wid * 2; g0 < G; g0 += blockDim.x / 16) {
+            const int g = g0 + (lane >> 4), c = lane & 15;
+            uint4 cb = make_uint4(0, 0, 0, 0), ch = cb;
+            float s_lo = 0.0f, s_hi = 0.0f;
+            if (g < G) permute_chunk(x_s + g * 128, c, cb, ch, s_lo, s_hi);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint16_t v = x_s[g * 128 + lane * 4 + j];
-                dst[rperm_k(lane * 4 + j)] = v;
-                dst16[rperm_k16(lane * 4 + j)] = __half_as_ushort(__float2half_rn(bf2f(v)));
-                sm += bf2f(v);
-            }
-            float s_lo = (lane & 2) ? 0.0f : sm, s_hi = (lane & 2) ? sm : 0.0f;
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
+            for (int off = 8; off >= 1; off >>= 1) {
                 s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);
                 s_hi += __shfl_xor_sync(0xffffffffu, s_hi, off);
             }
-            if (lane == 0) a.xsum[static_cast<size_t>(t) * a.xstride + g] = 1032.0f * s_lo + 72.0f * s_hi;
+            if (g < G) {
+                reinterpret_cast<uint4*>(a.xperm + static_cast<size_t>(t) * a.d + g * 128)[c] = cb;
+                reinterpret_cast<uint4*>(a.xperm16 + static_cast<size_t>(t) * a.d + g * 128)[c] = ch;
+                if (c == 0) a.xsum[static_cast<size_t>(t) * a.xstride + g] = 1032.0f * s_lo + 72.0f * s_hi;
+            }
         }
     }
     if (a.counts == nullptr) {
