@@ -165,6 +165,18 @@ int moe_ffn_bf16(const void* x, const int32_t* perm, const int32_t* offsets, int
                  void* workspace, size_t ws_bytes, float* y_perm, void* stream);
 int moe_gemv_max_tokens(void);
 
+/* K3/K4 on the 5th-generation tensor cores (tcgen05.mma, TMEM accumulators)
+ * for batched decode / prefill: the same contract as moe_ffn (x [T,d] bf16
+ * natural order, y_perm [T*k, d] fp32), 128-row x 128-token tiles per
+ * expert, SwiGLU fused into the gate/up epilogue.  bf16 experts run BF16
+ * operands; int4-g128 experts are dequantised on chip to fp16 q*s (exact
+ * for normal-range scales) against an fp16 copy of the activations.
+ * `workspace` needs moe_ffn_tc_workspace_bytes (no zero-fill needed). */
+size_t moe_ffn_tc_workspace_bytes(int T, int k, int d, int f);
+int moe_ffn_tc(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+               const moe_expert_weights* experts, int E, int d, int f, void* workspace, size_t ws_bytes,
+               float* y_perm, void* stream);
+
 /* K5: out[t] = bf16(residual[t] + sum_j w[t,j] * y_perm[inv_perm[t*k+j]]),
  * fp32 fma chain in j order; residual may be NULL. */
 int moe_combine(const float* y_perm, const int32_t* inv_perm, const float* w,

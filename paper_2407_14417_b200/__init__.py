@@ -121,6 +121,8 @@ def lib() -> C.CDLL:
         "moe_ffn_workspace_bytes": (C.c_size_t, [I, I, I, I, I]),
         "moe_ffn": (I, [VP, VP, VP, I, I, P(ExpertWeightsC), I, I, I, VP, C.c_size_t, VP, VP]),
         "moe_ffn_int4": (I, [VP, VP, VP, I, I, P(VP), P(VP), P(VP), P(VP), I, I, I, VP, C.c_size_t, VP, VP]),
+        "moe_ffn_tc_workspace_bytes": (C.c_size_t, [I, I, I, I]),
+        "moe_ffn_tc": (I, [VP, VP, VP, I, I, P(ExpertWeightsC), I, I, I, VP, C.c_size_t, VP, VP]),
         "moe_ffn_bf16": (I, [VP, VP, VP, I, I, P(VP), P(VP), I, I, I, VP, C.c_size_t, VP, VP]),
         "moe_pack_bf16_blocks": (I, [VP, I, I, VP, VP]),
         "moe_gemv_max_tokens": (I, []),
@@ -441,6 +443,18 @@ def ffn(x, perm, offsets, T, k, experts: Sequence[ExpertWeightsC], d, f, workspa
     arr = (ExpertWeightsC * len(experts))(*experts)
     _check(lib().moe_ffn(_ptr(x), _ptr(perm), _ptr(offsets), T, k, arr, len(experts), d, f, _ptr(workspace),
                          ws_bytes, _ptr(y_perm), _stream(stream)))
+
+
+def ffn_tc_workspace_bytes(T, k, d, f) -> int:
+    return lib().moe_ffn_tc_workspace_bytes(T, k, d, f)
+
+
+def ffn_tc(x, perm, offsets, T, k, experts: Sequence[ExpertWeightsC], d, f, workspace, ws_bytes, y_perm,
+           stream=None):
+    """K3/K4 grouped SwiGLU FFN on tcgen05 (batched decode / prefill)."""
+    arr = (ExpertWeightsC * len(experts))(*experts)
+    _check(lib().moe_ffn_tc(_ptr(x), _ptr(perm), _ptr(offsets), T, k, arr, len(experts), d, f, _ptr(workspace),
+                            ws_bytes, _ptr(y_perm), _stream(stream)))
 
 
 def pack_bf16_blocks(w, rows, cols, out, stream=None):

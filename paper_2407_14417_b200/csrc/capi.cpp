@@ -359,6 +359,24 @@ int moe_ffn(const void* x, const int32_t* perm, const int32_t* offsets, int T, i
     });
 }
 
+size_t moe_ffn_tc_workspace_bytes(int T, int k, int d, int f) { return moek_tc_workspace_bytes(T, k, d, f); }
+
+int moe_ffn_tc(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+               const moe_expert_weights* experts, int E, int d, int f, void* workspace, size_t ws_bytes,
+               float* y_perm, void* stream) {
+    return guarded([&] {
+        usage_if(E < 1 || E > MOE_MAX_EXPERTS || k < 1 || k > E, "bad E / k");
+        usage_if(d <= 0 || d % 128 != 0 || f <= 0 || f % 128 != 0, "d and f must be multiples of 128");
+        need_device();
+        if (T == 0) return;
+        usage_if(workspace == nullptr || ws_bytes < moek_tc_workspace_bytes(T, k, d, f),
+                 "workspace too small (moe_ffn_tc_workspace_bytes)");
+        const uint64_t mask = E >= 64 ? ~0ull : ((1ull << E) - 1ull);
+        const cudaError_t e = moek_ffn_tc(workspace, x, perm, offsets, T, k, experts, E, d, f, mask, y_perm, st(stream));
+        if (e != cudaSuccess) throw std::runtime_error(std::string("moe_ffn_tc: ") + cudaGetErrorString(e));
+    });
+}
+
 int moe_ffn_int4(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
                  const void* const* q_gate_up, const void* const* s_gate_up,
                  const void* const* q_down, const void* const* s_down, int E, int d, int f,

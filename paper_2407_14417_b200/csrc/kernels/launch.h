@@ -46,6 +46,12 @@ cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* 
                          const void* resid, int T, int k, const moe_expert_weights* experts, int E,
                          int d, int f, uint64_t active_mask, void* out, float* y, int xmode,
                          cudaStream_t stream);
+// tcgen05 grouped expert FFN (tc_gemm.cu): x natural [T][d] bf16 (already
+// normalised), every active expert's segment -> y_perm [T*k][d] fp32.
+size_t moek_tc_workspace_bytes(int T, int k, int d, int f);
+cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+                        const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask, float* y,
+                        cudaStream_t stream);
 // Storage-layout converters (logical row-major -> fragment blocks).
 cudaError_t moek_pack_bf16_blocks(const void* w, int rows, int cols, void* out, cudaStream_t stream);
 cudaError_t moek_quantize_blocks(const void* w, int rows, int cols, uint32_t* qb, void* sb,

@@ -1,0 +1,430 @@
+// tc_gemm.cu -- K3/K4 expert FFN on the 5th-generation tensor cores
+// (tcgen05.mma, fp32 accumulators in TMEM) for batched decode / prefill,
+// where an expert sees enough tokens that the contraction is a real GEMM.
+//
+// One CTA computes a 128-weight-row x 128-token tile of one expert:
+//   pass 0: D_gate, D_up = W_gate/up[rows] . X[tokens]^T -> fused SwiGLU
+//           epilogue h = bf16(silu(g) * u) (+ its fp16 copy) for the tile
+//   pass 1: D = W_down[rows] . H[tokens]^T -> y[slot][row] (fp32), combined
+//           afterwards by the K5 combine kernel.
+// Data path per 64-K chunk (2-stage pipeline):
+//   HBM --cp.async--> raw smem (weights in their fragment-block storage
+//   layout, token rows in natural order) --convert (all threads)-->
+//   canonical K-major SWIZZLE_128B tiles --tcgen05.mma (one thread,
+//   M=128, N=128, K=16 x 4)--> TMEM; tcgen05.commit -> mbarrier frees the
+//   stage.  bf16 experts run kind::f16 with BF16 operands; int4-g128 experts
+//   are dequantised in the convert step to fp16 q*s (exact: <= 11
+//   significant bits, for normal-range scales) and run with F16 operands
+//   against an fp16 copy of the activations.
+// The storage layout stays the GEMV's (fragment blocks), so one copy of the
+// weights serves both paths.
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace moek {
+namespace tc {
+
+constexpr int kThreads = 256;
+constexpr int kN = 128;        // tokens per tile (UMMA N)
+constexpr int kM = 128;        // weight rows per tile (UMMA M)
+constexpr int kKc = 64;        // K per chunk (one 128-byte swizzle atom of 16-bit values)
+constexpr int kTileBytes = kM * kKc * 2;  // 16 KB (A tile; B tile is the same for kN = 128)
+// raw stage: [A_gate raw 16 KB][A_up raw 16 KB][scales 2 x 256 B][B raw 16 KB]
+constexpr int kRawA = 16384;
+constexpr int kRawS = 256;
+constexpr int kRawBytes = 2 * kRawA + 2 * kRawS + kN * kKc * 2;
+// canonical stage: [A_gate 16 KB][A_up 16 KB][B 16 KB], 1024-aligned
+constexpr int kCanBytes = 3 * kTileBytes;
+constexpr int kSmemBytes = 1024 + 2 * kRawBytes + 2 * kCanBytes;
+
+struct TcArgs {
+    const int32_t* offsets;   // [E+1]
+    const int32_t* perm;      // [T*k]
+    int T, k, E, kshift;
+    int p;                    // 0 gate/up, 1 down
+    int d, f;
+    const uint16_t* bnat;     // natural B rows, bf16: pass 0 normalised x [T][d], pass 1 h [T*k][f]
+    const uint16_t* bnat16;   // the same as fp16 (int4 experts)
+    uint16_t* hout;           // pass 0: h [T*k][f] bf16
+    uint16_t* hout16;         // pass 0: h [T*k][f] fp16
+    float* y;                 // pass 1: y [T*k][d]
+    uint64_t active_mask;
+    moe_expert_weights ex[MOE_MAX_EXPERTS];
+};
+
+MOE_DEVI uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+MOE_DEVI void cp_async16(void* dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s32(dst)), "l"(src), "r"(src_bytes) : "memory");
+}
+MOE_DEVI void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s32(dst)), "l"(src) : "memory");
+}
+MOE_DEVI void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+MOE_DEVI void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+MOE_DEVI void mbar_init(uint64_t* bar) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(bar)) : "memory"); }
+MOE_DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(s32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// SWIZZLE_128B K-major smem descriptor (sm100 version 1): start >> 4, LBO 16 B
+// (unused for swizzled K-major), SBO 1024 B between 8-row groups.
+MOE_DEVI uint64_t sdesc(uint32_t addr) {
+    return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+// kind::f16 instruction descriptor: D f32, A/B format (0 f16, 1 bf16), K-major, N, M.
+MOE_DEVI uint32_t idesc(int fmt, int n, int m) {
+    return (1u << 4) | (static_cast<uint32_t>(fmt) << 7) | (static_cast<uint32_t>(fmt) << 10) |
+           (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+MOE_DEVI void umma(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t id, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(dtmem),
+        "l"(a), "l"(b), "r"(id), "r"(accum)
+        : "memory");
+}
+MOE_DEVI void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(bar))
+                 : "memory");
+}
+
+// byte offset of (row, k) in a K-major SWIZZLE_128B tile of 64 16-bit values per row
+MOE_DEVI int swz(int row, int kbyte) {
+    return (row >> 3) * 1024 + (row & 7) * 128 + ((((kbyte >> 4) ^ (row & 7)) & 7) << 4) + (kbyte & 15);
+}
+
+#define TMEM_LD32(taddr, v)                                                                                       \
+    asm volatile(                                                                                                 \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                        \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),       \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), \
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),            \
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),            \
+          "=r"(v[30]), "=r"(v[31])                                                                              \
+        : "r"(taddr))
+
+struct Tile {
+    int e, slot0, m, R0;  // expert, first slot, tokens in tile, first weight row
+};
+
+MOE_DEVI bool find_tile(const TcArgs& a, int RT, int b, Tile& tl) {
+    for (int e = 0; e < a.E; ++e) {
+        if (!((a.active_mask >> e) & 1ull)) continue;
+        const int o0 = a.offsets[e], m = a.offsets[e + 1] - o0;
+        if (m == 0) continue;
+        const int nt = (m + kN - 1) / kN;
+        if (b < nt * RT) {
+            const int tt = b / RT, rt = b - tt * RT;
+            tl.e = e;
+            tl.slot0 = o0 + tt * kN;
+            tl.m = min(kN, m - tt * kN);
+            tl.R0 = rt * kM;
+            return true;
+        }
+        b -= nt * RT;
+    }
+    return false;
+}
+
+// Issue the cp.async copies of chunk kc into a raw stage.
+MOE_DEVI void load_raw(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, uint8_t* raw, const int* brow,
+                       int tid) {
+    const moe_expert_weights& W = a.ex[tl.e];
+    const int G = K / 128, g = kc >> 1, hh = kc & 1;
+    const bool p4 = W.precision == MOE_P4;
+    for (int mat = 0; mat < nmat; ++mat) {
+        // pass 0: mat 0 = gate rows R0.., mat 1 = up rows f+R0..; pass 1: down rows R0..
+        const int row0 = (a.p == 0 && mat == 1) ? a.f + tl.R0 : tl.R0;
+        const uint8_t* wb = static_cast<const uint8_t*>(a.p == 0 ? W.w_gate_up : W.w_down);
+        uint8_t* dst = raw + mat * kRawA;
+        if (!p4) {
+            // 8 blocks x 2 KB (parts 4hh..4hh+3) = 1024 x 16 B
+            for (int pc = tid; pc < 1024; pc += kThreads) {
+                const int i = pc >> 7, rem = pc & 127;
+                const size_t blk = static_cast<size_t>(row0 / 16 + i) * G + g;
+                cp_async16(dst + pc * 16, wb + blk * 4096 + hh * 2048 + rem * 16, 16);
+            }
+        } else {
+            // 8 blocks x 64 (half, lane) x 8 B (words 2hh, 2hh+1)
+            for (int it = tid; it < 512; it += kThreads) {
+                const int i = it >> 6, hl = it & 63;
+                const size_t blk = static_cast<size_t>(row0 / 16 + i) * G + g;
+                cp_async8(dst + it * 8, wb + blk * 1024 + (hl * 4 + 2 * hh) * 4);
+            }
+            const uint8_t* sb = static_cast<const uint8_t*>(a.p == 0 ? W.s_gate_up : W.s_down);
+            if (tid < 16) {
+                const int i = tid >> 1, half16 = tid & 1;
+                const size_t blk = static_cast<size_t>(row0 / 16 + i) * G + g;
+                cp_async16(raw + 2 * kRawA + mat * kRawS + i * 32 + half16 * 16, sb + blk * 32 + half16 * 16, 16);
+            }
+        }
+    }
+    // token rows: 128 B each (natural order), zero-filled past the tile's tokens
+    const uint16_t* bsrc = p4 ? a.bnat16 : a.bnat;
+    uint8_t* bdst = raw + 2 * kRawA + 2 * kRawS;
+    for (int pc = tid; pc < kN * 8; pc += kThreads) {
+        const int n = pc >> 3, c = pc & 7;
+        const bool ok = n < tl.m;
+        const uint16_t* src = bsrc + static_cast<size_t>(ok ? brow[n] : brow[0]) * K + kc * kKc + c * 8;
+        cp_async16(bdst + pc * 16, src, ok ? 16 : 0);
+    }
+}
+
+// raw stage -> canonical swizzled tiles
+MOE_DEVI void convert(const TcArgs& a, const Tile& tl, int nmat, const uint8_t* raw, uint8_t* can, int tid) {
+    const bool p4 = a.ex[tl.e].precision == MOE_P4;
+    for (int mat = 0; mat < nmat; ++mat) {
+        const uint8_t* src = raw + mat * kRawA;
+        uint8_t* dst = can + mat * kTileBytes;
+        if (!p4) {
+            for (int pc = tid; pc < 1024; pc += kThreads) {
+                const int i = pc >> 7, kq = (pc >> 5) & 3, L = pc & 31;
+                const uint4 v = *reinterpret_cast<const uint4*>(src + pc * 16);
+                const int rlo = i * 16 + (L >> 2), rhi = rlo + 8;
+                const int kb = (kq * 16 + 2 * (L & 3)) * 2;  // byte of k within the 128-byte row
+                *reinterpret_cast<uint32_t*>(dst + swz(rlo, kb)) = v.x;
+                *reinterpret_cast<uint32_t*>(dst + swz(rhi, kb)) = v.y;
+                *reinterpret_cast<uint32_t*>(dst + swz(rlo, kb + 16)) = v.z;
+                *reinterpret_cast<uint32_t*>(dst + swz(rhi, kb + 16)) = v.w;
+            }
+        } else {
+            const uint8_t* sc = raw + 2 * kRawA + mat * kRawS;
+            const uint32_t m1032 = 0xE408E408u;  // fp16 (-1032, -1032)
+            const uint32_t m72 = 0xD480D480u;    // fp16 (-72, -72)
+            const uint32_t r16 = 0x2C002C00u;    // fp16 (1/16, 1/16)
+            for (int it = tid; it < 512; it += kThreads) {
+                const int i = it >> 6, hl = it & 63, half = hl >> 5, L = hl & 31;
+                const uint2 w2 = *reinterpret_cast<const uint2*>(src + it * 8);
+                const int row = i * 16 + half * 8 + (L >> 2);
+                const uint16_t sb = *reinterpret_cast<const uint16_t*>(sc + i * 32 + (L >> 2) * 4 + half * 2);
+                const __half sh = __float2half_rn(bf2f(sb));  // exact for normal-range scales
+                const __half2 s2 = __halves2half2(sh, sh);
+#pragma unroll
+                for (int qi = 0; qi < 2; ++qi) {
+                    const uint32_t w = qi ? w2.y : w2.x;
+                    const uint32_t lo0 = and_or(w, 0x000F000Fu, 0x64006400u);
+                    const uint32_t hi0 = and_or(w, 0x00F000F0u, 0x64006400u);
+                    const uint32_t lo1 = and_or(w >> 8, 0x000F000Fu, 0x64006400u);
+                    const uint32_t hi1 = and_or(w >> 8, 0x00F000F0u, 0x64006400u);
+                    // q exactly, then q*s exactly in fp16
+                    auto deq_lo = [&](uint32_t v) {
+                        __half2 q = __hadd2(*reinterpret_cast<const __half2*>(&v), *reinterpret_cast<const __half2*>(&m1032));
+                        q = __hmul2(q, s2);
+                        return *reinterpret_cast<uint32_t*>(&q);
+                    };
+                    auto deq_hi = [&](uint32_t v) {
+                        __half2 q = __hfma2(*reinterpret_cast<const __half2*>(&v), *reinterpret_cast<const __half2*>(&r16),
+                                            *reinterpret_cast<const __half2*>(&m72));
+                        q = __hmul2(q, s2);
+                        return *reinterpret_cast<uint32_t*>(&q);
+                    };
+                    // word qi covers kk = 2*(2hh+qi) + {0,1}; local kk' = 2qi + {0,1}
+                    const int kb0 = ((2 * qi) * 16 + 2 * (L & 3)) * 2;
+                    const int kb1 = ((2 * qi + 1) * 16 + 2 * (L & 3)) * 2;
+                    *reinterpret_cast<uint32_t*>(dst + swz(row, kb0)) = deq_lo(lo0);
+                    *reinterpret_cast<uint32_t*>(dst + swz(row, kb0 + 16)) = deq_hi(hi0);
+                    *reinterpret_cast<uint32_t*>(dst + swz(row, kb1)) = deq_lo(lo1);
+                    *reinterpret_cast<uint32_t*>(dst + swz(row, kb1 + 16)) = deq_hi(hi1);
+                }
+            }
+        }
+    }
+    // token rows: 16-byte chunks to their swizzled positions
+    const uint8_t* bs = raw + 2 * kRawA + 2 * kRawS;
+    uint8_t* bd = can + 2 * kTileBytes;
+    for (int pc = tid; pc < kN * 8; pc += kThreads) {
+        const int n = pc >> 3, c = pc & 7;
+        *reinterpret_cast<uint4*>(bd + swz(n, c * 16)) = *reinterpret_cast<const uint4*>(bs + pc * 16);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) tc_ffn_kernel(const __grid_constant__ TcArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    auto can = [&](int s) { return smem + s * kCanBytes; };
+    auto raw = [&](int s) { return smem + 2 * kCanBytes + s * kRawBytes; };
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ uint32_t tmem_slot;
+    __shared__ int brow[kN];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    pdl_wait();
+    pdl_trigger();
+    const int K = a.p == 0 ? a.d : a.f;
+    const int RT = (a.p == 0 ? a.f : a.d) / kM;
+    Tile tl;
+    if (!find_tile(a, RT, blockIdx.x, tl)) return;
+    const int nmat = a.p == 0 ? 2 : 1;
+    if (tid < kN) {
+        const int n = min(tid, tl.m - 1);
+        const int slot = tl.slot0 + n;
+        brow[tid] = a.p == 0 ? (a.kshift >= 0 ? a.perm[slot] >> a.kshift : a.perm[slot] / a.k) : slot;
+    }
+    if (tid == 0) {
+        mbar_init(&bar[0]);
+        mbar_init(&bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tmem_slot)),
+                     "r"(256)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_slot;
+    const int fmt = a.ex[tl.e].precision == MOE_P4 ? 0 : 1;
+    const uint32_t id = idesc(fmt, kN, kM);
+    const int nk = K / kKc;
+
+    load_raw(a, tl, nmat, K, 0, raw(0), brow, tid);
+    cp_commit();
+    uint32_t phase = 0;  // per-stage commit parity bits
+    for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc & 1;
+        if (kc + 1 < nk) load_raw(a, tl, nmat, K, kc + 1, raw(s ^ 1), brow, tid);
+        cp_commit();
+        cp_wait<1>();  // chunk kc landed
+        __syncthreads();
+        if (kc >= 2) {  // the MMAs of chunk kc-2 have read canonical stage s
+            mbar_wait(&bar[s], (phase >> s) & 1u);
+            phase ^= 1u << s;
+        }
+        convert(a, tl, nmat, raw(s), can(s), tid);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t cb = s32(can(s));
+#pragma unroll
+            for (int j = 0; j < kKc / 16; ++j) {
+                const uint64_t bdesc = sdesc(cb + 2 * kTileBytes + j * 32);
+                const uint32_t acc = (kc > 0 || j > 0) ? 1u : 0u;
+                umma(tmem, sdesc(cb + j * 32), bdesc, id, acc);
+                if (nmat == 2) umma(tmem + kN, sdesc(cb + kTileBytes + j * 32), bdesc, id, acc);
+            }
+            umma_commit(&bar[s]);
+        }
+    }
+    // drain: the last commits of both stages
+    for (int kc = max(0, nk - 2); kc < nk; ++kc) {
+        const int s = kc & 1;
+        mbar_wait(&bar[s], (phase >> s) & 1u);
+        phase ^= 1u << s;
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    // epilogue: warp w reads TMEM lanes 32*(w%4).. (weight rows) and token
+    // columns [64*(w/4), 64*(w/4)+64)
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    for (int cb = (warp >> 2) * 64; cb < (warp >> 2) * 64 + 64; cb += 32) {
+        uint32_t g[32];
+        TMEM_LD32(tmem + lane_base + cb, g);
+        if (a.p == 0) {
+            uint32_t u[32];
+            TMEM_LD32(tmem + lane_base + kN + cb, u);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const int n = cb + c;
+                if (n < tl.m) {
+                    const uint16_t hb = f2bf(silu_f(__uint_as_float(g[c])) * __uint_as_float(u[c]));
+                    const size_t o = static_cast<size_t>(tl.slot0 + n) * a.f + tl.R0 + row;
+                    a.hout[o] = hb;
+                    a.hout16[o] = __half_as_ushort(__float2half_rn(bf2f(hb)));
+                }
+            }
+        } else {
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const int n = cb + c;
+                if (n < tl.m) a.y[static_cast<size_t>(tl.slot0 + n) * a.d + tl.R0 + row] = __uint_as_float(g[c]);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+}
+
+// natural bf16 rows -> fp16 copy (pass-0 B operand of int4 experts)
+__global__ void to_f16_kernel(const uint16_t* __restrict__ x, long long n, uint16_t* __restrict__ y) {
+    pdl_wait();
+    pdl_trigger();
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        y[i] = __half_as_ushort(__float2half_rn(bf2f(x[i])));
+}
+
+}  // namespace tc
+}  // namespace moek
+
+size_t moek_tc_workspace_bytes(int T, int k, int d, int f) {
+    const size_t slots = static_cast<size_t>(T) * k;
+    return static_cast<size_t>(T) * d * 2 + 2 * slots * f * 2 + 1024;
+}
+
+// Grouped expert FFN on tcgen05 for every expert segment of a permutation:
+// x natural [T][d] bf16 (already normalised), y_perm [T*k][d] fp32.
+cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+                        const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask, float* y,
+                        cudaStream_t stream) {
+    using namespace moek::tc;
+    if (d % kM != 0 || f % kM != 0 || d % 128 != 0 || f % 128 != 0) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+        attr = true;
+    }
+    const size_t slots = static_cast<size_t>(T) * k;
+    uint16_t* x16 = static_cast<uint16_t*>(ws);
+    uint16_t* h = x16 + static_cast<size_t>(T) * d;
+    uint16_t* h16 = h + slots * f;
+    const long long nx = static_cast<long long>(T) * d;
+    MOE_CUDA_OK(moek::launch_pdl(to_f16_kernel, dim3(static_cast<unsigned>(std::min<long long>((nx + 255) / 256, 1184))),
+                                 dim3(256), 0, stream, static_cast<const uint16_t*>(x), nx, x16));
+    TcArgs a{};
+    a.offsets = offsets;
+    a.perm = perm;
+    a.T = T;
+    a.k = k;
+    a.E = E;
+    a.kshift = (k & (k - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(k)) : -1;
+    a.d = d;
+    a.f = f;
+    a.active_mask = active_mask;
+    for (int e = 0; e < E; ++e) a.ex[e] = experts[e];
+    const int ntiles_max = static_cast<int>((slots + kN - 1) / kN) + E;
+    // pass 0: gate/up + SwiGLU -> h
+    a.p = 0;
+    a.bnat = static_cast<const uint16_t*>(x);
+    a.bnat16 = x16;
+    a.hout = h;
+    a.hout16 = h16;
+    MOE_CUDA_OK(moek::launch_pdl(tc_ffn_kernel, dim3(static_cast<unsigned>(ntiles_max * (f / kM))), dim3(kThreads),
+                                 kSmemBytes, stream, a));
+    // pass 1: down -> y
+    a.p = 1;
+    a.bnat = h;
+    a.bnat16 = h16;
+    a.y = y;
+    return moek::launch_pdl(tc_ffn_kernel, dim3(static_cast<unsigned>(ntiles_max * (d / kM))), dim3(kThreads),
+                            kSmemBytes, stream, a);
+}

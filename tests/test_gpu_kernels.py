@@ -172,6 +172,48 @@ def test_ffn_grouped_vs_oracle(moe, orc, torch_mod, cuda, T, mix, shape):
         assert_close(y[lo:hi], y_ref, RTOL_F32, f"expert {e} ({'bf16' if prec[e] else 'int4'})")
 
 
+@pytest.mark.parametrize("mix", ["bf16", "int4", "mixed"])
+@pytest.mark.parametrize("T,shape", [(40, (512, 1792)), (300, (512, 1792)), (96, (4096, 14336))])
+def test_ffn_tcgen05_vs_oracle(moe, orc, torch_mod, cuda, T, shape, mix):
+    """K3/K4 on tcgen05 (batched / prefill path): every expert's y rows vs
+    the oracle FFN on the same tokens (bf16: BF16 operands; int4: on-chip
+    fp16 q*s, exact dequant values)."""
+    torch = torch_mod
+    (d, f), E, k = shape, 8, 2
+    m = orc.model(1, E, k, d, f, 99)
+    prec = {"bf16": [1] * E, "int4": [0] * E, "mixed": [0, 1] * (E // 2)}[mix]
+    x = orc.step_input(m, T, T)
+    wg = orc.router_weights(m, 0)
+    idx, w, _ = orc.gate_topk(x, wg, T, d, E, k)
+    counts, offsets, perm, inv = orc.permute(idx, T, E, k)
+    experts, host, keep = [], {}, []
+    for e in range(E):
+        dev, h = _expert_tensors(orc, torch, cuda, m, e, prec[e])
+        keep.append(dev)
+        host[e] = h
+        if prec[e] == 1:
+            experts.append(moe.expert_weights(moe.MOE_P16, dev[0], dev[1]))
+        else:
+            experts.append(moe.expert_weights(moe.MOE_P4, dev[0], dev[2], dev[1], dev[3]))
+    nws = moe.ffn_tc_workspace_bytes(T, k, d, f)
+    ws = torch.empty(nws, dtype=torch.uint8, device=cuda)
+    y = torch.full((T * k * d,), float("nan"), dtype=torch.float32, device=cuda)
+    moe.ffn_tc(to_dev(x, torch, cuda), to_dev(perm, torch, cuda), to_dev(offsets, torch, cuda), T, k, experts, d, f,
+               ws, nws, y)
+    torch.cuda.synchronize()
+    y = to_np(y, np.float32).reshape(T * k, d)
+    for e in range(E):
+        lo, hi = offsets[e], offsets[e + 1]
+        if lo == hi:
+            continue
+        xs = x[perm[lo:hi] // k]
+        if prec[e] == 1:
+            y_ref = orc.ffn_bf16(xs, hi - lo, host[e][0], host[e][1], d, f)
+        else:
+            y_ref = orc.ffn_int4(xs, hi - lo, *host[e], d, f)
+        assert_close(y[lo:hi], y_ref, RTOL_F32, f"expert {e} ({'bf16' if prec[e] else 'int4'})")
+
+
 def test_combine_bitexact(moe, orc, torch_mod, cuda):
     torch = torch_mod
     T, d, k = 9, 512, 2
