@@ -215,7 +215,8 @@ typedef struct {
     int32_t use_graphs;        /* capture decode steps in CUDA graphs            */
     float norm_eps;            /* > 0: Mixtral decoder-layer RMSNorm (unit weight) before every MoE
                                   block, out = x + MoE(RMSNorm(x)); 0: out = x + MoE(x) */
-    int32_t pad_;
+    int32_t tc_min_tokens;     /* decode batches T >= this use the tcgen05 expert GEMM, smaller ones
+                                  the streaming GEMV (0: default 64) */
 } moe_engine_config;
 
 int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan_entries,

@@ -34,6 +34,7 @@ struct EngineConfig {
     int device = 0;
     bool use_graphs = true;
     float norm_eps = 0.0f;    // > 0: pre-MoE RMSNorm (unit weight), residual = un-normalised x
+    int tc_min_tokens = 64;   // T >= this: tcgen05 expert GEMM instead of the streaming GEMV
 };
 
 class MoeEngine {

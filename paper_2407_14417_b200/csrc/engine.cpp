@@ -72,7 +72,10 @@ struct MoeEngine::Impl {
     int32_t* perm = nullptr;
     int32_t* inv = nullptr;
     unsigned int* ticket = nullptr;
-    float* y = nullptr;          // per-slot expert outputs (streamed-expert path)
+    float* y = nullptr;          // per-slot expert outputs (streamed-expert and tcgen05 paths)
+    int Tgemv = 0;               // largest T of the streaming-GEMV path (workspace sizing)
+    void* tcws = nullptr;        // tcgen05 path workspace (T >= tc_min_tokens)
+    uint16_t* xn = nullptr;      // [Tmax][d] normalised rows in natural order (tcgen05 path)
     GemvWorkspace gws{};
     void* gws_base = nullptr;
     int32_t* idx_host = nullptr;  // pinned [Tmax*K]
@@ -182,10 +185,16 @@ struct MoeEngine::Impl {
         dev_alloc(reinterpret_cast<void**>(&inv), TK * 4);
         dev_alloc(reinterpret_cast<void**>(&ticket), 4);
         dev_alloc(reinterpret_cast<void**>(&y), TK * d * 4);
-        const size_t ws_bytes = moek_gemv_workspace_bytes(Tmax, K, d, f);
+        // streaming GEMV below tc_min_tokens, tcgen05 GEMM from there on
+        Tgemv = std::min(Tmax, std::max(1, cfg.tc_min_tokens - 1));
+        const size_t ws_bytes = moek_gemv_workspace_bytes(Tgemv, K, d, f);
         dev_alloc(&gws_base, ws_bytes);
         ck(cudaMemsetAsync(gws_base, 0, ws_bytes, compute), "memset");
-        gws = moek_gemv_workspace_view(gws_base, Tmax, K, d, f);
+        gws = moek_gemv_workspace_view(gws_base, Tgemv, K, d, f);
+        if (Tmax >= cfg.tc_min_tokens) {
+            dev_alloc(&tcws, moek_tc_workspace_bytes(Tmax, K, d, f));
+            dev_alloc(reinterpret_cast<void**>(&xn), static_cast<size_t>(Tmax) * d * 2);
+        }
         ck(cudaMemsetAsync(ticket, 0, 4, compute), "memset");
         ck(cudaMemsetAsync(xin, 0, static_cast<size_t>(Tmax) * d * 2, compute), "memset");
         ck(cudaHostAlloc(reinterpret_cast<void**>(&idx_host), TK * 4, cudaHostAllocDefault), "cudaHostAlloc");
@@ -239,7 +248,7 @@ struct MoeEngine::Impl {
         graphs.clear();
         if (compute) cudaStreamSynchronize(compute);
         if (copy) cudaStreamSynchronize(copy);
-        void* devp[] = {dev_arena, swap, wg, xin, xout, xbuf[0], xbuf[1], idx, wts, counts, offsets, perm, inv, ticket, y,
+        void* devp[] = {tcws, xn, dev_arena, swap, wg, xin, xout, xbuf[0], xbuf[1], idx, wts, counts, offsets, perm, inv, ticket, y,
                          gws_base};
         for (void* p : devp)
             if (p) cudaFree(p);
@@ -257,6 +266,21 @@ struct MoeEngine::Impl {
     // swap slot, Static policy) -> combine with residual.
     void layer(int l, const uint16_t* x, int T, uint16_t* out, int32_t* idx_l, float* w_l, float* logits) {
         const moe_expert_weights* lw = weights.data() + static_cast<size_t>(l) * E;
+        const bool tc = T >= cfg.tc_min_tokens && !layer_has_cpu[static_cast<size_t>(l)];
+        if (tc) {
+            // tcgen05 path: route writes the normalised rows in natural order
+            ck(moek_route(x, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx_l, w_l, logits, counts, offsets,
+                          perm, inv, ticket, compute, nullptr, nullptr, nullptr, 0, cfg.norm_eps,
+                          cfg.norm_eps > 0.0f ? xn : nullptr),
+               "route");
+            counters.activations += static_cast<int64_t>(T) * K;
+            counters.hits += static_cast<int64_t>(T) * K;
+            ck(moek_ffn_tc(tcws, cfg.norm_eps > 0.0f ? xn : x, perm, offsets, T, K, lw, E, d, f, mask_all(), y,
+                           compute), "ffn_tc");
+            ck(moek_combine(y, inv, w_l, x, T, d, K, out, compute), "combine");
+            return;
+        }
+        if (T > Tgemv) throw UsageError("T exceeds the streaming-GEMV workspace (raise tc_min_tokens / max_tokens)");
         // route also writes the K-permuted activation copies the expert
         // GEMV reads (no separate permute kernel on the critical path)
         ck(moek_route(x, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx_l, w_l, logits, counts,
@@ -336,12 +360,20 @@ struct MoeEngine::Impl {
         for (int l = 0; l < L; ++l) {
             uint16_t* dst = l == L - 1 ? xout : xbuf[l & 1];
             const moe_expert_weights* lw = weights.data() + static_cast<size_t>(l) * E;
+            const bool tc = T >= cfg.tc_min_tokens;
             ck(moek_route(src, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx + l * TK, wts + l * TK,
-                          nullptr, counts, offsets, perm, inv, ticket, compute, gws.xperm, gws.xperm16, gws.xsum,
-                          moek_group_stride(d), cfg.norm_eps), "route");
+                          nullptr, counts, offsets, perm, inv, ticket, compute, tc ? nullptr : gws.xperm,
+                          tc ? nullptr : gws.xperm16, tc ? nullptr : gws.xsum, moek_group_stride(d), cfg.norm_eps,
+                          tc && cfg.norm_eps > 0.0f ? xn : nullptr), "route");
             ck(cudaEventRecord(ev[static_cast<size_t>(2 * l)], compute), "record");
-            ck(moek_ffn_mma(gws, src, perm, offsets, inv, wts + l * TK, src, T, K, lw, E, d, f, mask_all(), dst,
-                            nullptr, MOE_X_ROUTED, compute), "ffn");
+            if (tc) {
+                ck(moek_ffn_tc(tcws, cfg.norm_eps > 0.0f ? xn : src, perm, offsets, T, K, lw, E, d, f, mask_all(), y,
+                               compute), "ffn_tc");
+                ck(moek_combine(y, inv, wts + l * TK, src, T, d, K, dst, compute), "combine");
+            } else {
+                ck(moek_ffn_mma(gws, src, perm, offsets, inv, wts + l * TK, src, T, K, lw, E, d, f, mask_all(), dst,
+                                nullptr, MOE_X_ROUTED, compute), "ffn");
+            }
             ck(cudaEventRecord(ev[static_cast<size_t>(2 * l + 1)], compute), "record");
             src = dst;
         }
@@ -365,7 +397,8 @@ struct MoeEngine::Impl {
             ffn_bytes[l] = bytes;
         }
         for (auto& e : ev) cudaEventDestroy(e);
-        // route(+x permute), gate/up stream, SwiGLU finalize, down stream, combine finalize
+        // GEMV: route(+x permute), gate/up stream, SwiGLU finalize, down stream, combine finalize
+        // tcgen05: route, x->fp16, gate/up GEMM (+SwiGLU), down GEMM, combine
         if (kernels_per_step) *kernels_per_step = 5 * L;
     }
 
@@ -444,6 +477,10 @@ void MoeEngine::forward_layer(int layer, const void* x, int T, void* out, int32_
                               float* logits) {
     if (layer < 0 || layer >= impl_->L) throw ValidationError("layer out of range");
     if (T < 1 || T > impl_->Tmax) throw ValidationError("T must be in [1, max_tokens]");
+    // routing outputs are optional: default to the engine's own per-layer buffers
+    const size_t TK = static_cast<size_t>(impl_->Tmax) * impl_->K;
+    if (idx == nullptr) idx = impl_->idx + layer * TK;
+    if (w == nullptr) w = impl_->wts + layer * TK;
     impl_->layer(layer, static_cast<const uint16_t*>(x), T, static_cast<uint16_t*>(out), idx, w, logits);
 }
 

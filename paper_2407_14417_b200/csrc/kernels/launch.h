@@ -9,7 +9,8 @@
 cudaError_t moek_route(const void* x, const void* wg, int T, int d, int E, int k, int32_t* idx,
                        float* w, float* logits, int32_t* counts, int32_t* offsets, int32_t* perm,
                        int32_t* inv_perm, unsigned int* ticket, cudaStream_t stream, void* xperm = nullptr,
-                       void* xperm16 = nullptr, float* xsum = nullptr, int xstride = 0, float norm_eps = 0.0f);
+                       void* xperm16 = nullptr, float* xsum = nullptr, int xstride = 0, float norm_eps = 0.0f,
+                       void* xnat = nullptr);
 cudaError_t moek_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_t* offsets,
                          int32_t* perm, int32_t* inv_perm, cudaStream_t stream);
 // Workspace of the tensor-core GEMV FFN (must be zeroed once; the kernels

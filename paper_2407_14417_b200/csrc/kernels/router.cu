@@ -36,6 +36,7 @@ struct RouteArgs {
     float* xsum;
     int xstride;
     float norm_eps;        // > 0: unit-weight RMSNorm of x before routing / experts (oracle orc_rmsnorm)
+    uint16_t* xnat;        // optional: the (normalised) token rows in natural order [T][d]
 };
 
 // One logit in the pinned order.  x_s is the token row staged in smem.
@@ -270,6 +271,9 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
         __syncthreads();
     }
     ltrace(1, 0);
+    if (a.xnat != nullptr)
+        for (int i = threadIdx.x * 8; i + 8 <= a.d; i += blockDim.x * 8)
+            *reinterpret_cast<uint4*>(a.xnat + static_cast<size_t>(t) * a.d + i) = *reinterpret_cast<const uint4*>(x_s + i);
     for (int e = wid; e < a.E; e += blockDim.x / 32) {
         if (e != wid) preload_w(wpre, a.wg + static_cast<size_t>(e) * a.d, a.d, lane);
         const float v = router_dot(x_s, wpre, a.wg + static_cast<size_t>(e) * a.d, a.d, lane);
@@ -341,10 +345,11 @@ __global__ void __launch_bounds__(kRouteThreads) permute_kernel(const int32_t* i
 cudaError_t moek_route(const void* x, const void* wg, int T, int d, int E, int k, int32_t* idx,
                        float* w, float* logits, int32_t* counts, int32_t* offsets, int32_t* perm,
                        int32_t* inv_perm, unsigned int* ticket, cudaStream_t stream, void* xperm, void* xperm16,
-                       float* xsum, int xstride, float norm_eps) {
+                       float* xsum, int xstride, float norm_eps, void* xnat) {
     moek::RouteArgs a{static_cast<const uint16_t*>(x), static_cast<const uint16_t*>(wg), T, d, E, k,
                       idx, w, logits, counts, offsets, perm, inv_perm, ticket,
-                      static_cast<uint16_t*>(xperm), static_cast<uint16_t*>(xperm16), xsum, xstride, norm_eps};
+                      static_cast<uint16_t*>(xperm), static_cast<uint16_t*>(xperm16), xsum, xstride, norm_eps,
+                      static_cast<uint16_t*>(xnat)};
     // x row + logits [MOE_MAX_EXPERTS] + RMSNorm partials [kRouteThreads]
     const size_t smem = ((static_cast<size_t>(d) * 2 + 15) / 16) * 16 + (MOE_MAX_EXPERTS + moek::kRouteThreads) * 4;
     if (smem > 48 * 1024) {

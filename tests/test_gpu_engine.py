@@ -25,9 +25,9 @@ def quality_plan(moe, cfg, n4, seed, budget=10**15):
     return prof, moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, seed), moe.HardwareProfile(budget), prof)
 
 
-def make_engine(moe, cfg, plan, seed, T=1, graphs=True, eps=0.0):
+def make_engine(moe, cfg, plan, seed, T=1, graphs=True, eps=0.0, tc_min=0):
     return moe.MoeEngine(cfg["num_layers"], cfg["experts_per_layer"], cfg["top_k"], cfg["d_model"], cfg["d_ffn"],
-                         plan, max_tokens=T, seed=seed, use_graphs=graphs, norm_eps=eps)
+                         plan, max_tokens=T, seed=seed, use_graphs=graphs, norm_eps=eps, tc_min_tokens=tc_min)
 
 
 def layer_precisions(plan, layer, E):
@@ -210,4 +210,53 @@ def test_mixtral_stack_prenorm_is_finite(moe, torch_mod, cuda):
         assert np.isfinite(out).all()
         r = eng.last_routing(1)
         assert all(r[2 * l] != r[2 * l + 1] for l in range(32))
+    eng.close()
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-5])
+@pytest.mark.parametrize("T", [32, 100])
+def test_tiny_layer_parity_tcgen05(moe, orc, torch_mod, cuda, T, eps):
+    """Batched decode through the engine's tcgen05 expert GEMM (T >= tc_min):
+    routing bit-exact, layer output within tolerance, mixed int4/bf16 plan."""
+    torch = torch_mod
+    seed = 17
+    _, plan = quality_plan(moe, TINY, 8, 1)
+    eng = make_engine(moe, TINY, plan, seed, T, eps=eps, tc_min=16)
+    m = orc.model(2, 8, 2, 512, 1792, seed, eps)
+    x = orc.step_input(m, 3, T)
+    for layer in range(2):
+        out_ref, idx_ref, _, lg_ref = orc.moe_layer(m, layer, layer_precisions(plan, layer, 8), x, T)
+        out = torch.empty(T * 512, dtype=torch.int16, device=cuda)
+        idx = torch.empty(T * 2, dtype=torch.int32, device=cuda)
+        w = torch.empty(T * 2, dtype=torch.float32, device=cuda)
+        lg = torch.empty(T * 8, dtype=torch.float32, device=cuda)
+        eng.forward_layer(layer, to_dev(x, torch, cuda), T, out, idx, w, lg)
+        eng.sync()
+        assert np.array_equal(to_np(lg, np.float32).view(np.uint32).reshape(T, 8), lg_ref.view(np.uint32))
+        assert np.array_equal(to_np(idx, np.int32).reshape(T, 2), idx_ref)
+        got = to_np(out, np.uint16).reshape(T, 512)
+        assert_close(bf16_to_f32(got), bf16_to_f32(out_ref), RTOL_BF16, f"layer {layer}")
+        x = got
+    eng.close()
+
+
+@pytest.mark.parametrize("precision", [1, 0])
+def test_mixtral_layer_parity_tcgen05(moe, orc, torch_mod, cuda, precision):
+    """C5-shaped batch (128 tokens) on one Mixtral layer through tcgen05."""
+    torch = torch_mod
+    T = 128
+    cfg = dict(MIXTRAL, num_layers=1)
+    prof = moe.profile_for_shape(4096, 14336, 1)
+    plan = moe.assign_locations([precision] * 8, moe.HardwareProfile(10**15), prof)
+    eng = make_engine(moe, cfg, plan, 2025, T, eps=1e-5)
+    m = orc.model(1, 8, 2, 4096, 14336, 2025, 1e-5)
+    x = orc.step_input(m, 0, T)
+    out_ref, idx_ref, _, _ = orc.moe_layer(m, 0, [precision] * 8, x, T)
+    out = torch.empty(T * 4096, dtype=torch.int16, device=cuda)
+    idx = torch.empty(T * 2, dtype=torch.int32, device=cuda)
+    eng.forward_layer(0, to_dev(x, torch, cuda), T, out, idx)
+    eng.sync()
+    assert np.array_equal(to_np(idx, np.int32).reshape(T, 2), idx_ref)
+    assert_close(bf16_to_f32(to_np(out, np.uint16).reshape(T, 4096)), bf16_to_f32(out_ref), RTOL_BF16,
+                 f"mixtral layer tcgen05 {'bf16' if precision else 'int4'}")
     eng.close()
