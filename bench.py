@@ -46,6 +46,14 @@ NORM_EPS = 1e-5
 METRIC = "decode tokens/s vs #4-bit experts (Mixtral-8x7B shape); expert-FFN HBM GB/s"
 
 
+def _peak_tflops():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["bf16_tflops"])
+    except Exception:
+        return 1590.0
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -269,6 +277,47 @@ def run_ours(args, rank, world, device):
             e.close()
             del e
 
+    # ---- decode batch sweep at the headline n4 (GEMV below tc_min, tcgen05 from there) ----
+    batch = []
+    if args.batch_sweep and args.batch_points:
+        plan_b = moe.make_plan(moe.TaskRequest(moe.QUALITY, args.n4, 0), moe.HardwareProfile(10**15), prof)
+        eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan_b, max_tokens=max(args.batch_points),
+                            seed=args.seed + rank, device=device, norm_eps=NORM_EPS)
+        for tb in args.batch_points:
+            eng.synth_input(0, tb)
+            eng.decode(tb)
+            eng.sync()
+            m = time_engine(moe, torch, eng, tb, max(5, min(args.steps, 30)), 3)
+            batch.append({"batch": tb, "tokens_per_s": round(world * tb * 1000.0 / m, 1), "ms_per_step": round(m, 4),
+                          "path": "tcgen05" if tb >= 64 else "gemv"})
+        eng.close()
+        del eng
+
+    # ---- prefill: one Mixtral layer, tcgen05 expert GEMM, TFLOP/s ----------
+    prefill = []
+    if args.prefill and args.prefill_points:
+        prof1 = moe.profile_for_shape(D_MODEL, D_FFN, 1, EXPERTS, TOPK)
+        tf_peak = _peak_tflops()
+        for prec in (1, 0):
+            plan1 = moe.assign_locations([prec] * EXPERTS, moe.HardwareProfile(10**15), prof1)
+            eng = moe.MoeEngine(1, EXPERTS, TOPK, D_MODEL, D_FFN, plan1, max_tokens=max(args.prefill_points),
+                                seed=args.seed + rank, device=device, norm_eps=NORM_EPS)
+            for tp in args.prefill_points:
+                eng.synth_input(1, tp)
+                eng.decode(tp)
+                eng.sync()
+                fm = []
+                for _ in range(4):
+                    m_, _, _ = eng.profile_step(tp)
+                    fm.append(m_[0])
+                ffn = sorted(fm)[len(fm) // 2]
+                flops = 6.0 * D_MODEL * D_FFN * tp * TOPK
+                tf = flops / (ffn * 1e-3) / 1e12
+                prefill.append({"tokens": tp, "experts": "bf16" if prec else "int4-g128", "ffn_ms": round(ffn, 4),
+                                "tflops": round(tf, 1), "frac_of_peak": round(tf / tf_peak, 4)})
+            eng.close()
+            del eng
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tps, cores, sample = cpu_port_tokens_per_s(plan.precision[:EXPERTS], T, seconds=args.cpu_seconds)
@@ -298,8 +347,91 @@ def run_ours(args, rank, world, device):
             "kernels_per_step": kps,
             "clocks": clocks,
             "sweep": sweep,
+            "batch_sweep": batch,
+            "prefill_tcgen05": {"points": prefill, "peak_tflops": _peak_tflops(),
+                                "peak_kind": "MEASURED_PEAKS bf16_tflops (burst)",
+                                "flops": "6*d*f*T*k (gate/up + down, top-k=2)",
+                                "timed": "expert FFN launches of one layer (to_f16, 2 x tcgen05 GEMM, combine)"},
             "cpu_baseline": cpu,
             "bytes_per_expert": {"bf16": s16, "int4_g128": s4},
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_ep(args, rank, world, device):
+    """Expert-parallel decode over `world` GPUs (paper_2407_14417_b200/ep.py):
+    experts of every layer sharded (slot s -> rank s*world//8), T_local tokens
+    per rank (weak scaling), all-gather dispatch + reduce-scatter combine over
+    NCCL.  Timed with CUDA events between barriers, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import paper_2407_14417_b200 as moe
+    from paper_2407_14417_b200 import ep
+    prof = moe.profile_for_shape(D_MODEL, D_FFN, LAYERS, EXPERTS, TOPK)
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, args.n4, 0), moe.HardwareProfile(10**15), prof)
+    T_local = args.tokens
+    T = T_local * world
+    # identical synthetic weights on every rank (each rank reads only its shard)
+    eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan, max_tokens=T, seed=args.seed, device=device,
+                        norm_eps=NORM_EPS)
+    ops = ep.EngineOps(moe, torch, eng, rank, world, T, NORM_EPS, torch.device(f"cuda:{device}"))
+    dec = ep.ExpertParallelDecoder(dist, ops, rank, world, T_local, EXPERTS)
+    eng.synth_input(0, T)
+    eng.sync()
+    x_all = torch.as_tensor(_DevBytes(eng.input_ptr, T * D_MODEL * 2), device=f"cuda:{device}").view(torch.int16)
+    x_local = x_all[rank * T_local * D_MODEL:(rank + 1) * T_local * D_MODEL].clone()
+    for _ in range(args.warmup):
+        dec.decode(x_local)
+    torch.cuda.synchronize()
+    dist.barrier()
+    stream = torch.cuda.current_stream()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(5, min(args.steps, 50))
+    with ClockSampler(device) as clk:
+        start.record(stream)
+        for _ in range(steps):
+            dec.decode(x_local)
+        end.record(stream)
+        end.synchronize()
+    clocks = clk.summary()
+    ms = start.elapsed_time(end) / steps
+    t = torch.tensor([ms], device=f"cuda:{device}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    # e2e: pinned host rows in, output rows back, every step
+    xh = x_local.cpu().pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    xd = torch.empty_like(x_local)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        xd.copy_(xh, non_blocking=True)
+        out = dec.decode(xd)
+        oh.copy_(out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e2e_s = (time.perf_counter() - t0) / steps
+    t = torch.tensor([e2e_s], device=f"cuda:{device}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    eng.close()
+    if rank == 0:
+        xb = ep.exchange_bytes(T_local, world, D_MODEL)
+        line = {
+            "metric": METRIC, "value": round(world * T_local * 1000.0 / ms, 3), "unit": "tokens/s", "n_gpus": world,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 / int4-g128 weights, bf16 activations, fp32 accumulate",
+            "data": "synthetic (seeded counter-based generator)",
+            "config": {"workload": "mixtral8x7b-shape 32-layer MoE stack, expert-parallel batch-%d/GPU decode" % T_local,
+                       "n4": args.n4, "of": LAYERS * EXPERTS, "layer": "x + MoE(RMSNorm(x))",
+                       "parallelism": "ep%d" % world, "experts_per_gpu_per_layer": EXPERTS // world if world <= EXPERTS else 1,
+                       "exchange": "NCCL all-gather (dispatch) + reduce-scatter (combine) per layer",
+                       "exchange_bytes_per_layer_per_gpu": xb, "batch_per_gpu": T_local,
+                       "l2": "no flush: every step streams GBs of distinct expert weights per GPU"},
+            "e2e": {"value": round(world * T_local / e2e_s, 3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": world * T_local * D_MODEL * 2, "d2h_bytes_per_step": world * T_local * D_MODEL * 2},
+            # per layer: route, permute_rows, 2 streams, 2 finalizes, combine_partial, residual_add
+            "gpu_launches": 8 * LAYERS * steps, "clocks": clocks, "cpu_baseline": None,
+            "note": "expert parallel (not replicas): every GPU computes only its slots of each layer",
         }
         print(json.dumps(line), flush=True)
 
@@ -322,6 +454,14 @@ def main():
     ap.add_argument("--sweep-points", type=lambda s: [int(v) for v in s.split(",")],
                     default=[0, 32, 64, 96, 128, 160, 192, 224, 256])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of expert parallel")
+    ap.add_argument("--ep", action="store_true", help="expert-parallel code path even at N=1 (NCCL, 1 rank)")
+    ap.add_argument("--no-batch-sweep", dest="batch_sweep", action="store_false")
+    ap.add_argument("--batch-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],
+                    default=[1, 8, 32, 64, 128, 256])
+    ap.add_argument("--no-prefill", dest="prefill", action="store_false")
+    ap.add_argument("--prefill-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],
+                    default=[512, 2048, 4096])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -338,7 +478,18 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    run_ours(args, rank, world, local)
+    if (world > 1 and not args.replicas) or args.ep:
+        if world == 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(f"cuda:{local}"))
+        run_ep(args, rank, world, local)
+        if world == 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    else:
+        run_ours(args, rank, world, local)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

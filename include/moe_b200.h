@@ -127,6 +127,15 @@ double moe_expected_throughput(const moe_expert_state* entries, const moe_model_
 int moe_gate_topk(const void* x, const void* wg, int T, int d, int E, int k, int32_t* idx,
                   float* w, float* logits, void* stream);
 
+/* K1+K2 fused (the engine's route kernel): optional unit-weight RMSNorm
+ * (norm_eps > 0, pinned order = oracle orc_rmsnorm) of x, the router and,
+ * when counts != NULL, the stable permutation (offsets [E+1], perm, inv_perm;
+ * `ticket` = 4 zeroed bytes, left zeroed).  xnat (optional) receives the
+ * normalised rows [T,d] in natural order (the expert FFN input). */
+int moe_route(const void* x, const void* wg, int T, int d, int E, int k, float norm_eps, int32_t* idx, float* w,
+              float* logits, int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv_perm, void* xnat,
+              uint32_t* ticket, void* stream);
+
 /* K2: stable expert-major counting sort of the T*k (token, j) pairs.
  * counts [E], offsets [E+1], perm [T*k] (perm[pos] = t*k + j),
  * inv_perm [T*k] (inv_perm[t*k + j] = pos).  Bit-exact, no atomics. */
@@ -146,6 +155,8 @@ typedef struct {
 } moe_expert_weights;
 
 /* K3/K4: grouped SwiGLU FFN of every expert segment of a permutation, on the
+ * streaming GEMV (experts whose w_gate_up is NULL -- another rank's shard --
+ * are skipped and their y_perm rows left untouched), on the
  * tensor-core GEMV (<= 8 tokens per expert share each weight byte; larger
  * segments are tiled).  x [T,d] bf16 (natural order), offsets [E+1] (device),
  * experts[E] (host array of device pointers), y_perm [T*k, d] fp32.
@@ -181,6 +192,15 @@ int moe_ffn_tc(const void* x, const int32_t* perm, const int32_t* offsets, int T
  * fp32 fma chain in j order; residual may be NULL. */
 int moe_combine(const float* y_perm, const int32_t* inv_perm, const float* w,
                 const void* residual, int T, int d, int k, void* out, void* stream);
+
+/* Expert-parallel combine: this rank's share of every
+ * token's output, out[t] = sum over j with bit idx[t,j] of expert_mask of
+ * w[t,j] * y_perm[inv_perm[t*k+j]] (fp32, j order).  The shares of all ranks
+ * are summed by a reduce-scatter; moe_residual_add then forms
+ * out = bf16(residual + sum). */
+int moe_combine_partial(const float* y_perm, const int32_t* inv_perm, const float* w, const int32_t* idx,
+                        uint64_t expert_mask, int T, int d, int k, float* out, void* stream);
+int moe_residual_add(const void* residual, const float* part, int64_t n, void* out, void* stream);
 
 /* int4-g128 quantiser: logical row-major bf16 [rows,cols] -> int4 fragment
  * blocks q (rows*cols/8 uint32) + scale blocks s (rows*cols/128 bf16); the

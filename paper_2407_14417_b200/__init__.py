@@ -122,6 +122,9 @@ def lib() -> C.CDLL:
         "moe_ffn": (I, [VP, VP, VP, I, I, P(ExpertWeightsC), I, I, I, VP, C.c_size_t, VP, VP]),
         "moe_ffn_int4": (I, [VP, VP, VP, I, I, P(VP), P(VP), P(VP), P(VP), I, I, I, VP, C.c_size_t, VP, VP]),
         "moe_ffn_tc_workspace_bytes": (C.c_size_t, [I, I, I, I]),
+        "moe_route": (I, [VP, VP, I, I, I, I, C.c_float, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP]),
+        "moe_combine_partial": (I, [VP, VP, VP, VP, C.c_uint64, I, I, I, VP, VP]),
+        "moe_residual_add": (I, [VP, VP, C.c_int64, VP, VP]),
         "moe_ffn_tc": (I, [VP, VP, VP, I, I, P(ExpertWeightsC), I, I, I, VP, C.c_size_t, VP, VP]),
         "moe_ffn_bf16": (I, [VP, VP, VP, I, I, P(VP), P(VP), I, I, I, VP, C.c_size_t, VP, VP]),
         "moe_pack_bf16_blocks": (I, [VP, I, I, VP, VP]),
@@ -443,6 +446,23 @@ def ffn(x, perm, offsets, T, k, experts: Sequence[ExpertWeightsC], d, f, workspa
     arr = (ExpertWeightsC * len(experts))(*experts)
     _check(lib().moe_ffn(_ptr(x), _ptr(perm), _ptr(offsets), T, k, arr, len(experts), d, f, _ptr(workspace),
                          ws_bytes, _ptr(y_perm), _stream(stream)))
+
+
+def route(x, wg, T, d, E, k, norm_eps, idx, w, logits=None, counts=None, offsets=None, perm=None, inv_perm=None,
+          xnat=None, ticket=None, stream=None):
+    """K1+K2 fused (RMSNorm -> router -> top-k -> stable permutation)."""
+    _check(lib().moe_route(_ptr(x), _ptr(wg), T, d, E, k, C.c_float(norm_eps), _ptr(idx), _ptr(w), _ptr(logits),
+                           _ptr(counts), _ptr(offsets), _ptr(perm), _ptr(inv_perm), _ptr(xnat), _ptr(ticket),
+                           _stream(stream)))
+
+
+def combine_partial(y_perm, inv_perm, w, idx, expert_mask, T, d, k, out, stream=None):
+    _check(lib().moe_combine_partial(_ptr(y_perm), _ptr(inv_perm), _ptr(w), _ptr(idx), expert_mask, T, d, k,
+                                     _ptr(out), _stream(stream)))
+
+
+def residual_add(residual, part, n, out, stream=None):
+    _check(lib().moe_residual_add(_ptr(residual), _ptr(part), n, _ptr(out), _stream(stream)))
 
 
 def ffn_tc_workspace_bytes(T, k, d, f) -> int:

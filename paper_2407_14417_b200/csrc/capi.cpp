@@ -323,6 +323,42 @@ int moe_gate_topk(const void* x, const void* wg, int T, int d, int E, int k, int
     });
 }
 
+int moe_route(const void* x, const void* wg, int T, int d, int E, int k, float norm_eps, int32_t* idx, float* w,
+              float* logits, int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv_perm, void* xnat,
+              uint32_t* ticket, void* stream) {
+    return guarded([&] {
+        usage_if(T < 0 || d <= 0 || d % 8 != 0, "d must be a positive multiple of 8");
+        usage_if(E < 1 || E > MOE_MAX_EXPERTS || k < 1 || k > E || k > MOE_MAX_TOPK, "bad E / k");
+        usage_if(!(norm_eps >= 0.0f), "norm_eps must be >= 0");
+        usage_if(counts != nullptr && (offsets == nullptr || perm == nullptr || inv_perm == nullptr || ticket == nullptr),
+                 "the fused permutation needs offsets, perm, inv_perm and a zeroed ticket");
+        need_device();
+        if (T == 0) return;
+        const cudaError_t e = moek_route(x, wg, T, d, E, k, idx, w, logits, counts, offsets, perm, inv_perm, ticket,
+                                         st(stream), nullptr, nullptr, nullptr, 0, norm_eps, xnat);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("moe_route: ") + cudaGetErrorString(e));
+    });
+}
+
+int moe_combine_partial(const float* y_perm, const int32_t* inv_perm, const float* w, const int32_t* idx,
+                        uint64_t expert_mask, int T, int d, int k, float* out, void* stream) {
+    return guarded([&] {
+        usage_if(T < 0 || d <= 0 || d % 4 != 0 || k < 1, "bad T / d / k");
+        need_device();
+        const cudaError_t e = moek_combine_partial(y_perm, inv_perm, w, idx, expert_mask, T, d, k, out, st(stream));
+        if (e != cudaSuccess) throw std::runtime_error(std::string("moe_combine_partial: ") + cudaGetErrorString(e));
+    });
+}
+
+int moe_residual_add(const void* residual, const float* part, int64_t n, void* out, void* stream) {
+    return guarded([&] {
+        usage_if(n < 0, "bad n");
+        need_device();
+        const cudaError_t e = moek_residual_add(residual, part, n, out, st(stream));
+        if (e != cudaSuccess) throw std::runtime_error(std::string("moe_residual_add: ") + cudaGetErrorString(e));
+    });
+}
+
 int moe_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_t* offsets,
                 int32_t* perm, int32_t* inv_perm, void* stream) {
     return guarded([&] {
@@ -352,7 +388,9 @@ int moe_ffn(const void* x, const int32_t* perm, const int32_t* offsets, int T, i
         usage_if(workspace == nullptr || ws_bytes < moek_gemv_workspace_bytes(T, k, d, f),
                  "workspace too small (moe_ffn_workspace_bytes)");
         const GemvWorkspace ws = moek_gemv_workspace_view(workspace, T, k, d, f);
-        const uint64_t mask = E >= 64 ? ~0ull : ((1ull << E) - 1ull);
+        uint64_t mask = 0;  // experts without weights (another rank's shard) are skipped
+        for (int i = 0; i < E; ++i)
+            if (experts[i].w_gate_up != nullptr) mask |= 1ull << i;
         const cudaError_t e = moek_ffn_mma(ws, x, perm, offsets, nullptr, nullptr, nullptr, T, k, experts, E, d, f,
                                            mask, nullptr, y_perm, MOE_X_PERMUTE, st(stream));
         if (e != cudaSuccess) throw std::runtime_error(std::string("moe_ffn: ") + cudaGetErrorString(e));
@@ -371,7 +409,9 @@ int moe_ffn_tc(const void* x, const int32_t* perm, const int32_t* offsets, int T
         if (T == 0) return;
         usage_if(workspace == nullptr || ws_bytes < moek_tc_workspace_bytes(T, k, d, f),
                  "workspace too small (moe_ffn_tc_workspace_bytes)");
-        const uint64_t mask = E >= 64 ? ~0ull : ((1ull << E) - 1ull);
+        uint64_t mask = 0;  // experts without weights (another rank's shard) are skipped
+        for (int i = 0; i < E; ++i)
+            if (experts[i].w_gate_up != nullptr) mask |= 1ull << i;
         const cudaError_t e = moek_ffn_tc(workspace, x, perm, offsets, T, k, experts, E, d, f, mask, y_perm, st(stream));
         if (e != cudaSuccess) throw std::runtime_error(std::string("moe_ffn_tc: ") + cudaGetErrorString(e));
     });

@@ -60,6 +60,9 @@ cudaError_t moek_quantize_blocks(const void* w, int rows, int cols, uint32_t* qb
 cudaError_t moek_combine(const float* y, const int32_t* inv, const float* w, const void* res, int T,
                          int d, int k, void* out, cudaStream_t stream);
 cudaError_t moek_quantize(const void* w, int rows, int cols, uint32_t* q, void* s, cudaStream_t stream);
+cudaError_t moek_combine_partial(const float* y, const int32_t* inv, const float* w, const int32_t* idx,
+                                 unsigned long long mask, int T, int d, int k, float* out, cudaStream_t stream);
+cudaError_t moek_residual_add(const void* res, const float* part, long long n, void* out, cudaStream_t stream);
 cudaError_t moek_synth_weight(uint64_t seed, uint64_t uid, long long n, int shift, void* out,
                               cudaStream_t stream);
 cudaError_t moek_synth_input(uint64_t seed, uint64_t uid, long long n, void* out, cudaStream_t stream);

@@ -1,4 +1,6 @@
 // misc.cu -- K5 combine, the int4-g128 quantiser, synthetic tensor generators.
+#include <algorithm>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -33,6 +35,38 @@ __global__ void combine_kernel(const float* __restrict__ y, const int32_t* __res
     o.x = static_cast<uint32_t>(f2bf(acc[0])) | (static_cast<uint32_t>(f2bf(acc[1])) << 16);
     o.y = static_cast<uint32_t>(f2bf(acc[2])) | (static_cast<uint32_t>(f2bf(acc[3])) << 16);
     *reinterpret_cast<uint2*>(out + static_cast<size_t>(t) * d + c) = o;
+}
+
+// Expert-parallel combine: this rank's share of every token's output,
+// part[t, c] = sum over j with expert idx[t,j] in `mask` of w[t,j] * y[inv[t*k+j], c]
+// (fp32 fma chain in j order from 0); the ranks' shares are summed by a
+// reduce-scatter and added to the residual by residual_add_kernel.
+__global__ void combine_partial_kernel(const float* __restrict__ y, const int32_t* __restrict__ inv,
+                                       const float* __restrict__ w, const int32_t* __restrict__ idx,
+                                       unsigned long long mask, int T, int d, int k, float* __restrict__ out) {
+    const int groups = d / 4;
+    const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid >= static_cast<long long>(T) * groups) return;
+    const int t = static_cast<int>(gid / groups), c = static_cast<int>(gid - static_cast<long long>(t) * groups) * 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+        if (!((mask >> idx[t * k + j]) & 1ull)) continue;
+        const float wj = w[t * k + j];
+        const float4 v = *reinterpret_cast<const float4*>(y + static_cast<size_t>(inv[t * k + j]) * d + c);
+        acc.x = __fmaf_rn(wj, v.x, acc.x);
+        acc.y = __fmaf_rn(wj, v.y, acc.y);
+        acc.z = __fmaf_rn(wj, v.z, acc.z);
+        acc.w = __fmaf_rn(wj, v.w, acc.w);
+    }
+    *reinterpret_cast<float4*>(out + static_cast<size_t>(t) * d + c) = acc;
+}
+
+// out = bf16(res + part), one rounding
+__global__ void residual_add_kernel(const uint16_t* __restrict__ res, const float* __restrict__ part, long long n,
+                                    uint16_t* __restrict__ out) {
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[i] = f2bf(__fadd_rn(bf2f(res[i]), part[i]));
 }
 
 // int4-g128 RTN quantiser (oracle orc_quantize_g128): one warp per
@@ -177,6 +211,23 @@ cudaError_t moek_combine(const float* y, const int32_t* inv, const float* w, con
     const int threads = 256;
     moek::combine_kernel<<<static_cast<unsigned>((n + threads - 1) / threads), threads, 0, stream>>>(
         y, inv, w, static_cast<const uint16_t*>(res), T, d, k, static_cast<uint16_t*>(out));
+    return cudaGetLastError();
+}
+
+cudaError_t moek_combine_partial(const float* y, const int32_t* inv, const float* w, const int32_t* idx,
+                                 unsigned long long mask, int T, int d, int k, float* out, cudaStream_t stream) {
+    const long long n = static_cast<long long>(T) * (d / 4);
+    if (n == 0) return cudaSuccess;
+    moek::combine_partial_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(y, inv, w, idx, mask, T, d,
+                                                                                           k, out);
+    return cudaGetLastError();
+}
+
+cudaError_t moek_residual_add(const void* res, const float* part, long long n, void* out, cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    const long long blocks = std::min<long long>((n + 255) / 256, 4096);
+    moek::residual_add_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        static_cast<const uint16_t*>(res), part, n, static_cast<uint16_t*>(out));
     return cudaGetLastError();
 }
 

@@ -1,0 +1,195 @@
+"""Expert parallelism.
+
+CPU: two gloo ranks run the ExpertParallelDecoder orchestration (all-gather
+of the rows, replicated routing, own-expert FFN, partial combine,
+reduce-scatter, residual). The per-rank arithmetic is the CPU oracle
+(test-only). The test checks the result against the single-process oracle
+stack.
+
+GPU: G virtual ranks in one process use the real kernels (moe_route, the
+masked moe_ffn / moe_ffn_tc, moe_combine_partial, moe_residual_add). Their
+summed shares must reproduce the engine's layer output.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from helpers import RTOL_BF16, TINY, assert_close, bf16_to_f32, to_dev, to_np
+
+E, K, D, F, L, SEED, EPS = 8, 2, 512, 1792, 2, 77, 1e-5
+
+
+def _bf16_rne(x):
+    u = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+class OracleOps:
+    """Per-rank arithmetic of the EP decoder on the CPU oracle (test-only)."""
+
+    def __init__(self, torch, orc, m, precisions, rank, world):
+        from paper_2407_14417_b200 import ep
+        self.torch, self.orc, self.m = torch, orc, m
+        self.num_layers, self.d = m.num_layers, m.d_model
+        self.prec = precisions
+        self.mine = set(ep.local_slots(rank, m.num_experts, world))
+        self.wg = [orc.router_weights(m, l) for l in range(m.num_layers)]
+        self.ex = {}
+        for l in range(m.num_layers):
+            for s in self.mine:
+                e = l * m.num_experts + s
+                self.ex[(l, s)] = orc.expert_bf16(m, e) if precisions[e] == 1 else orc.expert_int4(m, e)
+
+    def empty_rows(self, n, fp32):
+        return self.torch.zeros(n, dtype=self.torch.float32 if fp32 else self.torch.int16)
+
+    def route(self, layer, xg, T):
+        m, orc = self.m, self.orc
+        x = xg.numpy().view(np.uint16).reshape(T, self.d)
+        xn = orc.rmsnorm(x, T, self.d, m.norm_eps)
+        idx, w, _ = orc.gate_topk(xn, self.wg[layer], T, self.d, m.num_experts, m.top_k)
+        counts, offsets, perm, inv = orc.permute(idx, T, m.num_experts, m.top_k)
+        return dict(layer=layer, xn=xn, idx=idx.reshape(-1), w=w.reshape(-1), offsets=offsets, perm=perm, inv=inv)
+
+    def ffn(self, layer, st, T):
+        m, orc, k = self.m, self.orc, self.m.top_k
+        y = np.zeros((T * k, self.d), np.float32)
+        for s in self.mine:
+            lo, hi = st["offsets"][s], st["offsets"][s + 1]
+            if lo == hi:
+                continue
+            xs = st["xn"][st["perm"][lo:hi] // k]
+            w = self.ex[(layer, s)]
+            if self.prec[layer * m.num_experts + s] == 1:
+                y[lo:hi] = orc.ffn_bf16(xs, hi - lo, w[0], w[1], self.d, m.d_ffn)
+            else:
+                y[lo:hi] = orc.ffn_int4(xs, hi - lo, *w, self.d, m.d_ffn)
+        return y
+
+    def combine_partial(self, st, y, mask, T, part):
+        k = self.m.top_k
+        out = np.zeros((T, self.d), np.float32)
+        for t in range(T):
+            for j in range(k):
+                if (mask >> int(st["idx"][t * k + j])) & 1:
+                    out[t] = (np.float64(st["w"][t * k + j]) * y[st["inv"][t * k + j]] + out[t]).astype(np.float32)
+        part.copy_(self.torch.from_numpy(out.reshape(-1)))
+
+    def residual_add(self, x_local, mine, out_local):
+        x = bf16_to_f32(x_local.numpy().view(np.uint16))
+        out_local.copy_(self.torch.from_numpy(_bf16_rne(x + mine.numpy()).view(np.int16)))
+
+
+def _ep_worker(rank, world, port, T_local, q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle.oracle import OracleLib
+    from paper_2407_14417_b200 import ep
+    import paper_2407_14417_b200 as moe
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = None
+    try:
+        orc = OracleLib()
+        m = orc.model(L, E, K, D, F, SEED, EPS)
+        prof = moe.profile_for_shape(D, F, L)
+        plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 1), moe.HardwareProfile(10**15), prof)
+        ops = OracleOps(torch, orc, m, plan.precision, rank, world)
+        dec = ep.ExpertParallelDecoder(dist, ops, rank, world, T_local, E)
+        T = T_local * world
+        x_all = orc.step_input(m, 5, T)
+        x_local = torch.from_numpy(x_all[rank * T_local:(rank + 1) * T_local].reshape(-1).view(np.int16).copy())
+        out = dec.decode(x_local).numpy().view(np.uint16).copy()
+    except Exception as exc:  # report instead of leaving the peer waiting
+        out = repr(exc)
+    finally:
+        q.put((rank, out))
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_partition_and_exchange_sizes():
+    from paper_2407_14417_b200 import ep
+    assert [ep.owner_of(s, 8, 8) for s in range(8)] == list(range(8))
+    assert [ep.owner_of(s, 8, 2) for s in range(8)] == [0, 0, 0, 0, 1, 1, 1, 1]
+    assert ep.local_slots(1, 8, 4) == [2, 3]
+    masks = [ep.expert_mask(r, 8, 4) for r in range(4)]
+    assert sum(masks) == 0xFF and all(a & b == 0 for i, a in enumerate(masks) for b in masks[i + 1:])
+    assert ep.exchange_bytes(1, 8, 4096) == {"all_gather": 7 * 8192, "reduce_scatter": 7 * 16384}
+
+
+@pytest.mark.parametrize("T_local", [1, 3])
+def test_ep_two_ranks_gloo_matches_single_process(orc, T_local):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ep_worker, args=(r, 2, port, T_local, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert not isinstance(res[r], str), f"rank {r}: {res[r]}"
+    for p in procs:
+        assert p.exitcode == 0
+    import paper_2407_14417_b200 as moe
+    m = orc.model(L, E, K, D, F, SEED, EPS)
+    prof = moe.profile_for_shape(D, F, L)
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 1), moe.HardwareProfile(10**15), prof)
+    T = 2 * T_local
+    x = orc.step_input(m, 5, T)
+    for l in range(L):
+        x, _, _, _ = orc.moe_layer(m, l, plan.precision[l * E:(l + 1) * E], x, T)
+    got = np.concatenate([res[0].reshape(T_local, D), res[1].reshape(T_local, D)])
+    assert_close(bf16_to_f32(got), bf16_to_f32(x), RTOL_BF16, "EP(2 ranks) vs single process")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,T", [(2, 3), (4, 4), (8, 8), (2, 96)])
+def test_ep_virtual_ranks_gpu(moe, cuda, world, T):
+    """The EP kernels on one GPU: G virtual ranks' shares summed == engine."""
+    import torch
+    from paper_2407_14417_b200 import ep
+    prof = moe.profile_for_shape(D, F, L)
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 1), moe.HardwareProfile(10**15), prof)
+    eng = moe.MoeEngine(L, E, K, D, F, plan, max_tokens=T, seed=SEED, use_graphs=False, norm_eps=EPS,
+                        tc_min_tokens=64)
+    eng.synth_input(2, T)
+    eng.sync()
+    x = torch.empty(T * D, dtype=torch.int16, device=cuda)
+    x.copy_(torch.as_tensor(_Dev(eng.input_ptr, T * D), device=cuda))
+    ref = torch.empty_like(x)
+    ridx = torch.empty(T * K, dtype=torch.int32, device=cuda)
+    eng.forward_layer(0, x, T, ref, ridx)
+    eng.sync()
+    total = torch.zeros(T * D, dtype=torch.float32, device=cuda)
+    for r in range(world):
+        ops = ep.EngineOps(moe, torch, eng, r, world, T, EPS, cuda)
+        ops.route(0, x, T)
+        y = ops.ffn(0, 0, T)
+        part = torch.zeros(T * D, dtype=torch.float32, device=cuda)
+        ops.combine_partial(0, y, ep.expert_mask(r, E, world), T, part)
+        total += part
+        assert torch.equal(ops.idx, ridx)
+    out = torch.empty_like(x)
+    moe.residual_add(x, total, T * D, out)
+    torch.cuda.synchronize()
+    assert_close(bf16_to_f32(to_np(out, np.uint16)), bf16_to_f32(to_np(ref, np.uint16)), RTOL_BF16,
+                 f"EP virtual ranks G={world}")
+    eng.close()
+
+
+class _Dev:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i2", "data": (ptr, False), "version": 3}
