@@ -318,6 +318,11 @@ def run_ours(args, rank, world, device):
             eng.close()
             del eng
 
+    # ---- C4: host-resident expert fraction streamed through the swap slot ----
+    host_split = None
+    if args.host_split and rank == 0:
+        host_split = host_split_sweep(moe, torch, prof, args, device)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tps, cores, sample = cpu_port_tokens_per_s(plan.precision[:EXPERTS], T, seconds=args.cpu_seconds)
@@ -348,6 +353,7 @@ def run_ours(args, rank, world, device):
             "clocks": clocks,
             "sweep": sweep,
             "batch_sweep": batch,
+            "host_split": host_split,
             "prefill_tcgen05": {"points": prefill, "peak_tflops": _peak_tflops(),
                                 "peak_kind": "MEASURED_PEAKS bf16_tflops (burst)",
                                 "flops": "6*d*f*T*k (gate/up + down, top-k=2)",
@@ -356,6 +362,76 @@ def run_ours(args, rank, world, device):
             "bytes_per_expert": {"bf16": s16, "int4_g128": s4},
         }
         print(json.dumps(line), flush=True)
+
+
+def h2d_gbs(torch, device, nbytes=1 << 30):
+    """Pinned host -> device copy bandwidth (cudaMemcpyAsync), best of 3."""
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+    best = 0.0
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = max(best, nbytes / (a.elapsed_time(b) * 1e-3) / 1e9)
+    del src, dst
+    return best
+
+
+def host_split_sweep(moe, torch, prof, args, device):
+    """C4: plan_quality(n4, budget) over budgets from full
+    residency down to the non-expert + swap floor; host-resident experts live
+    in a pinned arena and are re-streamed into the single swap slot on every
+    activation (Static policy, simulator.cpp:98-106).  Reports measured
+    tokens/s, the engine's counters == the reference cost model's simulate()
+    on the exported routing, and expected_throughput with the measured H2D
+    bandwidth and compute_penalty4 = 1."""
+    bw = h2d_gbs(torch, device)
+    n4 = args.host_split_n4
+    s16, s4 = moe.expert_size(prof, 1), moe.expert_size(prof, 0)
+    full = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 0), moe.HardwareProfile(10**15), prof)
+    experts_bytes = sum(s4 if p == 0 else s16 for p in full.precision)
+    floor = prof.size_nonexpert_bytes + max(s4 if n4 == LAYERS * EXPERTS else s16, s4)
+    rows = []
+    for frac in args.host_split_points:
+        budget = int(floor + frac * experts_bytes)
+        hw = moe.HardwareProfile(budget, bw * 1e9)
+        try:
+            plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 0), hw, prof)
+        except moe.MoeError as exc:
+            rows.append({"resident_frac": frac, "infeasible": str(exc)})
+            continue
+        eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan, max_tokens=1, seed=args.seed, device=device,
+                            norm_eps=NORM_EPS, use_graphs=True)
+        eng.synth_input(0, 1)
+        eng.decode(1)
+        eng.sync()
+        eng.reset_counters()
+        trace = []
+        steps = args.host_split_steps
+        t0 = time.perf_counter()
+        for st in range(steps):
+            eng.synth_input(st + 1, 1)
+            eng.decode(1)
+            eng.sync()
+            trace.extend(eng.last_routing(1))
+        el = time.perf_counter() - t0
+        c = eng.counters()
+        sim = moe.simulate(plan, trace, steps, prof, hw)
+        model_tps = moe.expected_throughput(plan, moe.ModelProfile(**{**prof.__dict__, "compute_penalty4": 1.0}), hw) \
+            if hasattr(prof, "__dict__") else None
+        rows.append({"resident_frac": frac, "gpu_budget_gb": round(budget / 1e9, 2), "experts_on_gpu": plan.n_gpu,
+                     "tokens_per_s": round(steps / el, 3), "hits": c.hits, "activations": c.activations,
+                     "bytes_transferred": c.bytes_transferred,
+                     "counters_equal_simulate": (c.activations, c.hits, c.bytes_transferred) ==
+                                                (sim.activations, sim.hits, sim.bytes_transferred),
+                     "model_tps_expected_throughput": round(model_tps, 3) if model_tps else None})
+        eng.close()
+        del eng
+    return {"n4": n4, "h2d_gbs_measured": round(bw, 1), "policy": "Static (single swap slot, planner.cpp:108)",
+            "steps_per_point": args.host_split_steps, "points": rows}
 
 
 def run_ep(args, rank, world, device):
@@ -460,6 +536,11 @@ def main():
     ap.add_argument("--batch-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],
                     default=[1, 8, 32, 64, 128, 256])
     ap.add_argument("--no-prefill", dest="prefill", action="store_false")
+    ap.add_argument("--no-host-split", dest="host_split", action="store_false")
+    ap.add_argument("--host-split-n4", type=int, default=256)
+    ap.add_argument("--host-split-points", type=lambda s: [float(v) for v in s.split(",")] if s else [],
+                    default=[1.0, 0.75, 0.5, 0.25, 0.0])
+    ap.add_argument("--host-split-steps", type=int, default=4)
     ap.add_argument("--prefill-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],
                     default=[512, 2048, 4096])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
