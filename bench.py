@@ -46,6 +46,14 @@ NORM_EPS = 1e-5
 METRIC = "decode tokens/s vs #4-bit experts (Mixtral-8x7B shape); expert-FFN HBM GB/s"
 
 
+def _traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01b_traffic.json")) as fh:
+            return int(json.load(fh)["stream_pair_dram_bytes"])
+    except Exception:
+        return None
+
+
 def _peak_tflops():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -344,8 +352,12 @@ def run_ours(args, rank, world, device):
             "e2e": {"value": round(e2e, 3), "unit": "tokens/s", "h2d_bytes_per_step": T * D_MODEL * 2,
                     "d2h_bytes_per_step": T * D_MODEL * 2},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "expert FFN (ffn_gateup_kernel + ffn_down_kernel) per layer",
+                         "frac": round(achieved / hbm_peak, 4), "traffic": _traffic(), "peak_kind": peak_kind,
+                         "traffic_note": "ncu dram read+write of the stream_kernel pair of one int4/int4 "
+                                         "token-layer (profiles/r01b_traffic.json) vs its 181,665,792 "
+                                         "algorithmic weight bytes",
+                         "kernel": "expert FFN per layer: stream_kernel (gate/up) + finalize_h + "
+                                   "stream_kernel (down) + finalize_out, CUDA events on the engine stream",
                          "bytes_per_launch": round(avg_bytes), "ms_per_launch": round(avg_ms, 5),
                          "ffn_share_of_step": round(ffn_share, 4)},
             "gpu_launches": kps * (args.steps),
