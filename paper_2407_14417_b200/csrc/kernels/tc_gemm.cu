@@ -19,6 +19,7 @@
 // The storage layout stays the GEMV's (fragment blocks), so one copy of the
 // weights serves both paths.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -34,7 +35,7 @@ constexpr int kTileBytes = kM * kKc * 2;  // 16 KB (A tile; B tile is the same f
 // raw stage: [A_gate raw 16 KB][A_up raw 16 KB][scales 2 x 256 B][B raw 16 KB]
 constexpr int kRawA = 16384;
 constexpr int kRawS = 256;
-constexpr int kRawBytes = 2 * kRawA + 2 * kRawS + kN * kKc * 2;
+constexpr int kRawBytes = 2 * kRawA + 2 * kRawS;  // weights only: token rows go straight to the canonical tile
 // canonical stage: [A_gate 16 KB][A_up 16 KB][B 16 KB], 1024-aligned
 constexpr int kCanBytes = 3 * kTileBytes;
 constexpr int kSmemBytes = 1024 + 2 * kRawBytes + 2 * kCanBytes;
@@ -51,6 +52,7 @@ struct TcArgs {
     uint16_t* hout16;         // pass 0: h [T*k][f] fp16
     float* y;                 // pass 1: y [T*k][d]
     uint64_t active_mask;
+    int dbg;                  // debug: bit0 skip convert, bit1 skip MMA, bit2 skip weight loads
     moe_expert_weights ex[MOE_MAX_EXPERTS];
 };
 
@@ -126,7 +128,9 @@ MOE_DEVI bool find_tile(const TcArgs& a, int RT, int b, Tile& tl) {
         if (m == 0) continue;
         const int nt = (m + kN - 1) / kN;
         if (b < nt * RT) {
-            const int tt = b / RT, rt = b - tt * RT;
+            // token tile fastest: the CTAs resident together share each weight
+            // row tile through L2 (one HBM read serves every token tile)
+            const int rt = b / nt, tt = b - rt * nt;
             tl.e = e;
             tl.slot0 = o0 + tt * kN;
             tl.m = min(kN, m - tt * kN);
@@ -138,127 +142,172 @@ MOE_DEVI bool find_tile(const TcArgs& a, int RT, int b, Tile& tl) {
     return false;
 }
 
-// Issue the cp.async copies of chunk kc into a raw stage.
-MOE_DEVI void load_raw(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, uint8_t* raw, const int* brow,
-                       int tid) {
+MOE_DEVI void mbar_init_n(uint64_t* bar, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(bar)), "r"(n) : "memory");
+}
+MOE_DEVI void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(bar)) : "memory");
+}
+MOE_DEVI void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(bar)), "r"(bytes) : "memory");
+}
+MOE_DEVI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(s32(dst)),
+        "l"(src), "r"(bytes), "r"(s32(bar))
+        : "memory");
+}
+
+// Warp roles (12 warps): 0 = TMA producer of raw weight blocks, 1 = MMA
+// issuer (one lane), 2 = token-row producer (cp.async straight into the
+// canonical tile), 4..11 = converters (raw -> canonical) and the epilogue.  kRaw raw stages and kCan canonical stages, all handed over by
+// mbarriers, so the producer runs up to kRaw chunks ahead of the converters
+// and the converters one canonical stage ahead of the tensor core.
+constexpr int kThreads2 = 384;
+constexpr int kConvThreads = 256;
+constexpr int kRaw = 2, kCan = 2, kBst = 4;
+constexpr int kCanA = 2 * kTileBytes;   // canonical A stage (gate + up)
+constexpr int kSmem2 = 1024 + kRaw * kRawBytes + kCan * kCanA + kBst * kTileBytes;
+
+// Raw stage layout: [A_gate raw 16 KB][A_up raw 16 KB][scales 2 x 256 B][B raw 16 KB].
+// bf16: 8 block halves of 2 KB per matrix (parts 4hh..4hh+3 of each block).
+// int4: the whole 1 KB block per row tile (both K halves; the convert step
+//       picks words 2hh, 2hh+1), 8 KB per matrix, + 8 x 32 B scales.
+MOE_DEVI uint32_t raw_bytes(bool p4, int nmat) { return nmat * (p4 ? 8 * 1024 + 256 : 16384); }
+
+MOE_DEVI void produce(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, uint8_t* raw, const int* brow,
+                      uint64_t* bar, int lane) {
     const moe_expert_weights& W = a.ex[tl.e];
     const int G = K / 128, g = kc >> 1, hh = kc & 1;
     const bool p4 = W.precision == MOE_P4;
+    if (lane == 0) mbar_expect_tx(bar, raw_bytes(p4, nmat));
+    __syncwarp();
     for (int mat = 0; mat < nmat; ++mat) {
-        // pass 0: mat 0 = gate rows R0.., mat 1 = up rows f+R0..; pass 1: down rows R0..
         const int row0 = (a.p == 0 && mat == 1) ? a.f + tl.R0 : tl.R0;
         const uint8_t* wb = static_cast<const uint8_t*>(a.p == 0 ? W.w_gate_up : W.w_down);
         uint8_t* dst = raw + mat * kRawA;
-        if (!p4) {
-            // 8 blocks x 2 KB (parts 4hh..4hh+3) = 1024 x 16 B
-            for (int pc = tid; pc < 1024; pc += kThreads) {
-                const int i = pc >> 7, rem = pc & 127;
-                const size_t blk = static_cast<size_t>(row0 / 16 + i) * G + g;
-                cp_async16(dst + pc * 16, wb + blk * 4096 + hh * 2048 + rem * 16, 16);
-            }
-        } else {
-            // 8 blocks x 64 (half, lane) x 8 B (words 2hh, 2hh+1)
-            for (int it = tid; it < 512; it += kThreads) {
-                const int i = it >> 6, hl = it & 63;
-                const size_t blk = static_cast<size_t>(row0 / 16 + i) * G + g;
-                cp_async8(dst + it * 8, wb + blk * 1024 + (hl * 4 + 2 * hh) * 4);
-            }
-            const uint8_t* sb = static_cast<const uint8_t*>(a.p == 0 ? W.s_gate_up : W.s_down);
-            if (tid < 16) {
-                const int i = tid >> 1, half16 = tid & 1;
-                const size_t blk = static_cast<size_t>(row0 / 16 + i) * G + g;
-                cp_async16(raw + 2 * kRawA + mat * kRawS + i * 32 + half16 * 16, sb + blk * 32 + half16 * 16, 16);
+        if (lane < 8) {
+            const size_t blk = static_cast<size_t>(row0 / 16 + lane) * G + g;
+            if (!p4) {
+                bulk_g2s(dst + lane * 2048, wb + blk * 4096 + hh * 2048, 2048, bar);
+            } else {
+                const uint8_t* sb = static_cast<const uint8_t*>(a.p == 0 ? W.s_gate_up : W.s_down);
+                bulk_g2s(dst + lane * 1024, wb + blk * 1024, 1024, bar);
+                bulk_g2s(raw + 2 * kRawA + mat * kRawS + lane * 32, sb + blk * 32, 32, bar);
             }
         }
     }
-    // token rows: 128 B each (natural order), zero-filled past the tile's tokens
+}
+
+// Token rows of chunk kc (natural order, 128 B per row) straight into their
+// swizzled positions of the canonical B tile with 16-byte cp.async by the 32
+// producer lanes, each lane's completion arriving on can_full (noinc).  Rows
+// past the tile's tokens repeat the last token (their D columns are never
+// stored).
+MOE_DEVI void produce_b(const TcArgs& a, bool p4, int K, int kc, uint8_t* bdst, const int* brow, uint64_t* bar,
+                        int lane) {
     const uint16_t* bsrc = p4 ? a.bnat16 : a.bnat;
-    uint8_t* bdst = raw + 2 * kRawA + 2 * kRawS;
-    for (int pc = tid; pc < kN * 8; pc += kThreads) {
+    for (int pc = lane; pc < kN * 8; pc += 32) {
         const int n = pc >> 3, c = pc & 7;
-        const bool ok = n < tl.m;
-        const uint16_t* src = bsrc + static_cast<size_t>(ok ? brow[n] : brow[0]) * K + kc * kKc + c * 8;
-        cp_async16(bdst + pc * 16, src, ok ? 16 : 0);
+        cp_async16(bdst + swz(n, c * 16), bsrc + static_cast<size_t>(brow[n]) * K + kc * kKc + c * 8, 16);
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(s32(bar)) : "memory");
+}
+
+// per-converter-thread swizzled destinations (identical for every chunk)
+struct ConvOffsets {
+    int a[4][4];   // bf16: piece j -> 4 word destinations
+    int q[2][8];   // int4: item j -> 8 word destinations
+    int qrow[2];   // int4: item j -> (raw word offset, scale offset) packed
+    int qsc[2];
+};
+
+MOE_DEVI void conv_offsets(int ct, int hh, ConvOffsets& o) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int pc = ct + j * kConvThreads;
+        const int i = pc >> 7, kq = (pc >> 5) & 3, L = pc & 31;
+        const int rlo = i * 16 + (L >> 2), rhi = rlo + 8;
+        const int kb = (kq * 16 + 2 * (L & 3)) * 2;
+        o.a[j][0] = swz(rlo, kb);
+        o.a[j][1] = swz(rhi, kb);
+        o.a[j][2] = swz(rlo, kb + 16);
+        o.a[j][3] = swz(rhi, kb + 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int it = ct + j * kConvThreads;
+        const int i = it >> 6, hl = it & 63, half = hl >> 5, L = hl & 31;
+        const int row = i * 16 + half * 8 + (L >> 2);
+        o.qrow[j] = i * 1024 + (hl * 4 + 2 * hh) * 4;
+        o.qsc[j] = i * 32 + (L >> 2) * 4 + half * 2;
+#pragma unroll
+        for (int qi = 0; qi < 2; ++qi) {
+            const int kb0 = ((2 * qi) * 16 + 2 * (L & 3)) * 2;
+            const int kb1 = ((2 * qi + 1) * 16 + 2 * (L & 3)) * 2;
+            o.q[j][qi * 4 + 0] = swz(row, kb0);
+            o.q[j][qi * 4 + 1] = swz(row, kb0 + 16);
+            o.q[j][qi * 4 + 2] = swz(row, kb1);
+            o.q[j][qi * 4 + 3] = swz(row, kb1 + 16);
+        }
     }
 }
 
-// raw stage -> canonical swizzled tiles
-MOE_DEVI void convert(const TcArgs& a, const Tile& tl, int nmat, const uint8_t* raw, uint8_t* can, int tid) {
-    const bool p4 = a.ex[tl.e].precision == MOE_P4;
+MOE_DEVI void convert2(bool p4, int nmat, const uint8_t* raw, uint8_t* can, int ct, const ConvOffsets& o) {
     for (int mat = 0; mat < nmat; ++mat) {
         const uint8_t* src = raw + mat * kRawA;
         uint8_t* dst = can + mat * kTileBytes;
         if (!p4) {
-            for (int pc = tid; pc < 1024; pc += kThreads) {
-                const int i = pc >> 7, kq = (pc >> 5) & 3, L = pc & 31;
-                const uint4 v = *reinterpret_cast<const uint4*>(src + pc * 16);
-                const int rlo = i * 16 + (L >> 2), rhi = rlo + 8;
-                const int kb = (kq * 16 + 2 * (L & 3)) * 2;  // byte of k within the 128-byte row
-                *reinterpret_cast<uint32_t*>(dst + swz(rlo, kb)) = v.x;
-                *reinterpret_cast<uint32_t*>(dst + swz(rhi, kb)) = v.y;
-                *reinterpret_cast<uint32_t*>(dst + swz(rlo, kb + 16)) = v.z;
-                *reinterpret_cast<uint32_t*>(dst + swz(rhi, kb + 16)) = v.w;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint4 v = *reinterpret_cast<const uint4*>(src + (ct + j * kConvThreads) * 16);
+                *reinterpret_cast<uint32_t*>(dst + o.a[j][0]) = v.x;
+                *reinterpret_cast<uint32_t*>(dst + o.a[j][1]) = v.y;
+                *reinterpret_cast<uint32_t*>(dst + o.a[j][2]) = v.z;
+                *reinterpret_cast<uint32_t*>(dst + o.a[j][3]) = v.w;
             }
         } else {
             const uint8_t* sc = raw + 2 * kRawA + mat * kRawS;
-            const uint32_t m1032 = 0xE408E408u;  // fp16 (-1032, -1032)
-            const uint32_t m72 = 0xD480D480u;    // fp16 (-72, -72)
-            const uint32_t r16 = 0x2C002C00u;    // fp16 (1/16, 1/16)
-            for (int it = tid; it < 512; it += kThreads) {
-                const int i = it >> 6, hl = it & 63, half = hl >> 5, L = hl & 31;
-                const uint2 w2 = *reinterpret_cast<const uint2*>(src + it * 8);
-                const int row = i * 16 + half * 8 + (L >> 2);
-                const uint16_t sb = *reinterpret_cast<const uint16_t*>(sc + i * 32 + (L >> 2) * 4 + half * 2);
+            const __half2 m1032 = __halves2half2(__ushort_as_half(0xE408), __ushort_as_half(0xE408));
+            const __half2 m72 = __halves2half2(__ushort_as_half(0xD480), __ushort_as_half(0xD480));
+            const __half2 r16 = __halves2half2(__ushort_as_half(0x2C00), __ushort_as_half(0x2C00));
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint2 w2 = *reinterpret_cast<const uint2*>(src + o.qrow[j]);
+                const uint16_t sb = *reinterpret_cast<const uint16_t*>(sc + o.qsc[j]);
                 const __half sh = __float2half_rn(bf2f(sb));  // exact for normal-range scales
                 const __half2 s2 = __halves2half2(sh, sh);
 #pragma unroll
                 for (int qi = 0; qi < 2; ++qi) {
                     const uint32_t w = qi ? w2.y : w2.x;
-                    const uint32_t lo0 = and_or(w, 0x000F000Fu, 0x64006400u);
-                    const uint32_t hi0 = and_or(w, 0x00F000F0u, 0x64006400u);
-                    const uint32_t lo1 = and_or(w >> 8, 0x000F000Fu, 0x64006400u);
-                    const uint32_t hi1 = and_or(w >> 8, 0x00F000F0u, 0x64006400u);
-                    // q exactly, then q*s exactly in fp16
-                    auto deq_lo = [&](uint32_t v) {
-                        __half2 q = __hadd2(*reinterpret_cast<const __half2*>(&v), *reinterpret_cast<const __half2*>(&m1032));
-                        q = __hmul2(q, s2);
-                        return *reinterpret_cast<uint32_t*>(&q);
-                    };
-                    auto deq_hi = [&](uint32_t v) {
-                        __half2 q = __hfma2(*reinterpret_cast<const __half2*>(&v), *reinterpret_cast<const __half2*>(&r16),
-                                            *reinterpret_cast<const __half2*>(&m72));
-                        q = __hmul2(q, s2);
-                        return *reinterpret_cast<uint32_t*>(&q);
-                    };
-                    // word qi covers kk = 2*(2hh+qi) + {0,1}; local kk' = 2qi + {0,1}
-                    const int kb0 = ((2 * qi) * 16 + 2 * (L & 3)) * 2;
-                    const int kb1 = ((2 * qi + 1) * 16 + 2 * (L & 3)) * 2;
-                    *reinterpret_cast<uint32_t*>(dst + swz(row, kb0)) = deq_lo(lo0);
-                    *reinterpret_cast<uint32_t*>(dst + swz(row, kb0 + 16)) = deq_hi(hi0);
-                    *reinterpret_cast<uint32_t*>(dst + swz(row, kb1)) = deq_lo(lo1);
-                    *reinterpret_cast<uint32_t*>(dst + swz(row, kb1 + 16)) = deq_hi(hi1);
+                    uint32_t v[4] = {and_or(w, 0x000F000Fu, 0x64006400u), and_or(w, 0x00F000F0u, 0x64006400u),
+                                     and_or(w >> 8, 0x000F000Fu, 0x64006400u), and_or(w >> 8, 0x00F000F0u, 0x64006400u)};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        __half2 h = *reinterpret_cast<__half2*>(&v[u]);
+                        h = (u & 1) ? __hfma2(h, r16, m72) : __hadd2(h, m1032);  // q exactly
+                        h = __hmul2(h, s2);                                      // q*s exactly
+                        *reinterpret_cast<__half2*>(dst + o.q[j][qi * 4 + u]) = h;
+                    }
                 }
             }
         }
     }
-    // token rows: 16-byte chunks to their swizzled positions
-    const uint8_t* bs = raw + 2 * kRawA + 2 * kRawS;
-    uint8_t* bd = can + 2 * kTileBytes;
-    for (int pc = tid; pc < kN * 8; pc += kThreads) {
-        const int n = pc >> 3, c = pc & 7;
-        *reinterpret_cast<uint4*>(bd + swz(n, c * 16)) = *reinterpret_cast<const uint4*>(bs + pc * 16);
-    }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) tc_ffn_kernel(const __grid_constant__ TcArgs a) {
+__global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_constant__ TcArgs a) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    auto can = [&](int s) { return smem + s * kCanBytes; };
-    auto raw = [&](int s) { return smem + 2 * kCanBytes + s * kRawBytes; };
-    __shared__ __align__(8) uint64_t bar[2];
+    // 1024-byte aligned base by pointer arithmetic (keeps the shared address
+    // space, so the converters use LDS/STS, not generic loads/stores)
+    uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
+    __shared__ __align__(8) uint64_t raw_full[kRaw], raw_empty[kRaw], can_full[kCan], can_empty[kCan], b_full[kBst],
+        b_empty[kBst], acc_full;
     __shared__ uint32_t tmem_slot;
     __shared__ int brow[kN];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    auto can = [&](int s) { return smem + s * kCanA; };
+    auto bst = [&](int s) { return smem + kCan * kCanA + s * kTileBytes; };
+    auto raw = [&](int s) { return smem + kCan * kCanA + kBst * kTileBytes + s * kRawBytes; };
 
     pdl_wait();
     pdl_trigger();
@@ -267,17 +316,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_ffn_kernel(const __grid_consta
     Tile tl;
     if (!find_tile(a, RT, blockIdx.x, tl)) return;
     const int nmat = a.p == 0 ? 2 : 1;
+    const bool p4 = a.ex[tl.e].precision == MOE_P4;
     if (tid < kN) {
         const int n = min(tid, tl.m - 1);
         const int slot = tl.slot0 + n;
         brow[tid] = a.p == 0 ? (a.kshift >= 0 ? a.perm[slot] >> a.kshift : a.perm[slot] / a.k) : slot;
     }
     if (tid == 0) {
-        mbar_init(&bar[0]);
-        mbar_init(&bar[1]);
+        for (int s = 0; s < kRaw; ++s) {
+            mbar_init_n(&raw_full[s], 1);  // producer expect_tx
+            mbar_init_n(&raw_empty[s], kConvThreads / 32);
+        }
+        for (int s = 0; s < kCan; ++s) {
+            mbar_init_n(&can_full[s], kConvThreads / 32);  // converter warps
+            mbar_init_n(&can_empty[s], 1);
+        }
+        for (int s = 0; s < kBst; ++s) {
+            mbar_init_n(&b_full[s], 32);  // token-row cp.async lanes (noinc)
+            mbar_init_n(&b_empty[s], 1);
+        }
+        mbar_init_n(&acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) {
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tmem_slot)),
                      "r"(256)
                      : "memory");
@@ -287,80 +348,104 @@ __global__ void __launch_bounds__(kThreads, 1) tc_ffn_kernel(const __grid_consta
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_slot;
-    const int fmt = a.ex[tl.e].precision == MOE_P4 ? 0 : 1;
-    const uint32_t id = idesc(fmt, kN, kM);
     const int nk = K / kKc;
 
-    load_raw(a, tl, nmat, K, 0, raw(0), brow, tid);
-    cp_commit();
-    uint32_t phase = 0;  // per-stage commit parity bits
-    for (int kc = 0; kc < nk; ++kc) {
-        const int s = kc & 1;
-        if (kc + 1 < nk) load_raw(a, tl, nmat, K, kc + 1, raw(s ^ 1), brow, tid);
-        cp_commit();
-        cp_wait<1>();  // chunk kc landed
-        __syncthreads();
-        if (kc >= 2) {  // the MMAs of chunk kc-2 have read canonical stage s
-            mbar_wait(&bar[s], (phase >> s) & 1u);
-            phase ^= 1u << s;
+    if (warp == 0) {
+        // ---- weight producer: kRaw chunks ahead of the converters ----
+        for (int kc = 0; kc < nk; ++kc) {
+            const int r = kc % kRaw, pass = kc / kRaw;
+            if (pass > 0) mbar_wait(&raw_empty[r], (pass - 1) & 1);
+            if (a.dbg & 4) {
+                if (lane == 0) mbar_arrive(&raw_full[r]);
+                __syncwarp();
+            } else {
+                produce(a, tl, nmat, K, kc, raw(r), brow, &raw_full[r], lane);
+            }
         }
-        convert(a, tl, nmat, raw(s), can(s), tid);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (tid == 0) {
+    } else if (warp == 2) {
+        // ---- token-row producer: kBst chunks ahead, into the B ring ----
+        for (int kb = 0; kb < nk; ++kb) {
+            const int b = kb % kBst;
+            if (kb >= kBst) mbar_wait(&b_empty[b], ((kb / kBst) - 1) & 1);
+            produce_b(a, p4, K, kb, bst(b), brow, &b_full[b], lane);
+        }
+    } else if (warp == 1) {
+        // ---- MMA issuer ----
+        const uint32_t id = idesc(p4 ? 0 : 1, kN, kM);
+        for (int kc = 0; kc < nk; ++kc) {
+            const int c = kc % kCan, b = kc % kBst;
+            mbar_wait(&can_full[c], (kc / kCan) & 1);
+            mbar_wait(&b_full[b], (kc / kBst) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t cb = s32(can(s));
+            if (lane == 0) {
+                const uint32_t cb = s32(can(c)), bb = s32(bst(b));
 #pragma unroll
-            for (int j = 0; j < kKc / 16; ++j) {
-                const uint64_t bdesc = sdesc(cb + 2 * kTileBytes + j * 32);
-                const uint32_t acc = (kc > 0 || j > 0) ? 1u : 0u;
-                umma(tmem, sdesc(cb + j * 32), bdesc, id, acc);
-                if (nmat == 2) umma(tmem + kN, sdesc(cb + kTileBytes + j * 32), bdesc, id, acc);
-            }
-            umma_commit(&bar[s]);
-        }
-    }
-    // drain: the last commits of both stages
-    for (int kc = max(0, nk - 2); kc < nk; ++kc) {
-        const int s = kc & 1;
-        mbar_wait(&bar[s], (phase >> s) & 1u);
-        phase ^= 1u << s;
-    }
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-    // epilogue: warp w reads TMEM lanes 32*(w%4).. (weight rows) and token
-    // columns [64*(w/4), 64*(w/4)+64)
-    const int row = (warp & 3) * 32 + lane;
-    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    for (int cb = (warp >> 2) * 64; cb < (warp >> 2) * 64 + 64; cb += 32) {
-        uint32_t g[32];
-        TMEM_LD32(tmem + lane_base + cb, g);
-        if (a.p == 0) {
-            uint32_t u[32];
-            TMEM_LD32(tmem + lane_base + kN + cb, u);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const int n = cb + c;
-                if (n < tl.m) {
-                    const uint16_t hb = f2bf(silu_f(__uint_as_float(g[c])) * __uint_as_float(u[c]));
-                    const size_t o = static_cast<size_t>(tl.slot0 + n) * a.f + tl.R0 + row;
-                    a.hout[o] = hb;
-                    a.hout16[o] = __half_as_ushort(__float2half_rn(bf2f(hb)));
+                for (int j = 0; j < kKc / 16; ++j) {
+                    if (a.dbg & 2) break;
+                    const uint64_t bdesc = sdesc(bb + j * 32);
+                    const uint32_t acc = (kc > 0 || j > 0) ? 1u : 0u;
+                    umma(tmem, sdesc(cb + j * 32), bdesc, id, acc);
+                    if (nmat == 2) umma(tmem + kN, sdesc(cb + kTileBytes + j * 32), bdesc, id, acc);
                 }
+                umma_commit(&can_empty[c]);
+                umma_commit(&b_empty[b]);
+                if (kc == nk - 1) umma_commit(&acc_full);
             }
-        } else {
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // ---- converters, then the epilogue ----
+        const int ct = tid - 128;
+        ConvOffsets o0, o1;  // K halves hh = 0 / 1 (int4 word selection differs)
+        conv_offsets(ct, 0, o0);
+        conv_offsets(ct, 1, o1);
+        for (int kc = 0; kc < nk; ++kc) {
+            const int r = kc % kRaw, c = kc % kCan;
+            mbar_wait(&raw_full[r], (kc / kRaw) & 1);
+            if (kc >= kCan) mbar_wait(&can_empty[c], ((kc / kCan) - 1) & 1);
+            if (!(a.dbg & 1)) convert2(p4, nmat, raw(r), can(c), ct, (kc & 1) ? o1 : o0);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&can_full[c]);
+                mbar_arrive(&raw_empty[r]);
+            }
+        }
+        mbar_wait(&acc_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int row = (warp & 3) * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const int c0 = ((warp - 4) >> 2) * 64;
+        for (int cb = c0; cb < c0 + 64; cb += 32) {
+            uint32_t g[32];
+            TMEM_LD32(tmem + lane_base + cb, g);
+            if (a.p == 0) {
+                uint32_t u[32];
+                TMEM_LD32(tmem + lane_base + kN + cb, u);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const int n = cb + c;
-                if (n < tl.m) a.y[static_cast<size_t>(tl.slot0 + n) * a.d + tl.R0 + row] = __uint_as_float(g[c]);
+                for (int c = 0; c < 32; ++c) {
+                    const int n = cb + c;
+                    if (n < tl.m) {
+                        const uint16_t hb = f2bf(silu_f(__uint_as_float(g[c])) * __uint_as_float(u[c]));
+                        const size_t o = static_cast<size_t>(tl.slot0 + n) * a.f + tl.R0 + row;
+                        a.hout[o] = hb;
+                        a.hout16[o] = __half_as_ushort(__float2half_rn(bf2f(hb)));
+                    }
+                }
+            } else {
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const int n = cb + c;
+                    if (n < tl.m) a.y[static_cast<size_t>(tl.slot0 + n) * a.d + tl.R0 + row] = __uint_as_float(g[c]);
+                }
             }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0)
+    if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
 }
 
@@ -390,7 +475,7 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     if (d % kM != 0 || f % kM != 0 || d % 128 != 0 || f % 128 != 0) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
-        MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+        MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2));
         attr = true;
     }
     const size_t slots = static_cast<size_t>(T) * k;
@@ -410,6 +495,8 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     a.d = d;
     a.f = f;
     a.active_mask = active_mask;
+    static const int dbg = getenv("MOE_TC_DBG") ? atoi(getenv("MOE_TC_DBG")) : 0;
+    a.dbg = dbg;
     for (int e = 0; e < E; ++e) a.ex[e] = experts[e];
     const int ntiles_max = static_cast<int>((slots + kN - 1) / kN) + E;
     // pass 0: gate/up + SwiGLU -> h
@@ -418,13 +505,13 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     a.bnat16 = x16;
     a.hout = h;
     a.hout16 = h16;
-    MOE_CUDA_OK(moek::launch_pdl(tc_ffn_kernel, dim3(static_cast<unsigned>(ntiles_max * (f / kM))), dim3(kThreads),
-                                 kSmemBytes, stream, a));
+    MOE_CUDA_OK(moek::launch_pdl(tc_ffn_kernel, dim3(static_cast<unsigned>(ntiles_max * (f / kM))), dim3(kThreads2),
+                                 kSmem2, stream, a));
     // pass 1: down -> y
     a.p = 1;
     a.bnat = h;
     a.bnat16 = h16;
     a.y = y;
-    return moek::launch_pdl(tc_ffn_kernel, dim3(static_cast<unsigned>(ntiles_max * (d / kM))), dim3(kThreads),
-                            kSmemBytes, stream, a);
+    return moek::launch_pdl(tc_ffn_kernel, dim3(static_cast<unsigned>(ntiles_max * (d / kM))), dim3(kThreads2),
+                            kSmem2, stream, a);
 }
