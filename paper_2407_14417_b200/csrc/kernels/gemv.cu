@@ -33,6 +33,8 @@
 // against an fp16 copy of the activations (exact for 2^-17 <= |x| <= 65504);
 // the per-128-K-group scale is applied after the group's integer-exact dot,
 // y += s * sum(q*x) -- the exact dequant values q*s.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -47,10 +49,12 @@ constexpr int kBRowPad = 64;             // activation row stride in a stage = G
 // <= W/32][activation rows <= B][bias terms 8 x 32 B].
 //   Batch : 8 warps, 8 KB weight items; activation area for up to 8 token
 //           rows (GK shrinks with the rows: m * (GK*256+64) <= B).
-//   Decode: 16 warps (4 per SM sub-partition, to hide the int4 decode /
-//           HMMA dependency chains), 4 KB weight items, one token row.
-template <int WARPS, int W, int B>
+//   Decode: 8 warps, 8 KB weight items; T == 1 (one token row per segment,
+//           <= 2 segments, rows of K <= 14336): the rows are resident per CTA.
+template <int WARPS, int W, int B, bool RES = false>
 struct StreamCfg {
+    static constexpr bool kRes = RES;     // activations resident per CTA (T == 1), not per item
+    static constexpr int kResBytes = RES ? 2 * (14336 * 2 + 512 * 4) : 0;  // 2 segments x (row of K <= 14336 + bias)
     static constexpr int kWarps = WARPS;
     static constexpr int kThreads = WARPS * 32;
     static constexpr int kW = W;
@@ -65,7 +69,9 @@ struct StreamCfg {
     static constexpr int kGk16 = W / 4096;  // max 128-K groups per bf16 item
 };
 using CfgBatch = StreamCfg<8, 8192, 4608>;
-using CfgDecode = StreamCfg<16, 4096, 1088>;
+// batch-1 decode: each segment's single activation row (and its int4 bias
+// terms) is loaded once per launch into shared memory; items carry only weights
+using CfgDecode = StreamCfg<8, 8192, 0, true>;
 constexpr int kChunk = 2;                // items per dynamic tail chunk
 constexpr int kMaxSlots = 512;           // permutation slots staged in smem by build_segs
 
@@ -84,6 +90,7 @@ struct StreamArgs {
     int* kpslot;              // [T*k]: K-parts written for the slot (0: expert not in this launch)
     unsigned int* sched;      // tail-pool counter (reset by the finalize kernel)
     int wait_first;           // 1: the predecessor produced the routing -> PDL wait before reading it
+    int dbg;                  // experiments (MOE_GEMV_DBG): bit0 skip activation copies, bit1 skip scale copies
     uint64_t active_mask;
     moe_expert_weights ex[MOE_MAX_EXPERTS];
 };
@@ -262,7 +269,7 @@ MOE_DEVI int perm_k16(int n) {
 template <class C>
 MOE_DEVI int pick_gk(int G, int prec, int m) {
     int cap = prec == MOE_P4 ? C::kGk4 : C::kGk16;
-    while (cap > 1 && m * (cap * 256 + kBRowPad) > C::kBBytes) cap >>= 1;
+    while (!C::kRes && cap > 1 && m * (cap * 256 + kBRowPad) > C::kBBytes) cap >>= 1;  // resident rows: no cap
     while (cap > 1 && G % cap) cap >>= 1;
     return cap;
 }
@@ -351,10 +358,12 @@ template <class C>
 MOE_DEVI void issue_weights(const StreamArgs& a, const SegTable& st, const Item& it, uint8_t* stage, uint64_t* bar,
                             uint64_t pol) {
     const int s = it.s, wb = st.wbytes[s], sb = st.sbytes[s], m = st.mcnt[s];
-    mbar_expect_tx(bar, wb + sb + m * st.gk[s] * 256 + (sb ? m * 32 : 0));
+    const int acts = (C::kRes || (a.dbg & 1)) ? 0 : m * st.gk[s] * 256 + (sb ? m * 32 : 0);
+    const int scl = (a.dbg & 2) ? 0 : sb;
+    mbar_expect_tx(bar, wb + scl + acts);
     const size_t blk = static_cast<size_t>(it.rt) * (a.K / 128) + static_cast<size_t>(it.kp) * st.gk[s];
     bulk_g2s_hint(stage + C::kStageW, st.wptr[s] + blk * (sb ? 1024 : 4096), wb, bar, pol);
-    if (sb) bulk_g2s_hint(stage + C::kStageS, st.sptr[s] + blk * 32, sb, bar, pol);
+    if (scl) bulk_g2s_hint(stage + C::kStageS, st.sptr[s] + blk * 32, sb, bar, pol);
 }
 
 // Issue the activation half: the item's K slice of every token row of the
@@ -362,6 +371,7 @@ MOE_DEVI void issue_weights(const StreamArgs& a, const SegTable& st, const Item&
 // bias-term chunk holding the item's groups.
 template <class C>
 MOE_DEVI void issue_acts(const StreamArgs& a, const SegTable& st, const Item& it, uint8_t* stage, uint64_t* bar) {
+    if (C::kRes || (a.dbg & 1)) return;
     const int s = it.s, m = st.mcnt[s], gk = st.gk[s];
     const int rowb = gk * 256;
     const size_t k0 = static_cast<size_t>(it.kp) * gk * 128;
@@ -432,29 +442,26 @@ struct Sched {
     }
 };
 
+// bp: this lane's activation chunks of the item's first group (groups at
+// stride 256 B); x0 / x1: the int4 bias terms of columns 2t / 2t+1 for the
+// item's first group.
 template <class C>
-MOE_DEVI void compute_item(const SegTable& st, const Item& it, const uint8_t* sp, int lane, float (&acc)[4]) {
-    const int gr = lane >> 2, t = lane & 3;
-    const int gk = st.gk[it.s], m_cnt = st.mcnt[it.s];
-    const int brl = min(gr, m_cnt - 1);
-    const int boff = C::kStageB + brl * (gk * 256 + kBRowPad) + t * 16;
+MOE_DEVI void compute_item(const SegTable& st, const Item& it, const uint8_t* sp, const uint8_t* bp, const float* x0,
+                           const float* x1, int lane, float (&acc)[4]) {
+    const int gk = st.gk[it.s];
     if (st.sbytes[it.s]) {
-        const int c0 = min(2 * t, m_cnt - 1), c1i = min(2 * t + 1, m_cnt - 1);
-        const int g0 = (it.kp * gk) & 7;
-        const float* x0 = reinterpret_cast<const float*>(sp + C::kStageX + c0 * 32) + g0;
-        const float* x1 = reinterpret_cast<const float*>(sp + C::kStageX + c1i * 32) + g0;
         if (C::kGk4 >= 8 && gk == 8) {
 #pragma unroll
             for (int g = 0; g < 8; ++g)
-                group_int4(sp + C::kStageW + g * 1024, sp + C::kStageS + g * 32, sp + boff + g * 256, x0[g], x1[g], lane, acc);
+                group_int4(sp + C::kStageW + g * 1024, sp + C::kStageS + g * 32, bp + g * 256, x0[g], x1[g], lane, acc);
         } else {
             for (int g = 0; g < gk; ++g)
-                group_int4(sp + C::kStageW + g * 1024, sp + C::kStageS + g * 32, sp + boff + g * 256, x0[g], x1[g], lane, acc);
+                group_int4(sp + C::kStageW + g * 1024, sp + C::kStageS + g * 32, bp + g * 256, x0[g], x1[g], lane, acc);
         }
     } else {
         float c1[4] = {0.f, 0.f, 0.f, 0.f};
-        group_bf16(sp + C::kStageW, sp + boff, lane, acc, c1);
-        if (C::kGk16 >= 2 && gk == 2) group_bf16(sp + C::kStageW + 4096, sp + boff + 256, lane, acc, c1);
+        group_bf16(sp + C::kStageW, bp, lane, acc, c1);
+        if (C::kGk16 >= 2 && gk == 2) group_bf16(sp + C::kStageW + 4096, bp + 256, lane, acc, c1);
 #pragma unroll
         for (int r = 0; r < 4; ++r) acc[r] += c1[r];
     }
@@ -470,9 +477,11 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
     __shared__ __align__(8) uint64_t bars[kWarps][kStages];
     __shared__ int cnt[2 * MOE_MAX_EXPERTS];
     __shared__ int sperm[kMaxSlots];
+    __shared__ __align__(8) uint64_t res_bar;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&bars[warp][s], 1);
+        if (C::kRes && warp == 0) mbar_init(&res_bar, 1);
         fence_mbar_init();
     }
     const unsigned long long t_entry = gtimer();
@@ -519,6 +528,24 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
     if (!a.wait_first) pdl_wait();  // activations of the predecessor
     pdl_trigger();
     ltrace(2 + 2 * a.p, 1);
+    // resident activations (T == 1): segment s's row at res + s*K*2, its bias
+    // terms at resx + s*bstride
+    uint8_t* res = smem + static_cast<size_t>(kWarps) * kStages * kStageBytes;
+    float* resx = reinterpret_cast<float*>(res + 2 * a.K * 2);
+    if (C::kRes) {
+        if (threadIdx.x == 0) {
+            uint32_t bytes = 0;
+            for (int s = 0; s < st.n; ++s) bytes += a.K * 2 + (st.sbytes[s] ? a.bstride * 4 : 0);
+            mbar_expect_tx(&res_bar, bytes);
+            for (int s = 0; s < st.n; ++s) {
+                const int br = st.brow[s][0];
+                const bool p4 = st.sbytes[s] != 0;
+                bulk_g2s(res + s * a.K * 2, (p4 ? a.b16h : a.b16) + static_cast<size_t>(br) * a.K, a.K * 2, &res_bar);
+                if (p4) bulk_g2s(resx + s * a.bstride, a.bsum + static_cast<size_t>(br) * a.bstride, a.bstride * 4, &res_bar);
+            }
+        }
+        mbar_wait(&res_bar, 0);
+    }
     if (lane == 0) {
         if (npro > 0) issue_acts<C>(a, st, it0, ring, &bars[warp][0]);
         if (npro > 1) issue_acts<C>(a, st, it1, ring + kStageBytes, &bars[warp][1]);
@@ -534,7 +561,22 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
         phase_bits ^= 1u << stage;
         uint8_t* sp = ring + stage * kStageBytes;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        compute_item<C>(st, it, sp, lane, acc);
+        {
+            const int gk = st.gk[it.s];
+            const uint8_t* bp;
+            const float *x0, *x1;
+            if (C::kRes) {
+                bp = res + it.s * a.K * 2 + it.kp * gk * 256 + t * 16;
+                x0 = x1 = resx + it.s * a.bstride + it.kp * gk;
+            } else {
+                const int m_cnt = st.mcnt[it.s];
+                bp = sp + C::kStageB + min(gr, m_cnt - 1) * (gk * 256 + kBRowPad) + t * 16;
+                const int g0 = (it.kp * gk) & 7;
+                x0 = reinterpret_cast<const float*>(sp + C::kStageX + min(2 * t, m_cnt - 1) * 32) + g0;
+                x1 = reinterpret_cast<const float*>(sp + C::kStageX + min(2 * t + 1, m_cnt - 1) * 32) + g0;
+            }
+            compute_item<C>(st, it, sp, bp, x0, x1, lane, acc);
+        }
         ++computed;
         // release the stage and refill it with the next item of the sequence
         fence_proxy_async();
@@ -777,7 +819,7 @@ namespace moek {
 template <class C>
 cudaError_t launch_stream_cfg(const StreamArgs& a, bool pdl, cudaStream_t stream) {
     static int grid = 0;
-    const size_t smem = static_cast<size_t>(C::kWarps) * kStages * C::kStageBytes;
+    const size_t smem = static_cast<size_t>(C::kWarps) * kStages * C::kStageBytes + C::kResBytes;
     if (grid == 0) {
         MOE_CUDA_OK(cudaFuncSetAttribute(stream_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int dev = 0, sms = 0;
@@ -791,6 +833,9 @@ cudaError_t launch_stream_cfg(const StreamArgs& a, bool pdl, cudaStream_t stream
 }
 
 cudaError_t launch_stream(const StreamArgs& a, bool pdl, cudaStream_t stream) {
+    static const bool dec = getenv("MOE_GEMV_CFG") == nullptr || atoi(getenv("MOE_GEMV_CFG")) != 0;
+    // resident rows: one token, <= 2 segments (k <= 2), rows and bias fit the reserved area
+    if (dec && a.T == 1 && a.k <= 2 && a.K <= 14336 && a.bstride <= 512) return launch_stream_cfg<CfgDecode>(a, pdl, stream);
     return launch_stream_cfg<CfgBatch>(a, pdl, stream);
 }
 
@@ -904,6 +949,8 @@ cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* 
     a.part = ws.part0;
     a.kpslot = ws.kpslot;
     a.sched = ws.sched;
+    static const int dbg = getenv("MOE_GEMV_DBG") ? atoi(getenv("MOE_GEMV_DBG")) : 0;
+    a.dbg = dbg;
     a.wait_first = xmode == MOE_X_ROUTED ? 1 : 0;
     MOE_CUDA_OK(moek::launch_stream(a, xmode != MOE_X_READY, stream));
     {
