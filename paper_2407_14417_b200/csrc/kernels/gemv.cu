@@ -489,7 +489,24 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
     // When the routing comes from two or more launches back, the segment
     // table and the first items' weight copies go out before the PDL wait;
     // their activation copies (the predecessor's output) after it.
-    if (a.wait_first) pdl_wait();
+    // resident activation rows (T == 1 configuration)
+    uint8_t* res = smem + static_cast<size_t>(kWarps) * kStages * kStageBytes;
+    float* resx = reinterpret_cast<float*>(res + 2 * a.K * 2);
+    auto res_pass0 = [&]() {
+        // gate/up pass: the one token's row in both formats + its bias terms,
+        // issued as soon as the predecessor is complete (before the table)
+        if (C::kRes && a.p == 0 && threadIdx.x == 0) {
+            mbar_expect_tx(&res_bar, 2 * a.K * 2 + a.bstride * 4);
+            bulk_g2s(res, a.b16, a.K * 2, &res_bar);
+            bulk_g2s(res + a.K * 2, a.b16h, a.K * 2, &res_bar);
+            bulk_g2s(resx, a.bsum, a.bstride * 4, &res_bar);
+        }
+    };
+    if (a.wait_first) {
+        pdl_wait();
+        if (C::kRes) __syncthreads();  // res_bar initialised
+        res_pass0();
+    }
     build_segs<C>(a, st, cnt, sperm);  // contains __syncthreads
     const uint64_t pol = policy_evict_first();
     const int W = static_cast<int>(gridDim.x) * kWarps;
@@ -525,14 +542,15 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
             npro = 2;
         }
     }
-    if (!a.wait_first) pdl_wait();  // activations of the predecessor
+    if (!a.wait_first) {
+        pdl_wait();  // activations of the predecessor
+        res_pass0();
+    }
     pdl_trigger();
     ltrace(2 + 2 * a.p, 1);
-    // resident activations (T == 1): segment s's row at res + s*K*2, its bias
-    // terms at resx + s*bstride
-    uint8_t* res = smem + static_cast<size_t>(kWarps) * kStages * kStageBytes;
-    float* resx = reinterpret_cast<float*>(res + 2 * a.K * 2);
-    if (C::kRes) {
+    if (C::kRes && a.p == 1) {
+        // resident activations, down pass: segment s's slot row (its expert's
+        // format) at res + s*K*2, its bias terms at resx + s*bstride
         if (threadIdx.x == 0) {
             uint32_t bytes = 0;
             for (int s = 0; s < st.n; ++s) bytes += a.K * 2 + (st.sbytes[s] ? a.bstride * 4 : 0);
@@ -544,12 +562,13 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
                 if (p4) bulk_g2s(resx + s * a.bstride, a.bsum + static_cast<size_t>(br) * a.bstride, a.bstride * 4, &res_bar);
             }
         }
-        mbar_wait(&res_bar, 0);
     }
-    if (lane == 0) {
+    // the prologue items' activation halves (per-item configuration)
+    if (!C::kRes && lane == 0) {
         if (npro > 0) issue_acts<C>(a, st, it0, ring, &bars[warp][0]);
         if (npro > 1) issue_acts<C>(a, st, it1, ring + kStageBytes, &bars[warp][1]);
     }
+    if (C::kRes) mbar_wait(&res_bar, 0);
     const unsigned long long t_wait = gtimer();
     int issued = npro, computed = 0;
     uint32_t phase_bits = 0;
@@ -566,8 +585,10 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
             const uint8_t* bp;
             const float *x0, *x1;
             if (C::kRes) {
-                bp = res + it.s * a.K * 2 + it.kp * gk * 256 + t * 16;
-                x0 = x1 = resx + it.s * a.bstride + it.kp * gk;
+                const bool p4 = st.sbytes[it.s] != 0;
+                const int row = a.p == 0 ? (p4 ? 1 : 0) : it.s;  // pass 0: format slot; pass 1: segment
+                bp = res + row * a.K * 2 + it.kp * gk * 256 + t * 16;
+                x0 = x1 = resx + (a.p == 0 ? 0 : it.s * a.bstride) + it.kp * gk;
             } else {
                 const int m_cnt = st.mcnt[it.s];
                 bp = sp + C::kStageB + min(gr, m_cnt - 1) * (gk * 256 + kBRowPad) + t * 16;

@@ -161,6 +161,36 @@ MOE_DEVI void block_permute(const int32_t* idx, int n, int E, int32_t* counts, i
     }
 }
 
+// The same stable counting sort for n <= 32 items by one warp, no block
+// barriers: lane i holds item i's expert; its position is the count of
+// items with a smaller expert, plus those with the same expert and a lower
+// index.
+MOE_DEVI void warp_permute(const int32_t* idx, int n, int E, int32_t* counts, int32_t* offsets, int32_t* perm,
+                           int32_t* inv_perm, int lane) {
+    const int ei = lane < n ? idx[lane] : 0x7fffffff;
+    int pos = 0;
+    for (int j = 0; j < n; ++j) {
+        const int ej = __shfl_sync(0xffffffffu, ei, j);
+        pos += (ej < ei) || (ej == ei && j < lane);
+    }
+    if (lane < n) {
+        perm[pos] = lane;
+        inv_perm[lane] = pos;
+    }
+    // counts / offsets: lane e (and e+32) counts its expert
+    for (int e = lane; e < E; e += 32) {
+        int c = 0, below = 0;
+        for (int j = 0; j < n; ++j) {
+            const int ej = idx[j];
+            c += ej == e;
+            below += ej < e;
+        }
+        counts[e] = c;
+        offsets[e] = below;
+        if (e == E - 1) offsets[E] = n;
+    }
+}
+
 // Top-k on logits by one warp, in registers: lane e holds logits e and
 // e+32; k rounds of a butterfly argmax (ties -> lower index) give the
 // selection in descending-logit order; weights = softmax over the selected
@@ -288,7 +318,9 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
     // chunks of 16 bytes, so each warp half assembles one group per pass
     if (a.xperm != nullptr) {
         const int G = a.d / 128;
-        for (int g0 = wid * 2; g0 < G; g0 += blockDim.x / 16) {
+        // warps 1.. (warp 0 is on the top-k / permutation critical path)
+        const int nw = blockDim.x / 32 - 1;
+        for (int g0 = (wid - 1) * 2; wid > 0 && g0 < G; g0 += nw * 2) {
             const int g = g0 + (lane >> 4), c = lane & 15;
             uint4 cb = make_uint4(0, 0, 0, 0), ch = cb;
             float s_lo = 0.0f, s_hi = 0.0f;
@@ -310,10 +342,12 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
         return;
     }
     if (gridDim.x == 1) {
-        // single token: permute straight from shared memory
-        __syncthreads();
-        ltrace(1, 2);
-        block_permute(s_idx, a.k, a.E, a.counts, a.offsets, a.perm, a.inv_perm);
+        // single token: warp 0 permutes straight from its top-k (shared memory)
+        if (wid == 0) {
+            __syncwarp();
+            ltrace(1, 2);
+            warp_permute(s_idx, a.k, a.E, a.counts, a.offsets, a.perm, a.inv_perm, lane);
+        }
         ltrace(0, 2);
         return;
     }
