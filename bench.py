@@ -415,34 +415,40 @@ def host_split_sweep(moe, torch, prof, args, device):
         except moe.MoeError as exc:
             rows.append({"resident_frac": frac, "infeasible": str(exc)})
             continue
-        eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan, max_tokens=1, seed=args.seed, device=device,
-                            norm_eps=NORM_EPS, use_graphs=True)
-        eng.synth_input(0, 1)
-        eng.decode(1)
-        eng.sync()
-        eng.reset_counters()
-        trace = []
-        steps = args.host_split_steps
-        t0 = time.perf_counter()
-        for st in range(steps):
-            eng.synth_input(st + 1, 1)
+        model_tps = moe.expected_throughput(plan, moe.ModelProfile(**{**prof.__dict__, "compute_penalty4": 1.0}), hw)
+        row = {"resident_frac": frac, "gpu_budget_gb": round(budget / 1e9, 2), "experts_on_gpu": plan.n_gpu,
+               "model_tps_expected_throughput": round(model_tps, 3)}
+        # Static (the paper's scheme) and LRU (its Mixtral-Offloading baseline)
+        for pol, cap in (("static", 0), ("lru", args.host_split_lru if plan.n_gpu < LAYERS * EXPERTS else 0)):
+            if pol == "lru" and cap == 0:
+                continue
+            eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan, max_tokens=1, seed=args.seed,
+                                device=device, norm_eps=NORM_EPS, use_graphs=True, lru_capacity=cap)
+            eng.synth_input(0, 1)
             eng.decode(1)
             eng.sync()
-            trace.extend(eng.last_routing(1))
-        el = time.perf_counter() - t0
-        c = eng.counters()
-        sim = moe.simulate(plan, trace, steps, prof, hw)
-        model_tps = moe.expected_throughput(plan, moe.ModelProfile(**{**prof.__dict__, "compute_penalty4": 1.0}), hw) \
-            if hasattr(prof, "__dict__") else None
-        rows.append({"resident_frac": frac, "gpu_budget_gb": round(budget / 1e9, 2), "experts_on_gpu": plan.n_gpu,
-                     "tokens_per_s": round(steps / el, 3), "hits": c.hits, "activations": c.activations,
-                     "bytes_transferred": c.bytes_transferred,
-                     "counters_equal_simulate": (c.activations, c.hits, c.bytes_transferred) ==
-                                                (sim.activations, sim.hits, sim.bytes_transferred),
-                     "model_tps_expected_throughput": round(model_tps, 3) if model_tps else None})
-        eng.close()
-        del eng
-    return {"n4": n4, "h2d_gbs_measured": round(bw, 1), "policy": "Static (single swap slot, planner.cpp:108)",
+            eng.reset_counters()
+            trace = []
+            steps = args.host_split_steps
+            t0 = time.perf_counter()
+            for st in range(steps):
+                eng.synth_input(st + 1, 1)
+                eng.decode(1)
+                eng.sync()
+                trace.extend(eng.last_routing(1))
+            el = time.perf_counter() - t0
+            c = eng.counters()
+            sim = moe.simulate(plan, trace, steps, prof, hw, lru_capacity=cap)
+            row[pol] = {"tokens_per_s": round(steps / el, 3), "hits": c.hits, "activations": c.activations,
+                        "bytes_transferred": c.bytes_transferred, "lru_slots": cap,
+                        "counters_equal_simulate": (c.activations, c.hits, c.bytes_transferred) ==
+                                                   (sim.activations, sim.hits, sim.bytes_transferred)}
+            eng.close()
+            del eng
+        rows.append(row)
+    return {"n4": n4, "h2d_gbs_measured": round(bw, 1),
+            "policies": "static = single swap slot re-streamed per activation (planner.cpp:108, simulator.cpp:98-106); "
+                        "lru = LRU cache of lru_slots device slots (simulator.cpp:37-62)",
             "steps_per_point": args.host_split_steps, "points": rows}
 
 
@@ -553,6 +559,7 @@ def main():
     ap.add_argument("--host-split-points", type=lambda s: [float(v) for v in s.split(",")] if s else [],
                     default=[1.0, 0.75, 0.5, 0.25, 0.0])
     ap.add_argument("--host-split-steps", type=int, default=4)
+    ap.add_argument("--host-split-lru", type=int, default=16, help="LRU device slots for the host-split LRU column")
     ap.add_argument("--prefill-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],
                     default=[512, 2048, 4096])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -237,6 +237,10 @@ typedef struct {
                                   block, out = x + MoE(RMSNorm(x)); 0: out = x + MoE(x) */
     int32_t tc_min_tokens;     /* decode batches T >= this use the tcgen05 expert GEMM, smaller ones
                                   the streaming GEMV (0: default 64) */
+    int32_t lru_capacity;      /* host-resident experts: 0 = Static (every activation re-streams into
+                                  the single swap slot, simulator.cpp:98-106); C >= top_k = LRU cache of
+                                  C device slots (simulator.cpp:37-62, the Mixtral-Offloading baseline) */
+    int32_t pad2_;
 } moe_engine_config;
 
 int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan_entries,

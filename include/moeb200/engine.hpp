@@ -35,6 +35,7 @@ struct EngineConfig {
     bool use_graphs = true;
     float norm_eps = 0.0f;    // > 0: pre-MoE RMSNorm (unit weight), residual = un-normalised x
     int tc_min_tokens = 64;   // T >= this: tcgen05 expert GEMM instead of the streaming GEMV
+    int lru_capacity = 0;     // 0: Static swap slot (simulator.hpp ResidencyPolicy::Static); >0: LRU of that many slots
 };
 
 class MoeEngine {

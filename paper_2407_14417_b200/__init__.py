@@ -81,7 +81,7 @@ class _EngineConfig(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("experts_per_layer", C.c_int32), ("top_k", C.c_int32),
                 ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("max_tokens", C.c_int32),
                 ("seed", C.c_uint64), ("device", C.c_int32), ("use_graphs", C.c_int32), ("norm_eps", C.c_float),
-                ("tc_min_tokens", C.c_int32)]
+                ("tc_min_tokens", C.c_int32), ("lru_capacity", C.c_int32), ("pad2_", C.c_int32)]
 
 
 _lib = None
@@ -504,12 +504,12 @@ class MoeEngine:
 
     def __init__(self, num_layers: int, experts_per_layer: int, top_k: int, d_model: int, d_ffn: int,
                  plan: PlacementPlan, max_tokens: int = 1, seed: int = 0, device: int = 0,
-                 use_graphs: bool = True, norm_eps: float = 0.0, tc_min_tokens: int = 0):
+                 use_graphs: bool = True, norm_eps: float = 0.0, tc_min_tokens: int = 0, lru_capacity: int = 0):
         self.L, self.E, self.k, self.d, self.f = num_layers, experts_per_layer, top_k, d_model, d_ffn
         self.max_tokens = max_tokens
         self.norm_eps = norm_eps
         cfg = _EngineConfig(num_layers, experts_per_layer, top_k, d_model, d_ffn, max_tokens, seed, device,
-                            1 if use_graphs else 0, norm_eps, tc_min_tokens)
+                            1 if use_graphs else 0, norm_eps, tc_min_tokens, lru_capacity, 0)
         h = C.c_void_p()
         _check(lib().moe_engine_create(C.byref(cfg), plan._entries(), C.byref(h)))
         self._h = h

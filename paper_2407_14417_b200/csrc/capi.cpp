@@ -519,6 +519,8 @@ int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan
         ec.norm_eps = cfg->norm_eps;
         usage_if(cfg->tc_min_tokens < 0, "tc_min_tokens must be >= 0");
         ec.tc_min_tokens = cfg->tc_min_tokens > 0 ? cfg->tc_min_tokens : 64;
+        usage_if(cfg->lru_capacity < 0, "lru_capacity must be >= 0");
+        ec.lru_capacity = cfg->lru_capacity;
         const int n = cfg->num_layers * cfg->experts_per_layer;
         PlacementPlan plan = to_plan(plan_entries, n, 0);
         plan.swap_slot_bytes = required_swap_bytes(plan, ec.profile);

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <list>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -48,14 +49,44 @@ struct MoeEngine::Impl {
     size_t size16 = 0, size4 = 0;
 
     cudaStream_t compute = nullptr, copy = nullptr;
-    cudaEvent_t copy_done = nullptr, slot_free = nullptr;
+    cudaEvent_t copy_done = nullptr;
 
     char* dev_arena = nullptr;
     size_t dev_bytes = 0;
     char* host_arena = nullptr;
     size_t host_bytes = 0;
-    char* swap = nullptr;
-    size_t swap_bytes = 0;
+    char* swap = nullptr;        // slot pool: 1 slot (Static) or lru_capacity slots (LRU)
+    size_t swap_bytes = 0;       // bytes per slot
+    int nslots = 1;
+    std::vector<cudaEvent_t> slot_free;
+    // LRU residency (simulator.cpp:37-62): host-resident experts cached in
+    // device slots, least recently used evicted; plan-resident ones pinned
+    std::list<int>* lru = nullptr;
+    std::map<int, std::list<int>::iterator> lru_pos;
+    std::map<int, int> lru_slot_of;   // cached expert -> slot
+    std::vector<int> lru_fill;        // this layer's misses -> the slot they stream into
+    bool lru_touch(int e) {
+        const auto it = lru_pos.find(e);
+        if (it == lru_pos.end()) return false;
+        lru->splice(lru->begin(), *lru, it->second);
+        return true;
+    }
+    void lru_insert(int e) {
+        int slot;
+        if (static_cast<int>(lru_pos.size()) >= nslots) {  // evict the least recently used
+            const int victim = lru->back();
+            lru->pop_back();
+            lru_pos.erase(victim);
+            slot = lru_slot_of[victim];
+            lru_slot_of.erase(victim);
+        } else {
+            slot = static_cast<int>(lru_pos.size());
+        }
+        lru->push_front(e);
+        lru_pos[e] = lru->begin();
+        lru_slot_of[e] = slot;
+        lru_fill[static_cast<size_t>(e)] = slot;
+    }
     uint16_t* wg = nullptr;  // [L][E][d]
 
     std::vector<moe_expert_weights> weights;  // [L*E]
@@ -136,7 +167,12 @@ struct MoeEngine::Impl {
         ck(cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking), "stream");
         ck(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "stream");
         ck(cudaEventCreateWithFlags(&copy_done, cudaEventDisableTiming), "event");
-        ck(cudaEventCreateWithFlags(&slot_free, cudaEventDisableTiming), "event");
+        if (c.lru_capacity > 0 && c.lru_capacity < c.profile.top_k)
+            throw ValidationError("lru_capacity must be 0 (Static) or >= top_k");
+        nslots = c.lru_capacity > 0 ? c.lru_capacity : 1;
+        slot_free.resize(static_cast<size_t>(nslots));
+        for (auto& ev : slot_free) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        if (c.lru_capacity > 0) lru = new std::list<int>();
 
         // arenas
         std::vector<size_t> off(static_cast<size_t>(L * E));
@@ -162,7 +198,7 @@ struct MoeEngine::Impl {
         if (dev_bytes) ck(cudaMalloc(&dev_arena, dev_bytes), "cudaMalloc(expert arena)");
         if (host_bytes) ck(cudaHostAlloc(&host_arena, host_bytes, cudaHostAllocDefault), "cudaHostAlloc(host arena)");
         swap_bytes = static_cast<size_t>(plan.swap_slot_bytes);
-        if (swap_bytes) ck(cudaMalloc(&swap, swap_bytes), "cudaMalloc(swap slot)");
+        if (swap_bytes) ck(cudaMalloc(&swap, swap_bytes * static_cast<size_t>(nslots)), "cudaMalloc(swap slots)");
         weights.resize(static_cast<size_t>(L * E));
         for (int i = 0; i < L * E; ++i) {
             const ExpertState st = plan.entries[static_cast<size_t>(i)];
@@ -255,7 +291,10 @@ struct MoeEngine::Impl {
         if (host_arena) cudaFreeHost(host_arena);
         if (idx_host) cudaFreeHost(idx_host);
         if (copy_done) cudaEventDestroy(copy_done);
-        if (slot_free) cudaEventDestroy(slot_free);
+        for (auto& ev : slot_free)
+            if (ev) cudaEventDestroy(ev);
+        delete lru;
+        lru = nullptr;
         if (compute) cudaStreamDestroy(compute);
         if (copy) cudaStreamDestroy(copy);
     }
@@ -297,14 +336,25 @@ struct MoeEngine::Impl {
             ck(cudaMemcpyAsync(idx_host, idx_l, static_cast<size_t>(T) * K * 4, cudaMemcpyDeviceToHost, compute), "D2H idx");
             ck(cudaStreamSynchronize(compute), "sync");
             uint64_t sel = 0;
+            lru_fill.assign(static_cast<size_t>(L) * E, -1);
+            // activation order of simulate(): tokens in order, each token's k
+            // slots ascending (the GatingTrace record order, gating.cpp:48)
+            std::vector<int32_t> order(idx_host, idx_host + static_cast<size_t>(T) * K);
+            for (int t = 0; t < T; ++t) std::sort(order.begin() + t * K, order.begin() + (t + 1) * K);
             for (int i = 0; i < T * K; ++i) {
-                const int s = idx_host[i];
+                const int s = order[static_cast<size_t>(i)];
                 sel |= 1ull << s;
-                const ExpertState st = plan.entries[static_cast<size_t>(l * E + s)];
-                if (st.location == Location::GPU) {
+                const int e = l * E + s;
+                const ExpertState st = plan.entries[static_cast<size_t>(e)];
+                // simulate()'s per-activation rule (simulator.cpp:98-106):
+                // GPU-resident, or (LRU) cached -> hit; else a transfer
+                bool hit = st.location == Location::GPU;
+                if (!hit && lru != nullptr) hit = lru_touch(e);
+                if (hit) {
                     ++counters.hits;
                 } else {
                     counters.bytes_transferred += static_cast<int64_t>(st.precision == Precision::P16 ? size16 : size4);
+                    if (lru != nullptr) lru_insert(e);
                 }
             }
             uint64_t resident = 0;
@@ -314,20 +364,38 @@ struct MoeEngine::Impl {
                 ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, lw, E, d, f, resident, nullptr, y,
                                 MOE_X_READY, compute), "ffn");
             std::vector<moe_expert_weights> tmp(lw, lw + E);
-            for (int s = 0; s < E; ++s) {
-                if (!((sel >> s) & 1ull) || location[static_cast<size_t>(l * E + s)] == MOE_GPU) continue;
+            uint64_t done = 0;
+            for (int i = 0; i < T * K; ++i) {  // host experts in activation order
+                const int s = idx_host[i];
+                if (location[static_cast<size_t>(l * E + s)] == MOE_GPU || ((done >> s) & 1ull)) continue;
+                done |= 1ull << s;
                 const moe_expert_weights& hw = lw[s];
                 const size_t sz = hw.precision == MOE_P16 ? size16 : size4;
-                // Static swap semantics: the slot is reused by the next miss
-                // only after the previous expert's FFN has consumed it.
-                ck(cudaStreamWaitEvent(copy, slot_free, 0), "wait");
-                ck(cudaMemcpyAsync(swap, hw.w_gate_up, sz, cudaMemcpyHostToDevice, copy), "H2D expert");
-                ck(cudaEventRecord(copy_done, copy), "record");
-                ck(cudaStreamWaitEvent(compute, copy_done, 0), "wait");
-                tmp[static_cast<size_t>(s)] = view(swap, hw.precision == MOE_P16 ? Precision::P16 : Precision::P4);
+                // the slot that holds (or will hold) expert l*E+s: an LRU hit
+                // computes from it directly; a miss -- every host activation
+                // under Static -- streams the expert in first, on the copy
+                // stream, after the slot's previous occupant was consumed
+                int slot = 0;
+                bool cached = false;
+                if (lru != nullptr) {
+                    // inserted by this layer's activations -> stream into its slot;
+                    // otherwise an LRU hit from an earlier step (capacity >= top_k,
+                    // so a touched expert is never evicted within its layer)
+                    const int fill = lru_fill[static_cast<size_t>(l * E + s)];
+                    cached = fill < 0;
+                    slot = cached ? lru_slot_of[l * E + s] : fill;
+                }
+                char* dst = swap + static_cast<size_t>(slot) * swap_bytes;
+                if (!cached) {
+                    ck(cudaStreamWaitEvent(copy, slot_free[static_cast<size_t>(slot)], 0), "wait");
+                    ck(cudaMemcpyAsync(dst, hw.w_gate_up, sz, cudaMemcpyHostToDevice, copy), "H2D expert");
+                    ck(cudaEventRecord(copy_done, copy), "record");
+                    ck(cudaStreamWaitEvent(compute, copy_done, 0), "wait");
+                }
+                tmp[static_cast<size_t>(s)] = view(dst, hw.precision == MOE_P16 ? Precision::P16 : Precision::P4);
                 ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, tmp.data(), E, d, f, 1ull << s, nullptr, y,
                                 MOE_X_READY, compute), "ffn");
-                ck(cudaEventRecord(slot_free, compute), "record");
+                ck(cudaEventRecord(slot_free[static_cast<size_t>(slot)], compute), "record");
             }
         }
         ck(moek_combine(y, inv, w_l, x, T, d, K, out, compute), "combine");
@@ -531,7 +599,7 @@ const void* MoeEngine::router(int layer) const {
 void MoeEngine::memory(int64_t* expert_bytes, int64_t* swap_bytes, int64_t* host_bytes,
                        int64_t* workspace_bytes) const {
     if (expert_bytes) *expert_bytes = static_cast<int64_t>(impl_->dev_bytes);
-    if (swap_bytes) *swap_bytes = static_cast<int64_t>(impl_->swap_bytes);
+    if (swap_bytes) *swap_bytes = static_cast<int64_t>(impl_->swap_bytes) * impl_->nslots;
     if (host_bytes) *host_bytes = static_cast<int64_t>(impl_->host_bytes);
     if (workspace_bytes) *workspace_bytes = static_cast<int64_t>(impl_->ws_bytes);
 }

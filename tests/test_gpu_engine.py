@@ -260,3 +260,39 @@ def test_mixtral_layer_parity_tcgen05(moe, orc, torch_mod, cuda, precision):
     assert_close(bf16_to_f32(to_np(out, np.uint16).reshape(T, 4096)), bf16_to_f32(out_ref), RTOL_BF16,
                  f"mixtral layer tcgen05 {'bf16' if precision else 'int4'}")
     eng.close()
+
+
+@pytest.mark.parametrize("cap", [2, 4, 7])
+def test_lru_counters_match_simulate(moe, ref, torch_mod, cuda, cap):
+    """§8f row f2: LRU residency (simulator.cpp:37-62) -- host-resident
+    experts cached in `cap` device slots.  hits / bytes_transferred equal the
+    reference simulate(Lru, cap) on the exported routing; outputs stay
+    bit-identical to the all-resident engine."""
+    torch = torch_mod
+    prof = moe.profile_for_shape(512, 1792, 2)
+    full = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 1), moe.HardwareProfile(10**15), prof)
+    s16 = moe.expert_size(prof, 1)
+    budget = int(prof.size_nonexpert_bytes + s16 + 0.3 * (moe.gpu_footprint(full, prof) - prof.size_nonexpert_bytes))
+    hw = moe.HardwareProfile(budget)
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 1), hw, prof)
+    assert plan.n_gpu < 16
+    eng = moe.MoeEngine(2, 8, 2, 512, 1792, plan, max_tokens=1, seed=11, lru_capacity=cap)
+    base = make_engine(moe, TINY, full, 11, 1)
+    trace = []
+    steps = 16
+    for step in range(steps):
+        for e in (eng, base):
+            e.synth_input(step, 1)
+            e.decode(1)
+            e.sync()
+        assert np.array_equal(read_device(torch, eng.output_ptr, 1024), read_device(torch, base.output_ptr, 1024))
+        trace.extend(eng.last_routing(1))
+    c = eng.counters()
+    st, sim = ref.simulate(prof, hw.transfer_bw_bytes_per_s, plan.precision, plan.location, plan.swap_slot_bytes,
+                           steps, np.array(trace, np.int32), cap)
+    assert st == 0
+    assert (c.activations, c.hits, c.bytes_transferred) == (sim[0], sim[1], sim[2])
+    static = moe.simulate(plan, trace, steps, prof, hw)
+    assert c.hits >= static.hits  # caching never loses hits
+    eng.close()
+    base.close()
