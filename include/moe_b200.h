@@ -92,6 +92,17 @@ int64_t moe_gpu_footprint(const moe_expert_state* entries, int64_t swap_slot_byt
 int moe_validate_plan(const moe_expert_state* entries, int n_entries, int64_t swap_slot_bytes,
                       const moe_hardware_profile* hw, const moe_model_profile* p, char* msg,
                       int cap);
+/* Plan artifact, `moeserve.plan.v1` JSON (serialize.hpp:18-19 write_plan /
+ * read_plan).  write: returns the length (required length when cap is too
+ * small; the text is copied only when it fits), -1 on error.  read: ParseError
+ * (format marker, row shape, precision / location words) and ValidationError
+ * (fingerprint, duplicate / missing / out-of-range expert) both return
+ * MOE_ERR_VALIDATION, as in the CLI; moe_last_error() tells them apart.
+ * entries holds L*E rows. */
+int64_t moe_write_plan(const moe_expert_state* entries, int64_t swap_slot_bytes, uint64_t seed,
+                       const moe_model_profile* p, char* buf, int64_t cap);
+int moe_read_plan(const char* document, const moe_model_profile* p, moe_expert_state* entries,
+                  int64_t* swap_slot_bytes, uint64_t* seed);
 
 /* ------------------------------------------------------------------------
  * Routing records (gating.hpp) and the reference cost model (simulator.hpp).

@@ -264,7 +264,11 @@ class RefLib:
             "ref_simulate": (I, [PR, D, VP, VP, I64, U64, I, VP, I, VP]),
             "ref_expected_throughput": (D, [PR, D, VP, VP, I64]),
             "ref_diff_plans": (I, [PR, D, VP, VP, VP, VP, VP, VP, I, P(I64), P(D)]),
+            "ref_have_serialize": (I, []),
         }
+        if L.ref_have_serialize():
+            sig["ref_write_plan"] = (I64, [PR, VP, VP, U64, I64, C.c_char_p, I64])
+            sig["ref_read_plan"] = (I, [C.c_char_p, PR, VP, VP, P(U64), P(I64)])
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
             fn.restype, fn.argtypes = res, args
@@ -307,6 +311,29 @@ class RefLib:
         buf = C.create_string_buffer(int(n) + 1)
         self.L.ref_write_trace(C.byref(self.profile(p)), tokens, _np_ptr(arr), buf, n + 1)
         return buf.value.decode()
+
+    @property
+    def has_serialize(self) -> bool:
+        return bool(self.L.ref_have_serialize())
+
+    def write_plan(self, p, prec, loc, seed, swap):
+        """serialize.cpp:99-117 (status, document)."""
+        pr, lo = np.ascontiguousarray(prec, np.int32), np.ascontiguousarray(loc, np.int32)
+        n = self.L.ref_write_plan(C.byref(self.profile(p)), _np_ptr(pr), _np_ptr(lo), seed, swap, None, 0)
+        if n < 0:
+            return int(-n), None
+        buf = C.create_string_buffer(int(n) + 1)
+        self.L.ref_write_plan(C.byref(self.profile(p)), _np_ptr(pr), _np_ptr(lo), seed, swap, buf, n + 1)
+        return 0, buf.value.decode()
+
+    def read_plan(self, doc, p):
+        """serialize.cpp:119-149 (status, prec, loc, seed, swap)."""
+        n = p.num_layers * p.experts_per_layer
+        prec, loc = np.zeros(n, np.int32), np.zeros(n, np.int32)
+        seed, swap = C.c_uint64(), C.c_int64()
+        st = self.L.ref_read_plan(doc.encode(), C.byref(self.profile(p)), _np_ptr(prec), _np_ptr(loc),
+                                  C.byref(seed), C.byref(swap))
+        return st, prec, loc, seed.value, swap.value
 
     def simulate(self, p, bw, prec, loc, swap, tokens, slots, lru=0):
         out = np.zeros(6, np.int64)

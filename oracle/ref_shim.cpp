@@ -15,6 +15,7 @@
 //   load_profiles        profiles.hpp:84  (profiles.cpp:148-211)
 //   expert_size / model_size / profile_fingerprint (profiles.cpp:221-256)
 //   diff_plans / estimate_cost (reconfig.cpp:19-82)
+//   write_plan / read_plan (serialize.cpp:99-149, when built with nlohmann)
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -26,6 +27,9 @@
 #include "moeserve/profiles.hpp"
 #include "moeserve/reconfig.hpp"
 #include "moeserve/simulator.hpp"
+#ifdef REF_HAVE_SERIALIZE
+#include "moeserve/serialize.hpp"
+#endif
 
 using namespace moeserve;
 
@@ -276,5 +280,40 @@ int ref_diff_plans(const ref_profile* p, double bw, const int32_t* prec_a, const
     });
     return st == 0 ? n : -st;
 }
+
+#ifdef REF_HAVE_SERIALIZE
+// Plan JSON (serialize.cpp:99-149).  Returns the document length (copied
+// when it fits `cap`), or -status on error.
+int64_t ref_write_plan(const ref_profile* p, const int32_t* prec, const int32_t* loc, uint64_t seed, int64_t swap,
+                       char* buf, int64_t cap) {
+    int64_t n = -1;
+    const int st = guarded([&] {
+        const ModelProfile m = to_model(p);
+        PlacementPlan plan = to_plan(prec, loc, m.num_experts(), swap, seed);
+        const std::string doc = write_plan(plan, m);
+        n = static_cast<int64_t>(doc.size());
+        if (buf != nullptr && n < cap) std::memcpy(buf, doc.c_str(), doc.size() + 1);
+    });
+    return st == 0 ? n : -st;
+}
+
+int ref_read_plan(const char* doc, const ref_profile* p, int32_t* prec, int32_t* loc, uint64_t* seed,
+                  int64_t* swap) {
+    return guarded([&] {
+        const ModelProfile m = to_model(p);
+        const PlacementPlan plan = read_plan(doc, m);
+        for (size_t i = 0; i < plan.entries.size(); ++i) {
+            prec[i] = static_cast<int32_t>(plan.entries[i].precision);
+            loc[i] = static_cast<int32_t>(plan.entries[i].location);
+        }
+        *seed = plan.seed;
+        *swap = plan.swap_slot_bytes;
+    });
+}
+
+int ref_have_serialize(void) { return 1; }
+#else
+int ref_have_serialize(void) { return 0; }
+#endif
 
 }  // extern "C"

@@ -112,6 +112,8 @@ def lib() -> C.CDLL:
         "moe_gpu_footprint": (I64, [P(ExpertStateC), I64, P(_ModelProfile)]),
         "moe_validate_plan": (I, [P(ExpertStateC), I, I64, P(_HardwareProfile), P(_ModelProfile), C.c_char_p, I]),
         "moe_generate_trace": (I, [P(_ModelProfile), I, U64, P(C.c_int32), P(U64)]),
+        "moe_write_plan": (I64, [P(ExpertStateC), I64, U64, P(_ModelProfile), C.c_char_p, I64]),
+        "moe_read_plan": (I, [C.c_char_p, P(_ModelProfile), P(ExpertStateC), P(I64), P(U64)]),
         "moe_write_trace": (I64, [P(_ModelProfile), I, P(C.c_int32), C.c_char_p, I64]),
         "moe_read_trace": (I, [C.c_char_p, P(C.c_int32), P(U64), P(C.c_int32), I64]),
         "moe_simulate": (I, [P(ExpertStateC), I64, P(C.c_int32), I, P(_ModelProfile), P(_HardwareProfile), I, P(SimReportC)]),
@@ -332,6 +334,25 @@ def validate_plan(plan: PlacementPlan, hw: HardwareProfile, profile: ModelProfil
     if n < 0:
         _check(1)
     return [s for s in buf.value.decode().split("\n") if s][:n]
+
+
+def write_plan(plan: PlacementPlan, profile: ModelProfile) -> str:
+    """`moeserve.plan.v1` JSON, byte-identical to serialize.cpp:99-117."""
+    ent = plan._entries()
+    n = lib().moe_write_plan(ent, plan.swap_slot_bytes, plan.seed, C.byref(profile._c()), None, 0)
+    if n < 0:
+        _check(1)
+    buf = C.create_string_buffer(n + 1)
+    lib().moe_write_plan(ent, plan.swap_slot_bytes, plan.seed, C.byref(profile._c()), buf, n + 1)
+    return buf.value.decode()
+
+
+def read_plan(document: str, profile: ModelProfile) -> PlacementPlan:
+    """Parse and check a plan document against `profile` (serialize.cpp:119-149)."""
+    arr = (ExpertStateC * profile.num_experts)()
+    swap, seed = C.c_int64(), C.c_uint64()
+    _check(lib().moe_read_plan(document.encode(), C.byref(profile._c()), arr, C.byref(swap), C.byref(seed)))
+    return PlacementPlan([a.precision for a in arr], [a.location for a in arr], swap.value, seed.value)
 
 
 # ----------------------------------------------------------------- traces / simulate

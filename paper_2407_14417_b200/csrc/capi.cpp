@@ -259,6 +259,31 @@ int moe_generate_trace(const moe_model_profile* p, int tokens, uint64_t seed, in
     });
 }
 
+int64_t moe_write_plan(const moe_expert_state* entries, int64_t swap_slot_bytes, uint64_t seed,
+                       const moe_model_profile* p, char* buf, int64_t cap) {
+    std::string s;
+    if (guarded([&] {
+            usage_if(entries == nullptr, "null argument");
+            const ModelProfile m = to_model(p);
+            PlacementPlan plan = to_plan(entries, m.num_experts(), swap_slot_bytes);
+            plan.seed = seed;
+            s = write_plan(plan, m);
+        }) != MOE_OK)
+        return -1;
+    if (buf && static_cast<int64_t>(s.size()) < cap) std::memcpy(buf, s.c_str(), s.size() + 1);
+    return static_cast<int64_t>(s.size());
+}
+
+int moe_read_plan(const char* document, const moe_model_profile* p, moe_expert_state* entries,
+                  int64_t* swap_slot_bytes, uint64_t* seed) {
+    return guarded([&] {
+        usage_if(entries == nullptr, "null argument");
+        const PlacementPlan plan = read_plan(document ? document : "", to_model(p));
+        from_plan(plan, entries, swap_slot_bytes);
+        if (seed) *seed = plan.seed;
+    });
+}
+
 int64_t moe_write_trace(const moe_model_profile* p, int tokens, const int32_t* slots, char* buf,
                         int64_t cap) {
     std::string s;

@@ -9,11 +9,11 @@
                     int4 experts enter HF as their exact dequant values q*s.
   generator_kat.json  sha256 of generated tensors + raw rand64 values, so the
                     generator itself is pinned independent of the oracle build.
-  reference_kat.json  plans / traces / simulate counters produced by the
-                    reference library compiled from /root/reference
-                    (oracle/_ref) on seeded random cases.
+  reference_kat.json  plans / traces / simulate counters / plan-JSON
+                    digests produced by the reference library compiled from
+                    /root/reference (oracle/_ref) on seeded random cases.
 
-Usage: python tests/golden/make_golden.py
+Usage: python tests/golden/make_golden.py [reference]
 """
 import hashlib
 import json
@@ -114,12 +114,19 @@ def make_reference_kat(ref):
             case.update({"precision": "".join(map(str, prec.tolist())), "location": "".join(map(str, loc.tolist())),
                          "swap": swap, "trace_seed": seed % 1000, "trace_sha256": sha(slots),
                          "sim": [int(v) for v in sim], "expected_tps": ref.expected_throughput(p, bw, prec, loc, swap)})
+            if ref.has_serialize:  # serialize.cpp:99-117 plan document
+                wst, doc = ref.write_plan(p, prec, loc, seed, swap)
+                assert wst == 0
+                case["plan_json_sha256"] = hashlib.sha256(doc.encode()).hexdigest()
         cases.append(case)
     with open(os.path.join(HERE, "reference_kat.json"), "w") as fh:
         json.dump({"profile": "mixtral-sec41", "fingerprint": hex(ref.fingerprint(p)), "cases": cases}, fh, indent=0)
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["reference"]:
+        make_reference_kat(RefLib())
+        sys.exit(0)
     orc = OracleLib()
     make_generator_kat(orc)
     make_tiny(orc)

@@ -117,6 +117,11 @@ def test_reference_kat_planner_and_simulator(moe):
         r = moe.simulate(plan, slots, 50, prof, hw)
         assert [r.activations, r.hits, r.bytes_transferred, r.transfer_ns, r.compute_ns, r.nonexpert_ns] == c["sim"]
         assert moe.expected_throughput(plan, prof, hw) == c["expected_tps"]
+        if "plan_json_sha256" in c:  # serialize.cpp:99-117, byte for byte
+            plan.seed = int(c["seed"])
+            doc = moe.write_plan(plan, prof)
+            assert hashlib.sha256(doc.encode()).hexdigest() == c["plan_json_sha256"]
+            assert moe.read_plan(doc, prof) == plan
 
 
 def test_rmsnorm_pinned_order(orc):

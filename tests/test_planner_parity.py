@@ -376,3 +376,73 @@ def test_live_load_profiles_match_reference(moe, ref):
                (rp.num_layers, rp.experts_per_layer, rp.top_k, rp.size_nonexpert_bytes, rp.size_expert16_bytes,
                 rp.quant_ratio, rp.compute_latency16_s, rp.compute_penalty4, rp.nonexpert_latency_s)
         assert (h.gpu_mem_bytes, h.transfer_bw_bytes_per_s) == (mem, bw)
+
+
+# ----------------------------------------------------------- plan artifact (serialize.cpp)
+def _plan_mutations(doc):
+    """Malformed / mismatched variants of a plan document, each rejected by
+    serialize.cpp:119-149 (ParseError or ValidationError)."""
+    import json
+    j = json.loads(doc)
+    out = [doc.replace("moeserve.plan.v1", "moeserve.plan.v2"), doc.replace('"format"', '"fmt"'),
+           "", "[]", "{", doc[: len(doc) // 2]]
+    fp = j["profile_fingerprint"]
+    out.append(doc.replace(fp, fp[:-1] + ("0" if fp[-1] != "0" else "1")))
+    for fn in (lambda e: e.pop(),                              # missing expert
+               lambda e: e.append(list(e[0])),                 # duplicate
+               lambda e: e[0].__setitem__(2, "p8"),            # unknown precision
+               lambda e: e[0].__setitem__(3, "disk"),          # unknown location
+               lambda e: e[0].pop(),                           # short row
+               lambda e: e[1].__setitem__(1, 99),              # slot out of range
+               lambda e: e[1].__setitem__(0, -1)):             # layer out of range
+        jj = json.loads(doc)
+        fn(jj["experts"])
+        out.append(json.dumps(jj))
+    return out
+
+
+def test_plan_json_roundtrip_and_errors(moe, kM):
+    plan = moe.make_plan(moe.TaskRequest(1, 100, 9), hw(moe, 40_000_000_000), kM)
+    doc = moe.write_plan(plan, kM)
+    assert doc.startswith('{\n  "format": "moeserve.plan.v1",\n') and doc.endswith("\n  ]\n}\n")
+    assert moe.read_plan(doc, kM) == plan
+    import json
+    assert moe.read_plan(json.dumps(json.loads(doc)), kM) == plan  # any JSON layout of the schema
+    for bad in _plan_mutations(doc):
+        with pytest.raises(moe.MoeError) as ei:
+            moe.read_plan(bad, kM)
+        assert ei.value.code == 3, bad[:80]
+    with pytest.raises(moe.ValidationError):  # a plan for another profile
+        moe.read_plan(doc, moe.mixtral_table1())
+
+
+def test_live_plan_json_matches_reference(moe, ref, kM):
+    if not ref.has_serialize:
+        pytest.skip("oracle/_ref built without serialize.cpp (no nlohmann/json)")
+    rng = np.random.default_rng(11)
+    rp = ref.default_profile(0)
+    for _ in range(40):
+        budget = int(rng.integers(1_000_000_000, 110_000_000_000))
+        n4 = int(rng.integers(0, 257))
+        seed = int(rng.integers(0, 2**64, dtype=np.uint64))
+        st, prec, loc, swap = ref.make_plan(rp, budget, MIX_BW, 1, n4, seed)
+        if st != 0:
+            continue
+        plan = moe.PlacementPlan(prec.tolist(), loc.tolist(), swap, seed)
+        wst, rdoc = ref.write_plan(rp, prec, loc, seed, swap)
+        assert wst == 0
+        doc = moe.write_plan(plan, kM)
+        assert doc == rdoc  # byte-identical to nlohmann dump(2)
+        rst, rprec, rloc, rseed, rswap = ref.read_plan(doc, rp)
+        assert rst == 0 and rprec.tolist() == plan.precision and rloc.tolist() == plan.location
+        assert (rseed, rswap) == (seed, swap)
+        for bad in _plan_mutations(doc):
+            rst = ref.read_plan(bad, rp)[0]
+            with pytest.raises(moe.MoeError) as ei:
+                moe.read_plan(bad, kM)
+            assert ei.value.code == rst, bad[:80]
+    # toy profile, empty-layer edge: 2x2 experts
+    tp = toy(moe)
+    rtp = ref.profile(tp)
+    plan = moe.PlacementPlan([0, 1, 1, 0], [1, 0, 1, 0], 400, 0)
+    assert moe.write_plan(plan, tp) == ref.write_plan(rtp, plan.precision, plan.location, 0, 400)[1]
