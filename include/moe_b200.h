@@ -127,6 +127,33 @@ int moe_simulate(const moe_expert_state* entries, int64_t swap_slot_bytes, const
 double moe_expected_throughput(const moe_expert_state* entries, const moe_model_profile* p,
                                const moe_hardware_profile* hw);
 
+/* Quality / memory / throughput sweep (pareto.hpp, cli.cpp:243-342).
+ * Anchors: builtin name "wikitext2" | "ptb" | "c4" (Table 2), or an
+ * INI document's [quality] section over a fallback (pareto.cpp:35-54). */
+int moe_builtin_anchors(const char* name, double* ppl_all16, double* ppl_all4);
+int moe_load_anchors(const char* document, double* ppl_all16, double* ppl_all4); /* in: fallback, out: result */
+int moe_ppl_estimate(int n4, double ppl_all16, double ppl_all4, int num_e, double* out);
+int moe_n4_for_budget(double ppl_budget, double ppl_all16, double ppl_all4, int num_e, int32_t* out);
+
+typedef struct {                 /* ParetoRow, cli.cpp:243-251 */
+    int64_t budget;
+    int32_t n4, feasible, on_frontier, n_gpu;
+    int64_t gpu_bytes;
+    double ppl;
+    moe_sim_report report;
+} moe_pareto_row;
+/* rows[g*n_budgets + b] for n4_grid[g] x budgets[b], frontier flags set. */
+int moe_pareto_sweep(const int64_t* budgets, int n_budgets, const int32_t* n4_grid, int n_grid,
+                     const moe_model_profile* p, const moe_hardware_profile* hw, int tokens, uint64_t seed,
+                     double ppl_all16, double ppl_all4, moe_pareto_row* rows);
+/* Frontier flags of arbitrary points (pareto.hpp:47-50). */
+int moe_frontier_mask(int n, const double* throughput_tps, const double* ppl, const int64_t* gpu_bytes,
+                      int32_t* on_frontier);
+/* The sweep table; measured = NULL gives the reference schema exactly,
+ * else 2 doubles per row (tok/s, hit rate; NaN = not measured) append
+ * measured_tps,measured_hit_rate.  Returns the length (see moe_write_plan). */
+int64_t moe_pareto_csv(const moe_pareto_row* rows, int n, const double* measured, char* buf, int64_t cap);
+
 /* ------------------------------------------------------------------------
  * Kernels (sm_100a).  Stream-ordered; all pointers are device pointers.
  * ---------------------------------------------------------------------- */

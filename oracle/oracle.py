@@ -265,6 +265,12 @@ class RefLib:
             "ref_expected_throughput": (D, [PR, D, VP, VP, I64]),
             "ref_diff_plans": (I, [PR, D, VP, VP, VP, VP, VP, VP, I, P(I64), P(D)]),
             "ref_have_serialize": (I, []),
+            "ref_builtin_anchors": (I, [C.c_char_p, P(D), P(D)]),
+            "ref_load_anchors": (I, [C.c_char_p, P(D), P(D)]),
+            "ref_ppl_estimate": (I, [I, D, D, I, P(D)]),
+            "ref_n4_for_budget": (I, [D, D, D, I, P(C.c_int32)]),
+            "ref_frontier_mask": (I, [I, VP, VP, VP, VP]),
+            "ref_pareto_sweep": (I, [PR, D, VP, I, VP, I, I, U64, D, D, VP]),
         }
         if L.ref_have_serialize():
             sig["ref_write_plan"] = (I64, [PR, VP, VP, U64, I64, C.c_char_p, I64])
@@ -311,6 +317,46 @@ class RefLib:
         buf = C.create_string_buffer(int(n) + 1)
         self.L.ref_write_trace(C.byref(self.profile(p)), tokens, _np_ptr(arr), buf, n + 1)
         return buf.value.decode()
+
+    # rows as (budget, n4, feasible, on_frontier, n_gpu, gpu_bytes, ppl,
+    # tokens, activations, hits, bytes_transferred, transfer_ns, compute_ns, nonexpert_ns)
+    PARETO_ROW = np.dtype([("budget", "<i8"), ("n4", "<i4"), ("feasible", "<i4"), ("on_frontier", "<i4"),
+                           ("n_gpu", "<i4"), ("gpu_bytes", "<i8"), ("ppl", "<f8"), ("tokens", "<i8"),
+                           ("activations", "<i8"), ("hits", "<i8"), ("bytes_transferred", "<i8"),
+                           ("transfer_ns", "<i8"), ("compute_ns", "<i8"), ("nonexpert_ns", "<i8")])
+
+    def pareto_sweep(self, p, bw, budgets, grid, tokens, seed, p16, p4):
+        """sweep_memory + ppl_estimate + frontier_mask (cli.cpp:308-342)."""
+        b = np.ascontiguousarray(budgets, np.int64)
+        g = np.ascontiguousarray(grid, np.int32)
+        rows = np.zeros(max(len(b) * len(g), 1), self.PARETO_ROW)
+        st = self.L.ref_pareto_sweep(C.byref(self.profile(p)), bw, _np_ptr(b), len(b), _np_ptr(g), len(g), tokens,
+                                     seed, p16, p4, rows.ctypes.data)
+        return st, rows[:len(b) * len(g)]
+
+    def ppl_estimate(self, n4, p16, p4, num_e):
+        out = C.c_double()
+        return self.L.ref_ppl_estimate(n4, p16, p4, num_e, C.byref(out)), out.value
+
+    def n4_for_budget(self, budget, p16, p4, num_e):
+        out = C.c_int32()
+        return self.L.ref_n4_for_budget(budget, p16, p4, num_e, C.byref(out)), out.value
+
+    def builtin_anchors(self, name):
+        a, b = C.c_double(), C.c_double()
+        return self.L.ref_builtin_anchors(name.encode(), C.byref(a), C.byref(b)), a.value, b.value
+
+    def load_anchors(self, doc, p16, p4):
+        a, b = C.c_double(p16), C.c_double(p4)
+        return self.L.ref_load_anchors(doc.encode(), C.byref(a), C.byref(b)), a.value, b.value
+
+    def frontier_mask(self, tps, ppl, gpu_bytes):
+        t = np.ascontiguousarray(tps, np.float64)
+        q = np.ascontiguousarray(ppl, np.float64)
+        g = np.ascontiguousarray(gpu_bytes, np.int64)
+        out = np.zeros(max(len(t), 1), np.int32)
+        st = self.L.ref_frontier_mask(len(t), t.ctypes.data, q.ctypes.data, g.ctypes.data, out.ctypes.data)
+        return st, out[:len(t)].astype(bool)
 
     @property
     def has_serialize(self) -> bool:

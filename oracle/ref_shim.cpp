@@ -16,6 +16,9 @@
 //   expert_size / model_size / profile_fingerprint (profiles.cpp:221-256)
 //   diff_plans / estimate_cost (reconfig.cpp:19-82)
 //   write_plan / read_plan (serialize.cpp:99-149, when built with nlohmann)
+//   anchors / ppl_estimate / n4_for_budget / frontier_mask (pareto.cpp) and
+//   the `pareto` sweep rows (cli.cpp:308-342 restated over sweep_memory,
+//   simulator.cpp:139-163 -- cli.cpp itself needs CLI11)
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -23,6 +26,7 @@
 
 #include "moeserve/errors.hpp"
 #include "moeserve/gating.hpp"
+#include "moeserve/pareto.hpp"
 #include "moeserve/planner.hpp"
 #include "moeserve/profiles.hpp"
 #include "moeserve/reconfig.hpp"
@@ -279,6 +283,95 @@ int ref_diff_plans(const ref_profile* p, double bw, const int32_t* prec_a, const
         *downtime = rp.est_downtime_s;
     });
     return st == 0 ? n : -st;
+}
+
+// ---- pareto (same row layout as moe_pareto_row in include/moe_b200.h)
+struct ref_pareto_row {
+    int64_t budget;
+    int32_t n4, feasible, on_frontier, n_gpu;
+    int64_t gpu_bytes;
+    double ppl;
+    int64_t tokens, activations, hits, bytes_transferred, transfer_ns, compute_ns, nonexpert_ns;
+};
+
+int ref_builtin_anchors(const char* name, double* p16, double* p4) {
+    return guarded([&] {
+        const auto a = builtin_anchors(name);
+        if (!a) throw UsageError("unknown dataset");
+        *p16 = a->ppl_all16;
+        *p4 = a->ppl_all4;
+    });
+}
+
+int ref_load_anchors(const char* doc, double* p16, double* p4) {
+    return guarded([&] {
+        const QualityAnchors a = load_anchors(doc, QualityAnchors{"", *p16, *p4});
+        *p16 = a.ppl_all16;
+        *p4 = a.ppl_all4;
+    });
+}
+
+int ref_ppl_estimate(int n4, double p16, double p4, int num_e, double* out) {
+    return guarded([&] { *out = ppl_estimate(n4, QualityAnchors{"", p16, p4}, num_e); });
+}
+
+int ref_n4_for_budget(double budget, double p16, double p4, int num_e, int32_t* out) {
+    return guarded([&] { *out = n4_for_budget(budget, QualityAnchors{"", p16, p4}, num_e); });
+}
+
+int ref_frontier_mask(int n, const double* tps, const double* ppl, const int64_t* gpu_bytes, int32_t* out) {
+    return guarded([&] {
+        std::vector<ParetoPoint> pts(static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i) pts[static_cast<size_t>(i)] = {0, 0, tps[i], ppl[i], gpu_bytes[i]};
+        const auto m = frontier_mask(pts);
+        for (int i = 0; i < n; ++i) out[i] = m[static_cast<size_t>(i)];
+    });
+}
+
+int ref_pareto_sweep(const ref_profile* p, double bw, const int64_t* budgets, int nb, const int32_t* grid, int ng,
+                     int tokens, uint64_t seed, double p16, double p4, ref_pareto_row* rows) {
+    return guarded([&] {
+        const ModelProfile m = to_model(p);
+        const QualityAnchors anchors{"", p16, p4};
+        const std::vector<bytes_t> bl(budgets, budgets + nb);
+        std::vector<ref_pareto_row> out;
+        std::vector<SimReport> reps;
+        for (int g = 0; g < ng; ++g) {
+            TaskRequest task;
+            task.preference = Preference::Quality;
+            task.n4_target = grid[g];
+            task.seed = seed;
+            const double ppl = ppl_estimate(grid[g], anchors, m.num_experts());
+            for (const SweepEntry& e : sweep_memory(bl, task, m, to_hw(1, bw), tokens, seed)) {
+                ref_pareto_row r{};
+                r.budget = e.budget;
+                r.n4 = grid[g];
+                r.feasible = e.feasible;
+                r.n_gpu = e.summary.n_gpu;
+                r.gpu_bytes = e.summary.gpu_bytes;
+                r.ppl = ppl;
+                r.tokens = e.report.tokens;
+                r.activations = e.report.activations;
+                r.hits = e.report.hits;
+                r.bytes_transferred = e.report.bytes_transferred;
+                r.transfer_ns = e.report.transfer_ns;
+                r.compute_ns = e.report.compute_ns;
+                r.nonexpert_ns = e.report.nonexpert_ns;
+                out.push_back(r);
+                reps.push_back(e.report);
+            }
+        }
+        std::vector<ParetoPoint> pts;
+        std::vector<size_t> at;
+        for (size_t i = 0; i < out.size(); ++i) {
+            if (!out[i].feasible) continue;
+            pts.push_back({out[i].budget, out[i].n4, reps[i].throughput_tps(), out[i].ppl, out[i].gpu_bytes});
+            at.push_back(i);
+        }
+        const auto mask = frontier_mask(pts);
+        for (size_t i = 0; i < pts.size(); ++i) out[at[i]].on_frontier = mask[i];
+        std::memcpy(rows, out.data(), out.size() * sizeof(ref_pareto_row));
+    });
 }
 
 #ifdef REF_HAVE_SERIALIZE

@@ -72,6 +72,11 @@ class SimReportC(C.Structure):
                 ("compute_ns", C.c_int64), ("nonexpert_ns", C.c_int64)]
 
 
+class ParetoRowC(C.Structure):
+    _fields_ = [("budget", C.c_int64), ("n4", C.c_int32), ("feasible", C.c_int32), ("on_frontier", C.c_int32),
+                ("n_gpu", C.c_int32), ("gpu_bytes", C.c_int64), ("ppl", C.c_double), ("report", SimReportC)]
+
+
 class ExpertWeightsC(C.Structure):
     _fields_ = [("precision", C.c_int32), ("pad_", C.c_int32), ("w_gate_up", C.c_void_p),
                 ("s_gate_up", C.c_void_p), ("w_down", C.c_void_p), ("s_down", C.c_void_p)]
@@ -118,6 +123,14 @@ def lib() -> C.CDLL:
         "moe_read_trace": (I, [C.c_char_p, P(C.c_int32), P(U64), P(C.c_int32), I64]),
         "moe_simulate": (I, [P(ExpertStateC), I64, P(C.c_int32), I, P(_ModelProfile), P(_HardwareProfile), I, P(SimReportC)]),
         "moe_expected_throughput": (D, [P(ExpertStateC), P(_ModelProfile), P(_HardwareProfile)]),
+        "moe_builtin_anchors": (I, [C.c_char_p, P(D), P(D)]),
+        "moe_load_anchors": (I, [C.c_char_p, P(D), P(D)]),
+        "moe_ppl_estimate": (I, [I, D, D, I, P(D)]),
+        "moe_n4_for_budget": (I, [D, D, D, I, P(C.c_int32)]),
+        "moe_pareto_sweep": (I, [P(I64), I, P(C.c_int32), I, P(_ModelProfile), P(_HardwareProfile), I, U64, D, D,
+                                 P(ParetoRowC)]),
+        "moe_frontier_mask": (I, [I, P(D), P(D), P(I64), P(C.c_int32)]),
+        "moe_pareto_csv": (I64, [P(ParetoRowC), I, P(D), C.c_char_p, I64]),
         "moe_gate_topk": (I, [VP, VP, I, I, I, I, VP, VP, VP, VP]),
         "moe_permute": (I, [VP, I, I, I, VP, VP, VP, VP, VP]),
         "moe_ffn_workspace_bytes": (C.c_size_t, [I, I, I, I, I]),
@@ -425,6 +438,99 @@ def simulate(plan: PlacementPlan, slots: Sequence[int], tokens: int, profile: Mo
 
 def expected_throughput(plan: PlacementPlan, profile: ModelProfile, hw: HardwareProfile) -> float:
     return lib().moe_expected_throughput(plan._entries(), C.byref(profile._c()), C.byref(hw._c()))
+
+
+# ----------------------------------------------------------------- pareto (f3)
+@dataclass
+class QualityAnchors:
+    """pareto.hpp:14-19; defaults = wikitext2 (Table 2)."""
+    ppl_all16: float = 3.81
+    ppl_all4: float = 4.00
+
+
+def builtin_anchors(name: str) -> QualityAnchors:
+    a, b = C.c_double(), C.c_double()
+    _check(lib().moe_builtin_anchors(name.encode(), C.byref(a), C.byref(b)))
+    return QualityAnchors(a.value, b.value)
+
+
+def load_anchors(document: str, fallback: QualityAnchors = None) -> QualityAnchors:
+    fallback = fallback or QualityAnchors()
+    a, b = C.c_double(fallback.ppl_all16), C.c_double(fallback.ppl_all4)
+    _check(lib().moe_load_anchors(document.encode(), C.byref(a), C.byref(b)))
+    return QualityAnchors(a.value, b.value)
+
+
+def ppl_estimate(n4: int, anchors: QualityAnchors, num_e: int) -> float:
+    out = C.c_double()
+    _check(lib().moe_ppl_estimate(n4, anchors.ppl_all16, anchors.ppl_all4, num_e, C.byref(out)))
+    return out.value
+
+
+def n4_for_budget(ppl_budget: float, anchors: QualityAnchors, num_e: int) -> int:
+    out = C.c_int32()
+    _check(lib().moe_n4_for_budget(ppl_budget, anchors.ppl_all16, anchors.ppl_all4, num_e, C.byref(out)))
+    return out.value
+
+
+def frontier_mask(throughput_tps: Sequence[float], ppl: Sequence[float], gpu_bytes: Sequence[int]) -> List[bool]:
+    n = len(throughput_tps)
+    out = (C.c_int32 * max(n, 1))()
+    _check(lib().moe_frontier_mask(n, (C.c_double * max(n, 1))(*throughput_tps), (C.c_double * max(n, 1))(*ppl),
+                                   (C.c_int64 * max(n, 1))(*gpu_bytes), out))
+    return [bool(v) for v in out[:n]]
+
+
+@dataclass
+class ParetoRow:
+    """cli.cpp:243-251: one (budget, n4) cell; `report` is the Static simulate."""
+    budget: int
+    n4: int
+    feasible: bool
+    on_frontier: bool
+    n_gpu: int
+    gpu_bytes: int
+    ppl: float
+    report: SimReport
+
+    def _c(self) -> ParetoRowC:
+        r = self.report
+        return ParetoRowC(self.budget, self.n4, int(self.feasible), int(self.on_frontier), self.n_gpu,
+                          self.gpu_bytes, self.ppl,
+                          SimReportC(r.tokens, r.activations, r.hits, r.bytes_transferred, r.transfer_ns,
+                                     r.compute_ns, r.nonexpert_ns))
+
+
+def pareto_sweep(budgets: Sequence[int], n4_grid: Sequence[int], profile: ModelProfile, hw: HardwareProfile,
+                 tokens: int = 2000, seed: int = 0, anchors: QualityAnchors = None) -> List[ParetoRow]:
+    """Rows for n4_grid x budgets (grid-major), frontier flags set (cli.cpp:308-342)."""
+    anchors = anchors or QualityAnchors()
+    nb, ng = len(budgets), len(n4_grid)
+    rows = (ParetoRowC * max(nb * ng, 1))()
+    _check(lib().moe_pareto_sweep((C.c_int64 * max(nb, 1))(*budgets), nb, (C.c_int32 * max(ng, 1))(*n4_grid), ng,
+                                  C.byref(profile._c()), C.byref(hw._c()), tokens, seed, anchors.ppl_all16,
+                                  anchors.ppl_all4, rows))
+    return [ParetoRow(r.budget, r.n4, bool(r.feasible), bool(r.on_frontier), r.n_gpu, r.gpu_bytes, r.ppl,
+                      SimReport._from_c(r.report)) for r in rows[:nb * ng]]
+
+
+def pareto_csv(rows: Sequence[ParetoRow], measured: Sequence = None) -> str:
+    """The reference sweep table (cli.cpp:253-270); `measured` = per-row
+    (tok/s, hit rate) or None appends measured_tps,measured_hit_rate."""
+    n = len(rows)
+    arr = (ParetoRowC * max(n, 1))(*[r._c() for r in rows])
+    meas = None
+    if measured is not None:
+        flat = []
+        for m in measured:
+            flat.extend((float("nan"), float("nan")) if m is None else (float(m[0]), float(m[1])))
+        meas = (C.c_double * max(len(flat), 1))(*flat)
+    k = lib().moe_pareto_csv(arr, n, meas, None, 0)
+    if k < 0:
+        _check(1)
+    buf = C.create_string_buffer(k + 1)
+    lib().moe_pareto_csv(arr, n, meas, buf, k + 1)
+    return buf.value.decode()
 
 
 # ----------------------------------------------------------------- kernels

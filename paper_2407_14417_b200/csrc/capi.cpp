@@ -13,6 +13,7 @@
 #include "kernels/launch.h"
 #include "moe_b200.h"
 #include "moeb200/engine.hpp"
+#include "moeb200/pareto.hpp"
 
 using namespace moeb200;
 
@@ -50,7 +51,7 @@ int guarded(F&& fn) {
     }
 }
 
-void usage_if(bool bad, const char* msg) {
+void usage_if(bool bad, const std::string& msg) {
     if (bad) throw UsageError(msg);
 }
 
@@ -332,6 +333,111 @@ double moe_expected_throughput(const moe_expert_state* entries, const moe_model_
         v = expected_throughput(to_plan(entries, m.num_experts(), 0), m, to_hw(hw));
     });
     return v;
+}
+
+namespace {
+
+QualityAnchors anchors_of(double p16, double p4) { return QualityAnchors{"", p16, p4}; }
+
+void to_c_report(const SimReport& r, moe_sim_report* out) {
+    *out = {r.tokens, r.activations, r.hits, r.bytes_transferred, r.transfer_ns, r.compute_ns, r.nonexpert_ns};
+}
+
+ParetoRow from_c_row(const moe_pareto_row& c) {
+    ParetoRow r;
+    r.budget = c.budget;
+    r.n4 = c.n4;
+    r.feasible = c.feasible != 0;
+    r.on_frontier = c.on_frontier != 0;
+    r.summary.n_gpu = c.n_gpu;
+    r.summary.gpu_bytes = c.gpu_bytes;
+    r.ppl = c.ppl;
+    const moe_sim_report& s = c.report;
+    r.report.tokens = static_cast<int>(s.tokens);
+    r.report.activations = s.activations;
+    r.report.hits = s.hits;
+    r.report.bytes_transferred = s.bytes_transferred;
+    r.report.transfer_ns = s.transfer_ns;
+    r.report.compute_ns = s.compute_ns;
+    r.report.nonexpert_ns = s.nonexpert_ns;
+    return r;
+}
+
+}  // namespace
+
+int moe_builtin_anchors(const char* name, double* ppl_all16, double* ppl_all4) {
+    return guarded([&] {
+        const auto a = builtin_anchors(name ? name : "");
+        usage_if(!a, std::string("unknown dataset '") + (name ? name : "") + "' (known: wikitext2, ptb, c4)");
+        *ppl_all16 = a->ppl_all16;
+        *ppl_all4 = a->ppl_all4;
+    });
+}
+
+int moe_load_anchors(const char* document, double* ppl_all16, double* ppl_all4) {
+    return guarded([&] {
+        const QualityAnchors a = load_anchors(document ? document : "", anchors_of(*ppl_all16, *ppl_all4));
+        *ppl_all16 = a.ppl_all16;
+        *ppl_all4 = a.ppl_all4;
+    });
+}
+
+int moe_ppl_estimate(int n4, double ppl_all16, double ppl_all4, int num_e, double* out) {
+    return guarded([&] { *out = ppl_estimate(n4, anchors_of(ppl_all16, ppl_all4), num_e); });
+}
+
+int moe_n4_for_budget(double ppl_budget, double ppl_all16, double ppl_all4, int num_e, int32_t* out) {
+    return guarded([&] { *out = n4_for_budget(ppl_budget, anchors_of(ppl_all16, ppl_all4), num_e); });
+}
+
+int moe_pareto_sweep(const int64_t* budgets, int n_budgets, const int32_t* n4_grid, int n_grid,
+                     const moe_model_profile* p, const moe_hardware_profile* hw, int tokens, uint64_t seed,
+                     double ppl_all16, double ppl_all4, moe_pareto_row* rows) {
+    return guarded([&] {
+        usage_if(rows == nullptr || n_budgets < 0 || n_grid < 0, "bad sweep arguments");
+        const std::vector<bytes_t> b(budgets, budgets + n_budgets);
+        const std::vector<int> g(n4_grid, n4_grid + n_grid);
+        const auto out = pareto_sweep(b, g, to_model(p), to_hw(hw), tokens, seed, anchors_of(ppl_all16, ppl_all4));
+        for (size_t i = 0; i < out.size(); ++i) {
+            const ParetoRow& r = out[i];
+            moe_pareto_row& c = rows[i];
+            c = {};
+            c.budget = r.budget;
+            c.n4 = r.n4;
+            c.feasible = r.feasible;
+            c.on_frontier = r.on_frontier;
+            c.n_gpu = r.summary.n_gpu;
+            c.gpu_bytes = r.summary.gpu_bytes;
+            c.ppl = r.ppl;
+            to_c_report(r.report, &c.report);
+        }
+    });
+}
+
+int moe_frontier_mask(int n, const double* throughput_tps, const double* ppl, const int64_t* gpu_bytes,
+                      int32_t* on_frontier) {
+    return guarded([&] {
+        std::vector<ParetoPoint> pts(static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i) pts[static_cast<size_t>(i)] = {0, 0, throughput_tps[i], ppl[i], gpu_bytes[i]};
+        const auto m = frontier_mask(pts);
+        for (int i = 0; i < n; ++i) on_frontier[i] = m[static_cast<size_t>(i)];
+    });
+}
+
+int64_t moe_pareto_csv(const moe_pareto_row* rows, int n, const double* measured, char* buf, int64_t cap) {
+    std::string s;
+    if (guarded([&] {
+            std::vector<ParetoRow> r;
+            std::vector<MeasuredCell> m;
+            for (int i = 0; i < n; ++i) {
+                r.push_back(from_c_row(rows[i]));
+                if (measured) m.push_back({measured[2 * i], measured[2 * i + 1]});
+            }
+            s = pareto_csv(r, measured ? &m : nullptr);
+        }) != MOE_OK)
+        return -1;
+    if (buf && static_cast<int64_t>(s.size()) < cap) std::memcpy(buf, s.c_str(), s.size() + 1);
+    return static_cast<int64_t>(s.size());
 }
 
 // ---------------------------------------------------------------- kernels

@@ -162,6 +162,12 @@ def test_host_streaming_counters_match_simulate(moe, ref, torch_mod, cuda, budge
     assert (c.activations, c.hits, c.bytes_transferred) == (sim[0], sim[1], sim[2])
     mine = moe.simulate(plan, trace, 12, prof, hw)
     assert (mine.activations, mine.hits, mine.bytes_transferred) == (sim[0], sim[1], sim[2])
+    # f4: the engine's real routing as a v1 trace file the reference tools replay
+    doc = moe.write_trace(prof, 12, trace)
+    assert doc == ref.write_trace(prof, 12, np.array(trace, np.int32))
+    tr = moe.read_trace(doc)
+    assert tr["slots"] == trace and tr["fingerprint"] == moe.profile_fingerprint(prof)
+    assert moe.read_plan(moe.write_plan(plan, prof), prof) == plan
     eng.close()
     base.close()
 
@@ -296,3 +302,23 @@ def test_lru_counters_match_simulate(moe, ref, torch_mod, cuda, cap):
     assert c.hits >= static.hits  # caching never loses hits
     eng.close()
     base.close()
+
+
+def test_measured_pareto_sweep_tiny(moe, cuda):
+    """f3: measured columns next to the simulated ones (tiny shape).  Fully
+    resident cells hit every activation."""
+    from paper_2407_14417_b200 import pareto
+    shape = (2, 8, 2, 512, 1792)
+    prof = moe.profile_for_shape(512, 1792, 2)
+    s16 = moe.expert_size(prof, 1)
+    budgets = [prof.size_nonexpert_bytes + 4 * s16, prof.size_nonexpert_bytes + 16 * s16]
+    rows, meas = pareto.measured_sweep(moe, budgets, [0, 16], shape, 12.285e9, 20, seed=3, steps=6)
+    assert len(rows) == 4
+    for r, m in zip(rows, meas):
+        assert r.feasible and m is not None and m[0] > 0
+        if r.n_gpu == 16:
+            assert r.report.hit_rate() == 1.0 and m[1] == 1.0
+        else:
+            assert 0.0 <= m[1] <= 1.0
+    doc = moe.pareto_csv(rows, meas)
+    assert len(doc.splitlines()) == 5 and ",-,-" not in doc

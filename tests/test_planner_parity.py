@@ -446,3 +446,115 @@ def test_live_plan_json_matches_reference(moe, ref, kM):
     rtp = ref.profile(tp)
     plan = moe.PlacementPlan([0, 1, 1, 0], [1, 0, 1, 0], 400, 0)
     assert moe.write_plan(plan, tp) == ref.write_plan(rtp, plan.precision, plan.location, 0, 400)[1]
+
+
+# ----------------------------------------------------------- pareto (f3)
+def _csv_restated(rows, measured=None):
+    """cli.cpp:253-270 restated over reference rows (+ the measured columns)."""
+    g = lambda v: "%.10g" % v  # format_double, serialize.cpp:93-97
+    out = ("budget_bytes,n4,n_gpu,gpu_bytes,throughput_tps,hit_rate,bytes_transferred,ppl_estimate,on_frontier,"
+           "status" + (",measured_tps,measured_hit_rate" if measured is not None else "") + "\n")
+    for i, r in enumerate(rows):
+        out += f"{int(r['budget'])},{int(r['n4'])},"
+        if r["feasible"]:
+            tot = (int(r["transfer_ns"]) + int(r["compute_ns"]) + int(r["nonexpert_ns"])) / 1e9
+            hit = 1.0 if r["activations"] == 0 else int(r["hits"]) / int(r["activations"])
+            out += (f"{int(r['n_gpu'])},{int(r['gpu_bytes'])},{g(int(r['tokens']) / tot)},{g(hit)},"
+                    f"{int(r['bytes_transferred'])},{g(float(r['ppl']))},{int(r['on_frontier'])},ok")
+        else:
+            out += f"-,-,-,-,-,{g(float(r['ppl']))},0,infeasible"
+        if measured is not None:
+            m = measured[i]
+            out += ",-,-" if (m is None or not r["feasible"]) else f",{g(m[0])},{g(m[1])}"
+        out += "\n"
+    return out
+
+
+def test_live_pareto_sweep_matches_reference(moe, ref, kM):
+    rng = np.random.default_rng(1407)
+    rp = ref.default_profile(0)
+    for case in range(6):
+        budgets = sorted(int(v) for v in rng.integers(3_000_000_000, 100_000_000_000, size=int(rng.integers(1, 7))))
+        grid = [int(v) for v in rng.integers(0, 257, size=int(rng.integers(1, 5)))]
+        seed = int(rng.integers(0, 2**63))
+        name = ("wikitext2", "ptb", "c4")[case % 3]
+        st, p16, p4 = ref.builtin_anchors(name)
+        a = moe.builtin_anchors(name)
+        assert st == 0 and (a.ppl_all16, a.ppl_all4) == (p16, p4)
+        st, rrows = ref.pareto_sweep(rp, MIX_BW, budgets, grid, 60, seed, p16, p4)
+        assert st == 0
+        rows = moe.pareto_sweep(budgets, grid, kM, hw(moe, 1), 60, seed, a)
+        assert len(rows) == len(rrows)
+        for r, q in zip(rows, rrows):
+            assert (r.budget, r.n4, r.feasible, r.on_frontier, r.ppl) == \
+                (q["budget"], q["n4"], bool(q["feasible"]), bool(q["on_frontier"]), q["ppl"])
+            if r.feasible:
+                assert (r.n_gpu, r.gpu_bytes) == (q["n_gpu"], q["gpu_bytes"])
+                rep = r.report
+                assert [rep.tokens, rep.activations, rep.hits, rep.bytes_transferred, rep.transfer_ns, rep.compute_ns,
+                        rep.nonexpert_ns] == [int(q[k]) for k in ("tokens", "activations", "hits", "bytes_transferred",
+                                                                   "transfer_ns", "compute_ns", "nonexpert_ns")]
+        assert moe.pareto_csv(rows) == _csv_restated(rrows)
+        meas = [None if i % 2 else (123.25 + i, 0.5) for i in range(len(rows))]
+        assert moe.pareto_csv(rows, meas) == _csv_restated(rrows, meas)
+
+
+def test_live_pareto_primitives_match_reference(moe, ref):
+    rng = np.random.default_rng(3)
+    for _ in range(200):  # frontier over random point clouds with ties
+        n = int(rng.integers(0, 40))
+        tps = rng.integers(0, 6, n).astype(np.float64)
+        ppl = rng.integers(0, 4, n) * 0.5 + 3.0
+        gb = rng.integers(0, 5, n).astype(np.int64)
+        st, mask = ref.frontier_mask(tps, ppl, gb)
+        assert st == 0 and moe.frontier_mask(tps.tolist(), ppl.tolist(), gb.tolist()) == mask.tolist()
+    anchors = [(3.81, 4.0), (13.59, 14.17), (7.24, 7.4), (5.0, 5.0), (0.5, 4.0), (4.0, 3.0), (1.0, 2.0)]
+    for p16, p4 in anchors:
+        for n4, num_e in ((0, 256), (77, 256), (256, 256), (257, 256), (-1, 8), (3, 0)):
+            st, v = ref.ppl_estimate(n4, p16, p4, num_e)
+            if st:
+                with pytest.raises(moe.MoeError) as ei:
+                    moe.ppl_estimate(n4, moe.QualityAnchors(p16, p4), num_e)
+                assert ei.value.code == st
+            else:
+                assert moe.ppl_estimate(n4, moe.QualityAnchors(p16, p4), num_e) == v
+        for budget in (3.0, p16, (p16 + p4) / 2, p4, p4 + 1):
+            st, v = ref.n4_for_budget(budget, p16, p4, 256)
+            if st:
+                with pytest.raises(moe.MoeError) as ei:
+                    moe.n4_for_budget(budget, moe.QualityAnchors(p16, p4), 256)
+                assert ei.value.code == st
+            else:
+                assert moe.n4_for_budget(budget, moe.QualityAnchors(p16, p4), 256) == v
+    docs = ["", "[quality]\ndataset = ptb\n", "[quality]\ndataset = mine\nppl_all16 = 5\nppl_all4 = 6\n",
+            "[quality]\nppl_all4 = 3.9\n", "[quality]\nppl_all4 = 3.0\n", "[quality]\nfoo = 1\n",
+            "[quality]\nppl_all16 = x\n", "[model]\ntop_k = 2\n[quality]\ndataset = c4\n"]
+    for doc in docs:
+        st, a, b = ref.load_anchors(doc, 3.81, 4.0)
+        if st:
+            with pytest.raises(moe.MoeError) as ei:
+                moe.load_anchors(doc)
+            assert ei.value.code == st, doc
+        else:
+            got = moe.load_anchors(doc)
+            assert (got.ppl_all16, got.ppl_all4) == (a, b), doc
+    with pytest.raises(moe.UsageError):
+        moe.builtin_anchors("imagenet")
+
+
+def test_pareto_cli_parsing_and_unmeasured_sweep(moe):
+    from paper_2407_14417_b200 import pareto
+    assert pareto.parse_mem_range(moe, "24GB:30GB:2GB") == [24 * 10**9, 26 * 10**9, 28 * 10**9, 30 * 10**9]
+    assert pareto.parse_mem_range(moe, "1GB") == [10**9]
+    for bad in ("1GB:2GB", "2GB:1GB:1GB", "1GB:2GB:0", "x"):
+        with pytest.raises(moe.MoeError):
+            pareto.parse_mem_range(moe, bad)
+    assert pareto.parse_n4_grid(moe, "0,5,256") == [0, 5, 256]
+    for bad in ("", "1,,2", "-1", "a"):
+        with pytest.raises(moe.UsageError):
+            pareto.parse_n4_grid(moe, bad)
+    rows, meas = pareto.measured_sweep(moe, [10**9, 5 * 10**9], [0, 16], (2, 8, 2, 512, 1792), 12.285e9, 20,
+                                       measure=False)
+    assert len(rows) == 4 and meas == [None] * 4
+    doc = moe.pareto_csv(rows, meas)
+    assert doc.splitlines()[0].endswith(",status,measured_tps,measured_hit_rate")
