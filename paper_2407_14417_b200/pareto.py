@@ -76,7 +76,7 @@ def measure_cell(moe, plan, shape: Tuple[int, int, int, int, int], steps: int, s
         eng.sync()
         el = time.perf_counter() - t0
         c = eng.counters()
-        return steps / el, c.hit_rate()
+        return steps / el, c.hit_rate
     finally:
         eng.close()
 

@@ -317,7 +317,7 @@ def test_measured_pareto_sweep_tiny(moe, cuda):
     for r, m in zip(rows, meas):
         assert r.feasible and m is not None and m[0] > 0
         if r.n_gpu == 16:
-            assert r.report.hit_rate() == 1.0 and m[1] == 1.0
+            assert r.report.hit_rate == 1.0 and m[1] == 1.0
         else:
             assert 0.0 <= m[1] <= 1.0
     doc = moe.pareto_csv(rows, meas)
