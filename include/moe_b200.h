@@ -127,6 +127,21 @@ int moe_simulate(const moe_expert_state* entries, int64_t swap_slot_bytes, const
 double moe_expected_throughput(const moe_expert_state* entries, const moe_model_profile* p,
                                const moe_hardware_profile* hw);
 
+/* Reconfiguration (reconfig.hpp:12-58): kinds 0 Offload, 1 Fetch, 2 Quantize,
+ * 3 Dequantize; each action records the expert's entry in the target plan. */
+typedef struct {
+    int32_t kind, layer, slot, target_precision, target_location, pad_;
+} moe_reconfig_action;
+/* diff_plans (reconfig.cpp:19-55): writes min(n, cap) actions, *n_actions = n. */
+int moe_diff_plans(const moe_expert_state* from, const moe_expert_state* to, uint64_t to_seed,
+                   const moe_model_profile* p, const moe_hardware_profile* hw, moe_reconfig_action* actions,
+                   int cap, int* n_actions, int64_t* bytes_moved, double* est_downtime_s);
+/* apply (reconfig.cpp:84-168): checked replay; budget may be NULL. */
+int moe_apply_reconfig(const moe_expert_state* plan, uint64_t plan_seed, const moe_reconfig_action* actions,
+                       int n_actions, uint64_t target_seed, const moe_model_profile* p,
+                       const moe_hardware_profile* budget, moe_expert_state* out, int64_t* out_swap,
+                       uint64_t* out_seed);
+
 /* Quality / memory / throughput sweep (pareto.hpp, cli.cpp:243-342).
  * Anchors: builtin name "wikitext2" | "ptb" | "c4" (Table 2), or an
  * INI document's [quality] section over a fallback (pareto.cpp:35-54). */
@@ -278,7 +293,9 @@ typedef struct {
     int32_t lru_capacity;      /* host-resident experts: 0 = Static (every activation re-streams into
                                   the single swap slot, simulator.cpp:98-106); C >= top_k = LRU cache of
                                   C device slots (simulator.cpp:37-62, the Mixtral-Offloading baseline) */
-    int32_t pad2_;
+    int32_t keep_masters;      /* 1: pinned host copy of every expert in both precisions (the reconfig
+                                  model's 16-bit CPU master, reconfig.hpp:39); needed by
+                                  moe_engine_reconfigure */
 } moe_engine_config;
 
 int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan_entries,
@@ -314,6 +331,19 @@ int moe_engine_last_routing(moe_engine* eng, int T, int32_t* slots_out);
 /* Cumulative SimReport counters of real runs (hits / bytes_transferred /
  * activations follow simulate() semantics for the engine's plan). */
 int moe_engine_counters(const moe_engine* eng, moe_sim_report* out);
+/* Execute diff_plans(current, target) on the device (needs keep_masters):
+ * Offload releases HBM, Fetch / in-place Dequantize copy host copies in,
+ * Quantize of a device-resident expert runs the int4-g128 quantiser on the
+ * device.  transfer_bw prices the model's est_downtime_s. */
+typedef struct {
+    int32_t actions, pad_;
+    int64_t bytes_moved;       /* model (estimate_cost)            */
+    double est_downtime_s;     /* model: bytes_moved / transfer_bw */
+    int64_t bytes_h2d;         /* measured bytes copied to the GPU */
+    double measured_s;         /* measured wall time (events)      */
+} moe_reconfig_report;
+int moe_engine_reconfigure(moe_engine* eng, const moe_expert_state* target, uint64_t target_seed,
+                           double transfer_bw_bytes_per_s, moe_reconfig_report* out);
 int moe_engine_reset_counters(moe_engine* eng);
 /* Per-expert device weight view (for tests); host-resident experts report
  * their pinned host pointers with location MOE_CPU. */

@@ -22,6 +22,7 @@
 #include "moe_b200.h"
 #include "moeb200/gating.hpp"
 #include "moeb200/planner.hpp"
+#include "moeb200/reconfig.hpp"
 #include "moeb200/simulator.hpp"
 
 namespace moeb200 {
@@ -36,6 +37,18 @@ struct EngineConfig {
     float norm_eps = 0.0f;    // > 0: pre-MoE RMSNorm (unit weight), residual = un-normalised x
     int tc_min_tokens = 64;   // T >= this: tcgen05 expert GEMM instead of the streaming GEMV
     int lru_capacity = 0;     // 0: Static swap slot (simulator.hpp ResidencyPolicy::Static); >0: LRU of that many slots
+    bool keep_masters = false;  // pinned host copy of every expert in both precisions (the reconfig
+                                // model's "16-bit master on the CPU", reconfig.hpp:39): required by reconfigure()
+};
+
+// What MoeEngine::reconfigure did: the model's numbers (diff_plans) and the
+// measured ones.
+struct ReconfigReport {
+    int actions = 0;
+    bytes_t bytes_moved = 0;      // model: CPU -> GPU bytes (estimate_cost)
+    double est_downtime_s = 0.0;  // model: bytes_moved / transfer bandwidth
+    bytes_t bytes_h2d = 0;        // measured: bytes copied host -> device
+    double measured_s = 0.0;      // measured: wall time of the executed action list (synchronised)
 };
 
 class MoeEngine {
@@ -58,6 +71,16 @@ class MoeEngine {
     // Eager step with CUDA events around every layer's expert FFN (see
     // engine.cpp); ffn_ms / ffn_bytes have num_layers entries.
     void profile_step(int T, float* ffn_ms, int64_t* ffn_bytes, int* kernels_per_step);
+
+    // Executes diff_plans(current plan, target) on the device (SURVEY.md §8f
+    // f1): Offload releases the device copy (the expert streams from its host
+    // copy afterwards), Fetch copies the host copy at the target precision
+    // into HBM, Quantize of a device-resident expert runs the int4-g128
+    // quantiser on the device, Dequantize of one pulls its 16-bit master.
+    // The replay is checked as apply() does; decode after it is bit-identical
+    // to an engine built with `target`.  Needs keep_masters.
+    ReconfigReport reconfigure(const PlacementPlan& target, const HardwareProfile& hw);
+    const PlacementPlan& plan() const;
 
     GatingTrace last_routing(int T);
     const SimReport& counters() const;

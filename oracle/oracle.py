@@ -265,6 +265,8 @@ class RefLib:
             "ref_expected_throughput": (D, [PR, D, VP, VP, I64]),
             "ref_diff_plans": (I, [PR, D, VP, VP, VP, VP, VP, VP, I, P(I64), P(D)]),
             "ref_have_serialize": (I, []),
+            "ref_reconfig_diff": (I, [PR, D, VP, VP, VP, VP, U64, VP, I, P(I64), P(D)]),
+            "ref_reconfig_apply": (I, [PR, VP, VP, U64, VP, I, U64, I64, VP, VP, P(I64), P(U64)]),
             "ref_builtin_anchors": (I, [C.c_char_p, P(D), P(D)]),
             "ref_load_anchors": (I, [C.c_char_p, P(D), P(D)]),
             "ref_ppl_estimate": (I, [I, D, D, I, P(D)]),
@@ -357,6 +359,29 @@ class RefLib:
         out = np.zeros(max(len(t), 1), np.int32)
         st = self.L.ref_frontier_mask(len(t), t.ctypes.data, q.ctypes.data, g.ctypes.data, out.ctypes.data)
         return st, out[:len(t)].astype(bool)
+
+    def reconfig_diff(self, p, bw, prec_a, loc_a, prec_b, loc_b, seed_b=0):
+        """diff_plans (reconfig.cpp:19-55): (status, [(kind, layer, slot, tprec, tloc)], bytes, downtime)."""
+        arrs = [np.ascontiguousarray(v, np.int32) for v in (prec_a, loc_a, prec_b, loc_b)]
+        cap = 4 * len(arrs[0]) + 4
+        acts = np.zeros(5 * cap, np.int32)
+        b, t = C.c_int64(), C.c_double()
+        n = self.L.ref_reconfig_diff(C.byref(self.profile(p)), bw, *[_np_ptr(a) for a in arrs], seed_b, _np_ptr(acts),
+                                     cap, C.byref(b), C.byref(t))
+        if n < 0:
+            return -n, None, None, None
+        return 0, [tuple(int(v) for v in acts[5 * i:5 * i + 5]) for i in range(n)], b.value, t.value
+
+    def reconfig_apply(self, p, prec, loc, seed, actions, target_seed, budget=0):
+        """apply (reconfig.cpp:84-168): (status, prec, loc, swap, seed)."""
+        n = p.num_layers * p.experts_per_layer
+        a = np.ascontiguousarray(np.array(actions, np.int32).reshape(-1), np.int32) if actions else np.zeros(5, np.int32)
+        op, ol = np.zeros(n, np.int32), np.zeros(n, np.int32)
+        sw, sd = C.c_int64(), C.c_uint64()
+        st = self.L.ref_reconfig_apply(C.byref(self.profile(p)), _np_ptr(np.ascontiguousarray(prec, np.int32)),
+                                       _np_ptr(np.ascontiguousarray(loc, np.int32)), seed, _np_ptr(a), len(actions),
+                                       target_seed, budget, _np_ptr(op), _np_ptr(ol), C.byref(sw), C.byref(sd))
+        return st, op, ol, sw.value, sd.value
 
     @property
     def has_serialize(self) -> bool:

@@ -285,6 +285,60 @@ int ref_diff_plans(const ref_profile* p, double bw, const int32_t* prec_a, const
     return st == 0 ? n : -st;
 }
 
+// Full action lists: 5 int32 per action (kind, layer, slot, target precision
+// 0 P4 / 1 P16, target location 0 GPU / 1 CPU).
+int ref_reconfig_diff(const ref_profile* p, double bw, const int32_t* prec_a, const int32_t* loc_a,
+                      const int32_t* prec_b, const int32_t* loc_b, uint64_t seed_b, int32_t* acts, int cap,
+                      int64_t* bytes, double* downtime) {
+    int n = -1;
+    const int st = guarded([&] {
+        const ModelProfile m = to_model(p);
+        const auto a = to_plan(prec_a, loc_a, m.num_experts(), 0, 0);
+        const auto b = to_plan(prec_b, loc_b, m.num_experts(), 0, seed_b);
+        const ReconfigPlan rp = diff_plans(a, b, m, to_hw(1, bw));
+        n = static_cast<int>(rp.actions.size());
+        for (int i = 0; i < n && i < cap; ++i) {
+            const ReconfigAction& x = rp.actions[static_cast<size_t>(i)];
+            acts[5 * i + 0] = static_cast<int32_t>(x.kind);
+            acts[5 * i + 1] = x.expert.layer;
+            acts[5 * i + 2] = x.expert.slot;
+            acts[5 * i + 3] = x.target_precision == Precision::P4 ? 0 : 1;
+            acts[5 * i + 4] = x.target_location == Location::GPU ? 0 : 1;
+        }
+        *bytes = rp.bytes_moved;
+        *downtime = rp.est_downtime_s;
+    });
+    return st == 0 ? n : -st;
+}
+
+int ref_reconfig_apply(const ref_profile* p, const int32_t* prec, const int32_t* loc, uint64_t seed,
+                       const int32_t* acts, int n, uint64_t target_seed, int64_t budget, int32_t* out_prec,
+                       int32_t* out_loc, int64_t* out_swap, uint64_t* out_seed) {
+    return guarded([&] {
+        const ModelProfile m = to_model(p);
+        PlacementPlan plan = to_plan(prec, loc, m.num_experts(), 0, seed);
+        plan.swap_slot_bytes = required_swap_bytes(plan, m);
+        ReconfigPlan rp;
+        rp.target_seed = target_seed;
+        for (int i = 0; i < n; ++i) {
+            ReconfigAction a;
+            a.kind = static_cast<ActionKind>(acts[5 * i]);
+            a.expert = ExpertId{acts[5 * i + 1], acts[5 * i + 2]};
+            a.target_precision = acts[5 * i + 3] == 0 ? Precision::P4 : Precision::P16;
+            a.target_location = acts[5 * i + 4] == 0 ? Location::GPU : Location::CPU;
+            rp.actions.push_back(a);
+        }
+        const HardwareProfile hw = to_hw(budget, 1.0);
+        const PlacementPlan r = apply(plan, rp, m, budget > 0 ? &hw : nullptr);
+        for (size_t i = 0; i < r.entries.size(); ++i) {
+            out_prec[i] = r.entries[i].precision == Precision::P4 ? 0 : 1;
+            out_loc[i] = r.entries[i].location == Location::GPU ? 0 : 1;
+        }
+        *out_swap = r.swap_slot_bytes;
+        *out_seed = r.seed;
+    });
+}
+
 // ---- pareto (same row layout as moe_pareto_row in include/moe_b200.h)
 struct ref_pareto_row {
     int64_t budget;

@@ -77,6 +77,16 @@ class ParetoRowC(C.Structure):
                 ("n_gpu", C.c_int32), ("gpu_bytes", C.c_int64), ("ppl", C.c_double), ("report", SimReportC)]
 
 
+class ReconfigActionC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("layer", C.c_int32), ("slot", C.c_int32), ("target_precision", C.c_int32),
+                ("target_location", C.c_int32), ("pad_", C.c_int32)]
+
+
+class ReconfigReportC(C.Structure):
+    _fields_ = [("actions", C.c_int32), ("pad_", C.c_int32), ("bytes_moved", C.c_int64), ("est_downtime_s", C.c_double),
+                ("bytes_h2d", C.c_int64), ("measured_s", C.c_double)]
+
+
 class ExpertWeightsC(C.Structure):
     _fields_ = [("precision", C.c_int32), ("pad_", C.c_int32), ("w_gate_up", C.c_void_p),
                 ("s_gate_up", C.c_void_p), ("w_down", C.c_void_p), ("s_down", C.c_void_p)]
@@ -86,7 +96,7 @@ class _EngineConfig(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("experts_per_layer", C.c_int32), ("top_k", C.c_int32),
                 ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("max_tokens", C.c_int32),
                 ("seed", C.c_uint64), ("device", C.c_int32), ("use_graphs", C.c_int32), ("norm_eps", C.c_float),
-                ("tc_min_tokens", C.c_int32), ("lru_capacity", C.c_int32), ("pad2_", C.c_int32)]
+                ("tc_min_tokens", C.c_int32), ("lru_capacity", C.c_int32), ("keep_masters", C.c_int32)]
 
 
 _lib = None
@@ -123,6 +133,11 @@ def lib() -> C.CDLL:
         "moe_read_trace": (I, [C.c_char_p, P(C.c_int32), P(U64), P(C.c_int32), I64]),
         "moe_simulate": (I, [P(ExpertStateC), I64, P(C.c_int32), I, P(_ModelProfile), P(_HardwareProfile), I, P(SimReportC)]),
         "moe_expected_throughput": (D, [P(ExpertStateC), P(_ModelProfile), P(_HardwareProfile)]),
+        "moe_diff_plans": (I, [P(ExpertStateC), P(ExpertStateC), U64, P(_ModelProfile), P(_HardwareProfile),
+                               P(ReconfigActionC), I, P(I), P(I64), P(D)]),
+        "moe_apply_reconfig": (I, [P(ExpertStateC), U64, P(ReconfigActionC), I, U64, P(_ModelProfile),
+                                   P(_HardwareProfile), P(ExpertStateC), P(I64), P(U64)]),
+        "moe_engine_reconfigure": (I, [VP, P(ExpertStateC), U64, D, P(ReconfigReportC)]),
         "moe_builtin_anchors": (I, [C.c_char_p, P(D), P(D)]),
         "moe_load_anchors": (I, [C.c_char_p, P(D), P(D)]),
         "moe_ppl_estimate": (I, [I, D, D, I, P(D)]),
@@ -440,6 +455,34 @@ def expected_throughput(plan: PlacementPlan, profile: ModelProfile, hw: Hardware
     return lib().moe_expected_throughput(plan._entries(), C.byref(profile._c()), C.byref(hw._c()))
 
 
+# ----------------------------------------------------------------- reconfiguration (f1)
+OFFLOAD, FETCH, QUANTIZE, DEQUANTIZE = 0, 1, 2, 3
+
+
+def diff_plans(src: PlacementPlan, dst: PlacementPlan, profile: ModelProfile, hw: HardwareProfile):
+    """reconfig.cpp:19-55: ([(kind, layer, slot, target_precision, target_location)], bytes_moved, est_downtime_s)."""
+    n = profile.num_experts
+    cap = 2 * n
+    acts = (ReconfigActionC * cap)()
+    cnt, b, t = C.c_int(), C.c_int64(), C.c_double()
+    _check(lib().moe_diff_plans(src._entries(), dst._entries(), dst.seed, C.byref(profile._c()), C.byref(hw._c()), acts,
+                                cap, C.byref(cnt), C.byref(b), C.byref(t)))
+    return ([(a.kind, a.layer, a.slot, a.target_precision, a.target_location) for a in acts[:cnt.value]], b.value,
+            t.value)
+
+
+def apply_reconfig(plan: PlacementPlan, actions, target_seed: int, profile: ModelProfile,
+                   budget: HardwareProfile = None) -> PlacementPlan:
+    """reconfig.cpp:84-168: checked replay of an action list."""
+    acts = (ReconfigActionC * max(len(actions), 1))(*[ReconfigActionC(*a, 0) for a in actions])
+    out = (ExpertStateC * profile.num_experts)()
+    sw, sd = C.c_int64(), C.c_uint64()
+    _check(lib().moe_apply_reconfig(plan._entries(), plan.seed, acts, len(actions), target_seed, C.byref(profile._c()),
+                                    C.byref(budget._c()) if budget is not None else None, out, C.byref(sw),
+                                    C.byref(sd)))
+    return PlacementPlan([a.precision for a in out], [a.location for a in out], sw.value, sd.value)
+
+
 # ----------------------------------------------------------------- pareto (f3)
 @dataclass
 class QualityAnchors:
@@ -631,12 +674,13 @@ class MoeEngine:
 
     def __init__(self, num_layers: int, experts_per_layer: int, top_k: int, d_model: int, d_ffn: int,
                  plan: PlacementPlan, max_tokens: int = 1, seed: int = 0, device: int = 0,
-                 use_graphs: bool = True, norm_eps: float = 0.0, tc_min_tokens: int = 0, lru_capacity: int = 0):
+                 use_graphs: bool = True, norm_eps: float = 0.0, tc_min_tokens: int = 0, lru_capacity: int = 0,
+                 keep_masters: bool = False):
         self.L, self.E, self.k, self.d, self.f = num_layers, experts_per_layer, top_k, d_model, d_ffn
         self.max_tokens = max_tokens
         self.norm_eps = norm_eps
         cfg = _EngineConfig(num_layers, experts_per_layer, top_k, d_model, d_ffn, max_tokens, seed, device,
-                            1 if use_graphs else 0, norm_eps, tc_min_tokens, lru_capacity, 0)
+                            1 if use_graphs else 0, norm_eps, tc_min_tokens, lru_capacity, 1 if keep_masters else 0)
         h = C.c_void_p()
         _check(lib().moe_engine_create(C.byref(cfg), plan._entries(), C.byref(h)))
         self._h = h
@@ -694,6 +738,14 @@ class MoeEngine:
         kps = C.c_int32()
         _check(lib().moe_engine_profile_step(self._h, T, ms, by, C.byref(kps)))
         return list(ms), list(by), kps.value
+
+    def reconfigure(self, target: PlacementPlan, transfer_bw_bytes_per_s: float) -> dict:
+        """Execute diff_plans(current, target) on the device (needs keep_masters)."""
+        r = ReconfigReportC()
+        _check(lib().moe_engine_reconfigure(self._h, target._entries(), target.seed, transfer_bw_bytes_per_s,
+                                            C.byref(r)))
+        return {"actions": r.actions, "bytes_moved": r.bytes_moved, "est_downtime_s": r.est_downtime_s,
+                "bytes_h2d": r.bytes_h2d, "measured_s": r.measured_s}
 
     def last_routing(self, T: int) -> List[int]:
         n = T * self.L * self.k

@@ -13,6 +13,7 @@
 #include "kernels/launch.h"
 #include "moe_b200.h"
 #include "moeb200/engine.hpp"
+#include "moeb200/reconfig.hpp"
 #include "moeb200/pareto.hpp"
 
 using namespace moeb200;
@@ -337,6 +338,65 @@ double moe_expected_throughput(const moe_expert_state* entries, const moe_model_
 
 namespace {
 
+ReconfigPlan to_reconfig(const moe_reconfig_action* acts, int n, uint64_t target_seed) {
+    ReconfigPlan rp;
+    rp.target_seed = target_seed;
+    for (int i = 0; i < n; ++i) {
+        const moe_reconfig_action& c = acts[i];
+        usage_if(c.kind < 0 || c.kind > 3, "unknown action kind");
+        ReconfigAction a;
+        a.kind = static_cast<ActionKind>(c.kind);
+        a.expert = ExpertId{c.layer, c.slot};
+        a.target_precision = c.target_precision == MOE_P4 ? Precision::P4 : Precision::P16;
+        a.target_location = c.target_location == MOE_GPU ? Location::GPU : Location::CPU;
+        rp.actions.push_back(a);
+    }
+    return rp;
+}
+
+}  // namespace
+
+int moe_diff_plans(const moe_expert_state* from, const moe_expert_state* to, uint64_t to_seed,
+                   const moe_model_profile* p, const moe_hardware_profile* hw, moe_reconfig_action* actions,
+                   int cap, int* n_actions, int64_t* bytes_moved, double* est_downtime_s) {
+    return guarded([&] {
+        usage_if(from == nullptr || to == nullptr || n_actions == nullptr, "null argument");
+        const ModelProfile m = to_model(p);
+        const PlacementPlan a = to_plan(from, m.num_experts(), 0);
+        PlacementPlan b = to_plan(to, m.num_experts(), 0);
+        b.seed = to_seed;
+        const ReconfigPlan rp = diff_plans(a, b, m, to_hw(hw));
+        *n_actions = static_cast<int>(rp.actions.size());
+        for (int i = 0; i < *n_actions && i < cap && actions; ++i) {
+            const ReconfigAction& x = rp.actions[static_cast<size_t>(i)];
+            actions[i] = {static_cast<int32_t>(x.kind), x.expert.layer, x.expert.slot,
+                          x.target_precision == Precision::P4 ? MOE_P4 : MOE_P16,
+                          x.target_location == Location::GPU ? MOE_GPU : MOE_CPU, 0};
+        }
+        if (bytes_moved) *bytes_moved = rp.bytes_moved;
+        if (est_downtime_s) *est_downtime_s = rp.est_downtime_s;
+    });
+}
+
+int moe_apply_reconfig(const moe_expert_state* plan, uint64_t plan_seed, const moe_reconfig_action* actions,
+                       int n_actions, uint64_t target_seed, const moe_model_profile* p,
+                       const moe_hardware_profile* budget, moe_expert_state* out, int64_t* out_swap,
+                       uint64_t* out_seed) {
+    return guarded([&] {
+        usage_if(plan == nullptr || out == nullptr || (n_actions > 0 && actions == nullptr), "null argument");
+        const ModelProfile m = to_model(p);
+        PlacementPlan pl = to_plan(plan, m.num_experts(), 0);
+        pl.swap_slot_bytes = required_swap_bytes(pl, m);
+        pl.seed = plan_seed;
+        const HardwareProfile hb = budget ? to_hw(budget) : HardwareProfile{};
+        const PlacementPlan r = apply(pl, to_reconfig(actions, n_actions, target_seed), m, budget ? &hb : nullptr);
+        from_plan(r, out, out_swap);
+        if (out_seed) *out_seed = r.seed;
+    });
+}
+
+namespace {
+
 QualityAnchors anchors_of(double p16, double p4) { return QualityAnchors{"", p16, p4}; }
 
 void to_c_report(const SimReport& r, moe_sim_report* out) {
@@ -652,6 +712,7 @@ int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan
         ec.tc_min_tokens = cfg->tc_min_tokens > 0 ? cfg->tc_min_tokens : 64;
         usage_if(cfg->lru_capacity < 0, "lru_capacity must be >= 0");
         ec.lru_capacity = cfg->lru_capacity;
+        ec.keep_masters = cfg->keep_masters != 0;
         const int n = cfg->num_layers * cfg->experts_per_layer;
         PlacementPlan plan = to_plan(plan_entries, n, 0);
         plan.swap_slot_bytes = required_swap_bytes(plan, ec.profile);
@@ -708,6 +769,21 @@ int moe_engine_last_routing(moe_engine* eng, int T, int32_t* slots_out) {
     return guarded([&] {
         const GatingTrace tr = eng->impl->last_routing(T);
         std::memcpy(slots_out, tr.slots.data(), tr.slots.size() * 4);
+    });
+}
+
+int moe_engine_reconfigure(moe_engine* eng, const moe_expert_state* target, uint64_t target_seed,
+                           double transfer_bw_bytes_per_s, moe_reconfig_report* out) {
+    return guarded([&] {
+        usage_if(eng == nullptr || target == nullptr, "null argument");
+        usage_if(!(transfer_bw_bytes_per_s > 0.0), "transfer bandwidth must be > 0");
+        const PlacementPlan& cur = eng->impl->plan();
+        PlacementPlan t = to_plan(target, static_cast<int>(cur.entries.size()), 0);
+        t.seed = target_seed;
+        HardwareProfile hw;
+        hw.transfer_bw_bytes_per_s = transfer_bw_bytes_per_s;
+        const ReconfigReport r = eng->impl->reconfigure(t, hw);
+        if (out) *out = {r.actions, 0, r.bytes_moved, r.est_downtime_s, r.bytes_h2d, r.measured_s};
     });
 }
 

@@ -90,6 +90,15 @@ struct MoeEngine::Impl {
     uint16_t* wg = nullptr;  // [L][E][d]
 
     std::vector<moe_expert_weights> weights;  // [L*E]
+    // keep_masters: pinned [L*E][bf16 blocks | int4 blocks]; reconfigure()'s
+    // device copies are per-expert allocations (`owned`), freed on release
+    char* master_arena = nullptr;
+    size_t master_stride = 0;
+    std::vector<char*> owned;                 // [L*E]
+    char* host_copy(int e, Precision p) const {
+        char* b = master_arena + static_cast<size_t>(e) * master_stride;
+        return p == Precision::P16 ? b : b + align_up(size16, 256);
+    }
     std::vector<int> location;                // [L*E]
     std::vector<char> layer_has_cpu;
 
@@ -186,8 +195,10 @@ struct MoeEngine::Impl {
                 off[static_cast<size_t>(i)] = dev_bytes;
                 dev_bytes += align_up(sz, 256);
             } else {
-                off[static_cast<size_t>(i)] = host_bytes;
-                host_bytes += align_up(sz, 256);
+                if (!c.keep_masters) {
+                    off[static_cast<size_t>(i)] = host_bytes;
+                    host_bytes += align_up(sz, 256);
+                }
                 layer_has_cpu[static_cast<size_t>(i / E)] = 1;
                 location[static_cast<size_t>(i)] = MOE_CPU;
                 swap_need = std::max(swap_need, sz);
@@ -197,12 +208,20 @@ struct MoeEngine::Impl {
             throw ValidationError("plan swap_slot_bytes smaller than the largest CPU-resident expert");
         if (dev_bytes) ck(cudaMalloc(&dev_arena, dev_bytes), "cudaMalloc(expert arena)");
         if (host_bytes) ck(cudaHostAlloc(&host_arena, host_bytes, cudaHostAllocDefault), "cudaHostAlloc(host arena)");
+        owned.assign(static_cast<size_t>(L * E), nullptr);
+        if (c.keep_masters) {
+            master_stride = align_up(size16, 256) + align_up(size4, 256);
+            ck(cudaHostAlloc(&master_arena, master_stride * static_cast<size_t>(L * E), cudaHostAllocDefault),
+               "cudaHostAlloc(master copies)");
+        }
         swap_bytes = static_cast<size_t>(plan.swap_slot_bytes);
         if (swap_bytes) ck(cudaMalloc(&swap, swap_bytes * static_cast<size_t>(nslots)), "cudaMalloc(swap slots)");
         weights.resize(static_cast<size_t>(L * E));
         for (int i = 0; i < L * E; ++i) {
             const ExpertState st = plan.entries[static_cast<size_t>(i)];
-            char* base = (st.location == Location::GPU ? dev_arena : host_arena) + off[static_cast<size_t>(i)];
+            char* base = st.location == Location::GPU ? dev_arena + off[static_cast<size_t>(i)]
+                         : c.keep_masters              ? host_copy(i, st.precision)
+                                                       : host_arena + off[static_cast<size_t>(i)];
             weights[static_cast<size_t>(i)] = view(base, st.precision);
         }
 
@@ -251,7 +270,7 @@ struct MoeEngine::Impl {
         char* master = nullptr;
         char* stage = nullptr;
         ck(cudaMalloc(&master, size16), "cudaMalloc(master)");
-        if (host_bytes) ck(cudaMalloc(&stage, size16), "cudaMalloc(stage)");
+        if (host_bytes || master_arena) ck(cudaMalloc(&stage, size16), "cudaMalloc(stage)");
         for (int e = 0; e < L * E; ++e) {
             const ExpertState st = plan.entries[static_cast<size_t>(e)];
             ck(moek_synth_weight(cfg.seed, uid_expert(e, 1), static_cast<long long>(2 * fd), sh_gu, master, compute), "synth");
@@ -268,7 +287,30 @@ struct MoeEngine::Impl {
                 ck(moek_quantize_blocks(master + 4 * fd, d, f, static_cast<uint32_t*>(const_cast<void*>(v.w_down)),
                                         const_cast<void*>(v.s_down), compute), "quantize");
             }
-            if (st.location == Location::CPU) {
+            if (master_arena) {
+                // both host copies: the plan precision from dst first (dst may be
+                // stage), then the other one made in stage
+                const Precision other = st.precision == Precision::P16 ? Precision::P4 : Precision::P16;
+                for (Precision p : {st.precision, other}) {
+                    const size_t sz = p == Precision::P16 ? size16 : size4;
+                    const void* src = dst;
+                    if (p != st.precision) {
+                        moe_expert_weights o = view(stage, p);
+                        if (p == Precision::P16) {
+                            ck(moek_pack_bf16_blocks(master, 2 * f, d, const_cast<void*>(o.w_gate_up), compute), "pack");
+                            ck(moek_pack_bf16_blocks(master + 4 * fd, d, f, const_cast<void*>(o.w_down), compute), "pack");
+                        } else {
+                            ck(moek_quantize_blocks(master, 2 * f, d, static_cast<uint32_t*>(const_cast<void*>(o.w_gate_up)),
+                                                    const_cast<void*>(o.s_gate_up), compute), "quantize");
+                            ck(moek_quantize_blocks(master + 4 * fd, d, f, static_cast<uint32_t*>(const_cast<void*>(o.w_down)),
+                                                    const_cast<void*>(o.s_down), compute), "quantize");
+                        }
+                        src = stage;
+                    }
+                    ck(cudaMemcpyAsync(host_copy(e, p), src, sz, cudaMemcpyDeviceToHost, compute), "D2H master");
+                    ck(cudaStreamSynchronize(compute), "sync");  // stage reused
+                }
+            } else if (st.location == Location::CPU) {
                 const size_t sz = st.precision == Precision::P16 ? size16 : size4;
                 ck(cudaMemcpyAsync(const_cast<void*>(weights[static_cast<size_t>(e)].w_gate_up), stage, sz,
                                    cudaMemcpyDeviceToHost, compute), "D2H");
@@ -279,10 +321,134 @@ struct MoeEngine::Impl {
         if (stage) cudaFree(stage);
     }
 
+
+    // ---- reconfiguration executor (reconfig.hpp; MoeEngine::reconfigure) ----
+    void release_dev(int e) {
+        // per-expert copies made by reconfigure are freed; arena copies stay
+        // allocated (the arena is one block) until the engine is destroyed
+        char*& p = owned[static_cast<size_t>(e)];
+        if (p) ck(cudaFreeAsync(p, compute), "cudaFreeAsync");
+        p = nullptr;
+    }
+    char* dev_new(int e, size_t bytes) {
+        char* p = nullptr;
+        ck(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, compute), "cudaMallocAsync(expert)");
+        owned[static_cast<size_t>(e)] = p;
+        return p;
+    }
+
+    ReconfigReport reconfigure(const PlacementPlan& target, const HardwareProfile& hw) {
+        if (!master_arena)
+            throw UsageError("reconfigure needs keep_masters (host copies of every expert, reconfig.hpp:39)");
+        const ReconfigPlan rp = diff_plans(plan, target, cfg.profile, hw);
+        const PlacementPlan next = apply(plan, rp, cfg.profile);  // checked replay (state, exclusivity)
+        if (next.entries != target.entries) throw ValidationError("action list does not reach the target plan");
+        ck(cudaStreamSynchronize(compute), "sync");
+        ck(cudaStreamSynchronize(copy), "sync");
+        for (auto& g : graphs) cudaGraphExecDestroy(g.second);  // expert pointers change
+        graphs.clear();
+        ReconfigReport rep;
+        rep.actions = static_cast<int>(rp.actions.size());
+        rep.bytes_moved = rp.bytes_moved;
+        rep.est_downtime_s = rp.est_downtime_s;
+        const size_t fd = static_cast<size_t>(f) * d;
+        char* logical = nullptr;  // Quantize scratch: one expert's logical bf16 matrices
+        cudaEvent_t t0, t1;
+        ck(cudaEventCreate(&t0), "event");
+        ck(cudaEventCreate(&t1), "event");
+        ck(cudaEventRecord(t0, compute), "record");
+        std::vector<ExpertState> cur = plan.entries;
+        for (const ReconfigAction& a : rp.actions) {
+            const int e = expert_index(cfg.profile, a.expert);
+            ExpertState& st = cur[static_cast<size_t>(e)];
+            moe_expert_weights& w = weights[static_cast<size_t>(e)];
+            switch (a.kind) {
+                case ActionKind::Offload:  // nothing moves toward the GPU: the host copy takes over
+                    release_dev(e);
+                    st.location = Location::CPU;
+                    w = view(host_copy(e, st.precision), st.precision);
+                    break;
+                case ActionKind::Quantize:
+                    st.precision = Precision::P4;
+                    if (st.location == Location::GPU) {  // on-device int4-g128 from the 16-bit copy
+                        if (!logical) ck(cudaMallocAsync(reinterpret_cast<void**>(&logical), size16, compute), "cudaMallocAsync");
+                        ck(moek_unpack_bf16_blocks(w.w_gate_up, 2 * f, d, logical, compute), "unpack");
+                        ck(moek_unpack_bf16_blocks(w.w_down, d, f, logical + 4 * fd, compute), "unpack");
+                        char* prev = owned[static_cast<size_t>(e)];
+                        owned[static_cast<size_t>(e)] = nullptr;
+                        moe_expert_weights q = view(dev_new(e, size4), Precision::P4);
+                        ck(moek_quantize_blocks(logical, 2 * f, d, static_cast<uint32_t*>(const_cast<void*>(q.w_gate_up)),
+                                                const_cast<void*>(q.s_gate_up), compute), "quantize");
+                        ck(moek_quantize_blocks(logical + 4 * fd, d, f, static_cast<uint32_t*>(const_cast<void*>(q.w_down)),
+                                                const_cast<void*>(q.s_down), compute), "quantize");
+                        if (prev) ck(cudaFreeAsync(prev, compute), "cudaFreeAsync");
+                        w = q;
+                    } else {
+                        w = view(host_copy(e, Precision::P4), Precision::P4);
+                    }
+                    break;
+                case ActionKind::Dequantize:
+                    st.precision = Precision::P16;
+                    if (st.location == Location::GPU) {  // in-place upgrade: pull the 16-bit master
+                        char* prev = owned[static_cast<size_t>(e)];
+                        owned[static_cast<size_t>(e)] = nullptr;
+                        char* nb = dev_new(e, size16);
+                        ck(cudaMemcpyAsync(nb, host_copy(e, Precision::P16), size16, cudaMemcpyHostToDevice, compute), "H2D");
+                        rep.bytes_h2d += static_cast<bytes_t>(size16);
+                        if (prev) ck(cudaFreeAsync(prev, compute), "cudaFreeAsync");
+                        w = view(nb, Precision::P16);
+                    } else {
+                        w = view(host_copy(e, Precision::P16), Precision::P16);
+                    }
+                    break;
+                case ActionKind::Fetch: {  // the host copy at its (destination) precision
+                    st.location = Location::GPU;
+                    const size_t sz = st.precision == Precision::P16 ? size16 : size4;
+                    char* nb = dev_new(e, sz);
+                    ck(cudaMemcpyAsync(nb, host_copy(e, st.precision), sz, cudaMemcpyHostToDevice, compute), "H2D");
+                    rep.bytes_h2d += static_cast<bytes_t>(sz);
+                    w = view(nb, st.precision);
+                    break;
+                }
+            }
+        }
+        if (logical) ck(cudaFreeAsync(logical, compute), "cudaFreeAsync");
+        ck(cudaEventRecord(t1, compute), "record");
+        ck(cudaEventSynchronize(t1), "sync");
+        float ms = 0.0f;
+        ck(cudaEventElapsedTime(&ms, t0, t1), "elapsed");
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        rep.measured_s = ms / 1e3;
+        // the new plan: residency flags, swap slot(s), LRU state
+        plan = next;
+        layer_has_cpu.assign(static_cast<size_t>(L), 0);
+        for (int i = 0; i < L * E; ++i) {
+            const bool cpu = plan.entries[static_cast<size_t>(i)].location == Location::CPU;
+            location[static_cast<size_t>(i)] = cpu ? MOE_CPU : MOE_GPU;
+            if (cpu) layer_has_cpu[static_cast<size_t>(i / E)] = 1;
+        }
+        if (static_cast<size_t>(plan.swap_slot_bytes) > swap_bytes) {
+            if (swap) ck(cudaFree(swap), "cudaFree(swap)");
+            swap_bytes = static_cast<size_t>(plan.swap_slot_bytes);
+            ck(cudaMalloc(&swap, swap_bytes * static_cast<size_t>(nslots)), "cudaMalloc(swap slots)");
+        }
+        if (lru) {
+            lru->clear();
+            lru_pos.clear();
+            lru_slot_of.clear();
+        }
+        return rep;
+    }
+
     void destroy() {
         for (auto& g : graphs) cudaGraphExecDestroy(g.second);
         graphs.clear();
         if (compute) cudaStreamSynchronize(compute);
+        for (char* p : owned)
+            if (p) cudaFree(p);
+        owned.clear();
+        if (master_arena) cudaFreeHost(master_arena);
         if (copy) cudaStreamSynchronize(copy);
         void* devp[] = {tcws, xn, dev_arena, swap, wg, xin, xout, xbuf[0], xbuf[1], idx, wts, counts, offsets, perm, inv, ticket, y,
                          gws_base};
@@ -557,6 +723,12 @@ void MoeEngine::sync() { ck(cudaStreamSynchronize(impl_->compute), "sync"); }
 void MoeEngine::profile_step(int T, float* ffn_ms, int64_t* ffn_bytes, int* kernels_per_step) {
     impl_->profile_step(T, ffn_ms, ffn_bytes, kernels_per_step);
 }
+
+ReconfigReport MoeEngine::reconfigure(const PlacementPlan& target, const HardwareProfile& hw) {
+    return impl_->reconfigure(target, hw);
+}
+
+const PlacementPlan& MoeEngine::plan() const { return impl_->plan; }
 
 GatingTrace MoeEngine::last_routing(int T) {
     Impl& m = *impl_;

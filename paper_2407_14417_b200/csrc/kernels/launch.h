@@ -54,6 +54,8 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
                         const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask, float* y,
                         cudaStream_t stream);
 // Storage-layout converters (logical row-major -> fragment blocks).
+// fragment blocks -> logical row-major bf16 (inverse of moek_pack_bf16_blocks)
+cudaError_t moek_unpack_bf16_blocks(const void* in, int rows, int cols, void* w, cudaStream_t stream);
 cudaError_t moek_pack_bf16_blocks(const void* w, int rows, int cols, void* out, cudaStream_t stream);
 cudaError_t moek_quantize_blocks(const void* w, int rows, int cols, uint32_t* qb, void* sb,
                                  cudaStream_t stream);

@@ -124,6 +124,21 @@ __global__ void pack_bf16_blocks_kernel(const uint16_t* __restrict__ w, int rows
     }
 }
 
+// Inverse of pack_bf16_blocks_kernel: fragment blocks -> logical row-major.
+__global__ void unpack_bf16_blocks_kernel(const uint16_t* __restrict__ in, int rows, int cols,
+                                          uint16_t* __restrict__ w) {
+    const long long n = static_cast<long long>(rows) * cols;
+    const int G = cols / 128;
+    for (long long o = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; o < n;
+         o += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int row = static_cast<int>(o / cols), c = static_cast<int>(o - static_cast<long long>(row) * cols);
+        const int rt = row >> 4, rr = row & 15, gr = rr & 7, half = rr >> 3;
+        const int p = perm_pos(c & 127), r = p & 31, lane = gr * 4 + (p >> 5);
+        const size_t blk = static_cast<size_t>(rt) * G + (c >> 7);
+        w[o] = in[blk * 2048 + static_cast<size_t>(((r >> 2) * 32 + lane) * 8 + (((r >> 1) & 1) * 2 + half) * 2 + (r & 1))];
+    }
+}
+
 // int4-g128 RTN quantiser writing the block layout: one warp per (row,
 // 128-group).  Same arithmetic as orc_quantize_g128.
 __global__ void quantize_blocks_kernel(const uint16_t* __restrict__ w, int rows, int cols,
@@ -247,6 +262,16 @@ cudaError_t moek_pack_bf16_blocks(const void* w, int rows, int cols, void* out, 
     if (blocks > 148 * 64) blocks = 148 * 64;
     moek::pack_bf16_blocks_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
         static_cast<const uint16_t*>(w), rows, cols, static_cast<uint16_t*>(out));
+    return cudaGetLastError();
+}
+
+cudaError_t moek_unpack_bf16_blocks(const void* in, int rows, int cols, void* w, cudaStream_t stream) {
+    const long long n = static_cast<long long>(rows) * cols;
+    if (n == 0) return cudaSuccess;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    moek::unpack_bf16_blocks_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        static_cast<const uint16_t*>(in), rows, cols, static_cast<uint16_t*>(w));
     return cudaGetLastError();
 }
 

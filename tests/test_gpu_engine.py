@@ -322,3 +322,52 @@ def test_measured_pareto_sweep_tiny(moe, cuda):
             assert 0.0 <= m[1] <= 1.0
     doc = moe.pareto_csv(rows, meas)
     assert len(doc.splitlines()) == 5 and ",-,-" not in doc
+
+
+@pytest.mark.parametrize("graphs", [True, False])
+def test_reconfigure_executor_bit_identical(moe, torch_mod, cuda, graphs):
+    """f1: reconfigure A -> B -> C on the device; every decode after a
+    reconfiguration is bit-identical to a fresh engine built with that plan,
+    the measured H2D bytes equal the model's bytes_moved, and the counters
+    equal simulate() on the new plan."""
+    torch = torch_mod
+    prof = moe.profile_for_shape(512, 1792, 2)
+    s16, s4 = moe.expert_size(prof, 1), moe.expert_size(prof, 0)
+    full = 16 * s16 + 1
+    plans = [moe.make_plan(moe.TaskRequest(moe.QUALITY, 4, 1), moe.HardwareProfile(full), prof),
+             moe.make_plan(moe.TaskRequest(moe.QUALITY, 12, 2), moe.HardwareProfile(4 * s16 + 2 * s4 + 1), prof),
+             moe.make_plan(moe.TaskRequest(moe.QUALITY, 2, 3), moe.HardwareProfile(9 * s16 + 1), prof),
+             moe.make_plan(moe.TaskRequest(moe.QUALITY, 4, 1), moe.HardwareProfile(full), prof)]
+    kinds = set()
+    eng = moe.MoeEngine(2, 8, 2, 512, 1792, plans[0], max_tokens=2, seed=21, use_graphs=graphs, norm_eps=1e-5,
+                        keep_masters=True)
+    for i, target in enumerate(plans[1:], 1):
+        acts, nbytes, _ = moe.diff_plans(plans[i - 1], target, prof, moe.HardwareProfile(1))
+        kinds |= {a[0] for a in acts}
+        rep = eng.reconfigure(target, 50e9)
+        assert rep["actions"] == len(acts) and rep["bytes_moved"] == nbytes and rep["bytes_h2d"] == nbytes
+        fresh = moe.MoeEngine(2, 8, 2, 512, 1792, target, max_tokens=2, seed=21, use_graphs=graphs, norm_eps=1e-5)
+        eng.reset_counters()
+        trace = []
+        for step in range(6):
+            for e in (eng, fresh):
+                e.synth_input(step, 2)
+                e.decode(2)
+                e.sync()
+            assert np.array_equal(read_device(torch, eng.output_ptr, 2 * 512), read_device(torch, fresh.output_ptr, 2 * 512))
+            trace.extend(eng.last_routing(2))
+        c = eng.counters()
+        sim = moe.simulate(target, trace, 12, prof, moe.HardwareProfile(1))
+        assert (c.activations, c.hits, c.bytes_transferred) == (sim.activations, sim.hits, sim.bytes_transferred)
+        fresh.close()
+    assert kinds == {moe.OFFLOAD, moe.FETCH, moe.QUANTIZE, moe.DEQUANTIZE}
+    eng.close()
+
+
+def test_reconfigure_needs_masters(moe, cuda):
+    prof = moe.profile_for_shape(512, 1792, 2)
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, 4, 1), moe.HardwareProfile(10**15), prof)
+    eng = moe.MoeEngine(2, 8, 2, 512, 1792, plan, seed=1)
+    with pytest.raises(moe.UsageError):
+        eng.reconfigure(plan, 50e9)
+    eng.close()
