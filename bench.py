@@ -331,6 +331,11 @@ def run_ours(args, rank, world, device):
     if args.host_split and rank == 0:
         host_split = host_split_sweep(moe, torch, prof, args, device)
 
+    # ---- f1: reconfiguration executor (plan -> plan on the device) ----
+    reconfig = None
+    if args.reconfig and rank == 0:
+        reconfig = reconfig_sweep(moe, torch, args, device)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tps, cores, sample = cpu_port_tokens_per_s(plan.precision[:EXPERTS], T, seconds=args.cpu_seconds)
@@ -366,6 +371,7 @@ def run_ours(args, rank, world, device):
             "sweep": sweep,
             "batch_sweep": batch,
             "host_split": host_split,
+            "reconfig": reconfig,
             "prefill_tcgen05": {"points": prefill, "peak_tflops": _peak_tflops(),
                                 "peak_kind": "MEASURED_PEAKS bf16_tflops (burst)",
                                 "flops": "6*d*f*T*k (gate/up + down, top-k=2)",
@@ -450,6 +456,47 @@ def host_split_sweep(moe, torch, prof, args, device):
             "policies": "static = single swap slot re-streamed per activation (planner.cpp:108, simulator.cpp:98-106); "
                         "lru = LRU cache of lru_slots device slots (simulator.cpp:37-62)",
             "steps_per_point": args.host_split_steps, "points": rows}
+
+
+def reconfig_sweep(moe, torch, args, device):
+    """MoeEngine.reconfigure between placement plans of a
+    Mixtral-shaped stack of args.reconfig_layers layers (host copies of every
+    expert in both precisions -- the reconfig model's CPU masters).  Per
+    transition: the action list of diff_plans, the model's bytes_moved and
+    est_downtime_s at the measured pinned H2D bandwidth, and the measured
+    device time of the executed list; then one decode step checks the engine
+    still runs."""
+    L = args.reconfig_layers
+    prof = moe.profile_for_shape(D_MODEL, D_FFN, L, EXPERTS, TOPK)
+    s16, s4 = moe.expert_size(prof, 1), moe.expert_size(prof, 0)
+    n = L * EXPERTS
+    bw = h2d_gbs(torch, device) * 1e9
+    full = n * s16 + 1
+    steps = [("n4=0 resident", 0, full), ("n4=half, 1/2 of the experts' bytes", n // 2, n * (s16 + s4) // 4),
+             ("n4=all resident", n, full), ("n4=0 resident", 0, full)]
+    plans = [moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 7), moe.HardwareProfile(b, bw), prof) for _, n4, b in steps]
+    eng = moe.MoeEngine(L, EXPERTS, TOPK, D_MODEL, D_FFN, plans[0], max_tokens=1, seed=args.seed, device=device,
+                        norm_eps=NORM_EPS, keep_masters=True)
+    rows = []
+    for i in range(1, len(plans)):
+        acts, _, _ = moe.diff_plans(plans[i - 1], plans[i], prof, moe.HardwareProfile(1, bw))
+        kinds = {}
+        for k, *_ in acts:
+            name = ("offload", "fetch", "quantize", "dequantize")[k]
+            kinds[name] = kinds.get(name, 0) + 1
+        r = eng.reconfigure(plans[i], bw)
+        eng.synth_input(0, 1)
+        eng.decode(1)
+        eng.sync()
+        rows.append({"from": steps[i - 1][0], "to": steps[i][0], "experts_on_gpu": plans[i].n_gpu, "actions": kinds,
+                     "bytes_moved": r["bytes_moved"], "bytes_h2d": r["bytes_h2d"],
+                     "est_downtime_s": round(r["est_downtime_s"], 5), "measured_s": round(r["measured_s"], 5),
+                     "measured_over_est": round(r["measured_s"] / r["est_downtime_s"], 3) if r["est_downtime_s"] else None})
+    eng.close()
+    return {"layers": L, "experts": n, "h2d_gbs_measured": round(bw / 1e9, 1),
+            "model": "reconfig.cpp:57-82 (CPU->GPU bytes / transfer bw); Quantize of a resident expert runs the "
+                     "int4-g128 quantiser on the device (not in the model's bytes)",
+            "transitions": rows}
 
 
 def run_ep(args, rank, world, device):
@@ -560,6 +607,8 @@ def main():
                     default=[1.0, 0.75, 0.5, 0.25, 0.0])
     ap.add_argument("--host-split-steps", type=int, default=4)
     ap.add_argument("--host-split-lru", type=int, default=16, help="LRU device slots for the host-split LRU column")
+    ap.add_argument("--no-reconfig", dest="reconfig", action="store_false")
+    ap.add_argument("--reconfig-layers", type=int, default=4, help="Mixtral-shaped layers of the reconfig stack")
     ap.add_argument("--prefill-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],
                     default=[512, 2048, 4096])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -3,7 +3,7 @@ cd $GRAFT_REPO_ROOT
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
 timeout 1500 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench.log | cut -c1-400
-Q="--no-sweep --no-batch-sweep --no-prefill --no-host-split --no-cpu-baseline"
+Q="--no-sweep --no-batch-sweep --no-prefill --no-host-split --no-reconfig --no-cpu-baseline"
 K='regex:route|stream_kernel|finalize|permute_rows|tc_ffn|to_f16|combine|residual'
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -s 330 -c 330 --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 $Q > gpurun_out/ncu_launch.log 2>&1; echo "ncu list rc=$?"
