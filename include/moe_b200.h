@@ -142,6 +142,18 @@ int moe_apply_reconfig(const moe_expert_state* plan, uint64_t plan_seed, const m
                        const moe_hardware_profile* budget, moe_expert_state* out, int64_t* out_swap,
                        uint64_t* out_seed);
 
+/* moeserve.reconfig.v1 (serialize.cpp:160-206).  write: bytes_moved and
+ * est_downtime_s are recomputed from the actions at hw (estimate_cost); returns
+ * the length (see moe_write_plan).  read: as the reference (format ->
+ * ParseError, fingerprint / bounds / stored bytes_moved -> ValidationError). */
+int64_t moe_write_reconfig(const moe_reconfig_action* actions, int n_actions, uint64_t target_seed,
+                           const moe_model_profile* p, const moe_hardware_profile* hw, char* buf, int64_t cap);
+int moe_read_reconfig(const char* document, const moe_model_profile* p, const moe_hardware_profile* hw,
+                      moe_reconfig_action* actions, int cap, int* n_actions, uint64_t* target_seed,
+                      int64_t* bytes_moved, double* est_downtime_s);
+/* SimReport as the reference's one-row CSV / JSON (serialize.cpp:218-243). */
+int64_t moe_report_text(const moe_sim_report* r, int json, char* buf, int64_t cap);
+
 /* Quality / memory / throughput sweep (pareto.hpp, cli.cpp:243-342).
  * Anchors: builtin name "wikitext2" | "ptb" | "c4" (Table 2), or an
  * INI document's [quality] section over a fallback (pareto.cpp:35-54). */

@@ -277,6 +277,9 @@ class RefLib:
         if L.ref_have_serialize():
             sig["ref_write_plan"] = (I64, [PR, VP, VP, U64, I64, C.c_char_p, I64])
             sig["ref_read_plan"] = (I, [C.c_char_p, PR, VP, VP, P(U64), P(I64)])
+            sig["ref_write_reconfig"] = (I64, [PR, D, VP, VP, VP, VP, U64, C.c_char_p, I64])
+            sig["ref_read_reconfig"] = (I, [C.c_char_p, PR, D, VP, I, P(I), P(U64), P(I64), P(D)])
+            sig["ref_report_text"] = (I64, [VP, I, C.c_char_p, I64])
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
             fn.restype, fn.argtypes = res, args
@@ -405,6 +408,34 @@ class RefLib:
         st = self.L.ref_read_plan(doc.encode(), C.byref(self.profile(p)), _np_ptr(prec), _np_ptr(loc),
                                   C.byref(seed), C.byref(swap))
         return st, prec, loc, seed.value, swap.value
+
+    def write_reconfig(self, p, bw, prec_a, loc_a, prec_b, loc_b, seed_b=0):
+        arrs = [np.ascontiguousarray(v, np.int32) for v in (prec_a, loc_a, prec_b, loc_b)]
+        args = [C.byref(self.profile(p)), bw] + [_np_ptr(a) for a in arrs] + [seed_b]
+        n = self.L.ref_write_reconfig(*args, None, 0)
+        if n < 0:
+            return int(-n), None
+        buf = C.create_string_buffer(int(n) + 1)
+        self.L.ref_write_reconfig(*args, buf, n + 1)
+        return 0, buf.value.decode()
+
+    def read_reconfig(self, doc, p, bw):
+        """(status, [(kind, layer, slot, tprec, tloc)], target_seed, bytes, downtime)."""
+        cap = 4 * p.num_layers * p.experts_per_layer + 8
+        acts = np.zeros(5 * cap, np.int32)
+        n, sd, b, t = C.c_int(), C.c_uint64(), C.c_int64(), C.c_double()
+        st = self.L.ref_read_reconfig(doc.encode(), C.byref(self.profile(p)), bw, _np_ptr(acts), cap, C.byref(n),
+                                      C.byref(sd), C.byref(b), C.byref(t))
+        if st:
+            return st, None, None, None, None
+        return 0, [tuple(int(v) for v in acts[5 * i:5 * i + 5]) for i in range(n.value)], sd.value, b.value, t.value
+
+    def report_text(self, counters, json=False):
+        c = np.ascontiguousarray(counters, np.int64)
+        n = self.L.ref_report_text(_np_ptr(c), 1 if json else 0, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        self.L.ref_report_text(_np_ptr(c), 1 if json else 0, buf, n + 1)
+        return buf.value.decode()
 
     def simulate(self, p, bw, prec, loc, swap, tokens, slots, lru=0):
         out = np.zeros(6, np.int64)

@@ -458,6 +458,60 @@ int ref_read_plan(const char* doc, const ref_profile* p, int32_t* prec, int32_t*
     });
 }
 
+// write_reconfig(diff_plans(a, b)) and read_reconfig; 5 int32 per action as
+// ref_reconfig_diff.
+int64_t ref_write_reconfig(const ref_profile* p, double bw, const int32_t* prec_a, const int32_t* loc_a,
+                           const int32_t* prec_b, const int32_t* loc_b, uint64_t seed_b, char* buf, int64_t cap) {
+    int64_t n = -1;
+    const int st = guarded([&] {
+        const ModelProfile m = to_model(p);
+        const ReconfigPlan rp = diff_plans(to_plan(prec_a, loc_a, m.num_experts(), 0, 0),
+                                           to_plan(prec_b, loc_b, m.num_experts(), 0, seed_b), m, to_hw(1, bw));
+        const std::string doc = write_reconfig(rp, m);
+        n = static_cast<int64_t>(doc.size());
+        if (buf != nullptr && n < cap) std::memcpy(buf, doc.c_str(), doc.size() + 1);
+    });
+    return st == 0 ? n : -st;
+}
+
+int ref_read_reconfig(const char* doc, const ref_profile* p, double bw, int32_t* acts, int cap, int* n,
+                      uint64_t* seed, int64_t* bytes, double* downtime) {
+    return guarded([&] {
+        const ReconfigPlan rp = read_reconfig(doc, to_model(p), to_hw(1, bw));
+        *n = static_cast<int>(rp.actions.size());
+        for (int i = 0; i < *n && i < cap; ++i) {
+            const ReconfigAction& x = rp.actions[static_cast<size_t>(i)];
+            acts[5 * i + 0] = static_cast<int32_t>(x.kind);
+            acts[5 * i + 1] = x.expert.layer;
+            acts[5 * i + 2] = x.expert.slot;
+            acts[5 * i + 3] = x.target_precision == Precision::P4 ? 0 : 1;
+            acts[5 * i + 4] = x.target_location == Location::GPU ? 0 : 1;
+        }
+        *seed = rp.target_seed;
+        *bytes = rp.bytes_moved;
+        *downtime = rp.est_downtime_s;
+    });
+}
+
+// report_csv / report_json of a SimReport given by its counters.
+int64_t ref_report_text(const int64_t* c, int json, char* buf, int64_t cap) {
+    int64_t n = -1;
+    const int st = guarded([&] {
+        SimReport r;
+        r.tokens = static_cast<int>(c[0]);
+        r.activations = c[1];
+        r.hits = c[2];
+        r.bytes_transferred = c[3];
+        r.transfer_ns = c[4];
+        r.compute_ns = c[5];
+        r.nonexpert_ns = c[6];
+        const std::string doc = json ? report_json(r) : report_csv(r);
+        n = static_cast<int64_t>(doc.size());
+        if (buf != nullptr && n < cap) std::memcpy(buf, doc.c_str(), doc.size() + 1);
+    });
+    return st == 0 ? n : -st;
+}
+
 int ref_have_serialize(void) { return 1; }
 #else
 int ref_have_serialize(void) { return 0; }

@@ -138,6 +138,10 @@ def lib() -> C.CDLL:
         "moe_apply_reconfig": (I, [P(ExpertStateC), U64, P(ReconfigActionC), I, U64, P(_ModelProfile),
                                    P(_HardwareProfile), P(ExpertStateC), P(I64), P(U64)]),
         "moe_engine_reconfigure": (I, [VP, P(ExpertStateC), U64, D, P(ReconfigReportC)]),
+        "moe_write_reconfig": (I64, [P(ReconfigActionC), I, U64, P(_ModelProfile), P(_HardwareProfile), C.c_char_p, I64]),
+        "moe_read_reconfig": (I, [C.c_char_p, P(_ModelProfile), P(_HardwareProfile), P(ReconfigActionC), I, P(I), P(U64),
+                                  P(I64), P(D)]),
+        "moe_report_text": (I64, [P(SimReportC), I, C.c_char_p, I64]),
         "moe_builtin_anchors": (I, [C.c_char_p, P(D), P(D)]),
         "moe_load_anchors": (I, [C.c_char_p, P(D), P(D)]),
         "moe_ppl_estimate": (I, [I, D, D, I, P(D)]),
@@ -481,6 +485,41 @@ def apply_reconfig(plan: PlacementPlan, actions, target_seed: int, profile: Mode
                                     C.byref(budget._c()) if budget is not None else None, out, C.byref(sw),
                                     C.byref(sd)))
     return PlacementPlan([a.precision for a in out], [a.location for a in out], sw.value, sd.value)
+
+
+def write_reconfig(actions, target_seed: int, profile: ModelProfile, hw: HardwareProfile) -> str:
+    """moeserve.reconfig.v1 JSON, byte-identical to serialize.cpp:160-176."""
+    acts = (ReconfigActionC * max(len(actions), 1))(*[ReconfigActionC(*a, 0) for a in actions])
+    args = (acts, len(actions), target_seed, C.byref(profile._c()), C.byref(hw._c()))
+    n = lib().moe_write_reconfig(*args, None, 0)
+    if n < 0:
+        _check(1)
+    buf = C.create_string_buffer(n + 1)
+    lib().moe_write_reconfig(*args, buf, n + 1)
+    return buf.value.decode()
+
+
+def read_reconfig(document: str, profile: ModelProfile, hw: HardwareProfile):
+    """serialize.cpp:178-206: (actions, target_seed, bytes_moved, est_downtime_s)."""
+    cap = 4 * profile.num_experts + 8
+    acts = (ReconfigActionC * cap)()
+    n, sd, b, t = C.c_int(), C.c_uint64(), C.c_int64(), C.c_double()
+    _check(lib().moe_read_reconfig(document.encode(), C.byref(profile._c()), C.byref(hw._c()), acts, cap, C.byref(n),
+                                   C.byref(sd), C.byref(b), C.byref(t)))
+    return ([(a.kind, a.layer, a.slot, a.target_precision, a.target_location) for a in acts[:n.value]], sd.value,
+            b.value, t.value)
+
+
+def report_text(report: "SimReport", json: bool = False) -> str:
+    """The reference's report_csv / report_json (serialize.cpp:218-243)."""
+    r = SimReportC(report.tokens, report.activations, report.hits, report.bytes_transferred, report.transfer_ns,
+                   report.compute_ns, report.nonexpert_ns)
+    n = lib().moe_report_text(C.byref(r), 1 if json else 0, None, 0)
+    if n < 0:
+        _check(1)
+    buf = C.create_string_buffer(n + 1)
+    lib().moe_report_text(C.byref(r), 1 if json else 0, buf, n + 1)
+    return buf.value.decode()
 
 
 # ----------------------------------------------------------------- pareto (f3)

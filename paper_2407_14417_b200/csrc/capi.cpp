@@ -14,6 +14,7 @@
 #include "moe_b200.h"
 #include "moeb200/engine.hpp"
 #include "moeb200/reconfig.hpp"
+#include "moeb200/serialize.hpp"
 #include "moeb200/pareto.hpp"
 
 using namespace moeb200;
@@ -355,6 +356,66 @@ ReconfigPlan to_reconfig(const moe_reconfig_action* acts, int n, uint64_t target
 }
 
 }  // namespace
+
+namespace {
+
+int64_t copy_text(const std::string& s, char* buf, int64_t cap) {
+    if (buf && static_cast<int64_t>(s.size()) < cap) std::memcpy(buf, s.c_str(), s.size() + 1);
+    return static_cast<int64_t>(s.size());
+}
+
+}  // namespace
+
+int64_t moe_write_reconfig(const moe_reconfig_action* actions, int n_actions, uint64_t target_seed,
+                           const moe_model_profile* p, const moe_hardware_profile* hw, char* buf, int64_t cap) {
+    std::string s;
+    if (guarded([&] {
+            usage_if(n_actions > 0 && actions == nullptr, "null argument");
+            const ModelProfile m = to_model(p);
+            ReconfigPlan rp = to_reconfig(actions, n_actions, target_seed);
+            std::tie(rp.bytes_moved, rp.est_downtime_s) = estimate_cost(rp, m, to_hw(hw));
+            s = write_reconfig(rp, m);
+        }) != MOE_OK)
+        return -1;
+    return copy_text(s, buf, cap);
+}
+
+int moe_read_reconfig(const char* document, const moe_model_profile* p, const moe_hardware_profile* hw,
+                      moe_reconfig_action* actions, int cap, int* n_actions, uint64_t* target_seed,
+                      int64_t* bytes_moved, double* est_downtime_s) {
+    return guarded([&] {
+        usage_if(n_actions == nullptr, "null argument");
+        const ReconfigPlan rp = read_reconfig(document ? document : "", to_model(p), to_hw(hw));
+        *n_actions = static_cast<int>(rp.actions.size());
+        for (int i = 0; i < *n_actions && i < cap && actions; ++i) {
+            const ReconfigAction& x = rp.actions[static_cast<size_t>(i)];
+            actions[i] = {static_cast<int32_t>(x.kind), x.expert.layer, x.expert.slot,
+                          x.target_precision == Precision::P4 ? MOE_P4 : MOE_P16,
+                          x.target_location == Location::GPU ? MOE_GPU : MOE_CPU, 0};
+        }
+        if (target_seed) *target_seed = rp.target_seed;
+        if (bytes_moved) *bytes_moved = rp.bytes_moved;
+        if (est_downtime_s) *est_downtime_s = rp.est_downtime_s;
+    });
+}
+
+int64_t moe_report_text(const moe_sim_report* r, int json, char* buf, int64_t cap) {
+    std::string s;
+    if (guarded([&] {
+            usage_if(r == nullptr, "null argument");
+            SimReport x;
+            x.tokens = static_cast<int>(r->tokens);
+            x.activations = r->activations;
+            x.hits = r->hits;
+            x.bytes_transferred = r->bytes_transferred;
+            x.transfer_ns = r->transfer_ns;
+            x.compute_ns = r->compute_ns;
+            x.nonexpert_ns = r->nonexpert_ns;
+            s = json ? report_json(x) : report_csv(x);
+        }) != MOE_OK)
+        return -1;
+    return copy_text(s, buf, cap);
+}
 
 int moe_diff_plans(const moe_expert_state* from, const moe_expert_state* to, uint64_t to_seed,
                    const moe_model_profile* p, const moe_hardware_profile* hw, moe_reconfig_action* actions,
