@@ -28,7 +28,6 @@ namespace moek {
 namespace tc {
 
 constexpr int kThreads = 256;
-constexpr int kN = 128;        // tokens per tile (UMMA N)
 constexpr int kM = 128;        // weight rows per tile (UMMA M)
 constexpr int kKc = 64;        // K per chunk (one 128-byte swizzle atom of 16-bit values)
 constexpr int kTileBytes = kM * kKc * 2;  // 16 KB (A tile; B tile is the same for kN = 128)
@@ -121,7 +120,9 @@ struct Tile {
     int e, slot0, m, R0;  // expert, first slot, tokens in tile, first weight row
 };
 
+template <int NT>
 MOE_DEVI bool find_tile(const TcArgs& a, int RT, int b, Tile& tl) {
+    constexpr int kN = NT;
     for (int e = 0; e < a.E; ++e) {
         if (!((a.active_mask >> e) & 1ull)) continue;
         const int o0 = a.offsets[e], m = a.offsets[e + 1] - o0;
@@ -165,9 +166,8 @@ MOE_DEVI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar
 // and the converters one canonical stage ahead of the tensor core.
 constexpr int kThreads2 = 384;
 constexpr int kConvThreads = 256;
-constexpr int kRaw = 2, kCan = 2, kBst = 4;
+constexpr int kRaw = 2, kCan = 2;
 constexpr int kCanA = 2 * kTileBytes;   // canonical A stage (gate + up)
-constexpr int kSmem2 = 1024 + kRaw * kRawBytes + kCan * kCanA + kBst * kTileBytes;
 
 // Raw stage layout: [A_gate raw 16 KB][A_up raw 16 KB][scales 2 x 256 B][B raw 16 KB].
 // bf16: 8 block halves of 2 KB per matrix (parts 4hh..4hh+3 of each block).
@@ -204,10 +204,11 @@ MOE_DEVI void produce(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, 
 // producer lanes, each lane's completion arriving on can_full (noinc).  Rows
 // past the tile's tokens repeat the last token (their D columns are never
 // stored).
+template <int NT>
 MOE_DEVI void produce_b(const TcArgs& a, bool p4, int K, int kc, uint8_t* bdst, const int* brow, uint64_t* bar,
-                        int lane) {
+                        int pt, int nprod) {
     const uint16_t* bsrc = p4 ? a.bnat16 : a.bnat;
-    for (int pc = lane; pc < kN * 8; pc += 32) {
+    for (int pc = pt; pc < NT * 8; pc += 32 * nprod) {
         const int n = pc >> 3, c = pc & 7;
         cp_async16(bdst + swz(n, c * 16), bsrc + static_cast<size_t>(brow[n]) * K + kc * kKc + c * 8, 16);
     }
@@ -295,7 +296,22 @@ MOE_DEVI void convert2(bool p4, int nmat, const uint8_t* raw, uint8_t* can, int 
     }
 }
 
+// NT tokens per tile (UMMA N): 128, or 256 for prefill-sized segments (twice
+// the MMA work per staged weight chunk; both TMEM halves hold gate / up).
+template <int NT>
+struct TcCfg {
+    static constexpr int kN = NT;
+    static constexpr int kBTile = NT * kKc * 2;        // B stage bytes
+    static constexpr int kBst = NT == 256 ? 2 : 4;     // B stages
+    static constexpr int kBProd = NT == 256 ? 2 : 1;   // token-row producer warps (2, 3)
+    static constexpr int kTmemCols = 2 * NT;           // gate + up accumulators
+    static constexpr int kSmem = 1024 + kRaw * kRawBytes + kCan * kCanA + kBst * kBTile;
+};
+
+template <int NT>
 __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_constant__ TcArgs a) {
+    using Cf = TcCfg<NT>;
+    constexpr int kN = Cf::kN, kBst = Cf::kBst;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte aligned base by pointer arithmetic (keeps the shared address
     // space, so the converters use LDS/STS, not generic loads/stores)
@@ -303,18 +319,18 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
     __shared__ __align__(8) uint64_t raw_full[kRaw], raw_empty[kRaw], can_full[kCan], can_empty[kCan], b_full[kBst],
         b_empty[kBst], acc_full;
     __shared__ uint32_t tmem_slot;
-    __shared__ int brow[kN];
+    __shared__ int brow[NT];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     auto can = [&](int s) { return smem + s * kCanA; };
-    auto bst = [&](int s) { return smem + kCan * kCanA + s * kTileBytes; };
-    auto raw = [&](int s) { return smem + kCan * kCanA + kBst * kTileBytes + s * kRawBytes; };
+    auto bst = [&](int s) { return smem + kCan * kCanA + s * Cf::kBTile; };
+    auto raw = [&](int s) { return smem + kCan * kCanA + kBst * Cf::kBTile + s * kRawBytes; };
 
     pdl_wait();
     pdl_trigger();
     const int K = a.p == 0 ? a.d : a.f;
     const int RT = (a.p == 0 ? a.f : a.d) / kM;
     Tile tl;
-    if (!find_tile(a, RT, blockIdx.x, tl)) return;
+    if (!find_tile<NT>(a, RT, blockIdx.x, tl)) return;
     const int nmat = a.p == 0 ? 2 : 1;
     const bool p4 = a.ex[tl.e].precision == MOE_P4;
     if (tid < kN) {
@@ -332,7 +348,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
             mbar_init_n(&can_empty[s], 1);
         }
         for (int s = 0; s < kBst; ++s) {
-            mbar_init_n(&b_full[s], 32);  // token-row cp.async lanes (noinc)
+            mbar_init_n(&b_full[s], 32 * Cf::kBProd);  // token-row cp.async lanes (noinc)
             mbar_init_n(&b_empty[s], 1);
         }
         mbar_init_n(&acc_full, 1);
@@ -340,7 +356,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tmem_slot)),
-                     "r"(256)
+                     "r"(Cf::kTmemCols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -362,12 +378,13 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
                 produce(a, tl, nmat, K, kc, raw(r), brow, &raw_full[r], lane);
             }
         }
-    } else if (warp == 2) {
-        // ---- token-row producer: kBst chunks ahead, into the B ring ----
+    } else if (warp == 2 || (Cf::kBProd == 2 && warp == 3)) {
+        // ---- token-row producer(s): kBst chunks ahead, into the B ring ----
+        const int pt = (warp - 2) * 32 + lane;
         for (int kb = 0; kb < nk; ++kb) {
             const int b = kb % kBst;
             if (kb >= kBst) mbar_wait(&b_empty[b], ((kb / kBst) - 1) & 1);
-            produce_b(a, p4, K, kb, bst(b), brow, &b_full[b], lane);
+            produce_b<NT>(a, p4, K, kb, bst(b), brow, &b_full[b], pt, Cf::kBProd);
         }
     } else if (warp == 1) {
         // ---- MMA issuer ----
@@ -415,8 +432,8 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int row = (warp & 3) * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-        const int c0 = ((warp - 4) >> 2) * 64;
-        for (int cb = c0; cb < c0 + 64; cb += 32) {
+        const int c0 = ((warp - 4) >> 2) * (kN / 2);
+        for (int cb = c0; cb < c0 + kN / 2; cb += 32) {
             uint32_t g[32];
             TMEM_LD32(tmem + lane_base + cb, g);
             if (a.p == 0) {
@@ -446,7 +463,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::kTmemCols) : "memory");
 }
 
 // natural bf16 rows -> fp16 copy (pass-0 B operand of int4 experts)
@@ -475,7 +492,10 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     if (d % kM != 0 || f % kM != 0 || d % 128 != 0 || f % 128 != 0) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
-        MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2));
+        MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         TcCfg<128>::kSmem));
+        MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         TcCfg<256>::kSmem));
         attr = true;
     }
     const size_t slots = static_cast<size_t>(T) * k;
@@ -498,20 +518,30 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     static const int dbg = getenv("MOE_TC_DBG") ? atoi(getenv("MOE_TC_DBG")) : 0;
     a.dbg = dbg;
     for (int e = 0; e < E; ++e) a.ex[e] = experts[e];
-    const int ntiles_max = static_cast<int>((slots + kN - 1) / kN) + E;
+    // 256-token tiles once the average active expert sees that many slots
+    // (MOE_TC_DBG bit3 forces 128, bit4 forces 256)
+    int nact = 0;
+    for (int e = 0; e < E; ++e) nact += static_cast<int>((active_mask >> e) & 1ull);
+    bool wide = nact > 0 && slots >= static_cast<size_t>(256) * nact;
+    if (dbg & 8) wide = false;
+    if (dbg & 16) wide = true;
+    const int NT = wide ? 256 : 128;
+    const int ntiles_max = static_cast<int>((slots + NT - 1) / NT) + E;
+    auto kern = wide ? tc_ffn_kernel<256> : tc_ffn_kernel<128>;
+    const int smem = wide ? TcCfg<256>::kSmem : TcCfg<128>::kSmem;
     // pass 0: gate/up + SwiGLU -> h
     a.p = 0;
     a.bnat = static_cast<const uint16_t*>(x);
     a.bnat16 = x16;
     a.hout = h;
     a.hout16 = h16;
-    MOE_CUDA_OK(moek::launch_pdl(tc_ffn_kernel, dim3(static_cast<unsigned>(ntiles_max * (f / kM))), dim3(kThreads2),
-                                 kSmem2, stream, a));
+    MOE_CUDA_OK(moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (f / kM))), dim3(kThreads2), smem,
+                                 stream, a));
     // pass 1: down -> y
     a.p = 1;
     a.bnat = h;
     a.bnat16 = h16;
     a.y = y;
-    return moek::launch_pdl(tc_ffn_kernel, dim3(static_cast<unsigned>(ntiles_max * (d / kM))), dim3(kThreads2),
-                            kSmem2, stream, a);
+    return moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (d / kM))), dim3(kThreads2), smem, stream,
+                            a);
 }
