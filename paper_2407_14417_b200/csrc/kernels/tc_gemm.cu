@@ -206,9 +206,9 @@ MOE_DEVI void produce(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, 
 // stored).
 template <int NT>
 MOE_DEVI void produce_b(const TcArgs& a, bool p4, int K, int kc, uint8_t* bdst, const int* brow, uint64_t* bar,
-                        int pt, int nprod) {
+                        int pt, int nprod, int nrows) {
     const uint16_t* bsrc = p4 ? a.bnat16 : a.bnat;
-    for (int pc = pt; pc < NT * 8; pc += 32 * nprod) {
+    for (int pc = pt; pc < nrows * 8; pc += 32 * nprod) {
         const int n = pc >> 3, c = pc & 7;
         cp_async16(bdst + swz(n, c * 16), bsrc + static_cast<size_t>(brow[n]) * K + kc * kKc + c * 8, 16);
     }
@@ -333,6 +333,8 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
     if (!find_tile<NT>(a, RT, blockIdx.x, tl)) return;
     const int nmat = a.p == 0 ? 2 : 1;
     const bool p4 = a.ex[tl.e].precision == MOE_P4;
+    // UMMA N: the tile's tokens rounded up to 16 (M = 128 allows 16..256)
+    const int nmma = min(kN, (tl.m + 15) / 16 * 16);
     if (tid < kN) {
         const int n = min(tid, tl.m - 1);
         const int slot = tl.slot0 + n;
@@ -384,11 +386,11 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
         for (int kb = 0; kb < nk; ++kb) {
             const int b = kb % kBst;
             if (kb >= kBst) mbar_wait(&b_empty[b], ((kb / kBst) - 1) & 1);
-            produce_b<NT>(a, p4, K, kb, bst(b), brow, &b_full[b], pt, Cf::kBProd);
+            produce_b<NT>(a, p4, K, kb, bst(b), brow, &b_full[b], pt, Cf::kBProd, nmma);
         }
     } else if (warp == 1) {
         // ---- MMA issuer ----
-        const uint32_t id = idesc(p4 ? 0 : 1, kN, kM);
+        const uint32_t id = idesc(p4 ? 0 : 1, nmma, kM);
         for (int kc = 0; kc < nk; ++kc) {
             const int c = kc % kCan, b = kc % kBst;
             mbar_wait(&can_full[c], (kc / kCan) & 1);
@@ -518,11 +520,11 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     static const int dbg = getenv("MOE_TC_DBG") ? atoi(getenv("MOE_TC_DBG")) : 0;
     a.dbg = dbg;
     for (int e = 0; e < E; ++e) a.ex[e] = experts[e];
-    // 256-token tiles once the average active expert sees that many slots
+    // 256-token tiles once the average active expert sees more than 128 slots
     // (MOE_TC_DBG bit3 forces 128, bit4 forces 256)
     int nact = 0;
     for (int e = 0; e < E; ++e) nact += static_cast<int>((active_mask >> e) & 1ull);
-    bool wide = nact > 0 && slots >= static_cast<size_t>(256) * nact;
+    bool wide = nact > 0 && slots > static_cast<size_t>(128) * nact;
     if (dbg & 8) wide = false;
     if (dbg & 16) wide = true;
     const int NT = wide ? 256 : 128;
