@@ -290,14 +290,14 @@ def run_ours(args, rank, world, device):
     if args.batch_sweep and args.batch_points:
         plan_b = moe.make_plan(moe.TaskRequest(moe.QUALITY, args.n4, 0), moe.HardwareProfile(10**15), prof)
         eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan_b, max_tokens=max(args.batch_points),
-                            seed=args.seed + rank, device=device, norm_eps=NORM_EPS)
+                            seed=args.seed + rank, device=device, norm_eps=NORM_EPS, tc_min_tokens=args.tc_min)
         for tb in args.batch_points:
             eng.synth_input(0, tb)
             eng.decode(tb)
             eng.sync()
             m = time_engine(moe, torch, eng, tb, max(5, min(args.steps, 30)), 3)
             batch.append({"batch": tb, "tokens_per_s": round(world * tb * 1000.0 / m, 1), "ms_per_step": round(m, 4),
-                          "path": "tcgen05" if tb >= 64 else "gemv"})
+                          "path": "tcgen05" if tb >= args.tc_min else "gemv"})
         eng.close()
         del eng
 
@@ -598,6 +598,7 @@ def main():
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of expert parallel")
     ap.add_argument("--ep", action="store_true", help="expert-parallel code path even at N=1 (NCCL, 1 rank)")
     ap.add_argument("--no-batch-sweep", dest="batch_sweep", action="store_false")
+    ap.add_argument("--tc-min", type=int, default=40, help="batch-sweep engine: tcgen05 expert GEMM from this T")
     ap.add_argument("--batch-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],
                     default=[1, 8, 32, 64, 128, 256])
     ap.add_argument("--no-prefill", dest="prefill", action="store_false")
