@@ -2,22 +2,26 @@
 // (tcgen05.mma, fp32 accumulators in TMEM) for batched decode / prefill,
 // where an expert sees enough tokens that the contraction is a real GEMM.
 //
-// One CTA computes a 128-weight-row x 128-token tile of one expert:
+// One CTA computes a 128-weight-row x (128 | 256)-token tile of one expert:
 //   pass 0: D_gate, D_up = W_gate/up[rows] . X[tokens]^T -> fused SwiGLU
 //           epilogue h = bf16(silu(g) * u) (+ its fp16 copy) for the tile
 //   pass 1: D = W_down[rows] . H[tokens]^T -> y[slot][row] (fp32), combined
 //           afterwards by the K5 combine kernel.
-// Data path per 64-K chunk (2-stage pipeline):
-//   HBM --cp.async--> raw smem (weights in their fragment-block storage
-//   layout, token rows in natural order) --convert (all threads)-->
-//   canonical K-major SWIZZLE_128B tiles --tcgen05.mma (one thread,
-//   M=128, N=128, K=16 x 4)--> TMEM; tcgen05.commit -> mbarrier frees the
-//   stage.  bf16 experts run kind::f16 with BF16 operands; int4-g128 experts
+// Data path per 64-K chunk, warp-specialised, all hand-offs on mbarriers:
+//   weights: HBM --bulk copy--> raw smem ring (fragment-block storage
+//     layout) --converter warps--> canonical K-major SWIZZLE_128B A tiles;
+//   tokens:  slot-ordered rows (gather kernel; h is slot-ordered already)
+//     --TMA 2D boxes, 128-byte swizzle--> canonical B tiles;
+//   one thread issues tcgen05.mma (M = 128, N = the tile's tokens rounded
+//   to 16, K = 16 x 4) into TMEM; tcgen05.commit frees the stages.  bf16 experts run kind::f16 with BF16 operands; int4-g128 experts
 //   are dequantised in the convert step to fp16 q*s (exact: <= 11
 //   significant bits, for normal-range scales) and run with F16 operands
 //   against an fp16 copy of the activations.
 // The storage layout stays the GEMV's (fragment blocks), so one copy of the
 // weights serves both paths.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -40,13 +44,16 @@ constexpr int kCanBytes = 3 * kTileBytes;
 constexpr int kSmemBytes = 1024 + 2 * kRawBytes + 2 * kCanBytes;
 
 struct TcArgs {
+    // B operand tensor maps (2D: K x rows in slot order, 64 x 64 boxes,
+    // SWIZZLE_128B): pass 0 the slot-ordered token rows (bf16 / fp16 copy),
+    // pass 1 h (bf16 / fp16)
+    CUtensorMap tmb;
+    CUtensorMap tmb16;
     const int32_t* offsets;   // [E+1]
     const int32_t* perm;      // [T*k]
     int T, k, E, kshift;
     int p;                    // 0 gate/up, 1 down
     int d, f;
-    const uint16_t* bnat;     // natural B rows, bf16: pass 0 normalised x [T][d], pass 1 h [T*k][f]
-    const uint16_t* bnat16;   // the same as fp16 (int4 experts)
     uint16_t* hout;           // pass 0: h [T*k][f] bf16
     uint16_t* hout16;         // pass 0: h [T*k][f] fp16
     float* y;                 // pass 1: y [T*k][d]
@@ -175,8 +182,8 @@ constexpr int kCanA = 2 * kTileBytes;   // canonical A stage (gate + up)
 //       picks words 2hh, 2hh+1), 8 KB per matrix, + 8 x 32 B scales.
 MOE_DEVI uint32_t raw_bytes(bool p4, int nmat) { return nmat * (p4 ? 8 * 1024 + 256 : 16384); }
 
-MOE_DEVI void produce(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, uint8_t* raw, const int* brow,
-                      uint64_t* bar, int lane) {
+MOE_DEVI void produce(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, uint8_t* raw, uint64_t* bar,
+                      int lane) {
     const moe_expert_weights& W = a.ex[tl.e];
     const int G = K / 128, g = kc >> 1, hh = kc & 1;
     const bool p4 = W.precision == MOE_P4;
@@ -199,20 +206,15 @@ MOE_DEVI void produce(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, 
     }
 }
 
-// Token rows of chunk kc (natural order, 128 B per row) straight into their
-// swizzled positions of the canonical B tile with 16-byte cp.async by the 32
-// producer lanes, each lane's completion arriving on can_full (noinc).  Rows
-// past the tile's tokens repeat the last token (their D columns are never
-// stored).
-template <int NT>
-MOE_DEVI void produce_b(const TcArgs& a, bool p4, int K, int kc, uint8_t* bdst, const int* brow, uint64_t* bar,
-                        int pt, int nprod, int nrows) {
-    const uint16_t* bsrc = p4 ? a.bnat16 : a.bnat;
-    for (int pc = pt; pc < nrows * 8; pc += 32 * nprod) {
-        const int n = pc >> 3, c = pc & 7;
-        cp_async16(bdst + swz(n, c * 16), bsrc + static_cast<size_t>(brow[n]) * K + kc * kKc + c * 8, 16);
-    }
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(s32(bar)) : "memory");
+// One 64-K x 64-row box of the B tensor map into its SWIZZLE_128B canonical
+// position (the TMA applies the same 16-byte-chunk XOR as swz(); the stage
+// is 1024-byte aligned), completing on `bar`.
+MOE_DEVI void tma_load_b(void* dst, const CUtensorMap* tm, int k0, int row0, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(s32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(k0), "r"(row0), "r"(s32(bar))
+        : "memory");
 }
 
 // per-converter-thread swizzled destinations (identical for every chunk)
@@ -303,7 +305,6 @@ struct TcCfg {
     static constexpr int kN = NT;
     static constexpr int kBTile = NT * kKc * 2;        // B stage bytes
     static constexpr int kBst = NT == 256 ? 2 : 4;     // B stages
-    static constexpr int kBProd = NT == 256 ? 2 : 1;   // token-row producer warps (2, 3)
     static constexpr int kTmemCols = 2 * NT;           // gate + up accumulators
     static constexpr int kSmem = 1024 + kRaw * kRawBytes + kCan * kCanA + kBst * kBTile;
 };
@@ -319,7 +320,6 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
     __shared__ __align__(8) uint64_t raw_full[kRaw], raw_empty[kRaw], can_full[kCan], can_empty[kCan], b_full[kBst],
         b_empty[kBst], acc_full;
     __shared__ uint32_t tmem_slot;
-    __shared__ int brow[NT];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     auto can = [&](int s) { return smem + s * kCanA; };
     auto bst = [&](int s) { return smem + kCan * kCanA + s * Cf::kBTile; };
@@ -335,11 +335,6 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
     const bool p4 = a.ex[tl.e].precision == MOE_P4;
     // UMMA N: the tile's tokens rounded up to 16 (M = 128 allows 16..256)
     const int nmma = min(kN, (tl.m + 15) / 16 * 16);
-    if (tid < kN) {
-        const int n = min(tid, tl.m - 1);
-        const int slot = tl.slot0 + n;
-        brow[tid] = a.p == 0 ? (a.kshift >= 0 ? a.perm[slot] >> a.kshift : a.perm[slot] / a.k) : slot;
-    }
     if (tid == 0) {
         for (int s = 0; s < kRaw; ++s) {
             mbar_init_n(&raw_full[s], 1);  // producer expect_tx
@@ -350,7 +345,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
             mbar_init_n(&can_empty[s], 1);
         }
         for (int s = 0; s < kBst; ++s) {
-            mbar_init_n(&b_full[s], 32 * Cf::kBProd);  // token-row cp.async lanes (noinc)
+            mbar_init_n(&b_full[s], 1);  // TMA expect_tx
             mbar_init_n(&b_empty[s], 1);
         }
         mbar_init_n(&acc_full, 1);
@@ -377,17 +372,22 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
                 if (lane == 0) mbar_arrive(&raw_full[r]);
                 __syncwarp();
             } else {
-                produce(a, tl, nmat, K, kc, raw(r), brow, &raw_full[r], lane);
+                produce(a, tl, nmat, K, kc, raw(r), &raw_full[r], lane);
             }
         }
-    } else if (warp == 2 || (Cf::kBProd == 2 && warp == 3)) {
-        // ---- token-row producer(s): kBst chunks ahead, into the B ring ----
-        const int pt = (warp - 2) * 32 + lane;
-        for (int kb = 0; kb < nk; ++kb) {
-            const int b = kb % kBst;
-            if (kb >= kBst) mbar_wait(&b_empty[b], ((kb / kBst) - 1) & 1);
-            produce_b<NT>(a, p4, K, kb, bst(b), brow, &b_full[b], pt, Cf::kBProd, nmma);
+    } else if (warp == 2) {
+        // ---- B producer: TMA boxes of the slot-ordered rows, kBst chunks ahead ----
+        if (lane == 0) {
+            const CUtensorMap* tm = p4 ? &a.tmb16 : &a.tmb;
+            const int nbox = (nmma + 63) / 64;
+            for (int kb = 0; kb < nk; ++kb) {
+                const int b = kb % kBst;
+                if (kb >= kBst) mbar_wait(&b_empty[b], ((kb / kBst) - 1) & 1);
+                mbar_expect_tx(&b_full[b], static_cast<uint32_t>(nbox) * 64 * 128);
+                for (int q = 0; q < nbox; ++q) tma_load_b(bst(b) + q * 8192, tm, kb * kKc, tl.slot0 + q * 64, &b_full[b]);
+            }
         }
+        __syncwarp();
     } else if (warp == 1) {
         // ---- MMA issuer ----
         const uint32_t id = idesc(p4 ? 0 : 1, nmma, kM);
@@ -468,13 +468,50 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::kTmemCols) : "memory");
 }
 
-// natural bf16 rows -> fp16 copy (pass-0 B operand of int4 experts)
-__global__ void to_f16_kernel(const uint16_t* __restrict__ x, long long n, uint16_t* __restrict__ y) {
+// Pass-0 B operand in slot order: xs[slot] = x[token of slot] (bf16) and
+// its fp16 copy (int4 experts), so every tile's token rows are one TMA box
+// column.  One 16-byte chunk per thread.
+__global__ void gather_rows_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ perm, int slots, int d,
+                                   int k, int kshift, uint16_t* __restrict__ xs, uint16_t* __restrict__ xs16) {
     pdl_wait();
     pdl_trigger();
-    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<long long>(gridDim.x) * blockDim.x)
-        y[i] = __half_as_ushort(__float2half_rn(bf2f(x[i])));
+    const int cpr = d / 8;
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+         i < static_cast<long long>(slots) * cpr; i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int slot = static_cast<int>(i / cpr), c = static_cast<int>(i - static_cast<long long>(slot) * cpr);
+        const int pv = perm[slot];
+        const int t = kshift >= 0 ? pv >> kshift : pv / k;
+        const uint4 v = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * d)[c];
+        reinterpret_cast<uint4*>(xs + static_cast<size_t>(slot) * d)[c] = v;
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        uint32_t h[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            h[q] = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(bf16_lo(w[q])))) |
+                   (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(bf16_hi(w[q])))) << 16);
+        reinterpret_cast<uint4*>(xs16 + static_cast<size_t>(slot) * d)[c] = make_uint4(h[0], h[1], h[2], h[3]);
+    }
+}
+
+// 2D tensor map over rows x K bf16/fp16 values (row stride K * 2 bytes),
+// 64 x 64 boxes, 128-byte swizzle -- the canonical B tile layout.
+cudaError_t encode_b(CUtensorMap* tm, const void* base, int K, int rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (enc == nullptr) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        MOE_CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (fn == nullptr || q != cudaDriverEntryPointSuccess) return cudaErrorNotSupported;
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kKc), 64};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 }  // namespace tc
@@ -482,7 +519,7 @@ __global__ void to_f16_kernel(const uint16_t* __restrict__ x, long long n, uint1
 
 size_t moek_tc_workspace_bytes(int T, int k, int d, int f) {
     const size_t slots = static_cast<size_t>(T) * k;
-    return static_cast<size_t>(T) * d * 2 + 2 * slots * f * 2 + 1024;
+    return 2 * slots * d * 2 + 2 * slots * f * 2 + 1024;  // xs, xs16, h, h16
 }
 
 // Grouped expert FFN on tcgen05 for every expert segment of a permutation:
@@ -501,12 +538,15 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
         attr = true;
     }
     const size_t slots = static_cast<size_t>(T) * k;
-    uint16_t* x16 = static_cast<uint16_t*>(ws);
-    uint16_t* h = x16 + static_cast<size_t>(T) * d;
+    uint16_t* xs = static_cast<uint16_t*>(ws);
+    uint16_t* xs16 = xs + slots * d;
+    uint16_t* h = xs16 + slots * d;
     uint16_t* h16 = h + slots * f;
-    const long long nx = static_cast<long long>(T) * d;
-    MOE_CUDA_OK(moek::launch_pdl(to_f16_kernel, dim3(static_cast<unsigned>(std::min<long long>((nx + 255) / 256, 1184))),
-                                 dim3(256), 0, stream, static_cast<const uint16_t*>(x), nx, x16));
+    const int kshift = (k & (k - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(k)) : -1;
+    const long long nch = static_cast<long long>(slots) * (d / 8);
+    MOE_CUDA_OK(moek::launch_pdl(gather_rows_kernel, dim3(static_cast<unsigned>(std::min<long long>((nch + 255) / 256, 2368))),
+                                 dim3(256), 0, stream, static_cast<const uint16_t*>(x), perm, static_cast<int>(slots), d, k,
+                                 kshift, xs, xs16));
     TcArgs a{};
     a.offsets = offsets;
     a.perm = perm;
@@ -533,16 +573,16 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     const int smem = wide ? TcCfg<256>::kSmem : TcCfg<128>::kSmem;
     // pass 0: gate/up + SwiGLU -> h
     a.p = 0;
-    a.bnat = static_cast<const uint16_t*>(x);
-    a.bnat16 = x16;
+    MOE_CUDA_OK(encode_b(&a.tmb, xs, d, static_cast<int>(slots)));
+    MOE_CUDA_OK(encode_b(&a.tmb16, xs16, d, static_cast<int>(slots)));
     a.hout = h;
     a.hout16 = h16;
     MOE_CUDA_OK(moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (f / kM))), dim3(kThreads2), smem,
                                  stream, a));
     // pass 1: down -> y
     a.p = 1;
-    a.bnat = h;
-    a.bnat16 = h16;
+    MOE_CUDA_OK(encode_b(&a.tmb, h, f, static_cast<int>(slots)));
+    MOE_CUDA_OK(encode_b(&a.tmb16, h16, f, static_cast<int>(slots)));
     a.y = y;
     return moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (d / kM))), dim3(kThreads2), smem, stream,
                             a);
