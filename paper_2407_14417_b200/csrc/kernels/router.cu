@@ -230,20 +230,23 @@ MOE_DEVI void warp_topk(const float* lg, int E, int k, int lane, int32_t* idx_ou
             if (bi == lane + 32) ok1 = false;
         }
     }
-    if (lane == 0) {
-        float ex[MOE_MAX_TOPK], sum = 0.0f;
+    // softmax over the selected logits: lane j < k takes sel[j]; the sum is
+    // accumulated in j order (as the oracle) from the lanes' exponentials
+    float mine = 0.0f;
+    int mid = 0;
 #pragma unroll
-        for (int j = 0; j < MOE_MAX_TOPK; ++j) {
-            ex[j] = j < k ? expf(sel[j] - sel[0]) : 0.0f;
-            if (j < k) sum += ex[j];
+    for (int j = 0; j < MOE_MAX_TOPK; ++j)
+        if (j == lane) {
+            mine = sel[j];
+            mid = sid[j];
         }
-#pragma unroll
-        for (int j = 0; j < MOE_MAX_TOPK; ++j)
-            if (j < k) {
-                idx_out[j] = sid[j];
-                w_out[j] = ex[j] / sum;
-                s_idx[j] = sid[j];
-            }
+    const float ex = lane < k ? expf(mine - sel[0]) : 0.0f;
+    float sum = 0.0f;
+    for (int j = 0; j < k; ++j) sum += __shfl_sync(0xffffffffu, ex, j);
+    if (lane < k) {
+        idx_out[lane] = mid;
+        w_out[lane] = ex / sum;
+        s_idx[lane] = mid;
     }
 }
 
@@ -297,7 +300,20 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
         __syncthreads();
         const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(lg_s[MOE_MAX_EXPERTS],
                                                                             static_cast<float>(a.d)), a.norm_eps)));
-        for (int i = threadIdx.x; i < a.d; i += blockDim.x) x_s[i] = f2bf(__fmul_rn(bf2f(x_s[i]), rstd));
+        // x * rstd, 8 elements (one 16-byte chunk) per thread and step
+        for (int i = threadIdx.x * 8; i < a.d; i += blockDim.x * 8) {
+            if (i + 8 <= a.d) {
+                uint4 v = *reinterpret_cast<const uint4*>(x_s + i);
+                uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    w[q] = static_cast<uint32_t>(f2bf(__fmul_rn(bf16_lo(w[q]), rstd))) |
+                           (static_cast<uint32_t>(f2bf(__fmul_rn(bf16_hi(w[q]), rstd))) << 16);
+                *reinterpret_cast<uint4*>(x_s + i) = make_uint4(w[0], w[1], w[2], w[3]);
+            } else {
+                for (int j = i; j < a.d; ++j) x_s[j] = f2bf(__fmul_rn(bf2f(x_s[j]), rstd));
+            }
+        }
         __syncthreads();
     }
     ltrace(1, 0);
