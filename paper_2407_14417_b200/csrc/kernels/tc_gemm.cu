@@ -365,8 +365,11 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
 
     if (warp == 0) {
         // ---- weight producer: kRaw chunks ahead of the converters ----
-        for (int kc = 0; kc < nk; ++kc) {
-            const int r = kc % kRaw, pass = kc / kRaw;
+        // raw units: one 64-K chunk for bf16; a 128-K chunk pair for int4,
+        // whose 1 KB blocks hold both K halves (loaded once, converted twice)
+        for (int kc = 0; kc < nk; kc += p4 ? 2 : 1) {
+            const int u = p4 ? kc >> 1 : kc;
+            const int r = u % kRaw, pass = u / kRaw;
             if (pass > 0) mbar_wait(&raw_empty[r], (pass - 1) & 1);
             if (a.dbg & 4) {
                 if (lane == 0) mbar_arrive(&raw_full[r]);
@@ -419,15 +422,16 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
         conv_offsets(ct, 0, o0);
         conv_offsets(ct, 1, o1);
         for (int kc = 0; kc < nk; ++kc) {
-            const int r = kc % kRaw, c = kc % kCan;
-            mbar_wait(&raw_full[r], (kc / kRaw) & 1);
+            const int u = p4 ? kc >> 1 : kc;
+            const int r = u % kRaw, c = kc % kCan;
+            mbar_wait(&raw_full[r], (u / kRaw) & 1);
             if (kc >= kCan) mbar_wait(&can_empty[c], ((kc / kCan) - 1) & 1);
             if (!(a.dbg & 1)) convert2(p4, nmat, raw(r), can(c), ct, (kc & 1) ? o1 : o0);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&can_full[c]);
-                mbar_arrive(&raw_empty[r]);
+                if (!p4 || (kc & 1)) mbar_arrive(&raw_empty[r]);
             }
         }
         mbar_wait(&acc_full, 0);
