@@ -598,7 +598,7 @@ def main():
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of expert parallel")
     ap.add_argument("--ep", action="store_true", help="expert-parallel code path even at N=1 (NCCL, 1 rank)")
     ap.add_argument("--no-batch-sweep", dest="batch_sweep", action="store_false")
-    ap.add_argument("--tc-min", type=int, default=40, help="batch-sweep engine: tcgen05 expert GEMM from this T")
+    ap.add_argument("--tc-min", type=int, default=32, help="batch-sweep engine: tcgen05 expert GEMM from this T")
     ap.add_argument("--batch-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],
                     default=[1, 8, 32, 64, 128, 256])
     ap.add_argument("--no-prefill", dest="prefill", action="store_false")

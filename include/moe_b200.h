@@ -301,7 +301,7 @@ typedef struct {
     float norm_eps;            /* > 0: Mixtral decoder-layer RMSNorm (unit weight) before every MoE
                                   block, out = x + MoE(RMSNorm(x)); 0: out = x + MoE(x) */
     int32_t tc_min_tokens;     /* decode batches T >= this use the tcgen05 expert GEMM, smaller ones
-                                  the streaming GEMV (0: default 40, the measured crossover) */
+                                  the streaming GEMV (0: default 32, the measured crossover) */
     int32_t lru_capacity;      /* host-resident experts: 0 = Static (every activation re-streams into
                                   the single swap slot, simulator.cpp:98-106); C >= top_k = LRU cache of
                                   C device slots (simulator.cpp:37-62, the Mixtral-Offloading baseline) */

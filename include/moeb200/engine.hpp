@@ -35,7 +35,7 @@ struct EngineConfig {
     int device = 0;
     bool use_graphs = true;
     float norm_eps = 0.0f;    // > 0: pre-MoE RMSNorm (unit weight), residual = un-normalised x
-    int tc_min_tokens = 40;   // T >= this: tcgen05 expert GEMM instead of the streaming GEMV (measured crossover)
+    int tc_min_tokens = 32;   // T >= this: tcgen05 expert GEMM instead of the streaming GEMV (measured crossover)
     int lru_capacity = 0;     // 0: Static swap slot (simulator.hpp ResidencyPolicy::Static); >0: LRU of that many slots
     bool keep_masters = false;  // pinned host copy of every expert in both precisions (the reconfig
                                 // model's "16-bit master on the CPU", reconfig.hpp:39): required by reconfigure()

@@ -770,7 +770,7 @@ int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan
         usage_if(!(cfg->norm_eps >= 0.0f), "norm_eps must be >= 0");
         ec.norm_eps = cfg->norm_eps;
         usage_if(cfg->tc_min_tokens < 0, "tc_min_tokens must be >= 0");
-        ec.tc_min_tokens = cfg->tc_min_tokens > 0 ? cfg->tc_min_tokens : 40;
+        ec.tc_min_tokens = cfg->tc_min_tokens > 0 ? cfg->tc_min_tokens : 32;
         usage_if(cfg->lru_capacity < 0, "lru_capacity must be >= 0");
         ec.lru_capacity = cfg->lru_capacity;
         ec.keep_masters = cfg->keep_masters != 0;

@@ -132,7 +132,7 @@ class EngineOps:
     MoeEngine's weights (router of every layer, this rank's experts)."""
 
     def __init__(self, moe, torch, engine, rank: int, world: int, T: int, norm_eps: float, device,
-                 tc_min_tokens: int = 40):
+                 tc_min_tokens: int = 32):
         self.moe, self.torch, self.eng = moe, torch, engine
         self.num_layers, self.E, self.k, self.d, self.f = engine.L, engine.E, engine.k, engine.d, engine.f
         self.norm_eps, self.device, self.T = norm_eps, device, T
