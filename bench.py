@@ -516,7 +516,10 @@ def run_ep(args, rank, world, device):
     eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan, max_tokens=T, seed=args.seed, device=device,
                         norm_eps=NORM_EPS)
     ops = ep.EngineOps(moe, torch, eng, rank, world, T, NORM_EPS, torch.device(f"cuda:{device}"))
-    dec = ep.ExpertParallelDecoder(dist, ops, rank, world, T_local, EXPERTS)
+    # exchange: the library's C-ABI NCCL path (moe_ep_dispatch / moe_ep_combine),
+    # or torch.distributed's collectives with --ep-torch
+    exch = None if args.ep_torch else ep.CapiExchange(moe, dist, rank, world, device, ops._stream)
+    dec = ep.ExpertParallelDecoder(dist, ops, rank, world, T_local, EXPERTS, exchange=exch)
     eng.synth_input(0, T)
     eng.sync()
     x_all = torch.as_tensor(_DevBytes(eng.input_ptr, T * D_MODEL * 2), device=f"cuda:{device}").view(torch.int16)
@@ -565,7 +568,8 @@ def run_ep(args, rank, world, device):
             "config": {"workload": "mixtral8x7b-shape 32-layer MoE stack, expert-parallel batch-%d/GPU decode" % T_local,
                        "n4": args.n4, "of": LAYERS * EXPERTS, "layer": "x + MoE(RMSNorm(x))",
                        "parallelism": "ep%d" % world, "experts_per_gpu_per_layer": EXPERTS // world if world <= EXPERTS else 1,
-                       "exchange": "NCCL all-gather (dispatch) + reduce-scatter (combine) per layer",
+                       "exchange": "NCCL all-gather (dispatch) + reduce-scatter (combine) per layer, via " +
+                                   ("torch.distributed" if args.ep_torch else "the C ABI (moe_ep_dispatch / moe_ep_combine)"),
                        "exchange_bytes_per_layer_per_gpu": xb, "batch_per_gpu": T_local,
                        "l2": "no flush: every step streams GBs of distinct expert weights per GPU"},
             "e2e": {"value": round(world * T_local / e2e_s, 3), "unit": "tokens/s",
@@ -597,6 +601,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of expert parallel")
     ap.add_argument("--ep", action="store_true", help="expert-parallel code path even at N=1 (NCCL, 1 rank)")
+    ap.add_argument("--ep-torch", action="store_true", help="EP exchange via torch.distributed instead of the C ABI")
     ap.add_argument("--no-batch-sweep", dest="batch_sweep", action="store_false")
     ap.add_argument("--tc-min", type=int, default=32, help="batch-sweep engine: tcgen05 expert GEMM from this T")
     ap.add_argument("--batch-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],

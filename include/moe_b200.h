@@ -343,6 +343,25 @@ int moe_engine_last_routing(moe_engine* eng, int T, int32_t* slots_out);
 /* Cumulative SimReport counters of real runs (hits / bytes_transferred /
  * activations follow simulate() semantics for the engine's plan). */
 int moe_engine_counters(const moe_engine* eng, moe_sim_report* out);
+
+/* ------------------------------------------------------------------------
+ * Expert-parallel exchange: NCCL over NVLink, loaded at
+ * run time.  Per layer: moe_ep_dispatch all-gathers every rank's token rows
+ * (bf16) into x_all[world*T_local][d]; the ranks route all rows and run their
+ * own experts (moe_ffn / moe_ffn_tc with the other shards NULL), form their
+ * shares (moe_combine_partial); moe_ep_combine reduce-scatters the fp32
+ * shares so each rank gets the sum for its T_local tokens, then
+ * moe_residual_add.  Errors: moe_ep_last_error().
+ * ---------------------------------------------------------------------- */
+#define MOE_EP_ID_BYTES 128
+typedef struct moe_ep_comm moe_ep_comm;
+const char* moe_ep_last_error(void);
+int moe_ep_unique_id(char id[MOE_EP_ID_BYTES]);                       /* ncclGetUniqueId, on one rank */
+int moe_ep_comm_init(const char id[MOE_EP_ID_BYTES], int world, int rank, int device, moe_ep_comm** out);
+int moe_ep_comm_wrap(void* nccl_comm, int world, int rank, moe_ep_comm** out);  /* an existing ncclComm_t */
+void moe_ep_comm_destroy(moe_ep_comm* comm);
+int moe_ep_dispatch(moe_ep_comm* comm, const void* x_local, int T_local, int d, void* x_all, void* stream);
+int moe_ep_combine(moe_ep_comm* comm, const float* part, int T_local, int d, float* mine, void* stream);
 /* Execute diff_plans(current, target) on the device (needs keep_masters):
  * Offload releases HBM, Fetch / in-place Dequantize copy host copies in,
  * Quantize of a device-resident expert runs the int4-g128 quantiser on the

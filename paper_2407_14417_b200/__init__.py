@@ -113,6 +113,13 @@ def lib() -> C.CDLL:
     P, I, I64, U64, D, VP = C.POINTER, C.c_int, C.c_int64, C.c_uint64, C.c_double, C.c_void_p
     sig = {
         "moe_last_error": (C.c_char_p, []),
+        "moe_ep_last_error": (C.c_char_p, []),
+        "moe_ep_unique_id": (I, [C.c_char_p]),
+        "moe_ep_comm_init": (I, [C.c_char_p, I, I, I, P(VP)]),
+        "moe_ep_comm_wrap": (I, [VP, I, I, P(VP)]),
+        "moe_ep_comm_destroy": (None, [VP]),
+        "moe_ep_dispatch": (I, [VP, VP, I, I, VP, VP]),
+        "moe_ep_combine": (I, [VP, VP, I, I, VP, VP]),
         "moe_version": (I, []),
         "moe_profile_builtin": (I, [I, P(_ModelProfile)]),
         "moe_profile_for_shape": (I, [I, I, I, I, I, I64, P(_ModelProfile)]),
@@ -457,6 +464,48 @@ def simulate(plan: PlacementPlan, slots: Sequence[int], tokens: int, profile: Mo
 
 def expected_throughput(plan: PlacementPlan, profile: ModelProfile, hw: HardwareProfile) -> float:
     return lib().moe_expected_throughput(plan._entries(), C.byref(profile._c()), C.byref(hw._c()))
+
+
+# ----------------------------------------------------------------- expert-parallel exchange
+def _ep_check(status: int):
+    if status != 0:
+        msg = lib().moe_ep_last_error().decode(errors="replace")
+        raise (UsageError if status == 2 else MoeError)(status, msg)
+
+
+def ep_unique_id() -> bytes:
+    """ncclGetUniqueId (on one rank; broadcast it to the others)."""
+    buf = C.create_string_buffer(128)
+    _ep_check(lib().moe_ep_unique_id(buf))
+    return buf.raw
+
+
+class EpComm:
+    """NCCL communicator of the C-ABI EP exchange (moe_ep_dispatch / moe_ep_combine)."""
+
+    def __init__(self, unique_id: bytes, world: int, rank: int, device: int = 0):
+        h = C.c_void_p()
+        _ep_check(lib().moe_ep_comm_init(C.create_string_buffer(unique_id, 128), world, rank, device, C.byref(h)))
+        self._h, self.world, self.rank = h, world, rank
+
+    def dispatch(self, x_local, T_local: int, d: int, x_all, stream=None):
+        """All-gather of bf16 token rows: x_all[world*T_local][d]."""
+        _ep_check(lib().moe_ep_dispatch(self._h, _ptr(x_local), T_local, d, _ptr(x_all), stream))
+
+    def combine(self, part, T_local: int, d: int, mine, stream=None):
+        """Reduce-scatter of fp32 shares: mine[T_local][d] = sum over ranks."""
+        _ep_check(lib().moe_ep_combine(self._h, _ptr(part), T_local, d, _ptr(mine), stream))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().moe_ep_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ----------------------------------------------------------------- reconfiguration (f1)

@@ -86,6 +86,28 @@ def reduce_scatter_rows(dist, out, inp, group=None):
         out.copy_(tmp[r * n:(r + 1) * n])
 
 
+class CapiExchange:
+    """The exchange through the C ABI (moe_ep_dispatch / moe_ep_combine on
+    an NCCL communicator of the library's own), instead of
+    torch.distributed's collectives.  `dist` only carries the unique id."""
+
+    def __init__(self, moe, dist, rank: int, world: int, device: int, stream_fn):
+        obj = [moe.ep_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        self.comm = moe.EpComm(obj[0], world, rank, device)
+        self.stream_fn = stream_fn
+
+    def all_gather_rows(self, out, inp):
+        n = inp.numel()
+        self.comm.dispatch(inp, 1, n, out, self.stream_fn())
+
+    def reduce_scatter_rows(self, out, inp):
+        self.comm.combine(inp, 1, out.numel(), out, self.stream_fn())
+
+    def close(self):
+        self.comm.close()
+
+
 class ExpertParallelDecoder:
     """Decode through an L-layer MoE stack with the experts sharded across
     the ranks of `group`.  `ops` supplies the per-layer arithmetic:
@@ -97,8 +119,10 @@ class ExpertParallelDecoder:
       ops.empty_rows(n, fp32) / ops.num_layers / ops.d
     """
 
-    def __init__(self, dist, ops, rank: int, world: int, T_local: int, experts_per_layer: int, group=None):
+    def __init__(self, dist, ops, rank: int, world: int, T_local: int, experts_per_layer: int, group=None,
+                 exchange=None):
         self.dist, self.ops, self.rank, self.world, self.group = dist, ops, rank, world, group
+        self.exchange = exchange  # CapiExchange, or None: torch.distributed collectives
         self.T_local, self.T = T_local, T_local * world
         self.mask = expert_mask(rank, experts_per_layer, world)
         d = ops.d
@@ -109,11 +133,17 @@ class ExpertParallelDecoder:
 
     def layer(self, layer: int, x_local, out_local):
         ops, T = self.ops, self.T
-        all_gather_rows(self.dist, self.xg, x_local, self.group)
+        if self.exchange is not None:
+            self.exchange.all_gather_rows(self.xg, x_local)
+        else:
+            all_gather_rows(self.dist, self.xg, x_local, self.group)
         state = ops.route(layer, self.xg, T)
         y = ops.ffn(layer, state, T)
         ops.combine_partial(state, y, self.mask, T, self.part)
-        reduce_scatter_rows(self.dist, self.mine, self.part, self.group)
+        if self.exchange is not None:
+            self.exchange.reduce_scatter_rows(self.mine, self.part)
+        else:
+            reduce_scatter_rows(self.dist, self.mine, self.part, self.group)
         ops.residual_add(x_local, self.mine, out_local)
         return state
 

@@ -193,3 +193,31 @@ def test_ep_virtual_ranks_gpu(moe, cuda, world, T):
 class _Dev:
     def __init__(self, ptr, n):
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i2", "data": (ptr, False), "version": 3}
+
+
+def test_ep_capi_unique_id(moe):
+    """moe_ep_unique_id needs NCCL but no GPU (bootstrap handle)."""
+    uid = moe.ep_unique_id()
+    assert len(uid) == 128 and any(uid)
+    with pytest.raises(moe.MoeError):
+        moe.EpComm(uid, 2, 5)  # rank outside the world: usage error before any NCCL call
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T_local", [1, 5])
+def test_ep_capi_single_rank_gpu(moe, cuda, T_local):
+    """World-1 C-ABI exchange: dispatch is a copy of the rows, combine a copy
+    of the shares (the multi-rank semantics are NCCL's all-gather /
+    reduce-scatter; one GPU per rank, so N > 1 runs under torchrun)."""
+    import torch
+    uid = moe.ep_unique_id()
+    comm = moe.EpComm(uid, 1, 0, 0)
+    x = torch.randint(-3000, 3000, (T_local * D,), dtype=torch.int16, device=cuda)
+    xa = torch.zeros_like(x)
+    comm.dispatch(x, T_local, D, xa, torch.cuda.current_stream().cuda_stream)
+    p = torch.randn(T_local * D, device=cuda)
+    m = torch.zeros_like(p)
+    comm.combine(p, T_local, D, m, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(xa, x) and torch.equal(m, p)
+    comm.close()
