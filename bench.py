@@ -364,7 +364,8 @@ def run_ours(args, rank, world, device):
                          "kernel": "expert FFN per layer: stream_kernel (gate/up) + finalize_h + "
                                    "stream_kernel (down) + finalize_out, CUDA events on the engine stream",
                          "bytes_per_launch": round(avg_bytes), "ms_per_launch": round(avg_ms, 5),
-                         "ffn_share_of_step": round(ffn_share, 4)},
+                         "ffn_share_of_step": round(ffn_share, 4),
+                         "frac_of_nominal_8000_gbs": round(achieved / 8000.0, 4)},
             "gpu_launches": kps * (args.steps),
             "kernels_per_step": kps,
             "clocks": clocks,
