@@ -31,17 +31,13 @@
 namespace moek {
 namespace tc {
 
-constexpr int kThreads = 256;
 constexpr int kM = 128;        // weight rows per tile (UMMA M)
 constexpr int kKc = 64;        // K per chunk (one 128-byte swizzle atom of 16-bit values)
 constexpr int kTileBytes = kM * kKc * 2;  // 16 KB (A tile; B tile is the same for kN = 128)
-// raw stage: [A_gate raw 16 KB][A_up raw 16 KB][scales 2 x 256 B][B raw 16 KB]
+// raw stage: [A_gate raw 16 KB][A_up raw 16 KB][scales 2 x 256 B]
 constexpr int kRawA = 16384;
 constexpr int kRawS = 256;
 constexpr int kRawBytes = 2 * kRawA + 2 * kRawS;  // weights only: token rows go straight to the canonical tile
-// canonical stage: [A_gate 16 KB][A_up 16 KB][B 16 KB], 1024-aligned
-constexpr int kCanBytes = 3 * kTileBytes;
-constexpr int kSmemBytes = 1024 + 2 * kRawBytes + 2 * kCanBytes;
 
 struct TcArgs {
     // B operand tensor maps (2D: K x rows in slot order, 64 x 64 boxes,
@@ -64,17 +60,6 @@ struct TcArgs {
 
 MOE_DEVI uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
-MOE_DEVI void cp_async16(void* dst, const void* src, int src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s32(dst)), "l"(src), "r"(src_bytes) : "memory");
-}
-MOE_DEVI void cp_async8(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s32(dst)), "l"(src) : "memory");
-}
-MOE_DEVI void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-MOE_DEVI void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-MOE_DEVI void mbar_init(uint64_t* bar) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(bar)) : "memory"); }
 MOE_DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -166,11 +151,12 @@ MOE_DEVI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar
         : "memory");
 }
 
-// Warp roles (12 warps): 0 = TMA producer of raw weight blocks, 1 = MMA
-// issuer (one lane), 2 = token-row producer (cp.async straight into the
-// canonical tile), 4..11 = converters (raw -> canonical) and the epilogue.  kRaw raw stages and kCan canonical stages, all handed over by
-// mbarriers, so the producer runs up to kRaw chunks ahead of the converters
-// and the converters one canonical stage ahead of the tensor core.
+// Warp roles (12 warps): 0 = bulk-copy producer of raw weight blocks, 1 =
+// MMA issuer (one lane), 2 = TMA producer of the token-row (B) boxes, 4..11 =
+// converters (raw -> canonical A tiles) and then the epilogue.  kRaw raw
+// stages, kCan canonical A stages and kBst B stages, all handed over by
+// mbarriers: the producers run ahead of the converters, the converters one
+// canonical stage ahead of the tensor core.
 constexpr int kThreads2 = 384;
 constexpr int kConvThreads = 256;
 constexpr int kRaw = 2, kCan = 2;
