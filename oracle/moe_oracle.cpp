@@ -429,10 +429,16 @@ inline BlockPos block_pos(int row, int k, int cols) {
     return b;
 }
 
-inline size_t bf16_block_index(const BlockPos& b) {  // in uint16 units
-    // part kk = r/4 holds lane's {a0, a1, a2, a3} of MMA kk: word (hi*2 + half)
-    return b.block * 2048 +
-           static_cast<size_t>(((b.r / 4) * 32 + b.lane) * 8 + (((b.r / 2) % 2) * 2 + b.half) * 2 + b.r % 2);
+// bf16 block = 16 rows x 128 K in UMMA "core matrix" order: [K half h][row
+// half cr][8-K column cc][row r8][8 K values] -- an 8 x 8 core matrix is 128
+// contiguous bytes, so a 64-K half is a canonical no-swizzle K-major tile
+// (core stride 128 B along K, 1024 B along M) and ldmatrix.x4 yields the
+// mma.m16n8k16 A fragments.
+inline size_t bf16_block_index(int row, int k, int cols) {  // in uint16 units
+    const size_t block = static_cast<size_t>(row / 16) * (cols / 128) + k / 128;
+    const int kin = k % 128, rr = row % 16;
+    return block * 2048 + static_cast<size_t>((kin / 64) * 1024 + (rr / 8) * 512 + ((kin % 64) / 8) * 64 + (rr % 8) * 8 +
+                                              kin % 8);
 }
 
 inline size_t int4_block_word(const BlockPos& b) {  // in uint32 units
@@ -444,13 +450,13 @@ inline size_t int4_block_word(const BlockPos& b) {  // in uint32 units
 void orc_pack_bf16_blocks(const uint16_t* w, int rows, int cols, uint16_t* out) {
 #pragma omp parallel for schedule(static)
     for (int r = 0; r < rows; ++r)
-        for (int c = 0; c < cols; ++c) out[bf16_block_index(block_pos(r, c, cols))] = w[static_cast<size_t>(r) * cols + c];
+        for (int c = 0; c < cols; ++c) out[bf16_block_index(r, c, cols)] = w[static_cast<size_t>(r) * cols + c];
 }
 
 void orc_unpack_bf16_blocks(const uint16_t* blk, int rows, int cols, uint16_t* out) {
 #pragma omp parallel for schedule(static)
     for (int r = 0; r < rows; ++r)
-        for (int c = 0; c < cols; ++c) out[static_cast<size_t>(r) * cols + c] = blk[bf16_block_index(block_pos(r, c, cols))];
+        for (int c = 0; c < cols; ++c) out[static_cast<size_t>(r) * cols + c] = blk[bf16_block_index(r, c, cols)];
 }
 
 void orc_pack_int4_blocks(const uint32_t* q, const uint16_t* s, int rows, int cols, uint32_t* qb,

@@ -239,12 +239,28 @@ MOE_DEVI void group_int4(const uint8_t* gp, const uint8_t* sc, const uint8_t* bp
 // lane's {a0, a1, a2, a3} of MMA kk, so one LDS.128 is one A operand; even
 // kk accumulate into acc, odd kk into the second chain c1.  Chunk c of the
 // bf16 activation copy holds (kk=2c: k<8, k>=8; kk=2c+1: k<8, k>=8).
+// ldmatrix.x4: the four 8x8 core matrices whose row addresses lanes 0-7,
+// 8-15, 16-23, 24-31 supply -> one mma.m16n8k16 A fragment {a0, a1, a2, a3}
+MOE_DEVI uint4 ldsm_x4(const uint8_t* p) {
+    uint4 v;
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+    return v;
+}
+
+// bf16 block in core-matrix order: K slice kk (16 wide) of the
+// 16-row block is the core matrices (row half q&1, 8-K column 2*(kk%4) +
+// (q>>1)) of K half kk/4; lane l supplies row l&7 of matrix q = l>>3.
 MOE_DEVI void group_bf16(const uint8_t* gp, const uint8_t* bp, int lane, float (&acc)[4], float (&c1)[4]) {
+    const int q = lane >> 3;
+    const uint8_t* lp = gp + (q & 1) * 1024 + (q >> 1) * 128 + (lane & 7) * 16;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         const uint4 b = lds128(bp + c * 64);
-        const uint4 e = lds128(gp + (2 * c) * 512 + lane * 16);
-        const uint4 o = lds128(gp + (2 * c + 1) * 512 + lane * 16);
+        const int k0 = 2 * c, k1 = 2 * c + 1;  // K slices of this step
+        const uint4 e = ldsm_x4(lp + (k0 >> 2) * 2048 + (k0 & 3) * 256);
+        const uint4 o = ldsm_x4(lp + (k1 >> 2) * 2048 + (k1 & 3) * 256);
         mma_bf16(acc, e.x, e.y, e.z, e.w, b.x, b.y);
         mma_bf16(c1, o.x, o.y, o.z, o.w, b.z, b.w);
     }

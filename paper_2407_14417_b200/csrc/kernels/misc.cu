@@ -102,12 +102,17 @@ __global__ void quantize_kernel(const uint16_t* __restrict__ w, int rows, int co
 }
 
 // ---- fragment-block storage layout (oracle orc_pack_*_blocks) -------------
-MOE_DEVI int perm_pos(int kin) {  // pi(k) within a 128-group
-    return ((kin & 7) >> 1) * 32 + (kin >> 4) * 4 + ((kin >> 3) & 1) * 2 + (kin & 1);
-}
 MOE_DEVI int inv_perm_pos(int p) {  // pi^-1
     const int t = p >> 5, r = p & 31;
     return (r >> 2) * 16 + ((r >> 1) & 1) * 8 + t * 2 + (r & 1);
+}
+
+// bf16 block (16 rows x 128 K) in UMMA core-matrix order (oracle
+// bf16_block_index): [K half][row half][8-K column][row][8 values].
+MOE_DEVI size_t bf16_block_pos(int row, int c, int G) {
+    const int kin = c & 127, rr = row & 15;
+    return (static_cast<size_t>(row >> 4) * G + (c >> 7)) * 2048 +
+           static_cast<size_t>((kin >> 6) * 1024 + (rr >> 3) * 512 + ((kin & 63) >> 3) * 64 + (rr & 7) * 8 + (kin & 7));
 }
 
 __global__ void pack_bf16_blocks_kernel(const uint16_t* __restrict__ w, int rows, int cols,
@@ -117,10 +122,7 @@ __global__ void pack_bf16_blocks_kernel(const uint16_t* __restrict__ w, int rows
     for (long long o = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; o < n;
          o += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int row = static_cast<int>(o / cols), c = static_cast<int>(o - static_cast<long long>(row) * cols);
-        const int rt = row >> 4, rr = row & 15, gr = rr & 7, half = rr >> 3;
-        const int p = perm_pos(c & 127), r = p & 31, lane = gr * 4 + (p >> 5);
-        const size_t blk = static_cast<size_t>(rt) * G + (c >> 7);
-        out[blk * 2048 + static_cast<size_t>(((r >> 2) * 32 + lane) * 8 + (((r >> 1) & 1) * 2 + half) * 2 + (r & 1))] = w[o];
+        out[bf16_block_pos(row, c, G)] = w[o];
     }
 }
 
@@ -132,10 +134,7 @@ __global__ void unpack_bf16_blocks_kernel(const uint16_t* __restrict__ in, int r
     for (long long o = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; o < n;
          o += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int row = static_cast<int>(o / cols), c = static_cast<int>(o - static_cast<long long>(row) * cols);
-        const int rt = row >> 4, rr = row & 15, gr = rr & 7, half = rr >> 3;
-        const int p = perm_pos(c & 127), r = p & 31, lane = gr * 4 + (p >> 5);
-        const size_t blk = static_cast<size_t>(rt) * G + (c >> 7);
-        w[o] = in[blk * 2048 + static_cast<size_t>(((r >> 2) * 32 + lane) * 8 + (((r >> 1) & 1) * 2 + half) * 2 + (r & 1))];
+        w[o] = in[bf16_block_pos(row, c, G)];
     }
 }
 

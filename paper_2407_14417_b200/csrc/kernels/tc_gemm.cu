@@ -75,6 +75,12 @@ MOE_DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
 MOE_DEVI uint64_t sdesc(uint32_t addr) {
     return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
 }
+// No-swizzle K-major descriptor over core-matrix storage (the bf16 weight
+// blocks as bulk-copied: 8 x 8 core matrices of 128 contiguous bytes, 128 B
+// apart along K (leading dimension), 1024 B apart along M (stride dimension)).
+MOE_DEVI uint64_t sdesc_core(uint32_t addr) {
+    return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (8ull << 16) | (64ull << 32) | (1ull << 46);
+}
 // kind::f16 instruction descriptor: D f32, A/B format (0 f16, 1 bf16), K-major, N, M.
 MOE_DEVI uint32_t idesc(int fmt, int n, int m) {
     return (1u << 4) | (static_cast<uint32_t>(fmt) << 7) | (static_cast<uint32_t>(fmt) << 10) |
@@ -324,7 +330,9 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
     if (tid == 0) {
         for (int s = 0; s < kRaw; ++s) {
             mbar_init_n(&raw_full[s], 1);  // producer expect_tx
-            mbar_init_n(&raw_empty[s], kConvThreads / 32);
+            // int4: freed by the converter warps; bf16: by the MMA commit (the
+            // raw core-matrix blocks are the A operand, no conversion)
+            mbar_init_n(&raw_empty[s], p4 ? kConvThreads / 32 : 1);
         }
         for (int s = 0; s < kCan; ++s) {
             mbar_init_n(&can_full[s], kConvThreads / 32);  // converter warps
@@ -381,21 +389,28 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
         // ---- MMA issuer ----
         const uint32_t id = idesc(p4 ? 0 : 1, nmma, kM);
         for (int kc = 0; kc < nk; ++kc) {
-            const int c = kc % kCan, b = kc % kBst;
-            mbar_wait(&can_full[c], (kc / kCan) & 1);
+            const int c = kc % kCan, b = kc % kBst, r = kc % kRaw;
+            if (p4)
+                mbar_wait(&can_full[c], (kc / kCan) & 1);
+            else
+                mbar_wait(&raw_full[r], (kc / kRaw) & 1);
             mbar_wait(&b_full[b], (kc / kBst) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (lane == 0) {
-                const uint32_t cb = s32(can(c)), bb = s32(bst(b));
+                const uint32_t cb = s32(can(c)), rb = s32(raw(r)), bb = s32(bst(b));
 #pragma unroll
                 for (int j = 0; j < kKc / 16; ++j) {
                     if (a.dbg & 2) break;
                     const uint64_t bdesc = sdesc(bb + j * 32);
                     const uint32_t acc = (kc > 0 || j > 0) ? 1u : 0u;
-                    umma(tmem, sdesc(cb + j * 32), bdesc, id, acc);
-                    if (nmat == 2) umma(tmem + kN, sdesc(cb + kTileBytes + j * 32), bdesc, id, acc);
+                    // A: canonical SW128 tile (int4, converted) or the raw core-matrix blocks (bf16)
+                    for (int mat = 0; mat < nmat; ++mat) {
+                        const uint64_t adesc = p4 ? sdesc(cb + mat * kTileBytes + j * 32)
+                                                  : sdesc_core(rb + mat * kRawA + j * 256);
+                        umma(tmem + mat * kN, adesc, bdesc, id, acc);
+                    }
                 }
-                umma_commit(&can_empty[c]);
+                umma_commit(p4 ? &can_empty[c] : &raw_empty[r]);
                 umma_commit(&b_empty[b]);
                 if (kc == nk - 1) umma_commit(&acc_full);
             }
@@ -407,17 +422,17 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
         ConvOffsets o0, o1;  // K halves hh = 0 / 1 (int4 word selection differs)
         conv_offsets(ct, 0, o0);
         conv_offsets(ct, 1, o1);
-        for (int kc = 0; kc < nk; ++kc) {
-            const int u = p4 ? kc >> 1 : kc;
+        for (int kc = 0; kc < (p4 ? nk : 0); ++kc) {  // bf16: nothing to convert
+            const int u = kc >> 1;
             const int r = u % kRaw, c = kc % kCan;
             mbar_wait(&raw_full[r], (u / kRaw) & 1);
             if (kc >= kCan) mbar_wait(&can_empty[c], ((kc / kCan) - 1) & 1);
-            if (!(a.dbg & 1)) convert2(p4, nmat, raw(r), can(c), ct, (kc & 1) ? o1 : o0);
+            if (!(a.dbg & 1)) convert2(true, nmat, raw(r), can(c), ct, (kc & 1) ? o1 : o0);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&can_full[c]);
-                if (!p4 || (kc & 1)) mbar_arrive(&raw_empty[r]);
+                if (kc & 1) mbar_arrive(&raw_empty[r]);
             }
         }
         mbar_wait(&acc_full, 0);
