@@ -166,6 +166,9 @@ MOE_DEVI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar
 constexpr int kThreads2 = 384;
 constexpr int kConvThreads = 256;
 constexpr int kRaw = 2, kCan = 2;
+// bf16 tiles convert nothing: the canonical A stages serve as two more raw
+// stages (a bf16 raw unit is 2 x 16 KB, the size of a canonical A stage)
+constexpr int kRawB = kRaw + kCan;
 constexpr int kCanA = 2 * kTileBytes;   // canonical A stage (gate + up)
 
 // Raw stage layout: [A_gate raw 16 KB][A_up raw 16 KB][scales 2 x 256 B][B raw 16 KB].
@@ -309,13 +312,15 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
     // 1024-byte aligned base by pointer arithmetic (keeps the shared address
     // space, so the converters use LDS/STS, not generic loads/stores)
     uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
-    __shared__ __align__(8) uint64_t raw_full[kRaw], raw_empty[kRaw], can_full[kCan], can_empty[kCan], b_full[kBst],
+    __shared__ __align__(8) uint64_t raw_full[kRawB], raw_empty[kRawB], can_full[kCan], can_empty[kCan], b_full[kBst],
         b_empty[kBst], acc_full;
     __shared__ uint32_t tmem_slot;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     auto can = [&](int s) { return smem + s * kCanA; };
     auto bst = [&](int s) { return smem + kCan * kCanA + s * Cf::kBTile; };
-    auto raw = [&](int s) { return smem + kCan * kCanA + kBst * Cf::kBTile + s * kRawBytes; };
+    auto raw = [&](int s) {
+        return s < kRaw ? smem + kCan * kCanA + kBst * Cf::kBTile + s * kRawBytes : smem + (s - kRaw) * kCanA;
+    };
 
     pdl_wait();
     pdl_trigger();
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
     // UMMA N: the tile's tokens rounded up to 16 (M = 128 allows 16..256)
     const int nmma = min(kN, (tl.m + 15) / 16 * 16);
     if (tid == 0) {
-        for (int s = 0; s < kRaw; ++s) {
+        for (int s = 0; s < kRawB; ++s) {
             mbar_init_n(&raw_full[s], 1);  // producer expect_tx
             // int4: freed by the converter warps; bf16: by the MMA commit (the
             // raw core-matrix blocks are the A operand, no conversion)
@@ -356,6 +361,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_slot;
     const int nk = K / kKc;
+    const int nraw = p4 ? kRaw : kRawB;  // raw stages in use
 
     if (warp == 0) {
         // ---- weight producer: kRaw chunks ahead of the converters ----
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
         // whose 1 KB blocks hold both K halves (loaded once, converted twice)
         for (int kc = 0; kc < nk; kc += p4 ? 2 : 1) {
             const int u = p4 ? kc >> 1 : kc;
-            const int r = u % kRaw, pass = u / kRaw;
+            const int r = u % nraw, pass = u / nraw;
             if (pass > 0) mbar_wait(&raw_empty[r], (pass - 1) & 1);
             if (a.dbg & 4) {
                 if (lane == 0) mbar_arrive(&raw_full[r]);
@@ -389,11 +395,11 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
         // ---- MMA issuer ----
         const uint32_t id = idesc(p4 ? 0 : 1, nmma, kM);
         for (int kc = 0; kc < nk; ++kc) {
-            const int c = kc % kCan, b = kc % kBst, r = kc % kRaw;
+            const int c = kc % kCan, b = kc % kBst, r = kc % nraw;
             if (p4)
                 mbar_wait(&can_full[c], (kc / kCan) & 1);
             else
-                mbar_wait(&raw_full[r], (kc / kRaw) & 1);
+                mbar_wait(&raw_full[r], (kc / nraw) & 1);
             mbar_wait(&b_full[b], (kc / kBst) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (lane == 0) {
