@@ -171,8 +171,9 @@ constexpr int kRaw = 2, kCan = 2;
 constexpr int kRawB = kRaw + kCan;
 constexpr int kCanA = 2 * kTileBytes;   // canonical A stage (gate + up)
 
-// Raw stage layout: [A_gate raw 16 KB][A_up raw 16 KB][scales 2 x 256 B][B raw 16 KB].
-// bf16: 8 block halves of 2 KB per matrix (parts 4hh..4hh+3 of each block).
+// Raw stage layout: [A_gate raw 16 KB][A_up raw 16 KB][scales 2 x 256 B].
+// bf16: the 64-K half (2 KB, core-matrix order) of each of the 8 row blocks
+//       per matrix -- a canonical no-swizzle K-major A tile as it lands.
 // int4: the whole 1 KB block per row tile (both K halves; the convert step
 //       picks words 2hh, 2hh+1), 8 KB per matrix, + 8 x 32 B scales.
 MOE_DEVI uint32_t raw_bytes(bool p4, int nmat) { return nmat * (p4 ? 8 * 1024 + 256 : 16384); }
@@ -214,24 +215,12 @@ MOE_DEVI void tma_load_b(void* dst, const CUtensorMap* tm, int k0, int row0, uin
 
 // per-converter-thread swizzled destinations (identical for every chunk)
 struct ConvOffsets {
-    int a[4][4];   // bf16: piece j -> 4 word destinations
     int q[2][8];   // int4: item j -> 8 word destinations
     int qrow[2];   // int4: item j -> (raw word offset, scale offset) packed
     int qsc[2];
 };
 
 MOE_DEVI void conv_offsets(int ct, int hh, ConvOffsets& o) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int pc = ct + j * kConvThreads;
-        const int i = pc >> 7, kq = (pc >> 5) & 3, L = pc & 31;
-        const int rlo = i * 16 + (L >> 2), rhi = rlo + 8;
-        const int kb = (kq * 16 + 2 * (L & 3)) * 2;
-        o.a[j][0] = swz(rlo, kb);
-        o.a[j][1] = swz(rhi, kb);
-        o.a[j][2] = swz(rlo, kb + 16);
-        o.a[j][3] = swz(rhi, kb + 16);
-    }
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int it = ct + j * kConvThreads;
@@ -251,50 +240,39 @@ MOE_DEVI void conv_offsets(int ct, int hh, ConvOffsets& o) {
     }
 }
 
-MOE_DEVI void convert2(bool p4, int nmat, const uint8_t* raw, uint8_t* can, int ct, const ConvOffsets& o) {
+// int4 raw blocks -> fp16 q*s in the canonical SW128 A tile (bf16 blocks are
+// already in core-matrix order and feed the MMA directly)
+MOE_DEVI void convert_int4(int nmat, const uint8_t* raw, uint8_t* can, int ct, const ConvOffsets& o) {
     for (int mat = 0; mat < nmat; ++mat) {
         const uint8_t* src = raw + mat * kRawA;
         uint8_t* dst = can + mat * kTileBytes;
-        if (!p4) {
+        const uint8_t* sc = raw + 2 * kRawA + mat * kRawS;
+        const __half2 m1032 = __halves2half2(__ushort_as_half(0xE408), __ushort_as_half(0xE408));
+        const __half2 m72 = __halves2half2(__ushort_as_half(0xD480), __ushort_as_half(0xD480));
+        const __half2 r16 = __halves2half2(__ushort_as_half(0x2C00), __ushort_as_half(0x2C00));
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint4 v = *reinterpret_cast<const uint4*>(src + (ct + j * kConvThreads) * 16);
-                *reinterpret_cast<uint32_t*>(dst + o.a[j][0]) = v.x;
-                *reinterpret_cast<uint32_t*>(dst + o.a[j][1]) = v.y;
-                *reinterpret_cast<uint32_t*>(dst + o.a[j][2]) = v.z;
-                *reinterpret_cast<uint32_t*>(dst + o.a[j][3]) = v.w;
-            }
-        } else {
-            const uint8_t* sc = raw + 2 * kRawA + mat * kRawS;
-            const __half2 m1032 = __halves2half2(__ushort_as_half(0xE408), __ushort_as_half(0xE408));
-            const __half2 m72 = __halves2half2(__ushort_as_half(0xD480), __ushort_as_half(0xD480));
-            const __half2 r16 = __halves2half2(__ushort_as_half(0x2C00), __ushort_as_half(0x2C00));
+        for (int j = 0; j < 2; ++j) {
+            const uint2 w2 = *reinterpret_cast<const uint2*>(src + o.qrow[j]);
+            const uint16_t sb = *reinterpret_cast<const uint16_t*>(sc + o.qsc[j]);
+            const __half sh = __float2half_rn(bf2f(sb));  // exact for normal-range scales
+            const __half2 s2 = __halves2half2(sh, sh);
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const uint2 w2 = *reinterpret_cast<const uint2*>(src + o.qrow[j]);
-                const uint16_t sb = *reinterpret_cast<const uint16_t*>(sc + o.qsc[j]);
-                const __half sh = __float2half_rn(bf2f(sb));  // exact for normal-range scales
-                const __half2 s2 = __halves2half2(sh, sh);
+            for (int qi = 0; qi < 2; ++qi) {
+                const uint32_t w = qi ? w2.y : w2.x;
+                uint32_t v[4] = {and_or(w, 0x000F000Fu, 0x64006400u), and_or(w, 0x00F000F0u, 0x64006400u),
+                                 and_or(w >> 8, 0x000F000Fu, 0x64006400u), and_or(w >> 8, 0x00F000F0u, 0x64006400u)};
 #pragma unroll
-                for (int qi = 0; qi < 2; ++qi) {
-                    const uint32_t w = qi ? w2.y : w2.x;
-                    uint32_t v[4] = {and_or(w, 0x000F000Fu, 0x64006400u), and_or(w, 0x00F000F0u, 0x64006400u),
-                                     and_or(w >> 8, 0x000F000Fu, 0x64006400u), and_or(w >> 8, 0x00F000F0u, 0x64006400u)};
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        __half2 h = *reinterpret_cast<__half2*>(&v[u]);
-                        h = (u & 1) ? __hfma2(h, r16, m72) : __hadd2(h, m1032);  // q exactly
-                        h = __hmul2(h, s2);                                      // q*s exactly
-                        *reinterpret_cast<__half2*>(dst + o.q[j][qi * 4 + u]) = h;
-                    }
+                for (int u = 0; u < 4; ++u) {
+                    __half2 h = *reinterpret_cast<__half2*>(&v[u]);
+                    h = (u & 1) ? __hfma2(h, r16, m72) : __hadd2(h, m1032);  // q exactly
+                    h = __hmul2(h, s2);                                      // q*s exactly
+                    *reinterpret_cast<__half2*>(dst + o.q[j][qi * 4 + u]) = h;
                 }
             }
         }
     }
 }
 
-// NT tokens per tile (UMMA N): 128, or 256 for prefill-sized segments (twice
-// the MMA work per staged weight chunk; both TMEM halves hold gate / up).
 template <int NT>
 struct TcCfg {
     static constexpr int kN = NT;
@@ -433,7 +411,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
             const int r = u % kRaw, c = kc % kCan;
             mbar_wait(&raw_full[r], (u / kRaw) & 1);
             if (kc >= kCan) mbar_wait(&can_empty[c], ((kc / kCan) - 1) & 1);
-            if (!(a.dbg & 1)) convert2(true, nmat, raw(r), can(c), ct, (kc & 1) ? o1 : o0);
+            if (!(a.dbg & 1)) convert_int4(nmat, raw(r), can(c), ct, (kc & 1) ? o1 : o0);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
