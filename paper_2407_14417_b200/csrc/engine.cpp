@@ -174,6 +174,14 @@ struct MoeEngine::Impl {
             throw std::runtime_error("no CUDA device: the MoE engine has no CPU fallback");
         ck(cudaSetDevice(c.device), "cudaSetDevice");
         ck(cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking), "stream");
+        if (c.keep_masters) {
+            // reconfigure() allocates per-expert copies stream-ordered: keep
+            // freed pool memory mapped instead of returning it at every sync
+            cudaMemPool_t pool;
+            ck(cudaDeviceGetDefaultMemPool(&pool, c.device), "mempool");
+            uint64_t keep = UINT64_MAX;
+            ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "mempool attr");
+        }
         ck(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "stream");
         ck(cudaEventCreateWithFlags(&copy_done, cudaEventDisableTiming), "event");
         if (c.lru_capacity > 0 && c.lru_capacity < c.profile.top_k)

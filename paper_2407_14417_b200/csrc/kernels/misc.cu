@@ -126,15 +126,20 @@ __global__ void pack_bf16_blocks_kernel(const uint16_t* __restrict__ w, int rows
     }
 }
 
-// Inverse of pack_bf16_blocks_kernel: fragment blocks -> logical row-major.
+// Inverse of pack_bf16_blocks_kernel, walked in storage order (coalesced
+// reads; each 8-value core-matrix row is one contiguous 16-byte write).
 __global__ void unpack_bf16_blocks_kernel(const uint16_t* __restrict__ in, int rows, int cols,
                                           uint16_t* __restrict__ w) {
     const long long n = static_cast<long long>(rows) * cols;
     const int G = cols / 128;
-    for (long long o = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; o < n;
-         o += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int row = static_cast<int>(o / cols), c = static_cast<int>(o - static_cast<long long>(row) * cols);
-        w[o] = in[bf16_block_pos(row, c, G)];
+    for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+         p += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int e = static_cast<int>(p & 7), r8 = static_cast<int>((p >> 3) & 7), cc = static_cast<int>((p >> 6) & 7);
+        const int cr = static_cast<int>((p >> 9) & 1), h = static_cast<int>((p >> 10) & 1);
+        const long long blk = p >> 11;
+        const int rt = static_cast<int>(blk / G), g = static_cast<int>(blk - static_cast<long long>(rt) * G);
+        const int row = rt * 16 + cr * 8 + r8, c = g * 128 + h * 64 + cc * 8 + e;
+        w[static_cast<size_t>(row) * cols + c] = in[p];
     }
 }
 
