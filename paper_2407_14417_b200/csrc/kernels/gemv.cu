@@ -73,6 +73,7 @@ using CfgBatch = StreamCfg<8, 8192, 4608>;
 // terms) is loaded once per launch into shared memory; items carry only weights
 using CfgDecode = StreamCfg<8, 8192, 0, true>;
 constexpr int kChunk = 2;                // items per dynamic tail chunk
+constexpr int kSmallPool = 2048;         // pools up to this many items are handed out one item per grab
 constexpr int kMaxSlots = 512;           // permutation slots staged in smem by build_segs
 
 struct StreamArgs {
@@ -420,9 +421,10 @@ struct Sched {
     int RT;
     Item it;               // item of index cur-1 (valid once started)
     int started;
+    int chunk;             // items per pool grab
 
     MOE_DEVI void grab_ahead() {
-        if (lane == 0) pend = atomicAdd(ctr, static_cast<unsigned>(kChunk));
+        if (lane == 0) pend = atomicAdd(ctr, static_cast<unsigned>(chunk));
     }
     MOE_DEVI void step(const SegTable& st) {
         if (++it.kp == st.kp[it.s]) {
@@ -444,7 +446,7 @@ struct Sched {
             if (start >= N) return false;
             jump = jump || start != cur;
             cur = start;
-            end = min(start + kChunk, N);
+            end = min(start + chunk, N);
             grab_ahead();
         }
         if (jump)
@@ -533,7 +535,11 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
 
     // static part: contiguous equal ranges over the first ~7/8 of the items
     const int N = st.N;
-    const int ns = N - min(N / 8, W * kChunk * 2);
+    // single-item grabs while the pool is small enough for one counter's
+    // atomic throughput (int4-heavy launches: a shorter tail); pairs above
+    const int pool = min(N / 8, W * kChunk * 2);
+    const int chunk = pool <= kSmallPool ? 1 : kChunk;
+    const int ns = N - pool;
     const int qs = ns / W, rs = ns - qs * W;
     Sched sc;
     sc.ctr = a.sched;
@@ -547,6 +553,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
     sc.RT = a.rows / 16;
     sc.started = 0;
     sc.it = Item{0, 0, 0};
+    sc.chunk = chunk;
 
     Item it0{0, 0, 0}, it1{0, 0, 0};
     int npro = 0;
