@@ -73,7 +73,7 @@ using CfgBatch = StreamCfg<8, 8192, 4608>;
 // terms) is loaded once per launch into shared memory; items carry only weights
 using CfgDecode = StreamCfg<8, 8192, 0, true>;
 constexpr int kChunk = 2;                // items per dynamic tail chunk
-constexpr int kSmallPool = 2048;         // pools up to this many items are handed out one item per grab
+constexpr int kSmallPool = 5000;         // pools up to this many items are handed out one item per grab
 constexpr int kMaxSlots = 512;           // permutation slots staged in smem by build_segs
 
 struct StreamArgs {
