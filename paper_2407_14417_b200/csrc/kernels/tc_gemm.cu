@@ -118,12 +118,13 @@ struct Tile {
     int e, slot0, m, R0;  // expert, first slot, tokens in tile, first weight row
 };
 
+// offs: the routing's expert offsets [E+1], staged in shared memory
 template <int NT>
-MOE_DEVI bool find_tile(const TcArgs& a, int RT, int b, Tile& tl) {
+MOE_DEVI bool find_tile(const TcArgs& a, const int* offs, int RT, int b, Tile& tl) {
     constexpr int kN = NT;
     for (int e = 0; e < a.E; ++e) {
         if (!((a.active_mask >> e) & 1ull)) continue;
-        const int o0 = a.offsets[e], m = a.offsets[e + 1] - o0;
+        const int o0 = offs[e], m = offs[e + 1] - o0;
         if (m == 0) continue;
         const int nt = (m + kN - 1) / kN;
         if (b < nt * RT) {
@@ -304,8 +305,12 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
     pdl_trigger();
     const int K = a.p == 0 ? a.d : a.f;
     const int RT = (a.p == 0 ? a.f : a.d) / kM;
+    // the E+1 offsets in one parallel load instead of a dependent chain
+    __shared__ int s_off[MOE_MAX_EXPERTS + 1];
+    if (tid <= a.E) s_off[tid] = a.offsets[tid];
+    __syncthreads();
     Tile tl;
-    if (!find_tile<NT>(a, RT, blockIdx.x, tl)) return;
+    if (!find_tile<NT>(a, s_off, RT, blockIdx.x, tl)) return;
     const int nmat = a.p == 0 ? 2 : 1;
     const bool p4 = a.ex[tl.e].precision == MOE_P4;
     // UMMA N: the tile's tokens rounded up to 16 (M = 128 allows 16..256)
