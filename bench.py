@@ -517,9 +517,15 @@ def run_ep(args, rank, world, device):
     eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan, max_tokens=T, seed=args.seed, device=device,
                         norm_eps=NORM_EPS)
     ops = ep.EngineOps(moe, torch, eng, rank, world, T, NORM_EPS, torch.device(f"cuda:{device}"))
-    # exchange: the library's C-ABI NCCL path (moe_ep_dispatch / moe_ep_combine),
-    # or torch.distributed's collectives with --ep-torch
-    exch = None if args.ep_torch else ep.CapiExchange(moe, dist, rank, world, device, ops._stream)
+    # exchange: the library's C-ABI NCCL path (moe_ep_dispatch / moe_ep_combine, default),
+    # the fused peer-memory kernels over CUDA IPC (--ep-exchange peer), or
+    # torch.distributed's collectives (--ep-exchange torch)
+    if args.ep_exchange == "torch":
+        exch = None
+    elif args.ep_exchange == "peer":
+        exch = ep.PeerExchange(moe, torch, rank, world, T_local, D_MODEL, torch.device(f"cuda:{device}"), dist=dist)
+    else:
+        exch = ep.CapiExchange(moe, dist, rank, world, device, ops._stream)
     dec = ep.ExpertParallelDecoder(dist, ops, rank, world, T_local, EXPERTS, exchange=exch)
     eng.synth_input(0, T)
     eng.sync()
@@ -569,8 +575,11 @@ def run_ep(args, rank, world, device):
             "config": {"workload": "mixtral8x7b-shape 32-layer MoE stack, expert-parallel batch-%d/GPU decode" % T_local,
                        "n4": args.n4, "of": LAYERS * EXPERTS, "layer": "x + MoE(RMSNorm(x))",
                        "parallelism": "ep%d" % world, "experts_per_gpu_per_layer": EXPERTS // world if world <= EXPERTS else 1,
-                       "exchange": "NCCL all-gather (dispatch) + reduce-scatter (combine) per layer, via " +
-                                   ("torch.distributed" if args.ep_torch else "the C ABI (moe_ep_dispatch / moe_ep_combine)"),
+                       "exchange": {"torch": "NCCL all-gather + reduce-scatter per layer via torch.distributed",
+                                    "capi": "NCCL all-gather + reduce-scatter per layer via the C ABI "
+                                            "(moe_ep_dispatch / moe_ep_combine)",
+                                    "peer": "fused peer-memory kernels over CUDA IPC (moe_ep_push_rows / "
+                                            "moe_ep_push_shares / moe_ep_reduce), no collective"}[args.ep_exchange],
                        "exchange_bytes_per_layer_per_gpu": xb, "batch_per_gpu": T_local,
                        "l2": "no flush: every step streams GBs of distinct expert weights per GPU"},
             "e2e": {"value": round(world * T_local / e2e_s, 3), "unit": "tokens/s",
@@ -602,7 +611,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of expert parallel")
     ap.add_argument("--ep", action="store_true", help="expert-parallel code path even at N=1 (NCCL, 1 rank)")
-    ap.add_argument("--ep-torch", action="store_true", help="EP exchange via torch.distributed instead of the C ABI")
+    ap.add_argument("--ep-exchange", choices=["capi", "peer", "torch"], default="capi",
+                    help="EP exchange: C-ABI NCCL (default), fused peer-memory kernels, or torch.distributed")
     ap.add_argument("--no-batch-sweep", dest="batch_sweep", action="store_false")
     ap.add_argument("--tc-min", type=int, default=32, help="batch-sweep engine: tcgen05 expert GEMM from this T")
     ap.add_argument("--batch-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],

@@ -362,6 +362,31 @@ int moe_ep_comm_wrap(void* nccl_comm, int world, int rank, moe_ep_comm** out);  
 void moe_ep_comm_destroy(moe_ep_comm* comm);
 int moe_ep_dispatch(moe_ep_comm* comm, const void* x_local, int T_local, int d, void* x_all, void* stream);
 int moe_ep_combine(moe_ep_comm* comm, const float* part, int T_local, int d, float* mine, void* stream);
+
+/* The same exchange fused into the kernels that produce it, over peer memory
+ * (NVLink P2P / CUDA IPC) instead of collectives.  Each rank owns one zeroed
+ * device buffer of moe_ep_peer_bytes and knows the G ranks' buffers (`bases`,
+ * its own included; IPC handles via moe_ep_peer_ipc_*).  Per layer, epoch + 1:
+ *   moe_ep_push_rows    own rows -> every peer's gather slot `rank`, release flag
+ *   moe_ep_wait_rows    until every rank's rows arrived; gathered rows at
+ *                       moe_ep_peer_rows(base) [G*T_local][d]
+ *   (route + own experts on the gathered rows)
+ *   moe_ep_push_shares  moe_combine_partial's share written straight into
+ *                       each owner's receive slot `rank`, release flag
+ *   moe_ep_reduce       out = bf16(x + sum over src in order) once all arrived */
+size_t moe_ep_peer_bytes(int G, int T_local, int d);
+void* moe_ep_peer_rows(void* base);
+int moe_ep_peer_ipc_handle(const void* base, char handle[64]);
+int moe_ep_peer_ipc_open(const char handle[64], void** peer_base);
+int moe_ep_peer_ipc_close(void* peer_base);
+int moe_ep_push_rows(const void* x_local, int T_local, int d, int rank, int G, const void* const* bases,
+                     uint32_t epoch, void* stream);
+int moe_ep_wait_rows(const void* my_base, int G, int T_local, int d, uint32_t epoch, void* stream);
+int moe_ep_push_shares(const float* y_perm, const int32_t* inv_perm, const float* w, const int32_t* idx,
+                       uint64_t expert_mask, int T_local, int d, int k, int rank, int G, const void* const* bases,
+                       uint32_t epoch, void* stream);
+int moe_ep_reduce(const void* x_local, int T_local, int d, int rank, int G, const void* const* bases,
+                  uint32_t epoch, void* out, void* stream);
 /* Execute diff_plans(current, target) on the device (needs keep_masters):
  * Offload releases HBM, Fetch / in-place Dequantize copy host copies in,
  * Quantize of a device-resident expert runs the int4-g128 quantiser on the

@@ -120,6 +120,15 @@ def lib() -> C.CDLL:
         "moe_ep_comm_destroy": (None, [VP]),
         "moe_ep_dispatch": (I, [VP, VP, I, I, VP, VP]),
         "moe_ep_combine": (I, [VP, VP, I, I, VP, VP]),
+        "moe_ep_peer_bytes": (C.c_size_t, [I, I, I]),
+        "moe_ep_peer_rows": (VP, [VP]),
+        "moe_ep_peer_ipc_handle": (I, [VP, C.c_char_p]),
+        "moe_ep_peer_ipc_open": (I, [C.c_char_p, P(VP)]),
+        "moe_ep_peer_ipc_close": (I, [VP]),
+        "moe_ep_push_rows": (I, [VP, I, I, I, I, P(VP), C.c_uint32, VP]),
+        "moe_ep_wait_rows": (I, [VP, I, I, I, C.c_uint32, VP]),
+        "moe_ep_push_shares": (I, [VP, VP, VP, VP, U64, I, I, I, I, I, P(VP), C.c_uint32, VP]),
+        "moe_ep_reduce": (I, [VP, I, I, I, I, P(VP), C.c_uint32, VP, VP]),
         "moe_version": (I, []),
         "moe_profile_builtin": (I, [I, P(_ModelProfile)]),
         "moe_profile_for_shape": (I, [I, I, I, I, I, I64, P(_ModelProfile)]),
@@ -506,6 +515,48 @@ class EpComm:
             self.close()
         except Exception:
             pass
+
+
+def ep_peer_bytes(G: int, T_local: int, d: int) -> int:
+    return lib().moe_ep_peer_bytes(G, T_local, d)
+
+
+def ep_peer_ipc_handle(base_ptr: int) -> bytes:
+    buf = C.create_string_buffer(64)
+    _check(lib().moe_ep_peer_ipc_handle(base_ptr, buf))
+    return buf.raw
+
+
+def ep_peer_ipc_open(handle: bytes) -> int:
+    p = C.c_void_p()
+    _check(lib().moe_ep_peer_ipc_open(C.create_string_buffer(handle, 64), C.byref(p)))
+    return p.value
+
+
+class PeerBases:
+    """The G exchange-buffer base pointers of moe_ep_push_rows & co."""
+
+    def __init__(self, ptrs):
+        self.G = len(ptrs)
+        self.arr = (C.c_void_p * self.G)(*ptrs)
+
+
+def ep_push_rows(x_local, T_local: int, d: int, rank: int, bases: PeerBases, epoch: int, stream=None):
+    _check(lib().moe_ep_push_rows(_ptr(x_local), T_local, d, rank, bases.G, bases.arr, epoch, stream))
+
+
+def ep_wait_rows(my_base: int, G: int, T_local: int, d: int, epoch: int, stream=None):
+    _check(lib().moe_ep_wait_rows(my_base, G, T_local, d, epoch, stream))
+
+
+def ep_push_shares(y, inv, w, idx, mask: int, T_local: int, d: int, k: int, rank: int, bases: PeerBases, epoch: int,
+                   stream=None):
+    _check(lib().moe_ep_push_shares(_ptr(y), _ptr(inv), _ptr(w), _ptr(idx), mask, T_local, d, k, rank, bases.G,
+                                    bases.arr, epoch, stream))
+
+
+def ep_reduce(x_local, T_local: int, d: int, rank: int, bases: PeerBases, epoch: int, out, stream=None):
+    _check(lib().moe_ep_reduce(_ptr(x_local), T_local, d, rank, bases.G, bases.arr, epoch, _ptr(out), stream))
 
 
 # ----------------------------------------------------------------- reconfiguration (f1)

@@ -848,6 +848,79 @@ int moe_engine_reconfigure(moe_engine* eng, const moe_expert_state* target, uint
     });
 }
 
+namespace {
+void cuda_ok(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace
+
+size_t moe_ep_peer_bytes(int G, int T_local, int d) { return moek_ep_peer_bytes(G, T_local, d); }
+
+void* moe_ep_peer_rows(void* base) { return base; }  // the gather rows lead the buffer
+
+int moe_ep_peer_ipc_handle(const void* base, char handle[64]) {
+    return guarded([&] {
+        usage_if(base == nullptr || handle == nullptr, "null argument");
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        cudaIpcMemHandle_t h;
+        cuda_ok(cudaIpcGetMemHandle(&h, const_cast<void*>(base)), "cudaIpcGetMemHandle");
+        std::memcpy(handle, &h, sizeof h);
+    });
+}
+
+int moe_ep_peer_ipc_open(const char handle[64], void** peer_base) {
+    return guarded([&] {
+        usage_if(handle == nullptr || peer_base == nullptr, "null argument");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        cuda_ok(cudaIpcOpenMemHandle(peer_base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    });
+}
+
+int moe_ep_peer_ipc_close(void* peer_base) {
+    return guarded([&] { cuda_ok(cudaIpcCloseMemHandle(peer_base), "cudaIpcCloseMemHandle"); });
+}
+
+int moe_ep_push_rows(const void* x_local, int T_local, int d, int rank, int G, const void* const* bases,
+                     uint32_t epoch, void* stream) {
+    return guarded([&] {
+        usage_if(x_local == nullptr || bases == nullptr || rank < 0 || rank >= G, "bad argument");
+        need_device();
+        cuda_ok(moek_ep_push_rows(x_local, T_local, d, rank, G, bases, epoch, static_cast<cudaStream_t>(stream)),
+                "ep push rows");
+    });
+}
+
+int moe_ep_wait_rows(const void* my_base, int G, int T_local, int d, uint32_t epoch, void* stream) {
+    return guarded([&] {
+        usage_if(my_base == nullptr, "null argument");
+        need_device();
+        cuda_ok(moek_ep_wait_rows(my_base, G, T_local, d, epoch, static_cast<cudaStream_t>(stream)), "ep wait");
+    });
+}
+
+int moe_ep_push_shares(const float* y_perm, const int32_t* inv_perm, const float* w, const int32_t* idx,
+                       uint64_t expert_mask, int T_local, int d, int k, int rank, int G, const void* const* bases,
+                       uint32_t epoch, void* stream) {
+    return guarded([&] {
+        usage_if(y_perm == nullptr || bases == nullptr || rank < 0 || rank >= G, "bad argument");
+        need_device();
+        cuda_ok(moek_ep_push_shares(y_perm, inv_perm, w, idx, expert_mask, T_local, d, k, rank, G, bases, epoch,
+                                    static_cast<cudaStream_t>(stream)),
+                "ep push shares");
+    });
+}
+
+int moe_ep_reduce(const void* x_local, int T_local, int d, int rank, int G, const void* const* bases, uint32_t epoch,
+                  void* out, void* stream) {
+    return guarded([&] {
+        usage_if(x_local == nullptr || out == nullptr || bases == nullptr || rank < 0 || rank >= G, "bad argument");
+        need_device();
+        cuda_ok(moek_ep_reduce(x_local, T_local, d, rank, G, bases, epoch, out, static_cast<cudaStream_t>(stream)),
+                "ep reduce");
+    });
+}
+
 int moe_engine_counters(const moe_engine* eng, moe_sim_report* out) {
     return guarded([&] {
         const SimReport& r = eng->impl->counters();

@@ -74,3 +74,16 @@ int moek_weight_shift(int K);
 cudaError_t moek_debug_gemv_trace(void* buf);
 // Debug: [6 kernels][entry, after wait, end] u64 globaltimer (min/min/max); null disables.
 cudaError_t moek_debug_layer_trace(void* buf, cudaStream_t stream);
+
+// Expert-parallel exchange over peer memory (ep_peer.cu): `bases` are the G
+// ranks' exchange buffers (moek_ep_peer_bytes each, zeroed once), this
+// rank's own included; epoch increases by one per layer step.
+size_t moek_ep_peer_bytes(int G, int T_local, int d);
+cudaError_t moek_ep_push_rows(const void* x_local, int T_local, int d, int rank, int G, const void* const* bases,
+                              uint32_t epoch, cudaStream_t stream);
+cudaError_t moek_ep_wait_rows(const void* my_base, int G, int T_local, int d, uint32_t epoch, cudaStream_t stream);
+cudaError_t moek_ep_push_shares(const float* y, const int32_t* inv, const float* w, const int32_t* idx,
+                                uint64_t mask, int T_local, int d, int k, int rank, int G, const void* const* bases,
+                                uint32_t epoch, cudaStream_t stream);
+cudaError_t moek_ep_reduce(const void* x_local, int T_local, int d, int rank, int G, const void* const* bases,
+                           uint32_t epoch, void* out, cudaStream_t stream);

@@ -108,6 +108,55 @@ class CapiExchange:
         self.comm.close()
 
 
+class PeerExchange:
+    """The exchange fused into kernels over peer memory (kernels/ep_peer.cu):
+    rows are pushed straight into every peer's gather buffer, shares straight
+    into their owner's receive buffer, each followed by a system-scope
+    release flag; no collective.  Buffers are shared by CUDA IPC handles
+    (one process per GPU), or passed in directly (`bases`: one process
+    driving G virtual ranks, as the single-GPU tests do)."""
+
+    fused = True
+
+    def __init__(self, moe, torch, rank: int, world: int, T_local: int, d: int, device, dist=None, bases=None,
+                 own=None):
+        self.moe, self.torch, self.rank, self.world, self.T_local, self.d = moe, torch, rank, world, T_local, d
+        self.nbytes = moe.ep_peer_bytes(world, T_local, d)
+        self.own = own if own is not None else torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
+        if bases is None:  # one process per GPU: exchange IPC handles
+            h = moe.ep_peer_ipc_handle(self.own.data_ptr())
+            handles = [None] * world
+            dist.all_gather_object(handles, h)
+            ptrs = [self.own.data_ptr() if r == rank else moe.ep_peer_ipc_open(handles[r]) for r in range(world)]
+        else:
+            ptrs = bases
+        self.bases = moe.PeerBases(ptrs)
+        rows = T_local * world * d
+        self.xg = torch.as_tensor(_DevView(self.own.data_ptr(), rows), device=device)
+        self.epoch = 0
+
+    def push_rows(self, x_local, stream):
+        self.epoch += 1
+        self.moe.ep_push_rows(x_local, self.T_local, self.d, self.rank, self.bases, self.epoch, stream)
+
+    def wait_rows(self, stream):
+        self.moe.ep_wait_rows(self.own.data_ptr(), self.world, self.T_local, self.d, self.epoch, stream)
+
+    def push_shares(self, ops, y, mask, stream):
+        self.moe.ep_push_shares(y, ops.inv, ops.w, ops.idx, mask, self.T_local, self.d, ops.k, self.rank, self.bases,
+                                self.epoch, stream)
+
+    def reduce(self, x_local, out_local, stream):
+        self.moe.ep_reduce(x_local, self.T_local, self.d, self.rank, self.bases, self.epoch, out_local, stream)
+
+
+class _DevView:
+    """int16 view of a raw device allocation (the gather rows at the buffer's head)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i2", "data": (ptr, False), "version": 3}
+
+
 class ExpertParallelDecoder:
     """Decode through an L-layer MoE stack with the experts sharded across
     the ranks of `group`.  `ops` supplies the per-layer arithmetic:
@@ -133,6 +182,15 @@ class ExpertParallelDecoder:
 
     def layer(self, layer: int, x_local, out_local):
         ops, T = self.ops, self.T
+        if getattr(self.exchange, "fused", False):
+            ex, stream = self.exchange, ops._stream()
+            ex.push_rows(x_local, stream)
+            ex.wait_rows(stream)
+            state = ops.route(layer, ex.xg, T)
+            y = ops.ffn(layer, state, T)
+            ex.push_shares(ops, y, self.mask, stream)
+            ex.reduce(x_local, out_local, stream)
+            return state
         if self.exchange is not None:
             self.exchange.all_gather_rows(self.xg, x_local)
         else:

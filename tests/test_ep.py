@@ -221,3 +221,49 @@ def test_ep_capi_single_rank_gpu(moe, cuda, T_local):
     torch.cuda.synchronize()
     assert torch.equal(xa, x) and torch.equal(m, p)
     comm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,T_local", [(2, 2), (4, 1), (8, 1), (2, 48)])
+def test_ep_peer_exchange_virtual_ranks_gpu(moe, cuda, world, T_local):
+    """The fused peer-memory exchange (kernels/ep_peer.cu) with G virtual ranks
+    in one process: phases in rank order on one stream (push rows -> route +
+    own experts + push shares -> reduce), each rank's output rows equal to the
+    engine's single-device layer."""
+    import torch
+    from paper_2407_14417_b200 import ep
+    T = world * T_local
+    prof = moe.profile_for_shape(D, F, L)
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 1), moe.HardwareProfile(10**15), prof)
+    eng = moe.MoeEngine(L, E, K, D, F, plan, max_tokens=T, seed=SEED, use_graphs=False, norm_eps=EPS)
+    eng.synth_input(3, T)
+    eng.sync()
+    x = torch.empty(T * D, dtype=torch.int16, device=cuda)
+    x.copy_(torch.as_tensor(_Dev(eng.input_ptr, T * D), device=cuda))
+    ref = torch.empty_like(x)
+    eng.forward_layer(0, x, T, ref)
+    eng.sync()
+    nb = moe.ep_peer_bytes(world, T_local, D)
+    bufs = [torch.zeros(nb, dtype=torch.uint8, device=cuda) for _ in range(world)]
+    ptrs = [b.data_ptr() for b in bufs]
+    ops = [ep.EngineOps(moe, torch, eng, r, world, T, EPS, cuda) for r in range(world)]
+    exs = [ep.PeerExchange(moe, torch, r, world, T_local, D, cuda, bases=ptrs, own=bufs[r]) for r in range(world)]
+    xl = [x[r * T_local * D:(r + 1) * T_local * D].clone() for r in range(world)]
+    outs = [torch.empty_like(xl[r]) for r in range(world)]
+    s = torch.cuda.current_stream().cuda_stream
+    for step in range(2):  # two layer steps: epochs 1 and 2 reuse the buffers
+        for r in range(world):
+            exs[r].push_rows(xl[r], s)
+        for r in range(world):
+            exs[r].wait_rows(s)
+            assert torch.equal(exs[r].xg[:T * D], x)
+            ops[r].route(0, exs[r].xg, T)
+            y = ops[r].ffn(0, 0, T)
+            exs[r].push_shares(ops[r], y, ep.expert_mask(r, E, world), s)
+        for r in range(world):
+            exs[r].reduce(xl[r], outs[r], s)
+        torch.cuda.synchronize()
+        got = torch.cat(outs)
+        assert_close(bf16_to_f32(to_np(got, np.uint16)), bf16_to_f32(to_np(ref, np.uint16)), RTOL_BF16,
+                     f"EP peer exchange G={world} step {step}")
+    eng.close()
