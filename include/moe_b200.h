@@ -375,6 +375,10 @@ int moe_ep_combine(moe_ep_comm* comm, const float* part, int T_local, int d, flo
  *                       each owner's receive slot `rank`, release flag
  *   moe_ep_reduce       out = bf16(x + sum over src in order) once all arrived */
 size_t moe_ep_peer_bytes(int G, int T_local, int d);
+/* A zeroed exchange buffer of its own cudaMalloc allocation (an IPC handle
+ * maps whole allocations, so the buffer must start one). */
+int moe_ep_peer_alloc(size_t bytes, void** base);
+int moe_ep_peer_free(void* base);
 void* moe_ep_peer_rows(void* base);
 int moe_ep_peer_ipc_handle(const void* base, char handle[64]);
 int moe_ep_peer_ipc_open(const char handle[64], void** peer_base);

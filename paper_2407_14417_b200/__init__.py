@@ -122,6 +122,8 @@ def lib() -> C.CDLL:
         "moe_ep_combine": (I, [VP, VP, I, I, VP, VP]),
         "moe_ep_peer_bytes": (C.c_size_t, [I, I, I]),
         "moe_ep_peer_rows": (VP, [VP]),
+        "moe_ep_peer_alloc": (I, [C.c_size_t, P(VP)]),
+        "moe_ep_peer_free": (I, [VP]),
         "moe_ep_peer_ipc_handle": (I, [VP, C.c_char_p]),
         "moe_ep_peer_ipc_open": (I, [C.c_char_p, P(VP)]),
         "moe_ep_peer_ipc_close": (I, [VP]),
@@ -519,6 +521,16 @@ class EpComm:
 
 def ep_peer_bytes(G: int, T_local: int, d: int) -> int:
     return lib().moe_ep_peer_bytes(G, T_local, d)
+
+
+def ep_peer_alloc(nbytes: int) -> int:
+    p = C.c_void_p()
+    _check(lib().moe_ep_peer_alloc(nbytes, C.byref(p)))
+    return p.value
+
+
+def ep_peer_free(base_ptr: int):
+    _check(lib().moe_ep_peer_free(base_ptr))
 
 
 def ep_peer_ipc_handle(base_ptr: int) -> bytes:

@@ -858,6 +858,19 @@ size_t moe_ep_peer_bytes(int G, int T_local, int d) { return moek_ep_peer_bytes(
 
 void* moe_ep_peer_rows(void* base) { return base; }  // the gather rows lead the buffer
 
+int moe_ep_peer_alloc(size_t bytes, void** base) {
+    return guarded([&] {
+        usage_if(base == nullptr || bytes == 0, "bad argument");
+        need_device();
+        cuda_ok(cudaMalloc(base, bytes), "cudaMalloc(exchange buffer)");
+        cuda_ok(cudaMemset(*base, 0, bytes), "cudaMemset");
+    });
+}
+
+int moe_ep_peer_free(void* base) {
+    return guarded([&] { cuda_ok(cudaFree(base), "cudaFree"); });
+}
+
 int moe_ep_peer_ipc_handle(const void* base, char handle[64]) {
     return guarded([&] {
         usage_if(base == nullptr || handle == nullptr, "null argument");

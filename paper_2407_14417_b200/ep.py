@@ -122,17 +122,20 @@ class PeerExchange:
                  own=None):
         self.moe, self.torch, self.rank, self.world, self.T_local, self.d = moe, torch, rank, world, T_local, d
         self.nbytes = moe.ep_peer_bytes(world, T_local, d)
-        self.own = own if own is not None else torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
-        if bases is None:  # one process per GPU: exchange IPC handles
-            h = moe.ep_peer_ipc_handle(self.own.data_ptr())
+        self._alloc = None
+        if bases is None:  # one process per GPU: own cudaMalloc allocation, IPC handles
+            self._alloc = moe.ep_peer_alloc(self.nbytes)
+            self.own_ptr = self._alloc
+            h = moe.ep_peer_ipc_handle(self.own_ptr)
             handles = [None] * world
             dist.all_gather_object(handles, h)
-            ptrs = [self.own.data_ptr() if r == rank else moe.ep_peer_ipc_open(handles[r]) for r in range(world)]
-        else:
+            ptrs = [self.own_ptr if r == rank else moe.ep_peer_ipc_open(handles[r]) for r in range(world)]
+        else:  # virtual ranks in one process: caller-owned zeroed buffers
+            self.own_ptr = own.data_ptr()
             ptrs = bases
         self.bases = moe.PeerBases(ptrs)
         rows = T_local * world * d
-        self.xg = torch.as_tensor(_DevView(self.own.data_ptr(), rows), device=device)
+        self.xg = torch.as_tensor(_DevView(self.own_ptr, rows), device=device)
         self.epoch = 0
 
     def push_rows(self, x_local, stream):
@@ -140,7 +143,7 @@ class PeerExchange:
         self.moe.ep_push_rows(x_local, self.T_local, self.d, self.rank, self.bases, self.epoch, stream)
 
     def wait_rows(self, stream):
-        self.moe.ep_wait_rows(self.own.data_ptr(), self.world, self.T_local, self.d, self.epoch, stream)
+        self.moe.ep_wait_rows(self.own_ptr, self.world, self.T_local, self.d, self.epoch, stream)
 
     def push_shares(self, ops, y, mask, stream):
         self.moe.ep_push_shares(y, ops.inv, ops.w, ops.idx, mask, self.T_local, self.d, ops.k, self.rank, self.bases,

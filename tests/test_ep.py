@@ -267,3 +267,17 @@ def test_ep_peer_exchange_virtual_ranks_gpu(moe, cuda, world, T_local):
         assert_close(bf16_to_f32(to_np(got, np.uint16)), bf16_to_f32(to_np(ref, np.uint16)), RTOL_BF16,
                      f"EP peer exchange G={world} step {step}")
     eng.close()
+
+
+@pytest.mark.gpu
+def test_ep_peer_exchange_two_processes_ipc_gpu(cuda):
+    """Two processes on one GPU share exchange buffers by CUDA IPC handles and
+    run the fused path, phased and flags-only (tools/ep_ipc_check.py): each
+    rank's rows equal the single-device layer."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", "2",
+                        os.path.join(root, "tools", "ep_ipc_check.py")], capture_output=True, text=True, timeout=240)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("rank") and "err" in l]
+    assert r.returncode == 0 and len(lines) == 4, r.stdout[-2000:] + r.stderr[-2000:]
