@@ -190,28 +190,29 @@ MOE_DEVI unsigned long long gtimer() {
 
 MOE_DEVI uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
-// fp16 magic-number decode of one packed word (4 LOP3 + 1 SHF): fp16 0x6400
-// is 1024 with ulp 1, so a nibble in mantissa bits 0-3 reads 1024+u and one
-// in bits 4-7 reads 1024+16u -- both exact, no per-nibble shift.
-//   lo0: nibbles (0,16) -> 1024+u      hi0: nibbles (4,20) -> 1024+16u
-//   lo1: nibbles (8,24)                hi1: nibbles (12,28)
-MOE_DEVI void decode_h(uint32_t w, uint32_t& lo0, uint32_t& hi0, uint32_t& lo1, uint32_t& hi1) {
-    lo0 = and_or(w, 0x000F000Fu, 0x64006400u);
-    hi0 = and_or(w, 0x00F000F0u, 0x64006400u);
-    const uint32_t w8 = w >> 8;
-    lo1 = and_or(w8, 0x000F000Fu, 0x64006400u);
-    hi1 = and_or(w8, 0x00F000F0u, 0x64006400u);
-}
-
 // One int4 group (16 rows x 128 K, 1024 B at gp + 32 B scales at sc); bp:
 // this lane's activation chunks of the group (4 x 16 B at stride 64).
-// Nibbles (0,16)/(8,24) of a word hold the K positions with k%16 < 8 ("lo",
-// value q+1032), nibbles (4,20)/(12,28) those with k%16 >= 8 ("hi", value
-// 16q+1152); two MMA chains accumulate them, and per group
-//   sum(q x) = c_lo + c_hi/16 - (1032 S_lo + 72 S_hi)
+// Nibbles (0,16)/(8,24) of a word hold the K positions with k%16 < 8 ("lo"),
+// nibbles (4,20)/(12,28) those with k%16 >= 8 ("hi").  The fp16 magic
+// numbers read them as exact values of the same unit: 0x6400 | nibble =
+// 1024 + u (lo) and 0x5400 | nibble<<4 = 64 + u (hi, ulp 1/16), u = q + 8,
+// so one MMA chain accumulates both and per group
+//   sum(q x) = c - (1032 S_lo + 72 S_hi)
 // with the bias term precomputed per activation group (B0: column 2t, B1:
-// 2t+1).  Then y += s * sum(q x): the exact dequant values q*s.  Chunk q of
-// the fp16 activation copy holds the K positions of (lo0, lo1, hi0, hi1).
+// 2t+1) and loaded as the chain's start value.  Then y += s * sum(q x): the
+// exact dequant values q*s.  Chunk q of the fp16 activation copy holds the
+// K positions of (lo0, lo1, hi0, hi1).
+// fp16 magic-number decode of one packed word (4 LOP3 + 1 SHF):
+//   lo0: nibbles (0,16) -> 1024+u      hi0: nibbles (4,20) -> 64+u
+//   lo1: nibbles (8,24)                hi1: nibbles (12,28)
+MOE_DEVI void decode_lohi(uint32_t w, uint32_t& lo0, uint32_t& hi0, uint32_t& lo1, uint32_t& hi1) {
+    lo0 = and_or(w, 0x000F000Fu, 0x64006400u);
+    hi0 = and_or(w, 0x00F000F0u, 0x54005400u);
+    const uint32_t w8 = w >> 8;
+    lo1 = and_or(w8, 0x000F000Fu, 0x64006400u);
+    hi1 = and_or(w8, 0x00F000F0u, 0x54005400u);
+}
+
 MOE_DEVI void group_int4(const uint8_t* gp, const uint8_t* sc, const uint8_t* bp, float B0, float B1, int lane,
                          float (&acc)[4]) {
     const uint32_t s2 = *reinterpret_cast<const uint32_t*>(sc + (lane >> 2) * 4);
@@ -219,21 +220,21 @@ MOE_DEVI void group_int4(const uint8_t* gp, const uint8_t* sc, const uint8_t* bp
     const uint4 wh = lds128(gp + 512 + lane * 16);
     const uint32_t lo[4] = {wl.x, wl.y, wl.z, wl.w};
     const uint32_t hi[4] = {wh.x, wh.y, wh.z, wh.w};
-    float cl[4] = {0.f, 0.f, 0.f, 0.f}, ch[4] = {0.f, 0.f, 0.f, 0.f};
+    float c[4] = {-B0, -B1, -B0, -B1};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint4 b = lds128(bp + q * 64);
         uint32_t a_l0, a_h0, a_l1, a_h1, c_l0, c_h0, c_l1, c_h1;
-        decode_h(lo[q], a_l0, a_h0, a_l1, a_h1);  // row gr
-        decode_h(hi[q], c_l0, c_h0, c_l1, c_h1);  // row gr+8
-        mma_f16(cl, a_l0, c_l0, a_l1, c_l1, b.x, b.y);
-        mma_f16(ch, a_h0, c_h0, a_h1, c_h1, b.z, b.w);
+        decode_lohi(lo[q], a_l0, a_h0, a_l1, a_h1);  // row gr
+        decode_lohi(hi[q], c_l0, c_h0, c_l1, c_h1);  // row gr+8
+        mma_f16(c, a_l0, c_l0, a_l1, c_l1, b.x, b.y);
+        mma_f16(c, a_h0, c_h0, a_h1, c_h1, b.z, b.w);
     }
     const float s_lo = bf16_lo(s2), s_hi = bf16_hi(s2);
-    acc[0] = __fmaf_rn(s_lo, __fmaf_rn(ch[0], 0.0625f, cl[0]) - B0, acc[0]);
-    acc[1] = __fmaf_rn(s_lo, __fmaf_rn(ch[1], 0.0625f, cl[1]) - B1, acc[1]);
-    acc[2] = __fmaf_rn(s_hi, __fmaf_rn(ch[2], 0.0625f, cl[2]) - B0, acc[2]);
-    acc[3] = __fmaf_rn(s_hi, __fmaf_rn(ch[3], 0.0625f, cl[3]) - B1, acc[3]);
+    acc[0] = __fmaf_rn(s_lo, c[0], acc[0]);
+    acc[1] = __fmaf_rn(s_lo, c[1], acc[1]);
+    acc[2] = __fmaf_rn(s_hi, c[2], acc[2]);
+    acc[3] = __fmaf_rn(s_hi, c[3], acc[3]);
 }
 
 // One bf16 group (16 rows x 128 K, 4096 B): part kk (512 B) holds every
