@@ -371,3 +371,37 @@ def test_reconfigure_needs_masters(moe, cuda):
     with pytest.raises(moe.UsageError):
         eng.reconfigure(plan, 50e9)
     eng.close()
+
+
+def test_reconfigure_with_lru_cache(moe, torch_mod, cuda):
+    """f1 x f2: an LRU engine reconfigured to a plan with a different host set
+    starts from an empty cache; its counters equal simulate(Lru) on the new
+    plan and its outputs equal a fresh all-resident engine."""
+    torch = torch_mod
+    prof = moe.profile_for_shape(512, 1792, 2)
+    s16 = moe.expert_size(prof, 1)
+    full = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 1), moe.HardwareProfile(10**15), prof)
+    a = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 1), moe.HardwareProfile(6 * s16), prof)
+    b = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 1), moe.HardwareProfile(4 * s16), prof)
+    assert a.location != b.location and b.n_gpu < 16
+    eng = moe.MoeEngine(2, 8, 2, 512, 1792, a, max_tokens=1, seed=11, lru_capacity=3, keep_masters=True)
+    base = make_engine(moe, TINY, full, 11, 1)
+    for step in range(4):
+        eng.synth_input(step, 1)
+        eng.decode(1)
+    eng.sync()
+    eng.reconfigure(b, 50e9)
+    eng.reset_counters()
+    trace = []
+    for step in range(10):
+        for e in (eng, base):
+            e.synth_input(step, 1)
+            e.decode(1)
+            e.sync()
+        assert np.array_equal(read_device(torch, eng.output_ptr, 1024), read_device(torch, base.output_ptr, 1024))
+        trace.extend(eng.last_routing(1))
+    c = eng.counters()
+    sim = moe.simulate(b, trace, 10, prof, moe.HardwareProfile(1), lru_capacity=3)
+    assert (c.activations, c.hits, c.bytes_transferred) == (sim.activations, sim.hits, sim.bytes_transferred)
+    eng.close()
+    base.close()
