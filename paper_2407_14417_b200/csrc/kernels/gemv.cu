@@ -695,7 +695,7 @@ MOE_DEVI float4 sum_kparts(const float* p, size_t kstride, int KP, int kg) {
 // bf16 and stored as bf16 (perm_k) and its exact fp16 copy (perm_k16), plus
 // the group's int4 bias term 1032*S_lo + 72*S_hi.
 constexpr int kFinHThreads = 64 * kKG;
-constexpr int kFinOQuads = 32;
+constexpr int kFinOQuads = 8;   // 32 outputs per block: T=1 spreads d=4096 over 128 blocks
 constexpr int kFinOThreads = kFinOQuads * kKG;
 __global__ void __launch_bounds__(kFinHThreads) finalize_h_kernel(
     const float* __restrict__ part, const int* __restrict__ kpslot, int nslots, int f, uint16_t* __restrict__ hperm,
