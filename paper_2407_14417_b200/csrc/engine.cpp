@@ -640,7 +640,7 @@ struct MoeEngine::Impl {
         }
         for (auto& e : ev) cudaEventDestroy(e);
         // GEMV: route(+x permute), gate/up stream, SwiGLU finalize, down stream, combine finalize
-        // tcgen05: route, x->fp16, gate/up GEMM (+SwiGLU), down GEMM, combine
+        // tcgen05: route, row gather, gate/up GEMM (+SwiGLU), down GEMM, combine
         if (kernels_per_step) *kernels_per_step = 5 * L;
     }
 
