@@ -239,3 +239,28 @@ def test_no_fallback_errors_are_loud(moe, torch_mod, cuda):
         moe.gate_topk(None, None, 1, 100, 8, 2, None, None)  # d % 8 != 0
     with pytest.raises(moe.UsageError):
         moe.ffn(None, None, None, 1, 2, [], 512, 1792, None, 0, None)  # E = 0
+
+
+def test_zero_tokens_are_noops(moe, orc, torch_mod, cuda):
+    """T = 0 (an empty batch, or a rank whose shard got no slots) is valid
+    input for every stateless entry point: nothing launches, nothing is
+    written, and the call succeeds."""
+    torch = torch_mod
+    d, f, E, k = 512, 1792, 8, 2
+    x = torch.zeros(d, dtype=torch.int16, device=cuda)
+    wg = torch.zeros(E * d, dtype=torch.int16, device=cuda)
+    idx = torch.full((k,), -7, dtype=torch.int32, device=cuda)
+    w = torch.full((k,), -7.0, dtype=torch.float32, device=cuda)
+    moe.gate_topk(x, wg, 0, d, E, k, idx, w)
+    moe.route(x, wg, 0, d, E, k, 1e-5, idx, w)
+    y = torch.full((k * d,), -7.0, dtype=torch.float32, device=cuda)
+    m = orc.model(1, E, k, d, f, 5)
+    dev, _ = _expert_tensors(orc, torch, cuda, m, 0, 1)
+    experts = [moe.expert_weights(moe.MOE_P16, dev[0], dev[1])] * E
+    offs = torch.zeros(E + 1, dtype=torch.int32, device=cuda)
+    moe.ffn(x, idx, offs, 0, k, experts, d, f, None, 0, y)
+    moe.ffn_tc(x, idx, offs, 0, k, experts, d, f, None, 0, y)
+    out = torch.full((d,), -7, dtype=torch.int16, device=cuda)
+    moe.combine(y, idx, w, None, 0, d, k, out)
+    torch.cuda.synchronize()
+    assert (idx == -7).all() and (w == -7.0).all() and (y == -7.0).all() and (out == -7).all()
