@@ -17,12 +17,15 @@ layers (route -> gate/up GEMV -> down GEMV -> combine, one CUDA graph).
             CUDA events per layer on its launch stream; algorithmic bytes =
             distinct selected experts' weights+scales + activations
   cpu_baseline  the CPU port (oracle/, OpenMP over all host threads) on a
-            bounded sample: one layer's experts prepared, T-token layer
-            forwards timed, extrapolated x32 layers
+            bounded sample: one token input through the full 32-layer stack
+            (its selected experts materialised, untimed), repeated
 
 No L2 flush is needed: one step streams 64 distinct experts (5.8-22.5 GB)
-through a 126 MB L2.  `--impl reference` times the CPU port alone (the
-reference, /root/reference, has no tensor math: SPEC.md:13).
+through a 126 MB L2.  `--impl reference` times the reference path on the
+host: the reference (/root/reference) has no tensor math, so
+its arm is the CPU port of this path (oracle/, OpenMP over every host
+thread) driven by the reference's own planner (oracle/_ref make_plan) --
+the whole 32-layer stack per step, never the product library.
 """
 from __future__ import annotations
 
@@ -46,12 +49,28 @@ NORM_EPS = 1e-5
 METRIC = "decode tokens/s vs #4-bit experts (Mixtral-8x7B shape); expert-FFN HBM GB/s"
 
 
-def _traffic():
+TRAFFIC_INPUT = 7  # the token input profile_step runs for the roofline (and tools/traffic.py under ncu)
+
+
+def _traffic(n4, T, alg_bytes_per_layer):
+    """ncu dram read+write per layer of the expert FFN launches, captured by
+    tools/traffic.py for this configuration and input (profiles/r02_traffic.json),
+    next to the algorithmic bytes of the same step; null when absent or when
+    the recorded algorithmic bytes disagree (another kernel or routing)."""
+    path = os.path.join(ROOT, "profiles", "r02_traffic.json")
     try:
-        with open(os.path.join(ROOT, "profiles", "r01b_traffic.json")) as fh:
-            return int(json.load(fh)["stream_pair_dram_bytes"])
+        with open(path) as fh:
+            t = json.load(fh)
     except Exception:
-        return None
+        return None, "no ncu traffic capture for this configuration"
+    if (t.get("n4"), t.get("tokens"), t.get("input")) != (n4, T, TRAFFIC_INPUT) or \
+            int(t["algorithmic_bytes_per_layer"]) != int(alg_bytes_per_layer):
+        return None, "profiles/r02_traffic.json was captured for another configuration"
+    return int(t["dram_bytes_per_layer"]), ("ncu dram__bytes_read+write per layer of the expert-FFN launches "
+                                             "(stream_kernel x2 + finalize_h + finalize_out) of one step on input %d, "
+                                             "averaged over the %d layers (profiles/r02_traffic.json, %s); "
+                                             "algorithmic %d B per layer" % (TRAFFIC_INPUT, LAYERS, t.get("commit", "?"),
+                                                                            int(t["algorithmic_bytes_per_layer"])))
 
 
 def _peak_tflops():
@@ -73,119 +92,212 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled every 10 ms through NVML on a
+    background thread during the timed region (nvidia-smi's 100 ms floor
+    missed short regions); one sample is always taken at exit."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    PERIOD_S = 0.010
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device_index: int):
         self.dev = device_index
-        self.proc = None
-        self.path = None
+        self.rows = []
+        self.err = None
+        self._stop = None
+        self._thr = None
+
+    def _sample(self, nv, h):
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.rows.append((sm, mx, r))
 
     def __enter__(self):
+        import threading
         try:
-            fd, self.path = tempfile.mkstemp(suffix=".csv")
-            os.close(fd)
-            self.out = open(self.path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=self.out, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.dev]) if vis and vis.split(",")[self.dev].isdigit() else self.dev
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
+        except Exception as exc:  # no NVML: report it, never fake a clock
+            self.err = f"nvml unavailable: {exc}"
+            return self
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self._sample(nv, h)
+                except Exception as exc:
+                    self.err = str(exc)
+                    return
+                self._stop.wait(self.PERIOD_S)
+            self._sample(nv, h)
+
+        self._thr = threading.Thread(target=run, daemon=True)
+        self._thr.start()
         return self
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-            self.out.close()
+        if self._thr is not None:
+            self._stop.set()
+            self._thr.join(timeout=5)
 
     def summary(self):
-        if self.proc is None or not self.path:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        rows = []
-        with open(self.path) as fh:
-            for line in fh:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 9:
-                    rows.append(parts)
-        os.unlink(self.path)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
-
-
-def cpu_port_tokens_per_s(n4_layer_prec, T, seconds=12.0, layer=0, seed=0):
-    """The CPU port (oracle) on one layer with prepared weights; returns
-    (tok/s extrapolated to 32 layers, threads, sample description)."""
-    from oracle.oracle import OracleLib
-    orc = OracleLib()
-    m = orc.model(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, seed, NORM_EPS)
-    prep = orc.prepare_layer(m, layer, n4_layer_prec)
-    x = orc.step_input(m, 0, T)
-    orc.moe_layer_w(m, prep, x, T)  # warm
-    reps, t0 = 0, time.perf_counter()
-    while True:
-        x_in = orc.step_input(m, reps + 1, T)
-        orc.moe_layer_w(m, prep, x_in, T)
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= seconds or reps >= 400:
-            break
-    per_layer = el / reps
-    tps = T / (per_layer * LAYERS)
-    n4l = sum(1 for p in n4_layer_prec if p == 0)
-    sample = (f"layer {layer} of {LAYERS} ({n4l}/8 experts int4 per the plan), {reps} x {T}-token layer forwards "
-              f"in {el:.1f} s, extrapolated x{LAYERS} layers")
-    return tps, orc.num_threads(), sample
-
-
-def run_reference(args, rank, world):
-    if rank != 0:
-        return
-    import paper_2407_14417_b200 as moe
-    prof = moe.profile_for_shape(D_MODEL, D_FFN, LAYERS, EXPERTS, TOPK)
-    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, args.n4, 0), moe.HardwareProfile(10**15), prof)
-    prec = plan.precision[:EXPERTS]
-    from oracle.oracle import OracleLib
-    orc = OracleLib()
-    m = orc.model(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, 0, NORM_EPS)
-    prep = orc.prepare_layer(m, 0, prec)
-    T = args.tokens
-    for w in range(args.warmup):
-        orc.moe_layer_w(m, prep, orc.step_input(m, w, T), T)
-    t0 = time.perf_counter()
-    for s in range(args.steps):
-        orc.moe_layer_w(m, prep, orc.step_input(m, 1000 + s, T), T)
-    el = time.perf_counter() - t0
-    per_layer = el / args.steps
-    tps = T / (per_layer * LAYERS)
-    sample = (f"layer 0 of {LAYERS} ({sum(1 for p in prec if p == 0)}/8 int4), {args.steps} x {T}-token layer "
-              f"forwards, extrapolated x{LAYERS} layers")
-    line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_layer * LAYERS * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16/int4-g128 (fp32 acc)",
-            "data": "synthetic (seeded generator)",
-            "config": {"workload": "mixtral8x7b-shape 32-layer MoE stack decode", "n4": args.n4, "batch": T,
-                       "d_model": D_MODEL, "d_ffn": D_FFN, "layers": LAYERS, "experts": EXPERTS, "top_k": TOPK},
-            "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": orc.num_threads(), "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "note": "reference repo has no tensor math (SPEC.md:13); CPU port of its path = oracle/ (OpenMP)"}
-    print(json.dumps(line), flush=True)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no samples"], "samples": 0}
+        reasons = sorted({n for _, _, r in self.rows for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "period_ms": self.PERIOD_S * 1e3,
+                "source": "NVML (nvmlDeviceGetClockInfo / CurrentClocksEventReasons)"}
 
 
 N_INPUTS = 8  # distinct token inputs per timing: the routing (and so the bytes) varies per input
+
+
+def bench_config(args, T, world, parallelism=None):
+    """The workload description both arms print (identical keys and values)."""
+    return {"workload": "mixtral8x7b-shape 32-layer MoE stack, batch-%d decode" % T, "n4": args.n4,
+            "layer": "x + MoE(RMSNorm(x)) (decoder-layer norm eps 1e-5, unit weight; no attention)",
+            "of": LAYERS * EXPERTS, "plan": "plan_quality seed 0, all device-resident",
+            "d_model": D_MODEL, "d_ffn": D_FFN, "layers": LAYERS, "experts": EXPERTS, "top_k": TOPK,
+            "batch": T, "parallelism": parallelism or ("single" if world == 1 else "replicas"),
+            "inputs": "%d distinct synthetic token inputs (1000..%d), steps split evenly over them (the routing, "
+                      "hence the expert bytes per step, varies with the input)" % (N_INPUTS, 1000 + N_INPUTS - 1),
+            "l2": "no flush: each step streams 5.8-22.5 GB of distinct expert weights >> 126 MB L2"}
+
+
+def reference_plan_precision(n4):
+    """plan_quality(n4, seed 0) precisions from the reference's own planner
+    (oracle/_ref: /root/reference/proj/src/planner.cpp make_plan), falling
+    back to the frozen reference output in tests/golden/mixtral_plans.json."""
+    try:
+        from oracle.oracle import RefLib, RefProfile
+        ref = RefLib()
+        prof = RefProfile(LAYERS, EXPERTS, TOPK, 0, 1, 6 * D_MODEL * D_FFN, 128.0 / 33.0, 1e-3, 1.0, 0.0)
+        st, prec, loc, _ = ref.make_plan(prof, 10**15, 12.285e9, 1, n4, 0)  # 1 = Quality
+        if st != 0:
+            raise RuntimeError(ref.err())
+        return [int(v) for v in prec], "oracle/_ref make_plan (the reference's planner)"
+    except (FileNotFoundError, OSError):
+        with open(os.path.join(ROOT, "tests", "golden", "mixtral_plans.json")) as fh:
+            return json.load(fh)["plans"][str(n4)], "tests/golden/mixtral_plans.json (reference make_plan output)"
+
+
+class CpuStack:
+    """The 32-layer stack on the CPU port (oracle/, OpenMP): layer = x +
+    MoE(RMSNorm(x)); experts are materialised on first use (untimed when
+    `prepare` runs them first) and kept."""
+
+    def __init__(self, precision, seed=0):
+        from oracle.oracle import OracleLib, OrcExpert, _np_ptr
+        self.orc = OracleLib()
+        self.m = self.orc.model(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, seed, NORM_EPS)
+        self.prec = precision
+        self.wg = [self.orc.router_weights(self.m, l) for l in range(LAYERS)]
+        self.arr = [(OrcExpert * EXPERTS)() for _ in range(LAYERS)]
+        for l in range(LAYERS):
+            for s_ in range(EXPERTS):
+                self.arr[l][s_].precision = precision[l * EXPERTS + s_]
+        self.keep = {}
+        self._ptr = _np_ptr
+        self.built = 0
+
+    def _ensure(self, l, slots):
+        for s_ in slots:
+            e = l * EXPERTS + int(s_)
+            if e in self.keep:
+                continue
+            a = self.arr[l][int(s_)]
+            if self.prec[e] == 1:
+                gu, dn = self.orc.expert_bf16(self.m, e)
+                self.keep[e] = (gu, dn)
+                a.w_gate_up, a.w_down = self._ptr(gu), self._ptr(dn)
+            else:
+                qgu, sgu, qd, sd = self.orc.expert_int4(self.m, e)
+                self.keep[e] = (qgu, sgu, qd, sd)
+                a.w_gate_up, a.s_gate_up, a.w_down, a.s_down = (self._ptr(v) for v in (qgu, sgu, qd, sd))
+            self.built += 1
+
+    def step(self, x, T, prepare=False):
+        for l in range(LAYERS):
+            if prepare:  # routing first, then the selected experts (untimed pass)
+                xn = self.orc.rmsnorm(x, T, D_MODEL, NORM_EPS)
+                idx, _, _ = self.orc.gate_topk(xn, self.wg[l], T, D_MODEL, EXPERTS, TOPK)
+                self._ensure(l, set(idx.reshape(-1).tolist()))
+            x, _ = self.orc.moe_layer_w(self.m, (self.wg[l], self.arr[l], None), x, T)
+        return x
+
+    def threads(self):
+        return self.orc.num_threads()
+
+
+def cpu_port_tokens_per_s(precision, T, seconds=12.0):
+    """cpu_baseline: one token input (1000) through the full 32-layer stack on
+    the CPU port; its selected experts materialised first (untimed), then
+    repeated for ~`seconds`.  Returns (tok/s, threads, sample)."""
+    stack = CpuStack(precision)
+    x0 = stack.orc.step_input(stack.m, 1000, T)
+    stack.step(x0, T, prepare=True)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        stack.step(x0, T)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or reps >= 200:
+            break
+    tps = T * reps / el
+    sample = (f"token input 1000 (batch {T}) through the full {LAYERS}-layer stack ({stack.built} selected experts "
+              f"materialised untimed), {reps} repeats in {el:.1f} s")
+    return tps, stack.threads(), sample
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference path on the host's cores.  Rank 0 only
+    (torchrun N > 1: the other ranks exit without work).  Never loads the
+    product library."""
+    if rank != 0:
+        return
+    T = args.tokens
+    prec, plan_src = reference_plan_precision(args.n4)
+    stack = CpuStack(prec)
+    inputs = [stack.orc.step_input(stack.m, 1000 + i, T) for i in range(N_INPUTS)]
+    t_prep = time.perf_counter()
+    for x in inputs:  # materialise every expert the inputs route to (untimed)
+        stack.step(x, T, prepare=True)
+    t_prep = time.perf_counter() - t_prep
+    for w in range(args.warmup):
+        stack.step(inputs[w % N_INPUTS], T)
+    per = [args.steps // N_INPUTS + (1 if i < args.steps % N_INPUTS else 0) for i in range(N_INPUTS)]
+    t0 = time.perf_counter()
+    for i in range(N_INPUTS):
+        for _ in range(per[i]):
+            stack.step(inputs[i], T)
+    el = time.perf_counter() - t0
+    ms = el / args.steps * 1e3
+    tps = T * args.steps / el
+    sample = (f"{args.steps} steps x batch {T} through the full {LAYERS}-layer stack, inputs 1000..{999 + N_INPUTS} "
+              f"rotated as in the GPU arm ({stack.built} experts materialised untimed in {t_prep:.0f} s)")
+    line = {"impl": "reference", "metric": METRIC, "value": round(tps, 4), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16 / int4-g128 weights, bf16 activations, fp32 accumulate",
+            "data": "synthetic (seeded counter-based generator, int4 = RTN-g128 of the bf16 masters)",
+            "config": bench_config(args, T, 1),
+            "cpu_baseline": {"value": round(tps, 4), "unit": "tokens/s", "cores": stack.threads(), "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(tps, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "plan_source": plan_src,
+            "note": "the reference has no tensor math (SPEC.md:13): its arm is the CPU port of this path "
+                    "(oracle/, OpenMP over all host threads), driven by the reference's planner"}
+    print(json.dumps(line), flush=True)
+
+
 
 
 def time_engine(moe, torch, eng, T, steps, warmup, inputs=N_INPUTS):
@@ -251,10 +363,11 @@ def run_ours(args, rank, world, device):
     # ---- roofline: per-layer expert FFN (gate/up + down), CUDA events -----
     ffn_ms, ffn_bytes = [], []
     for _ in range(3):
-        eng.synth_input(7, T)
+        eng.synth_input(TRAFFIC_INPUT, T)
         m_, b_, kps = eng.profile_step(T)
         ffn_ms += m_
         ffn_bytes += b_
+    traffic, traffic_note = _traffic(args.n4, T, round(sum(ffn_bytes[:LAYERS]) / LAYERS))
     avg_ms = sum(ffn_ms) / len(ffn_ms)
     avg_bytes = sum(ffn_bytes) / len(ffn_bytes)
     achieved = avg_bytes / (avg_ms * 1e-3) / 1e9
@@ -356,7 +469,7 @@ def run_ours(args, rank, world, device):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        tps, cores, sample = cpu_port_tokens_per_s(plan.precision[:EXPERTS], T, seconds=args.cpu_seconds)
+        tps, cores, sample = cpu_port_tokens_per_s(plan.precision, T, seconds=args.cpu_seconds)
         cpu = {"value": round(tps, 4), "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample}
 
     if rank == 0:
@@ -365,22 +478,12 @@ def run_ours(args, rank, world, device):
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16 / int4-g128 weights, bf16 activations, fp32 accumulate",
             "data": "synthetic (seeded counter-based generator, int4 = RTN-g128 of the bf16 masters)",
-            "config": {"workload": "mixtral8x7b-shape 32-layer MoE stack, batch-%d decode" % T, "n4": args.n4,
-                       "layer": "x + MoE(RMSNorm(x)) (decoder-layer norm eps 1e-5, unit weight; no attention)",
-                       "of": LAYERS * EXPERTS, "plan": "plan_quality seed 0, all device-resident",
-                       "d_model": D_MODEL, "d_ffn": D_FFN, "layers": LAYERS, "experts": EXPERTS, "top_k": TOPK,
-                       "batch": T, "parallelism": "replicas" if world > 1 else "single",
-                       "inputs": "%d distinct synthetic token inputs, steps split evenly over them (the routing, "
-                                 "hence the expert bytes per step, varies with the input)" % N_INPUTS,
-                       "l2": "no flush: each step streams %.1f GB of distinct expert weights >> 126 MB L2"
-                             % (step_bytes / 1e9)},
+            "config": bench_config(args, T, world),
             "e2e": {"value": round(e2e, 3), "unit": "tokens/s", "h2d_bytes_per_step": T * D_MODEL * 2,
                     "d2h_bytes_per_step": T * D_MODEL * 2},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(achieved / hbm_peak, 4), "traffic": _traffic(), "peak_kind": peak_kind,
-                         "traffic_note": "ncu dram read+write of the stream_kernel pair of one int4/int4 "
-                                         "token-layer (profiles/r01b_traffic.json) vs its 181,665,792 "
-                                         "algorithmic weight bytes",
+                         "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                         "traffic_note": traffic_note,
                          "kernel": "expert FFN per layer: stream_kernel (gate/up) + finalize_h + "
                                    "stream_kernel (down) + finalize_out, CUDA events on the engine stream",
                          "bytes_per_launch": round(avg_bytes), "ms_per_launch": round(avg_ms, 5),
@@ -401,6 +504,11 @@ def run_ours(args, rank, world, device):
             "bytes_per_expert": {"bf16": s16, "int4_g128": s4},
         }
         print(json.dumps(line), flush=True)
+        bad = [(r["resident_frac"], pol) for r in (host_split or {}).get("points", [])
+               for pol in ("static", "lru") if pol in r and not r[pol]["counters_equal_simulate"]]
+        if bad:  # the engine's counters must equal the reference cost model's on the exported routing
+            print(f"counters_equal_simulate is false at {bad}", file=sys.stderr, flush=True)
+            sys.exit(3)
 
 
 def h2d_gbs(torch, device, nbytes=1 << 30):
@@ -431,6 +539,21 @@ def host_split_sweep(moe, torch, prof, args, device):
     n4 = args.host_split_n4
     s16, s4 = moe.expert_size(prof, 1), moe.expert_size(prof, 0)
     full = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 0), moe.HardwareProfile(10**15), prof)
+    # model calibration: price the reference cost
+    # model at the measured B200 costs -- per-activation compute from the
+    # all-resident decode of this plan (CUDA events, graph replay), transfers
+    # at the measured pinned H2D bandwidth, compute_penalty4 = 1
+    eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, full, max_tokens=1, seed=args.seed, device=device,
+                        norm_eps=NORM_EPS)
+    eng.synth_input(0, 1)
+    eng.decode(1)
+    eng.sync()
+    ms_res = time_engine(moe, torch, eng, 1, 40, 3)
+    eng.close()
+    del eng
+    act_s = ms_res * 1e-3 / (LAYERS * TOPK)
+    calib = moe.ModelProfile(**{**prof.__dict__, "compute_latency16_s": act_s, "compute_penalty4": 1.0,
+                                "nonexpert_latency_s": 0.0})
     experts_bytes = sum(s4 if p == 0 else s16 for p in full.precision)
     floor = prof.size_nonexpert_bytes + max(s4 if n4 == LAYERS * EXPERTS else s16, s4)
     rows = []
@@ -442,7 +565,7 @@ def host_split_sweep(moe, torch, prof, args, device):
         except moe.MoeError as exc:
             rows.append({"resident_frac": frac, "infeasible": str(exc)})
             continue
-        model_tps = moe.expected_throughput(plan, moe.ModelProfile(**{**prof.__dict__, "compute_penalty4": 1.0}), hw)
+        model_tps = moe.expected_throughput(plan, calib, hw)
         row = {"resident_frac": frac, "gpu_budget_gb": round(budget / 1e9, 2), "experts_on_gpu": plan.n_gpu,
                "model_tps_expected_throughput": round(model_tps, 3)}
         # Static (the paper's scheme) and LRU (its Mixtral-Offloading baseline)
@@ -474,6 +597,11 @@ def host_split_sweep(moe, torch, prof, args, device):
             del eng
         rows.append(row)
     return {"n4": n4, "h2d_gbs_measured": round(bw, 1),
+            "model_calibration": {"resident_ms_per_step": round(ms_res, 4), "compute_latency16_s": act_s,
+                                  "compute_penalty4": 1.0, "nonexpert_latency_s": 0.0,
+                                  "transfer_bw_bytes_per_s": bw * 1e9,
+                                  "how": "all-resident decode of this plan (measured) / (layers x top_k); "
+                                         "transfers at the measured pinned H2D bandwidth"},
             "policies": "static = single swap slot re-streamed per activation (planner.cpp:108, simulator.cpp:98-106); "
                         "lru = LRU cache of lru_slots device slots (simulator.cpp:37-62)",
             "steps_per_point": args.host_split_steps, "points": rows}
@@ -646,20 +774,38 @@ def main():
     ap.add_argument("--host-split-n4", type=int, default=256)
     ap.add_argument("--host-split-points", type=lambda s: [float(v) for v in s.split(",")] if s else [],
                     default=[1.0, 0.75, 0.5, 0.25, 0.0])
-    ap.add_argument("--host-split-steps", type=int, default=4)
+    ap.add_argument("--host-split-steps", type=int, default=8)
     ap.add_argument("--host-split-lru", type=int, default=16, help="LRU device slots for the host-split LRU column")
     ap.add_argument("--no-reconfig", dest="reconfig", action="store_false")
     ap.add_argument("--reconfig-layers", type=int, default=4, help="Mixtral-shaped layers of the reconfig stack")
     ap.add_argument("--prefill-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],
                     default=[512, 2048, 4096])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--shape", choices=["mixtral", "tiny"], default="mixtral",
+                    help="tiny = BASELINE configs[0] (2 layers, d=512, ffn=1792) for quick checks; the bench "
+                         "line is always the Mixtral shape")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.shape == "tiny":
+        global D_MODEL, D_FFN, LAYERS
+        D_MODEL, D_FFN, LAYERS = 512, 1792, 2
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: relaunch this command under torchrun
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"--gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

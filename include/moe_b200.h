@@ -239,7 +239,20 @@ int moe_ffn_int4(const void* x, const int32_t* perm, const int32_t* offsets, int
 int moe_ffn_bf16(const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
                  const void* const* w_gate_up, const void* const* w_down, int E, int d, int f,
                  void* workspace, size_t ws_bytes, float* y_perm, void* stream);
-int moe_gemv_max_tokens(void);
+/* Largest T moe_ffn takes for E experts, top-k: its segment table holds
+ * min(E, T*k) + ceil(T*k/8) <= 64 (active expert, 8-token tile) segments.
+ * Larger batches belong on moe_ffn_tc. */
+int moe_gemv_max_tokens(int E, int k);
+
+/* fp16-operand range guard of the int4 paths (kernels/common.cuh).  Bit 0:
+ * a bf16 activation (x or h) above 65504 was copied to fp16 (inf); bit 1: a
+ * tcgen05 int4 dequantisation met a scale outside [2^-14, 8188] (q*s not
+ * exact).  Process-wide, sticky until read with clear != 0.  MoeEngine
+ * raises ValidationError (status 3) on it at sync for plans with int4
+ * experts.  No reference counterpart (the reference has no tensor math). */
+#define MOE_NUMERICS_F16_ACTIVATION 1u
+#define MOE_NUMERICS_F16_SCALE 2u
+int moe_numerics_status(int clear, uint32_t* flags);
 
 /* K3/K4 on the 5th-generation tensor cores (tcgen05.mma, TMEM accumulators)
  * for batched decode / prefill: the same contract as moe_ffn (x [T,d] bf16

@@ -180,7 +180,8 @@ def lib() -> C.CDLL:
         "moe_ffn_tc": (I, [VP, VP, VP, I, I, P(ExpertWeightsC), I, I, I, VP, C.c_size_t, VP, VP]),
         "moe_ffn_bf16": (I, [VP, VP, VP, I, I, P(VP), P(VP), I, I, I, VP, C.c_size_t, VP, VP]),
         "moe_pack_bf16_blocks": (I, [VP, I, I, VP, VP]),
-        "moe_gemv_max_tokens": (I, []),
+        "moe_gemv_max_tokens": (I, [I, I]),
+        "moe_numerics_status": (I, [I, C.POINTER(C.c_uint32)]),
         "moe_combine": (I, [VP, VP, VP, VP, I, I, I, VP, VP]),
         "moe_quantize_g128": (I, [VP, I, I, VP, VP, VP]),
         "moe_synth_weight_bf16": (I, [U64, U64, I64, I, VP, VP]),

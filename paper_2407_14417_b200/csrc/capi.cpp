@@ -127,6 +127,8 @@ void need_device() {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
         throw std::runtime_error("no CUDA device: kernels have no CPU fallback");
+    const cudaError_t e = moek_numerics_bind_device();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("numerics guard: ") + cudaGetErrorString(e));
 }
 
 cudaStream_t st(void* s) { return static_cast<cudaStream_t>(s); }
@@ -621,7 +623,14 @@ int moe_permute(const int32_t* idx, int T, int E, int k, int32_t* counts, int32_
     });
 }
 
-int moe_gemv_max_tokens(void) { return 8; }
+int moe_numerics_status(int clear, uint32_t* flags) {
+    return guarded([&] {
+        usage_if(flags == nullptr, "flags is null");
+        *flags = moek_numerics_status(clear);
+    });
+}
+
+int moe_gemv_max_tokens(int E, int k) { return moek_gemv_max_tokens(E, k); }
 
 size_t moe_ffn_workspace_bytes(int T, int k, int E, int d, int f) {
     if (T < 1 || k < 1 || E < 1 || d < 128 || f < 128) return 0;
@@ -637,6 +646,7 @@ int moe_ffn(const void* x, const int32_t* perm, const int32_t* offsets, int T, i
                  "d must be a multiple of 256 and f a multiple of 128");
         need_device();
         if (T == 0) return;
+        usage_if(T > moek_gemv_max_tokens(E, k), "T exceeds moe_gemv_max_tokens(E, k): use moe_ffn_tc");
         usage_if(workspace == nullptr || ws_bytes < moek_gemv_workspace_bytes(T, k, d, f),
                  "workspace too small (moe_ffn_workspace_bytes)");
         const GemvWorkspace ws = moek_gemv_workspace_view(workspace, T, k, d, f);

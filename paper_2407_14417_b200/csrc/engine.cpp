@@ -15,11 +15,54 @@
 #include <cmath>
 #include <list>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
 #include "kernels/launch.h"
 #include "moeb200/engine.hpp"
+
+#define MOE_CUDA_OK_HOST(expr)                      \
+    do {                                            \
+        cudaError_t err__ = (expr);                 \
+        if (err__ != cudaSuccess) return err__;     \
+    } while (0)
+
+// ---- fp16-operand range guard (kernels/common.cuh) ----------------------
+namespace {
+std::mutex g_num_mu;
+unsigned int* g_num_word = nullptr;  // mapped pinned host word, process-wide
+uint64_t g_num_bound = 0;            // devices whose kernel TUs point at it
+}  // namespace
+
+cudaError_t moek_numerics_bind_device() {
+    std::lock_guard<std::mutex> lk(g_num_mu);
+    int dev = 0;
+    MOE_CUDA_OK_HOST(cudaGetDevice(&dev));
+    if (dev < 64 && ((g_num_bound >> dev) & 1ull)) return cudaSuccess;
+    if (g_num_word == nullptr) {
+        void* h = nullptr;
+        MOE_CUDA_OK_HOST(cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+        g_num_word = static_cast<unsigned int*>(h);
+        *g_num_word = 0;
+    }
+    void* dp = nullptr;
+    MOE_CUDA_OK_HOST(cudaHostGetDevicePointer(&dp, g_num_word, 0));
+    unsigned int* p = static_cast<unsigned int*>(dp);
+    MOE_CUDA_OK_HOST(moek_numerics_bind_gemv(p));
+    MOE_CUDA_OK_HOST(moek_numerics_bind_router(p));
+    MOE_CUDA_OK_HOST(moek_numerics_bind_tc(p));
+    if (dev < 64) g_num_bound |= 1ull << dev;
+    return cudaSuccess;
+}
+
+unsigned int moek_numerics_status(int clear) {
+    std::lock_guard<std::mutex> lk(g_num_mu);
+    if (g_num_word == nullptr) return 0;
+    const unsigned int v = __atomic_load_n(g_num_word, __ATOMIC_ACQUIRE);
+    if (clear) __atomic_and_fetch(g_num_word, ~v, __ATOMIC_ACQ_REL);
+    return v;
+}
 
 namespace moeb200 {
 
@@ -61,10 +104,20 @@ struct MoeEngine::Impl {
     std::vector<cudaEvent_t> slot_free;
     // LRU residency (simulator.cpp:37-62): host-resident experts cached in
     // device slots, least recently used evicted; plan-resident ones pinned
+    // The accounting state (lru / lru_pos / lru_slot_of) is simulate()'s
+    // cache and is emptied by reset_counters(), as simulate() starts cold;
+    // slot_holds is the physical truth -- which expert's bytes each device
+    // slot holds -- and survives it.
     std::list<int>* lru = nullptr;
     std::map<int, std::list<int>::iterator> lru_pos;
     std::map<int, int> lru_slot_of;   // cached expert -> slot
-    std::vector<int> lru_fill;        // this layer's misses -> the slot they stream into
+    std::vector<int> slot_holds;      // [nslots]: expert whose weights the slot holds (-1: none)
+    void lru_clear() {
+        if (!lru) return;
+        lru->clear();
+        lru_pos.clear();
+        lru_slot_of.clear();
+    }
     bool lru_touch(int e) {
         const auto it = lru_pos.find(e);
         if (it == lru_pos.end()) return false;
@@ -85,7 +138,6 @@ struct MoeEngine::Impl {
         lru->push_front(e);
         lru_pos[e] = lru->begin();
         lru_slot_of[e] = slot;
-        lru_fill[static_cast<size_t>(e)] = slot;
     }
     uint16_t* wg = nullptr;  // [L][E][d]
 
@@ -173,6 +225,7 @@ struct MoeEngine::Impl {
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
             throw std::runtime_error("no CUDA device: the MoE engine has no CPU fallback");
         ck(cudaSetDevice(c.device), "cudaSetDevice");
+        ck(moek_numerics_bind_device(), "numerics guard");
         ck(cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking), "stream");
         if (c.keep_masters) {
             // reconfigure() allocates per-expert copies stream-ordered: keep
@@ -189,6 +242,7 @@ struct MoeEngine::Impl {
         nslots = c.lru_capacity > 0 ? c.lru_capacity : 1;
         slot_free.resize(static_cast<size_t>(nslots));
         for (auto& ev : slot_free) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        slot_holds.assign(static_cast<size_t>(nslots), -1);
         if (c.lru_capacity > 0) lru = new std::list<int>();
 
         // arenas
@@ -250,6 +304,10 @@ struct MoeEngine::Impl {
         dev_alloc(reinterpret_cast<void**>(&y), TK * d * 4);
         // streaming GEMV below tc_min_tokens, tcgen05 GEMM from there on
         Tgemv = std::min(Tmax, std::max(1, cfg.tc_min_tokens - 1));
+        if (Tgemv > moek_gemv_max_tokens(E, K))
+            throw UsageError("decode batches below tc_min_tokens exceed the streaming GEMV's limit for " +
+                             std::to_string(E) + " experts top-" + std::to_string(K) + " (moe_gemv_max_tokens = " +
+                             std::to_string(moek_gemv_max_tokens(E, K)) + "): lower tc_min_tokens");
         const size_t ws_bytes = moek_gemv_workspace_bytes(Tgemv, K, d, f);
         dev_alloc(&gws_base, ws_bytes);
         ck(cudaMemsetAsync(gws_base, 0, ws_bytes, compute), "memset");
@@ -441,11 +499,8 @@ struct MoeEngine::Impl {
             swap_bytes = static_cast<size_t>(plan.swap_slot_bytes);
             ck(cudaMalloc(&swap, swap_bytes * static_cast<size_t>(nslots)), "cudaMalloc(swap slots)");
         }
-        if (lru) {
-            lru->clear();
-            lru_pos.clear();
-            lru_slot_of.clear();
-        }
+        lru_clear();
+        slot_holds.assign(static_cast<size_t>(nslots), -1);  // slots may have been reallocated
         return rep;
     }
 
@@ -473,104 +528,118 @@ struct MoeEngine::Impl {
         if (copy) cudaStreamDestroy(copy);
     }
 
+    void check_numerics() {
+        bool int4 = false;
+        for (const ExpertState& st : plan.entries) int4 = int4 || st.precision == Precision::P4;
+        if (!int4) return;
+        const unsigned int v = moek_numerics_status(1);
+        if (v & MOE_NUM_F16_ACT_BIT)
+            throw ValidationError("int4 expert path: an activation (x or h) exceeds the fp16 range (|v| > 65504) "
+                                  "of the int4 kernels' fp16 operand copy; its output is not finite");
+        if (v & MOE_NUM_F16_SCALE_BIT)
+            throw ValidationError("int4 expert path (tcgen05): an int4-g128 scale lies outside [2^-14, 8188], "
+                                  "so the on-chip fp16 dequantisation q*s is inexact or infinite");
+    }
+
     uint64_t mask_all() const { return E >= 64 ? ~0ull : ((1ull << E) - 1ull); }
 
     // One MoE layer: route -> FFN (streaming CPU-resident experts through the
-    // swap slot, Static policy) -> combine with residual.
+    // swap slot(s)) -> combine with residual.  T < tc_min_tokens runs the
+    // streaming GEMV, T >= tc_min_tokens the tcgen05 GEMM; both serve plans
+    // with host-resident experts.
     void layer(int l, const uint16_t* x, int T, uint16_t* out, int32_t* idx_l, float* w_l, float* logits) {
         const moe_expert_weights* lw = weights.data() + static_cast<size_t>(l) * E;
-        const bool tc = T >= cfg.tc_min_tokens && !layer_has_cpu[static_cast<size_t>(l)];
+        const bool tc = T >= cfg.tc_min_tokens;
+        const bool host = layer_has_cpu[static_cast<size_t>(l)] != 0;
+        if (!tc && T > Tgemv) throw UsageError("T exceeds the streaming-GEMV workspace (raise tc_min_tokens / max_tokens)");
+        const uint16_t* xnorm = tc && cfg.norm_eps > 0.0f ? xn : x;  // tcgen05 B operand (natural order)
         if (tc) {
             // tcgen05 path: route writes the normalised rows in natural order
             ck(moek_route(x, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx_l, w_l, logits, counts, offsets,
                           perm, inv, ticket, compute, nullptr, nullptr, nullptr, 0, cfg.norm_eps,
                           cfg.norm_eps > 0.0f ? xn : nullptr),
                "route");
-            counters.activations += static_cast<int64_t>(T) * K;
+        } else {
+            // route also writes the K-permuted activation copies the expert
+            // GEMV reads (no separate permute kernel on the critical path)
+            ck(moek_route(x, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx_l, w_l, logits, counts,
+                          offsets, perm, inv, ticket, compute, gws.xperm, gws.xperm16, gws.xsum, moek_group_stride(d),
+                          cfg.norm_eps),
+               "route");
+        }
+        counters.activations += static_cast<int64_t>(T) * K;
+        // expert FFN of the experts in `mask` into the per-slot outputs y
+        auto ffn_y = [&](uint64_t mask, const moe_expert_weights* ew) {
+            if (tc)
+                ck(moek_ffn_tc(tcws, xnorm, perm, offsets, T, K, ew, E, d, f, mask, y, compute), "ffn_tc");
+            else
+                ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, ew, E, d, f, mask, nullptr, y, MOE_X_READY,
+                                compute), "ffn");
+        };
+        if (!host) {
             counters.hits += static_cast<int64_t>(T) * K;
-            ck(moek_ffn_tc(tcws, cfg.norm_eps > 0.0f ? xn : x, perm, offsets, T, K, lw, E, d, f, mask_all(), y,
-                           compute), "ffn_tc");
-            ck(moek_combine(y, inv, w_l, x, T, d, K, out, compute), "combine");
+            if (tc) {
+                ffn_y(mask_all(), lw);
+                ck(moek_combine(y, inv, w_l, x, T, d, K, out, compute), "combine");
+            } else {
+                ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, lw, E, d, f, mask_all(), out, nullptr,
+                                MOE_X_ROUTED, compute), "ffn");
+            }
             return;
         }
-        if (T > Tgemv) throw UsageError("T exceeds the streaming-GEMV workspace (raise tc_min_tokens / max_tokens)");
-        // route also writes the K-permuted activation copies the expert
-        // GEMV reads (no separate permute kernel on the critical path)
-        ck(moek_route(x, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx_l, w_l, logits, counts,
-                      offsets, perm, inv, ticket, compute, gws.xperm, gws.xperm16, gws.xsum, moek_group_stride(d),
-                      cfg.norm_eps),
-           "route");
-        counters.activations += static_cast<int64_t>(T) * K;
-        if (!layer_has_cpu[static_cast<size_t>(l)]) {
-            counters.hits += static_cast<int64_t>(T) * K;
-            ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, lw, E, d, f, mask_all(), out, nullptr,
-                            MOE_X_ROUTED, compute), "ffn");
-            return;
-        } else {
-            ck(cudaMemcpyAsync(idx_host, idx_l, static_cast<size_t>(T) * K * 4, cudaMemcpyDeviceToHost, compute), "D2H idx");
-            ck(cudaStreamSynchronize(compute), "sync");
-            uint64_t sel = 0;
-            lru_fill.assign(static_cast<size_t>(L) * E, -1);
-            // activation order of simulate(): tokens in order, each token's k
-            // slots ascending (the GatingTrace record order, gating.cpp:48)
-            std::vector<int32_t> order(idx_host, idx_host + static_cast<size_t>(T) * K);
-            for (int t = 0; t < T; ++t) std::sort(order.begin() + t * K, order.begin() + (t + 1) * K);
-            for (int i = 0; i < T * K; ++i) {
-                const int s = order[static_cast<size_t>(i)];
-                sel |= 1ull << s;
-                const int e = l * E + s;
-                const ExpertState st = plan.entries[static_cast<size_t>(e)];
-                // simulate()'s per-activation rule (simulator.cpp:98-106):
-                // GPU-resident, or (LRU) cached -> hit; else a transfer
-                bool hit = st.location == Location::GPU;
-                if (!hit && lru != nullptr) hit = lru_touch(e);
-                if (hit) {
-                    ++counters.hits;
-                } else {
-                    counters.bytes_transferred += static_cast<int64_t>(st.precision == Precision::P16 ? size16 : size4);
-                    if (lru != nullptr) lru_insert(e);
-                }
+        ck(cudaMemcpyAsync(idx_host, idx_l, static_cast<size_t>(T) * K * 4, cudaMemcpyDeviceToHost, compute), "D2H idx");
+        ck(cudaStreamSynchronize(compute), "sync");
+        // activation order of simulate(): tokens in order, each token's k
+        // slots ascending (the GatingTrace record order, gating.cpp:48).  At
+        // T > 1 this walks the batch inside the layer (the physical order of
+        // a batched step); simulate() walks a trace token-major across layers,
+        // so LRU hit counts equal it at T = 1 (Static at any T).
+        std::vector<int32_t> order(idx_host, idx_host + static_cast<size_t>(T) * K);
+        for (int t = 0; t < T; ++t) std::sort(order.begin() + t * K, order.begin() + (t + 1) * K);
+        uint64_t sel = 0;
+        for (int32_t s : order) sel |= 1ull << s;
+        uint64_t resident = 0;
+        for (int s = 0; s < E; ++s)
+            if (((sel >> s) & 1ull) && location[static_cast<size_t>(l * E + s)] == MOE_GPU) resident |= 1ull << s;
+        if (resident) ffn_y(resident, lw);
+        std::vector<moe_expert_weights> tmp(lw, lw + E);
+        uint64_t done = 0;
+        for (int i = 0; i < T * K; ++i) {
+            const int s = order[static_cast<size_t>(i)];
+            const int e = l * E + s;
+            const ExpertState st = plan.entries[static_cast<size_t>(e)];
+            // simulate()'s per-activation rule (simulator.cpp:98-106):
+            // GPU-resident, or (LRU) cached -> hit; else a transfer
+            bool hit = st.location == Location::GPU;
+            if (!hit && lru != nullptr) hit = lru_touch(e);
+            if (hit) {
+                ++counters.hits;
+            } else {
+                counters.bytes_transferred += static_cast<int64_t>(st.precision == Precision::P16 ? size16 : size4);
+                if (lru != nullptr) lru_insert(e);
             }
-            uint64_t resident = 0;
-            for (int s = 0; s < E; ++s)
-                if (((sel >> s) & 1ull) && location[static_cast<size_t>(l * E + s)] == MOE_GPU) resident |= 1ull << s;
-            if (resident)
-                ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, lw, E, d, f, resident, nullptr, y,
-                                MOE_X_READY, compute), "ffn");
-            std::vector<moe_expert_weights> tmp(lw, lw + E);
-            uint64_t done = 0;
-            for (int i = 0; i < T * K; ++i) {  // host experts in activation order
-                const int s = idx_host[i];
-                if (location[static_cast<size_t>(l * E + s)] == MOE_GPU || ((done >> s) & 1ull)) continue;
-                done |= 1ull << s;
-                const moe_expert_weights& hw = lw[s];
-                const size_t sz = hw.precision == MOE_P16 ? size16 : size4;
-                // the slot that holds (or will hold) expert l*E+s: an LRU hit
-                // computes from it directly; a miss -- every host activation
-                // under Static -- streams the expert in first, on the copy
-                // stream, after the slot's previous occupant was consumed
-                int slot = 0;
-                bool cached = false;
-                if (lru != nullptr) {
-                    // inserted by this layer's activations -> stream into its slot;
-                    // otherwise an LRU hit from an earlier step (capacity >= top_k,
-                    // so a touched expert is never evicted within its layer)
-                    const int fill = lru_fill[static_cast<size_t>(l * E + s)];
-                    cached = fill < 0;
-                    slot = cached ? lru_slot_of[l * E + s] : fill;
-                }
-                char* dst = swap + static_cast<size_t>(slot) * swap_bytes;
-                if (!cached) {
-                    ck(cudaStreamWaitEvent(copy, slot_free[static_cast<size_t>(slot)], 0), "wait");
-                    ck(cudaMemcpyAsync(dst, hw.w_gate_up, sz, cudaMemcpyHostToDevice, copy), "H2D expert");
-                    ck(cudaEventRecord(copy_done, copy), "record");
-                    ck(cudaStreamWaitEvent(compute, copy_done, 0), "wait");
-                }
-                tmp[static_cast<size_t>(s)] = view(dst, hw.precision == MOE_P16 ? Precision::P16 : Precision::P4);
-                ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, tmp.data(), E, d, f, 1ull << s, nullptr, y,
-                                MOE_X_READY, compute), "ffn");
-                ck(cudaEventRecord(slot_free[static_cast<size_t>(slot)], compute), "record");
+            if (st.location == Location::GPU || ((done >> s) & 1ull)) continue;
+            // first activation of host expert s in this layer: compute it now,
+            // from the slot the accounting gives it (it is there at this point
+            // of the walk; a later eviction in the same layer cannot affect a
+            // computation already ordered on the stream).  The slot's bytes are
+            // (re)streamed unless it already physically holds the expert.
+            done |= 1ull << s;
+            const moe_expert_weights& hw = lw[s];
+            const size_t sz = hw.precision == MOE_P16 ? size16 : size4;
+            const int slot = lru != nullptr ? lru_slot_of.at(e) : 0;
+            char* dst = swap + static_cast<size_t>(slot) * swap_bytes;
+            // Static re-streams every host activation (simulator.cpp:103-104)
+            if (lru == nullptr || slot_holds[static_cast<size_t>(slot)] != e) {
+                ck(cudaStreamWaitEvent(copy, slot_free[static_cast<size_t>(slot)], 0), "wait");
+                ck(cudaMemcpyAsync(dst, hw.w_gate_up, sz, cudaMemcpyHostToDevice, copy), "H2D expert");
+                ck(cudaEventRecord(copy_done, copy), "record");
+                ck(cudaStreamWaitEvent(compute, copy_done, 0), "wait");
+                slot_holds[static_cast<size_t>(slot)] = e;
             }
+            tmp[static_cast<size_t>(s)] = view(dst, hw.precision == MOE_P16 ? Precision::P16 : Precision::P4);
+            ffn_y(1ull << s, tmp.data());
+            ck(cudaEventRecord(slot_free[static_cast<size_t>(slot)], compute), "record");
         }
         ck(moek_combine(y, inv, w_l, x, T, d, K, out, compute), "combine");
     }
@@ -712,7 +781,7 @@ void MoeEngine::decode_host(const void* x_host, int T, void* out_host) {
     ck(cudaMemcpyAsync(impl_->xin, x_host, bytes, cudaMemcpyHostToDevice, impl_->compute), "H2D x");
     decode(T);
     ck(cudaMemcpyAsync(out_host, impl_->xout, bytes, cudaMemcpyDeviceToHost, impl_->compute), "D2H out");
-    ck(cudaStreamSynchronize(impl_->compute), "sync");
+    sync();
 }
 
 void MoeEngine::forward_layer(int layer, const void* x, int T, void* out, int32_t* idx, float* w,
@@ -726,7 +795,12 @@ void MoeEngine::forward_layer(int layer, const void* x, int T, void* out, int32_
     impl_->layer(layer, static_cast<const uint16_t*>(x), T, static_cast<uint16_t*>(out), idx, w, logits);
 }
 
-void MoeEngine::sync() { ck(cudaStreamSynchronize(impl_->compute), "sync"); }
+// Raises on the fp16-operand range guard when this engine's plan has int4
+// experts (only their paths compute on fp16 copies); the word is cleared.
+void MoeEngine::sync() {
+    ck(cudaStreamSynchronize(impl_->compute), "sync");
+    impl_->check_numerics();
+}
 
 void MoeEngine::profile_step(int T, float* ffn_ms, int64_t* ffn_bytes, int* kernels_per_step) {
     impl_->profile_step(T, ffn_ms, ffn_bytes, kernels_per_step);
@@ -761,7 +835,13 @@ GatingTrace MoeEngine::last_routing(int T) {
 }
 
 const SimReport& MoeEngine::counters() const { return impl_->counters; }
-void MoeEngine::reset_counters() { impl_->counters = SimReport{}; }
+// A new simulate() window: counters zeroed and the LRU accounting cache
+// emptied (simulate() starts cold, simulator.cpp:66-87); the device slots keep
+// their bytes, so an expert still physically present is not re-copied.
+void MoeEngine::reset_counters() {
+    impl_->counters = SimReport{};
+    impl_->lru_clear();
+}
 
 moe_expert_weights MoeEngine::expert(int layer, int slot, int* location) const {
     const Impl& m = *impl_;

@@ -104,6 +104,33 @@ constexpr float kInt4Bias = 136.0f;  // 128 (magic) + 8 (storage bias)
 MOE_DEVI void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 MOE_DEVI void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// fp16-operand range guard.  Both int4 paths multiply
+// against fp16 copies of bf16 activations (x, h) and tcgen05 dequantises int4
+// to fp16 q*s.  bf16 values above 65504 become inf in fp16, and scales
+// outside [2^-14, 8188] make q*s inexact or infinite.  The kernels that make
+// those fp16 values set a bit in one process-wide word of mapped pinned host
+// memory (zero cost unless it happens); the engine raises on it at its next
+// sync (moe_numerics_status).  Each translation unit holds its own pointer
+// (no -rdc), bound by its moek_numerics_bind_* function.
+enum { MOE_NUM_F16_ACT = 1u, MOE_NUM_F16_SCALE = 2u };
+static __device__ unsigned int* g_numerics = nullptr;
+MOE_DEVI void numerics_flag(unsigned int bit) {
+    unsigned int* p = g_numerics;
+    if (p != nullptr) atomicOr(p, bit);
+}
+// a bf16 value whose fp16 copy is not finite (every bf16 > 65504 is >= 65536)
+MOE_DEVI bool f16_overflow(float v) { return fabsf(v) > 65504.0f; }
+// int4 scale (bf16 bits) whose fp16 q*s, |q| <= 8, is not exact: zero is
+// fine, else 2^-14 <= |s| (fp16 normal) and 8|s| <= 65504 (|s| <= 8176 in bf16)
+MOE_DEVI bool f16_scale_bad(uint16_t sb) {
+    const uint32_t a = sb & 0x7fffu;
+    return a != 0 && (a < 0x3880u || a > 0x45ffu);
+}
+#define MOE_NUMERICS_BINDER(name)                                                         \
+    cudaError_t moek_numerics_bind_##name(unsigned int* p) {                              \
+        return cudaMemcpyToSymbol(moek::g_numerics, &p, sizeof(p));                       \
+    }
+
 // One 16-byte chunk of the K-permuted activation copies of a 128-element
 // group g (natural order in xg, any address space): chunk c*4+t holds, for
 // kk in {2c, 2c+1}, hi in {0,1}, e in {0,1}, the element kk*16 + hi*8 + t*2 + e:
@@ -128,6 +155,7 @@ MOE_DEVI void permute_chunk(const T* xg, int chunk, uint4& cb, uint4& ch, float&
             wh[hi * 2 + kq] = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f0))) |
                               (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f1))) << 16);
             if (hi) s_hi += f0 + f1; else s_lo += f0 + f1;
+            if (f16_overflow(f0) || f16_overflow(f1)) numerics_flag(MOE_NUM_F16_ACT);
         }
     }
     cb = make_uint4(wb[0], wb[1], wb[2], wb[3]);

@@ -33,6 +33,7 @@
 // against an fp16 copy of the activations (exact for 2^-17 <= |x| <= 65504);
 // the per-128-K-group scale is applied after the group's integer-exact dot,
 // y += s * sum(q*x) -- the exact dequant values q*s.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -859,6 +860,15 @@ __global__ void permute_rows_kernel(const uint16_t* __restrict__ x, int rows, in
 int group_stride(int K) { return (K / 128 + 7) / 8 * 8; }
 }  // namespace moek
 int moek_group_stride(int K) { return moek::group_stride(K); }
+// Largest T whose (active expert, 8-token tile) segments always fit the
+// kernel's table: at most min(E, T*k) experts are active and their segments
+// number at most min(E, T*k) + ceil(T*k / 8).
+int moek_gemv_max_tokens(int E, int k) {
+    if (E < 1 || k < 1) return 0;
+    int T = 0;
+    while (std::min(E, (T + 1) * k) + ((T + 1) * k + moek::kTile - 1) / moek::kTile <= moek::kMaxSegs) ++T;
+    return T;
+}
 namespace moek {
 
 template <class C>
@@ -970,7 +980,7 @@ cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* 
                          const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask, void* out,
                          float* y, int xmode, cudaStream_t stream) {
     // every (active expert, 8-token tile) segment must fit the kernel's table
-    if (E + (T * k + moek::kTile - 1) / moek::kTile > moek::kMaxSegs) return cudaErrorInvalidValue;
+    if (moek_gemv_max_tokens(E, k) < T) return cudaErrorInvalidValue;
     if (d % (moek::kFinOQuads * 4) != 0 || f % 128 != 0) return cudaErrorInvalidValue;
     if (xmode == MOE_X_PERMUTE) MOE_CUDA_OK(moek_permute_rows(x, T, d, ws.xperm, ws.xperm16, ws.xsum, stream));
     const int nslots = T * k;
@@ -1024,3 +1034,5 @@ cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* 
                             d, inv, wts, static_cast<const uint16_t*>(resid), static_cast<uint16_t*>(out), y,
                             ws.sched + 1);
 }
+
+MOE_NUMERICS_BINDER(gemv)

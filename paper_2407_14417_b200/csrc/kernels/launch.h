@@ -42,6 +42,8 @@ cudaError_t moek_permute_rows(const void* x, int rows, int K, void* xperm, void*
 //                  after an event wait for a streamed expert)
 enum { MOE_X_PERMUTE = 0, MOE_X_ROUTED = 1, MOE_X_READY = 2 };
 int moek_group_stride(int K);
+// Largest decode batch the streaming GEMV takes for E experts, top-k (segment table bound).
+int moek_gemv_max_tokens(int E, int k);
 cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* perm,
                          const int32_t* offsets, const int32_t* inv, const float* wts,
                          const void* resid, int T, int k, const moe_expert_weights* experts, int E,
@@ -53,6 +55,15 @@ size_t moek_tc_workspace_bytes(int T, int k, int d, int f);
 cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
                         const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask, float* y,
                         cudaStream_t stream);
+// fp16-operand range guard (common.cuh): bind each kernel translation unit
+// to the process-wide flag word (mapped pinned host memory) on the current device.
+cudaError_t moek_numerics_bind_gemv(unsigned int* p);
+cudaError_t moek_numerics_bind_router(unsigned int* p);
+cudaError_t moek_numerics_bind_tc(unsigned int* p);
+enum { MOE_NUM_F16_ACT_BIT = 1, MOE_NUM_F16_SCALE_BIT = 2 };  // = common.cuh MOE_NUM_F16_*
+// Binds the current device (once per device; engine.cpp) and reads / clears the word.
+cudaError_t moek_numerics_bind_device();
+unsigned int moek_numerics_status(int clear);
 // Storage-layout converters (logical row-major -> fragment blocks).
 // fragment blocks -> logical row-major bf16 (inverse of moek_pack_bf16_blocks)
 cudaError_t moek_unpack_bf16_blocks(const void* in, int rows, int cols, void* w, cudaStream_t stream);

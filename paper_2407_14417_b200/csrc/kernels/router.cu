@@ -420,3 +420,5 @@ cudaError_t moek_permute(const int32_t* idx, int T, int E, int k, int32_t* count
 cudaError_t moek_debug_layer_trace_router(void* host_ptr, cudaStream_t stream) {
     return cudaMemcpyToSymbolAsync(moek::g_layer_trace, host_ptr, sizeof(void*), 0, cudaMemcpyHostToDevice, stream);
 }
+
+MOE_NUMERICS_BINDER(router)

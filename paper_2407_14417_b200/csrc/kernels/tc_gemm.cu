@@ -255,6 +255,7 @@ MOE_DEVI void convert_int4(int nmat, const uint8_t* raw, uint8_t* can, int ct, c
         for (int j = 0; j < 2; ++j) {
             const uint2 w2 = *reinterpret_cast<const uint2*>(src + o.qrow[j]);
             const uint16_t sb = *reinterpret_cast<const uint16_t*>(sc + o.qsc[j]);
+            if (f16_scale_bad(sb)) numerics_flag(MOE_NUM_F16_SCALE);
             const __half sh = __float2half_rn(bf2f(sb));  // exact for normal-range scales
             const __half2 s2 = __halves2half2(sh, sh);
 #pragma unroll
@@ -443,6 +444,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
                         const uint16_t hb = f2bf(silu_f(__uint_as_float(g[c])) * __uint_as_float(u[c]));
                         const size_t o = static_cast<size_t>(tl.slot0 + n) * a.f + tl.R0 + row;
                         a.hout[o] = hb;
+                        if (f16_overflow(bf2f(hb))) numerics_flag(MOE_NUM_F16_ACT);
                         a.hout16[o] = __half_as_ushort(__float2half_rn(bf2f(hb)));
                     }
                 }
@@ -483,6 +485,7 @@ __global__ void gather_rows_kernel(const uint16_t* __restrict__ x, const int32_t
         for (int q = 0; q < 4; ++q)
             h[q] = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(bf16_lo(w[q])))) |
                    (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(bf16_hi(w[q])))) << 16);
+            if (f16_overflow(bf16_lo(w[q])) || f16_overflow(bf16_hi(w[q]))) numerics_flag(MOE_NUM_F16_ACT);
         reinterpret_cast<uint4*>(xs16 + static_cast<size_t>(slot) * d)[c] = make_uint4(h[0], h[1], h[2], h[3]);
     }
 }
@@ -581,3 +584,5 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     return moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (d / kM))), dim3(kThreads2), smem, stream,
                             a);
 }
+
+MOE_NUMERICS_BINDER(tc)

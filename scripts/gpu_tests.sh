@@ -1,2 +1,4 @@
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -25
+# GPU tests only (optionally a -k filter in $K)
+cd $GRAFT_REPO_ROOT
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider ${K:+-k "$K"} --durations=15 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -25 gpurun_out/pytest_gpu.log

@@ -18,6 +18,27 @@ def bf16_to_f32(a):
     return (np.asarray(a).astype(np.uint32) << 16).view(np.float32)
 
 
+def assert_delta_close(out_gpu, out_ref, x, rtol=RTOL_BF16, what=""):
+    """Elementwise check of a layer's MoE term: out = bf16(x + MoE(x)), so
+    compare out - x against the oracle's out - x element by element with
+    |gpu - ref| <= rtol * |ref - x| + ulp_bf16(ref) + floor, where one bf16
+    ulp at |out| absorbs the two independent output roundings and floor =
+    1e-3 * max|ref - x| keeps exact-zero terms meaningful.  Unlike a normwise
+    check on out, the residual cannot dilute an error in the MoE term."""
+    g = bf16_to_f32(out_gpu).astype(np.float64)
+    r = bf16_to_f32(out_ref).astype(np.float64)
+    xv = bf16_to_f32(x).astype(np.float64)
+    dref = r - xv
+    ulp = np.ldexp(1.0, np.frexp(np.abs(r))[1] - 8)  # bf16: 8 significant bits
+    floor = 1e-3 * max(np.abs(dref).max(), 1e-30)
+    err = np.abs(g - r)
+    tol = rtol * np.abs(dref) + ulp + floor
+    bad = err > tol
+    assert not bad.any(), (f"{what}: {int(bad.sum())} of {bad.size} elements off; worst |err| "
+                           f"{err[bad].max():.3e} at |moe term| {np.abs(dref)[bad][np.argmax(err[bad])]:.3e}")
+    return float((err / np.maximum(np.abs(dref), floor)).max())
+
+
 def normwise_err(got, ref):
     got = np.asarray(got, np.float64)
     ref = np.asarray(ref, np.float64)

@@ -172,12 +172,32 @@ def test_ffn_grouped_vs_oracle(moe, orc, torch_mod, cuda, T, mix, shape):
         assert_close(y[lo:hi], y_ref, RTOL_F32, f"expert {e} ({'bf16' if prec[e] else 'int4'})")
 
 
+def _sample_rows(lo, hi, full):
+    """All rows of a segment, or (large Mixtral segments) rows on both sides
+    of every 128-token tile boundary plus the segment's last rows."""
+    if full:
+        return np.arange(lo, hi)
+    picks = set()
+    for b in range(0, hi - lo, 128):
+        picks.update(lo + v for v in (b, b + 1, b + 127) if lo + v < hi)
+    picks.update(range(max(lo, hi - 3), hi))
+    return np.array(sorted(picks))
+
+
+# T * k > 128 * (active experts) selects the 256-token tile variant
+# (tc_gemm.cu moek_ffn_tc): T = 520 / 777 (tiny, 8 active experts; 777 ends
+# on a partial 256-token tile), skew (2 active experts, 600 slots), T = 1024
+# at Mixtral shape.
 @pytest.mark.parametrize("mix", ["bf16", "int4", "mixed"])
-@pytest.mark.parametrize("T,shape", [(40, (512, 1792)), (300, (512, 1792)), (96, (4096, 14336))])
-def test_ffn_tcgen05_vs_oracle(moe, orc, torch_mod, cuda, T, shape, mix):
+@pytest.mark.parametrize("T,shape,skew", [(40, (512, 1792), False), (300, (512, 1792), False),
+                                          (96, (4096, 14336), False), (520, (512, 1792), False),
+                                          (777, (512, 1792), False), (300, (512, 1792), True),
+                                          (1024, (4096, 14336), False)])
+def test_ffn_tcgen05_vs_oracle(moe, orc, torch_mod, cuda, T, shape, skew, mix):
     """K3/K4 on tcgen05 (batched / prefill path): every expert's y rows vs
     the oracle FFN on the same tokens (bf16: BF16 operands; int4: on-chip
-    fp16 q*s, exact dequant values)."""
+    fp16 q*s, exact dequant values).  Covers the 128- and 256-token tile
+    variants, partial last tiles and skewed routing."""
     torch = torch_mod
     (d, f), E, k = shape, 8, 2
     m = orc.model(1, E, k, d, f, 99)
@@ -185,7 +205,11 @@ def test_ffn_tcgen05_vs_oracle(moe, orc, torch_mod, cuda, T, shape, mix):
     x = orc.step_input(m, T, T)
     wg = orc.router_weights(m, 0)
     idx, w, _ = orc.gate_topk(x, wg, T, d, E, k)
+    if skew:  # every token on experts 5 and 2 (one int4, one bf16 in the mixed plan)
+        idx = np.tile(np.array([5, 2], np.int32), (T, 1))
     counts, offsets, perm, inv = orc.permute(idx, T, E, k)
+    wide = T * k > 128 * int((counts > 0).sum())
+    assert wide == (T in (520, 777, 1024) or skew)
     experts, host, keep = [], {}, []
     for e in range(E):
         dev, h = _expert_tensors(orc, torch, cuda, m, e, prec[e])
@@ -202,16 +226,18 @@ def test_ffn_tcgen05_vs_oracle(moe, orc, torch_mod, cuda, T, shape, mix):
                ws, nws, y)
     torch.cuda.synchronize()
     y = to_np(y, np.float32).reshape(T * k, d)
+    assert np.isfinite(y).all(), "every slot is written"
     for e in range(E):
         lo, hi = offsets[e], offsets[e + 1]
         if lo == hi:
             continue
-        xs = x[perm[lo:hi] // k]
+        rows = _sample_rows(lo, hi, full=d < 4096 or hi - lo <= 64)
+        xs = x[perm[rows] // k]
         if prec[e] == 1:
-            y_ref = orc.ffn_bf16(xs, hi - lo, host[e][0], host[e][1], d, f)
+            y_ref = orc.ffn_bf16(xs, len(rows), host[e][0], host[e][1], d, f)
         else:
-            y_ref = orc.ffn_int4(xs, hi - lo, *host[e], d, f)
-        assert_close(y[lo:hi], y_ref, RTOL_F32, f"expert {e} ({'bf16' if prec[e] else 'int4'})")
+            y_ref = orc.ffn_int4(xs, len(rows), *host[e], d, f)
+        assert_close(y[rows], y_ref, RTOL_F32, f"expert {e} ({'bf16' if prec[e] else 'int4'})")
 
 
 def test_combine_bitexact(moe, orc, torch_mod, cuda):
