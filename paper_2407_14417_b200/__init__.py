@@ -770,6 +770,17 @@ def ffn(x, perm, offsets, T, k, experts: Sequence[ExpertWeightsC], d, f, workspa
                          ws_bytes, _ptr(y_perm), _stream(stream)))
 
 
+NUMERICS_F16_ACTIVATION = 1
+NUMERICS_F16_SCALE = 2
+
+
+def numerics_status(clear: bool = True) -> int:
+    """fp16-operand range guard bits (moe_numerics_status); sticky until cleared."""
+    v = C.c_uint32()
+    _check(lib().moe_numerics_status(1 if clear else 0, C.byref(v)))
+    return v.value
+
+
 def route(x, wg, T, d, E, k, norm_eps, idx, w, logits=None, counts=None, offsets=None, perm=None, inv_perm=None,
           xnat=None, ticket=None, stream=None):
     """K1+K2 fused (RMSNorm -> router -> top-k -> stable permutation)."""

@@ -755,9 +755,10 @@ int moe_weight_shift(int K) { return weight_shift(K); }
 int moe_stream_expert(void* dst_dev, const void* src_pinned, size_t bytes, void* copy_stream,
                       void* done_event) {
     return guarded([&] {
+        usage_if(bytes > 0 && (dst_dev == nullptr || src_pinned == nullptr), "null buffer");
         need_device();
-        cudaError_t e = cudaMemcpyAsync(dst_dev, src_pinned, bytes, cudaMemcpyHostToDevice, st(copy_stream));
-        if (e == cudaSuccess && done_event) e = cudaEventRecord(static_cast<cudaEvent_t>(done_event), st(copy_stream));
+        const cudaError_t e = moek_stream_expert(dst_dev, src_pinned, bytes, st(copy_stream),
+                                                 static_cast<cudaEvent_t>(done_event));
         if (e != cudaSuccess) throw std::runtime_error(std::string("moe_stream_expert: ") + cudaGetErrorString(e));
     });
 }

@@ -56,6 +56,11 @@ cudaError_t moek_numerics_bind_device() {
     return cudaSuccess;
 }
 
+cudaError_t moek_stream_expert(void* dst, const void* src_pinned, size_t bytes, cudaStream_t copy, cudaEvent_t done) {
+    MOE_CUDA_OK_HOST(cudaMemcpyAsync(dst, src_pinned, bytes, cudaMemcpyHostToDevice, copy));
+    return done != nullptr ? cudaEventRecord(done, copy) : cudaSuccess;
+}
+
 unsigned int moek_numerics_status(int clear) {
     std::lock_guard<std::mutex> lk(g_num_mu);
     if (g_num_word == nullptr) return 0;
@@ -632,8 +637,7 @@ struct MoeEngine::Impl {
             // Static re-streams every host activation (simulator.cpp:103-104)
             if (lru == nullptr || slot_holds[static_cast<size_t>(slot)] != e) {
                 ck(cudaStreamWaitEvent(copy, slot_free[static_cast<size_t>(slot)], 0), "wait");
-                ck(cudaMemcpyAsync(dst, hw.w_gate_up, sz, cudaMemcpyHostToDevice, copy), "H2D expert");
-                ck(cudaEventRecord(copy_done, copy), "record");
+                ck(moek_stream_expert(dst, hw.w_gate_up, sz, copy, copy_done), "H2D expert");
                 ck(cudaStreamWaitEvent(compute, copy_done, 0), "wait");
                 slot_holds[static_cast<size_t>(slot)] = e;
             }

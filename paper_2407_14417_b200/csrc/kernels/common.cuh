@@ -106,8 +106,11 @@ MOE_DEVI void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :
 
 // fp16-operand range guard.  Both int4 paths multiply
 // against fp16 copies of bf16 activations (x, h) and tcgen05 dequantises int4
-// to fp16 q*s.  bf16 values above 65504 become inf in fp16, and scales
-// outside [2^-14, 8188] make q*s inexact or infinite.  The kernels that make
+// to fp16 q*s.  bf16 values above 65504 become inf in fp16; a 128-element
+// activation group whose largest magnitude is below 2^-14 keeps few or no
+// bits (the GEMV copies; single tiny elements in a normal group are
+// negligible and not flagged); scales outside [2^-14, 8188] make q*s
+// inexact or infinite.  The kernels that make
 // those fp16 values set a bit in one process-wide word of mapped pinned host
 // memory (zero cost unless it happens); the engine raises on it at its next
 // sync (moe_numerics_status).  Each translation unit holds its own pointer
@@ -139,11 +142,12 @@ MOE_DEVI bool f16_scale_bad(uint16_t sb) {
 // Also returns this chunk's partial sums over k%16 < 8 (hi = 0) and >= 8
 // (hi = 1) for the int4 bias term (summed in element order kk, e).
 template <class T>
-MOE_DEVI void permute_chunk(const T* xg, int chunk, uint4& cb, uint4& ch, float& s_lo, float& s_hi) {
+MOE_DEVI void permute_chunk(const T* xg, int chunk, uint4& cb, uint4& ch, float& s_lo, float& s_hi, float& amax) {
     const int c = chunk >> 2, t = chunk & 3;
     uint32_t wb[4], wh[4];
     s_lo = 0.0f;
     s_hi = 0.0f;
+    amax = 0.0f;
 #pragma unroll
     for (int kq = 0; kq < 2; ++kq) {
 #pragma unroll
@@ -156,10 +160,20 @@ MOE_DEVI void permute_chunk(const T* xg, int chunk, uint4& cb, uint4& ch, float&
                               (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f1))) << 16);
             if (hi) s_hi += f0 + f1; else s_lo += f0 + f1;
             if (f16_overflow(f0) || f16_overflow(f1)) numerics_flag(MOE_NUM_F16_ACT);
+            amax = fmaxf(amax, fmaxf(fabsf(f0), fabsf(f1)));
         }
     }
     cb = make_uint4(wb[0], wb[1], wb[2], wb[3]);
     ch = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+}
+
+// The 16 chunk maxima of a 128-element group (lanes xor 8..1 of a half
+// warp; every lane of the warp must call): a nonzero group entirely below
+// the fp16 normal range (2^-14) keeps few or no bits in its fp16 copy.
+MOE_DEVI void numerics_group_check(float amax, bool leader) {
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+    if (leader && amax > 0.0f && amax < 6.103515625e-05f) numerics_flag(MOE_NUM_F16_ACT);
 }
 
 // Debug layer trace (moe_debug_layer_trace): per kernel id, the earliest

@@ -740,8 +740,9 @@ __global__ void __launch_bounds__(kFinHThreads) finalize_h_kernel(
     for (int j = 0; j < 4; ++j) hs[lane * 4 + j] = f2bf(silu_f(gv[j]) * uv[j]);
     __syncwarp();
     uint4 cb = make_uint4(0, 0, 0, 0), ch = cb;
-    float s_lo = 0.0f, s_hi = 0.0f;
-    if (lane < 16) permute_chunk(hs, lane, cb, ch, s_lo, s_hi);
+    float s_lo = 0.0f, s_hi = 0.0f, amax = 0.0f;
+    if (lane < 16) permute_chunk(hs, lane, cb, ch, s_lo, s_hi, amax);
+    numerics_group_check(amax, lane == 0);
     const size_t o = static_cast<size_t>(slot) * f + g * 128;
     if (lane < 16) {
         reinterpret_cast<uint4*>(hperm + o)[lane] = cb;
@@ -844,8 +845,9 @@ __global__ void permute_rows_kernel(const uint16_t* __restrict__ x, int rows, in
     const long long r = ok ? hw / G : 0;
     const int g = ok ? static_cast<int>(hw - r * G) : 0;
     uint4 cb = make_uint4(0, 0, 0, 0), ch = cb;
-    float s_lo = 0.0f, s_hi = 0.0f;
-    if (ok) permute_chunk(x + r * K + g * 128, c, cb, ch, s_lo, s_hi);
+    float s_lo = 0.0f, s_hi = 0.0f, amax = 0.0f;
+    if (ok) permute_chunk(x + r * K + g * 128, c, cb, ch, s_lo, s_hi, amax);
+    numerics_group_check(amax, ok && c == 0);
 #pragma unroll
     for (int off = 8; off >= 1; off >>= 1) {
         s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);

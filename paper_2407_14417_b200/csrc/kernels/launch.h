@@ -55,6 +55,9 @@ size_t moek_tc_workspace_bytes(int T, int k, int d, int f);
 cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
                         const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask, float* y,
                         cudaStream_t stream);
+// Host-resident expert streaming (engine.cpp): pinned H2D of one expert on
+// the copy stream, recorded on `done` (may be null) for the compute stream.
+cudaError_t moek_stream_expert(void* dst, const void* src_pinned, size_t bytes, cudaStream_t copy, cudaEvent_t done);
 // fp16-operand range guard (common.cuh): bind each kernel translation unit
 // to the process-wide flag word (mapped pinned host memory) on the current device.
 cudaError_t moek_numerics_bind_gemv(unsigned int* p);

@@ -339,8 +339,9 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
         for (int g0 = (wid - 1) * 2; wid > 0 && g0 < G; g0 += nw * 2) {
             const int g = g0 + (lane >> 4), c = lane & 15;
             uint4 cb = make_uint4(0, 0, 0, 0), ch = cb;
-            float s_lo = 0.0f, s_hi = 0.0f;
-            if (g < G) permute_chunk(x_s + g * 128, c, cb, ch, s_lo, s_hi);
+            float s_lo = 0.0f, s_hi = 0.0f, amax = 0.0f;
+            if (g < G) permute_chunk(x_s + g * 128, c, cb, ch, s_lo, s_hi, amax);
+            numerics_group_check(amax, c == 0);
 #pragma unroll
             for (int off = 8; off >= 1; off >>= 1) {
                 s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);

@@ -482,10 +482,11 @@ __global__ void gather_rows_kernel(const uint16_t* __restrict__ x, const int32_t
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
         uint32_t h[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < 4; ++q) {
             h[q] = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(bf16_lo(w[q])))) |
                    (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(bf16_hi(w[q])))) << 16);
             if (f16_overflow(bf16_lo(w[q])) || f16_overflow(bf16_hi(w[q]))) numerics_flag(MOE_NUM_F16_ACT);
+        }
         reinterpret_cast<uint4*>(xs16 + static_cast<size_t>(slot) * d)[c] = make_uint4(h[0], h[1], h[2], h[3]);
     }
 }
