@@ -52,25 +52,27 @@ METRIC = "decode tokens/s vs #4-bit experts (Mixtral-8x7B shape); expert-FFN HBM
 TRAFFIC_INPUT = 7  # the token input profile_step runs for the roofline (and tools/traffic.py under ncu)
 
 
-def _traffic(n4, T, alg_bytes_per_layer):
-    """ncu dram read+write per layer of the expert FFN launches, captured by
+def _traffic(n4, T, alg_bytes, fused=False):
+    """ncu dram read+write of the dominant launch(es), captured by
     tools/traffic.py for this configuration and input (profiles/r02_traffic.json),
     next to the algorithmic bytes of the same step; null when absent or when
-    the recorded algorithmic bytes disagree (another kernel or routing)."""
+    the recorded algorithmic bytes disagree (another kernel or routing).
+    fused: per launch of decode_step_kernel (one step); else per layer of the
+    expert-FFN launches."""
     path = os.path.join(ROOT, "profiles", "r02_traffic.json")
     try:
         with open(path) as fh:
             t = json.load(fh)
     except Exception:
         return None, "no ncu traffic capture for this configuration"
-    if (t.get("n4"), t.get("tokens"), t.get("input")) != (n4, T, TRAFFIC_INPUT) or \
-            int(t["algorithmic_bytes_per_layer"]) != int(alg_bytes_per_layer):
-        return None, "profiles/r02_traffic.json was captured for another configuration"
-    return int(t["dram_bytes_per_layer"]), ("ncu dram__bytes_read+write per layer of the expert-FFN launches "
-                                             "(stream_kernel x2 + finalize_h + finalize_out) of one step on input %d, "
-                                             "averaged over the %d layers (profiles/r02_traffic.json, %s); "
-                                             "algorithmic %d B per layer" % (TRAFFIC_INPUT, LAYERS, t.get("commit", "?"),
-                                                                            int(t["algorithmic_bytes_per_layer"])))
+    key = "fused" if fused else "per_layer"
+    t = t.get(key, t if not fused else None)
+    if not t or (t.get("n4"), t.get("tokens"), t.get("input")) != (n4, T, TRAFFIC_INPUT) or \
+            int(t["algorithmic_bytes"]) != int(alg_bytes):
+        return None, "profiles/r02_traffic.json has no capture of this kernel / configuration"
+    return int(t["dram_bytes"]), ("ncu dram__bytes_read+write of %s on input %d (profiles/r02_traffic.json, "
+                                  "commit %s); algorithmic %d B" % (t["what"], TRAFFIC_INPUT, t.get("commit", "?"),
+                                                                    int(t["algorithmic_bytes"])))
 
 
 def _peak_tflops():
@@ -360,19 +362,40 @@ def run_ours(args, rank, world, device):
         ms = float(t.item())
     value = world * T * 1000.0 / ms
 
-    # ---- roofline: per-layer expert FFN (gate/up + down), CUDA events -----
-    ffn_ms, ffn_bytes = [], []
-    for _ in range(3):
-        eng.synth_input(TRAFFIC_INPUT, T)
-        m_, b_, kps = eng.profile_step(T)
-        ffn_ms += m_
-        ffn_bytes += b_
-    traffic, traffic_note = _traffic(args.n4, T, round(sum(ffn_bytes[:LAYERS]) / LAYERS))
-    avg_ms = sum(ffn_ms) / len(ffn_ms)
-    avg_bytes = sum(ffn_bytes) / len(ffn_bytes)
+    # ---- roofline ------------------------------------------------------------
+    # batch 1: the fused decode step is ONE launch (decode_step_kernel) --
+    # timed alone between CUDA events on the engine stream, against the
+    # algorithmic bytes of the routing it made; otherwise the per-layer
+    # expert FFN launches (gate/up stream + finalize_h + down stream +
+    # finalize_out) bracketed per layer
+    fused = eng.profile_fused() is not None
+    if fused:
+        runs = []
+        for _ in range(5):
+            eng.synth_input(TRAFFIC_INPUT, T)
+            runs.append(eng.profile_fused())
+        avg_ms = sorted(r[0] for r in runs)[len(runs) // 2]
+        avg_bytes = runs[0][1]
+        kps = 1
+        ffn_share = avg_ms / ms
+        traffic, traffic_note = _traffic(args.n4, T, avg_bytes, fused=True)
+        kernel_desc = ("decode_step_kernel: the whole %d-layer batch-1 step in one cooperative launch (routing, "
+                       "gate/up GEMV, SwiGLU, down GEMV, combine per layer), CUDA events on the engine stream; "
+                       "median of 5 launches on input %d" % (LAYERS, TRAFFIC_INPUT))
+    else:
+        ffn_ms, ffn_bytes = [], []
+        for _ in range(3):
+            eng.synth_input(TRAFFIC_INPUT, T)
+            m_, b_, kps = eng.profile_step(T)
+            ffn_ms += m_
+            ffn_bytes += b_
+        traffic, traffic_note = _traffic(args.n4, T, round(sum(ffn_bytes[:LAYERS]) / LAYERS))
+        avg_ms = sum(ffn_ms) / len(ffn_ms)
+        avg_bytes = sum(ffn_bytes) / len(ffn_bytes)
+        ffn_share = (avg_ms * LAYERS) / ms
+        kernel_desc = ("expert FFN per layer: stream_kernel (gate/up) + finalize_h + stream_kernel (down) + "
+                       "finalize_out, CUDA events on the engine stream")
     achieved = avg_bytes / (avg_ms * 1e-3) / 1e9
-    ffn_share = (avg_ms * LAYERS) / ms
-    step_bytes = sum(ffn_bytes[:LAYERS])
 
     # ---- e2e through the public API with host buffers -----------------------
     import numpy as np
@@ -484,10 +507,9 @@ def run_ours(args, rank, world, device):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                          "traffic_note": traffic_note,
-                         "kernel": "expert FFN per layer: stream_kernel (gate/up) + finalize_h + "
-                                   "stream_kernel (down) + finalize_out, CUDA events on the engine stream",
+                         "kernel": kernel_desc,
                          "bytes_per_launch": round(avg_bytes), "ms_per_launch": round(avg_ms, 5),
-                         "ffn_share_of_step": round(ffn_share, 4),
+                         "share_of_step": round(ffn_share, 4),
                          "frac_of_nominal_8000_gbs": round(achieved / 8000.0, 4)},
             "gpu_launches": kps * (args.steps),
             "kernels_per_step": kps,

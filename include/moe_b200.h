@@ -321,6 +321,10 @@ typedef struct {
     int32_t keep_masters;      /* 1: pinned host copy of every expert in both precisions (the reconfig
                                   model's 16-bit CPU master, reconfig.hpp:39); needed by
                                   moe_engine_reconfigure */
+    int32_t per_layer_decode;  /* 0 (default): a batch-1 decode step of an all-resident plan is ONE
+                                  cooperative persistent launch (routing, both GEMV passes, SwiGLU and
+                                  combine of every layer, grid barriers between phases); 1: five launches
+                                  per layer (the same arithmetic, bit-identical output) */
 } moe_engine_config;
 
 int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan_entries,
@@ -349,6 +353,11 @@ int moe_engine_sync(moe_engine* eng);
  * (selected experts' weights + activations), kernels launched per step. */
 int moe_engine_profile_step(moe_engine* eng, int T, float* ffn_ms, int64_t* ffn_bytes,
                             int32_t* kernels_per_step);
+/* The fused batch-1 step timed alone (one launch between CUDA events on the
+ * engine stream): *ms its duration, *bytes the algorithmic bytes it moves
+ * (every layer's distinct selected experts + activations).  Status 2 when
+ * the engine does not use the fused step. */
+int moe_engine_profile_fused(moe_engine* eng, float* ms, int64_t* bytes);
 void* moe_engine_stream(moe_engine* eng);
 /* Routing of the last decode step: slots [T, L, k] ascending per record
  * (GatingTrace layout, gating.hpp:22) -- host buffer. */
@@ -434,6 +443,14 @@ int moe_debug_gemv_trace(void* buf);
  * pre-filled with UINT64_MAX and end slots with 0; NULL disables.  Set in
  * stream order on `stream`, so it can bracket exactly one graph replay. */
 int moe_debug_layer_trace(void* buf, void* stream);
+/* Debug: device buffer [num_layers][#SMs][10] uint64 receiving, per layer and
+ * CTA of the fused batch-1 step, globaltimer stamps at: layer start, routing
+ * done, gate/up done, after barrier 1, SwiGLU done, after barrier 2, h rows
+ * resident, down done, after barrier 3, combine done; NULL disables. */
+int moe_debug_fused_trace(void* buf);
+/* Debug: device pointer and size of one of the engine's GEMV workspace
+ * buffers (0 gate/up partials, 1 down partials, 2 h bf16, 3 h fp16, 4 h bias). */
+int moe_debug_engine_buffer(moe_engine* eng, int which, void** ptr, size_t* bytes);
 
 #ifdef __cplusplus
 }

@@ -37,6 +37,8 @@ struct EngineConfig {
     float norm_eps = 0.0f;    // > 0: pre-MoE RMSNorm (unit weight), residual = un-normalised x
     int tc_min_tokens = 32;   // T >= this: tcgen05 expert GEMM instead of the streaming GEMV (measured crossover)
     int lru_capacity = 0;     // 0: Static swap slot (simulator.hpp ResidencyPolicy::Static); >0: LRU of that many slots
+    bool per_layer_decode = false;  // true: batch-1 decode as 5 launches per layer instead of the fused
+                                    // one-launch step (decode_step_kernel); for A/B and the host-split path
     bool keep_masters = false;  // pinned host copy of every expert in both precisions (the reconfig
                                 // model's "16-bit master on the CPU", reconfig.hpp:39): required by reconfigure()
 };
@@ -71,6 +73,15 @@ class MoeEngine {
     // Eager step with CUDA events around every layer's expert FFN (see
     // engine.cpp); ffn_ms / ffn_bytes have num_layers entries.
     void profile_step(int T, float* ffn_ms, int64_t* ffn_bytes, int* kernels_per_step);
+    // The fused batch-1 step (decode_step_kernel) timed alone: one launch on
+    // stream() between CUDA events -> its duration, and the algorithmic bytes
+    // it must move (all layers, from the routing it made).  False when the
+    // engine does not use the fused step.
+    bool profile_fused(float* ms, int64_t* bytes);
+    bool fused() const;
+    // Debug: device pointer + size of a GEMV workspace buffer (0 part0, 1
+    // part1, 2 hperm, 3 hperm16, 4 hsum) for intermediate comparisons.
+    void* debug_buffer(int which, size_t* bytes);
 
     // Executes diff_plans(current plan, target) on the device (SURVEY.md §8f
     // f1): Offload releases the device copy (the expert streams from its host

@@ -96,7 +96,8 @@ class _EngineConfig(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("experts_per_layer", C.c_int32), ("top_k", C.c_int32),
                 ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("max_tokens", C.c_int32),
                 ("seed", C.c_uint64), ("device", C.c_int32), ("use_graphs", C.c_int32), ("norm_eps", C.c_float),
-                ("tc_min_tokens", C.c_int32), ("lru_capacity", C.c_int32), ("keep_masters", C.c_int32)]
+                ("tc_min_tokens", C.c_int32), ("lru_capacity", C.c_int32), ("keep_masters", C.c_int32),
+                ("per_layer_decode", C.c_int32)]
 
 
 _lib = None
@@ -200,6 +201,9 @@ def lib() -> C.CDLL:
         "moe_engine_forward_layer": (I, [VP, I, VP, I, VP, VP, VP, VP]),
         "moe_engine_sync": (I, [VP]),
         "moe_engine_profile_step": (I, [VP, I, P(C.c_float), P(I64), P(C.c_int32)]),
+        "moe_engine_profile_fused": (I, [VP, P(C.c_float), P(I64)]),
+        "moe_debug_fused_trace": (I, [VP]),
+        "moe_debug_engine_buffer": (I, [VP, I, P(VP), P(C.c_size_t)]),
         "moe_engine_last_routing": (I, [VP, I, P(C.c_int32)]),
         "moe_engine_counters": (I, [VP, P(SimReportC)]),
         "moe_engine_reset_counters": (I, [VP]),
@@ -838,12 +842,13 @@ class MoeEngine:
     def __init__(self, num_layers: int, experts_per_layer: int, top_k: int, d_model: int, d_ffn: int,
                  plan: PlacementPlan, max_tokens: int = 1, seed: int = 0, device: int = 0,
                  use_graphs: bool = True, norm_eps: float = 0.0, tc_min_tokens: int = 0, lru_capacity: int = 0,
-                 keep_masters: bool = False):
+                 keep_masters: bool = False, per_layer_decode: bool = False):
         self.L, self.E, self.k, self.d, self.f = num_layers, experts_per_layer, top_k, d_model, d_ffn
         self.max_tokens = max_tokens
         self.norm_eps = norm_eps
         cfg = _EngineConfig(num_layers, experts_per_layer, top_k, d_model, d_ffn, max_tokens, seed, device,
-                            1 if use_graphs else 0, norm_eps, tc_min_tokens, lru_capacity, 1 if keep_masters else 0)
+                            1 if use_graphs else 0, norm_eps, tc_min_tokens, lru_capacity, 1 if keep_masters else 0,
+                            1 if per_layer_decode else 0)
         h = C.c_void_p()
         _check(lib().moe_engine_create(C.byref(cfg), plan._entries(), C.byref(h)))
         self._h = h
@@ -901,6 +906,16 @@ class MoeEngine:
         kps = C.c_int32()
         _check(lib().moe_engine_profile_step(self._h, T, ms, by, C.byref(kps)))
         return list(ms), list(by), kps.value
+
+    def profile_fused(self):
+        """The fused batch-1 step timed alone: (ms, algorithmic bytes) or None
+        when this engine decodes batch 1 layer by layer."""
+        ms, by = C.c_float(), C.c_int64()
+        st = lib().moe_engine_profile_fused(self._h, C.byref(ms), C.byref(by))
+        if st == 2:
+            return None
+        _check(st)
+        return ms.value, by.value
 
     def reconfigure(self, target: PlacementPlan, transfer_bw_bytes_per_s: float) -> dict:
         """Execute diff_plans(current, target) on the device (needs keep_masters)."""

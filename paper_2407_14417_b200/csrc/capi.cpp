@@ -778,6 +778,7 @@ int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan
         ec.seed = cfg->seed;
         ec.device = cfg->device;
         ec.use_graphs = cfg->use_graphs != 0;
+        ec.per_layer_decode = cfg->per_layer_decode != 0;
         usage_if(!(cfg->norm_eps >= 0.0f), "norm_eps must be >= 0");
         ec.norm_eps = cfg->norm_eps;
         usage_if(cfg->tc_min_tokens < 0, "tc_min_tokens must be >= 0");
@@ -834,6 +835,25 @@ int moe_engine_profile_step(moe_engine* eng, int T, float* ffn_ms, int64_t* ffn_
         int k = 0;
         eng->impl->profile_step(T, ffn_ms, ffn_bytes, &k);
         if (kernels_per_step) *kernels_per_step = k;
+    });
+}
+
+int moe_debug_engine_buffer(moe_engine* eng, int which, void** ptr, size_t* bytes) {
+    return guarded([&] { *ptr = eng->impl->debug_buffer(which, bytes); });
+}
+
+int moe_debug_fused_trace(void* buf) {
+    return guarded([&] {
+        need_device();
+        const cudaError_t e = moek_debug_fused_trace(buf);
+        if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    });
+}
+
+int moe_engine_profile_fused(moe_engine* eng, float* ms, int64_t* bytes) {
+    return guarded([&] {
+        usage_if(ms == nullptr || bytes == nullptr, "null output");
+        usage_if(!eng->impl->profile_fused(ms, bytes), "the engine does not use the fused batch-1 step");
     });
 }
 

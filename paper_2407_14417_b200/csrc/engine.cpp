@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <list>
 #include <map>
 #include <mutex>
@@ -177,6 +178,10 @@ struct MoeEngine::Impl {
     void* gws_base = nullptr;
     int32_t* idx_host = nullptr;  // pinned [Tmax*K]
     size_t ws_bytes = 0;
+    // fused batch-1 step (decode_step_kernel)
+    moe_expert_weights* dev_experts = nullptr;  // [L*E] device copy of `weights`
+    unsigned int* fused_ctl = nullptr;          // [L*2 tail-pool counters][2 barrier words]
+    bool fused_ok = false;
 
     SimReport counters;
     std::map<int, cudaGraphExec_t> graphs;
@@ -323,9 +328,60 @@ struct MoeEngine::Impl {
         }
         ck(cudaMemsetAsync(ticket, 0, 4, compute), "memset");
         ck(cudaMemsetAsync(xin, 0, static_cast<size_t>(Tmax) * d * 2, compute), "memset");
+        if (!cfg.per_layer_decode && moek_decode_step_supported(E, K, d, f)) {
+            dev_alloc(reinterpret_cast<void**>(&dev_experts), static_cast<size_t>(L) * E * sizeof(moe_expert_weights));
+            dev_alloc(reinterpret_cast<void**>(&fused_ctl), (static_cast<size_t>(L) * 2 + 2) * 4);
+            ck(cudaMemsetAsync(fused_ctl, 0, (static_cast<size_t>(L) * 2 + 2) * 4, compute), "memset");
+            fused_ok = true;
+        }
         ck(cudaHostAlloc(reinterpret_cast<void**>(&idx_host), TK * 4, cudaHostAllocDefault), "cudaHostAlloc");
 
         materialize();
+        upload_experts();
+    }
+
+    // the device expert table the fused step reads (after init / reconfigure)
+    void upload_experts() {
+        if (!dev_experts) return;
+        ck(cudaMemcpyAsync(dev_experts, weights.data(), weights.size() * sizeof(moe_expert_weights),
+                           cudaMemcpyHostToDevice, compute), "H2D expert table");
+        ck(cudaStreamSynchronize(compute), "sync");
+    }
+
+    bool use_fused(int T) const {
+        if (!fused_ok || T != 1) return false;
+        for (char c : layer_has_cpu)
+            if (c) return false;
+        return true;
+    }
+
+    void launch_fused() {
+        MoeDecodeArgs a{};
+        a.L = L;
+        a.E = E;
+        a.k = K;
+        a.d = d;
+        a.f = f;
+        a.norm_eps = cfg.norm_eps;
+        a.experts = dev_experts;
+        a.wg = wg;
+        a.x_in = xin;
+        a.xbuf0 = xbuf[0];
+        a.xbuf1 = xbuf[1];
+        a.x_out = xout;
+        a.idx = idx;
+        a.wts = wts;
+        a.idx_stride = Tmax * K;
+        a.part0 = gws.part0;
+        a.part1 = gws.part1;
+        a.hperm = static_cast<uint16_t*>(gws.hperm);
+        a.hperm16 = static_cast<uint16_t*>(gws.hperm16);
+        a.hsum = gws.hsum;
+        a.sched = fused_ctl;
+        a.bar = reinterpret_cast<unsigned long long*>(fused_ctl + static_cast<size_t>(L) * 2);
+        static const int bar_mode = getenv("MOE_BAR_MODE") ? atoi(getenv("MOE_BAR_MODE")) : 0;
+        a.bar_mode = bar_mode;
+        ck(moek_decode_step(a, compute), "decode_step");
     }
 
     // Synthetic weights: bf16 masters from the counter-based generator,
@@ -506,6 +562,7 @@ struct MoeEngine::Impl {
         }
         lru_clear();
         slot_holds.assign(static_cast<size_t>(nslots), -1);  // slots may have been reallocated
+        upload_experts();
         return rep;
     }
 
@@ -519,7 +576,7 @@ struct MoeEngine::Impl {
         if (master_arena) cudaFreeHost(master_arena);
         if (copy) cudaStreamSynchronize(copy);
         void* devp[] = {tcws, xn, dev_arena, swap, wg, xin, xout, xbuf[0], xbuf[1], idx, wts, counts, offsets, perm, inv, ticket, y,
-                         gws_base};
+                         gws_base, dev_experts, fused_ctl};
         for (void* p : devp)
             if (p) cudaFree(p);
         if (host_arena) cudaFreeHost(host_arena);
@@ -649,6 +706,12 @@ struct MoeEngine::Impl {
     }
 
     void run_layers(int T) {
+        if (use_fused(T)) {
+            launch_fused();
+            counters.activations += static_cast<int64_t>(T) * K * L;
+            counters.hits += static_cast<int64_t>(T) * K * L;
+            return;
+        }
         const uint16_t* src = xin;
         const size_t TK = static_cast<size_t>(Tmax) * K;
         for (int l = 0; l < L; ++l) {
@@ -715,6 +778,34 @@ struct MoeEngine::Impl {
         // GEMV: route(+x permute), gate/up stream, SwiGLU finalize, down stream, combine finalize
         // tcgen05: route, row gather, gate/up GEMM (+SwiGLU), down GEMM, combine
         if (kernels_per_step) *kernels_per_step = 5 * L;
+    }
+
+    bool profile_fused(float* ms, int64_t* bytes) {
+        if (!use_fused(1)) return false;
+        cudaEvent_t e0, e1;
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        ck(cudaEventRecord(e0, compute), "record");
+        launch_fused();
+        ck(cudaEventRecord(e1, compute), "record");
+        ck(cudaEventSynchronize(e1), "sync");
+        ck(cudaEventElapsedTime(ms, e0, e1), "elapsed");
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        const size_t TK = static_cast<size_t>(Tmax) * K;
+        std::vector<int32_t> all(static_cast<size_t>(L) * TK);
+        ck(cudaMemcpy(all.data(), idx, all.size() * 4, cudaMemcpyDeviceToHost), "D2H routing");
+        int64_t b = 0;
+        for (int l = 0; l < L; ++l) {
+            uint64_t sel = 0;
+            for (int i = 0; i < K; ++i) sel |= 1ull << all[static_cast<size_t>(l) * TK + static_cast<size_t>(i)];
+            for (int s = 0; s < E; ++s)
+                if ((sel >> s) & 1ull)
+                    b += static_cast<int64_t>(plan.entries[static_cast<size_t>(l * E + s)].precision == Precision::P16 ? size16 : size4);
+            b += static_cast<int64_t>(K) * d * 2 + static_cast<int64_t>(K) * f * 2 * 2 + static_cast<int64_t>(K) * d * 4;
+        }
+        *bytes = b;
+        return true;
     }
 
     bool graphable() const {
@@ -805,6 +896,22 @@ void MoeEngine::sync() {
     ck(cudaStreamSynchronize(impl_->compute), "sync");
     impl_->check_numerics();
 }
+
+bool MoeEngine::profile_fused(float* ms, int64_t* bytes) { return impl_->profile_fused(ms, bytes); }
+
+void* MoeEngine::debug_buffer(int which, size_t* bytes) {
+    Impl& m = *impl_;
+    const size_t kd = static_cast<size_t>(m.K);
+    switch (which) {
+        case 0: *bytes = static_cast<size_t>(m.d / 128) * kd * 2 * m.f * 4; return m.gws.part0;
+        case 1: *bytes = static_cast<size_t>(m.f / 128) * kd * m.d * 4; return m.gws.part1;
+        case 2: *bytes = kd * m.f * 2; return m.gws.hperm;
+        case 3: *bytes = kd * m.f * 2; return m.gws.hperm16;
+        case 4: *bytes = kd * moek_group_stride(m.f) * 4; return m.gws.hsum;
+        default: *bytes = 0; return nullptr;
+    }
+}
+bool MoeEngine::fused() const { return impl_->use_fused(1); }
 
 void MoeEngine::profile_step(int T, float* ffn_ms, int64_t* ffn_bytes, int* kernels_per_step) {
     impl_->profile_step(T, ffn_ms, ffn_bytes, kernels_per_step);

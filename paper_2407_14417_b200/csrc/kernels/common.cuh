@@ -167,6 +167,13 @@ MOE_DEVI void permute_chunk(const T* xg, int chunk, uint4& cb, uint4& ch, float&
     ch = make_uint4(wh[0], wh[1], wh[2], wh[3]);
 }
 
+// The int4 bias term of an activation group, 1032*S_lo + 72*S_hi, rounded
+// explicitly (no FMA contraction): every kernel that makes it -- route,
+// permute_rows, finalize_h, the fused step -- must produce the same bits.
+MOE_DEVI float int4_bias_term(float s_lo, float s_hi) {
+    return __fadd_rn(__fmul_rn(1032.0f, s_lo), __fmul_rn(72.0f, s_hi));
+}
+
 // The 16 chunk maxima of a 128-element group (lanes xor 8..1 of a half
 // warp; every lane of the warp must call): a nonzero group entirely below
 // the fp16 normal range (2^-14) keeps few or no bits in its fp16 copy.

@@ -38,6 +38,7 @@
 
 #include "common.cuh"
 #include "launch.h"
+#include "route_common.cuh"
 
 namespace moek {
 
@@ -698,6 +699,46 @@ MOE_DEVI float4 sum_kparts(const float* p, size_t kstride, int KP, int kg) {
 constexpr int kFinHThreads = 64 * kKG;
 constexpr int kFinOQuads = 8;   // 32 outputs per block: T=1 spreads d=4096 over 128 blocks
 constexpr int kFinOThreads = kFinOQuads * kKG;
+// SwiGLU tail of one (slot, 128-row group g of h) unit, warp 0 (lanes 0-31):
+// red[kg][q] holds the K-part-group sums of gate rows g*128+4q.. (q < 32) and
+// up rows (q >= 32); h rounded to bf16 goes out as the K-permuted bf16 copy,
+// its exact fp16 copy and the group's int4 bias term.  Shared by
+// finalize_h_kernel and the fused decode-step kernel (identical arithmetic).
+MOE_DEVI void swiglu_unit(const float4 (&red)[kKG][64], uint16_t* hs, int slot, int g, int f, uint16_t* __restrict__ hperm,
+                          uint16_t* __restrict__ hperm16, float* __restrict__ hsum, int hstride, int lane) {
+    float gv[4], uv[4];
+    {
+        float4 a = red[0][lane], b = red[0][32 + lane];
+#pragma unroll
+        for (int k2 = 1; k2 < kKG; ++k2) {
+            const float4 c = red[k2][lane], e = red[k2][32 + lane];
+            a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+            b.x += e.x; b.y += e.y; b.z += e.z; b.w += e.w;
+        }
+        gv[0] = a.x; gv[1] = a.y; gv[2] = a.z; gv[3] = a.w;
+        uv[0] = b.x; uv[1] = b.y; uv[2] = b.z; uv[3] = b.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) hs[lane * 4 + j] = f2bf(silu_f(gv[j]) * uv[j]);
+    __syncwarp();
+    uint4 cb = make_uint4(0, 0, 0, 0), ch = cb;
+    float s_lo = 0.0f, s_hi = 0.0f, amax = 0.0f;
+    if (lane < 16) permute_chunk(hs, lane, cb, ch, s_lo, s_hi, amax);
+    numerics_group_check(amax, lane == 0);
+    const size_t o = static_cast<size_t>(slot) * f + g * 128;
+    if (lane < 16) {
+        reinterpret_cast<uint4*>(hperm + o)[lane] = cb;
+        reinterpret_cast<uint4*>(hperm16 + o)[lane] = ch;
+    }
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) {
+        s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);
+        s_hi += __shfl_xor_sync(0xffffffffu, s_hi, off);
+    }
+    if (lane == 0) hsum[static_cast<size_t>(slot) * hstride + g] = int4_bias_term(s_lo, s_hi);
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(kFinHThreads) finalize_h_kernel(
     const float* __restrict__ part, const int* __restrict__ kpslot, int nslots, int f, uint16_t* __restrict__ hperm,
     uint16_t* __restrict__ hperm16, float* __restrict__ hsum, int hstride, unsigned int* sched) {
@@ -721,39 +762,7 @@ __global__ void __launch_bounds__(kFinHThreads) finalize_h_kernel(
     red[kg][q] = sum_kparts(part + static_cast<size_t>(slot) * rows + row, static_cast<size_t>(nslots) * rows, KP, kg);
     __syncthreads();
     if (threadIdx.x >= 32) return;
-    const int lane = threadIdx.x;
-    float gv[4], uv[4];
-    {
-        float4 a = red[0][lane], b = red[0][32 + lane];
-#pragma unroll
-        for (int k2 = 1; k2 < kKG; ++k2) {
-            const float4 c = red[k2][lane], e = red[k2][32 + lane];
-            a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
-            b.x += e.x; b.y += e.y; b.z += e.z; b.w += e.w;
-        }
-        gv[0] = a.x; gv[1] = a.y; gv[2] = a.z; gv[3] = a.w;
-        uv[0] = b.x; uv[1] = b.y; uv[2] = b.z; uv[3] = b.w;
-    }
-    // h rounded to bf16 into smem (natural order), then every lane writes one
-    // 16-byte chunk of each K-permuted copy
-#pragma unroll
-    for (int j = 0; j < 4; ++j) hs[lane * 4 + j] = f2bf(silu_f(gv[j]) * uv[j]);
-    __syncwarp();
-    uint4 cb = make_uint4(0, 0, 0, 0), ch = cb;
-    float s_lo = 0.0f, s_hi = 0.0f, amax = 0.0f;
-    if (lane < 16) permute_chunk(hs, lane, cb, ch, s_lo, s_hi, amax);
-    numerics_group_check(amax, lane == 0);
-    const size_t o = static_cast<size_t>(slot) * f + g * 128;
-    if (lane < 16) {
-        reinterpret_cast<uint4*>(hperm + o)[lane] = cb;
-        reinterpret_cast<uint4*>(hperm16 + o)[lane] = ch;
-    }
-#pragma unroll
-    for (int off = 8; off >= 1; off >>= 1) {
-        s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);
-        s_hi += __shfl_xor_sync(0xffffffffu, s_hi, off);
-    }
-    if (lane == 0) hsum[static_cast<size_t>(slot) * hstride + g] = 1032.0f * s_lo + 72.0f * s_hi;
+    swiglu_unit(red, hs, slot, g, f, hperm, hperm16, hsum, hstride, threadIdx.x);
     ltrace(3, 2);
 }
 
@@ -856,11 +865,514 @@ __global__ void permute_rows_kernel(const uint16_t* __restrict__ x, int rows, in
     if (!ok) return;
     reinterpret_cast<uint4*>(xp + r * K + g * 128)[c] = cb;
     reinterpret_cast<uint4*>(xp16 + r * K + g * 128)[c] = ch;
-    if (c == 0) xsum[r * xstride + g] = 1032.0f * s_lo + 72.0f * s_hi;
+    if (c == 0) xsum[r * xstride + g] = int4_bias_term(s_lo, s_hi);
 }
 
-int group_stride(int K) { return (K / 128 + 7) / 8 * 8; }
+__host__ __device__ inline int group_stride(int K) { return (K / 128 + 7) / 8 * 8; }
+
+// ===========================================================================
+// Fused batch-1 decode step: the whole L-layer stack in ONE persistent launch
+// (one CTA per SM, cooperative), replacing 5 launches per layer.  Per layer:
+//   R  every CTA routes the token itself (RMSNorm, logits, top-k, permutation
+//      -- route_common.cuh, bit-identical to route_kernel) straight into its
+//      resident activation rows, and builds both passes' segment tables;
+//   G  gate/up items (the streaming GEMV's items, rings, scheduler); once a
+//      warp has issued its last gate/up item its ring runs on into the down
+//      pass's weights, which do not depend on h;
+//   |  grid barrier
+//   H  SwiGLU finalize, (slot, 128-group) units spread over the CTAs;
+//   |  grid barrier
+//   D  h rows -> resident rows; down items (weights mostly already landed);
+//   |  grid barrier
+//   O  combine + residual, 32-output blocks spread over the CTAs -> x(l+1);
+//   |  grid barrier (not after the last layer)
+// The partial layouts, item decomposition, K-part sums and combine order are
+// those of the per-layer kernels, so the output is bit-identical to them.
+// What it removes per layer: 4 launch / PDL boundaries, the route kernel's
+// own round trips and the stream kernels' prologues (≈ 9 of ≈ 18 µs of
+// non-streaming time per int4 layer, profiles/README.md r02).
+using DecodeArgs = MoeDecodeArgs;
+
+// Debug (moe_debug_fused_trace): per layer and CTA, globaltimer stamps of the
+// phase boundaries [L][gridDim][kFusedStamps]; null (default) = off.
+constexpr int kFusedStamps = 10;
+__device__ unsigned long long* g_fused_trace = nullptr;
+MOE_DEVI void fstamp(int l, int i) {
+    unsigned long long* tr = g_fused_trace;
+    if (tr == nullptr || threadIdx.x != 0) return;
+    tr[(static_cast<size_t>(l) * gridDim.x + blockIdx.x) * kFusedStamps + i] = gtimer();
+}
+
+MOE_DEVI unsigned int ld_acquire_gpu(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+MOE_DEVI void st_release_gpu(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+MOE_DEVI void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Grid barrier over all CTAs (co-resident: cooperative launch) on one
+// monotonic 64-bit arrival counter: a CTA's arrival number tells it its
+// round r, and it proceeds once the counter reaches (r + 1) * gridDim.x.
+// One release fetch-add per CTA, acquire polling, no reset step.  mode 1:
+// a full fence + relaxed add instead of the release add (A/B).
+MOE_DEVI void grid_barrier(unsigned long long* ctr, int mode) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long old;
+        if (mode == 1) {
+            __threadfence();
+            asm volatile("atom.add.relaxed.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(ctr) : "memory");
+        } else {
+            asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(ctr) : "memory");
+        }
+        const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+// Segment table of one pass for a batch-1 step: one segment per selected
+// expert (mcnt = 1), in expert order -- build_segs' table for T = 1.
+template <class C>
+MOE_DEVI void build_segs_t1(SegTable& st, const moe_expert_weights* ex, const int32_t* offsets, int E, int p,
+                            int rows, int K) {
+    const int RT = rows / 16, G = K / 128;
+    int n = 0, acc = 0;
+    for (int e = 0; e < E; ++e) {
+        if (offsets[e + 1] == offsets[e]) continue;
+        const moe_expert_weights& W = ex[e];
+        const int gk = pick_gk<C>(G, W.precision, 1);
+        st.e[n] = e;
+        st.slot0[n] = offsets[e];
+        st.mcnt[n] = 1;
+        st.kp[n] = G / gk;
+        st.gk[n] = gk;
+        st.wptr[n] = static_cast<const uint8_t*>(p == 0 ? W.w_gate_up : W.w_down);
+        st.sptr[n] = static_cast<const uint8_t*>(p == 0 ? W.s_gate_up : W.s_down);
+        st.wbytes[n] = W.precision == MOE_P4 ? gk * 1024 : gk * 4096;
+        st.sbytes[n] = W.precision == MOE_P4 ? gk * 32 : 0;
+        st.pre[n] = acc;
+        for (int c = 0; c < kTile; ++c) st.brow[n][c] = p == 0 ? 0 : offsets[e];
+        acc += RT * (G / gk);
+        ++n;
+    }
+    st.pre[n] = acc;
+    st.n = n;
+    st.N = acc;
+}
+
+// The weight half of an item of a pass with reduction length K (issue_weights
+// without the activation bytes: resident rows).
+MOE_DEVI void issue_item_w(const SegTable& st, int K, const Item& it, uint8_t* stage, uint64_t* bar, uint64_t pol,
+                           int stage_s_off) {
+    const int s = it.s, wb = st.wbytes[s], sb = st.sbytes[s];
+    mbar_expect_tx(bar, wb + sb);
+    const size_t blk = static_cast<size_t>(it.rt) * (K / 128) + static_cast<size_t>(it.kp) * st.gk[s];
+    bulk_g2s_hint(stage, st.wptr[s] + blk * (sb ? 1024 : 4096), wb, bar, pol);
+    if (sb) bulk_g2s_hint(stage + stage_s_off, st.sptr[s] + blk * 32, sb, bar, pol);
+}
+
+MOE_DEVI void sched_init(Sched& sc, unsigned int* ctr, int N, int W, int wid, int lane, int RT) {
+    const int pool = min(N / 8, W * kChunk * 2);
+    sc.chunk = pool <= kSmallPool ? 1 : kChunk;
+    sc.ctr = ctr;
+    sc.N = N;
+    sc.ns = N - pool;
+    const int qs = sc.ns / W, rs = sc.ns - qs * W;
+    sc.cur = wid * qs + min(wid, rs);
+    sc.end = sc.cur + qs + (wid < rs ? 1 : 0);
+    sc.dyn = 0;
+    sc.pend = 0;
+    sc.lane = lane;
+    sc.RT = RT;
+    sc.started = 0;
+    sc.it = Item{0, 0, 0};
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __grid_constant__ DecodeArgs a) {
+    constexpr int kWarps = C::kWarps;
+    constexpr int kStageBytes = C::kStageBytes;
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ SegTable st[2];
+    __shared__ __align__(8) uint64_t bars[kWarps][kStages];
+    __shared__ __align__(8) uint64_t res_bar;
+    __shared__ __align__(16) moe_expert_weights s_ex[MOE_MAX_EXPERTS];
+    __shared__ float lg_s[MOE_MAX_EXPERTS + C::kThreads];
+    __shared__ int32_t s_idx[MOE_MAX_TOPK], s_counts[MOE_MAX_EXPERTS], s_offsets[MOE_MAX_EXPERTS + 1];
+    __shared__ int32_t s_perm[MOE_MAX_TOPK], s_inv[MOE_MAX_TOPK], s_topi[MOE_MAX_TOPK];
+    __shared__ float s_w[MOE_MAX_TOPK];
+    __shared__ uint16_t hs[2][128];
+    __shared__ float4 redo[MOE_MAX_TOPK][kKG][kFinOQuads];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+    const int d = a.d, f = a.f, E = a.E, k = a.k;
+    if (lane == 0) {
+        for (int s2 = 0; s2 < kStages; ++s2) mbar_init(&bars[warp][s2], 1);
+        if (warp == 0) mbar_init(&res_bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint64_t pol = policy_evict_first();
+    const int W = static_cast<int>(gridDim.x) * kWarps;
+    const int wid = static_cast<int>(blockIdx.x) * kWarps + warp;
+    const int gr = lane >> 2, t4 = lane & 3;
+    uint8_t* ring = smem + static_cast<size_t>(warp) * kStages * kStageBytes;
+    uint8_t* res = smem + static_cast<size_t>(kWarps) * kStages * kStageBytes;
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem);  // phase R scratch: raw row, then normalised row (rings idle)
+    uint16_t* xn = xs + d;
+    const int bs0 = group_stride(d), bs1 = group_stride(f);
+    uint32_t phase_bits = 0, res_phase = 0;
+    // router weights of the layer about to route, in registers: layer 0's
+    // here, layer l+1's before layer l's last barrier (its L2 prefetch went
+    // out at the start of layer l's gate/up phase)
+    uint4 wpre[kPreChunks];
+    if (warp < E) preload_w(wpre, a.wg + static_cast<size_t>(warp) * d, d, lane);
+
+    for (int l = 0; l < a.L; ++l) {
+        const uint16_t* xl = l == 0 ? a.x_in : ((l - 1) & 1 ? a.xbuf1 : a.xbuf0);
+        uint16_t* yl = l == a.L - 1 ? a.x_out : (l & 1 ? a.xbuf1 : a.xbuf0);
+        const uint16_t* wgl = a.wg + static_cast<size_t>(l) * E * d;
+        fstamp(l, 0);
+        // ---- R: route the token (every CTA, identical results) --------------
+        for (int i = tid; i < E * static_cast<int>(sizeof(moe_expert_weights) / 8); i += blockDim.x)
+            reinterpret_cast<uint2*>(s_ex)[i] =
+                reinterpret_cast<const uint2*>(a.experts + static_cast<size_t>(l) * E)[i];
+        for (int i = tid * 8; i < d; i += blockDim.x * 8)
+            *reinterpret_cast<uint4*>(xs + i) = __ldcg(reinterpret_cast<const uint4*>(xl + i));
+        __syncthreads();
+        const uint16_t* xr = xs;
+        if (a.norm_eps > 0.0f) {
+            float acc = 0.0f;  // route_kernel's pinned order
+            for (int c = 0; c * 256 + tid < d; ++c) {
+                const float v = bf2f(xs[c * 256 + tid]);
+                acc = __fmaf_rn(v, v, acc);
+            }
+            lg_s[MOE_MAX_EXPERTS + tid] = acc;
+            __syncthreads();
+            for (int s2 = 128; s2 >= 32; s2 >>= 1) {
+                if (tid < s2) lg_s[MOE_MAX_EXPERTS + tid] = __fadd_rn(lg_s[MOE_MAX_EXPERTS + tid], lg_s[MOE_MAX_EXPERTS + tid + s2]);
+                __syncthreads();
+            }
+            if (warp == 0) {
+                float v = lg_s[MOE_MAX_EXPERTS + lane];
+#pragma unroll
+                for (int s2 = 16; s2 >= 1; s2 >>= 1) v = __fadd_rn(v, __shfl_down_sync(0xffffffffu, v, s2));
+                if (lane == 0) lg_s[MOE_MAX_EXPERTS] = v;
+            }
+            __syncthreads();
+            const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(lg_s[MOE_MAX_EXPERTS], static_cast<float>(d)),
+                                                                    a.norm_eps)));
+            for (int i = tid * 8; i < d; i += blockDim.x * 8) {
+                uint4 v = *reinterpret_cast<const uint4*>(xs + i);
+                uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    w4[q] = static_cast<uint32_t>(f2bf(__fmul_rn(bf16_lo(w4[q]), rstd))) |
+                            (static_cast<uint32_t>(f2bf(__fmul_rn(bf16_hi(w4[q]), rstd))) << 16);
+                *reinterpret_cast<uint4*>(xn + i) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            }
+            __syncthreads();
+            xr = xn;
+        }
+        for (int e = warp; e < E; e += kWarps) {
+            if (e != warp) preload_w(wpre, wgl + static_cast<size_t>(e) * d, d, lane);
+            const float v = router_dot(xr, wpre, wgl + static_cast<size_t>(e) * d, d, lane);
+            if (lane == 0) lg_s[e] = v;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            warp_topk(lg_s, E, k, lane, s_topi, s_w, s_idx);
+            __syncwarp();
+            warp_permute(s_idx, k, E, s_counts, s_offsets, s_perm, s_inv, lane);
+            if (blockIdx.x == 0 && lane < k) {
+                a.idx[static_cast<size_t>(l) * a.idx_stride + lane] = s_topi[lane];
+                a.wts[static_cast<size_t>(l) * a.idx_stride + lane] = s_w[lane];
+            }
+        } else {
+            // resident activation rows of the gate/up pass: K-permuted bf16
+            // (res), fp16 (res + 2d) and the int4 bias terms (res + 4d)
+            uint16_t* rb = reinterpret_cast<uint16_t*>(res);
+            uint16_t* rh = rb + d;
+            float* rx = reinterpret_cast<float*>(res + 4 * d);
+            const int G = d / 128, nw = kWarps - 1;
+            for (int g0 = (warp - 1) * 2; g0 < G; g0 += nw * 2) {
+                const int g = g0 + (lane >> 4), c = lane & 15;
+                uint4 cb = make_uint4(0, 0, 0, 0), ch = cb;
+                float s_lo = 0.0f, s_hi = 0.0f, amax = 0.0f;
+                if (g < G) permute_chunk(xr + g * 128, c, cb, ch, s_lo, s_hi, amax);
+                numerics_group_check(amax, c == 0);
+#pragma unroll
+                for (int off = 8; off >= 1; off >>= 1) {
+                    s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);
+                    s_hi += __shfl_xor_sync(0xffffffffu, s_hi, off);
+                }
+                if (g < G) {
+                    reinterpret_cast<uint4*>(rb + g * 128)[c] = cb;
+                    reinterpret_cast<uint4*>(rh + g * 128)[c] = ch;
+                    if (c == 0) rx[g] = int4_bias_term(s_lo, s_hi);
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) build_segs_t1<C>(st[0], s_ex, s_offsets, E, 0, 2 * f, d);
+        if (tid == 32) build_segs_t1<C>(st[1], s_ex, s_offsets, E, 1, d, f);
+        fence_proxy_async();  // scratch (generic) writes before the rings' bulk copies
+        __syncthreads();
+        fstamp(l, 1);
+
+        if (l + 1 < a.L && blockIdx.x < 4 && tid == 0) {  // next layer's router weights -> L2
+            const uint32_t chunk = static_cast<uint32_t>(E) * d * 2 / 4;
+            if (chunk % 16 == 0)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(wgl + static_cast<size_t>(E) * d +
+                                                                            static_cast<size_t>(blockIdx.x) * chunk / 2),
+                             "r"(chunk)
+                             : "memory");
+        }
+        // ---- G: gate/up items, the ring running on into the down weights ------
+        Sched sc[2];
+        sched_init(sc[0], a.sched + 2 * l, st[0].N, W, wid, lane, (2 * f) / 16);
+        sched_init(sc[1], a.sched + 2 * l + 1, st[1].N, W, wid, lane, d / 16);
+        int np = 0;  // pass of the next item to issue
+        auto next_item = [&](Item& it, int& pass) -> bool {
+            if (np == 0) {
+                if (sc[0].next(st[0], it)) {
+                    pass = 0;
+                    return true;
+                }
+                np = 1;
+            }
+            if (sc[1].next(st[1], it)) {
+                pass = 1;
+                return true;
+            }
+            return false;
+        };
+        // the two stages' items live in registers (static indices only: a
+        // dynamically indexed array would go to local memory)
+        static_assert(kStages == 2, "two ring stages");
+        Item it0{0, 0, 0}, it1{0, 0, 0};
+        int ps0 = 0, ps1 = 0;
+        int issued = 0, computed = 0;
+        if (next_item(it0, ps0)) {
+            if (lane == 0) issue_item_w(st[ps0], ps0 ? f : d, it0, ring, &bars[warp][0], pol, C::kStageS);
+            ++issued;
+            if (next_item(it1, ps1)) {
+                if (lane == 0) issue_item_w(st[ps1], ps1 ? f : d, it1, ring + kStageBytes, &bars[warp][1], pol, C::kStageS);
+                ++issued;
+            }
+        }
+        for (int pass = 0; pass < 2; ++pass) {
+            if (pass == 1) {
+                // ---- H: SwiGLU finalize over (slot, 128-group) units -------------
+                fence_proxy_async();  // resident rows read (generic) before phase D's bulk copies
+                fstamp(l, 2);
+                grid_barrier(a.bar, a.bar_mode);
+                fstamp(l, 3);
+                const int Gf = f / 128;
+                const size_t rows2 = static_cast<size_t>(2) * f;
+                // up to two (slot, group) units per CTA at once: every K-part
+                // load issued before any sum is used; the K-part-group sums go
+                // to the (now free) resident area, warps 0 and 1 finish one unit each
+                typedef float4 RedT[kKG][64];
+                RedT* redu = reinterpret_cast<RedT*>(res);
+                for (int u0 = blockIdx.x; u0 < k * Gf; u0 += 2 * gridDim.x) {
+                    float4 v[2][2];
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int u = u0 + j * gridDim.x;
+                        const int slot = u / Gf, g = u - slot * Gf;
+#pragma unroll
+                        for (int h2 = 0; h2 < 2; ++h2) {
+                            const int q = tid & 63, kg = (tid >> 6) + h2 * 4;
+                            const int row = (q < 32 ? g * 128 + q * 4 : f + g * 128 + (q - 32) * 4);
+                            v[j][h2] = u < k * Gf ? sum_kparts(a.part0 + static_cast<size_t>(slot) * rows2 + row,
+                                                               static_cast<size_t>(k) * rows2, st[0].kp[slot], kg)
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+#pragma unroll
+                        for (int h2 = 0; h2 < 2; ++h2) redu[j][(tid >> 6) + h2 * 4][tid & 63] = v[j][h2];
+                    __syncthreads();
+                    if (warp < 2) {
+                        const int u = u0 + warp * gridDim.x;
+                        if (u < k * Gf) {
+                            const int slot = u / Gf, g = u - slot * Gf;
+                            swiglu_unit(redu[warp], hs[warp], slot, g, f, a.hperm, a.hperm16, a.hsum, bs1, lane);
+                        }
+                    }
+                    __syncthreads();
+                }
+                fence_proxy_async();  // generic scratch writes to the resident area before phase D's bulk copies
+                fstamp(l, 4);
+                grid_barrier(a.bar, a.bar_mode);
+                fstamp(l, 5);
+                // ---- D: h rows into the resident area (slot s's row in its format)
+                if (tid == 0) {
+                    fence_proxy_async_global();
+                    uint32_t bytes = 0;
+                    for (int s2 = 0; s2 < st[1].n; ++s2) bytes += f * 2 + (st[1].sbytes[s2] ? bs1 * 4 : 0);
+                    mbar_expect_tx(&res_bar, bytes);
+                    float* rx1 = reinterpret_cast<float*>(res + 2 * f * 2);
+                    for (int s2 = 0; s2 < st[1].n; ++s2) {
+                        const bool p4 = st[1].sbytes[s2] != 0;
+                        const int slot = st[1].slot0[s2];
+                        bulk_g2s(res + s2 * f * 2, (p4 ? a.hperm16 : a.hperm) + static_cast<size_t>(slot) * f, f * 2,
+                                 &res_bar);
+                        if (p4) bulk_g2s(rx1 + s2 * bs1, a.hsum + static_cast<size_t>(slot) * bs1, bs1 * 4, &res_bar);
+                    }
+                }
+                mbar_wait(&res_bar, res_phase);
+                res_phase ^= 1u;
+                fstamp(l, 6);
+            }
+            const int K = pass ? f : d, rows = pass ? d : 2 * f;
+            float* part = pass ? a.part1 : a.part0;
+            const float* resx = reinterpret_cast<const float*>(res + 2 * K * 2);
+            while (computed < issued) {
+                const int stage = computed & 1;
+                if ((stage ? ps1 : ps0) != pass) break;  // the next item belongs to the down pass
+                const Item it = stage ? it1 : it0;
+                mbar_wait(&bars[warp][stage], (phase_bits >> stage) & 1u);
+                phase_bits ^= 1u << stage;
+                uint8_t* sp = ring + stage * kStageBytes;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                {
+                    const SegTable& T = st[pass];
+                    const int gk = T.gk[it.s];
+                    const bool p4 = T.sbytes[it.s] != 0;
+                    const int row = pass == 0 ? (p4 ? 1 : 0) : it.s;
+                    const uint8_t* bp = res + row * K * 2 + it.kp * gk * 256 + t4 * 16;
+                    const float* x0 = resx + (pass == 0 ? 0 : it.s * bs1) + it.kp * gk;
+                    compute_item<C>(T, it, sp, bp, x0, x0, lane, acc);
+                }
+                ++computed;
+                fence_proxy_async();
+                __syncwarp();
+                Item nit;
+                int npass;
+                if (next_item(nit, npass)) {
+                    if (lane == 0)
+                        issue_item_w(st[npass], npass ? f : d, nit, sp, &bars[warp][stage], pol, C::kStageS);
+                    if (stage) {
+                        it1 = nit;
+                        ps1 = npass;
+                    } else {
+                        it0 = nit;
+                        ps0 = npass;
+                    }
+                    ++issued;
+                }
+                const SegTable& T = st[pass];
+                float* pp = part + (static_cast<size_t>(it.kp) * k + T.slot0[it.s] + 2 * t4) * rows + it.rt * 16 + gr;
+                if (t4 == 0) {  // one token: column 0
+                    __stcg(pp, acc[0]);
+                    __stcg(pp + 8, acc[2]);
+                }
+            }
+        }
+        // ---- O: combine + residual -> x(l+1) ---------------------------------
+        fstamp(l, 7);
+        grid_barrier(a.bar, a.bar_mode);
+        fstamp(l, 8);
+        if (blockIdx.x == 0 && tid < 2) a.sched[2 * l + tid] = 0;  // this layer's pools, for the next step
+        {
+            const int nb = d / (kFinOQuads * 4);
+            const size_t kstride = static_cast<size_t>(k) * d;
+            for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+                // threads [jj*64, jj*64+64) sum slot inv[jj]'s K-parts (all
+                // loads in flight together); the combine then runs in jj order
+                const int j0 = b * (kFinOQuads * 4);
+                const int jj = tid / kFinOThreads, r = tid % kFinOThreads;
+                const int q = r % kFinOQuads, kg = r / kFinOQuads;
+                const int j = j0 + q * 4;
+                if (jj < k) {
+                    const int slot = s_inv[jj];
+                    redo[jj][kg][q] = sum_kparts(a.part1 + static_cast<size_t>(slot) * d + j, kstride, st[1].kp[slot], kg);
+                }
+                __syncthreads();
+                if (tid < kFinOQuads) {
+                    float acc[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] = bf2f(xl[j + u]);
+                    for (int jx = 0; jx < k; ++jx) {
+                        float4 s4 = redo[jx][0][q];
+#pragma unroll
+                        for (int k2 = 1; k2 < kKG; ++k2) {
+                            const float4 c = redo[jx][k2][q];
+                            s4.x += c.x; s4.y += c.y; s4.z += c.z; s4.w += c.w;
+                        }
+                        const float w = s_w[jx];
+                        acc[0] = __fmaf_rn(w, s4.x, acc[0]);
+                        acc[1] = __fmaf_rn(w, s4.y, acc[1]);
+                        acc[2] = __fmaf_rn(w, s4.z, acc[2]);
+                        acc[3] = __fmaf_rn(w, s4.w, acc[3]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) yl[j + u] = f2bf(acc[u]);
+                }
+                __syncthreads();
+            }
+        }
+        fstamp(l, 9);
+        if (l + 1 < a.L) {
+            if (warp < E) preload_w(wpre, wgl + static_cast<size_t>(E) * d + static_cast<size_t>(warp) * d, d, lane);
+            grid_barrier(a.bar, a.bar_mode);
+        }
+    }
+}
 }  // namespace moek
+
+cudaError_t moek_debug_fused_trace(void* buf) {
+    return cudaMemcpyToSymbol(moek::g_fused_trace, &buf, sizeof(buf));
+}
+
+size_t moek_decode_step_smem() {
+    using C = moek::CfgDecode;
+    return static_cast<size_t>(C::kWarps) * moek::kStages * C::kStageBytes + C::kResBytes;
+}
+
+bool moek_decode_step_supported(int E, int k, int d, int f) {
+    // resident rows: <= 2 segments of K <= 14336 (CfgDecode's reserved area),
+    // 256-thread routing, 32-output combine blocks
+    return E >= 1 && E <= MOE_MAX_EXPERTS && k >= 1 && k <= 2 && k <= E && d % 256 == 0 && f % 128 == 0 &&
+           d <= 14336 && f <= 14336 && moek::group_stride(f) <= 512 && moek::group_stride(d) <= 512 &&
+           4 * d + 4 * moek::group_stride(d) <= moek::CfgDecode::kResBytes;
+}
+
+cudaError_t moek_decode_step(const MoeDecodeArgs& a, cudaStream_t stream) {
+    using C = moek::CfgDecode;
+    static int grid = 0;
+    const size_t smem = moek_decode_step_smem();
+    if (grid == 0) {
+        MOE_CUDA_OK(cudaFuncSetAttribute(moek::decode_step_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+        int dev = 0, sms = 0, per = 0;
+        MOE_CUDA_OK(cudaGetDevice(&dev));
+        MOE_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        MOE_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, moek::decode_step_kernel<C>, C::kThreads, smem));
+        if (per < 1) return cudaErrorCooperativeLaunchTooLarge;
+        grid = sms;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(C::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: the grid barriers rely on it
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, moek::decode_step_kernel<C>, a);
+}
 int moek_group_stride(int K) { return moek::group_stride(K); }
 // Largest T whose (active expert, 8-token tile) segments always fit the
 // kernel's table: at most min(E, T*k) experts are active and their segments

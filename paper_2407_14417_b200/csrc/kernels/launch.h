@@ -49,6 +49,38 @@ cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* 
                          const void* resid, int T, int k, const moe_expert_weights* experts, int E,
                          int d, int f, uint64_t active_mask, void* out, float* y, int xmode,
                          cudaStream_t stream);
+// Fused batch-1 decode step (gemv.cu decode_step_kernel): the whole L-layer
+// stack -- routing, gate/up GEMV, SwiGLU, down GEMV, combine + residual per
+// layer -- in one cooperative persistent launch with grid barriers between
+// the phases.  All experts device-resident; output bit-identical to the
+// per-layer kernels.  Buffers are the engine's; sched [L][2] and bar [2]
+// must be zero before the first launch (the kernel leaves them so).
+struct MoeDecodeArgs {
+    int L, E, k, d, f;
+    float norm_eps;
+    const moe_expert_weights* experts;  // [L*E] device table
+    const uint16_t* wg;                 // [L][E][d]
+    const uint16_t* x_in;               // [d]
+    uint16_t* xbuf0;
+    uint16_t* xbuf1;
+    uint16_t* x_out;
+    int32_t* idx;                       // [L][idx_stride] routing export
+    float* wts;
+    int idx_stride;
+    float* part0;                       // [d/128][k][2f]
+    float* part1;                       // [f/128][k][d]
+    uint16_t* hperm;                    // [k][f]
+    uint16_t* hperm16;
+    float* hsum;                        // [k][group_stride(f)]
+    unsigned int* sched;                // [L][2]
+    unsigned long long* bar;            // grid-barrier arrival counter (monotonic)
+    int bar_mode;                       // 0: release fetch-add; 1: fence + relaxed add (A/B)
+};
+bool moek_decode_step_supported(int E, int k, int d, int f);
+size_t moek_decode_step_smem();
+cudaError_t moek_decode_step(const MoeDecodeArgs& a, cudaStream_t stream);
+// Debug: [L][grid][10] u64 globaltimer stamps of the fused step's phases; null disables.
+cudaError_t moek_debug_fused_trace(void* buf);
 // tcgen05 grouped expert FFN (tc_gemm.cu): x natural [T][d] bf16 (already
 // normalised), every active expert's segment -> y_perm [T*k][d] fp32.
 size_t moek_tc_workspace_bytes(int T, int k, int d, int f);

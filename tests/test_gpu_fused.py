@@ -1,0 +1,57 @@
+"""The fused batch-1 decode step (gemv.cu decode_step_kernel: the whole stack
+in one cooperative launch, grid barriers between phases) against the
+per-layer kernels: outputs and routing bit-identical step after step, graph
+and eager, tiny and Mixtral shapes, every precision mix."""
+import numpy as np
+import pytest
+
+from helpers import MIXTRAL, TINY, read_device
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(moe, cfg, n4, seed, eps, graphs=True, plan_seed=0):
+    prof = moe.profile_for_shape(cfg["d_model"], cfg["d_ffn"], cfg["num_layers"], cfg["experts_per_layer"],
+                                 cfg["top_k"])
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, plan_seed), moe.HardwareProfile(10**15), prof)
+    mk = lambda per_layer: moe.MoeEngine(cfg["num_layers"], cfg["experts_per_layer"], cfg["top_k"], cfg["d_model"],
+                                         cfg["d_ffn"], plan, max_tokens=1, seed=seed, norm_eps=eps,
+                                         use_graphs=graphs, per_layer_decode=per_layer)
+    return mk(False), mk(True)
+
+
+@pytest.mark.parametrize("graphs", [True, False])
+@pytest.mark.parametrize("eps", [0.0, 1e-5])
+@pytest.mark.parametrize("n4", [0, 8, 16])
+def test_fused_equals_per_layer_tiny(moe, cuda, n4, eps, graphs):
+    import torch
+    fused, ref = _pair(moe, TINY, n4, 42, eps, graphs, plan_seed=1)
+    assert fused.profile_fused() is not None and ref.profile_fused() is None
+    for step in range(24):
+        for e in (fused, ref):
+            e.synth_input(step, 1)
+            e.decode(1)
+            e.sync()
+        assert np.array_equal(read_device(torch, fused.output_ptr, 1024), read_device(torch, ref.output_ptr, 1024)), step
+        assert fused.last_routing(1) == ref.last_routing(1), step
+    c = fused.counters()
+    assert c.tokens == 24 and c.activations == 24 * 2 * 2 == c.hits
+    fused.close()
+    ref.close()
+
+
+@pytest.mark.parametrize("n4", [0, 128, 256])
+def test_fused_equals_per_layer_mixtral(moe, cuda, n4):
+    import torch
+    fused, ref = _pair(moe, MIXTRAL, n4, 0, 1e-5)
+    for step in range(6):
+        for e in (fused, ref):
+            e.synth_input(1000 + step, 1)
+            e.decode(1)
+            e.sync()
+        assert np.array_equal(read_device(torch, fused.output_ptr, 8192), read_device(torch, ref.output_ptr, 8192)), step
+        assert fused.last_routing(1) == ref.last_routing(1), step
+    ms, nbytes = fused.profile_fused()
+    assert ms > 0 and nbytes > 32 * 2 * moe.expert_size(moe.profile_for_shape(4096, 14336, 32), 0)
+    fused.close()
+    ref.close()

@@ -1,20 +1,19 @@
-"""ncu DRAM traffic of the expert-FFN launches of one profiled decode step
-(the bench's roofline configuration) -> profiles/r02_traffic.json.
+"""ncu DRAM traffic of the bench's roofline kernels -> profiles/r02_traffic.json.
+
+Two captures at the headline configuration (n4, batch T, input bench.TRAFFIC_INPUT):
+  fused      one decode_step_kernel launch (the whole batch-1 step)
+  per_layer  the expert-FFN launches (stream_kernel x2, finalize_h, finalize_out)
+             of one per-layer-kernel step, summed and divided by the layers
 
 Usage (on the GPU box):
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
       --profile-from-start off --clock-control none --csv --log-file gpurun_out/traffic.csv \
       python tools/traffic.py run
   python tools/traffic.py summarize gpurun_out/traffic.csv gpurun_out/traffic_alg.json > profiles/r02_traffic.json
-
-`run` builds the bench engine (n4, batch T), warms it, then runs exactly one
-profile_step on input bench.TRAFFIC_INPUT between cudaProfilerStart/Stop and
-writes that step's per-layer algorithmic bytes next to the ncu log.
 """
 import csv
 import json
 import os
-import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -30,55 +29,71 @@ def run(n4=128, T=1, out="gpurun_out/traffic_alg.json"):
     import paper_2407_14417_b200 as moe
     prof = moe.profile_for_shape(bench.D_MODEL, bench.D_FFN, bench.LAYERS, bench.EXPERTS, bench.TOPK)
     plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 0), moe.HardwareProfile(10**15), prof)
+    res = {"n4": n4, "tokens": T, "input": bench.TRAFFIC_INPUT, "layers": bench.LAYERS}
+    # capture 1: the fused step
     eng = moe.MoeEngine(bench.LAYERS, bench.EXPERTS, bench.TOPK, bench.D_MODEL, bench.D_FFN, plan, max_tokens=T,
                         seed=0, norm_eps=bench.NORM_EPS)
     eng.synth_input(bench.TRAFFIC_INPUT, T)
-    eng.profile_step(T)  # warm (geometry caches, first-touch)
+    eng.profile_fused()
     eng.synth_input(bench.TRAFFIC_INPUT, T)
     eng.sync()
     torch.cuda.profiler.start()
-    _, fb, _ = eng.profile_step(T)
+    _, fb = eng.profile_fused()
     torch.cuda.profiler.stop()
     eng.close()
+    res["fused_algorithmic_bytes"] = fb
+    # capture 2: the per-layer kernels
+    eng = moe.MoeEngine(bench.LAYERS, bench.EXPERTS, bench.TOPK, bench.D_MODEL, bench.D_FFN, plan, max_tokens=T,
+                        seed=0, norm_eps=bench.NORM_EPS, per_layer_decode=True)
+    eng.synth_input(bench.TRAFFIC_INPUT, T)
+    eng.profile_step(T)
+    eng.synth_input(bench.TRAFFIC_INPUT, T)
+    eng.sync()
+    torch.cuda.profiler.start()
+    _, lb, _ = eng.profile_step(T)
+    torch.cuda.profiler.stop()
+    eng.close()
+    res["per_layer_algorithmic_bytes"] = round(sum(lb) / len(lb))
     with open(os.path.join(ROOT, out), "w") as fh:
-        json.dump({"n4": n4, "tokens": T, "input": bench.TRAFFIC_INPUT, "layers": bench.LAYERS,
-                   "algorithmic_bytes_per_layer": round(sum(fb) / len(fb)), "algorithmic_bytes": fb}, fh)
+        json.dump(res, fh)
 
 
-def summarize(csv_path, alg_path):
+def summarize(csv_path, alg_path, commit=""):
     with open(alg_path) as fh:
         alg = json.load(fh)
-    rows = []
     with open(csv_path) as fh:
         lines = [l for l in fh if l.startswith('"')]
-    for r in csv.DictReader(lines):
-        rows.append(r)
     per = {}
-    for r in rows:
-        name = r["Kernel Name"]
-        if not any(k in name for k in FFN_KERNELS):
-            continue
-        key = (r["ID"], name)
+    for r in csv.DictReader(lines):
         v = float(r["Metric Value"].replace(",", ""))
-        unit = r["Metric Unit"]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
-                 "nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(unit, 1)
-        per.setdefault(key, {})[r["Metric Name"]] = v * scale
-    dram = sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0) for m in per.values())
-    launches = len(per)
-    head = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True, cwd=ROOT).stdout.strip()
-    print(json.dumps({"n4": alg["n4"], "tokens": alg["tokens"], "input": alg["input"], "layers": alg["layers"],
-                      "ffn_launches": launches, "dram_bytes_step": round(dram),
-                      "dram_bytes_per_layer": round(dram / alg["layers"]),
-                      "algorithmic_bytes_per_layer": alg["algorithmic_bytes_per_layer"],
-                      "ratio": round(dram / alg["layers"] / alg["algorithmic_bytes_per_layer"], 4),
-                      "kernels": FFN_KERNELS, "commit": head,
-                      "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over one profile_step "
-                             "(tools/traffic.py)"}, indent=1))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
+                 "msecond": 1e6}.get(r["Metric Unit"], 1)
+        per.setdefault((int(r["ID"]), r["Kernel Name"]), {})[r["Metric Name"]] = v * scale
+
+    def dram(m):
+        return m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+
+    fused = [m for (i, n), m in per.items() if "decode_step_kernel" in n]
+    ffn = [m for (i, n), m in per.items() if any(k in n for k in FFN_KERNELS)]
+    base = {"n4": alg["n4"], "tokens": alg["tokens"], "input": alg["input"], "commit": commit}
+    out = {"how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (tools/traffic.py)"}
+    if fused:
+        m = fused[0]
+        out["fused"] = dict(base, what="one decode_step_kernel launch (whole %d-layer step)" % alg["layers"],
+                            dram_bytes=round(dram(m)), algorithmic_bytes=alg["fused_algorithmic_bytes"],
+                            ratio=round(dram(m) / alg["fused_algorithmic_bytes"], 4),
+                            ncu_time_us=round(m.get("gpu__time_duration.sum", 0) / 1e3, 1))
+    if ffn:
+        tot = sum(dram(m) for m in ffn)
+        out["per_layer"] = dict(base, what="the expert-FFN launches of one per-layer step, per layer (%d launches / "
+                                           "%d layers)" % (len(ffn), alg["layers"]),
+                                dram_bytes=round(tot / alg["layers"]), algorithmic_bytes=alg["per_layer_algorithmic_bytes"],
+                                ratio=round(tot / alg["layers"] / alg["per_layer_algorithmic_bytes"], 4))
+    print(json.dumps(out, indent=1))
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "run":
         run(*(int(v) for v in sys.argv[2:4]))
     else:
-        summarize(sys.argv[2], sys.argv[3])
+        summarize(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else "")
