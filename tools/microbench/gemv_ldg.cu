@@ -1,0 +1,245 @@
+// gemv_ldg.cu -- batch-1 int4-g128 GEMV data-path experiment: weights loaded
+// straight into registers (LDG.128, L1::no_allocate) with a per-warp register
+// ring D groups deep, instead of the bulk-copy smem ring of stream_kernel.
+// Same fragment-block layout and the same per-group arithmetic as
+// group_int4 (gemv.cu), so the partials are bit-identical to a naive kernel.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gemv_ldg gemv_ldg.cu
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); exit(1); } } while (0)
+#define DEVI __device__ __forceinline__
+
+DEVI uint32_t and_or(uint32_t a, uint32_t m, uint32_t o) {
+    uint32_t d; asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(m), "r"(o)); return d;
+}
+DEVI uint4 ld_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+DEVI uint32_t ld_nc32(const void* p) {
+    uint32_t r; asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p)); return r;
+}
+DEVI void mma_f16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3]) : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+DEVI void decode_lohi(uint32_t w, uint32_t& lo0, uint32_t& hi0, uint32_t& lo1, uint32_t& hi1) {
+    lo0 = and_or(w, 0x000F000Fu, 0x64006400u);
+    hi0 = and_or(w, 0x00F000F0u, 0x54005400u);
+    const uint32_t w8 = w >> 8;
+    lo1 = and_or(w8, 0x000F000Fu, 0x64006400u);
+    hi1 = and_or(w8, 0x00F000F0u, 0x54005400u);
+}
+DEVI float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+DEVI float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+
+// one group from registers; bp: this lane's activation chunks (smem), B: bias term
+DEVI void group_regs(uint4 wl, uint4 wh, uint32_t s2, const uint8_t* bp, float B, float (&acc)[4]) {
+    const uint32_t lo[4] = {wl.x, wl.y, wl.z, wl.w};
+    const uint32_t hi[4] = {wh.x, wh.y, wh.z, wh.w};
+    float c[4] = {-B, -B, -B, -B};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint4 b = *reinterpret_cast<const uint4*>(bp + q * 64);
+        uint32_t a_l0, a_h0, a_l1, a_h1, c_l0, c_h0, c_l1, c_h1;
+        decode_lohi(lo[q], a_l0, a_h0, a_l1, a_h1);
+        decode_lohi(hi[q], c_l0, c_h0, c_l1, c_h1);
+        mma_f16(c, a_l0, c_l0, a_l1, c_l1, b.x, b.y);
+        mma_f16(c, a_h0, c_h0, a_h1, c_h1, b.z, b.w);
+    }
+    const float s_lo = bf16_lo(s2), s_hi = bf16_hi(s2);
+    acc[0] = __fmaf_rn(s_lo, c[0], acc[0]);
+    acc[1] = __fmaf_rn(s_lo, c[1], acc[1]);
+    acc[2] = __fmaf_rn(s_hi, c[2], acc[2]);
+    acc[3] = __fmaf_rn(s_hi, c[3], acc[3]);
+}
+
+constexpr int GK = 8;  // groups per item (K-part)
+
+struct Args {
+    const uint8_t* W;   // [nexp][RT][G] x 1024
+    const uint8_t* S;   // [nexp][RT][G] x 32
+    const uint8_t* x16; // [K] fp16, permuted chunks
+    const float* xb;    // [G] bias terms
+    int K, R, nexp;
+    float* part;        // [KP][nexp][R]
+};
+
+template <int WARPS, int D>
+__global__ void __launch_bounds__(WARPS * 32, 1) k_ldg(Args a) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int G = a.K / 128, KP = G / GK, RT = a.R / 16;
+    for (int i = threadIdx.x * 16; i < a.K * 2; i += blockDim.x * 16)
+        *reinterpret_cast<uint4*>(sm + i) = *reinterpret_cast<const uint4*>(a.x16 + i);
+    float* sb = reinterpret_cast<float*>(sm + a.K * 2);
+    for (int i = threadIdx.x; i < G; i += blockDim.x) sb[i] = a.xb[i];
+    const int N = a.nexp * RT * KP;
+    const int Wn = gridDim.x * WARPS, wid = blockIdx.x * WARPS + warp;
+    const int beg = static_cast<int>(static_cast<long long>(N) * wid / Wn);
+    const int end = static_cast<int>(static_cast<long long>(N) * (wid + 1) / Wn);
+    // item i -> first block index: (e*RT + rt)*G + kp*GK  == (i / KP) * G + (i % KP) * GK
+    auto blk0 = [&](int i) -> size_t { return static_cast<size_t>(i / KP) * G + static_cast<size_t>(i % KP) * GK; };
+    uint4 bl[D], bh[D];
+    uint32_t bs[D];
+    if (beg < end) {
+        const size_t b0 = blk0(beg);
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const uint8_t* gp = a.W + (b0 + j) * 1024;
+            bl[j] = ld_stream(gp + lane * 16);
+            bh[j] = ld_stream(gp + 512 + lane * 16);
+            bs[j] = ld_nc32(a.S + (b0 + j) * 32 + (lane >> 2) * 4);
+        }
+    }
+    __syncthreads();
+    const int t4 = lane & 3, gr = lane >> 2;
+    for (int i = beg; i < end; ++i) {
+        const size_t b0 = blk0(i);
+        const size_t bn = i + 1 < end ? blk0(i + 1) : b0;  // next item (reload of own blocks at the end: harmless)
+        const int kp = i % KP;
+        const uint8_t* bp = sm + kp * GK * 256 + t4 * 16;
+        const float* xg = sb + kp * GK;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int g = 0; g < GK; ++g) {
+            const int s = g % D;
+            const uint4 wl = bl[s], wh = bh[s];
+            const uint32_t s2 = bs[s];
+            const size_t nb = g + D < GK ? b0 + g + D : bn + (g + D - GK);
+            const uint8_t* gp = a.W + nb * 1024;
+            bl[s] = ld_stream(gp + lane * 16);
+            bh[s] = ld_stream(gp + 512 + lane * 16);
+            bs[s] = ld_nc32(a.S + nb * 32 + (lane >> 2) * 4);
+            group_regs(wl, wh, s2, bp + g * 256, xg[g], acc);
+        }
+        const int e = i / (RT * KP), rt = (i / KP) % RT;
+        float* pp = a.part + (static_cast<size_t>(kp) * a.nexp + e) * a.R + rt * 16 + gr;
+        if (t4 == 0) {
+            __stcg(pp, acc[0]);
+            __stcg(pp + 8, acc[2]);
+        }
+    }
+}
+
+// naive: one warp per item, no pipelining (same arithmetic)
+__global__ void k_naive(Args a) {
+    const int lane = threadIdx.x & 31;
+    const int G = a.K / 128, KP = G / GK, RT = a.R / 16;
+    const int i = blockIdx.x;
+    const size_t b0 = static_cast<size_t>(i / KP) * G + static_cast<size_t>(i % KP) * GK;
+    const int kp = i % KP, t4 = lane & 3, gr = lane >> 2;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int g = 0; g < GK; ++g) {
+        const uint8_t* gp = a.W + (b0 + g) * 1024;
+        const uint4 wl = *reinterpret_cast<const uint4*>(gp + lane * 16);
+        const uint4 wh = *reinterpret_cast<const uint4*>(gp + 512 + lane * 16);
+        const uint32_t s2 = *reinterpret_cast<const uint32_t*>(a.S + (b0 + g) * 32 + (lane >> 2) * 4);
+        group_regs(wl, wh, s2, a.x16 + (kp * GK + g) * 256 + t4 * 16, a.xb[kp * GK + g], acc);
+    }
+    const int e = i / (RT * KP), rt = (i / KP) % RT;
+    float* pp = a.part + (static_cast<size_t>(kp) * a.nexp + e) * a.R + rt * 16 + gr;
+    if (t4 == 0) { pp[0] = acc[0]; pp[8] = acc[2]; }
+}
+
+static int g_sms = 148;
+
+template <int WARPS, int D>
+void run(const char* name, std::vector<Args>& sets, float* ref, size_t outn, int CTAS_PER_SM = 1) {
+    auto kern = k_ldg<WARPS, D>;
+    const Args& a0 = sets[0];
+    const size_t smem = a0.K * 2 + (a0.K / 128) * 4;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, WARPS * 32, smem));
+    const int grid = g_sms * std::min(per, CTAS_PER_SM);
+    // correctness on set 0
+    CK(cudaMemset(a0.part, 0, outn * 4));
+    kern<<<grid, WARPS * 32, smem>>>(a0);
+    CK(cudaDeviceSynchronize());
+    std::vector<float> got(outn), exp(outn);
+    CK(cudaMemcpy(got.data(), a0.part, outn * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(exp.data(), ref, outn * 4, cudaMemcpyDeviceToHost));
+    const bool ok = memcmp(got.data(), exp.data(), outn * 4) == 0;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    const int reps = 60;
+    for (int r = 0; r < 6; ++r) kern<<<grid, WARPS * 32, smem>>>(sets[r % sets.size()]);
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) kern<<<grid, WARPS * 32, smem>>>(sets[r % sets.size()]);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
+    const double bytes = (double)a0.nexp * a0.R * a0.K / 2 * (1.0 + 32.0 / 1024);
+    int regs = 0; cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern); regs = fa.numRegs;
+    printf("%-8s K=%5d R=%5d warps=%2d D=%d grid=%d regs=%d : %7.1f GB/s  %6.2f us  %s\n", name, a0.K, a0.R, WARPS, D, grid, regs,
+           bytes / (ms / reps * 1e-3) / 1e9, ms / reps * 1e3, ok ? "bit-exact" : "MISMATCH");
+}
+
+int main() {
+    CK(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0));
+    for (int shape = 0; shape < 2; ++shape) {
+        const int K = shape == 0 ? 4096 : 14336, R = shape == 0 ? 28672 : 4096, nexp = 2;
+        const size_t wbytes = (size_t)nexp * R * K / 2, sbytes = wbytes / 32;
+        const int nsets = 8;  // 8 x 117 MB > L2
+        std::vector<Args> sets;
+        std::vector<uint8_t> hw(wbytes), hs(sbytes);
+        uint32_t st = 12345u;
+        auto rnd = [&]() { st ^= st << 13; st ^= st >> 17; st ^= st << 5; return st; };
+        std::vector<uint16_t> hx(K);
+        for (int i = 0; i < K; ++i) { float v = ((int)(rnd() % 2001) - 1000) / 1000.0f; hx[i] = __half_as_ushort(__float2half(v)); }
+        std::vector<float> hb(K / 128);
+        for (auto& v : hb) v = ((int)(rnd() % 2001) - 1000) / 10.0f;
+        uint8_t *dx; float* db;
+        CK(cudaMalloc(&dx, K * 2)); CK(cudaMalloc(&db, K / 128 * 4));
+        CK(cudaMemcpy(dx, hx.data(), K * 2, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(db, hb.data(), K / 128 * 4, cudaMemcpyHostToDevice));
+        const size_t outn = (size_t)(K / 128 / GK) * nexp * R;
+        for (int s = 0; s < nsets; ++s) {
+            for (auto& v : hw) v = rnd() & 0xff;
+            for (size_t i = 0; i < sbytes; i += 2) { uint16_t sc = 0x3c00 + (rnd() % 512) - 256; hs[i] = sc & 0xff; hs[i + 1] = sc >> 8; }
+            Args a{};
+            uint8_t *dw, *ds; float* dp;
+            CK(cudaMalloc(&dw, wbytes)); CK(cudaMalloc(&ds, sbytes)); CK(cudaMalloc(&dp, outn * 4));
+            CK(cudaMemcpy(dw, hw.data(), wbytes, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(ds, hs.data(), sbytes, cudaMemcpyHostToDevice));
+            a.W = dw; a.S = ds; a.x16 = dx; a.xb = db; a.K = K; a.R = R; a.nexp = nexp; a.part = dp;
+            sets.push_back(a);
+            if (s == 0) break;  // fill the others with copies of set 0's bytes below
+        }
+        for (int s = 1; s < nsets; ++s) {
+            Args a = sets[0];
+            uint8_t *dw, *ds; float* dp;
+            CK(cudaMalloc(&dw, wbytes)); CK(cudaMalloc(&ds, sbytes)); CK(cudaMalloc(&dp, outn * 4));
+            CK(cudaMemcpy(dw, sets[0].W, wbytes, cudaMemcpyDeviceToDevice));
+            CK(cudaMemcpy(ds, sets[0].S, sbytes, cudaMemcpyDeviceToDevice));
+            a.W = dw; a.S = ds; a.part = dp;
+            sets.push_back(a);
+        }
+        float* ref; CK(cudaMalloc(&ref, outn * 4));
+        Args an = sets[0]; an.part = ref;
+        const int N = nexp * (R / 16) * (K / 128 / GK);
+        k_naive<<<N, 32>>>(an);
+        CK(cudaDeviceSynchronize());
+        run<8, 2>("ldg", sets, ref, outn);
+        run<8, 4>("ldg", sets, ref, outn);
+        run<12, 4>("ldg", sets, ref, outn);
+        run<16, 2>("ldg", sets, ref, outn);
+        run<16, 4>("ldg", sets, ref, outn);
+        run<16, 8>("ldg", sets, ref, outn);
+        run<24, 2>("ldg", sets, ref, outn);
+        run<24, 4>("ldg", sets, ref, outn);
+        run<32, 2>("ldg", sets, ref, outn);
+        run<8, 4>("ldg2cta", sets, ref, outn, 2);
+        run<8, 8>("ldg2cta", sets, ref, outn, 2);
+        run<16, 4>("ldg2cta", sets, ref, outn, 2);
+    }
+    return 0;
+}
