@@ -187,8 +187,9 @@ MOE_DEVI void numerics_group_check(float amax, bool leader) {
 // entry and post-PDL-wait globaltimer stamps (atomicMin) and the latest warp
 // end (atomicMax).  One copy per translation unit (no -rdc); null = off.
 static __device__ unsigned long long* g_layer_trace = nullptr;
-MOE_DEVI void ltrace(int id, int phase) {
-    unsigned long long* tr = g_layer_trace;
+// Kernels read the pointer once (ltr = g_layer_trace at entry) and pass it:
+// a load per call would stall every traced point on an L2 round trip.
+MOE_DEVI void ltrace(unsigned long long* tr, int id, int phase) {
     if (tr == nullptr || (threadIdx.x & 31) != 0) return;
     if (phase < 2 && threadIdx.x != 0) return;
     unsigned long long t;

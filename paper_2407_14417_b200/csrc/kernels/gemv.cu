@@ -506,7 +506,8 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
         fence_mbar_init();
     }
     const unsigned long long t_entry = gtimer();
-    ltrace(2 + 2 * a.p, 0);
+    unsigned long long* const ltr = g_layer_trace;
+    ltrace(ltr, 2 + 2 * a.p, 0);
     // When the routing comes from two or more launches back, the segment
     // table and the first items' weight copies go out before the PDL wait;
     // their activation copies (the predecessor's output) after it.
@@ -573,7 +574,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
         res_pass0();
     }
     pdl_trigger();
-    ltrace(2 + 2 * a.p, 1);
+    ltrace(ltr, 2 + 2 * a.p, 1);
     if (C::kRes && a.p == 1) {
         // resident activations, down pass: segment s's slot row (its expert's
         // format) at res + s*K*2, its bias terms at resx + s*bstride
@@ -649,7 +650,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) stream_kernel(const __grid_con
             __stcg(pp + a.rows + 8, acc[3]);
         }
     }
-    ltrace(2 + 2 * a.p, 2);
+    ltrace(ltr, 2 + 2 * a.p, 2);
     unsigned long long* tr = g_gemv_trace;
     if (tr != nullptr && lane == 0) {
         tr += (static_cast<size_t>(a.p) * W + static_cast<size_t>(wid)) * 8;
@@ -746,13 +747,14 @@ __global__ void __launch_bounds__(kFinHThreads) finalize_h_kernel(
     __shared__ uint16_t hs[128];
     const int G = f / 128;
     const int slot = blockIdx.x / G, g = blockIdx.x - slot * G;
-    ltrace(3, 0);
+    unsigned long long* const ltr = g_layer_trace;
+    ltrace(ltr, 3, 0);
     // Trigger first: the down-pass stream kernel only reads the routing
     // before its own PDL wait, so its CTAs may start (and prefetch weights)
     // as the gate/up stream's CTAs drain.
     pdl_trigger();
     pdl_wait();
-    ltrace(3, 1);
+    ltrace(ltr, 3, 1);
     if (blockIdx.x == 0 && threadIdx.x == 0) *sched = 0;  // the stream kernel is complete
     const int KP = kpslot[slot];
     if (KP == 0) return;
@@ -763,7 +765,7 @@ __global__ void __launch_bounds__(kFinHThreads) finalize_h_kernel(
     __syncthreads();
     if (threadIdx.x >= 32) return;
     swiglu_unit(red, hs, slot, g, f, hperm, hperm16, hsum, hstride, threadIdx.x);
-    ltrace(3, 2);
+    ltrace(ltr, 3, 2);
 }
 
 // Output finalize: one block per (token t, 128 output rows) -- or, with
@@ -779,10 +781,11 @@ __global__ void __launch_bounds__(kFinOThreads) finalize_out_kernel(
     const int nslots = T * k;
     const int nb = d / (kFinOQuads * 4);
     const int r = blockIdx.x / nb, j0 = (blockIdx.x - r * nb) * (kFinOQuads * 4);
-    ltrace(5, 0);
+    unsigned long long* const ltr = g_layer_trace;
+    ltrace(ltr, 5, 0);
     pdl_trigger();  // the next layer's route kernel preloads router weights before its wait
     pdl_wait();
-    ltrace(5, 1);
+    ltrace(ltr, 5, 1);
     if (blockIdx.x == 0 && threadIdx.x == 0) *sched = 0;
     const size_t kstride = static_cast<size_t>(nslots) * d;
     const int q = threadIdx.x % kFinOQuads, kg = threadIdx.x / kFinOQuads;
@@ -833,7 +836,7 @@ __global__ void __launch_bounds__(kFinOThreads) finalize_out_kernel(
 #pragma unroll
         for (int u = 0; u < 4; ++u) out[static_cast<size_t>(t) * d + j + u] = f2bf(acc[u]);
     }
-    ltrace(5, 2);
+    ltrace(ltr, 5, 2);
 }
 
 // x (natural, [rows][K]) -> K-permuted bf16 + fp16 copies and, per 128-K
@@ -846,10 +849,11 @@ __global__ void permute_rows_kernel(const uint16_t* __restrict__ x, int rows, in
     const int G = K / 128;
     const long long hw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 4;
     const int c = threadIdx.x & 15;
-    ltrace(1, 0);
+    unsigned long long* const ltr = g_layer_trace;
+    ltrace(ltr, 1, 0);
     pdl_wait();     // x is the previous layer's output
     pdl_trigger();
-    ltrace(1, 1);
+    ltrace(ltr, 1, 1);
     const bool ok = hw < static_cast<long long>(rows) * G;
     const long long r = ok ? hw / G : 0;
     const int g = ok ? static_cast<int>(hw - r * G) : 0;
@@ -895,12 +899,23 @@ using DecodeArgs = MoeDecodeArgs;
 
 // Debug (moe_debug_fused_trace): per layer and CTA, globaltimer stamps of the
 // phase boundaries [L][gridDim][kFusedStamps]; null (default) = off.
-constexpr int kFusedStamps = 10;
+constexpr int kFusedStamps = 18;  // 0-9 phase boundaries, 10-14 inside routing
 __device__ unsigned long long* g_fused_trace = nullptr;
-MOE_DEVI void fstamp(int l, int i) {
-    unsigned long long* tr = g_fused_trace;
-    if (tr == nullptr || threadIdx.x != 0) return;
-    tr[(static_cast<size_t>(l) * gridDim.x + blockIdx.x) * kFusedStamps + i] = gtimer();
+// The trace pointer is read once per kernel (ftr): a per-stamp load of the
+// global would put an L2 round trip in front of every phase.  Stamps are SM
+// cycles (clock64: a register read; %globaltimer reads cost ~0.5 us each).
+// Stamps are warp-uniform (every lane reads the clock, lane 0 stores, then
+// __syncwarp): a lane-0-only branch would leave the warp diverged into the
+// next shuffle and slow it down -- the trace must not change what it measures.
+MOE_DEVI void fstamp_lane0(unsigned long long* tr, int l, int i) {
+    if (tr == nullptr) return;
+    const unsigned long long c = clock64();
+    if ((threadIdx.x & 31) == 0) tr[(static_cast<size_t>(l) * gridDim.x + blockIdx.x) * kFusedStamps + i] = c;
+    __syncwarp();
+}
+MOE_DEVI void fstamp(unsigned long long* tr, int l, int i) {
+    if (tr == nullptr || threadIdx.x >= 32) return;
+    fstamp_lane0(tr, l, i);
 }
 
 MOE_DEVI unsigned int ld_acquire_gpu(const unsigned int* p) {
@@ -1012,6 +1027,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
     __shared__ float4 redo[MOE_MAX_TOPK][kKG][kFinOQuads];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
     const int d = a.d, f = a.f, E = a.E, k = a.k;
+    unsigned long long* const ftr = g_fused_trace;
     if (lane == 0) {
         for (int s2 = 0; s2 < kStages; ++s2) mbar_init(&bars[warp][s2], 1);
         if (warp == 0) mbar_init(&res_bar, 1);
@@ -1038,7 +1054,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
         const uint16_t* xl = l == 0 ? a.x_in : ((l - 1) & 1 ? a.xbuf1 : a.xbuf0);
         uint16_t* yl = l == a.L - 1 ? a.x_out : (l & 1 ? a.xbuf1 : a.xbuf0);
         const uint16_t* wgl = a.wg + static_cast<size_t>(l) * E * d;
-        fstamp(l, 0);
+        fstamp(ftr, l, 0);
         // ---- R: route the token (every CTA, identical results) --------------
         for (int i = tid; i < E * static_cast<int>(sizeof(moe_expert_weights) / 8); i += blockDim.x)
             reinterpret_cast<uint2*>(s_ex)[i] =
@@ -1046,6 +1062,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
         for (int i = tid * 8; i < d; i += blockDim.x * 8)
             *reinterpret_cast<uint4*>(xs + i) = __ldcg(reinterpret_cast<const uint4*>(xl + i));
         __syncthreads();
+        fstamp(ftr, l, 10);
         const uint16_t* xr = xs;
         if (a.norm_eps > 0.0f) {
             float acc = 0.0f;  // route_kernel's pinned order
@@ -1068,6 +1085,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
             __syncthreads();
             const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(lg_s[MOE_MAX_EXPERTS], static_cast<float>(d)),
                                                                     a.norm_eps)));
+            fstamp(ftr, l, 11);
             for (int i = tid * 8; i < d; i += blockDim.x * 8) {
                 uint4 v = *reinterpret_cast<const uint4*>(xs + i);
                 uint32_t w4[4] = {v.x, v.y, v.z, v.w};
@@ -1078,6 +1096,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
                 *reinterpret_cast<uint4*>(xn + i) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
             }
             __syncthreads();
+            fstamp(ftr, l, 12);
             xr = xn;
         }
         for (int e = warp; e < E; e += kWarps) {
@@ -1086,14 +1105,18 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
             if (lane == 0) lg_s[e] = v;
         }
         __syncthreads();
+        fstamp(ftr, l, 13);
         if (warp == 0) {
-            warp_topk(lg_s, E, k, lane, s_topi, s_w, s_idx);
+            if (lane == 0) {
+                lane_topk(lg_s, E, k, s_topi, nullptr, s_idx, s_w);
+                lane_permute(s_idx, k, E, s_counts, s_offsets, s_perm, s_inv);
+            }
             __syncwarp();
-            warp_permute(s_idx, k, E, s_counts, s_offsets, s_perm, s_inv, lane);
             if (blockIdx.x == 0 && lane < k) {
                 a.idx[static_cast<size_t>(l) * a.idx_stride + lane] = s_topi[lane];
                 a.wts[static_cast<size_t>(l) * a.idx_stride + lane] = s_w[lane];
             }
+            fstamp(ftr, l, 15);
         } else {
             // resident activation rows of the gate/up pass: K-permuted bf16
             // (res), fp16 (res + 2d) and the int4 bias terms (res + 4d)
@@ -1118,13 +1141,15 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
                     if (c == 0) rx[g] = int4_bias_term(s_lo, s_hi);
                 }
             }
+            if (warp == 1) fstamp_lane0(ftr, l, 16);
         }
         __syncthreads();
+        fstamp(ftr, l, 14);
         if (tid == 0) build_segs_t1<C>(st[0], s_ex, s_offsets, E, 0, 2 * f, d);
         if (tid == 32) build_segs_t1<C>(st[1], s_ex, s_offsets, E, 1, d, f);
         fence_proxy_async();  // scratch (generic) writes before the rings' bulk copies
         __syncthreads();
-        fstamp(l, 1);
+        fstamp(ftr, l, 1);
 
         if (l + 1 < a.L && blockIdx.x < 4 && tid == 0) {  // next layer's router weights -> L2
             const uint32_t chunk = static_cast<uint32_t>(E) * d * 2 / 4;
@@ -1171,9 +1196,9 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
             if (pass == 1) {
                 // ---- H: SwiGLU finalize over (slot, 128-group) units -------------
                 fence_proxy_async();  // resident rows read (generic) before phase D's bulk copies
-                fstamp(l, 2);
+                fstamp(ftr, l, 2);
                 grid_barrier(a.bar, a.bar_mode);
-                fstamp(l, 3);
+                fstamp(ftr, l, 3);
                 const int Gf = f / 128;
                 const size_t rows2 = static_cast<size_t>(2) * f;
                 // up to two (slot, group) units per CTA at once: every K-part
@@ -1211,9 +1236,9 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
                     __syncthreads();
                 }
                 fence_proxy_async();  // generic scratch writes to the resident area before phase D's bulk copies
-                fstamp(l, 4);
+                fstamp(ftr, l, 4);
                 grid_barrier(a.bar, a.bar_mode);
-                fstamp(l, 5);
+                fstamp(ftr, l, 5);
                 // ---- D: h rows into the resident area (slot s's row in its format)
                 if (tid == 0) {
                     fence_proxy_async_global();
@@ -1231,7 +1256,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
                 }
                 mbar_wait(&res_bar, res_phase);
                 res_phase ^= 1u;
-                fstamp(l, 6);
+                fstamp(ftr, l, 6);
             }
             const int K = pass ? f : d, rows = pass ? d : 2 * f;
             float* part = pass ? a.part1 : a.part0;
@@ -1279,9 +1304,9 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
             }
         }
         // ---- O: combine + residual -> x(l+1) ---------------------------------
-        fstamp(l, 7);
+        fstamp(ftr, l, 7);
         grid_barrier(a.bar, a.bar_mode);
-        fstamp(l, 8);
+        fstamp(ftr, l, 8);
         if (blockIdx.x == 0 && tid < 2) a.sched[2 * l + tid] = 0;  // this layer's pools, for the next step
         {
             const int nb = d / (kFinOQuads * 4);
@@ -1321,7 +1346,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
                 __syncthreads();
             }
         }
-        fstamp(l, 9);
+        fstamp(ftr, l, 9);
         if (l + 1 < a.L) {
             if (warp < E) preload_w(wpre, wgl + static_cast<size_t>(E) * d + static_cast<size_t>(warp) * d, d, lane);
             grid_barrier(a.bar, a.bar_mode);

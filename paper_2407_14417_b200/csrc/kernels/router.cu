@@ -123,14 +123,15 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
 
     const int t = blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    ltrace(0, 0);
+    unsigned long long* const ltr = g_layer_trace;
+    ltrace(ltr, 0, 0);
     // The router weights do not depend on the previous layer: this warp's
     // first expert row goes into registers before the PDL wait.
     uint4 wpre[kPreChunks];
     if (wid < a.E) preload_w(wpre, a.wg + static_cast<size_t>(wid) * a.d, a.d, lane);
     pdl_wait();     // x is the previous layer's output
     pdl_trigger();
-    ltrace(0, 1);
+    ltrace(ltr, 0, 1);
     const uint16_t* xt = a.x + static_cast<size_t>(t) * a.d;
     for (int i = threadIdx.x * 8; i < a.d; i += blockDim.x * 8) {
         if (i + 8 <= a.d)
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
         }
         __syncthreads();
     }
-    ltrace(1, 0);
+    ltrace(ltr, 1, 0);
     if (a.xnat != nullptr)
         for (int i = threadIdx.x * 8; i + 8 <= a.d; i += blockDim.x * 8)
             *reinterpret_cast<uint4*>(a.xnat + static_cast<size_t>(t) * a.d + i) = *reinterpret_cast<const uint4*>(x_s + i);
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
         if (lane == 0) lg_s[e] = v;
     }
     __syncthreads();
-    ltrace(1, 1);
+    ltrace(ltr, 1, 1);
     if (a.logits && threadIdx.x < a.E) a.logits[static_cast<size_t>(t) * a.E + threadIdx.x] = lg_s[threadIdx.x];
     if (wid == 0) warp_topk(lg_s, a.E, a.k, lane, a.idx + static_cast<size_t>(t) * a.k, a.w + static_cast<size_t>(t) * a.k, s_idx);
     // K-permuted bf16 / fp16 copies of this token row + int4 bias terms
@@ -219,17 +220,17 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
         }
     }
     if (a.counts == nullptr) {
-        ltrace(0, 2);
+        ltrace(ltr, 0, 2);
         return;
     }
     if (gridDim.x == 1) {
         // single token: warp 0 permutes straight from its top-k (shared memory)
         if (wid == 0) {
             __syncwarp();
-            ltrace(1, 2);
+            ltrace(ltr, 1, 2);
             warp_permute(s_idx, a.k, a.E, a.counts, a.offsets, a.perm, a.inv_perm, lane);
         }
-        ltrace(0, 2);
+        ltrace(ltr, 0, 2);
         return;
     }
     // Fused K2: the last CTA to finish permutes all tokens.
@@ -238,13 +239,13 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(RouteArgs a) {
     if (threadIdx.x == 0) s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last) {
-        ltrace(0, 2);
+        ltrace(ltr, 0, 2);
         return;
     }
     __threadfence();
     block_permute(a.idx, a.T * a.k, a.E, a.counts, a.offsets, a.perm, a.inv_perm);
     if (threadIdx.x == 0) *a.ticket = 0;
-    ltrace(0, 2);
+    ltrace(ltr, 0, 2);
 }
 
 __global__ void __launch_bounds__(kRouteThreads) permute_kernel(const int32_t* idx, int n, int E,

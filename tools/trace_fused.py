@@ -17,9 +17,10 @@ prof = moe.profile_for_shape(4096, 14336, L, 8, 2)
 plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 0), moe.HardwareProfile(10**15), prof)
 eng = moe.MoeEngine(L, 8, 2, 4096, 14336, plan, max_tokens=1, seed=0, norm_eps=1e-5)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
-S = 10
+S = 18
 names = ["layer start", "routing done", "gate/up done", "after bar 1", "swiglu done", "after bar 2", "h resident",
-         "down done", "after bar 3", "combine done"]
+         "down done", "after bar 3", "combine done", "r: x loaded", "r: rstd", "r: normalised", "r: logits",
+         "r: topk+rows", "r: w0 topk+perm", "r: w1 rows"]
 buf = torch.zeros(L * sms * S, dtype=torch.int64, device="cuda")
 eng.synth_input(0, 1)
 for _ in range(5):
@@ -37,11 +38,13 @@ for rep in range(5):
     tr = buf.cpu().numpy().reshape(L, sms, S).astype(np.float64)
     acc.append(tr)
 tr = np.median(np.stack(acc), axis=0)  # [L][sms][S]
-rel = (tr - tr[:, :, :1].min(axis=1, keepdims=True)) / 1e3  # us from the layer's first start
-print(f"== fused step, n4={n4}: phase stamps (us from the layer's earliest start; avg over {L} layers) "
+MHZ = float(os.environ.get("SM_MHZ", "1965"))  # stamps are SM cycles (clock64), per CTA
+rel = (tr - tr[:, :, :1]) / MHZ  # us from this CTA's own layer start
+print(f"== fused step, n4={n4}: phase stamps (us from each CTA's layer start, SM clock; avg over {L} layers) "
       f"min / median / max over {sms} CTAs")
-for i, n in enumerate(names):
+for i in [0, 10, 11, 12, 13, 15, 16, 14, 1, 2, 3, 4, 5, 6, 7, 8, 9]:
+    n = names[i]
     v = rel[:, :, i]
     print(f"   {n:14s} {v.min(axis=1).mean():7.2f} {np.median(v, axis=1).mean():7.2f} {v.max(axis=1).mean():7.2f}")
-span = (tr[1:, :, 0].min(axis=1) - tr[:-1, :, 0].min(axis=1)) / 1e3
-print(f"   layer period   {span.mean():7.2f} us  (step {(tr[-1, :, 9].max() - tr[0, :, 0].min()) / 1e3:.1f} us)")
+span = np.median(tr[1:, :, 0] - tr[:-1, :, 0], axis=1) / MHZ
+print(f"   layer period   {span.mean():7.2f} us (median over CTAs)")
