@@ -325,6 +325,11 @@ typedef struct {
                                   cooperative persistent launch (routing, both GEMV passes, SwiGLU and
                                   combine of every layer, grid barriers between phases); 1: five launches
                                   per layer (the same arithmetic, bit-identical output) */
+    int32_t ep_rank, ep_world; /* expert parallelism: ep_world > 1 shards every layer's
+                                  experts over ep_world engines (slot s on rank s*ep_world/E); this one
+                                  holds only its own.  decode() then sends each routed token row to its
+                                  expert's owner and gets the output back over peer memory (NVLink P2P /
+                                  CUDA IPC; moe_engine_ep_buffer / moe_engine_ep_set_peers).  0/1: off */
 } moe_engine_config;
 
 int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan_entries,
@@ -362,6 +367,13 @@ void* moe_engine_stream(moe_engine* eng);
 /* Routing of the last decode step: slots [T, L, k] ascending per record
  * (GatingTrace layout, gating.hpp:22) -- host buffer. */
 int moe_engine_last_routing(moe_engine* eng, int T, int32_t* slots_out);
+/* Expert parallelism: this rank's exchange buffer -- its own cudaMalloc
+ * allocation, to be shared with moe_ep_peer_ipc_handle -- and the G ranks'
+ * buffer bases in rank order (its own at ep_rank) before the first decode.
+ * Replaces nothing in the reference (single GPU): the north
+ * star's EP over NVLink, with the exchange inside the engine's step. */
+int moe_engine_ep_buffer(moe_engine* eng, void** base, int64_t* bytes);
+int moe_engine_ep_set_peers(moe_engine* eng, const void* const* bases, int32_t world);
 /* Cumulative SimReport counters of real runs (hits / bytes_transferred /
  * activations follow simulate() semantics for the engine's plan). */
 int moe_engine_counters(const moe_engine* eng, moe_sim_report* out);

@@ -41,6 +41,14 @@ struct EngineConfig {
                                     // one-launch step (decode_step_kernel); for A/B and the host-split path
     bool keep_masters = false;  // pinned host copy of every expert in both precisions (the reconfig
                                 // model's "16-bit master on the CPU", reconfig.hpp:39): required by reconfigure()
+    // Expert parallelism: ep_world > 1 shards every layer's
+    // experts over ep_world engines (one per GPU, or several on one GPU for
+    // tests); this one holds only the slots s with s*ep_world/E == ep_rank.
+    // Tokens stay on their rank; each layer sends only the routed rows to the
+    // experts' owners and gets their outputs back, over peer memory
+    // (ep_set_peers), all inside decode() (graph-captured).
+    int ep_rank = 0;
+    int ep_world = 1;
 };
 
 // What MoeEngine::reconfigure did: the model's numbers (diff_plans) and the
@@ -92,6 +100,12 @@ class MoeEngine {
     // to an engine built with `target`.  Needs keep_masters.
     ReconfigReport reconfigure(const PlacementPlan& target, const HardwareProfile& hw);
     const PlacementPlan& plan() const;
+
+    // Expert parallelism: this rank's exchange buffer (its own cudaMalloc
+    // allocation, so a CUDA IPC handle maps exactly it) and the G ranks'
+    // buffer bases in rank order (this one's included), set before decode.
+    void* ep_buffer(size_t* bytes);
+    void ep_set_peers(const void* const* bases, int world);
 
     GatingTrace last_routing(int T);
     const SimReport& counters() const;

@@ -97,7 +97,7 @@ class _EngineConfig(C.Structure):
                 ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("max_tokens", C.c_int32),
                 ("seed", C.c_uint64), ("device", C.c_int32), ("use_graphs", C.c_int32), ("norm_eps", C.c_float),
                 ("tc_min_tokens", C.c_int32), ("lru_capacity", C.c_int32), ("keep_masters", C.c_int32),
-                ("per_layer_decode", C.c_int32)]
+                ("per_layer_decode", C.c_int32), ("ep_rank", C.c_int32), ("ep_world", C.c_int32)]
 
 
 _lib = None
@@ -209,6 +209,8 @@ def lib() -> C.CDLL:
         "moe_engine_reset_counters": (I, [VP]),
         "moe_engine_expert": (I, [VP, I, I, P(ExpertWeightsC), P(C.c_int32)]),
         "moe_engine_router": (I, [VP, I, P(VP)]),
+        "moe_engine_ep_buffer": (I, [VP, P(VP), P(I64)]),
+        "moe_engine_ep_set_peers": (I, [VP, P(VP), I]),
         "moe_debug_gemv_trace": (I, [VP]),
         "moe_debug_layer_trace": (I, [VP, VP]),
     }
@@ -842,13 +844,14 @@ class MoeEngine:
     def __init__(self, num_layers: int, experts_per_layer: int, top_k: int, d_model: int, d_ffn: int,
                  plan: PlacementPlan, max_tokens: int = 1, seed: int = 0, device: int = 0,
                  use_graphs: bool = True, norm_eps: float = 0.0, tc_min_tokens: int = 0, lru_capacity: int = 0,
-                 keep_masters: bool = False, per_layer_decode: bool = False):
+                 keep_masters: bool = False, per_layer_decode: bool = False, ep_rank: int = 0, ep_world: int = 1):
         self.L, self.E, self.k, self.d, self.f = num_layers, experts_per_layer, top_k, d_model, d_ffn
+        self.ep_rank, self.ep_world = ep_rank, ep_world
         self.max_tokens = max_tokens
         self.norm_eps = norm_eps
         cfg = _EngineConfig(num_layers, experts_per_layer, top_k, d_model, d_ffn, max_tokens, seed, device,
                             1 if use_graphs else 0, norm_eps, tc_min_tokens, lru_capacity, 1 if keep_masters else 0,
-                            1 if per_layer_decode else 0)
+                            1 if per_layer_decode else 0, ep_rank, ep_world)
         h = C.c_void_p()
         _check(lib().moe_engine_create(C.byref(cfg), plan._entries(), C.byref(h)))
         self._h = h
@@ -897,6 +900,17 @@ class MoeEngine:
 
     def sync(self):
         _check(lib().moe_engine_sync(self._h))
+
+    def ep_buffer(self):
+        """(device pointer, bytes) of this rank's expert-parallel exchange buffer."""
+        p, n = C.c_void_p(), C.c_int64()
+        _check(lib().moe_engine_ep_buffer(self._h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def ep_set_peers(self, bases):
+        """Exchange-buffer bases of all ranks in rank order (this one's included)."""
+        arr = (C.c_void_p * len(bases))(*bases)
+        _check(lib().moe_engine_ep_set_peers(self._h, arr, len(bases)))
 
     def profile_step(self, T: int):
         """Per-layer expert-FFN milliseconds (CUDA events on the launch stream),

@@ -786,10 +786,28 @@ int moe_engine_create(const moe_engine_config* cfg, const moe_expert_state* plan
         usage_if(cfg->lru_capacity < 0, "lru_capacity must be >= 0");
         ec.lru_capacity = cfg->lru_capacity;
         ec.keep_masters = cfg->keep_masters != 0;
+        ec.ep_rank = cfg->ep_world > 1 ? cfg->ep_rank : 0;
+        ec.ep_world = cfg->ep_world > 1 ? cfg->ep_world : 1;
         const int n = cfg->num_layers * cfg->experts_per_layer;
         PlacementPlan plan = to_plan(plan_entries, n, 0);
         plan.swap_slot_bytes = required_swap_bytes(plan, ec.profile);
         *out = new moe_engine{new MoeEngine(ec, plan)};
+    });
+}
+
+int moe_engine_ep_buffer(moe_engine* eng, void** base, int64_t* bytes) {
+    return guarded([&] {
+        usage_if(eng == nullptr || base == nullptr, "null argument");
+        size_t b = 0;
+        *base = eng->impl->ep_buffer(&b);
+        if (bytes) *bytes = static_cast<int64_t>(b);
+    });
+}
+
+int moe_engine_ep_set_peers(moe_engine* eng, const void* const* bases, int32_t world) {
+    return guarded([&] {
+        usage_if(eng == nullptr, "null argument");
+        eng->impl->ep_set_peers(bases, world);
     });
 }
 

@@ -183,6 +183,23 @@ struct MoeEngine::Impl {
     unsigned int* fused_ctl = nullptr;          // [L*2 tail-pool counters][2 barrier words]
     bool fused_ok = false;
 
+    // expert parallelism (ep_a2a.cu): G ranks, this one owns slots s*G/E == rank
+    bool ep = false;
+    int G = 1, rank = 0, C = 0;          // C = entries per source rank (Tmax * K)
+    std::vector<char> mine;              // [E] slot owned by this rank
+    char* ep_buf = nullptr;              // rows | meta | ret | flags (peers write here)
+    size_t ep_bytes = 0;
+    std::vector<const void*> ep_peers;   // [G] exchange buffers, rank order
+    uint32_t* ep_epoch = nullptr;
+    int32_t *ep_keys = nullptr, *ep_counts = nullptr, *ep_offsets = nullptr, *ep_perm = nullptr, *ep_inv = nullptr,
+            *ep_iota = nullptr;
+    float* ep_y = nullptr;               // [G*C][d] per computed entry
+    uint16_t* ep_dense = nullptr;        // GEMV path: received rows in slot order [G*ep_Tgemv*K][d]
+    GemvWorkspace ep_gws{};
+    void* ep_gws_base = nullptr;
+    void* ep_tcws = nullptr;
+    int ep_Tgemv = 0;                    // largest local T served by the GEMV on the received rows
+
     SimReport counters;
     std::map<int, cudaGraphExec_t> graphs;
 
@@ -222,6 +239,16 @@ struct MoeEngine::Impl {
         if (E > MOE_MAX_EXPERTS) throw ValidationError("experts_per_layer exceeds MOE_MAX_EXPERTS");
         if (K > MOE_MAX_TOPK) throw ValidationError("top_k exceeds MOE_MAX_TOPK");
         if (Tmax < 1) throw ValidationError("max_tokens must be >= 1");
+        G = c.ep_world;
+        rank = c.ep_rank;
+        ep = G > 1;
+        if (G < 1 || G > 8 || rank < 0 || rank >= G) throw ValidationError("ep_world must be in [1, 8] and ep_rank in [0, ep_world)");
+        if (ep && (E < G || E >= MOE_MAX_EXPERTS))
+            throw ValidationError("expert parallelism needs ep_world <= experts_per_layer < MOE_MAX_EXPERTS");
+        if (ep && (c.lru_capacity > 0 || c.keep_masters))
+            throw UsageError("the expert-parallel engine serves device-resident experts (no LRU / reconfiguration masters)");
+        mine.assign(static_cast<size_t>(E), 1);
+        for (int s2 = 0; s2 < E; ++s2) mine[static_cast<size_t>(s2)] = !ep || s2 * G / E == rank;
         if (static_cast<int>(plan.entries.size()) != L * E)
             throw ValidationError("plan covers " + std::to_string(plan.entries.size()) +
                                   " experts, engine has " + std::to_string(L * E));
@@ -263,6 +290,10 @@ struct MoeEngine::Impl {
         for (int i = 0; i < L * E; ++i) {
             const ExpertState st = plan.entries[static_cast<size_t>(i)];
             const size_t sz = st.precision == Precision::P16 ? size16 : size4;
+            if (!mine[static_cast<size_t>(i % E)]) continue;  // another rank's expert: not held here
+            if (ep && st.location != Location::GPU)
+                throw UsageError("the expert-parallel engine serves device-resident experts: plan expert " +
+                                 std::to_string(i) + " is host-resident");
             if (st.location == Location::GPU) {
                 off[static_cast<size_t>(i)] = dev_bytes;
                 dev_bytes += align_up(sz, 256);
@@ -291,6 +322,11 @@ struct MoeEngine::Impl {
         weights.resize(static_cast<size_t>(L * E));
         for (int i = 0; i < L * E; ++i) {
             const ExpertState st = plan.entries[static_cast<size_t>(i)];
+            if (!mine[static_cast<size_t>(i % E)]) {
+                weights[static_cast<size_t>(i)] = moe_expert_weights{};
+                weights[static_cast<size_t>(i)].precision = st.precision == Precision::P16 ? MOE_P16 : MOE_P4;
+                continue;
+            }
             char* base = st.location == Location::GPU ? dev_arena + off[static_cast<size_t>(i)]
                          : c.keep_masters              ? host_copy(i, st.precision)
                                                        : host_arena + off[static_cast<size_t>(i)];
@@ -328,7 +364,8 @@ struct MoeEngine::Impl {
         }
         ck(cudaMemsetAsync(ticket, 0, 4, compute), "memset");
         ck(cudaMemsetAsync(xin, 0, static_cast<size_t>(Tmax) * d * 2, compute), "memset");
-        if (!cfg.per_layer_decode && moek_decode_step_supported(E, K, d, f)) {
+        if (ep) ep_alloc();
+        if (!ep && !cfg.per_layer_decode && moek_decode_step_supported(E, K, d, f)) {
             dev_alloc(reinterpret_cast<void**>(&dev_experts), static_cast<size_t>(L) * E * sizeof(moe_expert_weights));
             dev_alloc(reinterpret_cast<void**>(&fused_ctl), (static_cast<size_t>(L) * 2 + 2) * 4);
             ck(cudaMemsetAsync(fused_ctl, 0, (static_cast<size_t>(L) * 2 + 2) * 4, compute), "memset");
@@ -400,6 +437,7 @@ struct MoeEngine::Impl {
         if (host_bytes || master_arena) ck(cudaMalloc(&stage, size16), "cudaMalloc(stage)");
         for (int e = 0; e < L * E; ++e) {
             const ExpertState st = plan.entries[static_cast<size_t>(e)];
+            if (!mine[static_cast<size_t>(e % E)]) continue;  // another rank's expert
             ck(moek_synth_weight(cfg.seed, uid_expert(e, 1), static_cast<long long>(2 * fd), sh_gu, master, compute), "synth");
             ck(moek_synth_weight(cfg.seed, uid_expert(e, 2), static_cast<long long>(fd), sh_d, master + 4 * fd, compute), "synth");
             char* dst = st.location == Location::GPU ? static_cast<char*>(const_cast<void*>(weights[static_cast<size_t>(e)].w_gate_up))
@@ -576,7 +614,8 @@ struct MoeEngine::Impl {
         if (master_arena) cudaFreeHost(master_arena);
         if (copy) cudaStreamSynchronize(copy);
         void* devp[] = {tcws, xn, dev_arena, swap, wg, xin, xout, xbuf[0], xbuf[1], idx, wts, counts, offsets, perm, inv, ticket, y,
-                         gws_base, dev_experts, fused_ctl};
+                         gws_base, dev_experts, fused_ctl, ep_buf, ep_epoch, ep_keys, ep_counts, ep_offsets, ep_perm,
+                         ep_inv, ep_iota, ep_y, ep_gws_base, ep_tcws, ep_dense};
         for (void* p : devp)
             if (p) cudaFree(p);
         if (host_arena) cudaFreeHost(host_arena);
@@ -705,7 +744,107 @@ struct MoeEngine::Impl {
         ck(moek_combine(y, inv, w_l, x, T, d, K, out, compute), "combine");
     }
 
+    // ---- expert parallelism (ep_a2a.cu) ------------------------------------
+    void ep_alloc() {
+        // a rank's step spins on its peers' flags while the peers launch:
+        // no kernel of the step may be loaded lazily (first-launch loading
+        // can wait for the device to idle -> deadlock)
+        ck(moek_preload_gemv(), "preload");
+        ck(moek_preload_router(), "preload");
+        ck(moek_preload_misc(), "preload");
+        ck(moek_preload_tc(), "preload");
+        ck(moek_preload_ep(), "preload");
+        C = Tmax * K;
+        const int Tp = G * C;  // received entries, sparse (one region per source rank)
+        ep_bytes = moek_ep_a2a_bytes(G, C, d);
+        ck(cudaMalloc(reinterpret_cast<void**>(&ep_buf), ep_bytes), "cudaMalloc(ep exchange)");  // own allocation: IPC maps it whole
+        ck(cudaMemsetAsync(ep_buf, 0, ep_bytes, compute), "memset");
+        dev_alloc(reinterpret_cast<void**>(&ep_epoch), 4);
+        ck(cudaMemsetAsync(ep_epoch, 0, 4, compute), "memset");
+        dev_alloc(reinterpret_cast<void**>(&ep_keys), static_cast<size_t>(Tp) * 4);
+        dev_alloc(reinterpret_cast<void**>(&ep_counts), static_cast<size_t>(E + 1) * 4);
+        dev_alloc(reinterpret_cast<void**>(&ep_offsets), static_cast<size_t>(E + 2) * 4);
+        dev_alloc(reinterpret_cast<void**>(&ep_perm), static_cast<size_t>(Tp) * 4);
+        dev_alloc(reinterpret_cast<void**>(&ep_inv), static_cast<size_t>(Tp) * 4);
+        const int niota = std::max(C, Tp);
+        dev_alloc(reinterpret_cast<void**>(&ep_iota), static_cast<size_t>(niota) * 4);
+        dev_alloc(reinterpret_cast<void**>(&ep_y), static_cast<size_t>(Tp) * d * 4);
+        std::vector<int32_t> io(static_cast<size_t>(niota));
+        for (int i = 0; i < niota; ++i) io[static_cast<size_t>(i)] = i;
+        ck(cudaMemcpy(ep_iota, io.data(), io.size() * 4, cudaMemcpyHostToDevice), "H2D iota");
+        // owners run their experts on the received rows with k = 1: the GEMV
+        // while the worst case (every rank's entries to this one) fits its
+        // segment table, the tcgen05 GEMM from tc_min_tokens local tokens on
+        ep_Tgemv = std::min(Tmax, std::max(1, cfg.tc_min_tokens - 1));
+        while (ep_Tgemv > 0 && G * ep_Tgemv * K > moek_gemv_max_tokens(E, 1)) --ep_Tgemv;
+        if (ep_Tgemv > 0) {
+            const size_t b = moek_gemv_workspace_bytes(G * ep_Tgemv * K, 1, d, f);
+            dev_alloc(&ep_gws_base, b);
+            ck(cudaMemsetAsync(ep_gws_base, 0, b, compute), "memset");
+            ep_gws = moek_gemv_workspace_view(ep_gws_base, G * ep_Tgemv * K, 1, d, f);
+            dev_alloc(reinterpret_cast<void**>(&ep_dense), static_cast<size_t>(G) * ep_Tgemv * K * d * 2);
+            ck(cudaMemsetAsync(ep_dense, 0, static_cast<size_t>(G) * ep_Tgemv * K * d * 2, compute), "memset");
+        }
+        if (Tmax > ep_Tgemv) dev_alloc(&ep_tcws, moek_tc_workspace_bytes(Tp, 1, d, f));
+        if (!xn) dev_alloc(reinterpret_cast<void**>(&xn), static_cast<size_t>(Tmax) * d * 2);
+        ck(cudaStreamSynchronize(compute), "sync");
+    }
+
+    uint64_t mine_mask() const {
+        uint64_t m = 0;
+        for (int s2 = 0; s2 < E; ++s2)
+            if (mine[static_cast<size_t>(s2)]) m |= 1ull << s2;
+        return m;
+    }
+
+    // One expert-parallel layer: route this rank's T tokens, send each routed
+    // row to its expert's owner, run this rank's experts on what it received,
+    // return the outputs to their sources, combine.  All on `compute`.
+    void ep_layer(int l, const uint16_t* x, int T, uint16_t* out, int32_t* idx_l, float* w_l) {
+        const int Tp = G * C;
+        const uint16_t* xr = cfg.norm_eps > 0.0f ? xn : x;  // the experts' input rows (natural order)
+        ck(moek_route(x, wg + static_cast<size_t>(l) * E * d, T, d, E, K, idx_l, w_l, nullptr, nullptr, nullptr,
+                      nullptr, nullptr, ticket, compute, nullptr, nullptr, nullptr, 0, cfg.norm_eps,
+                      cfg.norm_eps > 0.0f ? xn : nullptr),
+           "route");
+        const void* const* peers = ep_peers.data();
+        ck(moek_ep_a2a_dispatch(xr, idx_l, T, K, E, d, C, rank, G, peers, ep_epoch, l, compute), "ep dispatch");
+        ck(moek_ep_a2a_wait(ep_buf, 0, G, C, d, ep_epoch, l, compute), "ep wait rows");
+        const int32_t* meta = reinterpret_cast<const int32_t*>(ep_buf + moek_ep_a2a_offset(G, C, d, 1));
+        const void* rows = ep_buf + moek_ep_a2a_offset(G, C, d, 0);
+        ck(moek_ep_a2a_keys(meta, Tp, E, ep_keys, compute), "ep keys");
+        ck(moek_permute(ep_keys, Tp, E + 1, 1, ep_counts, ep_offsets, ep_perm, ep_inv, compute), "ep permute");
+        const moe_expert_weights* lw = weights.data() + static_cast<size_t>(l) * E;
+        if (T <= ep_Tgemv) {
+            // received rows (G sparse regions of C entries) in slot order,
+            // then the GEMV with the identity permutation over them
+            const int Tg = G * ep_Tgemv * K;
+            ck(moek_ep_a2a_gather(rows, ep_perm, ep_offsets, E, d, Tg, ep_dense, compute), "ep gather");
+            ck(moek_ffn_mma(ep_gws, ep_dense, ep_iota, ep_offsets, ep_iota, nullptr, nullptr, Tg, 1, lw, E, d, f,
+                            mine_mask(), nullptr, ep_y, MOE_X_PERMUTE, compute),
+               "ep ffn");
+        } else {
+            ck(moek_ffn_tc(ep_tcws, rows, ep_perm, ep_offsets, Tp, 1, lw, E, d, f, mine_mask(), ep_y, compute), "ep ffn_tc");
+        }
+        ck(moek_ep_a2a_return(ep_y, ep_perm, ep_offsets, E, d, C, rank, G, peers, ep_epoch, l, compute), "ep return");
+        ck(moek_ep_a2a_wait(ep_buf, 1, G, C, d, ep_epoch, l, compute), "ep wait returns");
+        const float* ret = reinterpret_cast<const float*>(ep_buf + moek_ep_a2a_offset(G, C, d, 2));
+        ck(moek_combine(ret, ep_iota, w_l, x, T, d, K, out, compute), "ep combine");
+    }
+
     void run_layers(int T) {
+        if (ep) {
+            if (static_cast<int>(ep_peers.size()) != G) throw UsageError("expert-parallel engine: ep_set_peers first");
+            const uint16_t* src = xin;
+            const size_t TK = static_cast<size_t>(Tmax) * K;
+            for (int l = 0; l < L; ++l) {
+                uint16_t* dst = l == L - 1 ? xout : xbuf[l & 1];
+                ep_layer(l, src, T, dst, idx + l * TK, wts + l * TK);
+                src = dst;
+            }
+            ck(moek_ep_a2a_bump(ep_epoch, L, compute), "ep epoch");
+            return;
+        }
         if (use_fused(T)) {
             launch_fused();
             counters.activations += static_cast<int64_t>(T) * K * L;
@@ -863,6 +1002,23 @@ void MoeEngine::synth_input(int step, int T) {
     if (T < 1 || T > impl_->Tmax) throw ValidationError("T must be in [1, max_tokens]");
     ck(moek_synth_input(impl_->cfg.seed, uid_input(step), static_cast<long long>(T) * impl_->d, impl_->xin,
                         impl_->compute), "synth input");
+}
+
+void* MoeEngine::ep_buffer(size_t* bytes) {
+    if (bytes) *bytes = impl_->ep_bytes;
+    return impl_->ep_buf;
+}
+
+void MoeEngine::ep_set_peers(const void* const* bases, int world) {
+    Impl& m = *impl_;
+    if (!m.ep) throw UsageError("ep_set_peers: the engine is not expert-parallel (ep_world = 1)");
+    if (world != m.G || bases == nullptr) throw UsageError("ep_set_peers: expected " + std::to_string(m.G) + " buffer bases");
+    if (bases[m.rank] != m.ep_buf) throw UsageError("ep_set_peers: bases[ep_rank] must be this engine's own ep_buffer");
+    for (int r = 0; r < world; ++r)
+        if (bases[r] == nullptr) throw UsageError("ep_set_peers: null base for rank " + std::to_string(r));
+    m.ep_peers.assign(bases, bases + world);
+    for (auto& g : m.graphs) cudaGraphExecDestroy(g.second);  // captured with the old bases
+    m.graphs.clear();
 }
 
 void MoeEngine::decode(int T) {

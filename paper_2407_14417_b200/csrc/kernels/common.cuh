@@ -208,6 +208,12 @@ MOE_DEVI float warp_sum(float v) {
 
 MOE_DEVI float silu_f(float g) { return g / (1.0f + expf(-g)); }
 
+#define MOE_CUDA_OK_PRELOAD(expr)                           \
+    do {                                                    \
+        cudaError_t err__ = (expr);                         \
+        if (err__ != cudaSuccess) return err__;             \
+    } while (0)
+
 #define MOE_CUDA_OK(expr)                                   \
     do {                                                    \
         cudaError_t err__ = (expr);                         \

@@ -1575,3 +1575,18 @@ cudaError_t moek_ffn_mma(const GemvWorkspace& ws, const void* x, const int32_t* 
 }
 
 MOE_NUMERICS_BINDER(gemv)
+
+// Loads this unit's kernels now (cudaFuncGetAttributes).  Under lazy module
+// loading (CUDA 12 default) a kernel's first launch may wait for the device
+// to idle; the expert-parallel step has kernels that spin on a peer's flags,
+// so every kernel it can launch must be resident before the first step.
+cudaError_t moek_preload_gemv() {
+    cudaFuncAttributes fa;
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::stream_kernel<moek::CfgBatch>));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::stream_kernel<moek::CfgDecode>));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::finalize_h_kernel));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::finalize_out_kernel));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::permute_rows_kernel));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::decode_step_kernel<moek::CfgDecode>));
+    return cudaSuccess;
+}

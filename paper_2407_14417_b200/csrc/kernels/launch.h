@@ -105,6 +105,27 @@ cudaError_t moek_unpack_bf16_blocks(const void* in, int rows, int cols, void* w,
 cudaError_t moek_pack_bf16_blocks(const void* w, int rows, int cols, void* out, cudaStream_t stream);
 cudaError_t moek_quantize_blocks(const void* w, int rows, int cols, uint32_t* qb, void* sb,
                                  cudaStream_t stream);
+// Expert-parallel all-to-all of routed rows over peer memory (ep_a2a.cu).
+size_t moek_ep_a2a_bytes(int G, int C, int d);
+size_t moek_ep_a2a_offset(int G, int C, int d, int which);  // 0 rows, 1 meta, 2 ret, 3 flags
+cudaError_t moek_ep_a2a_dispatch(const void* xn, const int32_t* idx, int T, int k, int E, int d, int C, int rank,
+                                 int G, const void* const* bases, const uint32_t* epoch_base, int layer,
+                                 cudaStream_t stream);
+cudaError_t moek_ep_a2a_wait(const void* my_base, int which, int G, int C, int d, const uint32_t* epoch_base,
+                             int layer, cudaStream_t stream);
+cudaError_t moek_ep_a2a_keys(const int32_t* meta, int n, int E, int32_t* keys, cudaStream_t stream);
+cudaError_t moek_ep_a2a_return(const float* y, const int32_t* perm, const int32_t* offsets, int E, int d, int C,
+                               int rank, int G, const void* const* bases, const uint32_t* epoch_base, int layer,
+                               cudaStream_t stream);
+cudaError_t moek_ep_a2a_gather(const void* rows, const int32_t* perm, const int32_t* offsets, int E, int d,
+                               int max_rows, void* dense, cudaStream_t stream);
+cudaError_t moek_ep_a2a_bump(uint32_t* epoch_base, int L, cudaStream_t stream);
+// every kernel resident before the first expert-parallel step (lazy loading)
+cudaError_t moek_preload_gemv();
+cudaError_t moek_preload_router();
+cudaError_t moek_preload_misc();
+cudaError_t moek_preload_tc();
+cudaError_t moek_preload_ep();
 cudaError_t moek_combine(const float* y, const int32_t* inv, const float* w, const void* res, int T,
                          int d, int k, void* out, cudaStream_t stream);
 cudaError_t moek_quantize(const void* w, int rows, int cols, uint32_t* q, void* s, cudaStream_t stream);

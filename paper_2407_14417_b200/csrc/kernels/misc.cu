@@ -305,3 +305,15 @@ cudaError_t moek_synth_input(uint64_t seed, uint64_t uid, long long n, void* out
         moek::synth_key(seed, uid), n, static_cast<uint16_t*>(out));
     return cudaGetLastError();
 }
+
+// Loads this unit's kernels now (cudaFuncGetAttributes).  Under lazy module
+// loading (CUDA 12 default) a kernel's first launch may wait for the device
+// to idle; the expert-parallel step has kernels that spin on a peer's flags,
+// so every kernel it can launch must be resident before the first step.
+cudaError_t moek_preload_misc() {
+    cudaFuncAttributes fa;
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::combine_kernel));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::combine_partial_kernel));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::residual_add_kernel));
+    return cudaSuccess;
+}

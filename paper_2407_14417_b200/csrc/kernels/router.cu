@@ -288,3 +288,14 @@ cudaError_t moek_debug_layer_trace_router(void* host_ptr, cudaStream_t stream) {
 }
 
 MOE_NUMERICS_BINDER(router)
+
+// Loads this unit's kernels now (cudaFuncGetAttributes).  Under lazy module
+// loading (CUDA 12 default) a kernel's first launch may wait for the device
+// to idle; the expert-parallel step has kernels that spin on a peer's flags,
+// so every kernel it can launch must be resident before the first step.
+cudaError_t moek_preload_router() {
+    cudaFuncAttributes fa;
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::route_kernel));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::permute_kernel));
+    return cudaSuccess;
+}

@@ -587,3 +587,15 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
 }
 
 MOE_NUMERICS_BINDER(tc)
+
+// Loads this unit's kernels now (cudaFuncGetAttributes).  Under lazy module
+// loading (CUDA 12 default) a kernel's first launch may wait for the device
+// to idle; the expert-parallel step has kernels that spin on a peer's flags,
+// so every kernel it can launch must be resident before the first step.
+cudaError_t moek_preload_tc() {
+    cudaFuncAttributes fa;
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_kernel<128>));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_kernel<256>));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::gather_rows_kernel));
+    return cudaSuccess;
+}
