@@ -674,93 +674,129 @@ def reconfig_sweep(moe, torch, args, device):
             "transitions": rows}
 
 
+def _max_over_ranks(dist, v: float) -> float:
+    import torch
+    t = torch.tensor([v], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ep(args, rank, world, device):
-    """Expert-parallel decode over `world` GPUs (paper_2407_14417_b200/ep.py):
-    experts of every layer sharded (slot s -> rank s*world//8), T_local tokens
-    per rank (weak scaling), all-gather dispatch + reduce-scatter combine over
-    NCCL.  Timed with CUDA events between barriers, max over ranks."""
+    """Expert-parallel decode over `world` ranks: every rank's
+    MoeEngine holds only its slots of each layer (slot s -> rank s*world//8)
+    and T_local tokens (weak scaling); each layer sends only the routed token
+    rows to their experts' owners and gets the outputs back over peer memory
+    (ep_a2a.cu: NVLink P2P between GPUs, CUDA IPC handles), all inside the
+    engine's graph-captured decode step.  torch.distributed (gloo) only
+    carries the IPC handles, barriers and the max over ranks.  Timed with CUDA
+    events on the engine stream between barriers, max over ranks.  Ranks may
+    share a GPU (a 1-GPU box running --gpus 2): the exchange then crosses
+    process contexts on one device -- correct, but time-sliced, so such a
+    line measures the protocol, not NVLink."""
     import torch
     import torch.distributed as dist
     import paper_2407_14417_b200 as moe
-    from paper_2407_14417_b200 import ep
     prof = moe.profile_for_shape(D_MODEL, D_FFN, LAYERS, EXPERTS, TOPK)
     plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, args.n4, 0), moe.HardwareProfile(10**15), prof)
     T_local = args.tokens
-    T = T_local * world
-    # identical synthetic weights on every rank (each rank reads only its shard)
-    eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan, max_tokens=T, seed=args.seed, device=device,
-                        norm_eps=NORM_EPS)
-    ops = ep.EngineOps(moe, torch, eng, rank, world, T, NORM_EPS, torch.device(f"cuda:{device}"))
-    # exchange: the library's C-ABI NCCL path (moe_ep_dispatch / moe_ep_combine, default),
-    # the fused peer-memory kernels over CUDA IPC (--ep-exchange peer), or
-    # torch.distributed's collectives (--ep-exchange torch)
-    if args.ep_exchange == "torch":
-        exch = None
-    elif args.ep_exchange == "peer":
-        exch = ep.PeerExchange(moe, torch, rank, world, T_local, D_MODEL, torch.device(f"cuda:{device}"), dist=dist)
-    else:
-        exch = ep.CapiExchange(moe, dist, rank, world, device, ops._stream)
-    dec = ep.ExpertParallelDecoder(dist, ops, rank, world, T_local, EXPERTS, exchange=exch)
-    eng.synth_input(0, T)
+    eng = moe.MoeEngine(LAYERS, EXPERTS, TOPK, D_MODEL, D_FFN, plan, max_tokens=T_local, seed=args.seed,
+                        device=device, norm_eps=NORM_EPS, tc_min_tokens=args.tc_min, ep_rank=rank, ep_world=world)
+    base, _ = eng.ep_buffer()
+    handles = [None] * world
+    dist.all_gather_object(handles, moe.ep_peer_ipc_handle(base))
+    eng.ep_set_peers([base if r == rank else moe.ep_peer_ipc_open(handles[r]) for r in range(world)])
+    shared_gpu = world > torch.cuda.device_count()
+    n_in = 8
+    for w in range(args.warmup):
+        eng.synth_input(1000 + rank * n_in + (w % n_in), T_local)
+        eng.decode(T_local)
     eng.sync()
-    x_all = torch.as_tensor(_DevBytes(eng.input_ptr, T * D_MODEL * 2), device=f"cuda:{device}").view(torch.int16)
-    x_local = x_all[rank * T_local * D_MODEL:(rank + 1) * T_local * D_MODEL].clone()
-    for _ in range(args.warmup):
-        dec.decode(x_local)
-    torch.cuda.synchronize()
     dist.barrier()
-    stream = torch.cuda.current_stream()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps = max(5, min(args.steps, 50))
+    steps = max(5, min(args.steps, 10 if shared_gpu else 100))
+    stream = torch.cuda.ExternalStream(eng.stream_ptr)
+    ms_total = 0.0
     with ClockSampler(device) as clk:
-        start.record(stream)
-        for _ in range(steps):
-            dec.decode(x_local)
-        end.record(stream)
-        end.synchronize()
+        per = max(1, steps // n_in)
+        done = 0
+        for i in range(n_in):
+            k = per if i < n_in - 1 else steps - done
+            if k <= 0:
+                break
+            eng.synth_input(1000 + rank * n_in + i, T_local)
+            eng.decode(T_local)  # this input's first step, untimed
+            eng.sync()
+            start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            start.record(stream)
+            for _ in range(k):
+                eng.decode(T_local)
+            end.record(stream)
+            end.synchronize()
+            ms_total += start.elapsed_time(end)
+            done += k
     clocks = clk.summary()
-    ms = start.elapsed_time(end) / steps
-    t = torch.tensor([ms], device=f"cuda:{device}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    # e2e: pinned host rows in, output rows back, every step
-    xh = x_local.cpu().pin_memory()
+    ms = _max_over_ranks(dist, ms_total / done)
+    # per-rank algorithmic bytes of the last step: the distinct experts of this
+    # rank's slots selected by any rank's tokens, per layer
+    routes = [None] * world
+    dist.all_gather_object(routes, eng.last_routing(T_local))
+    sel = [set() for _ in range(LAYERS)]
+    for r in range(world):
+        for t in range(T_local):
+            for l in range(LAYERS):
+                for j in range(TOPK):
+                    sel[l].add(routes[r][(t * LAYERS + l) * TOPK + j])
+    b16, b4 = moe.expert_size(prof, moe.MOE_P16), moe.expert_size(prof, moe.MOE_P4)
+    prec = plan.precision
+    mine = [s for s in range(EXPERTS) if s * world // EXPERTS == rank]
+    my_bytes = sum((b16 if prec[l * EXPERTS + s] == moe.MOE_P16 else b4) for l in range(LAYERS) for s in sel[l]
+                   if s in mine)
+    max_bytes = _max_over_ranks(dist, float(my_bytes))
+    # e2e through the public API: pinned host tokens in, output back, every step
+    xh = torch.empty(T_local * D_MODEL, dtype=torch.int16).pin_memory()
     oh = torch.empty_like(xh).pin_memory()
-    xd = torch.empty_like(x_local)
+    eng.synth_input(1000 + rank * n_in, T_local)
+    eng.sync()
+    xh.copy_(torch.as_tensor(_DevBytes(eng.input_ptr, T_local * D_MODEL * 2), device=f"cuda:{device}").view(torch.int16).cpu())
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
-        xd.copy_(xh, non_blocking=True)
-        out = dec.decode(xd)
-        oh.copy_(out, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-    e2e_s = (time.perf_counter() - t0) / steps
-    t = torch.tensor([e2e_s], device=f"cuda:{device}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_s = float(t.item())
+        eng.decode_host(xh.data_ptr(), T_local, oh.data_ptr())
+    e2e_s = _max_over_ranks(dist, (time.perf_counter() - t0) / steps)
+    mem = eng.memory()
+    expert_gb = _max_over_ranks(dist, mem["expert_bytes"] / 1e9)
     eng.close()
     if rank == 0:
-        xb = ep.exchange_bytes(T_local, world, D_MODEL)
+        peak, peak_kind = peaks()
+        achieved = max_bytes / (ms * 1e-3) / 1e9
         line = {
             "metric": METRIC, "value": round(world * T_local * 1000.0 / ms, 3), "unit": "tokens/s", "n_gpus": world,
-            "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "steps": done, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16 / int4-g128 weights, bf16 activations, fp32 accumulate",
             "data": "synthetic (seeded counter-based generator)",
             "config": {"workload": "mixtral8x7b-shape 32-layer MoE stack, expert-parallel batch-%d/GPU decode" % T_local,
                        "n4": args.n4, "of": LAYERS * EXPERTS, "layer": "x + MoE(RMSNorm(x))",
-                       "parallelism": "ep%d" % world, "experts_per_gpu_per_layer": EXPERTS // world if world <= EXPERTS else 1,
-                       "exchange": {"torch": "NCCL all-gather + reduce-scatter per layer via torch.distributed",
-                                    "capi": "NCCL all-gather + reduce-scatter per layer via the C ABI "
-                                            "(moe_ep_dispatch / moe_ep_combine)",
-                                    "peer": "fused peer-memory kernels over CUDA IPC (moe_ep_push_rows / "
-                                            "moe_ep_push_shares / moe_ep_reduce), no collective"}[args.ep_exchange],
-                       "exchange_bytes_per_layer_per_gpu": xb, "batch_per_gpu": T_local,
+                       "parallelism": "ep%d" % world, "experts_per_gpu_per_layer": len(mine),
+                       "expert_gb_per_gpu": round(expert_gb, 3),
+                       "exchange": "routed-row all-to-all over peer memory inside the engine step (ep_a2a.cu): "
+                                   "dispatch 2*d B per routed (token, expert), return 4*d B",
+                       "exchange_bytes_per_layer_per_gpu": {"dispatch": T_local * TOPK * D_MODEL * 2,
+                                                            "return": T_local * TOPK * D_MODEL * 4},
+                       "ranks_share_gpu": shared_gpu, "batch_per_gpu": T_local,
+                       "inputs": "8 distinct synthetic token inputs per rank",
                        "l2": "no flush: every step streams GBs of distinct expert weights per GPU"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "what": "busiest rank's selected-expert bytes per step / step time (exchange and routing "
+                                 "included in the time)"},
             "e2e": {"value": round(world * T_local / e2e_s, 3), "unit": "tokens/s",
-                    "h2d_bytes_per_step": world * T_local * D_MODEL * 2, "d2h_bytes_per_step": world * T_local * D_MODEL * 2},
-            # per layer: route, permute_rows, 2 streams, 2 finalizes, combine_partial, residual_add
-            "gpu_launches": 8 * LAYERS * steps, "clocks": clocks, "cpu_baseline": None,
-            "note": "expert parallel (not replicas): every GPU computes only its slots of each layer",
+                    "h2d_bytes_per_step": world * T_local * D_MODEL * 2, "d2h_bytes_per_step": world * T_local * D_MODEL * 2,
+                    "how": "moe_engine_decode_host per rank (pinned H2D, step, D2H, sync), max over ranks"},
+            # per layer: route, dispatch, wait, keys, permute, (gather), FFN (permute_rows, 2 streams, 2 finalizes
+            # or gather + 2 tcgen05 + ...), return, wait, combine; + 1 epoch bump per step
+            "gpu_launches": (13 * LAYERS + 1) * done, "clocks": clocks, "cpu_baseline": None,
+            "note": "expert parallel (not replicas): every GPU holds and computes only its slots of each layer",
         }
         print(json.dumps(line), flush=True)
 
@@ -784,9 +820,6 @@ def main():
                     default=[0, 32, 64, 96, 128, 160, 192, 224, 256])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of expert parallel")
-    ap.add_argument("--ep", action="store_true", help="expert-parallel code path even at N=1 (NCCL, 1 rank)")
-    ap.add_argument("--ep-exchange", choices=["capi", "peer", "torch"], default="capi",
-                    help="EP exchange: C-ABI NCCL (default), fused peer-memory kernels, or torch.distributed")
     ap.add_argument("--no-batch-sweep", dest="batch_sweep", action="store_false")
     ap.add_argument("--tc-min", type=int, default=32, help="batch-sweep engine: tcgen05 expert GEMM from this T")
     ap.add_argument("--batch-points", type=lambda s: [int(v) for v in s.split(",")] if s else [],
@@ -832,20 +865,21 @@ def main():
         run_reference(args, rank, world)
         return
     import torch
+    ndev = max(1, torch.cuda.device_count())
+    local = local % ndev  # more ranks than GPUs (a 1-GPU box running --gpus 2): ranks share devices
     torch.cuda.set_device(local)
+    ep_mode = world > 1 and not args.replicas
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    if (world > 1 and not args.replicas) or args.ep:
-        if world == 1:
-            import torch.distributed as dist
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29533")
-            dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(f"cuda:{local}"))
+        # the expert-parallel exchange is the engine's own (peer memory); the
+        # process group only carries handles / barriers / maxima -> gloo, which
+        # also works when ranks share a GPU (NCCL refuses duplicate devices)
+        if ep_mode or world > ndev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if ep_mode:
         run_ep(args, rank, world, local)
-        if world == 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
     else:
         run_ours(args, rank, world, local)
     if world > 1:

@@ -125,7 +125,7 @@ __global__ void wait_kernel(const uint32_t* flags, int G, const uint32_t* epoch_
     if (static_cast<int>(threadIdx.x) < G) {
         const unsigned long long t0 = gtime();
         while (ld_acquire_sys(flags + threadIdx.x) < want)
-            if (gtime() - t0 > 5000000000ull) {
+            if (gtime() - t0 > 20000000000ull) {
                 printf("ep wait timeout: layer %d flag[%d]=%u want %u\n", layer, threadIdx.x, flags[threadIdx.x], want);
                 __trap();
             }

@@ -276,3 +276,74 @@ class EngineOps:
 
     def residual_add(self, x_local, mine, out_local):
         self.moe.residual_add(x_local, mine, x_local.numel(), out_local, self._stream())
+
+
+class RoutedA2ADecoder:
+    """Host mirror of the sharded engine's expert-parallel step
+    (MoeEngine with ep_world > 1, kernels/ep_a2a.cu), over torch.distributed
+    point-to-point messages, for the CPU (gloo) protocol tests.  Per layer:
+
+      1. each rank routes its own T tokens (ops.route: RMSNorm + top-k);
+      2. dispatch: entry e = t*k + j goes to the owner of expert idx[e]; every
+         rank sends each peer a fixed C = T*k entry buffer of rows + meta
+         (meta[e] = expert if that peer owns it, else -1 -- the engine writes
+         the same meta, and only the routed rows);
+      3. each owner runs its experts on the entries it received (ops.expert);
+      4. return: the output row of entry e goes back to its source at e;
+      5. combine: out[t] = bf16(x[t] + sum_j w[t,j] * y[t*k+j]) in j order.
+
+    `ops`: route(layer, x_local[T*d] uint16) -> (idx[T*k], w[T*k], xn[T][d]);
+    expert(layer, slot, rows[n][d]) -> y[n][d] fp32; combine(x_local, w, y, T)
+    -> out[T*d] uint16; num_layers, d, k, E."""
+
+    def __init__(self, dist, ops, rank: int, world: int, T_local: int):
+        self.dist, self.ops, self.rank, self.world, self.T = dist, ops, rank, world, T_local
+        self.E, self.k, self.d = ops.E, ops.k, ops.d
+        self.C = T_local * ops.k
+        self.mine = local_slots(rank, ops.E, world)
+
+    def _exchange(self, send):
+        """send[p] (one array per peer, equal shapes) -> recv[src]."""
+        torch = __import__("torch")
+        recv = [None] * self.world
+        reqs = []
+        for p in range(self.world):
+            if p == self.rank:
+                recv[p] = send[p].copy()
+                continue
+            buf = __import__("numpy").empty_like(send[p])
+            recv[p] = buf
+            reqs.append(self.dist.isend(torch.from_numpy(send[p]), p))
+            reqs.append(self.dist.irecv(torch.from_numpy(buf), p))
+        for r in reqs:
+            r.wait()
+        return recv
+
+    def layer(self, layer: int, x_local):
+        np = __import__("numpy")
+        ops, E, k, d, C, G = self.ops, self.E, self.k, self.d, self.C, self.world
+        idx, w, xn = ops.route(layer, x_local)
+        owner = [owner_of(int(s), E, G) for s in idx]
+        rows = [np.zeros((C, d), np.uint16) for _ in range(G)]
+        meta = [np.full(C, -1, np.int32) for _ in range(G)]
+        for e in range(C):
+            rows[owner[e]][e] = xn[e // k]
+            meta[owner[e]][e] = idx[e]
+        rrows, rmeta = self._exchange(rows), self._exchange(meta)
+        ret = [np.zeros((C, d), np.float32) for _ in range(G)]
+        for s in self.mine:  # this rank's experts on what it received, in (src, entry) order
+            at = [(src, e) for src in range(G) for e in range(C) if rmeta[src][e] == s]
+            if not at:
+                continue
+            y = ops.expert(layer, s, np.stack([rrows[src][e] for src, e in at]))
+            for (src, e), yr in zip(at, y):
+                ret[src][e] = yr
+        back = self._exchange(ret)
+        y_local = np.stack([back[owner[e]][e] for e in range(C)])
+        return ops.combine(x_local, w, y_local, self.T)
+
+    def decode(self, x_local, layers: Sequence[int] = None):
+        layers = range(self.ops.num_layers) if layers is None else layers
+        for l in layers:
+            x_local = self.layer(l, x_local)
+        return x_local

@@ -111,6 +111,64 @@ def _ep_worker(rank, world, port, T_local, q):
         dist.destroy_process_group()
 
 
+class OracleA2AOps:
+    """Per-rank arithmetic of the routed all-to-all mirror (ep.RoutedA2ADecoder)
+    on the CPU oracle (test-only): this rank's experts only."""
+
+    def __init__(self, orc, m, precisions, rank, world):
+        from paper_2407_14417_b200 import ep
+        self.orc, self.m, self.prec = orc, m, precisions
+        self.num_layers, self.d, self.k, self.E = m.num_layers, m.d_model, m.top_k, m.num_experts
+        self.wg = [orc.router_weights(m, l) for l in range(m.num_layers)]
+        self.ex = {}
+        for l in range(m.num_layers):
+            for s in ep.local_slots(rank, m.num_experts, world):
+                e = l * m.num_experts + s
+                self.ex[(l, s)] = orc.expert_bf16(m, e) if precisions[e] == 1 else orc.expert_int4(m, e)
+
+    def route(self, layer, x_local):
+        T = x_local.size // self.d
+        xn = self.orc.rmsnorm(x_local.reshape(T, self.d), T, self.d, self.m.norm_eps)
+        idx, w, _ = self.orc.gate_topk(xn, self.wg[layer], T, self.d, self.E, self.k)
+        return idx.reshape(-1), w.reshape(-1), xn
+
+    def expert(self, layer, s, rows):
+        w = self.ex[(layer, s)]
+        if self.prec[layer * self.E + s] == 1:
+            return self.orc.ffn_bf16(rows, len(rows), w[0], w[1], self.d, self.m.d_ffn)
+        return self.orc.ffn_int4(rows, len(rows), *w, self.d, self.m.d_ffn)
+
+    def combine(self, x_local, w, y, T):
+        inv = np.arange(T * self.k, dtype=np.int32)
+        return self.orc.combine(np.ascontiguousarray(y, np.float32), inv, np.ascontiguousarray(w, np.float32),
+                                x_local.reshape(T, self.d), T, self.d, self.k).reshape(-1)
+
+
+def _a2a_worker(rank, world, port, T_local, q):
+    import torch.distributed as dist
+
+    from oracle.oracle import OracleLib
+    from paper_2407_14417_b200 import ep
+    import paper_2407_14417_b200 as moe
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = None
+    try:
+        orc = OracleLib()
+        m = orc.model(L, E, K, D, F, SEED, EPS)
+        prof = moe.profile_for_shape(D, F, L)
+        plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 1), moe.HardwareProfile(10**15), prof)
+        dec = ep.RoutedA2ADecoder(dist, OracleA2AOps(orc, m, plan.precision, rank, world), rank, world, T_local)
+        x_all = orc.step_input(m, 5, T_local * world)
+        out = dec.decode(x_all[rank * T_local:(rank + 1) * T_local].reshape(-1).copy()).copy()
+    except Exception as exc:  # report instead of leaving the peers waiting
+        out = repr(exc)
+    finally:
+        q.put((rank, out))
+        dist.destroy_process_group()
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -281,3 +339,33 @@ def test_ep_peer_exchange_two_processes_ipc_gpu(cuda):
                         os.path.join(root, "tools", "ep_ipc_check.py")], capture_output=True, text=True, timeout=240)
     lines = [l for l in r.stdout.splitlines() if l.startswith("rank") and "err" in l]
     assert r.returncode == 0 and len(lines) == 4, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("world,T_local", [(2, 1), (2, 3), (4, 2)])
+def test_routed_a2a_gloo_matches_single_process(orc, world, T_local):
+    """The sharded engine's protocol (routed rows to owners, outputs back,
+    combine) with gloo ranks and the oracle as per-rank arithmetic equals the
+    single-process oracle stack."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_a2a_worker, args=(r, world, port, T_local, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(res[r], str), f"rank {r}: {res[r]}"
+    import paper_2407_14417_b200 as moe
+    m = orc.model(L, E, K, D, F, SEED, EPS)
+    prof = moe.profile_for_shape(D, F, L)
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 1), moe.HardwareProfile(10**15), prof)
+    T = world * T_local
+    x = orc.step_input(m, 5, T)
+    for l in range(L):
+        x, _, _, _ = orc.moe_layer(m, l, plan.precision[l * E:(l + 1) * E], x, T)
+    got = np.concatenate([res[r].reshape(T_local, D) for r in range(world)])
+    # the same per-entry arithmetic as the single process: bit-identical
+    assert np.array_equal(got, x.reshape(T, D)), "routed all-to-all (oracle arithmetic) differs from single process"
