@@ -54,7 +54,8 @@ struct TcArgs {
     uint16_t* hout16;         // pass 0: h [T*k][f] fp16
     float* y;                 // pass 1: y [T*k][d]
     uint64_t active_mask;
-    int dbg;                  // debug: bit0 skip convert, bit1 skip MMA, bit2 skip weight loads
+    int dbg;                  // debug: bit0 skip convert, bit1 skip MMA, bit2 skip weight loads,
+                              // bit5 bf16 halves as separate 2 KB reads (no pairing)
     moe_expert_weights ex[MOE_MAX_EXPERTS];
 };
 
@@ -199,6 +200,27 @@ MOE_DEVI void produce(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, 
                 bulk_g2s(dst + lane * 1024, wb + blk * 1024, 1024, bar);
                 bulk_g2s(raw + 2 * kRawA + mat * kRawS + lane * 32, sb + blk * 32, 32, bar);
             }
+        }
+    }
+}
+
+// bf16: chunks kc (even) and kc+1 = both halves of the same 4 KB blocks
+MOE_DEVI void produce_pair(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, uint8_t* raw0, uint8_t* raw1,
+                           uint64_t* bar0, uint64_t* bar1, int lane) {
+    const moe_expert_weights& W = a.ex[tl.e];
+    const int G = K / 128, g = kc >> 1;
+    if (lane == 0) {
+        mbar_expect_tx(bar0, nmat * 16384);
+        mbar_expect_tx(bar1, nmat * 16384);
+    }
+    __syncwarp();
+    for (int mat = 0; mat < nmat; ++mat) {
+        const int row0 = (a.p == 0 && mat == 1) ? a.f + tl.R0 : tl.R0;
+        const uint8_t* wb = static_cast<const uint8_t*>(a.p == 0 ? W.w_gate_up : W.w_down);
+        if (lane < 8) {
+            const size_t blk = static_cast<size_t>(row0 / 16 + lane) * G + g;
+            bulk_g2s(raw0 + mat * kRawA + lane * 2048, wb + blk * 4096, 2048, bar0);
+            bulk_g2s(raw1 + mat * kRawA + lane * 2048, wb + blk * 4096 + 2048, 2048, bar1);
         }
     }
 }
@@ -358,6 +380,14 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
             if (a.dbg & 4) {
                 if (lane == 0) mbar_arrive(&raw_full[r]);
                 __syncwarp();
+            } else if (!p4 && !(a.dbg & 32) && (kc & 1) == 0 && kc + 1 < nk) {
+                // both 64-K halves of each 4 KB bf16 block back to back: one
+                // DRAM-contiguous 4 KB read per block instead of two 2 KB
+                // reads a chunk apart
+                const int r1 = (u + 1) % nraw, pass1 = (u + 1) / nraw;
+                if (pass1 > 0) mbar_wait(&raw_empty[r1], (pass1 - 1) & 1);
+                produce_pair(a, tl, nmat, K, kc, raw(r), raw(r1), &raw_full[r], &raw_full[r1], lane);
+                ++kc;
             } else {
                 produce(a, tl, nmat, K, kc, raw(r), &raw_full[r], lane);
             }
