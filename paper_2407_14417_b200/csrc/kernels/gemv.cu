@@ -1010,6 +1010,98 @@ MOE_DEVI void sched_init(Sched& sc, unsigned int* ctr, int N, int W, int wid, in
     sc.it = Item{0, 0, 0};
 }
 
+// Batch-1 routing tail of the fused step, one warp, no serial single-thread
+// code and one barrier fewer: top-k on the E logits in registers (REDUX max
+// of order-preserving keys, lowest index among ties -- route_kernel's
+// warp_topk semantics), softmax over the selected logits in j order, the
+// T = 1 permutation (slots in expert order), and both passes' segment tables
+// (build_segs_t1's) filled by lanes 0..k-1 (gate/up) and 16..16+k-1 (down).
+MOE_DEVI uint32_t order_key(float v) {
+    const uint32_t u = __float_as_uint(v == 0.0f ? 0.0f : v);  // -0 ties with +0 (float compare)
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+template <class C>
+MOE_DEVI void route_tail_t1(const float* lg, const moe_expert_weights* ex, int E, int k, int d, int f, int lane,
+                            int32_t* topi, float* wts, int32_t* inv, SegTable& st0, SegTable& st1) {
+    const bool h0 = lane < E, h1 = lane + 32 < E;
+    const float v0 = h0 ? lg[lane] : 0.0f, v1 = h1 ? lg[lane + 32] : 0.0f;
+    uint32_t k0 = h0 ? order_key(v0) : 0u, k1 = h1 ? order_key(v1) : 0u;
+    bool a0 = h0, a1 = h1;
+    int sel[2] = {0, 0};
+    float sv[2] = {0.0f, 0.0f};
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        if (j >= k) break;
+        const uint32_t m = __reduce_max_sync(0xffffffffu, max(a0 ? k0 : 0u, a1 ? k1 : 0u));
+        const uint32_t b0 = __ballot_sync(0xffffffffu, a0 && k0 == m);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, a1 && k1 == m);
+        const int w = b0 ? __ffs(b0) - 1 : 32 + __ffs(b1) - 1;  // lowest index among the maxima
+        sel[j] = w;
+        sv[j] = __shfl_sync(0xffffffffu, w < 32 ? v0 : v1, w & 31);
+        if (w == lane) a0 = false;
+        if (w == lane + 32) a1 = false;
+    }
+    // softmax over the selected logits, sum in j order (warp_topk / the oracle)
+    float ex_[2] = {0.0f, 0.0f}, sum = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+        if (j < k) {
+            ex_[j] = expf(sv[j] - sv[0]);
+            sum += ex_[j];
+        }
+    // T = 1: slot of selection j = its rank among the selected experts
+    int pos[2] = {0, 0};
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            if (j < k && i < k && sel[i] < sel[j]) ++pos[j];
+    if (lane < k) {
+        const int j = lane;
+        topi[j] = sel[j == 0 ? 0 : 1];
+        wts[j] = ex_[j == 0 ? 0 : 1] / sum;
+        inv[j] = pos[j == 0 ? 0 : 1];
+    }
+    // segment s = the selected expert of rank s
+    const int p = lane >> 4, s = lane & 15;
+    SegTable& st = p ? st1 : st0;
+    const int rows = p ? d : 2 * f, K = p ? f : d;
+    const int RT = rows / 16, G = K / 128;
+    int e = 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+        if (j < k && pos[j] == s) e = sel[j];
+    int items = 0, gk = 1;
+    if (s < k && p < 2) {
+        const moe_expert_weights& W = ex[e];
+        gk = pick_gk<C>(G, W.precision, 1);
+        items = RT * (G / gk);
+    }
+    // prefix over the (<= 2) segments of this pass
+    const int prev = __shfl_up_sync(0xffffffffu, items, 1);
+    const int pre = s == 0 ? 0 : prev;
+    if (s < k && p < 2) {
+        const moe_expert_weights& W = ex[e];
+        st.e[s] = e;
+        st.slot0[s] = s;
+        st.mcnt[s] = 1;
+        st.kp[s] = G / gk;
+        st.gk[s] = gk;
+        st.wptr[s] = static_cast<const uint8_t*>(p == 0 ? W.w_gate_up : W.w_down);
+        st.sptr[s] = static_cast<const uint8_t*>(p == 0 ? W.s_gate_up : W.s_down);
+        st.wbytes[s] = W.precision == MOE_P4 ? gk * 1024 : gk * 4096;
+        st.sbytes[s] = W.precision == MOE_P4 ? gk * 32 : 0;
+        st.pre[s] = pre;
+#pragma unroll
+        for (int c = 0; c < kTile; ++c) st.brow[s][c] = p == 0 ? 0 : s;
+        if (s == k - 1) {
+            st.pre[k] = pre + items;
+            st.n = k;
+            st.N = pre + items;
+        }
+    }
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __grid_constant__ DecodeArgs a) {
     constexpr int kWarps = C::kWarps;
@@ -1107,10 +1199,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
         __syncthreads();
         fstamp(ftr, l, 13);
         if (warp == 0) {
-            if (lane == 0) {
-                lane_topk(lg_s, E, k, s_topi, nullptr, s_idx, s_w);
-                lane_permute(s_idx, k, E, s_counts, s_offsets, s_perm, s_inv);
-            }
+            route_tail_t1<C>(lg_s, s_ex, E, k, d, f, lane, s_topi, s_w, s_inv, st[0], st[1]);
             __syncwarp();
             if (blockIdx.x == 0 && lane < k) {
                 a.idx[static_cast<size_t>(l) * a.idx_stride + lane] = s_topi[lane];
@@ -1143,12 +1232,9 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
             }
             if (warp == 1) fstamp_lane0(ftr, l, 16);
         }
-        __syncthreads();
-        fstamp(ftr, l, 14);
-        if (tid == 0) build_segs_t1<C>(st[0], s_ex, s_offsets, E, 0, 2 * f, d);
-        if (tid == 32) build_segs_t1<C>(st[1], s_ex, s_offsets, E, 1, d, f);
         fence_proxy_async();  // scratch (generic) writes before the rings' bulk copies
         __syncthreads();
+        fstamp(ftr, l, 14);
         fstamp(ftr, l, 1);
 
         if (l + 1 < a.L && blockIdx.x < 4 && tid == 0) {  // next layer's router weights -> L2

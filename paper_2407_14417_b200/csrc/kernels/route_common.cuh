@@ -146,62 +146,4 @@ MOE_DEVI void warp_topk(const float* lg, int E, int k, int lane, int32_t* idx_ou
 }
 
 
-// Top-k of one token's logits by a single thread: k scans over the E logits
-// in index order, a candidate replaces the current best only when strictly
-// greater -- ties go to the lower index, selection in descending-logit order
-// (the same result as warp_topk, without shuffles); weights = softmax over
-// the selected logits, sum in j order.
-MOE_DEVI void lane_topk(const float* lg, int E, int k, int32_t* idx_out, float* w_out, int* s_idx, float* s_w) {
-    uint64_t used = 0;
-    float sel[MOE_MAX_TOPK];
-    int sid[MOE_MAX_TOPK];
-    for (int j = 0; j < k; ++j) {
-        int best = -1;
-        float bv = 0.0f;
-        for (int e = 0; e < E; ++e) {
-            if ((used >> e) & 1ull) continue;
-            const float v = lg[e];
-            if (best < 0 || v > bv) {
-                best = e;
-                bv = v;
-            }
-        }
-        used |= 1ull << best;
-        sel[j] = bv;
-        sid[j] = best;
-    }
-    float ex[MOE_MAX_TOPK];
-    float sum = 0.0f;
-    for (int j = 0; j < k; ++j) {
-        ex[j] = expf(sel[j] - sel[0]);
-        sum += ex[j];
-    }
-    for (int j = 0; j < k; ++j) {
-        const float w = ex[j] / sum;
-        if (idx_out) idx_out[j] = sid[j];
-        if (w_out) w_out[j] = w;
-        s_idx[j] = sid[j];
-        if (s_w) s_w[j] = w;
-    }
-}
-
-// warp_permute's stable counting sort by one thread (n <= MOE_MAX_TOPK).
-MOE_DEVI void lane_permute(const int32_t* idx, int n, int E, int32_t* counts, int32_t* offsets, int32_t* perm,
-                           int32_t* inv_perm) {
-    for (int e = 0; e < E; ++e) counts[e] = 0;
-    for (int i = 0; i < n; ++i) ++counts[idx[i]];
-    int acc = 0;
-    for (int e = 0; e < E; ++e) {
-        offsets[e] = acc;
-        acc += counts[e];
-    }
-    offsets[E] = n;
-    for (int i = 0; i < n; ++i) {
-        int pos = offsets[idx[i]];
-        for (int j = 0; j < i; ++j) pos += idx[j] == idx[i];
-        perm[pos] = i;
-        inv_perm[i] = pos;
-    }
-}
-
 }  // namespace moek
