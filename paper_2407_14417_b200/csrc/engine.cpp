@@ -182,6 +182,10 @@ struct MoeEngine::Impl {
     moe_expert_weights* dev_experts = nullptr;  // [L*E] device copy of `weights`
     unsigned int* fused_ctl = nullptr;          // [L*2 tail-pool counters][2 barrier words]
     bool fused_ok = false;
+    unsigned int* flow_ctl = nullptr;           // decode_flow_kernel's per-layer completion counters
+    float* flow_part = nullptr;                 // its partial buffers (sentinel-filled between uses)
+    size_t flow_part0_floats = 0;
+    bool flow_ok = false;                       // dataflow variant (default; MOE_FUSED=step: grid barriers)
 
     // expert parallelism (ep_a2a.cu): G ranks, this one owns slots s*G/E == rank
     bool ep = false;
@@ -370,6 +374,21 @@ struct MoeEngine::Impl {
             dev_alloc(reinterpret_cast<void**>(&fused_ctl), (static_cast<size_t>(L) * 2 + 2) * 4);
             ck(cudaMemsetAsync(fused_ctl, 0, (static_cast<size_t>(L) * 2 + 2) * 4, compute), "memset");
             fused_ok = true;
+            int dev = 0, sms = 0;
+            ck(cudaGetDevice(&dev), "cudaGetDevice");
+            ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+            const char* mode = getenv("MOE_FUSED");
+            if ((mode == nullptr || std::string(mode) != "step") && moek_decode_flow_supported(E, K, d, f, sms)) {
+                const size_t words = moek_decode_flow_ctl_words(L, K, d, f);
+                dev_alloc(reinterpret_cast<void**>(&flow_ctl), words * 4);
+                ck(cudaMemsetAsync(flow_ctl, 0, words * 4, compute), "memset");
+                // [d/128][K][2f] gate/up + [f/128][K][d] down partials, 0xffffffff = none pending
+                flow_part0_floats = static_cast<size_t>(d / 128) * K * 2 * f;
+                const size_t pf = flow_part0_floats + static_cast<size_t>(f / 128) * K * d;
+                dev_alloc(reinterpret_cast<void**>(&flow_part), pf * 4);
+                ck(cudaMemsetAsync(flow_part, 0xff, pf * 4, compute), "memset");
+                flow_ok = true;
+            }
         }
         ck(cudaHostAlloc(reinterpret_cast<void**>(&idx_host), TK * 4, cudaHostAllocDefault), "cudaHostAlloc");
 
@@ -418,7 +437,14 @@ struct MoeEngine::Impl {
         a.bar = reinterpret_cast<unsigned long long*>(fused_ctl + static_cast<size_t>(L) * 2);
         static const int bar_mode = getenv("MOE_BAR_MODE") ? atoi(getenv("MOE_BAR_MODE")) : 0;
         a.bar_mode = bar_mode;
-        ck(moek_decode_step(a, compute), "decode_step");
+        a.flow_ctl = flow_ctl;
+        if (flow_ok) {
+            a.part0 = flow_part;
+            a.part1 = flow_part + flow_part0_floats;
+            ck(moek_decode_flow(a, compute), "decode_flow");
+        } else {
+            ck(moek_decode_step(a, compute), "decode_step");
+        }
     }
 
     // Synthetic weights: bf16 masters from the counter-based generator,
@@ -614,7 +640,7 @@ struct MoeEngine::Impl {
         if (master_arena) cudaFreeHost(master_arena);
         if (copy) cudaStreamSynchronize(copy);
         void* devp[] = {tcws, xn, dev_arena, swap, wg, xin, xout, xbuf[0], xbuf[1], idx, wts, counts, offsets, perm, inv, ticket, y,
-                         gws_base, dev_experts, fused_ctl, ep_buf, ep_epoch, ep_keys, ep_counts, ep_offsets, ep_perm,
+                         gws_base, dev_experts, fused_ctl, flow_ctl, flow_part, ep_buf, ep_epoch, ep_keys, ep_counts, ep_offsets, ep_perm,
                          ep_inv, ep_iota, ep_y, ep_gws_base, ep_tcws, ep_dense};
         for (void* p : devp)
             if (p) cudaFree(p);

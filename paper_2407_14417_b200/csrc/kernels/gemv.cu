@@ -34,6 +34,7 @@
 // the per-128-K-group scale is applied after the group's integer-exact dot,
 // y += s * sum(q*x) -- the exact dequant values q*s.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -705,20 +706,10 @@ constexpr int kFinOThreads = kFinOQuads * kKG;
 // up rows (q >= 32); h rounded to bf16 goes out as the K-permuted bf16 copy,
 // its exact fp16 copy and the group's int4 bias term.  Shared by
 // finalize_h_kernel and the fused decode-step kernel (identical arithmetic).
-MOE_DEVI void swiglu_unit(const float4 (&red)[kKG][64], uint16_t* hs, int slot, int g, int f, uint16_t* __restrict__ hperm,
-                          uint16_t* __restrict__ hperm16, float* __restrict__ hsum, int hstride, int lane) {
-    float gv[4], uv[4];
-    {
-        float4 a = red[0][lane], b = red[0][32 + lane];
-#pragma unroll
-        for (int k2 = 1; k2 < kKG; ++k2) {
-            const float4 c = red[k2][lane], e = red[k2][32 + lane];
-            a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
-            b.x += e.x; b.y += e.y; b.z += e.z; b.w += e.w;
-        }
-        gv[0] = a.x; gv[1] = a.y; gv[2] = a.z; gv[3] = a.w;
-        uv[0] = b.x; uv[1] = b.y; uv[2] = b.z; uv[3] = b.w;
-    }
+// gv / uv: this lane's 4 summed gate rows g*128+4*lane.. and up rows.
+MOE_DEVI void swiglu_store(const float (&gv)[4], const float (&uv)[4], uint16_t* hs, int slot, int g, int f,
+                           uint16_t* __restrict__ hperm, uint16_t* __restrict__ hperm16, float* __restrict__ hsum,
+                           int hstride, int lane) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) hs[lane * 4 + j] = f2bf(silu_f(gv[j]) * uv[j]);
     __syncwarp();
@@ -738,6 +729,23 @@ MOE_DEVI void swiglu_unit(const float4 (&red)[kKG][64], uint16_t* hs, int slot, 
     }
     if (lane == 0) hsum[static_cast<size_t>(slot) * hstride + g] = int4_bias_term(s_lo, s_hi);
     __syncwarp();
+}
+
+MOE_DEVI void swiglu_unit(const float4 (&red)[kKG][64], uint16_t* hs, int slot, int g, int f, uint16_t* __restrict__ hperm,
+                          uint16_t* __restrict__ hperm16, float* __restrict__ hsum, int hstride, int lane) {
+    float gv[4], uv[4];
+    {
+        float4 a = red[0][lane], b = red[0][32 + lane];
+#pragma unroll
+        for (int k2 = 1; k2 < kKG; ++k2) {
+            const float4 c = red[k2][lane], e = red[k2][32 + lane];
+            a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+            b.x += e.x; b.y += e.y; b.z += e.z; b.w += e.w;
+        }
+        gv[0] = a.x; gv[1] = a.y; gv[2] = a.z; gv[3] = a.w;
+        uv[0] = b.x; uv[1] = b.y; uv[2] = b.z; uv[3] = b.w;
+    }
+    swiglu_store(gv, uv, hs, slot, g, f, hperm, hperm16, hsum, hstride, lane);
 }
 
 __global__ void __launch_bounds__(kFinHThreads) finalize_h_kernel(
@@ -1439,6 +1447,703 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
         }
     }
 }
+
+// ===========================================================================
+// Dataflow batch-1 decode step (decode_flow_kernel): the whole L-layer stack
+// in one cooperative launch like decode_step_kernel, with its intra-layer
+// grid barriers replaced by data readiness, so HBM streams through the
+// gate/up -> SwiGLU -> down hand-off without a gap:
+//   * items of both passes are dealt round-robin (item i -> warp i mod W,
+//     warps numbered SM-fastest) in h-chunk order: the gate/up items of h
+//     chunk c (8 SwiGLU units of 128 h rows) precede those of chunk c+1, and
+//     a warp runs straight from its last gate/up item into its down items;
+//     each lane decodes one of the warp's next 32 items, so the per-item cost
+//     is two shuffles;
+//   * streaming warps only store their fp32 partials: no counters, no
+//     fences.  The partial buffers hold a sentinel (0xffffffff, a NaN no
+//     arithmetic produces) wherever no partial is pending;
+//   * a ninth "finisher" warp per CTA owns the SwiGLU units and 16-row output
+//     tiles of index = blockIdx mod gridDim.  It polls a unit's last partial,
+//     then loads them all; once none is the sentinel it runs the SwiGLU
+//     (h rows -> global), puts the sentinel back and release-increments the
+//     unit's h-chunk counter.  It polls every h-chunk counter and bulk-copies
+//     each complete chunk into the CTA's resident h rows (one mbarrier per
+//     chunk, which the down items wait on), and finishes its output tiles the
+//     same way (combine + residual -> x(l+1), then the layer's x-ready counter);
+//   * a layer starts when the previous layer's x-ready counter is full.
+// Sums, SwiGLU and combine are the K-part orders of finalize_h /
+// finalize_out (sum_kparts, swiglu_store), so the output is bit-identical to
+// the per-layer kernels.  Counters live per layer in a.flow_ctl; the last
+// CTA to finish zeroes them for the next step.
+constexpr int kFlowStage = 8192 + 256;             // ring stage: one 8 KB item + its int4 scales
+constexpr int kFlowMaxChunks = 16;                    // 1024-row h chunks per slot (f <= 16384)
+constexpr uint32_t kFlowSentinel = 0xffffffffu;       // "no partial here" (memset 0xff)
+
+struct FlowTab {
+    const uint8_t* w[2][2];   // [pass][slot] fragment blocks of the slot's expert
+    const uint8_t* sc[2][2];  // int4 scales
+    int gk[2][2];             // 128-K groups per item
+    int kp[2][2];             // K-parts per row tile
+    int p4[2];                // slot's expert is int4
+    int U[2];                 // gate/up items per SwiGLU unit: 16 row tiles x kp[0][s]
+    int N0, N1;               // items per pass
+    int stride0, stride1;     // items per full chunk
+};
+
+struct FItem {
+    int pass, s, rt, kp, c;
+};
+
+MOE_DEVI FItem flow_item(const FlowTab& T, int i, int Gf, int f16, int RT1) {
+    FItem it;
+    if (i < T.N0) {  // chunk c, slot s, unit u of the chunk, tile t16 (8 gate, 8 up), K-part
+        const int c = i / T.stride0;
+        int r = i - c * T.stride0;
+        const int nu = min(8, Gf - 8 * c);
+        const int s = r < nu * T.U[0] ? 0 : 1;
+        if (s) r -= nu * T.U[0];
+        const int u = r / T.U[s];
+        const int r2 = r - u * T.U[s];
+        const int kp = T.kp[0][s];
+        const int t16 = r2 / kp;
+        const int g = 8 * c + u;
+        it.pass = 0;
+        it.s = s;
+        it.kp = r2 - t16 * kp;
+        it.c = c;
+        it.rt = t16 < 8 ? g * 8 + t16 : f16 + g * 8 + (t16 - 8);
+    } else {  // chunk c, slot s, output tile rt, K-part of the chunk
+        const int j = i - T.N0;
+        const int c = j / T.stride1;
+        int r = j - c * T.stride1;
+        const int nu = min(8, Gf - 8 * c);
+        const int nk0 = nu / T.gk[1][0];
+        const int s = r < nk0 * RT1 ? 0 : 1;
+        if (s) r -= nk0 * RT1;
+        const int nk = s ? nu / T.gk[1][1] : nk0;
+        const int rt = r / nk;
+        it.pass = 1;
+        it.s = s;
+        it.rt = rt;
+        it.c = c;
+        it.kp = (8 * c) / T.gk[1][s] + (r - rt * nk);
+    }
+    return it;
+}
+// packed: w0 = rt | kp << 16, w1 = pass | s << 1 | c << 2 (w1 < 0: no item)
+MOE_DEVI void flow_pack(const FItem& it, int& w0, int& w1) {
+    w0 = it.rt | (it.kp << 16);
+    w1 = it.pass | (it.s << 1) | (it.c << 2);
+}
+MOE_DEVI FItem flow_unpack(int w0, int w1) {
+    FItem it;
+    it.rt = w0 & 0xffff;
+    it.kp = w0 >> 16;
+    it.pass = w1 & 1;
+    it.s = (w1 >> 1) & 1;
+    it.c = w1 >> 2;
+    return it;
+}
+
+template <class C>
+MOE_DEVI void flow_issue(const FlowTab& T, const FItem& it, int K, uint8_t* stage, uint64_t* bar, uint64_t pol) {
+    const int gk = T.gk[it.pass][it.s];
+    const bool p4 = T.p4[it.s] != 0;
+    const int wb = p4 ? gk * 1024 : gk * 4096, sb = p4 ? gk * 32 : 0;
+    mbar_expect_tx(bar, wb + sb);
+    const size_t blk = static_cast<size_t>(it.rt) * (K / 128) + static_cast<size_t>(it.kp) * gk;
+    bulk_g2s_hint(stage, T.w[it.pass][it.s] + blk * (p4 ? 1024 : 4096), wb, bar, pol);
+    if (p4) bulk_g2s_hint(stage + C::kStageS, T.sc[it.pass][it.s] + blk * 32, sb, bar, pol);
+}
+
+// compute_item's arithmetic for one resident token row
+template <class C>
+MOE_DEVI void flow_compute(const uint8_t* sp, const uint8_t* bp, const float* x0, int gk, bool p4, int lane,
+                           float (&acc)[4]) {
+    if (p4) {
+        if (gk == 8) {
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+                group_int4(sp + g * 1024, sp + C::kStageS + g * 32, bp + g * 256, x0[g], x0[g], lane, acc);
+        } else {
+            for (int g = 0; g < gk; ++g)
+                group_int4(sp + g * 1024, sp + C::kStageS + g * 32, bp + g * 256, x0[g], x0[g], lane, acc);
+        }
+    } else {
+        float c1[4] = {0.f, 0.f, 0.f, 0.f};
+        group_bf16(sp, bp, lane, acc, c1);
+        if (gk == 2) group_bf16(sp + 4096, bp + 256, lane, acc, c1);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[r] += c1[r];
+    }
+}
+
+MOE_DEVI void red_release_gpu(unsigned int* p, unsigned int v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+MOE_DEVI uint32_t ld_relaxed_u32(const void* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+MOE_DEVI float4 ld_relaxed_f4(const float* p) {
+    float4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+MOE_DEVI void st_relaxed_f32(float* p, float v) {
+    asm volatile("st.relaxed.gpu.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+MOE_DEVI void st_sentinel4(float* p) {
+    const float s = __uint_as_float(kFlowSentinel);
+    asm volatile("st.relaxed.gpu.global.v4.f32 [%0], {%1,%1,%1,%1};" ::"l"(p), "f"(s) : "memory");
+}
+MOE_DEVI bool has_sentinel(const float4& v) {
+    return __float_as_uint(v.x) == kFlowSentinel || __float_as_uint(v.y) == kFlowSentinel ||
+           __float_as_uint(v.z) == kFlowSentinel || __float_as_uint(v.w) == kFlowSentinel;
+}
+
+// sum_kparts without its loop (KP <= 8 * kKG): the same additions in the
+// same order -- acc_u = 0 + v(kg + u*kKG) (0 past KP), then acc_0 + acc_1 +
+// ... + acc_7 -- with every load issued up front; *miss set if a loaded
+// partial is still the sentinel.
+MOE_DEVI float4 sum_kparts_r(const float* p, size_t kstride, int KP, int kg, bool* miss) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        v[u] = kg + u * kKG < KP ? ld_relaxed_f4(p + (kg + u * kKG) * kstride) : make_float4(0.f, 0.f, 0.f, 0.f);
+    bool m = false;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) m |= has_sentinel(v[u]);
+    *miss = *miss || m;
+    float4 acc = make_float4(0.f + v[0].x, 0.f + v[0].y, 0.f + v[0].z, 0.f + v[0].w);
+#pragma unroll
+    for (int u = 1; u < 8; ++u) {
+        acc.x += 0.f + v[u].x; acc.y += 0.f + v[u].y; acc.z += 0.f + v[u].z; acc.w += 0.f + v[u].w;
+    }
+    return acc;
+}
+
+// sum over kg of sum_kparts(p, kstride, KP, kg), added in kg order: the
+// finalize kernels' K-part reduction of 4 rows, for one lane.  KP <= 16
+// keeps every partial in registers (all loads in flight at once).
+MOE_DEVI float4 kpart_total(const float* p, size_t kstride, int KP, bool* miss) {
+    if (KP <= 16) {
+        float4 v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            v[i] = i < KP ? ld_relaxed_f4(p + i * kstride) : make_float4(0.f, 0.f, 0.f, 0.f);
+        bool m = false;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) m |= has_sentinel(v[i]);
+        *miss = *miss || m;
+        float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int kg = 0; kg < kKG; ++kg) {
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 x0 = v[kg], x1 = v[kg + kKG];
+            float4 acc = make_float4(0.f + x0.x, 0.f + x0.y, 0.f + x0.z, 0.f + x0.w);
+            acc.x += 0.f + x1.x; acc.y += 0.f + x1.y; acc.z += 0.f + x1.z; acc.w += 0.f + x1.w;
+#pragma unroll
+            for (int u = 2; u < 8; ++u) {  // K-parts >= 16: zero
+                acc.x += 0.f + z.x; acc.y += 0.f + z.y; acc.z += 0.f + z.z; acc.w += 0.f + z.w;
+            }
+            if (kg == 0) {
+                tot = acc;
+            } else {
+                tot.x += acc.x; tot.y += acc.y; tot.z += acc.z; tot.w += acc.w;
+            }
+        }
+        return tot;
+    }
+    float4 tot = sum_kparts_r(p, kstride, KP, 0, miss);
+#pragma unroll
+    for (int kg = 1; kg < kKG; ++kg) {
+        const float4 c = sum_kparts_r(p, kstride, KP, kg, miss);
+        tot.x += c.x; tot.y += c.y; tot.z += c.z; tot.w += c.w;
+    }
+    return tot;
+}
+
+// Batch-1 routing tail (route_tail_t1's selection, weights and permutation)
+// filling the flow table.
+template <class C>
+MOE_DEVI void route_tail_flow(const float* lg, const moe_expert_weights* ex, int E, int k, int d, int f, int lane,
+                              int32_t* topi, float* wts, int32_t* inv, FlowTab& T) {
+    const bool h0 = lane < E, h1 = lane + 32 < E;
+    const float v0 = h0 ? lg[lane] : 0.0f, v1 = h1 ? lg[lane + 32] : 0.0f;
+    const uint32_t k0 = h0 ? order_key(v0) : 0u, k1 = h1 ? order_key(v1) : 0u;
+    bool a0 = h0, a1 = h1;
+    int sel[2] = {0, 0};
+    float sv[2] = {0.0f, 0.0f};
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        if (j >= k) break;
+        const uint32_t m = __reduce_max_sync(0xffffffffu, max(a0 ? k0 : 0u, a1 ? k1 : 0u));
+        const uint32_t b0 = __ballot_sync(0xffffffffu, a0 && k0 == m);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, a1 && k1 == m);
+        const int w = b0 ? __ffs(b0) - 1 : 32 + __ffs(b1) - 1;
+        sel[j] = w;
+        sv[j] = __shfl_sync(0xffffffffu, w < 32 ? v0 : v1, w & 31);
+        if (w == lane) a0 = false;
+        if (w == lane + 32) a1 = false;
+    }
+    float ex_[2] = {0.0f, 0.0f}, sum = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+        if (j < k) {
+            ex_[j] = expf(sv[j] - sv[0]);
+            sum += ex_[j];
+        }
+    int pos[2] = {0, 0};
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            if (j < k && i < k && sel[i] < sel[j]) ++pos[j];
+    if (lane < k) {
+        const int j = lane;
+        topi[j] = sel[j == 0 ? 0 : 1];
+        wts[j] = ex_[j == 0 ? 0 : 1] / sum;
+        inv[j] = pos[j == 0 ? 0 : 1];
+    }
+    // lanes (p, s) = (0|1, 0|1) at 0, 1, 16, 17: pass p of slot s
+    const int p = lane >> 4, s = lane & 15;
+    if (p < 2 && s < 2) {
+        const int K = p ? f : d, G = K / 128;
+        if (s < k) {
+            int e = 0;
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+                if (j < k && pos[j] == s) e = sel[j];
+            const moe_expert_weights& W = ex[e];
+            const int gk = pick_gk<C>(G, W.precision, 1);
+            T.w[p][s] = static_cast<const uint8_t*>(p == 0 ? W.w_gate_up : W.w_down);
+            T.sc[p][s] = static_cast<const uint8_t*>(p == 0 ? W.s_gate_up : W.s_down);
+            T.gk[p][s] = gk;
+            T.kp[p][s] = G / gk;
+            if (p == 0) T.p4[s] = W.precision == MOE_P4 ? 1 : 0;
+        } else {
+            T.w[p][s] = nullptr;
+            T.sc[p][s] = nullptr;
+            T.gk[p][s] = 1;
+            T.kp[p][s] = 0;
+            if (p == 0) T.p4[s] = 0;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        const int Gf = f / 128, RT1 = d / 16;
+        T.U[0] = 16 * T.kp[0][0];
+        T.U[1] = 16 * T.kp[0][1];
+        T.stride0 = 8 * (T.U[0] + T.U[1]);
+        T.N0 = Gf * (T.U[0] + T.U[1]);
+        const int nk = 8 / T.gk[1][0] + (k > 1 ? 8 / T.gk[1][1] : 0);
+        T.stride1 = RT1 * nk;
+        T.N1 = RT1 * (T.kp[1][0] + T.kp[1][1]);
+    }
+}
+
+// per-layer counter block: [k*nC h chunks][x ready], padded
+__host__ __device__ inline int flow_layer_words(int k, int d, int f) {
+    (void)d;
+    const int nC = (f / 128 + 7) / 8;
+    return (k * nC + 1 + 31) / 32 * 32;
+}
+
+// The finisher warp of one layer: this CTA's SwiGLU units and output tiles
+// and every h chunk, as they become ready.
+template <class C>
+MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsigned int* ctl, uint8_t* hres,
+                            float* hbias, uint64_t (*hbar)[kFlowMaxChunks], uint16_t* hs, const int32_t* s_inv,
+                            const float* s_w, const uint16_t* xl, uint16_t* yl, int lane) {
+    const int d = a.d, f = a.f, k = a.k, Gf = f / 128, nC = (Gf + 7) / 8, RT1 = d / 16;
+    const int grid = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+    const int bs1 = group_stride(f);
+    unsigned int* hcnt = ctl;
+    unsigned int* xdone = hcnt + k * nC;
+    const int nU = b < k * Gf ? (k * Gf - b + grid - 1) / grid : 0;  // <= 32 (moek_decode_flow_supported)
+    const int nCh = k * nC;                                             // <= 32
+    const int nR = b < RT1 ? (RT1 - b + grid - 1) / grid : 0;           // <= 32
+    const size_t rows2 = static_cast<size_t>(2) * f, kstride0 = static_cast<size_t>(k) * rows2;
+    const size_t kstride1 = static_cast<size_t>(k) * d;
+    uint32_t pu = nU >= 32 ? 0xffffffffu : (1u << nU) - 1u;
+    uint32_t pc = nCh >= 32 ? 0xffffffffu : (1u << nCh) - 1u;
+    uint32_t pr = nR >= 32 ? 0xffffffffu : (1u << nR) - 1u;
+    const int kl = k - 1, kpl = T.kp[1][kl];  // the last down item of a tile: slot k-1, its last K-part
+    while (pu | pc | pr) {
+        bool progress = false;
+        // ---- SwiGLU units: the unit's last partial first, then all of them
+        if (pu) {
+            bool w = false;
+            if ((pu >> lane) & 1u) {
+                const int u = b + lane * grid, s = u / Gf, g = u - s * Gf;
+                const float* wp = a.part0 + (static_cast<size_t>(T.kp[0][s] - 1) * k + s) * rows2 + f + g * 128 + 7 * 16;
+                w = ld_relaxed_u32(wp) != kFlowSentinel;
+            }
+            uint32_t wm = __ballot_sync(0xffffffffu, w);
+            while (wm) {
+                const int i = __ffs(wm) - 1;
+                wm &= wm - 1;
+                const int u = b + i * grid, s = u / Gf, g = u - s * Gf, KP = T.kp[0][s];
+                float* pg = a.part0 + static_cast<size_t>(s) * rows2 + g * 128 + lane * 4;
+                bool miss = false;
+                const float4 gs = kpart_total(pg, kstride0, KP, &miss);
+                const float4 us = kpart_total(pg + f, kstride0, KP, &miss);
+                if (__any_sync(0xffffffffu, miss)) continue;
+                const float gv[4] = {gs.x, gs.y, gs.z, gs.w}, uv[4] = {us.x, us.y, us.z, us.w};
+                swiglu_store(gv, uv, hs, s, g, f, a.hperm, a.hperm16, a.hsum, bs1, lane);
+                for (int kp = 0; kp < KP; ++kp) {  // consumed: back to the sentinel
+                    st_sentinel4(pg + kp * kstride0);
+                    st_sentinel4(pg + f + kp * kstride0);
+                }
+                __syncwarp();
+                if (lane == 0) red_release_gpu(hcnt + s * nC + g / 8, 1u);
+                pu &= ~(1u << i);
+                progress = true;
+            }
+        }
+        // ---- h chunks: each ready chunk lane copies its chunk
+        if (pc) {
+            bool ready = false;
+            if ((pc >> lane) & 1u) {
+                const int c = lane % nC;
+                ready = ld_acquire_gpu(hcnt + lane) >= static_cast<unsigned int>(min(8, Gf - 8 * c));
+            }
+            if (ready) {
+                const int s = lane / nC, c = lane - s * nC;
+                const int nu = min(8, Gf - 8 * c);
+                const bool p4 = T.p4[s] != 0;
+                fence_proxy_async_global();
+                uint64_t* bar = &hbar[s][c];
+                mbar_expect_tx(bar, nu * 256 + (p4 ? 32 : 0));
+                bulk_g2s(hres + static_cast<size_t>(s) * f * 2 + c * 2048,
+                         (p4 ? a.hperm16 : a.hperm) + static_cast<size_t>(s) * f + c * 1024, nu * 256, bar);
+                if (p4) bulk_g2s(hbias + s * bs1 + 8 * c, a.hsum + static_cast<size_t>(s) * bs1 + 8 * c, 32, bar);
+            }
+            const uint32_t rm = __ballot_sync(0xffffffffu, ready);
+            pc &= ~rm;
+            progress = progress || rm != 0;
+        }
+        // ---- output tiles (their partials need every chunk): combine + residual
+        if (pr && pc == 0) {
+            bool w = false;
+            if ((pr >> lane) & 1u) {
+                const int rt = b + lane * grid;
+                w = ld_relaxed_u32(a.part1 + (static_cast<size_t>(kpl - 1) * k + kl) * d + rt * 16) != kFlowSentinel;
+            }
+            uint32_t wm = __ballot_sync(0xffffffffu, w);
+            while (wm) {
+                const int i = __ffs(wm) - 1;
+                wm &= wm - 1;
+                const int rt = b + i * grid;
+                const int q = lane >> 3, kg = lane & 7;
+                const int j = rt * 16 + q * 4;
+                bool miss = false;
+                float4 rr[2];
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj)  // both slots' loads in flight together
+                    rr[jj] = jj < k ? sum_kparts_r(a.part1 + static_cast<size_t>(s_inv[jj]) * d + j, kstride1,
+                                                   T.kp[1][s_inv[jj]], kg, &miss)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (__any_sync(0xffffffffu, miss)) continue;
+                const uint2 xr = __ldcg(reinterpret_cast<const uint2*>(xl + j));
+                float acc[4] = {bf16_lo(xr.x), bf16_hi(xr.x), bf16_lo(xr.y), bf16_hi(xr.y)};
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) {
+                    if (jj >= k) break;
+                    const float4 r = rr[jj];
+                    float4 s4;
+                    s4.x = __shfl_sync(0xffffffffu, r.x, q * 8);
+                    s4.y = __shfl_sync(0xffffffffu, r.y, q * 8);
+                    s4.z = __shfl_sync(0xffffffffu, r.z, q * 8);
+                    s4.w = __shfl_sync(0xffffffffu, r.w, q * 8);
+#pragma unroll
+                    for (int k2 = 1; k2 < kKG; ++k2) {
+                        s4.x += __shfl_sync(0xffffffffu, r.x, q * 8 + k2);
+                        s4.y += __shfl_sync(0xffffffffu, r.y, q * 8 + k2);
+                        s4.z += __shfl_sync(0xffffffffu, r.z, q * 8 + k2);
+                        s4.w += __shfl_sync(0xffffffffu, r.w, q * 8 + k2);
+                    }
+                    const float wj = s_w[jj];
+                    acc[0] = __fmaf_rn(wj, s4.x, acc[0]);
+                    acc[1] = __fmaf_rn(wj, s4.y, acc[1]);
+                    acc[2] = __fmaf_rn(wj, s4.z, acc[2]);
+                    acc[3] = __fmaf_rn(wj, s4.w, acc[3]);
+                }
+                if (kg == 0) {
+                    const uint2 o = make_uint2(static_cast<uint32_t>(f2bf(acc[0])) | (static_cast<uint32_t>(f2bf(acc[1])) << 16),
+                                               static_cast<uint32_t>(f2bf(acc[2])) | (static_cast<uint32_t>(f2bf(acc[3])) << 16));
+                    __stcg(reinterpret_cast<uint2*>(yl + j), o);
+                }
+                for (int jj = 0; jj < k; ++jj) {  // consumed: back to the sentinel
+                    const int slot = s_inv[jj];
+                    for (int kp = kg; kp < T.kp[1][slot]; kp += kKG)
+                        st_sentinel4(a.part1 + static_cast<size_t>(slot) * d + j + kp * kstride1);
+                }
+                __syncwarp();
+                if (lane == 0) red_release_gpu(xdone, 1u);
+                pr &= ~(1u << i);
+                progress = true;
+            }
+        }
+        if (!progress) __nanosleep(128);
+    }
+    // every chunk copy into the resident h rows landed before the next layer reuses them
+    for (int ch = lane; ch < nCh; ch += 32) mbar_wait(&hbar[ch / nC][ch % nC], static_cast<uint32_t>(l & 1));
+    __syncwarp();
+}
+
+// NW streaming warps with NS ring stages each (+ the finisher warp)
+template <class C, int NW, int NS>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __grid_constant__ DecodeArgs a) {
+    constexpr int kStageBytes = kFlowStage;
+    constexpr int kFlowWarps = NW;
+    static_assert(NS == 1 || NS == 2, "one or two ring stages per warp");
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ FlowTab tab;
+    __shared__ __align__(8) uint64_t bars[kFlowWarps][NS];
+    __shared__ __align__(8) uint64_t hbar[2][kFlowMaxChunks];
+    __shared__ __align__(16) moe_expert_weights s_ex[MOE_MAX_EXPERTS];
+    __shared__ float lg_s[MOE_MAX_EXPERTS + 256];
+    __shared__ int32_t s_inv[MOE_MAX_TOPK], s_topi[MOE_MAX_TOPK];
+    __shared__ float s_w[MOE_MAX_TOPK];
+    __shared__ __align__(16) uint16_t hs[128];
+    __shared__ int s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+    const int d = a.d, f = a.f, E = a.E, k = a.k;
+    const int Gf = f / 128, RT1 = d / 16, f16 = f / 16;
+    const int per_layer = flow_layer_words(k, d, f);
+    unsigned long long* const ftr = g_fused_trace;
+    if (lane == 0) {
+        if (warp < kFlowWarps)
+            for (int s2 = 0; s2 < NS; ++s2) mbar_init(&bars[warp][s2], 1);
+        if (warp == kFlowWarps)
+            for (int i = 0; i < 2 * kFlowMaxChunks; ++i) mbar_init(&hbar[i / kFlowMaxChunks][i % kFlowMaxChunks], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint64_t pol = policy_evict_first();
+    const int W = static_cast<int>(gridDim.x) * kFlowWarps;
+    const int wid = warp * static_cast<int>(gridDim.x) + static_cast<int>(blockIdx.x);  // SM-fastest
+    const int gr = lane >> 2, t4 = lane & 3;
+    uint8_t* ring = smem + static_cast<size_t>(warp) * NS * kStageBytes;
+    uint8_t* xres = smem + static_cast<size_t>(kFlowWarps) * NS * kStageBytes;  // bf16 row | fp16 row | bias
+    const int bs0 = group_stride(d), bs1 = group_stride(f);
+    uint8_t* hres = xres + 4 * d + 4 * bs0;                                             // k h rows | bias
+    float* hbias = reinterpret_cast<float*>(hres + 2 * 2 * f);
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem);  // routing scratch (rings idle)
+    uint16_t* xn = xs + d;
+    uint32_t phase_bits = 0;
+    uint4 wpre[kPreChunks];
+    if (warp < E && warp < kFlowWarps) preload_w(wpre, a.wg + static_cast<size_t>(warp) * d, d, lane);
+
+    for (int l = 0; l < a.L; ++l) {
+        const uint16_t* xl = l == 0 ? a.x_in : ((l - 1) & 1 ? a.xbuf1 : a.xbuf0);
+        uint16_t* yl = l == a.L - 1 ? a.x_out : (l & 1 ? a.xbuf1 : a.xbuf0);
+        const uint16_t* wgl = a.wg + static_cast<size_t>(l) * E * d;
+        unsigned int* ctl = a.flow_ctl + static_cast<size_t>(l) * per_layer;
+        fstamp(ftr, l, 0);
+        if (l > 0 && tid == 0) {  // the previous layer's output complete
+            const unsigned int* xready = a.flow_ctl + static_cast<size_t>(l - 1) * per_layer + k * ((Gf + 7) / 8);
+            while (ld_acquire_gpu(xready) < static_cast<unsigned int>(RT1)) {
+            }
+        }
+        // ---- R: route the token (every CTA, identical results) --------------
+        for (int i = tid; i < E * static_cast<int>(sizeof(moe_expert_weights) / 8); i += blockDim.x)
+            reinterpret_cast<uint2*>(s_ex)[i] = reinterpret_cast<const uint2*>(a.experts + static_cast<size_t>(l) * E)[i];
+        __syncthreads();
+        fstamp(ftr, l, 1);
+        for (int i = tid * 8; i < d; i += blockDim.x * 8)
+            *reinterpret_cast<uint4*>(xs + i) = __ldcg(reinterpret_cast<const uint4*>(xl + i));
+        __syncthreads();
+        const uint16_t* xr = xs;
+        if (a.norm_eps > 0.0f) {
+            if (tid < 256) {
+                float acc = 0.0f;  // route_kernel's pinned order
+                for (int c = 0; c * 256 + tid < d; ++c) {
+                    const float v = bf2f(xs[c * 256 + tid]);
+                    acc = __fmaf_rn(v, v, acc);
+                }
+                lg_s[MOE_MAX_EXPERTS + tid] = acc;
+            }
+            __syncthreads();
+            for (int s2 = 128; s2 >= 32; s2 >>= 1) {
+                if (tid < s2) lg_s[MOE_MAX_EXPERTS + tid] = __fadd_rn(lg_s[MOE_MAX_EXPERTS + tid], lg_s[MOE_MAX_EXPERTS + tid + s2]);
+                __syncthreads();
+            }
+            if (warp == 0) {
+                float v = lg_s[MOE_MAX_EXPERTS + lane];
+#pragma unroll
+                for (int s2 = 16; s2 >= 1; s2 >>= 1) v = __fadd_rn(v, __shfl_down_sync(0xffffffffu, v, s2));
+                if (lane == 0) lg_s[MOE_MAX_EXPERTS] = v;
+            }
+            __syncthreads();
+            const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(lg_s[MOE_MAX_EXPERTS], static_cast<float>(d)),
+                                                                    a.norm_eps)));
+            for (int i = tid * 8; i < d; i += blockDim.x * 8) {
+                uint4 v = *reinterpret_cast<const uint4*>(xs + i);
+                uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    w4[q] = static_cast<uint32_t>(f2bf(__fmul_rn(bf16_lo(w4[q]), rstd))) |
+                            (static_cast<uint32_t>(f2bf(__fmul_rn(bf16_hi(w4[q]), rstd))) << 16);
+                *reinterpret_cast<uint4*>(xn + i) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            }
+            __syncthreads();
+            xr = xn;
+        }
+        if (warp < kFlowWarps)
+            for (int e = warp; e < E; e += kFlowWarps) {
+                if (e != warp) preload_w(wpre, wgl + static_cast<size_t>(e) * d, d, lane);
+                const float v = router_dot(xr, wpre, wgl + static_cast<size_t>(e) * d, d, lane);
+                if (lane == 0) lg_s[e] = v;
+            }
+        __syncthreads();
+        fstamp(ftr, l, 2);
+        if (warp == 0) {
+            route_tail_flow<C>(lg_s, s_ex, E, k, d, f, lane, s_topi, s_w, s_inv, tab);
+            __syncwarp();
+            if (blockIdx.x == 0 && lane < k) {
+                a.idx[static_cast<size_t>(l) * a.idx_stride + lane] = s_topi[lane];
+                a.wts[static_cast<size_t>(l) * a.idx_stride + lane] = s_w[lane];
+            }
+        } else if (warp < kFlowWarps) {
+            // resident x row: K-permuted bf16, fp16 and the int4 bias terms
+            uint16_t* rb = reinterpret_cast<uint16_t*>(xres);
+            uint16_t* rh = rb + d;
+            float* rx = reinterpret_cast<float*>(xres + 4 * d);
+            const int G = d / 128, nw = kFlowWarps - 1;
+            for (int g0 = (warp - 1) * 2; g0 < G; g0 += nw * 2) {
+                const int g = g0 + (lane >> 4), c = lane & 15;
+                uint4 cb = make_uint4(0, 0, 0, 0), ch = cb;
+                float s_lo = 0.0f, s_hi = 0.0f, amax = 0.0f;
+                if (g < G) permute_chunk(xr + g * 128, c, cb, ch, s_lo, s_hi, amax);
+                numerics_group_check(amax, c == 0);
+#pragma unroll
+                for (int off = 8; off >= 1; off >>= 1) {
+                    s_lo += __shfl_xor_sync(0xffffffffu, s_lo, off);
+                    s_hi += __shfl_xor_sync(0xffffffffu, s_hi, off);
+                }
+                if (g < G) {
+                    reinterpret_cast<uint4*>(rb + g * 128)[c] = cb;
+                    reinterpret_cast<uint4*>(rh + g * 128)[c] = ch;
+                    if (c == 0) rx[g] = int4_bias_term(s_lo, s_hi);
+                }
+            }
+        }
+        fence_proxy_async();  // routing scratch (generic) writes before the rings' bulk copies
+        __syncthreads();
+        fstamp(ftr, l, 3);
+        if (l + 1 < a.L && blockIdx.x < 4 && tid == 0) {  // next layer's router weights -> L2
+            const uint32_t chunk = static_cast<uint32_t>(E) * d * 2 / 4;
+            if (chunk % 16 == 0)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(wgl + static_cast<size_t>(E) * d +
+                                                                            static_cast<size_t>(blockIdx.x) * chunk / 2),
+                             "r"(chunk)
+                             : "memory");
+        }
+        if (warp == kFlowWarps) {
+            flow_finisher<C>(a, tab, l, ctl, hres, hbias, hbar, hs, s_inv, s_w, xl, yl, lane);
+            if (ftr != nullptr) fstamp_lane0(ftr, l, 7);
+            continue;
+        }
+        // ---- streaming: this warp's items of both passes, round-robin ------
+        const FlowTab& T = tab;
+        const int N = T.N0 + T.N1;
+        const int nmine = wid < N ? (N - wid + W - 1) / W : 0;  // items of this warp
+        // lane j holds the warp's item (batch*32 + j), packed
+        int pk0 = 0, pk1 = -1;
+        auto decode_batch = [&](int j0) {
+            const int ix = wid + (j0 + lane) * W;
+            pk1 = -1;
+            if (j0 + lane < nmine) flow_pack(flow_item(T, ix, Gf, f16, RT1), pk0, pk1);
+        };
+        auto item_of = [&](int j) {
+            if ((j & 31) == 0) decode_batch(j);
+            return flow_unpack(__shfl_sync(0xffffffffu, pk0, j & 31), __shfl_sync(0xffffffffu, pk1, j & 31));
+        };
+        FItem it0{}, it1{};
+        int issued = 0, computed = 0;
+        if (nmine > 0) {
+            it0 = item_of(0);
+            if (lane == 0) flow_issue<C>(T, it0, it0.pass ? f : d, ring, &bars[warp][0], pol);
+            issued = 1;
+            if (NS == 2 && nmine > 1) {
+                it1 = item_of(1);
+                if (lane == 0) flow_issue<C>(T, it1, it1.pass ? f : d, ring + kStageBytes, &bars[warp][1], pol);
+                issued = 2;
+            }
+        }
+        bool first_down = true;
+        while (computed < issued) {
+            const int stage = NS == 2 ? computed & 1 : 0;
+            const FItem it = stage ? it1 : it0;
+            mbar_wait(&bars[warp][stage], (phase_bits >> stage) & 1u);
+            phase_bits ^= 1u << stage;
+            if (it.pass == 1) {
+                if (first_down) {
+                    first_down = false;
+                    if (warp == 0) fstamp(ftr, l, 4);
+                }
+                mbar_wait(&hbar[it.s][it.c], static_cast<uint32_t>(l & 1));
+            }
+            uint8_t* sp = ring + stage * kStageBytes;
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            {
+                const int gk = T.gk[it.pass][it.s];
+                const bool p4 = T.p4[it.s] != 0;
+                const uint8_t* bp;
+                const float* x0;
+                if (it.pass == 0) {
+                    bp = xres + (p4 ? 2 * d : 0) + it.kp * gk * 256 + t4 * 16;
+                    x0 = reinterpret_cast<const float*>(xres + 4 * d) + it.kp * gk;
+                } else {
+                    bp = hres + static_cast<size_t>(it.s) * f * 2 + it.kp * gk * 256 + t4 * 16;
+                    x0 = hbias + it.s * bs1 + it.kp * gk;
+                }
+                flow_compute<C>(sp, bp, x0, gk, p4, lane, acc);
+            }
+            ++computed;
+            fence_proxy_async();
+            __syncwarp();
+            if (issued < nmine) {
+                const FItem nit = item_of(issued);
+                if (lane == 0) flow_issue<C>(T, nit, nit.pass ? f : d, sp, &bars[warp][stage], pol);
+                if (stage) it1 = nit; else it0 = nit;
+                ++issued;
+            }
+            const int rows = it.pass ? d : 2 * f;
+            float* pp = (it.pass ? a.part1 : a.part0) + (static_cast<size_t>(it.kp) * k + it.s) * rows + it.rt * 16 + gr;
+            if (t4 == 0) {
+                st_relaxed_f32(pp, acc[0]);
+                st_relaxed_f32(pp + 8, acc[2]);
+            }
+        }
+        fence_proxy_async();  // resident rows / stages read (generic) before the next layer's bulk copies
+        if (warp == 0) fstamp(ftr, l, 5);
+        if (l + 1 < a.L && warp < E)
+            preload_w(wpre, wgl + static_cast<size_t>(E) * d + static_cast<size_t>(warp) * d, d, lane);
+    }
+    // the last CTA out zeroes the counters for the next step
+    __syncthreads();
+    unsigned int* exitc = a.flow_ctl + static_cast<size_t>(a.L) * per_layer;
+    if (tid == 0) {
+        unsigned int old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(exitc) : "memory");
+        s_last = old == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        const int words = a.L * per_layer;
+        for (int i = tid; i < words / 4; i += blockDim.x) __stcg(reinterpret_cast<uint4*>(a.flow_ctl) + i, make_uint4(0, 0, 0, 0));
+        __syncthreads();
+        if (tid == 0) *exitc = 0;
+    }
+}
 }  // namespace moek
 
 cudaError_t moek_debug_fused_trace(void* buf) {
@@ -1485,6 +2190,83 @@ cudaError_t moek_decode_step(const MoeDecodeArgs& a, cudaStream_t stream) {
     return cudaLaunchKernelEx(&cfg, moek::decode_step_kernel<C>, a);
 }
 int moek_group_stride(int K) { return moek::group_stride(K); }
+
+namespace {
+// streaming-warp x stage shapes of the dataflow step (MOE_FLOW_CFG picks one; A/B)
+struct FlowShape {
+    int nw, ns;
+};
+FlowShape flow_shape() {
+    static FlowShape sh{0, 0};
+    if (sh.nw == 0) {
+        sh = FlowShape{7, 2};
+        if (const char* e = getenv("MOE_FLOW_CFG")) {
+            int nw = 0, ns = 0;
+            if (sscanf(e, "%dx%d", &nw, &ns) == 2) sh = FlowShape{nw, ns};
+        }
+    }
+    return sh;
+}
+template <int NW, int NS>
+cudaError_t launch_flow(const MoeDecodeArgs& a, size_t smem, cudaStream_t stream) {
+    using C = moek::CfgDecode;
+    auto kern = moek::decode_flow_kernel<C, NW, NS>;
+    static size_t smem_set = 0;
+    static int grid = 0;
+    if (smem > smem_set) {
+        MOE_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        smem_set = smem;
+    }
+    if (grid == 0) {
+        int dev = 0, sms = 0, per = 0;
+        MOE_CUDA_OK(cudaGetDevice(&dev));
+        MOE_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        MOE_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, (NW + 1) * 32, smem));
+        if (per < 1) return cudaErrorCooperativeLaunchTooLarge;
+        grid = sms;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3((NW + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: the readiness waits rely on it
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+}  // namespace
+
+size_t moek_decode_flow_smem(int d, int f) {
+    const FlowShape sh = flow_shape();
+    return static_cast<size_t>(sh.nw) * sh.ns * moek::kFlowStage + 4 * static_cast<size_t>(d) +
+           4 * moek::group_stride(d) + 4 * static_cast<size_t>(f) + 8 * moek::group_stride(f);
+}
+
+size_t moek_decode_flow_ctl_words(int L, int k, int d, int f) {
+    return static_cast<size_t>(L) * moek::flow_layer_words(k, d, f) + 32;
+}
+
+bool moek_decode_flow_supported(int E, int k, int d, int f, int sms) {
+    if (!moek_decode_step_supported(E, k, d, f) || sms < 1) return false;
+    const int Gf = f / 128, nC = (Gf + 7) / 8;
+    // one finisher warp per CTA: <= 32 units, h chunks and output tiles each (a lane apiece)
+    const bool fin = (k * Gf + sms - 1) / sms <= 32 && k * nC <= 32 && (d / 16 + sms - 1) / sms <= 32;
+    return nC <= moek::kFlowMaxChunks && d / 128 <= 2 * 64 && Gf <= 2 * 64 && fin &&
+           moek_decode_flow_smem(d, f) + 8 * 1024 <= 227 * 1024;
+}
+
+cudaError_t moek_decode_flow(const MoeDecodeArgs& a, cudaStream_t stream) {
+    const size_t smem = moek_decode_flow_smem(a.d, a.f);
+    const FlowShape sh = flow_shape();
+    if (sh.nw == 15 && sh.ns == 1) return launch_flow<15, 1>(a, smem, stream);
+    if (sh.nw == 11 && sh.ns == 1) return launch_flow<11, 1>(a, smem, stream);
+    if (sh.nw == 7 && sh.ns == 2) return launch_flow<7, 2>(a, smem, stream);
+    if (sh.nw == 8 && sh.ns == 2) return launch_flow<8, 2>(a, smem, stream);
+    return cudaErrorInvalidValue;
+}
 // Largest T whose (active expert, 8-token tile) segments always fit the
 // kernel's table: at most min(E, T*k) experts are active and their segments
 // number at most min(E, T*k) + ceil(T*k / 8).
@@ -1674,5 +2456,6 @@ cudaError_t moek_preload_gemv() {
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::finalize_out_kernel));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::permute_rows_kernel));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::decode_step_kernel<moek::CfgDecode>));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::decode_flow_kernel<moek::CfgDecode, 7, 2>));
     return cudaSuccess;
 }

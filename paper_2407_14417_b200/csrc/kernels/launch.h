@@ -75,10 +75,16 @@ struct MoeDecodeArgs {
     unsigned int* sched;                // [L][2]
     unsigned long long* bar;            // grid-barrier arrival counter (monotonic)
     int bar_mode;                       // 0: release fetch-add; 1: fence + relaxed add (A/B)
+    unsigned int* flow_ctl;             // decode_flow_kernel: moek_decode_flow_ctl_words() zeroed words
 };
 bool moek_decode_step_supported(int E, int k, int d, int f);
 size_t moek_decode_step_smem();
 cudaError_t moek_decode_step(const MoeDecodeArgs& a, cudaStream_t stream);
+// Dataflow variant (counters instead of grid barriers); sms = the grid.
+bool moek_decode_flow_supported(int E, int k, int d, int f, int sms);
+size_t moek_decode_flow_smem(int d, int f);
+size_t moek_decode_flow_ctl_words(int L, int k, int d, int f);
+cudaError_t moek_decode_flow(const MoeDecodeArgs& a, cudaStream_t stream);
 // Debug: [L][grid][10] u64 globaltimer stamps of the fused step's phases; null disables.
 cudaError_t moek_debug_fused_trace(void* buf);
 // tcgen05 grouped expert FFN (tc_gemm.cu): x natural [T][d] bf16 (already

@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+for c in 15x1 11x1 7x2 8x2; do MOE_FLOW_CFG=$c timeout 120 python tools/flow_tps.py 0,128,256 | sed "s/^/$c /"; done
+MOE_FLOW_CFG=15x1 timeout 300 python -m pytest tests/test_gpu_fused.py -x -q -p no:cacheprovider 2>&1 | tail -2

@@ -55,3 +55,29 @@ def test_fused_equals_per_layer_mixtral(moe, cuda, n4):
     assert ms > 0 and nbytes > 32 * 2 * moe.expert_size(moe.profile_for_shape(4096, 14336, 32), 0)
     fused.close()
     ref.close()
+
+
+@pytest.mark.parametrize("shape,n4", [("tiny", 8), ("mixtral", 128), ("mixtral", 256)])
+def test_flow_equals_step(moe, cuda, monkeypatch, shape, n4):
+    """The dataflow step (decode_flow_kernel, counters) and the grid-barrier
+    step (decode_step_kernel) give bit-identical outputs and routing."""
+    import torch
+    cfg = TINY if shape == "tiny" else MIXTRAL
+    prof = moe.profile_for_shape(cfg["d_model"], cfg["d_ffn"], cfg["num_layers"], cfg["experts_per_layer"],
+                                 cfg["top_k"])
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 1), moe.HardwareProfile(10**15), prof)
+    engs = []
+    for mode in ("flow", "step"):
+        monkeypatch.setenv("MOE_FUSED", mode)
+        engs.append(moe.MoeEngine(cfg["num_layers"], cfg["experts_per_layer"], cfg["top_k"], cfg["d_model"],
+                                  cfg["d_ffn"], plan, max_tokens=1, seed=3, norm_eps=1e-5))
+    n = 2 * cfg["d_model"]
+    for step in range(8):
+        for e in engs:
+            e.synth_input(500 + step, 1)
+            e.decode(1)
+            e.sync()
+        assert np.array_equal(read_device(torch, engs[0].output_ptr, n), read_device(torch, engs[1].output_ptr, n)), step
+        assert engs[0].last_routing(1) == engs[1].last_routing(1), step
+    for e in engs:
+        e.close()

@@ -1,5 +1,6 @@
-"""A/B of the batch-1 decode: fused one-launch step vs five launches per layer
-(CUDA-event timed graph replays, 8 inputs), Mixtral shape, n4 sweep."""
+"""A/B of the batch-1 decode: the fused one-launch step (dataflow
+decode_flow_kernel, grid-barrier decode_step_kernel) vs five launches per
+layer (CUDA-event timed graph replays, 8 inputs), Mixtral shape, n4 sweep."""
 import os
 import sys
 
@@ -14,18 +15,18 @@ pts = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "0,128,256").split
 for n4 in pts:
     plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 0), moe.HardwareProfile(10**15), prof)
     row = {}
-    for per_layer in (True, False):
+    for name in ("per-layer", "step", "flow"):
+        os.environ["MOE_FUSED"] = name
         eng = moe.MoeEngine(32, 8, 2, 4096, 14336, plan, max_tokens=1, seed=0, norm_eps=1e-5,
-                            per_layer_decode=per_layer)
+                            per_layer_decode=name == "per-layer")
         eng.synth_input(0, 1)
         eng.decode(1)
         eng.sync()
         ms = bench.time_engine(moe, torch, eng, 1, 80, 3)
         extra = ""
-        if not per_layer:
+        if name != "per-layer":
             fm, fb = eng.profile_fused()
-            extra = f"  fused launch {fm:.4f} ms, {fb / fm / 1e6:.1f} GB/s"
-        row["per-layer" if per_layer else "fused"] = (ms, extra)
+            extra = f" (launch {fm:.4f} ms, {fb / fm / 1e6:.0f} GB/s)"
+        row[name] = f"{1000 / ms:7.1f} tok/s{extra}"
         eng.close()
-    print(f"n4={n4:3d}  per-layer {1000 / row['per-layer'][0]:7.1f} tok/s   fused {1000 / row['fused'][0]:7.1f} tok/s"
-          f"{row['fused'][1]}", flush=True)
+    print(f"n4={n4:3d}  " + "   ".join(f"{k} {v}" for k, v in row.items()), flush=True)

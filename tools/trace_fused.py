@@ -1,4 +1,5 @@
-"""Phase timeline of the fused batch-1 decode step (decode_step_kernel):
+"""Phase timeline of the fused batch-1 decode step (decode_flow_kernel, or
+decode_step_kernel with MOE_FUSED=step):
 per layer, globaltimer stamps of every CTA at the phase boundaries, reported
 as min / median / max over CTAs relative to the layer's first stamp,
 averaged over the layers.  usage: python tools/trace_fused.py [n4] [steps]"""
@@ -18,6 +19,7 @@ plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, n4, 0), moe.HardwareProfile(10
 eng = moe.MoeEngine(L, 8, 2, 4096, 14336, plan, max_tokens=1, seed=0, norm_eps=1e-5)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
 S = 18
+FLOW = os.environ.get("MOE_FUSED", "flow") != "step"
 names = ["layer start", "routing done", "gate/up done", "after bar 1", "swiglu done", "after bar 2", "h resident",
          "down done", "after bar 3", "combine done", "r: x loaded", "r: rstd", "r: normalised", "r: logits",
          "r: topk+rows", "r: w0 topk+perm", "r: w1 rows"]
@@ -40,9 +42,14 @@ for rep in range(5):
 tr = np.median(np.stack(acc), axis=0)  # [L][sms][S]
 MHZ = float(os.environ.get("SM_MHZ", "1965"))  # stamps are SM cycles (clock64), per CTA
 rel = (tr - tr[:, :, :1]) / MHZ  # us from this CTA's own layer start
-print(f"== fused step, n4={n4}: phase stamps (us from each CTA's layer start, SM clock; avg over {L} layers) "
+print(f"== fused step ({'flow' if FLOW else 'step'}), n4={n4}: phase stamps (us from each CTA's layer start, SM clock; avg over {L} layers) "
       f"min / median / max over {sms} CTAs")
-for i in [0, 10, 11, 12, 13, 15, 16, 14, 1, 2, 3, 4, 5, 6, 7, 8, 9]:
+order = [0, 10, 11, 12, 13, 15, 16, 14, 1, 2, 3, 4, 5, 6, 7, 8, 9]
+if FLOW:  # decode_flow_kernel's stamps (warp 0, finisher warp at 7)
+    names[:8] = ["layer start", "x ready", "logits", "routing done", "w0 first down", "w0 items done", "-",
+                 "finisher done"]
+    order = [0, 1, 2, 3, 4, 5, 7]
+for i in order:
     n = names[i]
     v = rel[:, :, i]
     print(f"   {n:14s} {v.min(axis=1).mean():7.2f} {np.median(v, axis=1).mean():7.2f} {v.max(axis=1).mean():7.2f}")
