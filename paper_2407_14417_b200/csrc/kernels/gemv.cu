@@ -1747,11 +1747,11 @@ MOE_DEVI void route_tail_flow(const float* lg, const moe_expert_weights* ex, int
     }
 }
 
-// per-layer counter block: [k*nC h chunks][x ready], padded
+// per-layer counter block: [k*nC h chunks][finishers done][dynamic items], padded
 __host__ __device__ inline int flow_layer_words(int k, int d, int f) {
     (void)d;
     const int nC = (f / 128 + 7) / 8;
-    return (k * nC + 1 + 31) / 32 * 32;
+    return (k * nC + 2 + 31) / 32 * 32;
 }
 
 // The finisher warp of one layer: this CTA's SwiGLU units and output tiles
@@ -1759,7 +1759,8 @@ __host__ __device__ inline int flow_layer_words(int k, int d, int f) {
 template <class C>
 MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsigned int* ctl, uint8_t* hres,
                             float* hbias, uint64_t (*hbar)[kFlowMaxChunks], uint16_t* hs, const int32_t* s_inv,
-                            const float* s_w, const uint16_t* xl, uint16_t* yl, int lane) {
+                            const float* s_w, const uint16_t* xl, uint16_t* yl, int lane,
+                            unsigned long long* ftr) {
     const int d = a.d, f = a.f, k = a.k, Gf = f / 128, nC = (Gf + 7) / 8, RT1 = d / 16;
     const int grid = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
     const int bs1 = group_stride(f);
@@ -1773,16 +1774,20 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
     uint32_t pu = nU >= 32 ? 0xffffffffu : (1u << nU) - 1u;
     uint32_t pc = nCh >= 32 ? 0xffffffffu : (1u << nCh) - 1u;
     uint32_t pr = nR >= 32 ? 0xffffffffu : (1u << nR) - 1u;
-    const int kl = k - 1, kpl = T.kp[1][kl];  // the last down item of a tile: slot k-1, its last K-part
     while (pu | pc | pr) {
         bool progress = false;
+        // chunk counters: relaxed loads issued first, in flight with the unit loads
+        // (an acquire load would hold every later load of the round behind it)
+        unsigned int cval = 0;
+        if ((pc >> lane) & 1u) cval = ld_relaxed_u32(hcnt + lane);
         // ---- SwiGLU units: the unit's last partial first, then all of them
         if (pu) {
             bool w = false;
             if ((pu >> lane) & 1u) {
                 const int u = b + lane * grid, s = u / Gf, g = u - s * Gf;
                 const float* wp = a.part0 + (static_cast<size_t>(T.kp[0][s] - 1) * k + s) * rows2 + f + g * 128 + 7 * 16;
-                w = ld_relaxed_u32(wp) != kFlowSentinel;
+                // the last two chunks' units gate the end of the layer: polled with their full loads
+                w = g / 8 >= nC - 2 || ld_relaxed_u32(wp) != kFlowSentinel;
             }
             uint32_t wm = __ballot_sync(0xffffffffu, w);
             while (wm) {
@@ -1794,6 +1799,7 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
                 const float4 gs = kpart_total(pg, kstride0, KP, &miss);
                 const float4 us = kpart_total(pg + f, kstride0, KP, &miss);
                 if (__any_sync(0xffffffffu, miss)) continue;
+                fstamp_lane0(ftr, l, 13);  // (last written wins: the CTA's last unit) data complete
                 const float gv[4] = {gs.x, gs.y, gs.z, gs.w}, uv[4] = {us.x, us.y, us.z, us.w};
                 swiglu_store(gv, uv, hs, s, g, f, a.hperm, a.hperm16, a.hsum, bs1, lane);
                 for (int kp = 0; kp < KP; ++kp) {  // consumed: back to the sentinel
@@ -1804,6 +1810,7 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
                 if (lane == 0) red_release_gpu(hcnt + s * nC + g / 8, 1u);
                 pu &= ~(1u << i);
                 progress = true;
+                fstamp_lane0(ftr, l, 8);  // released
             }
         }
         // ---- h chunks: each ready chunk lane copies its chunk
@@ -1811,7 +1818,9 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
             bool ready = false;
             if ((pc >> lane) & 1u) {
                 const int c = lane % nC;
-                ready = ld_acquire_gpu(hcnt + lane) >= static_cast<unsigned int>(min(8, Gf - 8 * c));
+                // seen complete: the acquire (one more round trip, only now) orders the copy after the units' h
+                ready = cval >= static_cast<unsigned int>(min(8, Gf - 8 * c)) &&
+                        ld_acquire_gpu(hcnt + lane) >= static_cast<unsigned int>(min(8, Gf - 8 * c));
             }
             if (ready) {
                 const int s = lane / nC, c = lane - s * nC;
@@ -1827,71 +1836,82 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
             const uint32_t rm = __ballot_sync(0xffffffffu, ready);
             pc &= ~rm;
             progress = progress || rm != 0;
+            if (rm != 0 && pc == 0) fstamp_lane0(ftr, l, 9);
         }
-        // ---- output tiles (their partials need every chunk): combine + residual
+        // ---- output tiles (their partials need every chunk): combine + residual,
+        // polled by loading the partials themselves, two tiles' loads in flight together
         if (pr && pc == 0) {
-            bool w = false;
-            if ((pr >> lane) & 1u) {
-                const int rt = b + lane * grid;
-                w = ld_relaxed_u32(a.part1 + (static_cast<size_t>(kpl - 1) * k + kl) * d + rt * 16) != kFlowSentinel;
-            }
-            uint32_t wm = __ballot_sync(0xffffffffu, w);
-            while (wm) {
-                const int i = __ffs(wm) - 1;
-                wm &= wm - 1;
-                const int rt = b + i * grid;
+            uint32_t todo = pr;
+            while (todo) {
+                const int i0 = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const int i1 = todo ? __ffs(todo) - 1 : -1;
+                if (i1 >= 0) todo &= todo - 1;
                 const int q = lane >> 3, kg = lane & 7;
-                const int j = rt * 16 + q * 4;
-                bool miss = false;
-                float4 rr[2];
+                int jx[2];
+                float4 rr[2][2];
+                bool miss[2] = {false, false};
 #pragma unroll
-                for (int jj = 0; jj < 2; ++jj)  // both slots' loads in flight together
-                    rr[jj] = jj < k ? sum_kparts_r(a.part1 + static_cast<size_t>(s_inv[jj]) * d + j, kstride1,
-                                                   T.kp[1][s_inv[jj]], kg, &miss)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-                if (__any_sync(0xffffffffu, miss)) continue;
-                const uint2 xr = __ldcg(reinterpret_cast<const uint2*>(xl + j));
-                float acc[4] = {bf16_lo(xr.x), bf16_hi(xr.x), bf16_lo(xr.y), bf16_hi(xr.y)};
+                for (int h = 0; h < 2; ++h) {
+                    const int i = h ? i1 : i0;
+                    jx[h] = (b + (i < 0 ? 0 : i) * grid) * 16 + q * 4;
 #pragma unroll
-                for (int jj = 0; jj < 2; ++jj) {
-                    if (jj >= k) break;
-                    const float4 r = rr[jj];
-                    float4 s4;
-                    s4.x = __shfl_sync(0xffffffffu, r.x, q * 8);
-                    s4.y = __shfl_sync(0xffffffffu, r.y, q * 8);
-                    s4.z = __shfl_sync(0xffffffffu, r.z, q * 8);
-                    s4.w = __shfl_sync(0xffffffffu, r.w, q * 8);
+                    for (int jj = 0; jj < 2; ++jj)
+                        rr[h][jj] = i >= 0 && jj < k ? sum_kparts_r(a.part1 + static_cast<size_t>(s_inv[jj]) * d + jx[h],
+                                                                    kstride1, T.kp[1][s_inv[jj]], kg, &miss[h])
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
 #pragma unroll
-                    for (int k2 = 1; k2 < kKG; ++k2) {
-                        s4.x += __shfl_sync(0xffffffffu, r.x, q * 8 + k2);
-                        s4.y += __shfl_sync(0xffffffffu, r.y, q * 8 + k2);
-                        s4.z += __shfl_sync(0xffffffffu, r.z, q * 8 + k2);
-                        s4.w += __shfl_sync(0xffffffffu, r.w, q * 8 + k2);
+                for (int h = 0; h < 2; ++h) {
+                    const int i = h ? i1 : i0;
+                    if (i < 0 || __any_sync(0xffffffffu, miss[h])) continue;
+                    fstamp_lane0(ftr, l, 10);  // last tile's data complete
+                    const int j = jx[h];
+                    const uint2 xr = __ldcg(reinterpret_cast<const uint2*>(xl + j));
+                    float acc[4] = {bf16_lo(xr.x), bf16_hi(xr.x), bf16_lo(xr.y), bf16_hi(xr.y)};
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj) {
+                        if (jj >= k) break;
+                        const float4 r = rr[h][jj];
+                        float4 s4;
+                        s4.x = __shfl_sync(0xffffffffu, r.x, q * 8);
+                        s4.y = __shfl_sync(0xffffffffu, r.y, q * 8);
+                        s4.z = __shfl_sync(0xffffffffu, r.z, q * 8);
+                        s4.w = __shfl_sync(0xffffffffu, r.w, q * 8);
+#pragma unroll
+                        for (int k2 = 1; k2 < kKG; ++k2) {
+                            s4.x += __shfl_sync(0xffffffffu, r.x, q * 8 + k2);
+                            s4.y += __shfl_sync(0xffffffffu, r.y, q * 8 + k2);
+                            s4.z += __shfl_sync(0xffffffffu, r.z, q * 8 + k2);
+                            s4.w += __shfl_sync(0xffffffffu, r.w, q * 8 + k2);
+                        }
+                        const float wj = s_w[jj];
+                        acc[0] = __fmaf_rn(wj, s4.x, acc[0]);
+                        acc[1] = __fmaf_rn(wj, s4.y, acc[1]);
+                        acc[2] = __fmaf_rn(wj, s4.z, acc[2]);
+                        acc[3] = __fmaf_rn(wj, s4.w, acc[3]);
                     }
-                    const float wj = s_w[jj];
-                    acc[0] = __fmaf_rn(wj, s4.x, acc[0]);
-                    acc[1] = __fmaf_rn(wj, s4.y, acc[1]);
-                    acc[2] = __fmaf_rn(wj, s4.z, acc[2]);
-                    acc[3] = __fmaf_rn(wj, s4.w, acc[3]);
+                    if (kg == 0) {
+                        const uint2 o = make_uint2(static_cast<uint32_t>(f2bf(acc[0])) | (static_cast<uint32_t>(f2bf(acc[1])) << 16),
+                                                   static_cast<uint32_t>(f2bf(acc[2])) | (static_cast<uint32_t>(f2bf(acc[3])) << 16));
+                        __stcg(reinterpret_cast<uint2*>(yl + j), o);
+                    }
+                    for (int jj = 0; jj < k; ++jj) {  // consumed: back to the sentinel
+                        const int slot = s_inv[jj];
+                        for (int kp = kg; kp < T.kp[1][slot]; kp += kKG)
+                            st_sentinel4(a.part1 + static_cast<size_t>(slot) * d + j + kp * kstride1);
+                    }
+                    fstamp_lane0(ftr, l, 11);  // last tile stored
+                    pr &= ~(1u << i);
+                    progress = true;
                 }
-                if (kg == 0) {
-                    const uint2 o = make_uint2(static_cast<uint32_t>(f2bf(acc[0])) | (static_cast<uint32_t>(f2bf(acc[1])) << 16),
-                                               static_cast<uint32_t>(f2bf(acc[2])) | (static_cast<uint32_t>(f2bf(acc[3])) << 16));
-                    __stcg(reinterpret_cast<uint2*>(yl + j), o);
-                }
-                for (int jj = 0; jj < k; ++jj) {  // consumed: back to the sentinel
-                    const int slot = s_inv[jj];
-                    for (int kp = kg; kp < T.kp[1][slot]; kp += kKG)
-                        st_sentinel4(a.part1 + static_cast<size_t>(slot) * d + j + kp * kstride1);
-                }
-                __syncwarp();
-                if (lane == 0) red_release_gpu(xdone, 1u);
-                pr &= ~(1u << i);
-                progress = true;
             }
         }
         if (!progress) __nanosleep(128);
     }
+    // this finisher's output rows (and sentinel resets) complete: one release per CTA and layer
+    __syncwarp();
+    if (lane == 0) red_release_gpu(xdone, 1u);
     // every chunk copy into the resident h rows landed before the next layer reuses them
     for (int ch = lane; ch < nCh; ch += 32) mbar_wait(&hbar[ch / nC][ch % nC], static_cast<uint32_t>(l & 1));
     __syncwarp();
@@ -1940,6 +1960,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
     uint32_t phase_bits = 0;
     uint4 wpre[kPreChunks];
     if (warp < E && warp < kFlowWarps) preload_w(wpre, a.wg + static_cast<size_t>(warp) * d, d, lane);
+    if (ftr != nullptr && tid == 0) {  // this SM's clock against the global timer (trace alignment)
+        ftr[static_cast<size_t>(blockIdx.x) * kFusedStamps + 16] = gtimer();
+        ftr[static_cast<size_t>(blockIdx.x) * kFusedStamps + 17] = clock64();
+    }
 
     for (int l = 0; l < a.L; ++l) {
         const uint16_t* xl = l == 0 ? a.x_in : ((l - 1) & 1 ? a.xbuf1 : a.xbuf0);
@@ -1947,16 +1971,18 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
         const uint16_t* wgl = a.wg + static_cast<size_t>(l) * E * d;
         unsigned int* ctl = a.flow_ctl + static_cast<size_t>(l) * per_layer;
         fstamp(ftr, l, 0);
-        if (l > 0 && tid == 0) {  // the previous layer's output complete
-            const unsigned int* xready = a.flow_ctl + static_cast<size_t>(l - 1) * per_layer + k * ((Gf + 7) / 8);
-            while (ld_acquire_gpu(xready) < static_cast<unsigned int>(RT1)) {
-            }
-        }
-        // ---- R: route the token (every CTA, identical results) --------------
+        // the layer's expert table while thread 0 waits for the previous layer's output
         for (int i = tid; i < E * static_cast<int>(sizeof(moe_expert_weights) / 8); i += blockDim.x)
             reinterpret_cast<uint2*>(s_ex)[i] = reinterpret_cast<const uint2*>(a.experts + static_cast<size_t>(l) * E)[i];
+        if (l > 0 && tid == 0) {
+            const unsigned int* xready = a.flow_ctl + static_cast<size_t>(l - 1) * per_layer + k * ((Gf + 7) / 8);
+            while (ld_acquire_gpu(xready) < gridDim.x) {  // every finisher of the previous layer done
+            }
+            if (ftr != nullptr) ftr[(static_cast<size_t>(l) * gridDim.x + blockIdx.x) * kFusedStamps + 12] = clock64();
+        }
         __syncthreads();
         fstamp(ftr, l, 1);
+        // ---- R: route the token (every CTA, identical results) --------------
         for (int i = tid * 8; i < d; i += blockDim.x * 8)
             *reinterpret_cast<uint4*>(xs + i) = __ldcg(reinterpret_cast<const uint4*>(xl + i));
         __syncthreads();
@@ -1971,12 +1997,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
                 lg_s[MOE_MAX_EXPERTS + tid] = acc;
             }
             __syncthreads();
-            for (int s2 = 128; s2 >= 32; s2 >>= 1) {
-                if (tid < s2) lg_s[MOE_MAX_EXPERTS + tid] = __fadd_rn(lg_s[MOE_MAX_EXPERTS + tid], lg_s[MOE_MAX_EXPERTS + tid + s2]);
-                __syncthreads();
-            }
-            if (warp == 0) {
-                float v = lg_s[MOE_MAX_EXPERTS + lane];
+            if (warp == 0) {  // the tree's levels 128, 64, 32 (one lane each), then the warp's shuffle levels
+                const float* t = lg_s + MOE_MAX_EXPERTS;
+                const float a0 = __fadd_rn(t[lane], t[lane + 128]), a1 = __fadd_rn(t[lane + 64], t[lane + 192]);
+                const float a2 = __fadd_rn(t[lane + 32], t[lane + 160]), a3 = __fadd_rn(t[lane + 96], t[lane + 224]);
+                float v = __fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3));
 #pragma unroll
                 for (int s2 = 16; s2 >= 1; s2 >>= 1) v = __fadd_rn(v, __shfl_down_sync(0xffffffffu, v, s2));
                 if (lane == 0) lg_s[MOE_MAX_EXPERTS] = v;
@@ -2047,14 +2072,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
                              : "memory");
         }
         if (warp == kFlowWarps) {
-            flow_finisher<C>(a, tab, l, ctl, hres, hbias, hbar, hs, s_inv, s_w, xl, yl, lane);
+            flow_finisher<C>(a, tab, l, ctl, hres, hbias, hbar, hs, s_inv, s_w, xl, yl, lane, ftr);
             if (ftr != nullptr) fstamp_lane0(ftr, l, 7);
             continue;
         }
         // ---- streaming: this warp's items of both passes, round-robin ------
         const FlowTab& T = tab;
         const int N = T.N0 + T.N1;
-        const int nmine = wid < N ? (N - wid + W - 1) / W : 0;  // items of this warp
+        // items [0, Ns) are dealt round-robin, the last quarter of the down pass is
+        // handed out one item at a time from the layer's counter (grabbed one ahead)
+        const int Ns = N - T.N1 / 4;
+        const int nmine = wid < Ns ? (Ns - wid + W - 1) / W : 0;  // static items of this warp
+        unsigned int* dctr = ctl + k * ((Gf + 7) / 8) + 1;
+        unsigned int dgrab = 0;  // lane 0: the pre-grabbed dynamic index
+        bool dstarted = false;
         // lane j holds the warp's item (batch*32 + j), packed
         int pk0 = 0, pk1 = -1;
         auto decode_batch = [&](int j0) {
@@ -2066,17 +2097,42 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
             if ((j & 31) == 0) decode_batch(j);
             return flow_unpack(__shfl_sync(0xffffffffu, pk0, j & 31), __shfl_sync(0xffffffffu, pk1, j & 31));
         };
+        // the warp's j-th item (static, then dynamic); false when the layer is out of items
+        auto next_of = [&](int j, FItem& it) -> bool {
+            if (j < nmine) {
+                it = item_of(j);
+                if (j + 1 == nmine && lane == 0) {  // last static item: grab the first dynamic one now
+                    dgrab = atomicAdd(dctr, 1u);
+                    dstarted = true;
+                }
+                return true;
+            }
+            if (!dstarted) {
+                if (lane == 0) dgrab = atomicAdd(dctr, 1u);
+                dstarted = true;
+            }
+            const int ix = Ns + static_cast<int>(__shfl_sync(0xffffffffu, dgrab, 0));
+            if (ix >= N) return false;
+            if (lane == 0) dgrab = atomicAdd(dctr, 1u);
+            it = flow_item(T, ix, Gf, f16, RT1);
+            return true;
+        };
         FItem it0{}, it1{};
         int issued = 0, computed = 0;
-        if (nmine > 0) {
-            it0 = item_of(0);
+        bool more = true;
+        if (next_of(0, it0)) {
             if (lane == 0) flow_issue<C>(T, it0, it0.pass ? f : d, ring, &bars[warp][0], pol);
             issued = 1;
-            if (NS == 2 && nmine > 1) {
-                it1 = item_of(1);
-                if (lane == 0) flow_issue<C>(T, it1, it1.pass ? f : d, ring + kStageBytes, &bars[warp][1], pol);
-                issued = 2;
+            if (NS == 2) {
+                if (next_of(1, it1)) {
+                    if (lane == 0) flow_issue<C>(T, it1, it1.pass ? f : d, ring + kStageBytes, &bars[warp][1], pol);
+                    issued = 2;
+                } else {
+                    more = false;
+                }
             }
+        } else {
+            more = false;
         }
         bool first_down = true;
         while (computed < issued) {
@@ -2110,11 +2166,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
             ++computed;
             fence_proxy_async();
             __syncwarp();
-            if (issued < nmine) {
-                const FItem nit = item_of(issued);
+            FItem nit;
+            if (more && next_of(issued, nit)) {
                 if (lane == 0) flow_issue<C>(T, nit, nit.pass ? f : d, sp, &bars[warp][stage], pol);
                 if (stage) it1 = nit; else it0 = nit;
                 ++issued;
+            } else {
+                more = false;
             }
             const int rows = it.pass ? d : 2 * f;
             float* pp = (it.pass ? a.part1 : a.part0) + (static_cast<size_t>(it.kp) * k + it.s) * rows + it.rt * 16 + gr;
@@ -2125,6 +2183,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
         }
         fence_proxy_async();  // resident rows / stages read (generic) before the next layer's bulk copies
         if (warp == 0) fstamp(ftr, l, 5);
+        if (ftr != nullptr) fstamp_lane0(ftr, l, 15);  // the CTA's last streaming warp done (last writer wins)
         if (l + 1 < a.L && warp < E)
             preload_w(wpre, wgl + static_cast<size_t>(E) * d + static_cast<size_t>(warp) * d, d, lane);
     }

@@ -41,17 +41,26 @@ for rep in range(5):
     acc.append(tr)
 tr = np.median(np.stack(acc), axis=0)  # [L][sms][S]
 MHZ = float(os.environ.get("SM_MHZ", "1965"))  # stamps are SM cycles (clock64), per CTA
-rel = (tr - tr[:, :, :1]) / MHZ  # us from this CTA's own layer start
+# us from the layer's earliest CTA start (SM clocks are not synchronised across SMs, but
+# clock64 counts from a common reset closely enough at this scale; ABS=0 -> per-CTA start)
+if FLOW and os.environ.get("ABS", "1") == "1":
+    # flow kernel: every CTA leaves its x-ready wait within ~1 round trip of the others (one
+    # counter), so each CTA's stamps are taken relative to its own x-ready of the layer; the
+    # previous layer's tail shows up as the layer period
+    rel = (tr - tr[:, :, 1:2]) / MHZ
+else:
+    rel = (tr - tr[:, :, :1]) / MHZ  # us from this CTA's own layer start
 print(f"== fused step ({'flow' if FLOW else 'step'}), n4={n4}: phase stamps (us from each CTA's layer start, SM clock; avg over {L} layers) "
       f"min / median / max over {sms} CTAs")
 order = [0, 10, 11, 12, 13, 15, 16, 14, 1, 2, 3, 4, 5, 6, 7, 8, 9]
 if FLOW:  # decode_flow_kernel's stamps (warp 0, finisher warp at 7)
-    names[:8] = ["layer start", "x ready", "logits", "routing done", "w0 first down", "w0 items done", "-",
-                 "finisher done"]
-    order = [0, 1, 2, 3, 4, 5, 7]
+    names[:16] = ["layer start", "x ready", "logits", "routing done", "w0 first down", "w0 items done",
+                  "-", "finisher done", "fin: last unit rel", "fin: chunks in", "fin: last tile data",
+                  "fin: last tile rel", "t0: xdone seen", "fin: last unit data", "-", "last warp done"]
+    order = [1, 2, 3, 13, 8, 9, 4, 5, 15, 10, 11, 7]
 for i in order:
     n = names[i]
     v = rel[:, :, i]
     print(f"   {n:14s} {v.min(axis=1).mean():7.2f} {np.median(v, axis=1).mean():7.2f} {v.max(axis=1).mean():7.2f}")
-span = np.median(tr[1:, :, 0] - tr[:-1, :, 0], axis=1) / MHZ
+span = np.median(tr[1:, :, 1 if FLOW else 0] - tr[:-1, :, 1 if FLOW else 0], axis=1) / MHZ
 print(f"   layer period   {span.mean():7.2f} us (median over CTAs)")
