@@ -1959,7 +1959,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
     uint16_t* xn = xs + d;
     uint32_t phase_bits = 0;
     uint4 wpre[kPreChunks];
-    if (warp < E && warp < kFlowWarps) preload_w(wpre, a.wg + static_cast<size_t>(warp) * d, d, lane);
+    if (warp < E) preload_w(wpre, a.wg + static_cast<size_t>(warp) * d, d, lane);  // the finisher warp routes too
     if (ftr != nullptr && tid == 0) {  // this SM's clock against the global timer (trace alignment)
         ftr[static_cast<size_t>(blockIdx.x) * kFusedStamps + 16] = gtimer();
         ftr[static_cast<size_t>(blockIdx.x) * kFusedStamps + 17] = clock64();
@@ -2021,12 +2021,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
             __syncthreads();
             xr = xn;
         }
-        if (warp < kFlowWarps)
-            for (int e = warp; e < E; e += kFlowWarps) {
-                if (e != warp) preload_w(wpre, wgl + static_cast<size_t>(e) * d, d, lane);
-                const float v = router_dot(xr, wpre, wgl + static_cast<size_t>(e) * d, d, lane);
-                if (lane == 0) lg_s[e] = v;
-            }
+        for (int e = warp; e < E; e += kFlowWarps + 1) {  // every warp, the finisher included: one logit each
+            if (e != warp) preload_w(wpre, wgl + static_cast<size_t>(e) * d, d, lane);
+            const float v = router_dot(xr, wpre, wgl + static_cast<size_t>(e) * d, d, lane);
+            if (lane == 0) lg_s[e] = v;
+        }
         __syncthreads();
         fstamp(ftr, l, 2);
         if (warp == 0) {
@@ -2074,6 +2073,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
         if (warp == kFlowWarps) {
             flow_finisher<C>(a, tab, l, ctl, hres, hbias, hbar, hs, s_inv, s_w, xl, yl, lane, ftr);
             if (ftr != nullptr) fstamp_lane0(ftr, l, 7);
+            if (l + 1 < a.L && warp < E)
+                preload_w(wpre, wgl + static_cast<size_t>(E) * d + static_cast<size_t>(warp) * d, d, lane);
             continue;
         }
         // ---- streaming: this warp's items of both passes, round-robin ------
