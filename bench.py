@@ -57,7 +57,7 @@ def _traffic(n4, T, alg_bytes, fused=False):
     tools/traffic.py for this configuration and input (profiles/r02_traffic.json),
     next to the algorithmic bytes of the same step; null when absent or when
     the recorded algorithmic bytes disagree (another kernel or routing).
-    fused: per launch of decode_step_kernel (one step); else per layer of the
+    fused: per launch of the fused step kernel (one step); else per layer of the
     expert-FFN launches."""
     path = os.path.join(ROOT, "profiles", "r02_traffic.json")
     try:
@@ -363,7 +363,7 @@ def run_ours(args, rank, world, device):
     value = world * T * 1000.0 / ms
 
     # ---- roofline ------------------------------------------------------------
-    # batch 1: the fused decode step is ONE launch (decode_step_kernel) --
+    # batch 1: the fused decode step is ONE launch (decode_flow_kernel) --
     # timed alone between CUDA events on the engine stream, against the
     # algorithmic bytes of the routing it made; otherwise the per-layer
     # expert FFN launches (gate/up stream + finalize_h + down stream +
@@ -379,9 +379,12 @@ def run_ours(args, rank, world, device):
         kps = 1
         ffn_share = avg_ms / ms
         traffic, traffic_note = _traffic(args.n4, T, avg_bytes, fused=True)
-        kernel_desc = ("decode_step_kernel: the whole %d-layer batch-1 step in one cooperative launch (routing, "
-                       "gate/up GEMV, SwiGLU, down GEMV, combine per layer), CUDA events on the engine stream; "
-                       "median of 5 launches on input %d" % (LAYERS, TRAFFIC_INPUT))
+        kernel_desc = ("%s: the whole %d-layer batch-1 step in one cooperative launch (routing, "
+                       "gate/up GEMV, SwiGLU, down GEMV, combine per layer%s), CUDA events on the engine stream; "
+                       "median of 5 launches on input %d" % (
+                           "decode_step_kernel" if os.environ.get("MOE_FUSED") == "step" else "decode_flow_kernel",
+                           LAYERS, "" if os.environ.get("MOE_FUSED") == "step" else
+                           "; dataflow hand-offs, no grid barriers inside a layer", TRAFFIC_INPUT))
     else:
         ffn_ms, ffn_bytes = [], []
         for _ in range(3):

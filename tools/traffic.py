@@ -1,7 +1,7 @@
 """ncu DRAM traffic of the bench's roofline kernels -> profiles/r02_traffic.json.
 
 Two captures at the headline configuration (n4, batch T, input bench.TRAFFIC_INPUT):
-  fused      one decode_step_kernel launch (the whole batch-1 step)
+  fused      one fused-step launch (decode_flow_kernel: the whole batch-1 step)
   per_layer  the expert-FFN launches (stream_kernel x2, finalize_h, finalize_out)
              of one per-layer-kernel step, summed and divided by the layers
 
@@ -73,13 +73,14 @@ def summarize(csv_path, alg_path, commit=""):
     def dram(m):
         return m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
 
-    fused = [m for (i, n), m in per.items() if "decode_step_kernel" in n]
+    fused = [(n, m) for (i, n), m in per.items() if "decode_flow_kernel" in n or "decode_step_kernel" in n]
     ffn = [m for (i, n), m in per.items() if any(k in n for k in FFN_KERNELS)]
     base = {"n4": alg["n4"], "tokens": alg["tokens"], "input": alg["input"], "commit": commit}
     out = {"how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (tools/traffic.py)"}
     if fused:
-        m = fused[0]
-        out["fused"] = dict(base, what="one decode_step_kernel launch (whole %d-layer step)" % alg["layers"],
+        name, m = fused[0]
+        kname = "decode_flow_kernel" if "decode_flow_kernel" in name else "decode_step_kernel"
+        out["fused"] = dict(base, what="one %s launch (whole %d-layer step)" % (kname, alg["layers"]),
                             dram_bytes=round(dram(m)), algorithmic_bytes=alg["fused_algorithmic_bytes"],
                             ratio=round(dram(m) / alg["fused_algorithmic_bytes"], 4),
                             ncu_time_us=round(m.get("gpu__time_duration.sum", 0) / 1e3, 1))
