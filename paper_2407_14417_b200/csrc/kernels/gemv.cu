@@ -1720,11 +1720,14 @@ MOE_DEVI void route_tail_flow(const float* lg, const moe_expert_weights* ex, int
             for (int j = 0; j < 2; ++j)
                 if (j < k && pos[j] == s) e = sel[j];
             const moe_expert_weights& W = ex[e];
-            const int gk = pick_gk<C>(G, W.precision, 1);
+            // pick_gk<C>(G, precision, 1) for resident rows without its loop: the largest
+            // power of two <= cap dividing G is min(cap, lowest set bit of G)
+            const int cap = W.precision == MOE_P4 ? C::kGk4 : C::kGk16;
+            const int gk = min(cap, G & -G);
             T.w[p][s] = static_cast<const uint8_t*>(p == 0 ? W.w_gate_up : W.w_down);
             T.sc[p][s] = static_cast<const uint8_t*>(p == 0 ? W.s_gate_up : W.s_down);
             T.gk[p][s] = gk;
-            T.kp[p][s] = G / gk;
+            T.kp[p][s] = G >> (__ffs(gk) - 1);
             if (p == 0) T.p4[s] = W.precision == MOE_P4 ? 1 : 0;
         } else {
             T.w[p][s] = nullptr;
@@ -1741,7 +1744,7 @@ MOE_DEVI void route_tail_flow(const float* lg, const moe_expert_weights* ex, int
         T.U[1] = 16 * T.kp[0][1];
         T.stride0 = 8 * (T.U[0] + T.U[1]);
         T.N0 = Gf * (T.U[0] + T.U[1]);
-        const int nk = 8 / T.gk[1][0] + (k > 1 ? 8 / T.gk[1][1] : 0);
+        const int nk = (8 >> (__ffs(T.gk[1][0]) - 1)) + (k > 1 ? 8 >> (__ffs(T.gk[1][1]) - 1) : 0);
         T.stride1 = RT1 * nk;
         T.N1 = RT1 * (T.kp[1][0] + T.kp[1][1]);
     }
