@@ -81,3 +81,33 @@ def test_flow_equals_step(moe, cuda, monkeypatch, shape, n4):
         assert engs[0].last_routing(1) == engs[1].last_routing(1), step
     for e in engs:
         e.close()
+
+
+@pytest.mark.parametrize("shape", [
+    dict(num_layers=3, experts_per_layer=8, top_k=1, d_model=512, d_ffn=1792),     # one slot per token
+    dict(num_layers=2, experts_per_layer=16, top_k=2, d_model=768, d_ffn=640),     # 5 h groups: one partial chunk
+    dict(num_layers=2, experts_per_layer=4, top_k=2, d_model=1024, d_ffn=2176),    # 17 groups: 3 chunks, last of 1
+])
+def test_flow_odd_shapes_equal_per_layer(moe, cuda, shape):
+    """decode_flow_kernel at shapes the Mixtral tests do not reach (k = 1, E = 16,
+    h-chunk counts with a partial last chunk) against the per-layer kernels."""
+    import torch
+    prof = moe.profile_for_shape(shape["d_model"], shape["d_ffn"], shape["num_layers"], shape["experts_per_layer"],
+                                 shape["top_k"])
+    n_exp = shape["num_layers"] * shape["experts_per_layer"]
+    plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, n_exp // 2, 5), moe.HardwareProfile(10**15), prof)
+    mk = lambda per_layer: moe.MoeEngine(shape["num_layers"], shape["experts_per_layer"], shape["top_k"],
+                                         shape["d_model"], shape["d_ffn"], plan, max_tokens=1, seed=11,
+                                         norm_eps=1e-5, per_layer_decode=per_layer)
+    fused, ref = mk(False), mk(True)
+    assert fused.profile_fused() is not None
+    n = 2 * shape["d_model"]
+    for step in range(10):
+        for e in (fused, ref):
+            e.synth_input(77 + step, 1)
+            e.decode(1)
+            e.sync()
+        assert np.array_equal(read_device(torch, fused.output_ptr, n), read_device(torch, ref.output_ptr, n)), step
+        assert fused.last_routing(1) == ref.last_routing(1), step
+    fused.close()
+    ref.close()
