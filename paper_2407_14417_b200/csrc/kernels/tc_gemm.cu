@@ -494,6 +494,328 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::kTmemCols) : "memory");
 }
 
+// ===========================================================================
+// Persistent 128-token variant (tc_ffn_persist): one CTA per SM walks the
+// tile list (t = blockIdx, blockIdx + grid, ...), every role running straight
+// from one tile into the next -- no per-tile prologue, no pipeline drain, the
+// epilogue of tile i overlapping the mainloop of tile i+1 through two TMEM
+// accumulator buffers (512 columns).  Shared memory: region R (4 x 32 KB) is
+// the bf16 raw ring, or for int4 tiles two canonical A stages + three compact
+// raw units; region B holds four 16 KB B stages.  At a change of precision
+// between consecutive tiles the weight producer waits for the previous
+// tile's accumulators (so R is no longer read) before reusing R.
+constexpr int kPRaw4Unit = 2 * 8192 + 2 * kRawS;  // compact int4 raw unit: [A_gate 8 KB][A_up 8 KB][scales]
+constexpr int kPSmem = 1024 + 4 * 32768 + 4 * 128 * kKc * 2;  // R + B
+
+MOE_DEVI void produce4c(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, uint8_t* raw, uint64_t* bar, int lane) {
+    const moe_expert_weights& W = a.ex[tl.e];
+    const int G = K / 128, g = kc >> 1;
+    if (lane == 0) mbar_expect_tx(bar, nmat * (8 * 1024 + 256));
+    __syncwarp();
+    for (int mat = 0; mat < nmat; ++mat) {
+        const int row0 = (a.p == 0 && mat == 1) ? a.f + tl.R0 : tl.R0;
+        const uint8_t* wb = static_cast<const uint8_t*>(a.p == 0 ? W.w_gate_up : W.w_down);
+        const uint8_t* sb = static_cast<const uint8_t*>(a.p == 0 ? W.s_gate_up : W.s_down);
+        if (lane < 8) {
+            const size_t blk = static_cast<size_t>(row0 / 16 + lane) * G + g;
+            bulk_g2s(raw + mat * 8192 + lane * 1024, wb + blk * 1024, 1024, bar);
+            bulk_g2s(raw + 2 * 8192 + mat * kRawS + lane * 32, sb + blk * 32, 32, bar);
+        }
+    }
+}
+
+// convert_int4 over the compact raw unit layout
+MOE_DEVI void convert_int4c(int nmat, const uint8_t* raw, uint8_t* can, int ct, const ConvOffsets& o) {
+    for (int mat = 0; mat < nmat; ++mat) {
+        const uint8_t* src = raw + mat * 8192;
+        uint8_t* dst = can + mat * kTileBytes;
+        const uint8_t* sc = raw + 2 * 8192 + mat * kRawS;
+        const __half2 m1032 = __halves2half2(__ushort_as_half(0xE408), __ushort_as_half(0xE408));
+        const __half2 m72 = __halves2half2(__ushort_as_half(0xD480), __ushort_as_half(0xD480));
+        const __half2 r16 = __halves2half2(__ushort_as_half(0x2C00), __ushort_as_half(0x2C00));
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const uint2 w2 = *reinterpret_cast<const uint2*>(src + o.qrow[j]);
+            const uint16_t sb = *reinterpret_cast<const uint16_t*>(sc + o.qsc[j]);
+            if (f16_scale_bad(sb)) numerics_flag(MOE_NUM_F16_SCALE);
+            const __half sh = __float2half_rn(bf2f(sb));
+            const __half2 s2 = __halves2half2(sh, sh);
+#pragma unroll
+            for (int qi = 0; qi < 2; ++qi) {
+                const uint32_t w = qi ? w2.y : w2.x;
+                uint32_t v[4] = {and_or(w, 0x000F000Fu, 0x64006400u), and_or(w, 0x00F000F0u, 0x64006400u),
+                                 and_or(w >> 8, 0x000F000Fu, 0x64006400u), and_or(w >> 8, 0x00F000F0u, 0x64006400u)};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    __half2 h = *reinterpret_cast<__half2*>(&v[u]);
+                    h = (u & 1) ? __hfma2(h, r16, m72) : __hadd2(h, m1032);
+                    h = __hmul2(h, s2);
+                    *reinterpret_cast<__half2*>(dst + o.q[j][qi * 4 + u]) = h;
+                }
+            }
+        }
+    }
+}
+
+// nsplit > 1 (down pass): tile (e, row tile, K split ks) covers chunks ks*nk/nsplit ..; its
+// y rows go to ypart[ks] (summed in split order by split_reduce_kernel)
+__global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_constant__ TcArgs a, int ntiles, int nsplit,
+                                                               float* ypart) {
+    constexpr int kN = 128, kBst = 4, kBTile = kN * kKc * 2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
+    __shared__ __align__(8) uint64_t rb_full[4], rb_empty[4], r4_full[3], r4_empty[3], cn_full[2], cn_empty[2],
+        b_full[kBst], b_empty[kBst], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_slot;
+    __shared__ int s_off[MOE_MAX_EXPERTS + 1];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint8_t* R = smem;
+    uint8_t* Bst = smem + 4 * 32768;
+    auto rawb = [&](int s) { return R + s * 32768; };
+    auto can = [&](int s) { return R + s * 32768; };
+    auto raw4 = [&](int s) { return R + 2 * 32768 + s * kPRaw4Unit; };
+    auto bst = [&](int s) { return Bst + s * kBTile; };
+
+    pdl_wait();
+    pdl_trigger();
+    const int K = a.p == 0 ? a.d : a.f;
+    const int RT = (a.p == 0 ? a.f : a.d) / kM;
+    const int nmat = a.p == 0 ? 2 : 1;
+    const int nks = K / kKc / nsplit;  // chunks per tile
+    const int grid = static_cast<int>(gridDim.x);
+    if (tid <= a.E) s_off[tid] = a.offsets[tid];
+    if (tid == 0) {
+        for (int s = 0; s < 4; ++s) {
+            mbar_init_n(&rb_full[s], 1);
+            mbar_init_n(&rb_empty[s], 1);  // MMA commit
+        }
+        for (int s = 0; s < 3; ++s) {
+            mbar_init_n(&r4_full[s], 1);
+            mbar_init_n(&r4_empty[s], kConvThreads / 32);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init_n(&cn_full[s], kConvThreads / 32);
+            mbar_init_n(&cn_empty[s], 1);
+            mbar_init_n(&acc_full[s], 1);
+            mbar_init_n(&acc_empty[s], kConvThreads / 32);
+        }
+        for (int s = 0; s < kBst; ++s) {
+            mbar_init_n(&b_full[s], 1);
+            mbar_init_n(&b_empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tmem_slot)), "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_slot;
+    // (row tile, K split) enumerated as one index: find_tile's R0 / 128 = rt * nsplit + ks
+    auto tile_of = [&](int i, Tile& tl, int& kc0) {
+        if (!find_tile<128>(a, s_off, RT * nsplit, static_cast<int>(blockIdx.x) + i * grid, tl)) return false;
+        const int rtk = tl.R0 / kM, ks = rtk % nsplit;
+        tl.R0 = (rtk / nsplit) * kM;
+        kc0 = ks * nks;
+        return true;
+    };
+    auto is_p4 = [&](const Tile& tl) { return a.ex[tl.e].precision == MOE_P4; };
+    const int my_tiles = static_cast<int>(blockIdx.x) < ntiles ? (ntiles - static_cast<int>(blockIdx.x) + grid - 1) / grid : 0;
+
+    if (warp == 0) {
+        // ---- weight producer ----
+        int ub = 0, u4 = 0, prev = -1;
+        for (int i = 0; i < my_tiles; ++i) {
+            Tile tl;
+            int kc0;
+            if (!tile_of(i, tl, kc0)) break;  // past the routing's last tile
+            const bool p4 = is_p4(tl);
+            if (prev >= 0 && prev != static_cast<int>(p4))  // region R changes role: the previous tile's MMAs first
+                mbar_wait(&acc_full[(i - 1) & 1], static_cast<uint32_t>(((i - 1) >> 1) & 1));
+            prev = p4;
+            if (p4) {
+                for (int kc = kc0; kc < kc0 + nks; kc += 2, ++u4) {
+                    const int r = u4 % 3;
+                    if (u4 >= 3) mbar_wait(&r4_empty[r], static_cast<uint32_t>(((u4 / 3) - 1) & 1));
+                    produce4c(a, tl, nmat, K, kc, raw4(r), &r4_full[r], lane);
+                }
+            } else {
+                for (int kc = kc0; kc < kc0 + nks; kc += 2, ub += 2) {  // both 64-K halves of each 4 KB block
+                    const int r0 = ub % 4, r1 = (ub + 1) % 4;
+                    if (ub >= 4) mbar_wait(&rb_empty[r0], static_cast<uint32_t>(((ub / 4) - 1) & 1));
+                    if (ub + 1 >= 4) mbar_wait(&rb_empty[r1], static_cast<uint32_t>((((ub + 1) / 4) - 1) & 1));
+                    produce_pair(a, tl, nmat, K, kc, rawb(r0), rawb(r1), &rb_full[r0], &rb_full[r1], lane);
+                }
+            }
+        }
+    } else if (warp == 2) {
+        // ---- B producer ----
+        if (lane == 0) {
+            int kb = 0;
+            for (int i = 0; i < my_tiles; ++i) {
+                Tile tl;
+                int kc0;
+                if (!tile_of(i, tl, kc0)) break;
+                const CUtensorMap* tm = is_p4(tl) ? &a.tmb16 : &a.tmb;
+                const int nbox = (min(kN, (tl.m + 15) / 16 * 16) + 63) / 64;
+                for (int kc = kc0; kc < kc0 + nks; ++kc, ++kb) {
+                    const int b = kb % kBst;
+                    if (kb >= kBst) mbar_wait(&b_empty[b], static_cast<uint32_t>(((kb / kBst) - 1) & 1));
+                    mbar_expect_tx(&b_full[b], static_cast<uint32_t>(nbox) * 64 * 128);
+                    for (int q = 0; q < nbox; ++q) tma_load_b(bst(b) + q * 8192, tm, kc * kKc, tl.slot0 + q * 64, &b_full[b]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---- MMA issuer ----
+        int cb = 0, c4 = 0, kb = 0;
+        for (int i = 0; i < my_tiles; ++i) {
+            Tile tl;
+            int kc0;
+            if (!tile_of(i, tl, kc0)) break;  // past the routing's last tile
+            const bool p4 = is_p4(tl);
+            const int nmma = min(kN, (tl.m + 15) / 16 * 16);
+            const uint32_t id = idesc(p4 ? 0 : 1, nmma, kM);
+            const int buf = i & 1;
+            if (i >= 2) mbar_wait(&acc_empty[buf], static_cast<uint32_t>(((i >> 1) - 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t dacc = tmem + buf * 256;
+            for (int kc = kc0; kc < kc0 + nks; ++kc, ++kb) {
+                const int b = kb % kBst;
+                int slot;
+                if (p4) {
+                    slot = c4 % 2;
+                    mbar_wait(&cn_full[slot], static_cast<uint32_t>((c4 / 2) & 1));
+                } else {
+                    slot = cb % 4;
+                    mbar_wait(&rb_full[slot], static_cast<uint32_t>((cb / 4) & 1));
+                }
+                mbar_wait(&b_full[b], static_cast<uint32_t>((kb / kBst) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (lane == 0) {
+                    const uint32_t ab = s32(p4 ? can(slot) : rawb(slot)), bb = s32(bst(b));
+#pragma unroll
+                    for (int j = 0; j < kKc / 16; ++j) {
+                        const uint64_t bdesc = sdesc(bb + j * 32);
+                        const uint32_t acc = (kc > kc0 || j > 0) ? 1u : 0u;
+                        for (int mat = 0; mat < nmat; ++mat) {
+                            const uint64_t adesc = p4 ? sdesc(ab + mat * kTileBytes + j * 32)
+                                                      : sdesc_core(ab + mat * kRawA + j * 256);
+                            umma(dacc + mat * kN, adesc, bdesc, id, acc);
+                        }
+                    }
+                    umma_commit(p4 ? &cn_empty[slot] : &rb_empty[slot]);
+                    umma_commit(&b_empty[b]);
+                    if (kc == kc0 + nks - 1) umma_commit(&acc_full[buf]);
+                }
+                __syncwarp();
+                if (p4) ++c4; else ++cb;
+            }
+        }
+    } else if (warp >= 4) {
+        // ---- converters (int4 tiles), then each tile's epilogue ----
+        const int ct = tid - 128;
+        ConvOffsets o0, o1;
+        conv_offsets(ct, 0, o0);
+        conv_offsets(ct, 1, o1);
+        int u4 = 0, c4 = 0;
+        const int row = (warp & 3) * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const int c0 = ((warp - 4) >> 2) * (kN / 2);
+        for (int i = 0; i < my_tiles; ++i) {
+            Tile tl;
+            int kc0;
+            if (!tile_of(i, tl, kc0)) break;  // past the routing's last tile
+            if (is_p4(tl)) {
+                for (int kc = kc0; kc < kc0 + nks; ++kc, ++c4) {
+                    const int r = u4 % 3, c = c4 % 2;
+                    if ((kc & 1) == 0) mbar_wait(&r4_full[r], static_cast<uint32_t>((u4 / 3) & 1));
+                    if (c4 >= 2) mbar_wait(&cn_empty[c], static_cast<uint32_t>(((c4 / 2) - 1) & 1));
+                    convert_int4c(nmat, raw4(r), can(c), ct, (kc & 1) ? o1 : o0);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&cn_full[c]);
+                        if (kc & 1) mbar_arrive(&r4_empty[r]);
+                    }
+                    if (kc & 1) ++u4;
+                }
+            }
+            const int buf = i & 1;
+            mbar_wait(&acc_full[buf], static_cast<uint32_t>((i >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t dacc = tmem + buf * 256;
+            for (int cbk = c0; cbk < c0 + kN / 2; cbk += 32) {
+                uint32_t g[32];
+                TMEM_LD32(dacc + lane_base + cbk, g);
+                if (a.p == 0) {
+                    uint32_t u[32];
+                    TMEM_LD32(dacc + lane_base + kN + cbk, u);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const int n = cbk + c;
+                        if (n < tl.m) {
+                            const uint16_t hb = f2bf(silu_f(__uint_as_float(g[c])) * __uint_as_float(u[c]));
+                            const size_t o = static_cast<size_t>(tl.slot0 + n) * a.f + tl.R0 + row;
+                            a.hout[o] = hb;
+                            if (f16_overflow(bf2f(hb))) numerics_flag(MOE_NUM_F16_ACT);
+                            a.hout16[o] = __half_as_ushort(__float2half_rn(bf2f(hb)));
+                        }
+                    }
+                } else {
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const int n = cbk + c;
+                        if (n < tl.m) {
+                            float* yo = nsplit > 1 ? ypart + static_cast<size_t>(kc0 / nks) * a.T * a.k * a.d : a.y;
+                            yo[static_cast<size_t>(tl.slot0 + n) * a.d + tl.R0 + row] = __uint_as_float(g[c]);
+                        }
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
+// y[slot][j] = sum over K splits of ypart[ks][slot][j], in split order, for the
+// slots of this launch's experts only (other rows of y are left untouched, as
+// the unsplit kernel leaves them).  One block per slot row (grid-stride).
+__global__ void split_reduce_kernel(const float4* __restrict__ ypart, const int32_t* __restrict__ offsets, int E,
+                                    uint64_t active_mask, int slots, int d4, int nsplit, float4* __restrict__ y) {
+    __shared__ int s_off[MOE_MAX_EXPERTS + 1];
+    pdl_wait();
+    pdl_trigger();
+    if (threadIdx.x <= E) s_off[threadIdx.x] = offsets[threadIdx.x];
+    __syncthreads();
+    const size_t plane = static_cast<size_t>(slots) * d4;
+    for (int slot = blockIdx.x; slot < slots; slot += gridDim.x) {
+        int e = 0;
+        while (e < E && s_off[e + 1] <= slot) ++e;
+        if (e >= E || !((active_mask >> e) & 1ull)) continue;
+        for (int j = threadIdx.x; j < d4; j += blockDim.x) {
+            const size_t i = static_cast<size_t>(slot) * d4 + j;
+            float4 acc = __ldcg(ypart + i);
+            for (int ks = 1; ks < nsplit; ++ks) {
+                const float4 v = __ldcg(ypart + static_cast<size_t>(ks) * plane + i);
+                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            }
+            y[i] = acc;
+        }
+    }
+}
+
 // Pass-0 B operand in slot order: xs[slot] = x[token of slot] (bf16) and
 // its fp16 copy (int4 experts), so every tile's token rows are one TMA box
 // column.  One 16-byte chunk per thread.
@@ -545,9 +867,12 @@ cudaError_t encode_b(CUtensorMap* tm, const void* base, int K, int rows) {
 }  // namespace tc
 }  // namespace moek
 
+constexpr int kDownSplit = 4;  // K splits of the down pass on the persistent kernel
+
 size_t moek_tc_workspace_bytes(int T, int k, int d, int f) {
     const size_t slots = static_cast<size_t>(T) * k;
-    return 2 * slots * d * 2 + 2 * slots * f * 2 + 1024;  // xs, xs16, h, h16
+    // xs, xs16, h, h16, the down pass's split partials
+    return 2 * slots * d * 2 + 2 * slots * f * 2 + static_cast<size_t>(kDownSplit) * slots * d * 4 + 1024;
 }
 
 // Grouped expert FFN on tcgen05 for every expert segment of a permutation:
@@ -570,6 +895,7 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     uint16_t* xs16 = xs + slots * d;
     uint16_t* h = xs16 + slots * d;
     uint16_t* h16 = h + slots * f;
+    float* ypart = reinterpret_cast<float*>(h16 + slots * f);
     const int kshift = (k & (k - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(k)) : -1;
     const long long nch = static_cast<long long>(slots) * (d / 8);
     MOE_CUDA_OK(moek::launch_pdl(gather_rows_kernel, dim3(static_cast<unsigned>(std::min<long long>((nch + 255) / 256, 2368))),
@@ -599,19 +925,47 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     const int ntiles_max = static_cast<int>((slots + NT - 1) / NT) + E;
     auto kern = wide ? tc_ffn_kernel<256> : tc_ffn_kernel<128>;
     const int smem = wide ? TcCfg<256>::kSmem : TcCfg<128>::kSmem;
+    // 128-token tiles: the persistent kernel over the exact tile count (MOE_TC_DBG bit 8 of 256: off)
+    const bool persist = !wide && !(dbg & 256);
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        MOE_CUDA_OK(cudaGetDevice(&dev));
+        MOE_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
+    }
+    // exact tile counts per pass need the routing (device); the persistent grid instead
+    // walks tiles [0, ntiles_max * RT) and skips the empty ones (find_tile returns false)
     // pass 0: gate/up + SwiGLU -> h
     a.p = 0;
     MOE_CUDA_OK(encode_b(&a.tmb, xs, d, static_cast<int>(slots)));
     MOE_CUDA_OK(encode_b(&a.tmb16, xs16, d, static_cast<int>(slots)));
     a.hout = h;
     a.hout16 = h16;
-    MOE_CUDA_OK(moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (f / kM))), dim3(kThreads2), smem,
-                                 stream, a));
+    if (persist) {
+        const int nt0 = ntiles_max * (f / kM);
+        MOE_CUDA_OK(moek::launch_pdl(tc_ffn_persist, dim3(static_cast<unsigned>(std::min(nt0, sms))), dim3(kThreads2), kPSmem,
+                                     stream, a, nt0, 1, static_cast<float*>(nullptr)));
+    } else {
+        MOE_CUDA_OK(moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (f / kM))), dim3(kThreads2), smem,
+                                     stream, a));
+    }
     // pass 1: down -> y
     a.p = 1;
     MOE_CUDA_OK(encode_b(&a.tmb, h, f, static_cast<int>(slots)));
     MOE_CUDA_OK(encode_b(&a.tmb16, h16, f, static_cast<int>(slots)));
     a.y = y;
+    if (persist) {
+        // K split in kDownSplit parts when every part keeps whole int4 chunk pairs
+        const int ns = (f / kKc) % (2 * kDownSplit) == 0 && !(dbg & 512) ? kDownSplit : 1;
+        const int nt1 = ntiles_max * (d / kM) * ns;
+        MOE_CUDA_OK(moek::launch_pdl(tc_ffn_persist, dim3(static_cast<unsigned>(std::min(nt1, sms))), dim3(kThreads2), kPSmem,
+                                     stream, a, nt1, ns, ypart));
+        if (ns == 1) return cudaSuccess;
+        return moek::launch_pdl(split_reduce_kernel, dim3(static_cast<unsigned>(std::min<size_t>(slots, 2048))), dim3(256), 0,
+                                stream, reinterpret_cast<const float4*>(ypart), offsets, E, active_mask,
+                                static_cast<int>(slots), d / 4, ns, reinterpret_cast<float4*>(y));
+    }
     return moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (d / kM))), dim3(kThreads2), smem, stream,
                             a);
 }
@@ -626,6 +980,8 @@ cudaError_t moek_preload_tc() {
     cudaFuncAttributes fa;
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_kernel<128>));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_kernel<256>));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_persist));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::split_reduce_kernel));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::gather_rows_kernel));
     return cudaSuccess;
 }
