@@ -505,7 +505,14 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
 // between consecutive tiles the weight producer waits for the previous
 // tile's accumulators (so R is no longer read) before reusing R.
 constexpr int kPRaw4Unit = 2 * 8192 + 2 * kRawS;  // compact int4 raw unit: [A_gate 8 KB][A_up 8 KB][scales]
-constexpr int kPSmem = 1024 + 4 * 32768 + 4 * 128 * kKc * 2;  // R + B
+#ifndef MOE_TCP_CAN
+#define MOE_TCP_CAN 2
+#endif
+constexpr int kPCan = MOE_TCP_CAN;                  // int4 canonical A stages in R
+constexpr int kPRaw4 = kPCan == 3 ? 2 : 3;          // int4 raw units in R after them
+constexpr int kPBst = kPCan == 3 ? 3 : 4;           // B stages
+constexpr int kPR = kPCan == 3 ? 5 * 32768 - 16384 : 4 * 32768;  // region R bytes (>= 4 bf16 raw stages)
+constexpr int kPSmem = 1024 + kPR + kPBst * 128 * kKc * 2;  // R + B
 
 MOE_DEVI void produce4c(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, uint8_t* raw, uint64_t* bar, int lane) {
     const moe_expert_weights& W = a.ex[tl.e];
@@ -561,19 +568,19 @@ MOE_DEVI void convert_int4c(int nmat, const uint8_t* raw, uint8_t* can, int ct, 
 // y rows go to ypart[ks] (summed in split order by split_reduce_kernel)
 __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_constant__ TcArgs a, int ntiles, int nsplit,
                                                                float* ypart) {
-    constexpr int kN = 128, kBst = 4, kBTile = kN * kKc * 2;
+    constexpr int kN = 128, kBst = kPBst, kBTile = kN * kKc * 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
-    __shared__ __align__(8) uint64_t rb_full[4], rb_empty[4], r4_full[3], r4_empty[3], cn_full[2], cn_empty[2],
+    __shared__ __align__(8) uint64_t rb_full[4], rb_empty[4], r4_full[kPRaw4], r4_empty[kPRaw4], cn_full[kPCan], cn_empty[kPCan],
         b_full[kBst], b_empty[kBst], acc_full[2], acc_empty[2];
     __shared__ uint32_t tmem_slot;
     __shared__ int s_off[MOE_MAX_EXPERTS + 1];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     uint8_t* R = smem;
-    uint8_t* Bst = smem + 4 * 32768;
+    uint8_t* Bst = smem + kPR;
     auto rawb = [&](int s) { return R + s * 32768; };
     auto can = [&](int s) { return R + s * 32768; };
-    auto raw4 = [&](int s) { return R + 2 * 32768 + s * kPRaw4Unit; };
+    auto raw4 = [&](int s) { return R + kPCan * 32768 + s * kPRaw4Unit; };
     auto bst = [&](int s) { return Bst + s * kBTile; };
 
     pdl_wait();
@@ -589,13 +596,15 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
             mbar_init_n(&rb_full[s], 1);
             mbar_init_n(&rb_empty[s], 1);  // MMA commit
         }
-        for (int s = 0; s < 3; ++s) {
+        for (int s = 0; s < kPRaw4; ++s) {
             mbar_init_n(&r4_full[s], 1);
             mbar_init_n(&r4_empty[s], kConvThreads / 32);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kPCan; ++s) {
             mbar_init_n(&cn_full[s], kConvThreads / 32);
             mbar_init_n(&cn_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             mbar_init_n(&acc_full[s], 1);
             mbar_init_n(&acc_empty[s], kConvThreads / 32);
         }
@@ -638,8 +647,8 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
             prev = p4;
             if (p4) {
                 for (int kc = kc0; kc < kc0 + nks; kc += 2, ++u4) {
-                    const int r = u4 % 3;
-                    if (u4 >= 3) mbar_wait(&r4_empty[r], static_cast<uint32_t>(((u4 / 3) - 1) & 1));
+                    const int r = u4 % kPRaw4;
+                    if (u4 >= kPRaw4) mbar_wait(&r4_empty[r], static_cast<uint32_t>(((u4 / kPRaw4) - 1) & 1));
                     produce4c(a, tl, nmat, K, kc, raw4(r), &r4_full[r], lane);
                 }
             } else {
@@ -688,8 +697,8 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                 const int b = kb % kBst;
                 int slot;
                 if (p4) {
-                    slot = c4 % 2;
-                    mbar_wait(&cn_full[slot], static_cast<uint32_t>((c4 / 2) & 1));
+                    slot = c4 % kPCan;
+                    mbar_wait(&cn_full[slot], static_cast<uint32_t>((c4 / kPCan) & 1));
                 } else {
                     slot = cb % 4;
                     mbar_wait(&rb_full[slot], static_cast<uint32_t>((cb / 4) & 1));
@@ -732,9 +741,9 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
             if (!tile_of(i, tl, kc0)) break;  // past the routing's last tile
             if (is_p4(tl)) {
                 for (int kc = kc0; kc < kc0 + nks; ++kc, ++c4) {
-                    const int r = u4 % 3, c = c4 % 2;
-                    if ((kc & 1) == 0) mbar_wait(&r4_full[r], static_cast<uint32_t>((u4 / 3) & 1));
-                    if (c4 >= 2) mbar_wait(&cn_empty[c], static_cast<uint32_t>(((c4 / 2) - 1) & 1));
+                    const int r = u4 % kPRaw4, c = c4 % kPCan;
+                    if ((kc & 1) == 0) mbar_wait(&r4_full[r], static_cast<uint32_t>((u4 / kPRaw4) & 1));
+                    if (c4 >= kPCan) mbar_wait(&cn_empty[c], static_cast<uint32_t>(((c4 / kPCan) - 1) & 1));
                     convert_int4c(nmat, raw4(r), can(c), ct, (kc & 1) ? o1 : o0);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
