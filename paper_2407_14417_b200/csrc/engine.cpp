@@ -184,7 +184,7 @@ struct MoeEngine::Impl {
     bool fused_ok = false;
     unsigned int* flow_ctl = nullptr;           // decode_flow_kernel's per-layer completion counters
     float* flow_part = nullptr;                 // its partial buffers (sentinel-filled between uses)
-    size_t flow_part0_floats = 0;
+    size_t flow_part0_floats = 0, flow_part1_floats = 0;
     bool flow_ok = false;                       // dataflow variant (default; MOE_FUSED=step: grid barriers)
 
     // expert parallelism (ep_a2a.cu): G ranks, this one owns slots s*G/E == rank
@@ -383,8 +383,10 @@ struct MoeEngine::Impl {
                 dev_alloc(reinterpret_cast<void**>(&flow_ctl), words * 4);
                 ck(cudaMemsetAsync(flow_ctl, 0, words * 4, compute), "memset");
                 // [d/128][K][2f] gate/up + [f/128][K][d] down partials, 0xffffffff = none pending
+                // two of each (by layer parity)
                 flow_part0_floats = static_cast<size_t>(d / 128) * K * 2 * f;
-                const size_t pf = flow_part0_floats + static_cast<size_t>(f / 128) * K * d;
+                flow_part1_floats = static_cast<size_t>(f / 128) * K * d;
+                const size_t pf = 2 * (flow_part0_floats + flow_part1_floats);
                 dev_alloc(reinterpret_cast<void**>(&flow_part), pf * 4);
                 ck(cudaMemsetAsync(flow_part, 0xff, pf * 4, compute), "memset");
                 flow_ok = true;
@@ -440,7 +442,9 @@ struct MoeEngine::Impl {
         a.flow_ctl = flow_ctl;
         if (flow_ok) {
             a.part0 = flow_part;
-            a.part1 = flow_part + flow_part0_floats;
+            a.part1 = flow_part + 2 * flow_part0_floats;
+            a.part0_stride = flow_part0_floats;
+            a.part1_stride = flow_part1_floats;
             ck(moek_decode_flow(a, compute), "decode_flow");
         } else {
             ck(moek_decode_step(a, compute), "decode_step");

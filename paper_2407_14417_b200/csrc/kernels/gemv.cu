@@ -1774,6 +1774,11 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
     const int nR = b < RT1 ? (RT1 - b + grid - 1) / grid : 0;           // <= 32
     const size_t rows2 = static_cast<size_t>(2) * f, kstride0 = static_cast<size_t>(k) * rows2;
     const size_t kstride1 = static_cast<size_t>(k) * d;
+    // this layer's partial buffers (two per pass, by layer parity: a buffer's sentinel
+    // resets, issued after this finisher's releases, only have to land before layer l + 2)
+    float* const P0 = a.part0 + static_cast<size_t>(l & 1) * a.part0_stride;
+    float* const P1 = a.part1 + static_cast<size_t>(l & 1) * a.part1_stride;
+    uint32_t reset_tiles = 0;
     uint32_t pu = nU >= 32 ? 0xffffffffu : (1u << nU) - 1u;
     uint32_t pc = nCh >= 32 ? 0xffffffffu : (1u << nCh) - 1u;
     uint32_t pr = nR >= 32 ? 0xffffffffu : (1u << nR) - 1u;
@@ -1788,7 +1793,7 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
             bool w = false;
             if ((pu >> lane) & 1u) {
                 const int u = b + lane * grid, s = u / Gf, g = u - s * Gf;
-                const float* wp = a.part0 + (static_cast<size_t>(T.kp[0][s] - 1) * k + s) * rows2 + f + g * 128 + 7 * 16;
+                const float* wp = P0 + (static_cast<size_t>(T.kp[0][s] - 1) * k + s) * rows2 + f + g * 128 + 7 * 16;
                 // the last two chunks' units gate the end of the layer: polled with their full loads
                 w = g / 8 >= nC - 2 || ld_relaxed_u32(wp) != kFlowSentinel;
             }
@@ -1797,7 +1802,7 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
                 const int i = __ffs(wm) - 1;
                 wm &= wm - 1;
                 const int u = b + i * grid, s = u / Gf, g = u - s * Gf, KP = T.kp[0][s];
-                float* pg = a.part0 + static_cast<size_t>(s) * rows2 + g * 128 + lane * 4;
+                float* pg = P0 + static_cast<size_t>(s) * rows2 + g * 128 + lane * 4;
                 bool miss = false;
                 const float4 gs = kpart_total(pg, kstride0, KP, &miss);
                 const float4 us = kpart_total(pg + f, kstride0, KP, &miss);
@@ -1805,12 +1810,12 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
                 fstamp_lane0(ftr, l, 13);  // (last written wins: the CTA's last unit) data complete
                 const float gv[4] = {gs.x, gs.y, gs.z, gs.w}, uv[4] = {us.x, us.y, us.z, us.w};
                 swiglu_store(gv, uv, hs, s, g, f, a.hperm, a.hperm16, a.hsum, bs1, lane);
-                for (int kp = 0; kp < KP; ++kp) {  // consumed: back to the sentinel
+                __syncwarp();
+                if (lane == 0) red_release_gpu(hcnt + s * nC + g / 8, 1u);
+                for (int kp = 0; kp < KP; ++kp) {  // consumed: back to the sentinel (after the release)
                     st_sentinel4(pg + kp * kstride0);
                     st_sentinel4(pg + f + kp * kstride0);
                 }
-                __syncwarp();
-                if (lane == 0) red_release_gpu(hcnt + s * nC + g / 8, 1u);
                 pu &= ~(1u << i);
                 progress = true;
                 fstamp_lane0(ftr, l, 8);  // released
@@ -1860,7 +1865,7 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
                     jx[h] = (b + (i < 0 ? 0 : i) * grid) * 16 + q * 4;
 #pragma unroll
                     for (int jj = 0; jj < 2; ++jj)
-                        rr[h][jj] = i >= 0 && jj < k ? sum_kparts_r(a.part1 + static_cast<size_t>(s_inv[jj]) * d + jx[h],
+                        rr[h][jj] = i >= 0 && jj < k ? sum_kparts_r(P1 + static_cast<size_t>(s_inv[jj]) * d + jx[h],
                                                                     kstride1, T.kp[1][s_inv[jj]], kg, &miss[h])
                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
@@ -1899,11 +1904,7 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
                                                    static_cast<uint32_t>(f2bf(acc[2])) | (static_cast<uint32_t>(f2bf(acc[3])) << 16));
                         __stcg(reinterpret_cast<uint2*>(yl + j), o);
                     }
-                    for (int jj = 0; jj < k; ++jj) {  // consumed: back to the sentinel
-                        const int slot = s_inv[jj];
-                        for (int kp = kg; kp < T.kp[1][slot]; kp += kKG)
-                            st_sentinel4(a.part1 + static_cast<size_t>(slot) * d + j + kp * kstride1);
-                    }
+                    reset_tiles |= 1u << i;  // consumed: back to the sentinel after the release
                     fstamp_lane0(ftr, l, 11);  // last tile stored
                     pr &= ~(1u << i);
                     progress = true;
@@ -1912,9 +1913,17 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
         }
         if (!progress) __nanosleep(128);
     }
-    // this finisher's output rows (and sentinel resets) complete: one release per CTA and layer
+    // this finisher's output rows complete: one release per CTA and layer
     __syncwarp();
     if (lane == 0) red_release_gpu(xdone, 1u);
+    for (uint32_t m = reset_tiles; m; m &= m - 1) {
+        const int rt = b + (__ffs(m) - 1) * grid, q = lane >> 3, kg = lane & 7, j = rt * 16 + q * 4;
+        for (int jj = 0; jj < k; ++jj) {
+            const int slot = s_inv[jj];
+            for (int kp = kg; kp < T.kp[1][slot]; kp += kKG)
+                st_sentinel4(P1 + static_cast<size_t>(slot) * d + j + kp * kstride1);
+        }
+    }
     // every chunk copy into the resident h rows landed before the next layer reuses them
     for (int ch = lane; ch < nCh; ch += 32) mbar_wait(&hbar[ch / nC][ch % nC], static_cast<uint32_t>(l & 1));
     __syncwarp();
@@ -2179,7 +2188,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
                 more = false;
             }
             const int rows = it.pass ? d : 2 * f;
-            float* pp = (it.pass ? a.part1 : a.part0) + (static_cast<size_t>(it.kp) * k + it.s) * rows + it.rt * 16 + gr;
+            float* pp = (it.pass ? a.part1 + static_cast<size_t>(l & 1) * a.part1_stride
+                                 : a.part0 + static_cast<size_t>(l & 1) * a.part0_stride) +
+                        (static_cast<size_t>(it.kp) * k + it.s) * rows + it.rt * 16 + gr;
             if (t4 == 0) {
                 st_relaxed_f32(pp, acc[0]);
                 st_relaxed_f32(pp + 8, acc[2]);

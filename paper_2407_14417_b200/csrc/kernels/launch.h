@@ -76,6 +76,7 @@ struct MoeDecodeArgs {
     unsigned long long* bar;            // grid-barrier arrival counter (monotonic)
     int bar_mode;                       // 0: release fetch-add; 1: fence + relaxed add (A/B)
     unsigned int* flow_ctl;             // decode_flow_kernel: moek_decode_flow_ctl_words() zeroed words
+    size_t part0_stride, part1_stride;  // decode_flow_kernel: floats between the two (layer-parity) partial buffers
 };
 bool moek_decode_step_supported(int E, int k, int d, int f);
 size_t moek_decode_step_smem();
