@@ -1911,7 +1911,7 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
                 }
             }
         }
-        if (!progress) __nanosleep(128);
+        if (!progress && !(pc == 0 && pr != 0)) __nanosleep(128);  // the last tiles: poll without pause
     }
     // this finisher's output rows complete: one release per CTA and layer
     __syncwarp();
