@@ -236,31 +236,36 @@ MOE_DEVI void tma_load_b(void* dst, const CUtensorMap* tm, int k0, int row0, uin
         : "memory");
 }
 
-// per-converter-thread swizzled destinations (identical for every chunk)
+// per-converter-thread offsets (identical for every chunk).  A warp's 32
+// threads are one item j: the 8 rows of a row half (lane = row % 8 * 4 + t),
+// which is stmatrix's lane layout: word qi of the 4 lanes t of a row gives
+// the row's 16-byte chunks 4qi .. 4qi+3 (nibble pairs u, gemv.cu group_int4),
+// so one stmatrix.x4 per (j, qi) stores 4 whole 8 x 8 matrices (lane l
+// supplies the address of row l % 8 of matrix l / 8 = chunk 4qi + l / 8).
 struct ConvOffsets {
-    int q[2][8];   // int4: item j -> 8 word destinations
-    int qrow[2];   // int4: item j -> (raw word offset, scale offset) packed
-    int qsc[2];
+    int stm[2][2];  // int4: (item j, word qi) -> this lane's stmatrix row address
+    int qrow[2];    // int4: item j -> raw word offset
+    int qsc[2];     // int4: item j -> scale offset
 };
 
 MOE_DEVI void conv_offsets(int ct, int hh, ConvOffsets& o) {
+    const int lane = ct & 31;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int it = ct + j * kConvThreads;
         const int i = it >> 6, hl = it & 63, half = hl >> 5, L = hl & 31;
-        const int row = i * 16 + half * 8 + (L >> 2);
         o.qrow[j] = i * 1024 + (hl * 4 + 2 * hh) * 4;
         o.qsc[j] = i * 32 + (L >> 2) * 4 + half * 2;
+        const int srow = i * 16 + half * 8 + (lane & 7);  // row this lane addresses for stmatrix
 #pragma unroll
-        for (int qi = 0; qi < 2; ++qi) {
-            const int kb0 = ((2 * qi) * 16 + 2 * (L & 3)) * 2;
-            const int kb1 = ((2 * qi + 1) * 16 + 2 * (L & 3)) * 2;
-            o.q[j][qi * 4 + 0] = swz(row, kb0);
-            o.q[j][qi * 4 + 1] = swz(row, kb0 + 16);
-            o.q[j][qi * 4 + 2] = swz(row, kb1);
-            o.q[j][qi * 4 + 3] = swz(row, kb1 + 16);
-        }
+        for (int qi = 0; qi < 2; ++qi) o.stm[j][qi] = swz(srow, (4 * qi + (lane >> 3)) * 16);
     }
+}
+
+MOE_DEVI void stmatrix_x4(uint32_t addr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(r0), "r"(r1), "r"(r2),
+                 "r"(r3)
+                 : "memory");
 }
 
 // int4 raw blocks -> fp16 q*s in the canonical SW128 A tile (bf16 blocks are
@@ -290,8 +295,9 @@ MOE_DEVI void convert_int4(int nmat, const uint8_t* raw, uint8_t* can, int ct, c
                     __half2 h = *reinterpret_cast<__half2*>(&v[u]);
                     h = (u & 1) ? __hfma2(h, r16, m72) : __hadd2(h, m1032);  // q exactly
                     h = __hmul2(h, s2);                                      // q*s exactly
-                    *reinterpret_cast<__half2*>(dst + o.q[j][qi * 4 + u]) = h;
+                    v[u] = *reinterpret_cast<uint32_t*>(&h);
                 }
+                stmatrix_x4(s32(dst) + o.stm[j][qi], v[0], v[1], v[2], v[3]);
             }
         }
     }
@@ -557,8 +563,9 @@ MOE_DEVI void convert_int4c(int nmat, const uint8_t* raw, uint8_t* can, int ct, 
                     __half2 h = *reinterpret_cast<__half2*>(&v[u]);
                     h = (u & 1) ? __hfma2(h, r16, m72) : __hadd2(h, m1032);
                     h = __hmul2(h, s2);
-                    *reinterpret_cast<__half2*>(dst + o.q[j][qi * 4 + u]) = h;
+                    v[u] = *reinterpret_cast<uint32_t*>(&h);
                 }
+                stmatrix_x4(s32(dst) + o.stm[j][qi], v[0], v[1], v[2], v[3]);
             }
         }
     }
