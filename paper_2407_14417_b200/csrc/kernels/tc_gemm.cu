@@ -514,10 +514,17 @@ constexpr int kPRaw4Unit = 2 * 8192 + 2 * kRawS;  // compact int4 raw unit: [A_g
 #ifndef MOE_TCP_CAN
 #define MOE_TCP_CAN 2
 #endif
-constexpr int kPCan = MOE_TCP_CAN;                  // int4 canonical A stages in R
-constexpr int kPRaw4 = kPCan == 3 ? 2 : 3;          // int4 raw units in R after them
-constexpr int kPBst = kPCan == 3 ? 3 : 4;           // B stages
-constexpr int kPR = kPCan == 3 ? 5 * 32768 - 16384 : 4 * 32768;  // region R bytes (>= 4 bf16 raw stages)
+// MOE_TCP_WIDE: int4 canonical stages of a whole 128-K raw unit (both 64-K halves,
+// 64 KB): one convert -> MMA hand-off per unit instead of per chunk
+#ifndef MOE_TCP_WIDE
+#define MOE_TCP_WIDE 0
+#endif
+constexpr bool kPWide = MOE_TCP_WIDE != 0;
+constexpr int kPCan = kPWide ? 2 : MOE_TCP_CAN;     // int4 canonical A stages in R
+constexpr int kPCanBytes = kPWide ? 65536 : 32768;
+constexpr int kPRaw4 = kPWide || kPCan == 3 ? 2 : 3;  // int4 raw units in R after them
+constexpr int kPBst = kPWide || kPCan == 3 ? 3 : 4;   // B stages
+constexpr int kPR = kPWide ? 165888 : kPCan == 3 ? 5 * 32768 - 16384 : 4 * 32768;  // region R (>= 4 bf16 raw stages)
 constexpr int kPSmem = 1024 + kPR + kPBst * 128 * kKc * 2;  // R + B
 
 MOE_DEVI void produce4c(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, uint8_t* raw, uint64_t* bar, int lane) {
@@ -586,8 +593,8 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
     uint8_t* R = smem;
     uint8_t* Bst = smem + kPR;
     auto rawb = [&](int s) { return R + s * 32768; };
-    auto can = [&](int s) { return R + s * 32768; };
-    auto raw4 = [&](int s) { return R + kPCan * 32768 + s * kPRaw4Unit; };
+    auto can = [&](int s) { return R + s * kPCanBytes; };
+    auto raw4 = [&](int s) { return R + kPCan * kPCanBytes + s * kPRaw4Unit; };
     auto bst = [&](int s) { return Bst + s * kBTile; };
 
     pdl_wait();
@@ -704,8 +711,9 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                 const int b = kb % kBst;
                 int slot;
                 if (p4) {
-                    slot = c4 % kPCan;
-                    mbar_wait(&cn_full[slot], static_cast<uint32_t>((c4 / kPCan) & 1));
+                    const int cu = kPWide ? c4 >> 1 : c4;  // canonical stage use
+                    slot = cu % kPCan;
+                    if (!kPWide || (c4 & 1) == 0) mbar_wait(&cn_full[slot], static_cast<uint32_t>((cu / kPCan) & 1));
                 } else {
                     slot = cb % 4;
                     mbar_wait(&rb_full[slot], static_cast<uint32_t>((cb / 4) & 1));
@@ -713,7 +721,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                 mbar_wait(&b_full[b], static_cast<uint32_t>((kb / kBst) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 if (lane == 0) {
-                    const uint32_t ab = s32(p4 ? can(slot) : rawb(slot)), bb = s32(bst(b));
+                    const uint32_t ab = s32(p4 ? can(slot) + (kPWide ? (c4 & 1) * 32768 : 0) : rawb(slot)), bb = s32(bst(b));
 #pragma unroll
                     for (int j = 0; j < kKc / 16; ++j) {
                         const uint64_t bdesc = sdesc(bb + j * 32);
@@ -724,7 +732,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                             umma(dacc + mat * kN, adesc, bdesc, id, acc);
                         }
                     }
-                    umma_commit(p4 ? &cn_empty[slot] : &rb_empty[slot]);
+                    if (!p4 || !kPWide || (c4 & 1) == 1) umma_commit(p4 ? &cn_empty[slot] : &rb_empty[slot]);
                     umma_commit(&b_empty[b]);
                     if (kc == kc0 + nks - 1) umma_commit(&acc_full[buf]);
                 }
@@ -746,7 +754,21 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
             Tile tl;
             int kc0;
             if (!tile_of(i, tl, kc0)) break;  // past the routing's last tile
-            if (is_p4(tl)) {
+            if (is_p4(tl) && kPWide) {
+                for (int kc = kc0; kc < kc0 + nks; kc += 2, ++u4) {  // one hand-off per raw unit
+                    const int r = u4 % kPRaw4, c = u4 % kPCan;
+                    mbar_wait(&r4_full[r], static_cast<uint32_t>((u4 / kPRaw4) & 1));
+                    if (u4 >= kPCan) mbar_wait(&cn_empty[c], static_cast<uint32_t>(((u4 / kPCan) - 1) & 1));
+                    convert_int4c(nmat, raw4(r), can(c), ct, o0);
+                    convert_int4c(nmat, raw4(r), can(c) + 32768, ct, o1);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&cn_full[c]);
+                        mbar_arrive(&r4_empty[r]);
+                    }
+                }
+            } else if (is_p4(tl)) {
                 for (int kc = kc0; kc < kc0 + nks; ++kc, ++c4) {
                     const int r = u4 % kPRaw4, c = c4 % kPCan;
                     if ((kc & 1) == 0) mbar_wait(&r4_full[r], static_cast<uint32_t>((u4 / kPRaw4) & 1));
