@@ -74,7 +74,10 @@ struct StreamCfg {
 using CfgBatch = StreamCfg<8, 8192, 4608>;
 // batch-1 decode: each segment's single activation row (and its int4 bias
 // terms) is loaded once per launch into shared memory; items carry only weights
-using CfgDecode = StreamCfg<8, 8192, 0, true>;
+#ifndef MOE_DECODE_ITEM
+#define MOE_DECODE_ITEM 8192  // bytes of weights per batch-1 item (A/B: 4096)
+#endif
+using CfgDecode = StreamCfg<8, MOE_DECODE_ITEM, 0, true>;
 constexpr int kChunk = 2;                // items per dynamic tail chunk
 constexpr int kSmallPool = 5000;         // pools up to this many items are handed out one item per grab
 constexpr int kMaxSlots = 512;           // permutation slots staged in smem by build_segs
@@ -1475,7 +1478,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
 // finalize_out (sum_kparts, swiglu_store), so the output is bit-identical to
 // the per-layer kernels.  Counters live per layer in a.flow_ctl; the last
 // CTA to finish zeroes them for the next step.
-constexpr int kFlowStage = 8192 + 256;             // ring stage: one 8 KB item + its int4 scales
+constexpr int kFlowStage = CfgDecode::kW + CfgDecode::kW / 32;  // ring stage: one item + its int4 scales
 constexpr int kFlowMaxChunks = 16;                    // 1024-row h chunks per slot (f <= 16384)
 constexpr uint32_t kFlowSentinel = 0xffffffffu;       // "no partial here" (memset 0xff)
 
@@ -1627,6 +1630,35 @@ MOE_DEVI float4 sum_kparts_r(const float* p, size_t kstride, int KP, int kg, boo
     return acc;
 }
 
+// The same for 8 * kKG < KP <= 16 * kKG: sum_kparts' two passes,
+// acc_u = (0 + v(kg + u*kKG)) + v(kg + 64 + u*kKG) (0 past KP).
+MOE_DEVI float4 sum_kparts_r2(const float* p, size_t kstride, int KP, int kg, bool* miss) {
+    float4 acc;
+    bool m = false;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const float4 v = kg + u * kKG < KP ? ld_relaxed_f4(p + (kg + u * kKG) * kstride) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 w = kg + 8 * kKG + u * kKG < KP ? ld_relaxed_f4(p + (kg + 8 * kKG + u * kKG) * kstride)
+                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        m |= has_sentinel(v) || has_sentinel(w);
+        float4 e = make_float4(0.f + v.x, 0.f + v.y, 0.f + v.z, 0.f + v.w);
+        if (kg + 8 * kKG < KP) {
+            e.x += w.x; e.y += w.y; e.z += w.z; e.w += w.w;
+        }
+        if (u == 0) {
+            acc = e;
+        } else {
+            acc.x += e.x; acc.y += e.y; acc.z += e.z; acc.w += e.w;
+        }
+    }
+    *miss = *miss || m;
+    return acc;
+}
+
+MOE_DEVI float4 sum_kparts_any(const float* p, size_t kstride, int KP, int kg, bool* miss) {
+    return KP > 8 * kKG ? sum_kparts_r2(p, kstride, KP, kg, miss) : sum_kparts_r(p, kstride, KP, kg, miss);
+}
+
 // sum over kg of sum_kparts(p, kstride, KP, kg), added in kg order: the
 // finalize kernels' K-part reduction of 4 rows, for one lane.  KP <= 16
 // keeps every partial in registers (all loads in flight at once).
@@ -1659,10 +1691,10 @@ MOE_DEVI float4 kpart_total(const float* p, size_t kstride, int KP, bool* miss) 
         }
         return tot;
     }
-    float4 tot = sum_kparts_r(p, kstride, KP, 0, miss);
+    float4 tot = sum_kparts_any(p, kstride, KP, 0, miss);
 #pragma unroll
     for (int kg = 1; kg < kKG; ++kg) {
-        const float4 c = sum_kparts_r(p, kstride, KP, kg, miss);
+        const float4 c = sum_kparts_any(p, kstride, KP, kg, miss);
         tot.x += c.x; tot.y += c.y; tot.z += c.z; tot.w += c.w;
     }
     return tot;
@@ -1865,7 +1897,7 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
                     jx[h] = (b + (i < 0 ? 0 : i) * grid) * 16 + q * 4;
 #pragma unroll
                     for (int jj = 0; jj < 2; ++jj)
-                        rr[h][jj] = i >= 0 && jj < k ? sum_kparts_r(P1 + static_cast<size_t>(s_inv[jj]) * d + jx[h],
+                        rr[h][jj] = i >= 0 && jj < k ? sum_kparts_any(P1 + static_cast<size_t>(s_inv[jj]) * d + jx[h],
                                                                     kstride1, T.kp[1][s_inv[jj]], kg, &miss[h])
                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
@@ -2336,6 +2368,8 @@ cudaError_t moek_decode_flow(const MoeDecodeArgs& a, cudaStream_t stream) {
     const size_t smem = moek_decode_flow_smem(a.d, a.f);
     const FlowShape sh = flow_shape();
     if (sh.nw == 15 && sh.ns == 1) return launch_flow<15, 1>(a, smem, stream);
+    if (sh.nw == 15 && sh.ns == 2) return launch_flow<15, 2>(a, smem, stream);
+    if (sh.nw == 11 && sh.ns == 2) return launch_flow<11, 2>(a, smem, stream);
     if (sh.nw == 11 && sh.ns == 1) return launch_flow<11, 1>(a, smem, stream);
     if (sh.nw == 7 && sh.ns == 2) return launch_flow<7, 2>(a, smem, stream);
     if (sh.nw == 8 && sh.ns == 2) return launch_flow<8, 2>(a, smem, stream);
