@@ -35,7 +35,9 @@ def main():
           and re.match(r'^[\d.,]+$', r[i] or 'x')]
     tot = sum(v for _, v in st)
     print('stalls:', ', '.join(f"{k.split('stalled_')[1]}={v / tot:.2f}" for k, v in sorted(st, key=lambda x: -x[1])[:9]))
-    src = list(csv.reader(io.StringIO(run([rep, '--page', 'source', '--csv', '--print-source', 'sass']))))
+    # the source page of launch idx alone (an unfiltered export repeats the first kernel's block)
+    src = list(csv.reader(io.StringIO(run([rep, '--page', 'source', '--csv', '--print-source', 'sass',
+                                           '--launch-skip', str(idx), '--launch-count', '1']))))
     hh = src[1]
     si, ie = hh.index('Warp Stall Sampling (All Samples)'), hh.index('Instructions Executed')
     blocks, cur = [], None
@@ -46,7 +48,7 @@ def main():
             continue
         if cur is not None and len(row) > si and row[si].isdigit():
             cur.append(row)
-    data = blocks[idx]
+    data = blocks[0]
     mix, smp = collections.Counter(), collections.Counter()
     for row in data:
         ins = re.sub(r'^@!?U?P\w+\s+', '', row[1].strip())
