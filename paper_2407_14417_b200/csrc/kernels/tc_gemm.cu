@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cstdio>
 #include "common.cuh"
 #include "launch.h"
 
@@ -55,7 +56,8 @@ struct TcArgs {
     float* y;                 // pass 1: y [T*k][d]
     uint64_t active_mask;
     int dbg;                  // debug: bit0 skip convert, bit1 skip MMA, bit2 skip weight loads,
-                              // bit5 bf16 halves as separate 2 KB reads (no pairing)
+                              // bit5 bf16 halves as separate 2 KB reads (no pairing),
+                              // bit11 skip epilogue stores, bit12 skip B loads
     moe_expert_weights ex[MOE_MAX_EXPERTS];
 };
 
@@ -94,6 +96,43 @@ MOE_DEVI void umma(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t id, uint32_t
         "l"(a), "l"(b), "r"(id), "r"(accum)
         : "memory");
 }
+// SiLU for the tcgen05 epilogues (MUFU ex2 + fast divide, a few ulp of fp32,
+// far inside the bf16 rounding of h): the pass-0 epilogue holds the
+// accumulator while it runs, so its instruction count is on the critical path
+MOE_DEVI float silu_fast(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
+// silu(g) = g/2 * (1 + tanh(g/2)): one MUFU op instead of two (ex2 + rcp) --
+// the pass-0 drain of tc_ffn_wide is MUFU-bound; tanh.approx's ~2^-11
+// relative error stays below h's bf16 rounding step (2^-8)
+MOE_DEVI float silu_tanh(float g) {
+    const float hg = 0.5f * g;
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(hg));
+    return __fmaf_rn(hg, t, hg);
+}
+
+// (lo, hi) -> packed bf16x2, round to nearest even (one F2FP; NaN -> 0x7fff, not f2bf's 0x7fc0)
+MOE_DEVI uint32_t bf16x2_rn(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// Warp-converged forms: every lane runs the issue loop with warp-uniform
+// operands (kept in uniform registers, no per-MMA R2UR / elect waterfall) and
+// one elected lane issues.
+MOE_DEVI void umma_elect(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t id, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(dtmem),
+        "l"(a), "l"(b), "r"(id), "r"(accum)
+        : "memory");
+}
+MOE_DEVI void umma_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(s32(bar))
+        : "memory");
+}
 MOE_DEVI void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(bar))
                  : "memory");
@@ -104,6 +143,11 @@ MOE_DEVI int swz(int row, int kbyte) {
     return (row >> 3) * 1024 + (row & 7) * 128 + ((((kbyte >> 4) ^ (row & 7)) & 7) << 4) + (kbyte & 15);
 }
 
+#define TMEM_LD16(taddr, v)                                                                                       \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),      \
+                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]) \
+                 : "r"(taddr))
 #define TMEM_LD32(taddr, v)                                                                                       \
     asm volatile(                                                                                                 \
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
@@ -406,6 +450,10 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
             for (int kb = 0; kb < nk; ++kb) {
                 const int b = kb % kBst;
                 if (kb >= kBst) mbar_wait(&b_empty[b], ((kb / kBst) - 1) & 1);
+                if (a.dbg & 4096) {
+                    mbar_arrive(&b_full[b]);
+                    continue;
+                }
                 mbar_expect_tx(&b_full[b], static_cast<uint32_t>(nbox) * 64 * 128);
                 for (int q = 0; q < nbox; ++q) tma_load_b(bst(b) + q * 8192, tm, kb * kKc, tl.slot0 + q * 64, &b_full[b]);
             }
@@ -466,7 +514,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
         const int row = (warp & 3) * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const int c0 = ((warp - 4) >> 2) * (kN / 2);
-        for (int cb = c0; cb < c0 + kN / 2; cb += 32) {
+        for (int cb = c0; cb < c0 + kN / 2 && !(a.dbg & 2048); cb += 32) {
             uint32_t g[32];
             TMEM_LD32(tmem + lane_base + cb, g);
             if (a.p == 0) {
@@ -477,11 +525,13 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
                 for (int c = 0; c < 32; ++c) {
                     const int n = cb + c;
                     if (n < tl.m) {
-                        const uint16_t hb = f2bf(silu_f(__uint_as_float(g[c])) * __uint_as_float(u[c]));
+                        const uint16_t hb = f2bf(silu_fast(__uint_as_float(g[c])) * __uint_as_float(u[c]));
                         const size_t o = static_cast<size_t>(tl.slot0 + n) * a.f + tl.R0 + row;
                         a.hout[o] = hb;
-                        if (f16_overflow(bf2f(hb))) numerics_flag(MOE_NUM_F16_ACT);
-                        a.hout16[o] = __half_as_ushort(__float2half_rn(bf2f(hb)));
+                        if (p4) {  // the fp16 copy feeds only an int4 down pass
+                            if (f16_overflow(bf2f(hb))) numerics_flag(MOE_NUM_F16_ACT);
+                            a.hout16[o] = __half_as_ushort(__float2half_rn(bf2f(hb)));
+                        }
                     }
                 }
             } else {
@@ -798,11 +848,13 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                     for (int c = 0; c < 32; ++c) {
                         const int n = cbk + c;
                         if (n < tl.m) {
-                            const uint16_t hb = f2bf(silu_f(__uint_as_float(g[c])) * __uint_as_float(u[c]));
+                            const uint16_t hb = f2bf(silu_fast(__uint_as_float(g[c])) * __uint_as_float(u[c]));
                             const size_t o = static_cast<size_t>(tl.slot0 + n) * a.f + tl.R0 + row;
                             a.hout[o] = hb;
-                            if (f16_overflow(bf2f(hb))) numerics_flag(MOE_NUM_F16_ACT);
-                            a.hout16[o] = __half_as_ushort(__float2half_rn(bf2f(hb)));
+                            if (is_p4(tl)) {  // the fp16 copy feeds only an int4 down pass
+                                if (f16_overflow(bf2f(hb))) numerics_flag(MOE_NUM_F16_ACT);
+                                a.hout16[o] = __half_as_ushort(__float2half_rn(bf2f(hb)));
+                            }
                         }
                     }
                 } else {
@@ -851,6 +903,270 @@ __global__ void split_reduce_kernel(const float4* __restrict__ ypart, const int3
             }
             y[i] = acc;
         }
+    }
+}
+
+// ===========================================================================
+// Persistent bf16 256-token variant (tc_ffn_wide): prefill-sized launches.
+// One CTA per SM walks the tile list like tc_ffn_persist, at N = 256 (the
+// operand bytes per MMA flop of a 128 x 256 tile are 3/4 of a 128 x 128
+// tile's).  Shared memory: kWRaw 32 KB weight stages + kWB 32 KB B stages.
+// TMEM: pass 0 needs gate + up = 512 columns, so one accumulator: the
+// epilogue warps read their 128 columns of both into registers (h packed to
+// bf16, 64 registers), release the accumulator, and store while the next
+// tile's MMAs run; pass 1 (256 columns) double-buffers the accumulator.
+#ifndef MOE_TCW_RAW
+#define MOE_TCW_RAW 4
+#endif
+#ifndef MOE_TCW_B
+#define MOE_TCW_B 3
+#endif
+#ifndef MOE_TCW_A1
+#define MOE_TCW_A1 4
+#endif
+constexpr int kWRaw = MOE_TCW_RAW, kWB = MOE_TCW_B, kWA1 = MOE_TCW_A1;
+constexpr int kWSmem = 1024 + kWRaw * 32768 + kWB * 256 * kKc * 2;
+constexpr int kWB1 = (kWSmem - 1024 - kWA1 * 16384) / (256 * kKc * 2);  // pass-1 B stages
+constexpr int kWMaxA = kWRaw > kWA1 ? kWRaw : kWA1, kWMaxB = kWB > kWB1 ? kWB : kWB1;
+static_assert(kWB1 >= 1, "pass-1 stage split");
+static_assert(kWSmem + 1024 <= 232448, "tc_ffn_wide stages exceed shared memory");
+#ifndef MOE_TCW_PF
+#define MOE_TCW_PF 0
+#endif
+constexpr int kWPf = MOE_TCW_PF;  // weight L2 prefetch distance (chunks; even, 0 = off)
+static_assert(kWPf % 2 == 0, "prefetch whole 128-K blocks");
+
+// MOE_TC_DBG bit 15: CTA 0 stamps (SM clock) of its third tile's chunks -- weight
+// issue, B issue, weight full seen by the MMA thread, B full seen, MMA
+// committed -- printed at exit (latency probe)
+__device__ unsigned int g_wtrace[5][64];
+MOE_DEVI unsigned int clk32() {
+    unsigned int c;
+    asm volatile("mov.u32 %0, %%clock;" : "=r"(c));
+    return c;
+}
+
+__global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide(const __grid_constant__ TcArgs a, int ntiles) {
+    constexpr int kN = 256, kBTile = kN * kKc * 2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
+    __shared__ __align__(8) uint64_t rb_full[kWMaxA], rb_empty[kWMaxA], b_full[kWMaxB], b_empty[kWMaxB], acc_full[2],
+        acc_empty[2];
+    __shared__ uint32_t tmem_slot;
+    __shared__ int s_off[MOE_MAX_EXPERTS + 1];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nmat = a.p == 0 ? 2 : 1;
+    // pass 0: kWRaw 32 KB weight stages + kWB B stages; pass 1 (16 KB weight
+    // stages): kWA1 weight stages and the rest of the pool as B stages
+    const int nA = a.p == 0 ? kWRaw : kWA1, nB = a.p == 0 ? kWB : kWB1;
+    const int sA = nmat * kRawA;
+    auto rawb = [&](int s) { return smem + s * sA; };
+    auto bst = [&](int s) { return smem + nA * sA + s * kBTile; };
+
+    pdl_wait();
+    pdl_trigger();
+    const int K = a.p == 0 ? a.d : a.f;
+    const int RT = (a.p == 0 ? a.f : a.d) / kM;
+    const int nk = K / kKc;
+    const int grid = static_cast<int>(gridDim.x);
+    if (tid <= a.E) s_off[tid] = a.offsets[tid];
+    if (tid == 0) {
+        for (int s = 0; s < nA; ++s) {
+            mbar_init_n(&rb_full[s], 1);
+            mbar_init_n(&rb_empty[s], 1);  // MMA commit
+        }
+        for (int s = 0; s < nB; ++s) {
+            mbar_init_n(&b_full[s], 1);
+            mbar_init_n(&b_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init_n(&acc_full[s], 1);
+            mbar_init_n(&acc_empty[s], kConvThreads / 32);  // the epilogue warps
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tmem_slot)), "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_slot;
+    const int my_tiles = static_cast<int>(blockIdx.x) < ntiles ? (ntiles - static_cast<int>(blockIdx.x) + grid - 1) / grid : 0;
+    auto tile_of = [&](int i, Tile& tl) { return find_tile<256>(a, s_off, RT, static_cast<int>(blockIdx.x) + i * grid, tl); };
+    // accumulator use i: pass 0 has one buffer (use i waits for release i-1),
+    // pass 1 two (use i waits for release i-2)
+    const int nbuf = a.p == 0 ? 1 : 2;
+    const bool trace = (a.dbg & 32768) && blockIdx.x == 0;
+    auto stamp = [&](int w, int i, int kc) {
+        if (trace && i == 2 && kc < 64) g_wtrace[w][kc] = clk32();
+    };
+
+    if (warp == 0) {
+        // ---- weight producer: both 64-K halves of each 4 KB block back to back ----
+        int ub = 0;
+        const bool unpaired = a.dbg & 32;  // one 2 KB read per block and chunk, each stage refilled as it frees
+        const int pf = (a.dbg & 65536) ? 16 : kWPf;
+        for (int i = 0; i < my_tiles; ++i) {
+            Tile tl;
+            if (!tile_of(i, tl)) break;
+            const bool pf_cta = pf > 0 && (!(a.dbg & 131072) || tl.slot0 == s_off[tl.e]);  // bit 17: first token tile only
+            for (int kc = 0; kc < nk; kc += unpaired ? 1 : 2, ub += unpaired ? 1 : 2) {
+                const int r0 = ub % nA, r1 = (ub + 1) % nA;
+                if (ub >= nA) mbar_wait(&rb_empty[r0], static_cast<uint32_t>(((ub / nA) - 1) & 1));
+                if (!unpaired && ub + 1 >= nA) mbar_wait(&rb_empty[r1], static_cast<uint32_t>((((ub + 1) / nA) - 1) & 1));
+                stamp(0, i, kc);
+                if (pf_cta && (kc & 1) == 0 && kc + pf < nk && lane < 8) {
+                    // the 4 KB blocks pf chunks ahead into L2: the smem ring then waits on L2, not DRAM
+                    const moe_expert_weights& W = a.ex[tl.e];
+                    const uint8_t* wb = static_cast<const uint8_t*>(a.p == 0 ? W.w_gate_up : W.w_down);
+                    for (int mat = 0; mat < nmat; ++mat) {
+                        const int row0 = (a.p == 0 && mat == 1) ? a.f + tl.R0 : tl.R0;
+                        const size_t blk = static_cast<size_t>(row0 / 16 + lane) * (K / 128) + ((kc + pf) >> 1);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 4096;" ::"l"(wb + blk * 4096) : "memory");
+                    }
+                }
+                if (a.dbg & 4) {
+                    if (lane == 0) {
+                        mbar_arrive(&rb_full[r0]);
+                        if (!unpaired) mbar_arrive(&rb_full[r1]);
+                    }
+                    __syncwarp();
+                } else if (unpaired) {
+                    produce(a, tl, nmat, K, kc, rawb(r0), &rb_full[r0], lane);
+                } else {
+                    produce_pair(a, tl, nmat, K, kc, rawb(r0), rawb(r1), &rb_full[r0], &rb_full[r1], lane);
+                }
+            }
+        }
+    } else if (warp == 2) {
+        // ---- B producer ----
+        if (lane == 0) {
+            int kb = 0;
+            for (int i = 0; i < my_tiles; ++i) {
+                Tile tl;
+                if (!tile_of(i, tl)) break;
+                const int nbox = (min(kN, (tl.m + 15) / 16 * 16) + 63) / 64;
+                for (int kc = 0; kc < nk; ++kc, ++kb) {
+                    const int b = kb % nB;
+                    if (kb >= nB) mbar_wait(&b_empty[b], static_cast<uint32_t>(((kb / nB) - 1) & 1));
+                    stamp(1, i, kc);
+                    if (a.dbg & 4096) {
+                        mbar_arrive(&b_full[b]);
+                        continue;
+                    }
+                    mbar_expect_tx(&b_full[b], static_cast<uint32_t>(nbox) * 64 * 128);
+                    for (int q = 0; q < nbox; ++q) tma_load_b(bst(b) + q * 8192, &a.tmb, kc * kKc, tl.slot0 + q * 64, &b_full[b]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---- MMA issuer ----
+        int kb = 0;
+        for (int i = 0; i < my_tiles; ++i) {
+            Tile tl;
+            if (!tile_of(i, tl)) break;
+            const int nmma = min(kN, (tl.m + 15) / 16 * 16);
+            const uint32_t id = idesc(1, nmma, kM);
+            const int buf = i % nbuf;
+            if (i >= nbuf) mbar_wait(&acc_empty[buf], static_cast<uint32_t>(((i / nbuf) - 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t dacc = tmem + buf * kN;
+            for (int kc = 0; kc < nk; ++kc, ++kb) {
+                const int r = kb % nA, b = kb % nB;
+                mbar_wait(&rb_full[r], static_cast<uint32_t>((kb / nA) & 1));
+                if (lane == 0) stamp(2, i, kc);
+                mbar_wait(&b_full[b], static_cast<uint32_t>((kb / nB) & 1));
+                if (lane == 0) stamp(3, i, kc);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t ab = s32(rawb(r)), bb = s32(bst(b));
+                if (a.dbg & 8192) {  // handshake probe: plain arrives instead of commits
+                    if (lane == 0) {
+                        mbar_arrive(&rb_empty[r]);
+                        mbar_arrive(&b_empty[b]);
+                        if (kc == nk - 1) mbar_arrive(&acc_full[buf]);
+                    }
+                } else {
+                    if (!(a.dbg & 2)) {
+#pragma unroll
+                        for (int j = 0; j < kKc / 16; ++j) {
+                            const uint64_t bdesc = sdesc(bb + j * 32);
+                            const uint32_t acc = (kc > 0 || j > 0) ? 1u : 0u;
+                            umma_elect(dacc, sdesc_core(ab + j * 256), bdesc, id, acc);
+                            if (nmat == 2) umma_elect(dacc + kN, sdesc_core(ab + kRawA + j * 256), bdesc, id, acc);
+                        }
+                    }
+                    umma_commit_elect(&rb_empty[r]);
+                    umma_commit_elect(&b_empty[b]);
+                    if (kc == nk - 1) umma_commit_elect(&acc_full[buf]);
+                }
+                if (lane == 0) stamp(4, i, kc);
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 4) {
+        // ---- epilogue ----
+        const int row = (warp & 3) * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const int c0 = ((warp - 4) >> 2) * (kN / 2);
+        for (int i = 0; i < my_tiles; ++i) {
+            Tile tl;
+            if (!tile_of(i, tl)) break;
+            const int buf = i % nbuf;
+            mbar_wait(&acc_full[buf], static_cast<uint32_t>((i / nbuf) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t dacc = tmem + buf * kN;
+            if (a.p == 0) {
+                // h for this thread's row x 128 columns, packed, then the accumulator is free
+                uint32_t hp[kN / 4];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    uint32_t g[16], u[16];
+                    TMEM_LD16(dacc + lane_base + c0 + q * 16, g);
+                    TMEM_LD16(dacc + lane_base + kN + c0 + q * 16, u);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int c = 0; c < 16; c += 2) {
+                        hp[q * 8 + c / 2] = bf16x2_rn(silu_tanh(__uint_as_float(g[c])) * __uint_as_float(u[c]),
+                                                      silu_tanh(__uint_as_float(g[c + 1])) * __uint_as_float(u[c + 1]));
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[buf]);
+                if (!(a.dbg & 2048)) {
+                    uint16_t* ho = a.hout + static_cast<size_t>(tl.slot0 + c0) * a.f + tl.R0 + row;
+#pragma unroll
+                    for (int c = 0; c < kN / 2; ++c)
+                        if (c0 + c < tl.m) ho[static_cast<size_t>(c) * a.f] = static_cast<uint16_t>(hp[c >> 1] >> ((c & 1) * 16));
+                }
+            } else {
+                for (int cbk = c0; cbk < c0 + kN / 2 && cbk < tl.m && !(a.dbg & 2048); cbk += 32) {
+                    uint32_t g[32];
+                    TMEM_LD32(dacc + lane_base + cbk, g);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        if (cbk + c < tl.m)
+                            a.y[static_cast<size_t>(tl.slot0 + cbk + c) * a.d + tl.R0 + row] = __uint_as_float(g[c]);
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[buf]);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    if (trace && tid == 0 && my_tiles > 2) {
+        const unsigned int t0 = g_wtrace[0][0];
+        for (int kc = 0; kc < min(nk, 64); ++kc)
+            printf("WTRACE p%d kc %2d wiss %7d biss %7d wfull %7d bfull %7d mma %7d\n", a.p, kc, g_wtrace[0][kc] - t0,
+                   g_wtrace[1][kc] - t0, g_wtrace[2][kc] - t0, g_wtrace[3][kc] - t0, g_wtrace[4][kc] - t0);
     }
 }
 
@@ -972,6 +1288,25 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
         MOE_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
     }
+    // wide launches: bf16 experts through the persistent tc_ffn_wide (MOE_TC_DBG
+    // bit 14: off), int4 experts through tc_ffn_kernel<256>
+    uint64_t mask16 = 0;
+    for (int e = 0; e < E; ++e)
+        if (((active_mask >> e) & 1ull) && experts[e].precision != MOE_P4) mask16 |= 1ull << e;
+    const bool wpers = wide && mask16 != 0 && !(dbg & 16384);
+    const uint64_t mask_single = wpers ? (active_mask & ~mask16) : active_mask;
+    static bool wide_attr = false;
+    if (wpers && !wide_attr) {
+        MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem));
+        wide_attr = true;
+    }
+    auto launch_wide = [&](int rows) -> cudaError_t {
+        TcArgs aw = a;
+        aw.active_mask = mask16;
+        const int nt = ntiles_max * (rows / kM);
+        return moek::launch_pdl(tc_ffn_wide, dim3(static_cast<unsigned>(std::min(nt, sms))), dim3(kThreads2), kWSmem,
+                                stream, aw, nt);
+    };
     // exact tile counts per pass need the routing (device); the persistent grid instead
     // walks tiles [0, ntiles_max * RT) and skips the empty ones (find_tile returns false)
     // pass 0: gate/up + SwiGLU -> h
@@ -985,8 +1320,13 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
         MOE_CUDA_OK(moek::launch_pdl(tc_ffn_persist, dim3(static_cast<unsigned>(std::min(nt0, sms))), dim3(kThreads2), kPSmem,
                                      stream, a, nt0, 1, static_cast<float*>(nullptr)));
     } else {
-        MOE_CUDA_OK(moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (f / kM))), dim3(kThreads2), smem,
-                                     stream, a));
+        if (wpers) MOE_CUDA_OK(launch_wide(f));
+        if (mask_single) {
+            TcArgs as = a;
+            as.active_mask = mask_single;
+            MOE_CUDA_OK(moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (f / kM))), dim3(kThreads2), smem,
+                                         stream, as));
+        }
     }
     // pass 1: down -> y
     a.p = 1;
@@ -1004,8 +1344,12 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
                                 stream, reinterpret_cast<const float4*>(ypart), offsets, E, active_mask,
                                 static_cast<int>(slots), d / 4, ns, reinterpret_cast<float4*>(y));
     }
+    if (wpers) MOE_CUDA_OK(launch_wide(d));
+    if (!mask_single) return cudaSuccess;
+    TcArgs as = a;
+    as.active_mask = mask_single;
     return moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (d / kM))), dim3(kThreads2), smem, stream,
-                            a);
+                            as);
 }
 
 MOE_NUMERICS_BINDER(tc)
@@ -1020,6 +1364,7 @@ cudaError_t moek_preload_tc() {
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_kernel<256>));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_persist));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::split_reduce_kernel));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_wide));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::gather_rows_kernel));
     return cudaSuccess;
 }

@@ -9,7 +9,7 @@ import paper_2407_14417_b200 as moe  # noqa: E402
 
 pts = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "2048,4096").split(",")]
 prof1 = moe.profile_for_shape(bench.D_MODEL, bench.D_FFN, 1, bench.EXPERTS, bench.TOPK)
-for prec in (1, 0):
+for prec in [int(p) for p in os.environ.get("PREC", "1,0").split(",")]:
     plan1 = moe.assign_locations([prec] * bench.EXPERTS, moe.HardwareProfile(10**15), prof1)
     eng = moe.MoeEngine(1, bench.EXPERTS, bench.TOPK, bench.D_MODEL, bench.D_FFN, plan1, max_tokens=max(pts), seed=0,
                         norm_eps=bench.NORM_EPS)
