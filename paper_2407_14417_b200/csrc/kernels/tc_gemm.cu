@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
                 mbar_wait(&raw_full[r], (kc / nraw) & 1);
             mbar_wait(&b_full[b], (kc / kBst) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (lane == 0) {
+            {  // warp-converged issue (umma_elect)
                 const uint32_t cb = s32(can(c)), rb = s32(raw(r)), bb = s32(bst(b));
 #pragma unroll
                 for (int j = 0; j < kKc / 16; ++j) {
@@ -481,14 +481,13 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_kernel(const __grid_const
                     for (int mat = 0; mat < nmat; ++mat) {
                         const uint64_t adesc = p4 ? sdesc(cb + mat * kTileBytes + j * 32)
                                                   : sdesc_core(rb + mat * kRawA + j * 256);
-                        umma(tmem + mat * kN, adesc, bdesc, id, acc);
+                        umma_elect(tmem + mat * kN, adesc, bdesc, id, acc);
                     }
                 }
-                umma_commit(p4 ? &can_empty[c] : &raw_empty[r]);
-                umma_commit(&b_empty[b]);
-                if (kc == nk - 1) umma_commit(&acc_full);
+                umma_commit_elect(p4 ? &can_empty[c] : &raw_empty[r]);
+                umma_commit_elect(&b_empty[b]);
+                if (kc == nk - 1) umma_commit_elect(&acc_full);
             }
-            __syncwarp();
         }
     } else if (warp >= 4) {
         // ---- converters, then the epilogue ----
@@ -770,7 +769,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                 }
                 mbar_wait(&b_full[b], static_cast<uint32_t>((kb / kBst) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (lane == 0) {
+                {  // warp-converged issue (umma_elect)
                     const uint32_t ab = s32(p4 ? can(slot) + (kPWide ? (c4 & 1) * 32768 : 0) : rawb(slot)), bb = s32(bst(b));
 #pragma unroll
                     for (int j = 0; j < kKc / 16; ++j) {
@@ -779,14 +778,13 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                         for (int mat = 0; mat < nmat; ++mat) {
                             const uint64_t adesc = p4 ? sdesc(ab + mat * kTileBytes + j * 32)
                                                       : sdesc_core(ab + mat * kRawA + j * 256);
-                            umma(dacc + mat * kN, adesc, bdesc, id, acc);
+                            umma_elect(dacc + mat * kN, adesc, bdesc, id, acc);
                         }
                     }
-                    if (!p4 || !kPWide || (c4 & 1) == 1) umma_commit(p4 ? &cn_empty[slot] : &rb_empty[slot]);
-                    umma_commit(&b_empty[b]);
-                    if (kc == kc0 + nks - 1) umma_commit(&acc_full[buf]);
+                    if (!p4 || !kPWide || (c4 & 1) == 1) umma_commit_elect(p4 ? &cn_empty[slot] : &rb_empty[slot]);
+                    umma_commit_elect(&b_empty[b]);
+                    if (kc == kc0 + nks - 1) umma_commit_elect(&acc_full[buf]);
                 }
-                __syncwarp();
                 if (p4) ++c4; else ++cb;
             }
         }
