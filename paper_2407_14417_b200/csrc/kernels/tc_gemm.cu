@@ -571,10 +571,21 @@ constexpr int kPRaw4Unit = 2 * 8192 + 2 * kRawS;  // compact int4 raw unit: [A_g
 constexpr bool kPWide = MOE_TCP_WIDE != 0;
 constexpr int kPCan = kPWide ? 2 : MOE_TCP_CAN;     // int4 canonical A stages in R
 constexpr int kPCanBytes = kPWide ? 65536 : 32768;
-constexpr int kPRaw4 = kPWide || kPCan == 3 ? 2 : 3;  // int4 raw units in R after them
-constexpr int kPBst = kPWide || kPCan == 3 ? 3 : 4;   // B stages
-constexpr int kPR = kPWide ? 165888 : kPCan == 3 ? 5 * 32768 - 16384 : 4 * 32768;  // region R (>= 4 bf16 raw stages)
+// MOE_TCP_RB: bf16 raw stages in R (32 KB each); MOE_TCP_B: B stages (16 KB; 0 = by kPCan)
+// 5 + 4 measured best for batched decode (4+4: -1..4 %, 6+2: -7 %, 6+1: -30 %)
+#ifndef MOE_TCP_RB
+#define MOE_TCP_RB 5
+#endif
+#ifndef MOE_TCP_B
+#define MOE_TCP_B 4
+#endif
+constexpr int kPRb = MOE_TCP_RB;
+constexpr int kPBst = MOE_TCP_B ? MOE_TCP_B : (kPWide || kPCan == 3 ? 3 : 4);  // B stages
+constexpr int kPR0 = kPWide ? 165888 : kPCan == 3 ? 5 * 32768 - 16384 : 4 * 32768;
+constexpr int kPR = kPR0 > kPRb * 32768 ? kPR0 : kPRb * 32768;  // region R
+constexpr int kPRaw4 = (kPR - kPCan * kPCanBytes) / kPRaw4Unit;  // int4 raw units in R after the canonical stages
 constexpr int kPSmem = 1024 + kPR + kPBst * 128 * kKc * 2;  // R + B
+static_assert(kPSmem + 1024 <= 232448 && kPRaw4 >= 2, "tc_ffn_persist stages exceed shared memory");
 
 MOE_DEVI void produce4c(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, uint8_t* raw, uint64_t* bar, int lane) {
     const moe_expert_weights& W = a.ex[tl.e];
@@ -634,7 +645,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
     constexpr int kN = 128, kBst = kPBst, kBTile = kN * kKc * 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
-    __shared__ __align__(8) uint64_t rb_full[4], rb_empty[4], r4_full[kPRaw4], r4_empty[kPRaw4], cn_full[kPCan], cn_empty[kPCan],
+    __shared__ __align__(8) uint64_t rb_full[kPRb], rb_empty[kPRb], r4_full[kPRaw4], r4_empty[kPRaw4], cn_full[kPCan], cn_empty[kPCan],
         b_full[kBst], b_empty[kBst], acc_full[2], acc_empty[2];
     __shared__ uint32_t tmem_slot;
     __shared__ int s_off[MOE_MAX_EXPERTS + 1];
@@ -655,7 +666,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
     const int grid = static_cast<int>(gridDim.x);
     if (tid <= a.E) s_off[tid] = a.offsets[tid];
     if (tid == 0) {
-        for (int s = 0; s < 4; ++s) {
+        for (int s = 0; s < kPRb; ++s) {
             mbar_init_n(&rb_full[s], 1);
             mbar_init_n(&rb_empty[s], 1);  // MMA commit
         }
@@ -716,9 +727,9 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                 }
             } else {
                 for (int kc = kc0; kc < kc0 + nks; kc += 2, ub += 2) {  // both 64-K halves of each 4 KB block
-                    const int r0 = ub % 4, r1 = (ub + 1) % 4;
-                    if (ub >= 4) mbar_wait(&rb_empty[r0], static_cast<uint32_t>(((ub / 4) - 1) & 1));
-                    if (ub + 1 >= 4) mbar_wait(&rb_empty[r1], static_cast<uint32_t>((((ub + 1) / 4) - 1) & 1));
+                    const int r0 = ub % kPRb, r1 = (ub + 1) % kPRb;
+                    if (ub >= kPRb) mbar_wait(&rb_empty[r0], static_cast<uint32_t>(((ub / kPRb) - 1) & 1));
+                    if (ub + 1 >= kPRb) mbar_wait(&rb_empty[r1], static_cast<uint32_t>((((ub + 1) / kPRb) - 1) & 1));
                     produce_pair(a, tl, nmat, K, kc, rawb(r0), rawb(r1), &rb_full[r0], &rb_full[r1], lane);
                 }
             }
@@ -764,8 +775,8 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                     slot = cu % kPCan;
                     if (!kPWide || (c4 & 1) == 0) mbar_wait(&cn_full[slot], static_cast<uint32_t>((cu / kPCan) & 1));
                 } else {
-                    slot = cb % 4;
-                    mbar_wait(&rb_full[slot], static_cast<uint32_t>((cb / 4) & 1));
+                    slot = cb % kPRb;
+                    mbar_wait(&rb_full[slot], static_cast<uint32_t>((cb / kPRb) & 1));
                 }
                 mbar_wait(&b_full[b], static_cast<uint32_t>((kb / kBst) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
