@@ -949,6 +949,7 @@ static_assert(kWPf % 2 == 0, "prefetch whole 128-K blocks");
 // issue, B issue, weight full seen by the MMA thread, B full seen, MMA
 // committed -- printed at exit (latency probe)
 __device__ unsigned int g_wtrace[5][64];
+__device__ unsigned int g_wtrace2[2][4][64];  // tc_ffn_wide2: [rank][weight issue, forwarder, pair full, MMA][chunk]
 MOE_DEVI unsigned int clk32() {
     unsigned int c;
     asm volatile("mov.u32 %0, %%clock;" : "=r"(c));
@@ -1179,6 +1180,280 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide(const __grid_constan
     }
 }
 
+// ===========================================================================
+// CTA-pair persistent variant (tc_ffn_wide2, clusters of 2): the same tile
+// loop as tc_ffn_wide with tcgen05.mma.cta_group::2, M = 256.  CTA r of a
+// pair holds rows R0 + 128r .. of the pair's 256-row tile (its own weights)
+// and tokens [r N/2, (r+1) N/2) of the tile's B, and accumulates its 128 rows
+// x N columns in its own TMEM.  Each SM's stages hold half of B, so the same
+// shared memory keeps more chunks in flight (pass 0: 48 KB per chunk instead
+// of 64, pass 1: 32 instead of 48) -- the operand streams are latency-bound.
+// Hand-offs: each CTA loads its own stages on its own barriers; a forwarder
+// lane per CTA arrives on the leader's pair barrier once both of its stages
+// landed; the leader's MMA warp issues, and its commits multicast the stage
+// releases and accumulator-ready signals to both CTAs; both CTAs' epilogue
+// warps release the accumulator on the leader's barrier.
+#ifndef MOE_TCW2_A0
+#define MOE_TCW2_A0 5
+#endif
+#ifndef MOE_TCW2_A1
+#define MOE_TCW2_A1 8
+#endif
+constexpr int kW2Pool = 224 * 1024;
+constexpr int kW2A0 = MOE_TCW2_A0, kW2B0 = (kW2Pool - kW2A0 * 32768) / 16384;  // pass 0: 32 KB A, 16 KB B stages
+constexpr int kW2A1 = MOE_TCW2_A1, kW2B1 = (kW2Pool - kW2A1 * 16384) / 16384;  // pass 1: 16 KB A, 16 KB B stages
+constexpr int kW2MaxA = kW2A0 > kW2A1 ? kW2A0 : kW2A1, kW2MaxB = kW2B0 > kW2B1 ? kW2B0 : kW2B1;
+constexpr int kW2Np = 16;  // pair-barrier ring (> the chunks a forwarder can run ahead)
+constexpr int kW2Smem = 1024 + kW2Pool;
+static_assert(kW2MaxA < kW2Np && kW2MaxB < kW2Np && kW2B0 >= 2 && kW2B1 >= 2, "tc_ffn_wide2 stage split");
+
+MOE_DEVI uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+MOE_DEVI void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+MOE_DEVI uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+MOE_DEVI void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+MOE_DEVI void mbar_arrive_remote_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+MOE_DEVI void umma2_elect(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t id, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(dtmem),
+        "l"(a), "l"(b), "r"(id), "r"(accum)
+        : "memory");
+}
+MOE_DEVI void umma2_commit_both_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b16 m;\n\telect.sync _|e, 0xffffffff;\n\tmov.b16 m, 3;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}" ::"r"(
+            s32(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_constant__ TcArgs a, int ntiles) {
+    constexpr int kN = 256, kBHalf = 128 * kKc * 2;  // 16 KB: 128 token rows x 64 K
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
+    __shared__ __align__(8) uint64_t rb_full[kW2MaxA], rb_empty[kW2MaxA], b_full[kW2MaxB], b_empty[kW2MaxB],
+        pair_full[kW2Np], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_slot;
+    __shared__ int s_off[MOE_MAX_EXPERTS + 1];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int nmat = a.p == 0 ? 2 : 1;
+    const int nA = a.p == 0 ? kW2A0 : kW2A1, nB = a.p == 0 ? kW2B0 : kW2B1;
+    const int sA = nmat * kRawA;
+    auto rawb = [&](int s) { return smem + s * sA; };
+    auto bst = [&](int s) { return smem + nA * sA + s * kBHalf; };
+
+    pdl_wait();
+    pdl_trigger();
+    const int K = a.p == 0 ? a.d : a.f;
+    const int RP = (a.p == 0 ? a.f : a.d) / (2 * kM);  // 256-row pair tiles per expert
+    const int nk = K / kKc;
+    const int npair = static_cast<int>(gridDim.x) / 2, pair = static_cast<int>(blockIdx.x) / 2;
+    if (tid <= a.E) s_off[tid] = a.offsets[tid];
+    if (tid == 0) {
+        for (int s = 0; s < nA; ++s) {
+            mbar_init_n(&rb_full[s], 1);
+            mbar_init_n(&rb_empty[s], 1);  // the leader's multicast commit
+        }
+        for (int s = 0; s < nB; ++s) {
+            mbar_init_n(&b_full[s], 1);
+            mbar_init_n(&b_empty[s], 1);
+        }
+        for (int s = 0; s < kW2Np; ++s) mbar_init_n(&pair_full[s], 2);  // one forwarder arrival per CTA
+        for (int s = 0; s < 2; ++s) {
+            mbar_init_n(&acc_full[s], 1);
+            mbar_init_n(&acc_empty[s], 2 * (kConvThreads / 32));  // both CTAs' epilogue warps
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tmem_slot)), "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();  // the peer's barriers exist before any remote arrive or multicast commit
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_slot;
+    const int my_tiles = pair < ntiles ? (ntiles - pair + npair - 1) / npair : 0;
+    // the pair's tile i: 256 rows (this CTA's 128 at R0) x up to 256 tokens; both CTAs agree
+    auto tile_of = [&](int i, Tile& tl) {
+        if (!find_tile<256>(a, s_off, RP, pair + i * npair, tl)) return false;
+        tl.R0 = tl.R0 * 2 + static_cast<int>(rank) * kM;  // find_tile's R0 = pair-row-tile * 128
+        return true;
+    };
+    auto n_of = [&](const Tile& tl) { return min(kN, (tl.m + 31) / 32 * 32); };  // both halves whole 16-column steps
+    const int nbuf = a.p == 0 ? 1 : 2;
+    const bool trace = (a.dbg & 32768) && blockIdx.x < 2;
+    auto stamp = [&](int w, int i, int kc) {
+        if (trace && i == 2 && kc < 64) g_wtrace2[rank][w][kc] = clk32();
+    };
+
+    if (warp == 0) {
+        // ---- this CTA's weight rows, both 64-K halves of each 4 KB block back to back ----
+        int ub = 0;
+        for (int i = 0; i < my_tiles; ++i) {
+            Tile tl;
+            if (!tile_of(i, tl)) break;
+            for (int kc = 0; kc < nk; kc += 2, ub += 2) {
+                const int r0 = ub % nA, r1 = (ub + 1) % nA;
+                if (ub >= nA) mbar_wait(&rb_empty[r0], static_cast<uint32_t>(((ub / nA) - 1) & 1));
+                if (ub + 1 >= nA) mbar_wait(&rb_empty[r1], static_cast<uint32_t>((((ub + 1) / nA) - 1) & 1));
+                if (lane == 0) stamp(0, i, kc);
+                produce_pair(a, tl, nmat, K, kc, rawb(r0), rawb(r1), &rb_full[r0], &rb_full[r1], lane);
+            }
+        }
+    } else if (warp == 2) {
+        // ---- this CTA's half of the tile's tokens ----
+        if (lane == 0) {
+            int kb = 0;
+            for (int i = 0; i < my_tiles; ++i) {
+                Tile tl;
+                if (!tile_of(i, tl)) break;
+                const int halfn = n_of(tl) / 2, nbox = (halfn + 63) / 64;
+                const int row0 = tl.slot0 + static_cast<int>(rank) * halfn;
+                for (int kc = 0; kc < nk; ++kc, ++kb) {
+                    const int b = kb % nB;
+                    if (kb >= nB) mbar_wait(&b_empty[b], static_cast<uint32_t>(((kb / nB) - 1) & 1));
+                    mbar_expect_tx(&b_full[b], static_cast<uint32_t>(nbox) * 64 * 128);
+                    for (int q = 0; q < nbox; ++q) tma_load_b(bst(b) + q * 8192, &a.tmb, kc * kKc, row0 + q * 64, &b_full[b]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 3) {
+        // ---- forwarder: both of this CTA's stages of chunk kb landed -> the leader's pair barrier ----
+        if (lane == 0) {
+            int kb = 0;
+            for (int i = 0; i < my_tiles; ++i) {
+                Tile tl;
+                if (!tile_of(i, tl)) break;
+                for (int kc = 0; kc < nk; ++kc, ++kb) {
+                    mbar_wait(&rb_full[kb % nA], static_cast<uint32_t>((kb / nA) & 1));
+                    mbar_wait(&b_full[kb % nB], static_cast<uint32_t>((kb / nB) & 1));
+                    stamp(1, i, kc);
+                    // relaxed: the stages' bytes already landed (this lane observed the
+                    // complete_tx); a release at cluster scope costs ~1,400 cycles per
+                    // chunk on the critical path (MOE_TC_DBG bit 19 selects it: 1193 -> 756 TF/s)
+                    if (a.dbg & 524288)
+                        mbar_arrive_remote(mapa_shared(s32(&pair_full[kb % kW2Np]), 0));
+                    else
+                        mbar_arrive_remote_relaxed(mapa_shared(s32(&pair_full[kb % kW2Np]), 0));
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---- the leader's MMA warp ----
+        if (rank == 0) {
+            int kb = 0;
+            for (int i = 0; i < my_tiles; ++i) {
+                Tile tl;
+                if (!tile_of(i, tl)) break;
+                const uint32_t id = idesc(1, n_of(tl), 2 * kM);
+                const int buf = i % nbuf;
+                if (i >= nbuf) mbar_wait(&acc_empty[buf], static_cast<uint32_t>(((i / nbuf) - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t dacc = tmem + buf * kN;
+                for (int kc = 0; kc < nk; ++kc, ++kb) {
+                    const int r = kb % nA, b = kb % nB;
+                    mbar_wait(&pair_full[kb % kW2Np], static_cast<uint32_t>((kb / kW2Np) & 1));
+                    if (lane == 0) stamp(2, i, kc);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t ab = s32(rawb(r)), bb = s32(bst(b));
+#pragma unroll
+                    for (int j = 0; j < kKc / 16; ++j) {
+                        const uint64_t bdesc = sdesc(bb + j * 32);
+                        const uint32_t acc = (kc > 0 || j > 0) ? 1u : 0u;
+                        umma2_elect(dacc, sdesc_core(ab + j * 256), bdesc, id, acc);
+                        if (nmat == 2) umma2_elect(dacc + kN, sdesc_core(ab + kRawA + j * 256), bdesc, id, acc);
+                    }
+                    umma2_commit_both_elect(&rb_empty[r]);
+                    umma2_commit_both_elect(&b_empty[b]);
+                    if (kc == nk - 1) umma2_commit_both_elect(&acc_full[buf]);
+                    if (lane == 0) stamp(3, i, kc);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        // ---- epilogue: this CTA's 128 rows x the tile's tokens ----
+        const int row = (warp & 3) * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const int c0 = ((warp - 4) >> 2) * (kN / 2);
+        const uint32_t leader_empty0 = mapa_shared(s32(&acc_empty[0]), 0), leader_empty1 = mapa_shared(s32(&acc_empty[1]), 0);
+        for (int i = 0; i < my_tiles; ++i) {
+            Tile tl;
+            if (!tile_of(i, tl)) break;
+            const int buf = i % nbuf;
+            mbar_wait(&acc_full[buf], static_cast<uint32_t>((i / nbuf) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t dacc = tmem + buf * kN;
+            if (a.p == 0) {
+                uint32_t hp[kN / 4];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    uint32_t g[16], u[16];
+                    TMEM_LD16(dacc + lane_base + c0 + q * 16, g);
+                    TMEM_LD16(dacc + lane_base + kN + c0 + q * 16, u);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int c = 0; c < 16; c += 2) {
+                        hp[q * 8 + c / 2] = bf16x2_rn(silu_tanh(__uint_as_float(g[c])) * __uint_as_float(u[c]),
+                                                      silu_tanh(__uint_as_float(g[c + 1])) * __uint_as_float(u[c + 1]));
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(buf ? leader_empty1 : leader_empty0);
+                uint16_t* ho = a.hout + static_cast<size_t>(tl.slot0 + c0) * a.f + tl.R0 + row;
+#pragma unroll
+                for (int c = 0; c < kN / 2; ++c)
+                    if (c0 + c < tl.m) ho[static_cast<size_t>(c) * a.f] = static_cast<uint16_t>(hp[c >> 1] >> ((c & 1) * 16));
+            } else {
+                for (int cbk = c0; cbk < c0 + kN / 2 && cbk < tl.m; cbk += 32) {
+                    uint32_t g[32];
+                    TMEM_LD32(dacc + lane_base + cbk, g);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        if (cbk + c < tl.m)
+                            a.y[static_cast<size_t>(tl.slot0 + cbk + c) * a.d + tl.R0 + row] = __uint_as_float(g[c]);
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(buf ? leader_empty1 : leader_empty0);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();  // neither CTA frees TMEM while the pair's MMAs may still write it
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    if (trace && tid == 0 && rank == 0 && my_tiles > 2) {
+        const unsigned int t0 = g_wtrace2[0][0][0];
+        for (int kc = 0; kc < min(nk, 64); ++kc)
+            printf("W2TRACE p%d kc %2d wiss0 %7d wiss1 %7d fwd0 %7d fwd1 %7d pfull %7d mma %7d\n", a.p, kc,
+                   g_wtrace2[0][0][kc] - t0, g_wtrace2[1][0][kc] - t0, g_wtrace2[0][1][kc] - t0,
+                   g_wtrace2[1][1][kc] - t0, g_wtrace2[0][2][kc] - t0, g_wtrace2[0][3][kc] - t0);
+    }
+}
+
 // Pass-0 B operand in slot order: xs[slot] = x[token of slot] (bf16) and
 // its fp16 copy (int4 experts), so every tile's token rows are one TMA box
 // column.  One 16-byte chunk per thread.
@@ -1309,9 +1584,33 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
         MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem));
         wide_attr = true;
     }
+    const bool wpair = !(dbg & 262144) && (f / kM) % 2 == 0 && (d / kM) % 2 == 0;  // MOE_TC_DBG bit 18: single-CTA tiles
+    static bool pair_attr = false;
+    if (wpers && wpair && !pair_attr) {
+        MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_wide2, cudaFuncAttributeMaxDynamicSharedMemorySize, kW2Smem));
+        pair_attr = true;
+    }
     auto launch_wide = [&](int rows) -> cudaError_t {
         TcArgs aw = a;
         aw.active_mask = mask16;
+        if (wpair && !(rows == f && (dbg & 1048576))) {  // bit 20: single-CTA tiles for the gate/up pass
+            const int np = ntiles_max * (rows / kM / 2);
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(np, sms / 2)));
+            cfg.blockDim = dim3(kThreads2);
+            cfg.dynamicSmemBytes = kW2Smem;
+            cfg.stream = stream;
+            cudaLaunchAttribute attr[2];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[1].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 2;
+            return cudaLaunchKernelEx(&cfg, tc_ffn_wide2, aw, np);
+        }
         const int nt = ntiles_max * (rows / kM);
         return moek::launch_pdl(tc_ffn_wide, dim3(static_cast<unsigned>(std::min(nt, sms))), dim3(kThreads2), kWSmem,
                                 stream, aw, nt);
@@ -1374,6 +1673,7 @@ cudaError_t moek_preload_tc() {
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_persist));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::split_reduce_kernel));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_wide));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_wide2));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::gather_rows_kernel));
     return cudaSuccess;
 }
