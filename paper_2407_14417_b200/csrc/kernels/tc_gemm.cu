@@ -604,38 +604,73 @@ MOE_DEVI void produce4c(const TcArgs& a, const Tile& tl, int nmat, int K, int kc
     }
 }
 
-// convert_int4 over the compact raw unit layout
+// convert_int4 over the compact raw unit layout.  Every raw word and scale of
+// the chunk is loaded first, then converted and stored: the stores carry no
+// memory clobber, so the loads are not serialised behind them (the
+// canonical stage is read only by the tensor core, after the converters'
+// proxy fence and barrier arrive, which are ordered asm statements).
+MOE_DEVI void stmatrix_x4_nc(uint32_t addr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(r0), "r"(r1), "r"(r2),
+                 "r"(r3));
+}
 MOE_DEVI void convert_int4c(int nmat, const uint8_t* raw, uint8_t* can, int ct, const ConvOffsets& o) {
-    for (int mat = 0; mat < nmat; ++mat) {
-        const uint8_t* src = raw + mat * 8192;
-        uint8_t* dst = can + mat * kTileBytes;
-        const uint8_t* sc = raw + 2 * 8192 + mat * kRawS;
-        const __half2 m1032 = __halves2half2(__ushort_as_half(0xE408), __ushort_as_half(0xE408));
-        const __half2 m72 = __halves2half2(__ushort_as_half(0xD480), __ushort_as_half(0xD480));
-        const __half2 r16 = __halves2half2(__ushort_as_half(0x2C00), __ushort_as_half(0x2C00));
+    uint2 w2[2][2];
+    uint16_t sb[2][2];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const uint2 w2 = *reinterpret_cast<const uint2*>(src + o.qrow[j]);
-            const uint16_t sb = *reinterpret_cast<const uint16_t*>(sc + o.qsc[j]);
-            if (f16_scale_bad(sb)) numerics_flag(MOE_NUM_F16_SCALE);
-            const __half sh = __float2half_rn(bf2f(sb));
-            const __half2 s2 = __halves2half2(sh, sh);
+    for (int mat = 0; mat < 2; ++mat) {
+        if (mat < nmat) {
 #pragma unroll
-            for (int qi = 0; qi < 2; ++qi) {
-                const uint32_t w = qi ? w2.y : w2.x;
-                uint32_t v[4] = {and_or(w, 0x000F000Fu, 0x64006400u), and_or(w, 0x00F000F0u, 0x64006400u),
-                                 and_or(w >> 8, 0x000F000Fu, 0x64006400u), and_or(w >> 8, 0x00F000F0u, 0x64006400u)};
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    __half2 h = *reinterpret_cast<__half2*>(&v[u]);
-                    h = (u & 1) ? __hfma2(h, r16, m72) : __hadd2(h, m1032);
-                    h = __hmul2(h, s2);
-                    v[u] = *reinterpret_cast<uint32_t*>(&h);
-                }
-                stmatrix_x4(s32(dst) + o.stm[j][qi], v[0], v[1], v[2], v[3]);
+            for (int j = 0; j < 2; ++j) {
+                w2[mat][j] = *reinterpret_cast<const uint2*>(raw + mat * 8192 + o.qrow[j]);
+                sb[mat][j] = *reinterpret_cast<const uint16_t*>(raw + 2 * 8192 + mat * kRawS + o.qsc[j]);
             }
         }
     }
+    const __half2 m1032 = __halves2half2(__ushort_as_half(0xE408), __ushort_as_half(0xE408));
+    const __half2 m72 = __halves2half2(__ushort_as_half(0xD480), __ushort_as_half(0xD480));
+    const __half2 r16 = __halves2half2(__ushort_as_half(0x2C00), __ushort_as_half(0x2C00));
+#pragma unroll
+    for (int mat = 0; mat < 2; ++mat) {
+        if (mat < nmat) {
+            const uint32_t dst = s32(can + mat * kTileBytes);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (f16_scale_bad(sb[mat][j])) numerics_flag(MOE_NUM_F16_SCALE);
+                const __half sh = __float2half_rn(bf2f(sb[mat][j]));
+                const __half2 s2 = __halves2half2(sh, sh);
+#pragma unroll
+                for (int qi = 0; qi < 2; ++qi) {
+                    const uint32_t w = qi ? w2[mat][j].y : w2[mat][j].x;
+                    uint32_t v[4] = {and_or(w, 0x000F000Fu, 0x64006400u), and_or(w, 0x00F000F0u, 0x64006400u),
+                                     and_or(w >> 8, 0x000F000Fu, 0x64006400u), and_or(w >> 8, 0x00F000F0u, 0x64006400u)};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        __half2 h = *reinterpret_cast<__half2*>(&v[u]);
+                        h = (u & 1) ? __hfma2(h, r16, m72) : __hadd2(h, m1032);
+                        h = __hmul2(h, s2);
+                        v[u] = *reinterpret_cast<uint32_t*>(&h);
+                    }
+                    stmatrix_x4_nc(dst + o.stm[j][qi], v[0], v[1], v[2], v[3]);
+                }
+            }
+        }
+    }
+}
+
+// MOE_TC_DBG bit 15 (builds with -DMOE_TC_TRACE=1): CTA 0 stamps (SM clock) of its third tile's chunks -- chunks (tc_ffn_wide:
+// weight issue, B issue, weight full seen by the MMA thread, B full seen, MMA
+// committed; tc_ffn_persist int4 tiles: unit issue, converter start, converter
+// done, MMA sees the canonical stage, MMA committed) -- printed at exit (latency probe)
+#ifndef MOE_TC_TRACE
+#define MOE_TC_TRACE 0  // the probe costs the int4 converter loop ~10 %: compiled in only on request
+#endif
+constexpr bool kTcTrace = MOE_TC_TRACE != 0;
+__device__ unsigned int g_wtrace[6][64];
+__device__ unsigned int g_wtrace2[2][4][64];  // tc_ffn_wide2: [rank][weight issue, forwarder, pair full, MMA][chunk]
+MOE_DEVI unsigned int clk32() {
+    unsigned int c;
+    asm volatile("mov.u32 %0, %%clock;" : "=r"(c));
+    return c;
 }
 
 // nsplit > 1 (down pass): tile (e, row tile, K split ks) covers chunks ks*nk/nsplit ..; its
@@ -707,6 +742,10 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
     };
     auto is_p4 = [&](const Tile& tl) { return a.ex[tl.e].precision == MOE_P4; };
     const int my_tiles = static_cast<int>(blockIdx.x) < ntiles ? (ntiles - static_cast<int>(blockIdx.x) + grid - 1) / grid : 0;
+    const bool trace = kTcTrace && (a.dbg & 32768) && blockIdx.x == 0;
+    auto stamp = [&](int w, int i, int c) {
+        if (trace && i == 2 && c < 64) g_wtrace[w][c] = clk32();
+    };
 
     if (warp == 0) {
         // ---- weight producer ----
@@ -723,6 +762,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                 for (int kc = kc0; kc < kc0 + nks; kc += 2, ++u4) {
                     const int r = u4 % kPRaw4;
                     if (u4 >= kPRaw4) mbar_wait(&r4_empty[r], static_cast<uint32_t>(((u4 / kPRaw4) - 1) & 1));
+                    if (lane == 0) stamp(0, i, kc - kc0);
                     produce4c(a, tl, nmat, K, kc, raw4(r), &r4_full[r], lane);
                 }
             } else {
@@ -774,11 +814,13 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                     const int cu = kPWide ? c4 >> 1 : c4;  // canonical stage use
                     slot = cu % kPCan;
                     if (!kPWide || (c4 & 1) == 0) mbar_wait(&cn_full[slot], static_cast<uint32_t>((cu / kPCan) & 1));
+                    if (lane == 0) stamp(3, i, kc - kc0);
                 } else {
                     slot = cb % kPRb;
                     mbar_wait(&rb_full[slot], static_cast<uint32_t>((cb / kPRb) & 1));
                 }
                 mbar_wait(&b_full[b], static_cast<uint32_t>((kb / kBst) & 1));
+                if (lane == 0) stamp(5, i, kc - kc0);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 {  // warp-converged issue (umma_elect)
                     const uint32_t ab = s32(p4 ? can(slot) + (kPWide ? (c4 & 1) * 32768 : 0) : rawb(slot)), bb = s32(bst(b));
@@ -795,6 +837,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                     if (!p4 || !kPWide || (c4 & 1) == 1) umma_commit_elect(p4 ? &cn_empty[slot] : &rb_empty[slot]);
                     umma_commit_elect(&b_empty[b]);
                     if (kc == kc0 + nks - 1) umma_commit_elect(&acc_full[buf]);
+                    if (lane == 0) stamp(4, i, kc - kc0);
                 }
                 if (p4) ++c4; else ++cb;
             }
@@ -832,9 +875,11 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                     const int r = u4 % kPRaw4, c = c4 % kPCan;
                     if ((kc & 1) == 0) mbar_wait(&r4_full[r], static_cast<uint32_t>((u4 / kPRaw4) & 1));
                     if (c4 >= kPCan) mbar_wait(&cn_empty[c], static_cast<uint32_t>(((c4 / kPCan) - 1) & 1));
+                    if (ct == 0) stamp(1, i, kc - kc0);
                     convert_int4c(nmat, raw4(r), can(c), ct, (kc & 1) ? o1 : o0);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
+                    if (ct == 0) stamp(2, i, kc - kc0);
                     if (lane == 0) {
                         mbar_arrive(&cn_full[c]);
                         if (kc & 1) mbar_arrive(&r4_empty[r]);
@@ -886,6 +931,13 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    if (trace && tid == 0 && my_tiles > 2) {
+        const unsigned int t0 = g_wtrace[0][0];
+        for (int c = 0; c < min(nks, 64); ++c)
+            printf("PTRACE p%d c %2d uiss %7d cstart %7d cdone %7d cfull %7d bfull %7d mma %7d\n", a.p, c,
+                   g_wtrace[0][c] - t0, g_wtrace[1][c] - t0, g_wtrace[2][c] - t0, g_wtrace[3][c] - t0,
+                   g_wtrace[5][c] - t0, g_wtrace[4][c] - t0);
+    }
 }
 
 // y[slot][j] = sum over K splits of ypart[ks][slot][j], in split order, for the
@@ -945,16 +997,6 @@ static_assert(kWSmem + 1024 <= 232448, "tc_ffn_wide stages exceed shared memory"
 constexpr int kWPf = MOE_TCW_PF;  // weight L2 prefetch distance (chunks; even, 0 = off)
 static_assert(kWPf % 2 == 0, "prefetch whole 128-K blocks");
 
-// MOE_TC_DBG bit 15: CTA 0 stamps (SM clock) of its third tile's chunks -- weight
-// issue, B issue, weight full seen by the MMA thread, B full seen, MMA
-// committed -- printed at exit (latency probe)
-__device__ unsigned int g_wtrace[5][64];
-__device__ unsigned int g_wtrace2[2][4][64];  // tc_ffn_wide2: [rank][weight issue, forwarder, pair full, MMA][chunk]
-MOE_DEVI unsigned int clk32() {
-    unsigned int c;
-    asm volatile("mov.u32 %0, %%clock;" : "=r"(c));
-    return c;
-}
 
 __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide(const __grid_constant__ TcArgs a, int ntiles) {
     constexpr int kN = 256, kBTile = kN * kKc * 2;
@@ -1009,7 +1051,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide(const __grid_constan
     // accumulator use i: pass 0 has one buffer (use i waits for release i-1),
     // pass 1 two (use i waits for release i-2)
     const int nbuf = a.p == 0 ? 1 : 2;
-    const bool trace = (a.dbg & 32768) && blockIdx.x == 0;
+    const bool trace = kTcTrace && (a.dbg & 32768) && blockIdx.x == 0;
     auto stamp = [&](int w, int i, int kc) {
         if (trace && i == 2 && kc < 64) g_wtrace[w][kc] = clk32();
     };
@@ -1299,7 +1341,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_consta
     };
     auto n_of = [&](const Tile& tl) { return min(kN, (tl.m + 31) / 32 * 32); };  // both halves whole 16-column steps
     const int nbuf = a.p == 0 ? 1 : 2;
-    const bool trace = (a.dbg & 32768) && blockIdx.x < 2;
+    const bool trace = kTcTrace && (a.dbg & 32768) && blockIdx.x < 2;
     auto stamp = [&](int w, int i, int kc) {
         if (trace && i == 2 && kc < 64) g_wtrace2[rank][w][kc] = clk32();
     };
