@@ -117,6 +117,52 @@ MOE_DEVI uint32_t bf16x2_rn(float lo, float hi) {
     return r;
 }
 
+// One 64-K chunk of MMAs (4 k-steps x nmat matrices) and its two stage
+// commits in ONE asm block under one elect.sync: descriptors advance by adds
+// inside the block, so the issuing lane pays no per-MMA elect/branch/R2UR
+// chain (at N = 64 the per-instruction issue cost, ~95 cycles with one asm
+// statement per MMA, was 3x the tensor floor of 32).  a0/b0: the chunk's
+// first descriptors; aj/bj: per-16-K steps; amat: the second matrix's offset.
+MOE_DEVI void umma_chunk(int nmat, uint32_t d0, uint32_t d1, uint64_t a0, uint64_t amat, uint64_t aj, uint64_t b0,
+                         uint64_t bj, uint32_t id, uint32_t acc0, uint64_t* bar_a, uint64_t* bar_b) {
+    if (nmat == 2) {
+        asm volatile(
+            "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a, b, m;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %8, 0;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+            "add.s64 m, %2, %3;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %5, %7, p;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%1], m, %5, %7, p;\n\t"
+            "add.s64 a, %2, %4;\n\tadd.s64 m, m, %4;\n\tadd.s64 b, %5, %6;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %7, t;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%1], m, b, %7, t;\n\t"
+            "add.s64 a, a, %4;\n\tadd.s64 m, m, %4;\n\tadd.s64 b, b, %6;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %7, t;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%1], m, b, %7, t;\n\t"
+            "add.s64 a, a, %4;\n\tadd.s64 m, m, %4;\n\tadd.s64 b, b, %6;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %7, t;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%1], m, b, %7, t;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n}" ::"r"(d0),
+            "r"(d1), "l"(a0), "l"(amat), "l"(aj), "l"(b0), "l"(bj), "r"(id), "r"(acc0), "r"(s32(bar_a)), "r"(s32(bar_b))
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a, b;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %6, 0;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
+            "add.s64 a, %1, %2;\n\tadd.s64 b, %3, %4;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n\t"
+            "add.s64 a, a, %2;\n\tadd.s64 b, b, %4;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n\t"
+            "add.s64 a, a, %2;\n\tadd.s64 b, b, %4;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n}" ::"r"(d0),
+            "l"(a0), "l"(aj), "l"(b0), "l"(bj), "r"(id), "r"(acc0), "r"(s32(bar_a)), "r"(s32(bar_b))
+            : "memory");
+    }
+}
+
 // Warp-converged forms: every lane runs the issue loop with warp-uniform
 // operands (kept in uniform registers, no per-MMA R2UR / elect waterfall) and
 // one elected lane issues.
@@ -822,20 +868,23 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                 mbar_wait(&b_full[b], static_cast<uint32_t>((kb / kBst) & 1));
                 if (lane == 0) stamp(5, i, kc - kc0);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                {  // warp-converged issue (umma_elect)
+                {
                     const uint32_t ab = s32(p4 ? can(slot) + (kPWide ? (c4 & 1) * 32768 : 0) : rawb(slot)), bb = s32(bst(b));
+                    const bool rel = !p4 || !kPWide || (c4 & 1) == 1;  // the A stage is released with this chunk
+                    if (!rel) {  // kPWide builds, first half of a canonical unit: only B is released
 #pragma unroll
-                    for (int j = 0; j < kKc / 16; ++j) {
-                        const uint64_t bdesc = sdesc(bb + j * 32);
-                        const uint32_t acc = (kc > kc0 || j > 0) ? 1u : 0u;
-                        for (int mat = 0; mat < nmat; ++mat) {
-                            const uint64_t adesc = p4 ? sdesc(ab + mat * kTileBytes + j * 32)
-                                                      : sdesc_core(ab + mat * kRawA + j * 256);
-                            umma_elect(dacc + mat * kN, adesc, bdesc, id, acc);
+                        for (int j = 0; j < kKc / 16; ++j) {
+                            const uint64_t bdesc = sdesc(bb + j * 32);
+                            const uint32_t acc = (kc > kc0 || j > 0) ? 1u : 0u;
+                            for (int mat = 0; mat < nmat; ++mat)
+                                umma_elect(dacc + mat * kN, sdesc(ab + mat * kTileBytes + j * 32), bdesc, id, acc);
                         }
+                        umma_commit_elect(&b_empty[b]);
+                    } else {
+                        umma_chunk(nmat, dacc, dacc + kN, p4 ? sdesc(ab) : sdesc_core(ab),
+                                   p4 ? (kTileBytes >> 4) : (kRawA >> 4), p4 ? 2 : 16, sdesc(bb), 2, id,
+                                   kc > kc0 ? 1u : 0u, p4 ? &cn_empty[slot] : &rb_empty[slot], &b_empty[b]);
                     }
-                    if (!p4 || !kPWide || (c4 & 1) == 1) umma_commit_elect(p4 ? &cn_empty[slot] : &rb_empty[slot]);
-                    umma_commit_elect(&b_empty[b]);
                     if (kc == kc0 + nks - 1) umma_commit_elect(&acc_full[buf]);
                     if (lane == 0) stamp(4, i, kc - kc0);
                 }
