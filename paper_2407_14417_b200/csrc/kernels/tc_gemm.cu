@@ -46,6 +46,12 @@ struct TcArgs {
     // pass 1 h (bf16 / fp16)
     CUtensorMap tmb;
     CUtensorMap tmb16;
+    // fused persistent launch (tc_ffn_persist, fused = 1): the down pass's B maps (h),
+    // and per (expert, token tile, K split) counters of finished gate/up tiles
+    CUtensorMap tmh;
+    CUtensorMap tmh16;
+    unsigned int* dep;
+    int dep_tt;               // token tiles per expert in dep's index
     const int32_t* offsets;   // [E+1]
     const int32_t* perm;      // [T*k]
     int T, k, E, kshift;
@@ -207,6 +213,7 @@ MOE_DEVI int swz(int row, int kbyte) {
 
 struct Tile {
     int e, slot0, m, R0;  // expert, first slot, tokens in tile, first weight row
+    int p;                // pass: 0 gate/up, 1 down (a.p, except in a fused launch)
 };
 
 // offs: the routing's expert offsets [E+1], staged in shared memory
@@ -226,6 +233,7 @@ MOE_DEVI bool find_tile(const TcArgs& a, const int* offs, int RT, int b, Tile& t
             tl.slot0 = o0 + tt * kN;
             tl.m = min(kN, m - tt * kN);
             tl.R0 = rt * kM;
+            tl.p = a.p;
             return true;
         }
         b -= nt * RT;
@@ -233,6 +241,11 @@ MOE_DEVI bool find_tile(const TcArgs& a, const int* offs, int RT, int b, Tile& t
     return false;
 }
 
+MOE_DEVI unsigned int ld_acquire_gpu_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 MOE_DEVI void mbar_init_n(uint64_t* bar, uint32_t n) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(bar)), "r"(n) : "memory");
 }
@@ -278,15 +291,15 @@ MOE_DEVI void produce(const TcArgs& a, const Tile& tl, int nmat, int K, int kc, 
     if (lane == 0) mbar_expect_tx(bar, raw_bytes(p4, nmat));
     __syncwarp();
     for (int mat = 0; mat < nmat; ++mat) {
-        const int row0 = (a.p == 0 && mat == 1) ? a.f + tl.R0 : tl.R0;
-        const uint8_t* wb = static_cast<const uint8_t*>(a.p == 0 ? W.w_gate_up : W.w_down);
+        const int row0 = (tl.p == 0 && mat == 1) ? a.f + tl.R0 : tl.R0;
+        const uint8_t* wb = static_cast<const uint8_t*>(tl.p == 0 ? W.w_gate_up : W.w_down);
         uint8_t* dst = raw + mat * kRawA;
         if (lane < 8) {
             const size_t blk = static_cast<size_t>(row0 / 16 + lane) * G + g;
             if (!p4) {
                 bulk_g2s(dst + lane * 2048, wb + blk * 4096 + hh * 2048, 2048, bar);
             } else {
-                const uint8_t* sb = static_cast<const uint8_t*>(a.p == 0 ? W.s_gate_up : W.s_down);
+                const uint8_t* sb = static_cast<const uint8_t*>(tl.p == 0 ? W.s_gate_up : W.s_down);
                 bulk_g2s(dst + lane * 1024, wb + blk * 1024, 1024, bar);
                 bulk_g2s(raw + 2 * kRawA + mat * kRawS + lane * 32, sb + blk * 32, 32, bar);
             }
@@ -305,8 +318,8 @@ MOE_DEVI void produce_pair(const TcArgs& a, const Tile& tl, int nmat, int K, int
     }
     __syncwarp();
     for (int mat = 0; mat < nmat; ++mat) {
-        const int row0 = (a.p == 0 && mat == 1) ? a.f + tl.R0 : tl.R0;
-        const uint8_t* wb = static_cast<const uint8_t*>(a.p == 0 ? W.w_gate_up : W.w_down);
+        const int row0 = (tl.p == 0 && mat == 1) ? a.f + tl.R0 : tl.R0;
+        const uint8_t* wb = static_cast<const uint8_t*>(tl.p == 0 ? W.w_gate_up : W.w_down);
         if (lane < 8) {
             const size_t blk = static_cast<size_t>(row0 / 16 + lane) * G + g;
             bulk_g2s(raw0 + mat * kRawA + lane * 2048, wb + blk * 4096, 2048, bar0);
@@ -639,9 +652,9 @@ MOE_DEVI void produce4c(const TcArgs& a, const Tile& tl, int nmat, int K, int kc
     if (lane == 0) mbar_expect_tx(bar, nmat * (8 * 1024 + 256));
     __syncwarp();
     for (int mat = 0; mat < nmat; ++mat) {
-        const int row0 = (a.p == 0 && mat == 1) ? a.f + tl.R0 : tl.R0;
-        const uint8_t* wb = static_cast<const uint8_t*>(a.p == 0 ? W.w_gate_up : W.w_down);
-        const uint8_t* sb = static_cast<const uint8_t*>(a.p == 0 ? W.s_gate_up : W.s_down);
+        const int row0 = (tl.p == 0 && mat == 1) ? a.f + tl.R0 : tl.R0;
+        const uint8_t* wb = static_cast<const uint8_t*>(tl.p == 0 ? W.w_gate_up : W.w_down);
+        const uint8_t* sb = static_cast<const uint8_t*>(tl.p == 0 ? W.s_gate_up : W.s_down);
         if (lane < 8) {
             const size_t blk = static_cast<size_t>(row0 / 16 + lane) * G + g;
             bulk_g2s(raw + mat * 8192 + lane * 1024, wb + blk * 1024, 1024, bar);
@@ -722,7 +735,7 @@ MOE_DEVI unsigned int clk32() {
 // nsplit > 1 (down pass): tile (e, row tile, K split ks) covers chunks ks*nk/nsplit ..; its
 // y rows go to ypart[ks] (summed in split order by split_reduce_kernel)
 __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_constant__ TcArgs a, int ntiles, int nsplit,
-                                                               float* ypart) {
+                                                               float* ypart, int fused) {
     constexpr int kN = 128, kBst = kPBst, kBTile = kN * kKc * 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
@@ -740,10 +753,12 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
 
     pdl_wait();
     pdl_trigger();
-    const int K = a.p == 0 ? a.d : a.f;
-    const int RT = (a.p == 0 ? a.f : a.d) / kM;
-    const int nmat = a.p == 0 ? 2 : 1;
-    const int nks = K / kKc / nsplit;  // chunks per tile
+    // per-tile pass parameters (a fused launch walks the gate/up tiles, then the down tiles)
+    auto K_of = [&](const Tile& t) { return t.p == 0 ? a.d : a.f; };
+    auto nmat_of = [&](const Tile& t) { return t.p == 0 ? 2 : 1; };
+    auto ns_of = [&](const Tile& t) { return t.p == 0 ? 1 : nsplit; };
+    auto nks_of = [&](const Tile& t) { return K_of(t) / kKc / ns_of(t); };  // chunks per tile
+    const int RT0 = a.f / kM;
     const int grid = static_cast<int>(gridDim.x);
     if (tid <= a.E) s_off[tid] = a.offsets[tid];
     if (tid == 0) {
@@ -778,13 +793,30 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_slot;
+    // fused: the gate/up tiles come first, n0 of them
+    int n0 = 0;
+    if (fused)
+        for (int e = 0; e < a.E; ++e)
+            if ((a.active_mask >> e) & 1ull) n0 += (s_off[e + 1] - s_off[e] + kN - 1) / kN * RT0;
     // (row tile, K split) enumerated as one index: find_tile's R0 / 128 = rt * nsplit + ks
     auto tile_of = [&](int i, Tile& tl, int& kc0) {
-        if (!find_tile<128>(a, s_off, RT * nsplit, static_cast<int>(blockIdx.x) + i * grid, tl)) return false;
-        const int rtk = tl.R0 / kM, ks = rtk % nsplit;
-        tl.R0 = (rtk / nsplit) * kM;
-        kc0 = ks * nks;
+        int t = static_cast<int>(blockIdx.x) + i * grid, p = a.p;
+        if (fused) {
+            p = t < n0 ? 0 : 1;
+            if (p == 1) t -= n0;
+        }
+        const int nsp = p == 0 ? 1 : nsplit;
+        if (!find_tile<128>(a, s_off, (p == 0 ? a.f : a.d) / kM * nsp, t, tl)) return false;
+        tl.p = p;
+        const int rtk = tl.R0 / kM, ks = rtk % nsp;
+        tl.R0 = (rtk / nsp) * kM;
+        kc0 = ks * nks_of(tl);
         return true;
+    };
+    // fused: counter of (expert, token tile, K split): the gate/up tiles whose h columns
+    // fall in that split of the down pass's K; a down tile waits for RT0 / nsplit of them
+    auto dep_of = [&](const Tile& t, int ks) {
+        return a.dep + ((t.e * a.dep_tt + (t.slot0 - s_off[t.e]) / kN) * nsplit + ks);
     };
     auto is_p4 = [&](const Tile& tl) { return a.ex[tl.e].precision == MOE_P4; };
     const int my_tiles = static_cast<int>(blockIdx.x) < ntiles ? (ntiles - static_cast<int>(blockIdx.x) + grid - 1) / grid : 0;
@@ -801,6 +833,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
             int kc0;
             if (!tile_of(i, tl, kc0)) break;  // past the routing's last tile
             const bool p4 = is_p4(tl);
+            const int K = K_of(tl), nmat = nmat_of(tl), nks = nks_of(tl);
             if (prev >= 0 && prev != static_cast<int>(p4))  // region R changes role: the previous tile's MMAs first
                 mbar_wait(&acc_full[(i - 1) & 1], static_cast<uint32_t>(((i - 1) >> 1) & 1));
             prev = p4;
@@ -828,8 +861,16 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                 Tile tl;
                 int kc0;
                 if (!tile_of(i, tl, kc0)) break;
-                const CUtensorMap* tm = is_p4(tl) ? &a.tmb16 : &a.tmb;
+                const bool down_f = fused && tl.p == 1;
+                const CUtensorMap* tm = down_f ? (is_p4(tl) ? &a.tmh16 : &a.tmh) : (is_p4(tl) ? &a.tmb16 : &a.tmb);
                 const int nbox = (min(kN, (tl.m + 15) / 16 * 16) + 63) / 64;
+                const int nks = nks_of(tl);
+                if (down_f) {
+                    // this token tile's h columns of this K split, written by other CTAs' gate/up tiles
+                    const unsigned int* dp = dep_of(tl, kc0 / nks);
+                    while (ld_acquire_gpu_u32(dp) < static_cast<unsigned int>(RT0 / nsplit)) __nanosleep(64);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // their generic stores before our TMA reads
+                }
                 for (int kc = kc0; kc < kc0 + nks; ++kc, ++kb) {
                     const int b = kb % kBst;
                     if (kb >= kBst) mbar_wait(&b_empty[b], static_cast<uint32_t>(((kb / kBst) - 1) & 1));
@@ -847,6 +888,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
             int kc0;
             if (!tile_of(i, tl, kc0)) break;  // past the routing's last tile
             const bool p4 = is_p4(tl);
+            const int nmat = nmat_of(tl), nks = nks_of(tl);
             const int nmma = min(kN, (tl.m + 15) / 16 * 16);
             const uint32_t id = idesc(p4 ? 0 : 1, nmma, kM);
             const int buf = i & 1;
@@ -905,6 +947,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
             Tile tl;
             int kc0;
             if (!tile_of(i, tl, kc0)) break;  // past the routing's last tile
+            const int nmat = nmat_of(tl), nks = nks_of(tl);
             if (is_p4(tl) && kPWide) {
                 for (int kc = kc0; kc < kc0 + nks; kc += 2, ++u4) {  // one hand-off per raw unit
                     const int r = u4 % kPRaw4, c = u4 % kPCan;
@@ -943,7 +986,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
             for (int cbk = c0; cbk < c0 + kN / 2; cbk += 32) {
                 uint32_t g[32];
                 TMEM_LD32(dacc + lane_base + cbk, g);
-                if (a.p == 0) {
+                if (tl.p == 0) {
                     uint32_t u[32];
                     TMEM_LD32(dacc + lane_base + kN + cbk, u);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -966,7 +1009,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
                     for (int c = 0; c < 32; ++c) {
                         const int n = cbk + c;
                         if (n < tl.m) {
-                            float* yo = nsplit > 1 ? ypart + static_cast<size_t>(kc0 / nks) * a.T * a.k * a.d : a.y;
+                            float* yo = ns_of(tl) > 1 ? ypart + static_cast<size_t>(kc0 / nks) * a.T * a.k * a.d : a.y;
                             yo[static_cast<size_t>(tl.slot0 + n) * a.d + tl.R0 + row] = __uint_as_float(g[c]);
                         }
                     }
@@ -975,6 +1018,12 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
+            if (fused && tl.p == 0) {
+                // publish this tile's h columns to the down tiles that read them
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" ::"r"(kConvThreads) : "memory");
+                if (ct == 0) atomicAdd(dep_of(tl, (tl.R0 / kM) / (RT0 / nsplit)), 1u);
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -982,7 +1031,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_persist(const __grid_cons
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
     if (trace && tid == 0 && my_tiles > 2) {
         const unsigned int t0 = g_wtrace[0][0];
-        for (int c = 0; c < min(nks, 64); ++c)
+        for (int c = 0; c < 64; ++c)
             printf("PTRACE p%d c %2d uiss %7d cstart %7d cdone %7d cfull %7d bfull %7d mma %7d\n", a.p, c,
                    g_wtrace[0][c] - t0, g_wtrace[1][c] - t0, g_wtrace[2][c] - t0, g_wtrace[3][c] - t0,
                    g_wtrace[5][c] - t0, g_wtrace[4][c] - t0);
@@ -1600,8 +1649,9 @@ constexpr int kDownSplit = 4;  // K splits of the down pass on the persistent ke
 
 size_t moek_tc_workspace_bytes(int T, int k, int d, int f) {
     const size_t slots = static_cast<size_t>(T) * k;
-    // xs, xs16, h, h16, the down pass's split partials
-    return 2 * slots * d * 2 + 2 * slots * f * 2 + static_cast<size_t>(kDownSplit) * slots * d * 4 + 1024;
+    // xs, xs16, h, h16, the down pass's split partials, the fused launch's tile counters
+    return 2 * slots * d * 2 + 2 * slots * f * 2 + static_cast<size_t>(kDownSplit) * slots * d * 4 +
+           static_cast<size_t>(MOE_MAX_EXPERTS) * (slots / 128 + 2) * kDownSplit * 4 + 1024;
 }
 
 // Grouped expert FFN on tcgen05 for every expert segment of a permutation:
@@ -1625,6 +1675,8 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     uint16_t* h = xs16 + slots * d;
     uint16_t* h16 = h + slots * f;
     float* ypart = reinterpret_cast<float*>(h16 + slots * f);
+    unsigned int* dep = reinterpret_cast<unsigned int*>(ypart + static_cast<size_t>(kDownSplit) * slots * d);
+    const int dep_tt = static_cast<int>(slots / 128 + 2);
     const int kshift = (k & (k - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(k)) : -1;
     const long long nch = static_cast<long long>(slots) * (d / 8);
     MOE_CUDA_OK(moek::launch_pdl(gather_rows_kernel, dim3(static_cast<unsigned>(std::min<long long>((nch + 255) / 256, 2368))),
@@ -1714,10 +1766,37 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     MOE_CUDA_OK(encode_b(&a.tmb16, xs16, d, static_cast<int>(slots)));
     a.hout = h;
     a.hout16 = h16;
+    // K split of the persistent down pass in kDownSplit parts when every part keeps whole
+    // int4 chunk pairs
+    const int ns = (f / kKc) % (2 * kDownSplit) == 0 && !(dbg & 512) ? kDownSplit : 1;
+    // one persistent launch for both passes (MOE_TC_DBG bit 21: two): the down tiles of
+    // a (token tile, K split) start once its gate/up tiles are stored, so the last
+    // gate/up wave shares the machine with the first down tiles
+    const bool fuse = persist && !(dbg & 2097152) && (f / kM) % ns == 0;
+    if (fuse) {
+        MOE_CUDA_OK(encode_b(&a.tmb, xs, d, static_cast<int>(slots)));
+        MOE_CUDA_OK(encode_b(&a.tmb16, xs16, d, static_cast<int>(slots)));
+        MOE_CUDA_OK(encode_b(&a.tmh, h, f, static_cast<int>(slots)));
+        MOE_CUDA_OK(encode_b(&a.tmh16, h16, f, static_cast<int>(slots)));
+        a.p = 0;
+        a.hout = h;
+        a.hout16 = h16;
+        a.y = y;
+        a.dep = dep;
+        a.dep_tt = dep_tt;
+        MOE_CUDA_OK(cudaMemsetAsync(dep, 0, static_cast<size_t>(E) * dep_tt * ns * 4, stream));
+        const int nt = ntiles_max * (f / kM) + ntiles_max * (d / kM) * ns;
+        MOE_CUDA_OK(moek::launch_pdl(tc_ffn_persist, dim3(static_cast<unsigned>(std::min(nt, sms))), dim3(kThreads2), kPSmem,
+                                     stream, a, nt, ns, ypart, 1));
+        if (ns == 1) return cudaSuccess;
+        return moek::launch_pdl(split_reduce_kernel, dim3(static_cast<unsigned>(std::min<size_t>(slots, 2048))), dim3(256), 0,
+                                stream, reinterpret_cast<const float4*>(ypart), offsets, E, active_mask,
+                                static_cast<int>(slots), d / 4, ns, reinterpret_cast<float4*>(y));
+    }
     if (persist) {
         const int nt0 = ntiles_max * (f / kM);
         MOE_CUDA_OK(moek::launch_pdl(tc_ffn_persist, dim3(static_cast<unsigned>(std::min(nt0, sms))), dim3(kThreads2), kPSmem,
-                                     stream, a, nt0, 1, static_cast<float*>(nullptr)));
+                                     stream, a, nt0, 1, static_cast<float*>(nullptr), 0));
     } else {
         if (wpers) MOE_CUDA_OK(launch_wide(f));
         if (mask_single) {
@@ -1733,11 +1812,9 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     MOE_CUDA_OK(encode_b(&a.tmb16, h16, f, static_cast<int>(slots)));
     a.y = y;
     if (persist) {
-        // K split in kDownSplit parts when every part keeps whole int4 chunk pairs
-        const int ns = (f / kKc) % (2 * kDownSplit) == 0 && !(dbg & 512) ? kDownSplit : 1;
         const int nt1 = ntiles_max * (d / kM) * ns;
         MOE_CUDA_OK(moek::launch_pdl(tc_ffn_persist, dim3(static_cast<unsigned>(std::min(nt1, sms))), dim3(kThreads2), kPSmem,
-                                     stream, a, nt1, ns, ypart));
+                                     stream, a, nt1, ns, ypart, 0));
         if (ns == 1) return cudaSuccess;
         return moek::launch_pdl(split_reduce_kernel, dim3(static_cast<unsigned>(std::min<size_t>(slots, 2048))), dim3(256), 0,
                                 stream, reinterpret_cast<const float4*>(ypart), offsets, E, active_mask,
