@@ -714,8 +714,8 @@ struct MoeEngine::Impl {
         if (!host) {
             counters.hits += static_cast<int64_t>(T) * K;
             if (tc) {
-                ffn_y(mask_all(), lw);
-                ck(moek_combine(y, inv, w_l, x, T, d, K, out, compute), "combine");
+                ck(moek_ffn_tc_combine(tcws, xnorm, perm, offsets, T, K, lw, E, d, f, mask_all(), y, inv, w_l, x, out,
+                                       compute), "ffn_tc+combine");
             } else {
                 ck(moek_ffn_mma(gws, x, perm, offsets, inv, w_l, x, T, K, lw, E, d, f, mask_all(), out, nullptr,
                                 MOE_X_ROUTED, compute), "ffn");
@@ -918,9 +918,8 @@ struct MoeEngine::Impl {
                           tc && cfg.norm_eps > 0.0f ? xn : nullptr), "route");
             ck(cudaEventRecord(ev[static_cast<size_t>(2 * l)], compute), "record");
             if (tc) {
-                ck(moek_ffn_tc(tcws, cfg.norm_eps > 0.0f ? xn : src, perm, offsets, T, K, lw, E, d, f, mask_all(), y,
-                               compute), "ffn_tc");
-                ck(moek_combine(y, inv, wts + l * TK, src, T, d, K, dst, compute), "combine");
+                ck(moek_ffn_tc_combine(tcws, cfg.norm_eps > 0.0f ? xn : src, perm, offsets, T, K, lw, E, d, f,
+                                       mask_all(), y, inv, wts + l * TK, src, dst, compute), "ffn_tc+combine");
             } else {
                 ck(moek_ffn_mma(gws, src, perm, offsets, inv, wts + l * TK, src, T, K, lw, E, d, f, mask_all(), dst,
                                 nullptr, MOE_X_ROUTED, compute), "ffn");

@@ -94,6 +94,14 @@ size_t moek_tc_workspace_bytes(int T, int k, int d, int f);
 cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
                         const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask, float* y,
                         cudaStream_t stream);
+// moek_ffn_tc followed by the K5 combine (out = bf16(res + sum_j w_j y_j), moek_combine's
+// arithmetic): when the down pass ran K-split in the fused persistent launch, the combine
+// reads the split partials directly (no y round trip, no split_reduce launch); otherwise
+// y is written and moek_combine runs.  Bit-identical to moek_ffn_tc + moek_combine.
+cudaError_t moek_ffn_tc_combine(void* ws, const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+                                const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask,
+                                float* y, const int32_t* inv, const float* w, const void* res, void* out,
+                                cudaStream_t stream);
 // Host-resident expert streaming (engine.cpp): pinned H2D of one expert on
 // the copy stream, recorded on `done` (may be null) for the compute stream.
 cudaError_t moek_stream_expert(void* dst, const void* src_pinned, size_t bytes, cudaStream_t copy, cudaEvent_t done);

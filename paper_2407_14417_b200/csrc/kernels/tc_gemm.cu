@@ -1065,6 +1065,45 @@ __global__ void split_reduce_kernel(const float4* __restrict__ ypart, const int3
     }
 }
 
+// K5 from the down pass's split partials: y_slot = ypart[0] + ypart[1] + ... in split
+// order (split_reduce_kernel's arithmetic), then combine_kernel's fma chain in j order.
+__global__ void combine_splits_kernel(const float4* __restrict__ ypart, int slots, int nsplit,
+                                      const int32_t* __restrict__ inv, const float* __restrict__ w,
+                                      const uint16_t* __restrict__ res, int T, int d, int k, uint16_t* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
+    const int d4 = d / 4;
+    const size_t plane = static_cast<size_t>(slots) * d4;
+    const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid >= static_cast<long long>(T) * d4) return;
+    const int t = static_cast<int>(gid / d4), c4 = static_cast<int>(gid - static_cast<long long>(t) * d4);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (res) {
+        const uint2 r = *reinterpret_cast<const uint2*>(res + static_cast<size_t>(t) * d + c4 * 4);
+        acc[0] = bf16_lo(r.x);
+        acc[1] = bf16_hi(r.x);
+        acc[2] = bf16_lo(r.y);
+        acc[3] = bf16_hi(r.y);
+    }
+    for (int j = 0; j < k; ++j) {
+        const float wj = w[t * k + j];
+        const size_t i = static_cast<size_t>(inv[t * k + j]) * d4 + c4;
+        float4 v = __ldcg(ypart + i);
+        for (int ks = 1; ks < nsplit; ++ks) {
+            const float4 q = __ldcg(ypart + static_cast<size_t>(ks) * plane + i);
+            v.x += q.x; v.y += q.y; v.z += q.z; v.w += q.w;
+        }
+        acc[0] = __fmaf_rn(wj, v.x, acc[0]);
+        acc[1] = __fmaf_rn(wj, v.y, acc[1]);
+        acc[2] = __fmaf_rn(wj, v.z, acc[2]);
+        acc[3] = __fmaf_rn(wj, v.w, acc[3]);
+    }
+    uint2 o;
+    o.x = static_cast<uint32_t>(f2bf(acc[0])) | (static_cast<uint32_t>(f2bf(acc[1])) << 16);
+    o.y = static_cast<uint32_t>(f2bf(acc[2])) | (static_cast<uint32_t>(f2bf(acc[3])) << 16);
+    *reinterpret_cast<uint2*>(out + static_cast<size_t>(t) * d + c4 * 4) = o;
+}
+
 // ===========================================================================
 // Persistent bf16 256-token variant (tc_ffn_wide): prefill-sized launches.
 // One CTA per SM walks the tile list like tc_ffn_persist, at N = 256 (the
@@ -1656,10 +1695,18 @@ size_t moek_tc_workspace_bytes(int T, int k, int d, int f) {
 
 // Grouped expert FFN on tcgen05 for every expert segment of a permutation:
 // x natural [T][d] bf16 (already normalised), y_perm [T*k][d] fp32.
-cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+namespace {
+struct TcCombine {  // optional K5 fused into the down pass's reduction (moek_ffn_tc_combine)
+    const int32_t* inv;
+    const float* w;
+    const void* res;
+    void* out;
+};
+cudaError_t ffn_tc_impl(void* ws, const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
                         const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask, float* y,
-                        cudaStream_t stream) {
+                        const TcCombine* cmb, bool* combined, cudaStream_t stream) {
     using namespace moek::tc;
+    *combined = false;
     if (d % kM != 0 || f % kM != 0 || d % 128 != 0 || f % 128 != 0) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
@@ -1789,6 +1836,14 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
         MOE_CUDA_OK(moek::launch_pdl(tc_ffn_persist, dim3(static_cast<unsigned>(std::min(nt, sms))), dim3(kThreads2), kPSmem,
                                      stream, a, nt, ns, ypart, 1));
         if (ns == 1) return cudaSuccess;
+        if (cmb != nullptr && !(dbg & 4194304)) {  // MOE_TC_DBG bit 22: split_reduce + combine instead
+            *combined = true;
+            const long long n = static_cast<long long>(T) * (d / 4);
+            return moek::launch_pdl(combine_splits_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0,
+                                    stream, reinterpret_cast<const float4*>(ypart), static_cast<int>(slots), ns, cmb->inv,
+                                    cmb->w, static_cast<const uint16_t*>(cmb->res), T, d, k,
+                                    static_cast<uint16_t*>(cmb->out));
+        }
         return moek::launch_pdl(split_reduce_kernel, dim3(static_cast<unsigned>(std::min<size_t>(slots, 2048))), dim3(256), 0,
                                 stream, reinterpret_cast<const float4*>(ypart), offsets, E, active_mask,
                                 static_cast<int>(slots), d / 4, ns, reinterpret_cast<float4*>(y));
@@ -1827,6 +1882,28 @@ cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int3
     return moek::launch_pdl(kern, dim3(static_cast<unsigned>(ntiles_max * (d / kM))), dim3(kThreads2), smem, stream,
                             as);
 }
+}  // namespace
+
+cudaError_t moek_ffn_tc(void* ws, const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+                        const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask, float* y,
+                        cudaStream_t stream) {
+    bool combined;
+    return ffn_tc_impl(ws, x, perm, offsets, T, k, experts, E, d, f, active_mask, y, nullptr, &combined, stream);
+}
+
+cudaError_t moek_ffn_tc_combine(void* ws, const void* x, const int32_t* perm, const int32_t* offsets, int T, int k,
+                                const moe_expert_weights* experts, int E, int d, int f, uint64_t active_mask,
+                                float* y, const int32_t* inv, const float* w, const void* res, void* out,
+                                cudaStream_t stream) {
+    // every slot must come from this launch for the partials to hold the whole y
+    const uint64_t all = E >= 64 ? ~0ull : ((1ull << E) - 1ull);
+    const TcCombine cmb{inv, w, res, out};
+    bool combined = false;
+    MOE_CUDA_OK(ffn_tc_impl(ws, x, perm, offsets, T, k, experts, E, d, f, active_mask, y,
+                            (active_mask & all) == all ? &cmb : nullptr, &combined, stream));
+    if (combined) return cudaSuccess;
+    return moek_combine(y, inv, w, res, T, d, k, out, stream);
+}
 
 MOE_NUMERICS_BINDER(tc)
 
@@ -1840,6 +1917,7 @@ cudaError_t moek_preload_tc() {
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_kernel<256>));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_persist));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::split_reduce_kernel));
+    MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::combine_splits_kernel));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_wide));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::tc_ffn_wide2));
     MOE_CUDA_OK_PRELOAD(cudaFuncGetAttributes(&fa, moek::tc::gather_rows_kernel));

@@ -499,3 +499,41 @@ def test_host_split_tcgen05_batch(moe, torch_mod, cuda, lru):
     assert c.activations == 3 * T * 2 * 2 and c.bytes_transferred > 0
     eng.close()
     base.close()
+
+
+_COMBINE_PROBE = r"""
+import hashlib, os, sys
+sys.path.insert(0, os.getcwd())
+sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+import numpy as np, torch
+import paper_2407_14417_b200 as moe
+from helpers import read_device
+prof = moe.profile_for_shape(4096, 14336, 2, 8, 2)
+plan = moe.make_plan(moe.TaskRequest(moe.QUALITY, 8, 3), moe.HardwareProfile(10**15), prof)
+eng = moe.MoeEngine(2, 8, 2, 4096, 14336, plan, max_tokens=64, seed=9, norm_eps=1e-5, tc_min_tokens=32)
+h = hashlib.sha256()
+for step in range(3):
+    eng.synth_input(40 + step, 64)
+    eng.decode(64)
+    eng.sync()
+    h.update(read_device(torch, eng.output_ptr, 64 * 4096 * 2).tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_tc_combine_from_split_partials_bitexact(moe, cuda):
+    """moek_ffn_tc_combine: the K5 combine read straight from the fused launch's
+    down-pass split partials gives the same bits as split_reduce + combine
+    (MOE_TC_DBG bit 22), on a mixed bf16/int4 Mixtral-shaped stack at T = 64."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    digests = []
+    for dbg in ("0", "4194304"):
+        env = dict(os.environ, MOE_TC_DBG=dbg)
+        r = subprocess.run([sys.executable, "-c", _COMBINE_PROBE], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        digests.append(r.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1]
