@@ -1637,9 +1637,13 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_consta
 // its fp16 copy (int4 experts), so every tile's token rows are one TMA box
 // column.  One 16-byte chunk per thread.
 __global__ void gather_rows_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ perm, int slots, int d,
-                                   int k, int kshift, uint16_t* __restrict__ xs, uint16_t* __restrict__ xs16) {
+                                   int k, int kshift, uint16_t* __restrict__ xs, uint16_t* __restrict__ xs16,
+                                   unsigned int* __restrict__ dep, int ndep) {
     pdl_wait();
     pdl_trigger();
+    // the fused launch's tile counters (its PDL wait orders this before any use; the
+    // previous layer's fused launch finished before our own wait returned)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ndep; i += gridDim.x * blockDim.x) dep[i] = 0u;
     const int cpr = d / 8;
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
          i < static_cast<long long>(slots) * cpr; i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -1725,10 +1729,6 @@ cudaError_t ffn_tc_impl(void* ws, const void* x, const int32_t* perm, const int3
     unsigned int* dep = reinterpret_cast<unsigned int*>(ypart + static_cast<size_t>(kDownSplit) * slots * d);
     const int dep_tt = static_cast<int>(slots / 128 + 2);
     const int kshift = (k & (k - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(k)) : -1;
-    const long long nch = static_cast<long long>(slots) * (d / 8);
-    MOE_CUDA_OK(moek::launch_pdl(gather_rows_kernel, dim3(static_cast<unsigned>(std::min<long long>((nch + 255) / 256, 2368))),
-                                 dim3(256), 0, stream, static_cast<const uint16_t*>(x), perm, static_cast<int>(slots), d, k,
-                                 kshift, xs, xs16));
     TcArgs a{};
     a.offsets = offsets;
     a.perm = perm;
@@ -1820,6 +1820,11 @@ cudaError_t ffn_tc_impl(void* ws, const void* x, const int32_t* perm, const int3
     // a (token tile, K split) start once its gate/up tiles are stored, so the last
     // gate/up wave shares the machine with the first down tiles
     const bool fuse = persist && !(dbg & 2097152) && (f / kM) % ns == 0;
+    const int ndep = fuse ? E * dep_tt * ns : 0;
+    const long long nch = static_cast<long long>(slots) * (d / 8);
+    MOE_CUDA_OK(moek::launch_pdl(gather_rows_kernel, dim3(static_cast<unsigned>(std::min<long long>((nch + 255) / 256, 2368))),
+                                 dim3(256), 0, stream, static_cast<const uint16_t*>(x), perm, static_cast<int>(slots), d, k,
+                                 kshift, xs, xs16, dep, ndep));
     if (fuse) {
         MOE_CUDA_OK(encode_b(&a.tmb, xs, d, static_cast<int>(slots)));
         MOE_CUDA_OK(encode_b(&a.tmb16, xs16, d, static_cast<int>(slots)));
@@ -1831,7 +1836,6 @@ cudaError_t ffn_tc_impl(void* ws, const void* x, const int32_t* perm, const int3
         a.y = y;
         a.dep = dep;
         a.dep_tt = dep_tt;
-        MOE_CUDA_OK(cudaMemsetAsync(dep, 0, static_cast<size_t>(E) * dep_tt * ns * 4, stream));
         const int nt = ntiles_max * (f / kM) + ntiles_max * (d / kM) * ns;
         MOE_CUDA_OK(moek::launch_pdl(tc_ffn_persist, dim3(static_cast<unsigned>(std::min(nt, sms))), dim3(kThreads2), kPSmem,
                                      stream, a, nt, ns, ypart, 1));
