@@ -1382,6 +1382,7 @@ constexpr int kW2Pool = 224 * 1024;
 constexpr int kW2A0 = MOE_TCW2_A0, kW2B0 = (kW2Pool - kW2A0 * 32768) / 16384;  // pass 0: 32 KB A, 16 KB B stages
 constexpr int kW2A1 = MOE_TCW2_A1, kW2B1 = (kW2Pool - kW2A1 * 16384) / 16384;  // pass 1: 16 KB A, 16 KB B stages
 constexpr int kW2MaxA = kW2A0 > kW2A1 ? kW2A0 : kW2A1, kW2MaxB = kW2B0 > kW2B1 ? kW2B0 : kW2B1;
+constexpr int kW2R4 = 5;   // int4 raw units in region R (pass 0: 5, pass 1: 3 fit)
 constexpr int kW2Np = 16;  // pair-barrier ring (> the chunks a forwarder can run ahead)
 constexpr int kW2Smem = 1024 + kW2Pool;
 static_assert(kW2MaxA < kW2Np && kW2MaxB < kW2Np && kW2B0 >= 2 && kW2B1 >= 2, "tc_ffn_wide2 stage split");
@@ -1425,7 +1426,7 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_consta
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
     __shared__ __align__(8) uint64_t rb_full[kW2MaxA], rb_empty[kW2MaxA], b_full[kW2MaxB], b_empty[kW2MaxB],
-        pair_full[kW2Np], acc_full[2], acc_empty[2];
+        pair_full[kW2Np], acc_full[2], acc_empty[2], r4_full[kW2R4], r4_empty[kW2R4], cn_full[2], cn_empty[2];
     __shared__ uint32_t tmem_slot;
     __shared__ int s_off[MOE_MAX_EXPERTS + 1];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1435,6 +1436,12 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_consta
     const int sA = nmat * kRawA;
     auto rawb = [&](int s) { return smem + s * sA; };
     auto bst = [&](int s) { return smem + nA * sA + s * kBHalf; };
+    // int4 tiles reuse region R (the bf16 weight ring): two canonical fp16 A stages, then
+    // compact raw units (tc_ffn_persist's layout)
+    const int nR4 = min(kW2R4, (nA * sA - 2 * 32768) / kPRaw4Unit);
+    auto can = [&](int s) { return smem + s * 32768; };
+    auto raw4 = [&](int s) { return smem + 2 * 32768 + s * kPRaw4Unit; };
+    auto is_p4 = [&](const Tile& t) { return a.ex[t.e].precision == MOE_P4; };
 
     pdl_wait();
     pdl_trigger();
@@ -1456,6 +1463,12 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_consta
         for (int s = 0; s < 2; ++s) {
             mbar_init_n(&acc_full[s], 1);
             mbar_init_n(&acc_empty[s], 2 * (kConvThreads / 32));  // both CTAs' epilogue warps
+            mbar_init_n(&cn_full[s], kConvThreads / 32);          // this CTA's converter warps
+            mbar_init_n(&cn_empty[s], 1);                         // the leader's multicast commit
+        }
+        for (int s = 0; s < kW2R4; ++s) {
+            mbar_init_n(&r4_full[s], 1);
+            mbar_init_n(&r4_empty[s], kConvThreads / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -1484,11 +1497,24 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_consta
     };
 
     if (warp == 0) {
-        // ---- this CTA's weight rows, both 64-K halves of each 4 KB block back to back ----
-        int ub = 0;
+        // ---- this CTA's weight rows: bf16 both 64-K halves of each 4 KB block back to
+        // back; int4 one compact raw unit per 128-K group ----
+        int ub = 0, u4 = 0, prev = -1;
         for (int i = 0; i < my_tiles; ++i) {
             Tile tl;
             if (!tile_of(i, tl)) break;
+            const bool p4 = is_p4(tl);
+            if (prev >= 0 && prev != static_cast<int>(p4))  // region R changes role: the previous tile's MMAs first
+                mbar_wait(&acc_full[(i - 1) % nbuf], static_cast<uint32_t>(((i - 1) / nbuf) & 1));
+            prev = p4;
+            if (p4) {
+                for (int kc = 0; kc < nk; kc += 2, ++u4) {
+                    const int r = u4 % nR4;
+                    if (u4 >= nR4) mbar_wait(&r4_empty[r], static_cast<uint32_t>(((u4 / nR4) - 1) & 1));
+                    produce4c(a, tl, nmat, K, kc, raw4(r), &r4_full[r], lane);
+                }
+                continue;
+            }
             for (int kc = 0; kc < nk; kc += 2, ub += 2) {
                 const int r0 = ub % nA, r1 = (ub + 1) % nA;
                 if (ub >= nA) mbar_wait(&rb_empty[r0], static_cast<uint32_t>(((ub / nA) - 1) & 1));
@@ -1506,11 +1532,12 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_consta
                 if (!tile_of(i, tl)) break;
                 const int halfn = n_of(tl) / 2, nbox = (halfn + 63) / 64;
                 const int row0 = tl.slot0 + static_cast<int>(rank) * halfn;
+                const CUtensorMap* tm = is_p4(tl) ? &a.tmb16 : &a.tmb;  // int4 tiles multiply fp16 activations
                 for (int kc = 0; kc < nk; ++kc, ++kb) {
                     const int b = kb % nB;
                     if (kb >= nB) mbar_wait(&b_empty[b], static_cast<uint32_t>(((kb / nB) - 1) & 1));
                     mbar_expect_tx(&b_full[b], static_cast<uint32_t>(nbox) * 64 * 128);
-                    for (int q = 0; q < nbox; ++q) tma_load_b(bst(b) + q * 8192, &a.tmb, kc * kKc, row0 + q * 64, &b_full[b]);
+                    for (int q = 0; q < nbox; ++q) tma_load_b(bst(b) + q * 8192, tm, kc * kKc, row0 + q * 64, &b_full[b]);
                 }
             }
         }
@@ -1518,12 +1545,19 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_consta
     } else if (warp == 3) {
         // ---- forwarder: both of this CTA's stages of chunk kb landed -> the leader's pair barrier ----
         if (lane == 0) {
-            int kb = 0;
+            int kb = 0, cb = 0, c4 = 0;
             for (int i = 0; i < my_tiles; ++i) {
                 Tile tl;
                 if (!tile_of(i, tl)) break;
+                const bool p4 = is_p4(tl);
                 for (int kc = 0; kc < nk; ++kc, ++kb) {
-                    mbar_wait(&rb_full[kb % nA], static_cast<uint32_t>((kb / nA) & 1));
+                    if (p4) {
+                        mbar_wait(&cn_full[c4 & 1], static_cast<uint32_t>((c4 >> 1) & 1));
+                        ++c4;
+                    } else {
+                        mbar_wait(&rb_full[cb % nA], static_cast<uint32_t>((cb / nA) & 1));
+                        ++cb;
+                    }
                     mbar_wait(&b_full[kb % nB], static_cast<uint32_t>((kb / nB) & 1));
                     stamp(1, i, kc);
                     // relaxed: the stages' bytes already landed (this lane observed the
@@ -1540,29 +1574,45 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_consta
     } else if (warp == 1) {
         // ---- the leader's MMA warp ----
         if (rank == 0) {
-            int kb = 0;
+            int kb = 0, cb = 0, c4 = 0;
             for (int i = 0; i < my_tiles; ++i) {
                 Tile tl;
                 if (!tile_of(i, tl)) break;
-                const uint32_t id = idesc(1, n_of(tl), 2 * kM);
+                const bool p4 = is_p4(tl);
+                const uint32_t id = idesc(p4 ? 0 : 1, n_of(tl), 2 * kM);
                 const int buf = i % nbuf;
                 if (i >= nbuf) mbar_wait(&acc_empty[buf], static_cast<uint32_t>(((i / nbuf) - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t dacc = tmem + buf * kN;
                 for (int kc = 0; kc < nk; ++kc, ++kb) {
-                    const int r = kb % nA, b = kb % nB;
+                    const int b = kb % nB;
                     mbar_wait(&pair_full[kb % kW2Np], static_cast<uint32_t>((kb / kW2Np) & 1));
                     if (lane == 0) stamp(2, i, kc);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t ab = s32(rawb(r)), bb = s32(bst(b));
+                    const uint32_t bb = s32(bst(b));
+                    if (p4) {  // canonical SW128 fp16 A stages written by the converters
+                        const uint32_t ab = s32(can(c4 & 1));
 #pragma unroll
-                    for (int j = 0; j < kKc / 16; ++j) {
-                        const uint64_t bdesc = sdesc(bb + j * 32);
-                        const uint32_t acc = (kc > 0 || j > 0) ? 1u : 0u;
-                        umma2_elect(dacc, sdesc_core(ab + j * 256), bdesc, id, acc);
-                        if (nmat == 2) umma2_elect(dacc + kN, sdesc_core(ab + kRawA + j * 256), bdesc, id, acc);
+                        for (int j = 0; j < kKc / 16; ++j) {
+                            const uint64_t bdesc = sdesc(bb + j * 32);
+                            const uint32_t acc = (kc > 0 || j > 0) ? 1u : 0u;
+                            umma2_elect(dacc, sdesc(ab + j * 32), bdesc, id, acc);
+                            if (nmat == 2) umma2_elect(dacc + kN, sdesc(ab + kTileBytes + j * 32), bdesc, id, acc);
+                        }
+                        umma2_commit_both_elect(&cn_empty[c4 & 1]);
+                        ++c4;
+                    } else {  // the raw bf16 core-matrix blocks
+                        const uint32_t ab = s32(rawb(cb % nA));
+#pragma unroll
+                        for (int j = 0; j < kKc / 16; ++j) {
+                            const uint64_t bdesc = sdesc(bb + j * 32);
+                            const uint32_t acc = (kc > 0 || j > 0) ? 1u : 0u;
+                            umma2_elect(dacc, sdesc_core(ab + j * 256), bdesc, id, acc);
+                            if (nmat == 2) umma2_elect(dacc + kN, sdesc_core(ab + kRawA + j * 256), bdesc, id, acc);
+                        }
+                        umma2_commit_both_elect(&rb_empty[cb % nA]);
+                        ++cb;
                     }
-                    umma2_commit_both_elect(&rb_empty[r]);
                     umma2_commit_both_elect(&b_empty[b]);
                     if (kc == nk - 1) umma2_commit_both_elect(&acc_full[buf]);
                     if (lane == 0) stamp(3, i, kc);
@@ -1576,9 +1626,31 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_consta
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const int c0 = ((warp - 4) >> 2) * (kN / 2);
         const uint32_t leader_empty0 = mapa_shared(s32(&acc_empty[0]), 0), leader_empty1 = mapa_shared(s32(&acc_empty[1]), 0);
+        const int ct = tid - 128;
+        ConvOffsets o0, o1;
+        conv_offsets(ct, 0, o0);
+        conv_offsets(ct, 1, o1);
+        int u4 = 0, c4 = 0;
         for (int i = 0; i < my_tiles; ++i) {
             Tile tl;
             if (!tile_of(i, tl)) break;
+            const bool p4 = is_p4(tl);
+            if (p4) {
+                // ---- converters: this CTA's int4 rows -> fp16 q*s canonical A stages ----
+                for (int kc = 0; kc < nk; ++kc, ++c4) {
+                    const int r = u4 % nR4, c = c4 & 1;
+                    if ((kc & 1) == 0) mbar_wait(&r4_full[r], static_cast<uint32_t>((u4 / nR4) & 1));
+                    if (c4 >= 2) mbar_wait(&cn_empty[c], static_cast<uint32_t>(((c4 >> 1) - 1) & 1));
+                    convert_int4c(nmat, raw4(r), can(c), ct, (kc & 1) ? o1 : o0);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&cn_full[c]);
+                        if (kc & 1) mbar_arrive(&r4_empty[r]);
+                    }
+                    if (kc & 1) ++u4;
+                }
+            }
             const int buf = i % nbuf;
             mbar_wait(&acc_full[buf], static_cast<uint32_t>((i / nbuf) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1600,10 +1672,22 @@ __global__ void __launch_bounds__(kThreads2, 1) tc_ffn_wide2(const __grid_consta
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive_remote(buf ? leader_empty1 : leader_empty0);
-                uint16_t* ho = a.hout + static_cast<size_t>(tl.slot0 + c0) * a.f + tl.R0 + row;
+                const size_t o = static_cast<size_t>(tl.slot0 + c0) * a.f + tl.R0 + row;
+                uint16_t* ho = a.hout + o;
 #pragma unroll
                 for (int c = 0; c < kN / 2; ++c)
                     if (c0 + c < tl.m) ho[static_cast<size_t>(c) * a.f] = static_cast<uint16_t>(hp[c >> 1] >> ((c & 1) * 16));
+                if (p4) {  // the fp16 copy feeds only an int4 down pass
+                    uint16_t* h16 = a.hout16 + o;
+#pragma unroll
+                    for (int c = 0; c < kN / 2; ++c) {
+                        if (c0 + c < tl.m) {
+                            const float hv = bf2f(static_cast<uint16_t>(hp[c >> 1] >> ((c & 1) * 16)));
+                            if (f16_overflow(hv)) numerics_flag(MOE_NUM_F16_ACT);
+                            h16[static_cast<size_t>(c) * a.f] = __half_as_ushort(__float2half_rn(hv));
+                        }
+                    }
+                }
             } else {
                 for (int cbk = c0; cbk < c0 + kN / 2 && cbk < tl.m; cbk += 32) {
                     uint32_t g[32];
@@ -1764,9 +1848,13 @@ cudaError_t ffn_tc_impl(void* ws, const void* x, const int32_t* perm, const int3
     }
     // wide launches: bf16 experts through the persistent tc_ffn_wide (MOE_TC_DBG
     // bit 14: off), int4 experts through tc_ffn_kernel<256>
+    // (the CTA-pair kernel converts int4 tiles too: MOE_TC_DBG bit 23 sends them to
+    // tc_ffn_kernel<256> instead)
+    const bool wpair = !(dbg & 262144) && (f / kM) % 2 == 0 && (d / kM) % 2 == 0;  // MOE_TC_DBG bit 18: single-CTA tiles
     uint64_t mask16 = 0;
     for (int e = 0; e < E; ++e)
-        if (((active_mask >> e) & 1ull) && experts[e].precision != MOE_P4) mask16 |= 1ull << e;
+        if (((active_mask >> e) & 1ull) && (experts[e].precision != MOE_P4 || (wpair && !(dbg & 8388608))))
+            mask16 |= 1ull << e;
     const bool wpers = wide && mask16 != 0 && !(dbg & 16384);
     const uint64_t mask_single = wpers ? (active_mask & ~mask16) : active_mask;
     static bool wide_attr = false;
@@ -1774,7 +1862,6 @@ cudaError_t ffn_tc_impl(void* ws, const void* x, const int32_t* perm, const int3
         MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem));
         wide_attr = true;
     }
-    const bool wpair = !(dbg & 262144) && (f / kM) % 2 == 0 && (d / kM) % 2 == 0;  // MOE_TC_DBG bit 18: single-CTA tiles
     static bool pair_attr = false;
     if (wpers && wpair && !pair_attr) {
         MOE_CUDA_OK(cudaFuncSetAttribute(tc_ffn_wide2, cudaFuncAttributeMaxDynamicSharedMemorySize, kW2Smem));
@@ -1783,7 +1870,7 @@ cudaError_t ffn_tc_impl(void* ws, const void* x, const int32_t* perm, const int3
     auto launch_wide = [&](int rows) -> cudaError_t {
         TcArgs aw = a;
         aw.active_mask = mask16;
-        if (wpair && !(rows == f && (dbg & 1048576))) {  // bit 20: single-CTA tiles for the gate/up pass
+        if (wpair) {
             const int np = ntiles_max * (rows / kM / 2);
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(np, sms / 2)));

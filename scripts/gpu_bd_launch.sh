@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bd_launches.csv python tools/tc_tps.py 0 256 > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bd_launches.csv python tools/tc_tps.py ${N4:-0} 256 > /dev/null 2>&1
 python - <<'PY'
 import csv, collections
 rows=[r for r in csv.reader(open('gpurun_out/bd_launches.csv')) if len(r)>10]
