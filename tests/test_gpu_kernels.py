@@ -187,12 +187,12 @@ def _sample_rows(lo, hi, full):
 # T * k > 128 * (active experts) selects the 256-token tile variant
 # (tc_gemm.cu moek_ffn_tc): T = 520 / 777 (tiny, 8 active experts; 777 ends
 # on a partial 256-token tile), skew (2 active experts, 600 slots), T = 1024
-# at Mixtral shape.
+# at Mixtral shape; f = 1920 (odd row-tile count) for the non-pair fallback.
 @pytest.mark.parametrize("mix", ["bf16", "int4", "mixed"])
 @pytest.mark.parametrize("T,shape,skew", [(40, (512, 1792), False), (300, (512, 1792), False),
                                           (96, (4096, 14336), False), (520, (512, 1792), False),
                                           (777, (512, 1792), False), (300, (512, 1792), True),
-                                          (1024, (4096, 14336), False)])
+                                          (1024, (4096, 14336), False), (520, (512, 1920), False)])
 def test_ffn_tcgen05_vs_oracle(moe, orc, torch_mod, cuda, T, shape, skew, mix):
     """K3/K4 on tcgen05 (batched / prefill path): every expert's y rows vs
     the oracle FFN on the same tokens (bf16: BF16 operands; int4: on-chip
@@ -210,6 +210,8 @@ def test_ffn_tcgen05_vs_oracle(moe, orc, torch_mod, cuda, T, shape, skew, mix):
     counts, offsets, perm, inv = orc.permute(idx, T, E, k)
     wide = T * k > 128 * int((counts > 0).sum())
     assert wide == (T in (520, 777, 1024) or skew)
+    # f = 1920: an odd count of 128-row tiles, so wide launches take the single-CTA
+    # tc_ffn_wide (bf16) + tc_ffn_kernel<256> (int4) instead of the CTA-pair kernel
     experts, host, keep = [], {}, []
     for e in range(E):
         dev, h = _expert_tensors(orc, torch, cuda, m, e, prec[e])
