@@ -1772,7 +1772,10 @@ cudaError_t encode_b(CUtensorMap* tm, const void* base, int K, int rows) {
 }  // namespace tc
 }  // namespace moek
 
-constexpr int kDownSplit = 4;  // K splits of the down pass on the persistent kernel
+#ifndef MOE_TC_DOWN_SPLIT
+#define MOE_TC_DOWN_SPLIT 4
+#endif
+constexpr int kDownSplit = MOE_TC_DOWN_SPLIT;  // K splits of the down pass on the persistent kernel
 
 size_t moek_tc_workspace_bytes(int T, int k, int d, int f) {
     const size_t slots = static_cast<size_t>(T) * k;
