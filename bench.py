@@ -525,8 +525,8 @@ def run_ours(args, rank, world, device):
                                 "peak_kind": "MEASURED_PEAKS bf16_tflops (burst)",
                                 "flops": "6*d*f*T*k (gate/up + down, top-k=2)",
                                 "timed": "expert FFN launches of one layer (gather, 2 x tcgen05 GEMM, combine)",
-                                "kernels": "above 128 slots per expert: tc_ffn_wide2 (persistent, cta_group::2 "
-                                           "M=256 x N=256 tiles, bf16 and int4 experts); at most 128: "
+                                "kernels": "from 128 slots per expert: tc_ffn_wide2 (persistent, cta_group::2 "
+                                           "M=256 x N=256 tiles, bf16 and int4 experts); below 128: "
                                            "tc_ffn_persist (128-token tiles, both passes in one launch)"},
             "cpu_baseline": cpu,
             "bytes_per_expert": {"bf16": s16, "int4_g128": s4},

@@ -184,7 +184,7 @@ def _sample_rows(lo, hi, full):
     return np.array(sorted(picks))
 
 
-# T * k > 128 * (active experts) selects the 256-token tile variant
+# T * k >= 128 * (active experts) selects the 256-token tile variant
 # (tc_gemm.cu moek_ffn_tc): T = 520 / 777 (tiny, 8 active experts; 777 ends
 # on a partial 256-token tile), skew (2 active experts, 600 slots), T = 1024
 # at Mixtral shape; f = 1920 (odd row-tile count) for the non-pair fallback.
@@ -208,7 +208,7 @@ def test_ffn_tcgen05_vs_oracle(moe, orc, torch_mod, cuda, T, shape, skew, mix):
     if skew:  # every token on experts 5 and 2 (one int4, one bf16 in the mixed plan)
         idx = np.tile(np.array([5, 2], np.int32), (T, 1))
     counts, offsets, perm, inv = orc.permute(idx, T, E, k)
-    wide = T * k > 128 * int((counts > 0).sum())
+    wide = T * k >= 128 * int((counts > 0).sum())
     assert wide == (T in (520, 777, 1024) or skew)
     # f = 1920: an odd count of 128-row tiles, so wide launches take the single-CTA
     # tc_ffn_wide (bf16) + tc_ffn_kernel<256> (int4) instead of the CTA-pair kernel
