@@ -61,9 +61,17 @@ struct TcArgs {
     uint16_t* hout16;         // pass 0: h [T*k][f] fp16
     float* y;                 // pass 1: y [T*k][d]
     uint64_t active_mask;
-    int dbg;                  // debug: bit0 skip convert, bit1 skip MMA, bit2 skip weight loads,
-                              // bit5 bf16 halves as separate 2 KB reads (no pairing),
-                              // bit11 skip epilogue stores, bit12 skip B loads
+    int dbg;                  // MOE_TC_DBG (A/B and ablation switches, 0 in production):
+                              // kernel ablations: bit0 skip convert, bit1 skip MMA, bit2 skip weight
+                              // loads, bit5 bf16 halves as separate 2 KB reads, bit11 skip epilogue
+                              // stores, bit12 skip B loads, bit13 plain arrives instead of commits,
+                              // bit15 clock probe (-DMOE_TC_TRACE=1 builds), bit16/17 weight L2
+                              // prefetch; dispatch: bit3/4 force 128/256-token tiles, bit8 per-tile
+                              // (non-persistent) 128-token kernel, bit9 no down-pass K split, bit14
+                              // no persistent wide kernel, bit18 single-CTA wide kernel, bit19
+                              // release.cluster forwarder arrive, bit21 two launches instead of the
+                              // fused one, bit22 split_reduce + combine, bit23 int4 wide tiles on
+                              // tc_ffn_kernel<256>
     moe_expert_weights ex[MOE_MAX_EXPERTS];
 };
 
