@@ -2027,8 +2027,18 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
         __syncthreads();
         fstamp(ftr, l, 1);
         // ---- R: route the token (every CTA, identical results) --------------
-        for (int i = tid * 8; i < d; i += blockDim.x * 8)
-            *reinterpret_cast<uint4*>(xs + i) = __ldcg(reinterpret_cast<const uint4*>(xl + i));
+        {  // every row load of the thread in flight at once: one L2 round trip, not d / 2048 (+0.4 % at n4 = 256)
+            const int bd = static_cast<int>(blockDim.x) * 8;
+            uint4 xv[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (tid * 8 + r * bd < d) xv[r] = __ldcg(reinterpret_cast<const uint4*>(xl + tid * 8 + r * bd));
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (tid * 8 + r * bd < d) *reinterpret_cast<uint4*>(xs + tid * 8 + r * bd) = xv[r];
+            for (int i = tid * 8 + 4 * bd; i < d; i += bd)
+                *reinterpret_cast<uint4*>(xs + i) = __ldcg(reinterpret_cast<const uint4*>(xl + i));
+        }
         __syncthreads();
         const uint16_t* xr = xs;
         if (a.norm_eps > 0.0f) {
