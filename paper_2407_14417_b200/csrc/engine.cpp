@@ -184,6 +184,7 @@ struct MoeEngine::Impl {
     bool fused_ok = false;
     unsigned int* flow_ctl = nullptr;           // decode_flow_kernel's per-layer completion counters
     float* flow_part = nullptr;                 // its partial buffers (sentinel-filled between uses)
+    uint16_t* flow_x = nullptr;                 // its 3 layer-output rows (0xffff = not yet written)
     size_t flow_part0_floats = 0, flow_part1_floats = 0;
     bool flow_ok = false;                       // dataflow variant (default; MOE_FUSED=step: grid barriers)
 
@@ -389,6 +390,8 @@ struct MoeEngine::Impl {
                 const size_t pf = 2 * (flow_part0_floats + flow_part1_floats);
                 dev_alloc(reinterpret_cast<void**>(&flow_part), pf * 4);
                 ck(cudaMemsetAsync(flow_part, 0xff, pf * 4, compute), "memset");
+                dev_alloc(reinterpret_cast<void**>(&flow_x), static_cast<size_t>(3) * d * 2);
+                ck(cudaMemsetAsync(flow_x, 0xff, static_cast<size_t>(3) * d * 2, compute), "memset");
                 flow_ok = true;
             }
         }
@@ -445,6 +448,9 @@ struct MoeEngine::Impl {
             a.part1 = flow_part + 2 * flow_part0_floats;
             a.part0_stride = flow_part0_floats;
             a.part1_stride = flow_part1_floats;
+            a.xbuf0 = flow_x;
+            a.xbuf1 = flow_x + d;
+            a.xbuf2 = flow_x + 2 * static_cast<size_t>(d);
             ck(moek_decode_flow(a, compute), "decode_flow");
         } else {
             ck(moek_decode_step(a, compute), "decode_step");
@@ -644,7 +650,7 @@ struct MoeEngine::Impl {
         if (master_arena) cudaFreeHost(master_arena);
         if (copy) cudaStreamSynchronize(copy);
         void* devp[] = {tcws, xn, dev_arena, swap, wg, xin, xout, xbuf[0], xbuf[1], idx, wts, counts, offsets, perm, inv, ticket, y,
-                         gws_base, dev_experts, fused_ctl, flow_ctl, flow_part, ep_buf, ep_epoch, ep_keys, ep_counts, ep_offsets, ep_perm,
+                         gws_base, dev_experts, fused_ctl, flow_ctl, flow_part, flow_x, ep_buf, ep_epoch, ep_keys, ep_counts, ep_offsets, ep_perm,
                          ep_inv, ep_iota, ep_y, ep_gws_base, ep_tcws, ep_dense};
         for (void* p : devp)
             if (p) cudaFree(p);

@@ -1581,6 +1581,29 @@ MOE_DEVI void flow_compute(const uint8_t* sp, const uint8_t* bp, const float* x0
     }
 }
 
+// Layer-output rows of the dataflow step (x(1) .. x(L-1)) rotate through 3
+// buffers holding 0xffff (a bf16 NaN f2bf never produces) wherever a row
+// element is not yet written.  A layer starts by loading x(l) itself until no
+// element is the sentinel -- one L2 round trip instead of a counter acquire
+// followed by the row load.  Layer m's finisher resets its own tiles of
+// buffer (m+1)%3 (x(m-1): every CTA finished reading it, since x(m) is
+// complete) before its first x(m+1) store, with a release fence between; the
+// readers' acquire fence after the load closes the pair.  The last CTA out
+// resets all three for the next launch.
+MOE_DEVI uint4 ld_relaxed_u4(const void* p) {
+    uint4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+MOE_DEVI bool has_x_sentinel(const uint4& v) {
+    return (__vcmpeq2(v.x, 0xffffffffu) | __vcmpeq2(v.y, 0xffffffffu) | __vcmpeq2(v.z, 0xffffffffu) |
+            __vcmpeq2(v.w, 0xffffffffu)) != 0u;
+}
+MOE_DEVI uint16_t* flow_xbuf(const MoeDecodeArgs& a, int i) { return i == 0 ? a.xbuf0 : i == 1 ? a.xbuf1 : a.xbuf2; }
+
 MOE_DEVI void red_release_gpu(unsigned int* p, unsigned int v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -1811,6 +1834,14 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
     float* const P0 = a.part0 + static_cast<size_t>(l & 1) * a.part0_stride;
     float* const P1 = a.part1 + static_cast<size_t>(l & 1) * a.part1_stride;
     uint32_t reset_tiles = 0;
+    {  // this CTA's tiles of the row buffer x(l+2) will use, back to the sentinel (it holds x(l-1), read by now)
+        uint16_t* xr = flow_xbuf(a, (l + 1) % 3);
+        for (int i = lane; i < nR * 2; i += 32)
+            __stcg(reinterpret_cast<uint4*>(xr + (b + (i >> 1) * grid) * 16) + (i & 1),
+                   make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu));
+        __threadfence();  // release: these resets and the previous layer's partial resets before any x(l+1) store
+        __syncwarp();
+    }
     uint32_t pu = nU >= 32 ? 0xffffffffu : (1u << nU) - 1u;
     uint32_t pc = nCh >= 32 ? 0xffffffffu : (1u << nCh) - 1u;
     uint32_t pr = nR >= 32 ? 0xffffffffu : (1u << nR) - 1u;
@@ -1934,7 +1965,8 @@ MOE_DEVI void flow_finisher(const DecodeArgs& a, const FlowTab& T, int l, unsign
                     if (kg == 0) {
                         const uint2 o = make_uint2(static_cast<uint32_t>(f2bf(acc[0])) | (static_cast<uint32_t>(f2bf(acc[1])) << 16),
                                                    static_cast<uint32_t>(f2bf(acc[2])) | (static_cast<uint32_t>(f2bf(acc[3])) << 16));
-                        __stcg(reinterpret_cast<uint2*>(yl + j), o);
+                        asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};" ::"l"(yl + j), "r"(o.x), "r"(o.y)
+                                     : "memory");
                     }
                     reset_tiles |= 1u << i;  // consumed: back to the sentinel after the release
                     fstamp_lane0(ftr, l, 11);  // last tile stored
@@ -2010,36 +2042,52 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
     }
 
     for (int l = 0; l < a.L; ++l) {
-        const uint16_t* xl = l == 0 ? a.x_in : ((l - 1) & 1 ? a.xbuf1 : a.xbuf0);
-        uint16_t* yl = l == a.L - 1 ? a.x_out : (l & 1 ? a.xbuf1 : a.xbuf0);
+        const uint16_t* xl = l == 0 ? a.x_in : flow_xbuf(a, (l - 1) % 3);
+        uint16_t* yl = l == a.L - 1 ? a.x_out : flow_xbuf(a, l % 3);
         const uint16_t* wgl = a.wg + static_cast<size_t>(l) * E * d;
         unsigned int* ctl = a.flow_ctl + static_cast<size_t>(l) * per_layer;
         fstamp(ftr, l, 0);
         // the layer's expert table while thread 0 waits for the previous layer's output
         for (int i = tid; i < E * static_cast<int>(sizeof(moe_expert_weights) / 8); i += blockDim.x)
             reinterpret_cast<uint2*>(s_ex)[i] = reinterpret_cast<const uint2*>(a.experts + static_cast<size_t>(l) * E)[i];
-        if (l > 0 && tid == 0) {
-            const unsigned int* xready = a.flow_ctl + static_cast<size_t>(l - 1) * per_layer + k * ((Gf + 7) / 8);
-            while (ld_acquire_gpu(xready) < gridDim.x) {  // every finisher of the previous layer done
-            }
-            if (ftr != nullptr) ftr[(static_cast<size_t>(l) * gridDim.x + blockIdx.x) * kFusedStamps + 12] = clock64();
-        }
         __syncthreads();
         fstamp(ftr, l, 1);
         // ---- R: route the token (every CTA, identical results) --------------
-        {  // every row load of the thread in flight at once: one L2 round trip, not d / 2048 (+0.4 % at n4 = 256)
+        // x(l): every row load of the thread in flight at once; for l > 0 the
+        // loads themselves wait for the previous layer (sentinel rows, above)
+        {
             const int bd = static_cast<int>(blockDim.x) * 8;
             uint4 xv[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r)
-                if (tid * 8 + r * bd < d) xv[r] = __ldcg(reinterpret_cast<const uint4*>(xl + tid * 8 + r * bd));
+                if (tid * 8 + r * bd < d)
+                    xv[r] = l == 0 ? __ldcg(reinterpret_cast<const uint4*>(xl + tid * 8 + r * bd))
+                                   : ld_relaxed_u4(xl + tid * 8 + r * bd);
+            if (l > 0) {
+                for (;;) {
+                    bool miss = false;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        if (tid * 8 + r * bd < d && has_x_sentinel(xv[r])) {
+                            miss = true;
+                            xv[r] = ld_relaxed_u4(xl + tid * 8 + r * bd);
+                        }
+                    if (!miss) break;
+                }
+            }
 #pragma unroll
             for (int r = 0; r < 4; ++r)
                 if (tid * 8 + r * bd < d) *reinterpret_cast<uint4*>(xs + tid * 8 + r * bd) = xv[r];
-            for (int i = tid * 8 + 4 * bd; i < d; i += bd)
-                *reinterpret_cast<uint4*>(xs + i) = __ldcg(reinterpret_cast<const uint4*>(xl + i));
+            for (int i = tid * 8 + 4 * bd; i < d; i += bd) {
+                uint4 v = l == 0 ? __ldcg(reinterpret_cast<const uint4*>(xl + i)) : ld_relaxed_u4(xl + i);
+                while (l > 0 && has_x_sentinel(v)) v = ld_relaxed_u4(xl + i);
+                *reinterpret_cast<uint4*>(xs + i) = v;
+            }
+            if (l > 0) __threadfence();  // acquire: the writers' stores before their release fence
         }
         __syncthreads();
+        if (ftr != nullptr && tid == 0)
+            ftr[(static_cast<size_t>(l) * gridDim.x + blockIdx.x) * kFusedStamps + 12] = clock64();
         const uint16_t* xr = xs;
         if (a.norm_eps > 0.0f) {
             if (tid < 256) {
@@ -2256,6 +2304,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) decode_flow_kernel(const __g
     if (s_last) {
         const int words = a.L * per_layer;
         for (int i = tid; i < words / 4; i += blockDim.x) __stcg(reinterpret_cast<uint4*>(a.flow_ctl) + i, make_uint4(0, 0, 0, 0));
+        for (int i = tid; i < 3 * (d / 8); i += blockDim.x)  // every row buffer back to the sentinel
+            __stcg(reinterpret_cast<uint4*>(flow_xbuf(a, i / (d / 8))) + i % (d / 8),
+                   make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu));
         __syncthreads();
         if (tid == 0) *exitc = 0;
     }

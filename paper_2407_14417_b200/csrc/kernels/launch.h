@@ -63,6 +63,7 @@ struct MoeDecodeArgs {
     const uint16_t* x_in;               // [d]
     uint16_t* xbuf0;
     uint16_t* xbuf1;
+    uint16_t* xbuf2;                    // decode_flow_kernel: third layer-output row (0xffff-filled, see gemv.cu)
     uint16_t* x_out;
     int32_t* idx;                       // [L][idx_stride] routing export
     float* wts;
