@@ -1473,7 +1473,8 @@ __global__ void __launch_bounds__(C::kThreads, 1) decode_step_kernel(const __gri
 //     each complete chunk into the CTA's resident h rows (one mbarrier per
 //     chunk, which the down items wait on), and finishes its output tiles the
 //     same way (combine + residual -> x(l+1), then the layer's x-ready counter);
-//   * a layer starts when the previous layer's x-ready counter is full.
+//   * a layer starts by loading x(l) until none of it is the 0xffff sentinel
+//     (3 rotating row buffers; see ld_relaxed_u4 below).
 // Sums, SwiGLU and combine are the K-part orders of finalize_h /
 // finalize_out (sum_kparts, swiglu_store), so the output is bit-identical to
 // the per-layer kernels.  Counters live per layer in a.flow_ctl; the last
