@@ -111,3 +111,28 @@ def test_flow_odd_shapes_equal_per_layer(moe, cuda, shape):
         assert fused.last_routing(1) == ref.last_routing(1), step
     fused.close()
     ref.close()
+
+
+@pytest.mark.parametrize("shape,n4,steps", [("tiny", 8, 150), ("mixtral", 128, 20), ("mixtral", 256, 20)])
+def test_flow_back_to_back_launches(moe, cuda, shape, n4, steps):
+    """Two dataflow launches queued back to back (no host sync between): the
+    second starts on the row buffers and counters the first left behind
+    (sentinel rows reset by its last CTA out), so every checked step also
+    checks the previous launch's clean-up.  Bit-identical to the per-layer
+    kernels on the same inputs."""
+    import torch
+    cfg = TINY if shape == "tiny" else MIXTRAL
+    flow, ref = _pair(moe, cfg, n4, 7, 1e-5, plan_seed=2)
+    assert flow.profile_fused() is not None
+    n = 2 * cfg["d_model"]
+    for step in range(steps):
+        for e in (flow, ref):
+            e.synth_input(900 + step, 1)
+            e.decode(1)
+            e.synth_input(3000 + step, 1)
+            e.decode(1)
+            e.sync()
+        assert np.array_equal(read_device(torch, flow.output_ptr, n), read_device(torch, ref.output_ptr, n)), step
+        assert flow.last_routing(1) == ref.last_routing(1), step
+    flow.close()
+    ref.close()
